@@ -1,0 +1,222 @@
+/*
+ * renyi_b200.h — C ABI of the B200-native randomized matrix-based Rényi
+ * entropy hot path (librenyi_b200.so).
+ *
+ * The reference (arxiv 2205.07426 artifact, proj/) has no FFI: its path sits
+ * behind C++ value-semantic functions over Eigen matrices. Each entry point
+ * below names the reference function it replaces (file:line, relative to the
+ * reference's root). Conventions:
+ *   - every call returns an int status: 0 = ok, 1..10 = the reference's errc
+ *     kinds + 1 (proj/include/renyi/common.hpp:14-25), 20+ = device/runtime;
+ *     renyi_last_error() returns the thread's last message;
+ *   - host matrices are column-major (the reference's Eigen layout) with an
+ *     explicit leading dimension where noted; kernels (A) are symmetric n x n;
+ *   - device state lives behind opaque handles; the caller owns host buffers.
+ * Statuses 1,4,5,8,10 are "usage" errors (reference CLI exit 2), the others
+ * numerical/runtime (exit 3) — see proj/include/renyi/common.hpp:33-44.
+ */
+#ifndef RENYI_B200_H
+#define RENYI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+enum {
+    RENYI_OK = 0,
+    RENYI_E_INVALID_ARGUMENT = 1,
+    RENYI_E_ZERO_DIAGONAL = 2,
+    RENYI_E_NON_FINITE = 3,
+    RENYI_E_SIZE_MISMATCH = 4,
+    RENYI_E_DOMAIN_ERROR = 5,
+    RENYI_E_RANK_COLLAPSE = 6,
+    RENYI_E_NON_POSITIVE_TRACE = 7,
+    RENYI_E_ALPHA_IS_ONE = 8,
+    RENYI_E_DEGENERATE_BOUNDS = 9,
+    RENYI_E_PARSE_ERROR = 10,
+    RENYI_E_CUDA = 20,
+    RENYI_E_NCCL = 21,
+    RENYI_E_OOM = 22,
+    RENYI_E_NO_DEVICE = 23,
+    RENYI_E_INTERNAL = 24
+};
+
+/* storage/compute precision of a device kernel matrix */
+enum { RENYI_F64 = 0, RENYI_F32 = 1 };
+/* probe distributions */
+enum { RENYI_PROBE_GAUSSIAN = 0, RENYI_PROBE_RADEMACHER = 1 };
+/* estimator methods (renyi::Method, proj/include/renyi/entropy.hpp:12) */
+enum { RENYI_METHOD_EXACT = 0, RENYI_METHOD_INT = 1, RENYI_METHOD_TAYLOR = 2, RENYI_METHOD_CHEBYSHEV = 3,
+       RENYI_METHOD_AUTO = 4 };
+/* matrix functions (renyi::MatrixFunctionSpec, proj/include/renyi/poly.hpp:32-70) */
+enum { RENYI_MATFUN_INT_POWER = 0, RENYI_MATFUN_TAYLOR = 1, RENYI_MATFUN_CHEBYSHEV = 2 };
+
+typedef struct renyi_ctx renyi_ctx;
+typedef struct renyi_kernel renyi_kernel;
+
+/* MatrixFunctionSpec::{int_power,taylor,chebyshev} arguments; coefficients
+ * (binomials, Chebyshev node sums, safeguard) are derived inside exactly as the
+ * reference factories do (proj/src/poly.cpp:60-80). */
+typedef struct {
+    int kind;     /* RENYI_MATFUN_* */
+    double alpha; /* integer value for INT_POWER */
+    int degree;   /* m (ignored for INT_POWER) */
+    double u, v;  /* Taylor uses v; Chebyshev uses [u, v] before the safeguard */
+} renyi_matfun;
+
+/* SketchConfig + probe injection (proj/include/renyi/hutchpp.hpp:12-18). */
+typedef struct {
+    int s_q, s_g;          /* sketch / residual probe columns (s_q = 0: plain Hutchinson) */
+    uint64_t seed;
+    int probe_kind;        /* RENYI_PROBE_* when the probes are drawn from the seed */
+    const double* sketch;  /* optional n x s_q column-major (NULL: draw) */
+    const double* probes;  /* optional n x s_g column-major (NULL: draw) */
+} renyi_sketch;
+
+typedef struct { /* TraceEstimate, proj/include/renyi/hutchpp.hpp:20-30 */
+    double value, low_rank_part, residual_part;
+    int queries_used, sketch_rank, exact;
+} renyi_trace_estimate;
+
+typedef struct { /* PowerOptions, proj/include/renyi/spectrum.hpp:22-30 */
+    int max_iters;
+    double tol;
+    uint64_t seed;
+    double rank_floor;
+} renyi_power_options;
+
+typedef struct { /* SpectrumBounds, proj/include/renyi/spectrum.hpp:12-20 */
+    double u, v, kappa;
+    int iterations_used, v_converged, u_converged, rank_deficient;
+} renyi_spectrum_bounds;
+
+typedef struct { /* PowerResult, proj/include/renyi/spectrum.hpp:35-39 */
+    double rayleigh;
+    int iterations, converged;
+} renyi_power_result;
+
+typedef struct { /* EstimatorParams, proj/include/renyi/entropy.hpp:18-30 (+ probe/split extensions) */
+    double alpha;
+    int method;
+    int s, m;
+    double epsilon, delta;
+    uint64_t seed;
+    renyi_power_options power;
+    int has_bounds;
+    renyi_spectrum_bounds bounds;
+    int probe_kind; /* RENYI_PROBE_*; the reference draws Gaussian probes */
+    int s_q, s_g;   /* explicit Hutch++ split; -1 = reference split floor(s/4), s - 2 floor(s/4) */
+} renyi_estimator_params;
+
+typedef struct { /* EntropyEstimate, proj/include/renyi/entropy.hpp:32-41 */
+    double entropy, trace_estimate;
+    int method_used, s_used, m_used;
+    int has_bounds;
+    renyi_spectrum_bounds bounds_used;
+    double elapsed;
+    int deterministic;
+    renyi_trace_estimate trace;
+} renyi_entropy_estimate;
+
+typedef struct { /* MutualInformation, proj/include/renyi/measures.hpp:24-29 */
+    double value, vars_entropy, target_entropy, joint_entropy;
+} renyi_mi_estimate;
+
+/* ---- errors, context ---------------------------------------------------- */
+const char* renyi_last_error(void);
+int renyi_status_is_usage(int status); /* renyi::error::is_usage, common.hpp:33-44 */
+int renyi_ctx_create(int device, renyi_ctx** out);
+int renyi_ctx_destroy(renyi_ctx* ctx);
+int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc);
+int renyi_ctx_sync(renyi_ctx* ctx);
+/* CUDA-event timing of block-product launches (bench instrumentation) */
+int renyi_ctx_profile(renyi_ctx* ctx, int enable);
+int renyi_ctx_profile_read(renyi_ctx* ctx, int* launches, double* milliseconds);
+int renyi_ctx_launch_count(renyi_ctx* ctx, long* launches);
+
+/* ---- kernel matrices (proj/include/renyi/kernel.hpp:45-56) --------------- */
+/* build_kernel(X, GaussianKernel{sigma}) — proj/src/kernel.cpp:35-72 + ops.cpp:39-47 */
+int renyi_kernel_build_gaussian(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                                int precision, renyi_kernel** out);
+/* hadamard_joint({build_kernel(X), build_kernel(Y)}) fused from samples — kernel.cpp:74-101 */
+int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                      double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                      int precision, renyi_kernel** out);
+/* NormalizedKernel(Matrix) — kernel.hpp:33 (caller asserts the invariants) */
+int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int precision, renyi_kernel** out);
+/* hadamard_joint({a, b}) — kernel.cpp:74-101 */
+int renyi_kernel_hadamard_joint(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b, renyi_kernel** out);
+int renyi_kernel_size(const renyi_kernel* k, int64_t* n);
+int renyi_kernel_download(renyi_ctx* ctx, const renyi_kernel* k, double* out);
+int renyi_kernel_destroy(renyi_kernel* k);
+
+/* ---- hot-path seams ------------------------------------------------------- */
+/* ops::matmul_panel(a, x) — proj/src/ops.cpp:98-107: Y = A V, V n x s */
+int renyi_matmul_panel(renyi_ctx* ctx, const renyi_kernel* k, const double* v, int s, double* y);
+/* ops::matvec(a, x) — proj/src/ops.cpp:73-85 */
+int renyi_matvec(renyi_ctx* ctx, const renyi_kernel* k, const double* x, double* y);
+/* apply_panel(spec, a, x) — proj/src/poly.cpp:158-164 */
+int renyi_apply_panel(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const double* v, int s,
+                      double* y);
+/* fused x_j^T f(A) x_j per column (projected_trace without the vector) — hutchpp.cpp:33-39 */
+int renyi_matfun_traces(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const double* x, int s,
+                        double* traces);
+
+/* ---- estimators ------------------------------------------------------------- */
+/* power_method — proj/src/spectrum.cpp:25-49 (shift = 0: A, else shift*I - A) */
+int renyi_power_method(renyi_ctx* ctx, const renyi_kernel* k, const renyi_power_options* opts, double shift,
+                       renyi_power_result* out);
+/* estimate_bounds — proj/src/spectrum.cpp:80-103 */
+int renyi_estimate_bounds(renyi_ctx* ctx, const renyi_kernel* k, const renyi_power_options* opts,
+                          renyi_spectrum_bounds* out);
+/* hutchpp — proj/src/hutchpp.cpp:69-115 */
+int renyi_hutchpp(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const renyi_sketch* cfg,
+                  renyi_trace_estimate* out);
+/* estimate — proj/src/entropy.cpp:201-275 */
+int renyi_estimate(renyi_ctx* ctx, const renyi_kernel* k, const renyi_estimator_params* p,
+                   renyi_entropy_estimate* out);
+/* entropy_int / entropy_taylor / entropy_chebyshev — proj/src/entropy.cpp:111-135 */
+int renyi_entropy_int(renyi_ctx* ctx, const renyi_kernel* k, int alpha, int s, uint64_t seed,
+                      renyi_entropy_estimate* out);
+int renyi_entropy_taylor(renyi_ctx* ctx, const renyi_kernel* k, double alpha, int s, int m, double v,
+                         uint64_t seed, renyi_entropy_estimate* out);
+int renyi_entropy_chebyshev(renyi_ctx* ctx, const renyi_kernel* k, double alpha, int s, int m, double u, double v,
+                            uint64_t seed, renyi_entropy_estimate* out);
+/* mutual_information({a}, b, params) — proj/src/measures.cpp:36-46 */
+int renyi_mutual_information(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b,
+                             const renyi_estimator_params* p, renyi_mi_estimate* out);
+/* the same from samples, one n x n matrix resident at a time (cmd_mutual_info, renyi_cli.cpp:156-188) */
+int renyi_mutual_information_samples(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                     double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                     const renyi_estimator_params* p, int precision, renyi_mi_estimate* out);
+/* north star: build_kernel(X, sigma) + estimate(A, params) (cmd_entropy, renyi_cli.cpp:144-154) */
+int renyi_entropy(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                  const renyi_estimator_params* p, int precision, renyi_entropy_estimate* out);
+
+/* ---- host-side arithmetic (no device) ------------------------------------------ */
+void renyi_default_params(renyi_estimator_params* p);      /* EstimatorParams{} defaults */
+void renyi_default_power_options(renyi_power_options* o);  /* PowerOptions{} defaults */
+uint64_t renyi_mix64(uint64_t x);                            /* rng.cpp:8-14 */
+uint64_t renyi_derive_key(uint64_t seed, uint64_t tag);      /* rng.cpp:16-18 */
+uint64_t renyi_hash_name(const char* name);                  /* rng.cpp:20-28 */
+/* detail::gaussian_panel (hutchpp.cpp:13-22); kind RENYI_PROBE_RADEMACHER = sign of the top bit */
+int renyi_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out);
+int renyi_binomial_coeffs(double alpha, int m, double* out);                   /* poly.cpp:10-16 */
+int renyi_chebyshev_coeffs(double alpha, int m, double u, double v, double* out); /* poly.cpp:42-46 */
+double renyi_chebyshev_safeguard(double u, double v);                           /* poly.hpp:27-30 */
+double renyi_taylor_tail_constant(double alpha, int k_max);                     /* poly.cpp:48-58 */
+int renyi_matfun_scalar(const renyi_matfun* f, double lambda, double* out);     /* poly.cpp:166-168 */
+long renyi_expected_queries(const renyi_matfun* f, int s);                      /* hutchpp.cpp:117-121 */
+int renyi_select_params(double alpha, double epsilon, double delta, const renyi_spectrum_bounds* b, int64_t n,
+                        int method, int* s, int* m);                            /* entropy.cpp:137-176 */
+int renyi_mu_bound(double u, double v, double alpha, int64_t n, double* mu, double* lower, double* upper);
+int renyi_entropy_from_trace(double trace, double alpha, double* out);          /* entropy.cpp:62-69 */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RENYI_B200_H */

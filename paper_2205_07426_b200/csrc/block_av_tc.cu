@@ -1,0 +1,320 @@
+// Y = A · V, the hot block product (reference seam: ops::matmul_panel,
+// proj/src/ops.cpp:98-107, called from proj/src/poly.cpp:155-163 and
+// proj/src/hutchpp.cpp:90).
+//
+// B200 design:
+//   * A lives in HBM as two fp16 planes (hi, lo) of A·n·2^14, i.e. the same
+//     4 bytes/entry as fp32 but split so the 5th-gen tensor cores can consume it.
+//     The iterate V is stored the same way, column-major, with a per-column
+//     power-of-two scale chosen by the previous pass's epilogue.
+//   * Y ≈ A_hi·V_hi + (A_hi·V_lo + A_lo·V_hi): three tcgen05.mma (kind::f16,
+//     fp32 accumulate) per K=16 step; the dropped lo·lo term is 2^-22 relative.
+//   * Persistent stream-K schedule: 148 CTAs each own one contiguous range of
+//     (row-block, k-tile) iterations, so every SM streams the same number of A
+//     bytes. Ranges that end inside a row block write an fp32 partial to a slot
+//     (slot = row_block + cta, unique along the monotone staircase); the pass
+//     epilogue kernel sums the slots of a row block in CTA order (deterministic).
+//   * Accumulation into TMEM is chunked (KC k-tiles) and drained into fp32
+//     registers (round-to-nearest adds), bounding the tensor core's internal
+//     accumulation error; the main and correction products use separate TMEM
+//     accumulators. Two accumulator sets double-buffer the drain.
+//   * Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM owner),
+//     warps 2..5 = TMEM drain / partial writers.
+#include <cstdio>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rb {
+
+namespace {
+
+constexpr int BM = 128;  // UMMA M: rows of A per tile
+constexpr int BK = 64;   // K per tile: one 128-byte swizzle row of fp16
+
+template <int NPAD>
+struct TcCfg {
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kVBytes = NPAD * BK * 2;
+    static constexpr int kStageBytes = 2 * kABytes + 2 * kVBytes;
+    static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kTmemCols = (4 * NPAD <= 32) ? 32 : (4 * NPAD <= 64) ? 64 : (4 * NPAD <= 128) ? 128
+                                                           : (4 * NPAD <= 256) ? 256 : 512;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024;
+    static constexpr int kThreads = 192;
+    static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 128, "NPAD must be a multiple of 16 in [16,128]");
+    static_assert(kStages >= 2, "need at least double buffering");
+};
+
+struct TcArgs {
+    int64_t total_iters;  // row_blocks * k_tiles
+    int k_tiles;          // k tiles per row block
+    int kc;               // k tiles per TMEM chunk
+    float* partial;       // [slots][NPAD][BM]
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(192, 1)
+    block_av_tc_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                       const __grid_constant__ CUtensorMap map_vhi, const __grid_constant__ CUtensorMap map_vlo,
+                       TcArgs args) {
+    using C = TcCfg<NPAD>;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[C::kStages];
+    __shared__ __align__(8) uint64_t empty_bar[C::kStages];
+    __shared__ __align__(8) uint64_t tmem_full_bar[2];
+    __shared__ __align__(8) uint64_t tmem_empty_bar[2];
+    __shared__ uint32_t tmem_base_smem;
+
+    const int warp = threadIdx.x / kWarp;
+    const int lane = threadIdx.x % kWarp;
+    const int G = gridDim.x;
+    const int cta = blockIdx.x;
+
+    const uint32_t smem_base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* smem_base = smem_raw + (smem_base_u32 - smem_u32(smem_raw));
+
+    const int64_t it_begin = (args.total_iters * cta) / G;
+    const int64_t it_end = (args.total_iters * (cta + 1)) / G;
+    const int KT = args.k_tiles;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&map_ahi);
+        prefetch_tmap(&map_alo);
+        prefetch_tmap(&map_vhi);
+        prefetch_tmap(&map_vlo);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmem_full_bar[b], 1);
+            mbar_init(&tmem_empty_bar[b], 4 * kWarp);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(&tmem_base_smem, C::kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = tmem_base_smem;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            const uint64_t pol_stream = policy_evict_first();
+            const uint64_t pol_keep = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t it = it_begin; it < it_end; ++it) {
+                const int r = static_cast<int>(it / KT);
+                const int k = static_cast<int>(it - static_cast<int64_t>(r) * KT);
+                mbar_wait(&empty_bar[stage], phase ^ 1u);
+                uint8_t* st = smem_base + stage * C::kStageBytes;
+                mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+                tma_load_2d(st, &map_ahi, &full_bar[stage], k * BK, r * BM, pol_stream);
+                tma_load_2d(st + C::kABytes, &map_alo, &full_bar[stage], k * BK, r * BM, pol_stream);
+                tma_load_2d(st + 2 * C::kABytes, &map_vhi, &full_bar[stage], k * BK, 0, pol_keep);
+                tma_load_2d(st + 2 * C::kABytes + C::kVBytes, &map_vlo, &full_bar[stage], k * BK, 0, pol_keep);
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_f16_f32(BM, NPAD);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t chunk = 0;
+            int64_t it = it_begin;
+            while (it < it_end) {
+                const int64_t r = it / KT;
+                const int64_t seg_end = min(it_end, (r + 1) * KT);
+                while (it < seg_end) {
+                    const int64_t cend = min(seg_end, it + args.kc);
+                    const uint32_t buf = chunk & 1u;
+                    const uint32_t use = chunk >> 1;
+                    mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t d_main = tmem_base + buf * (2 * NPAD);
+                    const uint32_t d_corr = d_main + NPAD;
+                    const int64_t cstart = it;
+                    for (; it < cend; ++it) {
+                        mbar_wait(&full_bar[stage], phase);
+                        tc_fence_after();
+                        const uint32_t st = smem_base_u32 + stage * C::kStageBytes;
+                        const uint32_t a_hi = st;
+                        const uint32_t a_lo = st + C::kABytes;
+                        const uint32_t v_hi = st + 2 * C::kABytes;
+                        const uint32_t v_lo = v_hi + C::kVBytes;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const uint32_t off = kk * 32;  // 16 fp16 along K = 32 bytes
+                            const uint32_t acc = (it > cstart || kk > 0) ? 1u : 0u;
+                            const uint64_t dah = umma_desc_sw128(a_hi + off);
+                            const uint64_t dal = umma_desc_sw128(a_lo + off);
+                            const uint64_t dvh = umma_desc_sw128(v_hi + off);
+                            const uint64_t dvl = umma_desc_sw128(v_lo + off);
+                            umma_f16(d_main, dah, dvh, idesc, acc);
+                            umma_f16(d_corr, dah, dvl, idesc, acc);
+                            umma_f16(d_corr, dal, dvh, idesc, 1u);
+                        }
+                        umma_commit(&empty_bar[stage]);
+                        if (++stage == C::kStages) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+                    umma_commit(&tmem_full_bar[buf]);
+                    ++chunk;
+                }
+            }
+        }
+    } else {
+        // ---------------- TMEM drain (warps 2..5) ----------------
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_local = quarter * 32 + lane;
+        const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+        float acc[NPAD];
+#pragma unroll
+        for (int j = 0; j < NPAD; ++j) acc[j] = 0.f;
+        uint32_t chunk = 0;
+        int64_t it = it_begin;
+        while (it < it_end) {
+            const int64_t r = it / KT;
+            const int64_t seg_end = min(it_end, (r + 1) * KT);
+            while (it < seg_end) {
+                const int64_t cend = min(seg_end, it + args.kc);
+                const uint32_t buf = chunk & 1u;
+                const uint32_t use = chunk >> 1;
+                mbar_wait(&tmem_full_bar[buf], use & 1u);
+                tc_fence_after();
+                const uint32_t t_main = lane_base + buf * (2 * NPAD);
+#pragma unroll
+                for (int j0 = 0; j0 < NPAD; j0 += 16) {
+                    float m[16], c[16];
+                    tmem_ld16(t_main + j0, m);
+                    tmem_ld16(t_main + NPAD + j0, c);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i] + c[i];
+                }
+                tc_fence_before();
+                mbar_arrive(&tmem_empty_bar[buf]);
+                it = cend;
+                ++chunk;
+            }
+            // segment finished: publish the partial for row block r
+            const int64_t slot = r + cta;
+            float* dst = args.partial + (slot * NPAD) * BM + row_local;
+#pragma unroll
+            for (int j = 0; j < NPAD; ++j) {
+                dst[j * BM] = acc[j];
+                acc[j] = 0.f;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_base, C::kTmemCols);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+                  uint32_t box_inner, uint32_t box_outer) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {pitch_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int NPAD>
+cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan, float* partial,
+                      cudaStream_t stream) {
+    using C = TcCfg<NPAD>;
+    CUtensorMap m_ahi, m_alo, m_vhi, m_vlo;
+    bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM) &&
+              make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM) &&
+              make_map_f16(&m_vhi, v.hi, v.n, v.cols, v.ld * 2ull, BK, NPAD) &&
+              make_map_f16(&m_vlo, v.lo, v.n, v.cols, v.ld * 2ull, BK, NPAD);
+    if (!ok) return cudaErrorInvalidValue;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(block_av_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    TcArgs args;
+    args.total_iters = plan.total_iters;
+    args.k_tiles = plan.k_tiles;
+    args.kc = plan.kc;
+    args.partial = partial;
+    block_av_tc_kernel<NPAD><<<plan.grid, C::kThreads, C::kSmemBytes, stream>>>(m_ahi, m_alo, m_vhi, m_vlo, args);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int tc_block_rows() { return BM; }
+int tc_block_k() { return BK; }
+
+StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc) {
+    StreamKPlan p;
+    p.row_blocks = static_cast<int>((rows + BM - 1) / BM);
+    p.k_tiles = static_cast<int>((cols + BK - 1) / BK);
+    p.total_iters = static_cast<int64_t>(p.row_blocks) * p.k_tiles;
+    p.grid = grid;
+    if (p.total_iters < grid) p.grid = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
+    p.kc = kc;
+    p.slots = p.row_blocks + p.grid;
+    return p;
+}
+
+int tc_npad(int cols) { return ((cols + 15) / 16) * 16; }
+
+cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
+                               float* partial, cudaStream_t stream) {
+    const int npad = tc_npad(v.cols);
+    switch (npad) {
+        case 16: return launch_tc<16>(a, v, plan, partial, stream);
+        case 32: return launch_tc<32>(a, v, plan, partial, stream);
+        case 48: return launch_tc<48>(a, v, plan, partial, stream);
+        case 64: return launch_tc<64>(a, v, plan, partial, stream);
+        case 80: return launch_tc<80>(a, v, plan, partial, stream);
+        case 96: return launch_tc<96>(a, v, plan, partial, stream);
+        case 112: return launch_tc<112>(a, v, plan, partial, stream);
+        case 128: return launch_tc<128>(a, v, plan, partial, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace rb

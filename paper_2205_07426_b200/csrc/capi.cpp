@@ -1,0 +1,518 @@
+// C ABI (include/renyi_b200.h) over the C++ engine. Exceptions never cross the
+// boundary: every entry point maps rb::Error to its status code and stores the
+// message for renyi_last_error().
+#pragma GCC visibility push(default)
+#include "../../include/renyi_b200.h"
+#pragma GCC visibility pop
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "engine.h"
+
+struct renyi_ctx {
+    explicit renyi_ctx(int device) : ctx(device) {}
+    rb::Context ctx;
+};
+
+struct renyi_kernel {
+    rb::KernelPtr k;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return RENYI_OK;
+    } catch (const rb::Error& e) {
+        g_last_error = e.what();
+        return e.code();
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return RENYI_E_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return RENYI_E_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown failure";
+        return RENYI_E_INTERNAL;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) rb::fail(rb::kInvalidArgument, std::string(what) + " is NULL");
+}
+
+rb::MatFun to_matfun(const renyi_matfun* f) {
+    need(f, "matrix function");
+    switch (f->kind) {
+        case RENYI_MATFUN_INT_POWER: {
+            const double r = std::round(f->alpha);
+            if (std::abs(f->alpha - r) > 1e-9) rb::fail(rb::kInvalidArgument, "int_power needs an integer alpha");
+            return rb::MatFun::int_power(static_cast<int>(r));
+        }
+        case RENYI_MATFUN_TAYLOR:
+            return rb::MatFun::taylor(f->alpha, f->degree, f->v);
+        case RENYI_MATFUN_CHEBYSHEV:
+            return rb::MatFun::chebyshev(f->alpha, f->degree, f->u, f->v);
+        default:
+            rb::fail(rb::kInvalidArgument, "unknown matrix function kind");
+    }
+}
+
+rb::PowerOpts to_power(const renyi_power_options* o) {
+    rb::PowerOpts p;
+    if (o) {
+        p.max_iters = o->max_iters;
+        p.tol = o->tol;
+        p.seed = o->seed;
+        p.rank_floor = o->rank_floor;
+    }
+    return p;
+}
+
+rb::SpectrumBoundsH to_bounds(const renyi_spectrum_bounds& b) {
+    rb::SpectrumBoundsH h;
+    h.u = b.u, h.v = b.v, h.kappa = b.kappa;
+    h.iterations_used = b.iterations_used;
+    h.v_converged = b.v_converged != 0, h.u_converged = b.u_converged != 0, h.rank_deficient = b.rank_deficient != 0;
+    return h;
+}
+
+void from_bounds(const rb::SpectrumBoundsH& h, renyi_spectrum_bounds* b) {
+    b->u = h.u, b->v = h.v, b->kappa = h.kappa;
+    b->iterations_used = h.iterations_used;
+    b->v_converged = h.v_converged, b->u_converged = h.u_converged, b->rank_deficient = h.rank_deficient;
+}
+
+rb::EstParams to_params(const renyi_estimator_params* p) {
+    need(p, "estimator params");
+    rb::EstParams q;
+    q.alpha = p->alpha;
+    q.method = p->method;
+    q.s = p->s, q.m = p->m;
+    q.epsilon = p->epsilon, q.delta = p->delta;
+    q.seed = p->seed;
+    q.power = to_power(&p->power);
+    q.has_bounds = p->has_bounds != 0;
+    q.bounds = to_bounds(p->bounds);
+    q.probe_kind = p->probe_kind;
+    q.s_q = p->s_q, q.s_g = p->s_g;
+    return q;
+}
+
+void from_trace(const rb::TraceEst& t, renyi_trace_estimate* o) {
+    o->value = t.value, o->low_rank_part = t.low_rank_part, o->residual_part = t.residual_part;
+    o->queries_used = t.queries_used, o->sketch_rank = t.sketch_rank, o->exact = t.exact;
+}
+
+void from_entropy(const rb::EntropyEst& e, renyi_entropy_estimate* o) {
+    o->entropy = e.entropy, o->trace_estimate = e.trace_estimate;
+    o->method_used = e.method_used, o->s_used = e.s_used, o->m_used = e.m_used;
+    o->has_bounds = e.has_bounds;
+    from_bounds(e.bounds_used, &o->bounds_used);
+    o->elapsed = e.elapsed;
+    o->deterministic = e.deterministic;
+    from_trace(e.trace, &o->trace);
+}
+
+void check_precision(int precision) {
+    if (precision != RENYI_F64 && precision != RENYI_F32) rb::fail(rb::kInvalidArgument, "unknown precision");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* renyi_last_error(void) { return g_last_error.c_str(); }
+
+int renyi_status_is_usage(int s) {
+    return s == RENYI_E_INVALID_ARGUMENT || s == RENYI_E_SIZE_MISMATCH || s == RENYI_E_DOMAIN_ERROR ||
+           s == RENYI_E_PARSE_ERROR || s == RENYI_E_ALPHA_IS_ONE;
+}
+
+int renyi_ctx_create(int device, renyi_ctx** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = new renyi_ctx(device);
+    });
+}
+
+int renyi_ctx_destroy(renyi_ctx* ctx) {
+    return guarded([&] { delete ctx; });
+}
+
+int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        if (grid < 0 || kc < 1) rb::fail(rb::kInvalidArgument, "grid >= 0 and kc >= 1 required");
+        ctx->ctx.grid = grid;
+        ctx->ctx.kc = kc;
+    });
+}
+
+int renyi_ctx_sync(renyi_ctx* ctx) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        ctx->ctx.sync();
+    });
+}
+
+int renyi_ctx_profile(renyi_ctx* ctx, int enable) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        ctx->ctx.prof_enable(enable != 0);
+    });
+}
+
+int renyi_ctx_profile_read(renyi_ctx* ctx, int* launches, double* ms) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        need(launches, "launches");
+        need(ms, "milliseconds");
+        ctx->ctx.prof_read(launches, ms);
+    });
+}
+
+int renyi_ctx_launch_count(renyi_ctx* ctx, long* launches) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        need(launches, "launches");
+        *launches = ctx->ctx.launches;
+    });
+}
+
+int renyi_kernel_build_gaussian(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                                int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(out, "out");
+        check_precision(precision);
+        auto* k = new renyi_kernel;
+        try {
+            k->k = rb::build_gaussian(ctx->ctx, x, n, d, ldx, sigma, precision);
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                      double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                      int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(y, "second samples"), need(out, "out");
+        check_precision(precision);
+        auto* k = new renyi_kernel;
+        try {
+            k->k = rb::build_gaussian(ctx->ctx, x, n, dx, ldx, sigma_x, precision, y, dy, ldy, sigma_y);
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(a, "matrix"), need(out, "out");
+        check_precision(precision);
+        auto* k = new renyi_kernel;
+        try {
+            k->k = rb::from_matrix(ctx->ctx, a, n, precision);
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int renyi_kernel_hadamard_joint(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(a, "kernel a"), need(b, "kernel b"), need(out, "out");
+        auto* k = new renyi_kernel;
+        try {
+            k->k = rb::hadamard_joint(ctx->ctx, *a->k, *b->k);
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int renyi_kernel_size(const renyi_kernel* k, int64_t* n) {
+    return guarded([&] {
+        need(k, "kernel"), need(n, "n");
+        *n = k->k->n;
+    });
+}
+
+int renyi_kernel_download(renyi_ctx* ctx, const renyi_kernel* k, double* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        rb::download(ctx->ctx, *k->k, out);
+    });
+}
+
+int renyi_kernel_destroy(renyi_kernel* k) {
+    return guarded([&] { delete k; });
+}
+
+int renyi_matmul_panel(renyi_ctx* ctx, const renyi_kernel* k, const double* v, int s, double* y) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(v, "panel"), need(y, "out");
+        if (s < 1) rb::fail(rb::kInvalidArgument, "panel needs at least one column");
+        rb::block_product(ctx->ctx, *k->k, v, s, y);
+    });
+}
+
+int renyi_matvec(renyi_ctx* ctx, const renyi_kernel* k, const double* x, double* y) {
+    return renyi_matmul_panel(ctx, k, x, 1, y);
+}
+
+int renyi_apply_panel(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const double* v, int s,
+                      double* y) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(v, "panel"), need(y, "out");
+        if (s < 1) rb::fail(rb::kInvalidArgument, "panel needs at least one column");
+        rb::apply_panel(ctx->ctx, *k->k, to_matfun(f), v, s, y);
+    });
+}
+
+int renyi_matfun_traces(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const double* x, int s,
+                        double* traces) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(x, "panel"), need(traces, "out");
+        if (s < 1) rb::fail(rb::kInvalidArgument, "panel needs at least one column");
+        rb::matfun_traces(ctx->ctx, *k->k, to_matfun(f), x, s, traces);
+    });
+}
+
+int renyi_power_method(renyi_ctx* ctx, const renyi_kernel* k, const renyi_power_options* opts, double shift,
+                       renyi_power_result* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        const rb::PowerRes r = rb::power_method(ctx->ctx, *k->k, to_power(opts), shift);
+        out->rayleigh = r.rayleigh, out->iterations = r.iterations, out->converged = r.converged;
+    });
+}
+
+int renyi_estimate_bounds(renyi_ctx* ctx, const renyi_kernel* k, const renyi_power_options* opts,
+                          renyi_spectrum_bounds* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        from_bounds(rb::estimate_bounds(ctx->ctx, *k->k, to_power(opts)), out);
+    });
+}
+
+int renyi_hutchpp(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const renyi_sketch* cfg,
+                  renyi_trace_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(cfg, "sketch config"), need(out, "out");
+        rb::SketchCfg c;
+        c.s_q = cfg->s_q, c.s_g = cfg->s_g, c.seed = cfg->seed, c.probe_kind = cfg->probe_kind;
+        c.sketch = cfg->sketch, c.probes = cfg->probes;
+        from_trace(rb::hutchpp(ctx->ctx, *k->k, to_matfun(f), c), out);
+    });
+}
+
+int renyi_estimate(renyi_ctx* ctx, const renyi_kernel* k, const renyi_estimator_params* p,
+                   renyi_entropy_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        from_entropy(rb::estimate(ctx->ctx, *k->k, to_params(p)), out);
+    });
+}
+
+int renyi_entropy_int(renyi_ctx* ctx, const renyi_kernel* k, int alpha, int s, uint64_t seed,
+                      renyi_entropy_estimate* out) {
+    renyi_estimator_params p;
+    renyi_default_params(&p);
+    p.alpha = alpha, p.method = RENYI_METHOD_INT, p.s = s, p.seed = seed;
+    if (alpha < 2) {
+        g_last_error = "entropy_int needs integer alpha >= 2";
+        return RENYI_E_INVALID_ARGUMENT;
+    }
+    return renyi_estimate(ctx, k, &p, out);
+}
+
+int renyi_entropy_taylor(renyi_ctx* ctx, const renyi_kernel* k, double alpha, int s, int m, double v,
+                         uint64_t seed, renyi_entropy_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        rb::validate_alpha(alpha);
+        rb::require_non_integer(alpha, "entropy_taylor");
+        const int m_min = static_cast<int>(std::ceil(alpha)) + 1;
+        if (m < m_min)
+            rb::fail(rb::kInvalidArgument, "entropy_taylor needs m >= ceil(alpha)+1 = " + std::to_string(m_min));
+        rb::EstParams p;
+        p.alpha = alpha, p.method = rb::kMethodTaylor, p.s = s, p.m = m, p.seed = seed;
+        p.has_bounds = true;
+        p.bounds.v = v;
+        p.bounds.u = 0.0;
+        rb::EntropyEst e = rb::estimate(ctx->ctx, *k->k, p);
+        e.has_bounds = false;
+        from_entropy(e, out);
+    });
+}
+
+int renyi_entropy_chebyshev(renyi_ctx* ctx, const renyi_kernel* k, double alpha, int s, int m, double u, double v,
+                            uint64_t seed, renyi_entropy_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        rb::validate_alpha(alpha);
+        rb::require_non_integer(alpha, "entropy_chebyshev");
+        rb::EstParams p;
+        p.alpha = alpha, p.method = rb::kMethodChebyshev, p.s = s, p.m = m, p.seed = seed;
+        p.has_bounds = true;
+        p.bounds.u = u;
+        p.bounds.v = v;
+        rb::EntropyEst e = rb::estimate(ctx->ctx, *k->k, p);
+        e.has_bounds = false;
+        from_entropy(e, out);
+    });
+}
+
+int renyi_mutual_information(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b,
+                             const renyi_estimator_params* p, renyi_mi_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(a, "kernel a"), need(b, "kernel b"), need(out, "out");
+        const rb::MutualInfo mi = rb::mutual_information(ctx->ctx, *a->k, *b->k, to_params(p));
+        out->value = mi.value, out->vars_entropy = mi.vars_entropy;
+        out->target_entropy = mi.target_entropy, out->joint_entropy = mi.joint_entropy;
+    });
+}
+
+int renyi_mutual_information_samples(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                     double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                     const renyi_estimator_params* p, int precision, renyi_mi_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(y, "target samples"), need(out, "out");
+        check_precision(precision);
+        const rb::MutualInfo mi = rb::mutual_information_samples(ctx->ctx, x, n, dx, ldx, sigma_x, y, dy, ldy,
+                                                                 sigma_y, to_params(p), precision);
+        out->value = mi.value, out->vars_entropy = mi.vars_entropy;
+        out->target_entropy = mi.target_entropy, out->joint_entropy = mi.joint_entropy;
+    });
+}
+
+int renyi_entropy(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                  const renyi_estimator_params* p, int precision, renyi_entropy_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(out, "out");
+        check_precision(precision);
+        rb::KernelPtr k = rb::build_gaussian(ctx->ctx, x, n, d, ldx, sigma, precision);
+        from_entropy(rb::estimate(ctx->ctx, *k, to_params(p)), out);
+    });
+}
+
+// ---- host arithmetic ----
+void renyi_default_power_options(renyi_power_options* o) {
+    if (!o) return;
+    o->max_iters = 100;
+    o->tol = 1e-6;
+    o->seed = 0;
+    o->rank_floor = 1e-12;
+}
+
+void renyi_default_params(renyi_estimator_params* p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    p->alpha = 2.0;
+    p->method = RENYI_METHOD_AUTO;
+    p->epsilon = 1e-2;
+    p->delta = 1e-2;
+    renyi_default_power_options(&p->power);
+    p->bounds.v = 1.0;
+    p->bounds.kappa = INFINITY;
+    p->bounds.v_converged = p->bounds.u_converged = 1;
+    p->probe_kind = RENYI_PROBE_GAUSSIAN;
+    p->s_q = p->s_g = -1;
+}
+
+uint64_t renyi_mix64(uint64_t x) { return rb::mix64(x); }
+uint64_t renyi_derive_key(uint64_t seed, uint64_t tag) { return rb::derive_key(seed, tag); }
+uint64_t renyi_hash_name(const char* name) { return name ? rb::hash_name(name) : 0; }
+
+int renyi_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out) {
+    return guarded([&] {
+        need(label, "label"), need(out, "out");
+        if (n < 0 || cols < 0) rb::fail(rb::kInvalidArgument, "negative panel size");
+        rb::probe_panel(n, cols, seed, label, kind, out);
+    });
+}
+
+int renyi_binomial_coeffs(double alpha, int m, double* out) {
+    return guarded([&] {
+        need(out, "out");
+        const auto b = rb::binomial_coeffs(alpha, m);
+        std::copy(b.begin(), b.end(), out);
+    });
+}
+
+int renyi_chebyshev_coeffs(double alpha, int m, double u, double v, double* out) {
+    return guarded([&] {
+        need(out, "out");
+        const auto c = rb::chebyshev_power_coeffs(alpha, m, u, v);
+        std::copy(c.begin(), c.end(), out);
+    });
+}
+
+double renyi_chebyshev_safeguard(double u, double v) { return rb::chebyshev_safeguard(u, v); }
+double renyi_taylor_tail_constant(double alpha, int k_max) { return rb::taylor_tail_constant(alpha, k_max); }
+
+int renyi_matfun_scalar(const renyi_matfun* f, double lambda, double* out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = to_matfun(f).scalar_value(lambda);
+    });
+}
+
+long renyi_expected_queries(const renyi_matfun* f, int s) {
+    try {
+        const rb::MatFun m = to_matfun(f);
+        const long s_q = s / 4, s_g = s - 2 * (s / 4);
+        return s_q + static_cast<long>(m.query_cost()) * (s_q + s_g) + 2 * s_g;
+    } catch (const rb::Error& e) {
+        g_last_error = e.what();
+        return -1;
+    }
+}
+
+int renyi_select_params(double alpha, double epsilon, double delta, const renyi_spectrum_bounds* b, int64_t n,
+                        int method, int* s, int* m) {
+    return guarded([&] {
+        need(b, "bounds"), need(s, "s"), need(m, "m");
+        const rb::SelectedParams sp = rb::select_params(alpha, epsilon, delta, to_bounds(*b), n, method);
+        *s = sp.s, *m = sp.m;
+    });
+}
+
+int renyi_mu_bound(double u, double v, double alpha, int64_t n, double* mu, double* lower, double* upper) {
+    return guarded([&] {
+        const rb::MuBoundH b = rb::mu_bound(u, v, alpha, n);
+        if (mu) *mu = b.mu;
+        if (lower) *lower = b.lower;
+        if (upper) *upper = b.upper;
+    });
+}
+
+int renyi_entropy_from_trace(double trace, double alpha, double* out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = rb::entropy_from_trace(trace, alpha);
+    });
+}
+
+}  // extern "C"

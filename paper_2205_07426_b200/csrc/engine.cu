@@ -1,0 +1,1036 @@
+// Host engine: see engine.h. Control flow restates the reference estimator
+// (proj/src/{kernel,spectrum,poly,hutchpp,entropy,measures}.cpp); all O(n^2)
+// and O(n·s) work runs in the sm_100a kernels, only O(s^2) scalars and the
+// per-pass trace partials come back to the host.
+#include "engine.h"
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+namespace rb {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    (void)cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) fail(kOutOfMemory, std::string(what) + ": out of device memory");
+    fail(kCudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- DevBuf
+DevBuf::~DevBuf() { release(); }
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        release();
+        p_ = o.p_, n_ = o.n_;
+        o.p_ = nullptr, o.n_ = 0;
+    }
+    return *this;
+}
+void DevBuf::alloc(size_t bytes) {
+    release();
+    if (bytes == 0) return;
+    cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
+    n_ = bytes;
+}
+void DevBuf::ensure(size_t bytes) {
+    if (bytes > n_) alloc(bytes);
+}
+void DevBuf::release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr, n_ = 0;
+}
+
+// ---------------------------------------------------------------- Context
+Context::Context(int device) : device_(device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        (void)cudaGetLastError();
+        fail(kNoDevice, "no CUDA device is visible; the renyi_b200 path requires an sm_100a GPU");
+    }
+    if (device < 0 || device >= count) fail(kInvalidArgument, "device index out of range");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) fail(kNoDevice, std::string("renyi_b200 kernels target sm_100a; found ") + prop.name);
+    sms_ = prop.multiProcessorCount;
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    probe_err.alloc(sizeof(int));
+}
+
+Context::~Context() {
+    cudaSetDevice(device_);
+    for (auto& e : events_) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Context::sync() { cuda_check(cudaStreamSynchronize(stream_), "stream synchronize"); }
+
+void Context::prof_enable(bool on) {
+    prof_ = on;
+    prof_used_ = 0;
+}
+void Context::prof_begin() {
+    if (!prof_) return;
+    if (prof_used_ == events_.size()) {
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+        events_.push_back({a, b});
+    }
+    cuda_check(cudaEventRecord(events_[prof_used_].first, stream_), "cudaEventRecord");
+}
+void Context::prof_end() {
+    if (!prof_) return;
+    cuda_check(cudaEventRecord(events_[prof_used_].second, stream_), "cudaEventRecord");
+    ++prof_used_;
+}
+void Context::prof_read(int* n, double* ms) {
+    sync();
+    double total = 0.0;
+    for (size_t i = 0; i < prof_used_; ++i) {
+        float t = 0.f;
+        cuda_check(cudaEventElapsedTime(&t, events_[i].first, events_[i].second), "cudaEventElapsedTime");
+        total += t;
+    }
+    *n = static_cast<int>(prof_used_);
+    *ms = total;
+    prof_used_ = 0;
+}
+
+namespace {
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+inline void launched(Context& ctx, cudaError_t e, const char* what) {
+    cuda_check(e, what);
+    ++ctx.launches;
+}
+
+void check_finite(const double* x, int64_t n, int64_t d, int64_t ld, double* max_abs) {
+    double mx = 0.0;
+    for (int64_t j = 0; j < d; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            const double v = x[i + j * ld];
+            if (!std::isfinite(v)) fail(kNonFinite, "sample matrix contains non-finite values");
+            mx = std::max(mx, std::abs(v));
+        }
+    *max_abs = mx;
+}
+
+void shard_rows(Context& ctx, int64_t n, int64_t* row0, int64_t* rows) {
+    if (!ctx.exchange || ctx.exchange->world() == 1) {
+        *row0 = 0, *rows = n;
+        return;
+    }
+    const int r = ctx.exchange->rank(), w = ctx.exchange->world();
+    // equal shards (multiple of 128 rows except the last) so the all-gather is uniform
+    const int64_t per = round_up((n + w - 1) / w, 128);
+    *row0 = std::min<int64_t>(n, per * r);
+    *rows = std::min<int64_t>(n, per * (r + 1)) - *row0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- kernel matrices
+KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
+                         const double* y, int64_t dy, int64_t ldy, double sigma_y) {
+    // validate_samples (proj/src/kernel.cpp:25-29) + sigma check (kernel.cpp:42)
+    if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
+    if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
+    if (!(sigma > 0.0)) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
+    double mx = 0.0, my = 0.0;
+    check_finite(x, n, d, ldx, &mx);
+    if (y) {
+        if (dy < 1) fail(kInvalidArgument, "second variable needs at least one feature");
+        if (!(sigma_y > 0.0)) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
+        check_finite(y, n, dy, ldy, &my);
+    }
+    if (prec == kF32 && std::max(mx, my) > 1e18)
+        fail(kNonFinite, "sample values exceed the fp32 range of the fp32 configuration");
+
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    auto k = std::make_unique<KernelMatrix>();
+    k->n = n;
+    k->prec = prec;
+    shard_rows(ctx, n, &k->row0, &k->rows);
+    k->ld = round_up(n, 8);
+    const double inv_n = 1.0 / static_cast<double>(n);
+    k->normalized = true;
+    k->a_norm = 1.0;
+
+    // samples, row-major on the device
+    const int64_t dtot = d + (y ? dy : 0);
+    std::vector<double> xr(static_cast<size_t>(n) * dtot);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = 0; j < d; ++j) xr[i * d + j] = x[i + j * ldx];
+    }
+    double* yr_host = nullptr;
+    if (y) {
+        yr_host = xr.data() + n * d;
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < dy; ++j) yr_host[i * dy + j] = y[i + j * ldy];
+    }
+    DevBuf xs;
+    xs.alloc(xr.size() * sizeof(double));
+    cuda_check(cudaMemcpyAsync(xs.as<double>(), xr.data(), xr.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx.stream()),
+               "upload samples");
+    GramArgs g;
+    g.x = xs.as<double>();
+    g.dx = static_cast<int>(d);
+    g.inv_two_sigma2_x = 1.0 / (2.0 * sigma * sigma);
+    g.y = y ? xs.as<double>() + n * d : nullptr;
+    g.dy = static_cast<int>(dy);
+    g.inv_two_sigma2_y = y ? 1.0 / (2.0 * sigma_y * sigma_y) : 0.0;
+    g.n = n;
+    g.row0 = k->row0;
+    g.rows = k->rows;
+    g.ld = k->ld;
+    g.inv_n = inv_n;
+    g.f32_compute = prec == kF32 ? 1 : 0;
+    const size_t elems = static_cast<size_t>(k->rows) * k->ld;
+    if (prec == kF32) {
+        k->hi.alloc(elems * sizeof(__half));
+        k->lo.alloc(elems * sizeof(__half));
+        k->unscale = inv_n / kSplitScale;
+        launched(ctx, launch_gram_split(g, k->hi.as<__half>(), k->lo.as<__half>(), ctx.stream()), "gram_split");
+    } else {
+        k->a64.alloc(elems * sizeof(double));
+        k->unscale = 1.0;
+        launched(ctx, launch_gram_f64(g, k->a64.as<double>(), ctx.stream()), "gram_f64");
+    }
+    ctx.sync();  // xs goes out of scope
+    return k;
+}
+
+KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
+    if (n < 1) fail(kInvalidArgument, "matrix must be non-empty");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    auto k = std::make_unique<KernelMatrix>();
+    k->n = n;
+    k->prec = prec;
+    shard_rows(ctx, n, &k->row0, &k->rows);
+    k->ld = round_up(n, 8);
+    k->normalized = false;
+    std::vector<double> rm(static_cast<size_t>(k->rows) * k->ld, 0.0);
+    double mx = 0.0, norm = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double rs = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            const double v = a[i + j * n];
+            if (!std::isfinite(v)) fail(kNonFinite, "matrix contains non-finite values");
+            rs += std::abs(v);
+            mx = std::max(mx, std::abs(v));
+        }
+        norm = std::max(norm, rs);
+    }
+    for (int64_t i = 0; i < k->rows; ++i)
+        for (int64_t j = 0; j < n; ++j) rm[i * k->ld + j] = a[(k->row0 + i) + j * n];
+    k->a_norm = norm;
+    DevBuf up;
+    up.alloc(rm.size() * sizeof(double));
+    cuda_check(cudaMemcpyAsync(up.as<double>(), rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx.stream()),
+               "upload matrix");
+    if (prec == kF32) {
+        int e = 0;
+        if (mx > 0.0) {
+            int E;
+            std::frexp(mx, &E);  // mx < 2^E
+            e = kSplitScaleLog2 - E;
+        }
+        const double scale = std::ldexp(1.0, e);
+        k->unscale = std::ldexp(1.0, -e);
+        const size_t elems = static_cast<size_t>(k->rows) * k->ld;
+        k->hi.alloc(elems * sizeof(__half));
+        k->lo.alloc(elems * sizeof(__half));
+        cuda_check(cudaMemsetAsync(k->hi.as<__half>(), 0, elems * sizeof(__half), ctx.stream()), "memset");
+        cuda_check(cudaMemsetAsync(k->lo.as<__half>(), 0, elems * sizeof(__half), ctx.stream()), "memset");
+        launched(ctx,
+                 launch_matrix_to_split(up.as<double>(), k->rows, n, k->ld, scale, k->hi.as<__half>(),
+                                        k->lo.as<__half>(), k->ld, ctx.stream()),
+                 "matrix_to_split");
+        ctx.sync();
+    } else {
+        k->unscale = 1.0;
+        ctx.sync();
+        k->a64 = std::move(up);
+    }
+    return k;
+}
+
+KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix& b) {
+    // proj/src/kernel.cpp:74-101 with L = 2 (the product is commutative, so the
+    // canonical content order only matters for L >= 3 rounding)
+    if (a.n != b.n)
+        fail(kSizeMismatch,
+             "hadamard_joint kernel sizes differ: " + std::to_string(a.n) + " vs " + std::to_string(b.n));
+    if (a.prec != b.prec) fail(kInvalidArgument, "hadamard_joint needs kernels of the same precision");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    auto c = std::make_unique<KernelMatrix>();
+    c->n = a.n, c->row0 = a.row0, c->rows = a.rows, c->ld = a.ld, c->prec = a.prec;
+    const double nd = static_cast<double>(a.n);
+    const double inv_n = 1.0 / nd;
+    // |n A_ij B_ij| row sums: <= n * max|B| * ||A||_inf (<= 1 for normalised factors)
+    c->a_norm = (a.normalized && b.normalized) ? 1.0 : std::max(1.0, a.a_norm * b.a_norm * nd);
+    c->normalized = a.normalized && b.normalized;
+    const size_t elems = static_cast<size_t>(c->rows) * c->ld;
+    if (a.prec == kF32) {
+        c->unscale = inv_n / kSplitScale;
+        const double factor = nd * a.unscale * b.unscale / c->unscale;
+        const double diag = inv_n / c->unscale;
+        c->hi.alloc(elems * sizeof(__half));
+        c->lo.alloc(elems * sizeof(__half));
+        launched(ctx,
+                 launch_hadamard_split(a.hi.as<__half>(), a.lo.as<__half>(), b.hi.as<__half>(), b.lo.as<__half>(),
+                                       c->rows, c->n, c->ld, c->row0, factor, diag, c->hi.as<__half>(),
+                                       c->lo.as<__half>(), ctx.stream()),
+                 "hadamard_split");
+    } else {
+        c->unscale = 1.0;
+        c->a64.alloc(elems * sizeof(double));
+        launched(ctx,
+                 launch_hadamard_f64(a.a64.as<double>(), b.a64.as<double>(), c->rows, c->n, c->ld, c->row0, nd,
+                                     c->a64.as<double>(), ctx.stream()),
+                 "hadamard_f64");
+    }
+    ctx.sync();
+    return c;
+}
+
+void download(Context& ctx, const KernelMatrix& k, double* out) {
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    std::vector<double> rm(static_cast<size_t>(k.rows) * k.n);
+    if (k.prec == kF32) {
+        DevBuf tmp;
+        tmp.alloc(rm.size() * sizeof(double));
+        launched(ctx,
+                 launch_split_to_f64(k.hi.as<__half>(), k.lo.as<__half>(), k.rows, k.n, k.ld, k.unscale,
+                                     tmp.as<double>(), k.n, ctx.stream()),
+                 "split_to_f64");
+        cuda_check(cudaMemcpyAsync(rm.data(), tmp.as<double>(), rm.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx.stream()),
+                   "download");
+        ctx.sync();
+    } else {
+        cuda_check(cudaMemcpy2DAsync(rm.data(), k.n * sizeof(double), k.a64.as<double>(), k.ld * sizeof(double),
+                                     k.n * sizeof(double), k.rows, cudaMemcpyDeviceToHost, ctx.stream()),
+                   "download");
+        ctx.sync();
+    }
+    for (int64_t i = 0; i < k.rows; ++i)
+        for (int64_t j = 0; j < k.n; ++j) out[(k.row0 + i) + j * k.n] = rm[i * k.n + j];
+}
+
+// ---------------------------------------------------------------- panel sessions
+namespace {
+
+class PanelSession {
+public:
+    PanelSession(Context& ctx, const KernelMatrix& k, const double* x, int64_t ldx, int s, int max_passes,
+                 double* acc_out, double acc_coef0)
+        : ctx_(ctx), k_(k), s_(s), max_passes_(max_passes), acc_(acc_out) {
+        if (s < 1 || s > kMaxPanelCols) fail(kInternal, "panel width must be in [1,128]");
+        if (ctx.exchange && ctx.exchange->world() > 1 && k.rows != k.n)
+            fail(kInvalidArgument, "row-sharded panels need the multi-rank exchange path");
+        rows_ = k.rows;
+        ld_ = round_up(k.n, 8);
+        R_ = static_cast<int>((rows_ + 127) / 128);
+        const size_t st = k.prec == kF32 ? sizeof(float) : sizeof(double);
+        for (auto& b : ctx.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
+        if (k.prec == kF32) {
+            ctx.vhi.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
+            ctx.vlo.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
+        }
+        const size_t P1 = static_cast<size_t>(max_passes) + 1;
+        ctx.stats.ensure(P1 * 3 * R_ * s * sizeof(double));
+        ctx.red.ensure(P1 * 3 * s * sizeof(double));
+        ctx.cmax.ensure(P1 * s * sizeof(unsigned));
+        ctx.eexp.ensure(P1 * s * sizeof(int));
+        cuda_check(cudaMemsetAsync(ctx.cmax.as<unsigned>(), 0, P1 * s * sizeof(unsigned), ctx.stream()), "memset");
+        if (k.prec == kF32) {
+            const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
+            plan_ = make_streamk_plan(rows_, k.n, grid, ctx.kc);
+            npad_ = tc_npad(s);
+            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * 128 * sizeof(float));
+            PrepArgs<float> p{};
+            p.x = x, p.ldx = ldx, p.rows = rows_, p.s = s, p.ld = ld_;
+            p.t0 = buf<float>(0);
+            p.cmax0 = ctx.cmax.as<unsigned>();
+            p.stats = ctx.stats.as<double>();
+            p.e0 = ctx.eexp.as<int>();
+            p.vhi = ctx.vhi.as<__half>(), p.vlo = ctx.vlo.as<__half>();
+            p.acc = acc_out, p.acc_coef = acc_coef0;
+            launched(ctx, launch_prepare_split(p, ctx.stream()), "prepare");
+        } else {
+            plan_ = make_f64_plan(rows_, k.n);
+            npad_ = f64_npad(s);
+            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * 128 * sizeof(double));
+            PrepArgs<double> p{};
+            p.x = x, p.ldx = ldx, p.rows = rows_, p.s = s, p.ld = ld_;
+            p.t0 = buf<double>(0);
+            p.cmax0 = ctx.cmax.as<unsigned>();
+            p.stats = ctx.stats.as<double>();
+            p.acc = acc_out, p.acc_coef = acc_coef0;
+            launched(ctx, launch_prepare_f64(p, ctx.stream()), "prepare");
+        }
+    }
+
+    void step(double a1, double a2, double a3, double acc_coef) {
+        if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
+        const int k = k_done_;
+        const size_t s = static_cast<size_t>(s_);
+        if (k_.prec == kF32) {
+            SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
+            SplitPanelView v{ctx_.vhi.as<__half>(), ctx_.vlo.as<__half>(), k_.n, s_, ld_};
+            ctx_.prof_begin();
+            launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()), "block_av_tc");
+            ctx_.prof_end();
+            EpiArgs<float, float> e{};
+            e.partial = ctx_.partial.as<float>();
+            e.npad = npad_;
+            e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
+            e.rows = rows_, e.s = s_, e.ld = ld_;
+            e.e_cur = ctx_.eexp.as<int>() + k * s;
+            e.e_next = ctx_.eexp.as<int>() + (k + 1) * s;
+            e.unscale = k_.unscale;
+            e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;
+            e.cmax_prev = k > 0 ? ctx_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
+            e.cmax_new = ctx_.cmax.as<unsigned>() + (k + 1) * s;
+            e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm;
+            e.t_cur = buf<float>(k);
+            e.t_prev = k > 0 ? buf<float>(k - 1) : nullptr;
+            e.t_new = buf<float>(k + 1);
+            e.x0 = buf<float>(0);
+            e.vhi = ctx_.vhi.as<__half>(), e.vlo = ctx_.vlo.as<__half>();
+            e.stats = ctx_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
+            e.acc = acc_, e.acc_coef = acc_coef;
+            launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
+        } else {
+            ctx_.prof_begin();
+            launched(ctx_,
+                     launch_block_av_f64(k_.a64.as<double>(), rows_, k_.n, k_.ld, buf<double>(k), s_, ld_,
+                                         ctx_.partial.as<double>(), ctx_.stream()),
+                     "block_av_f64");
+            ctx_.prof_end();
+            EpiArgs<double, double> e{};
+            e.partial = ctx_.partial.as<double>();
+            e.npad = npad_;
+            e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
+            e.rows = rows_, e.s = s_, e.ld = ld_;
+            e.unscale = 1.0;
+            e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;
+            e.cmax_prev = k > 0 ? ctx_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
+            e.cmax_new = ctx_.cmax.as<unsigned>() + (k + 1) * s;
+            e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm;
+            e.t_cur = buf<double>(k);
+            e.t_prev = k > 0 ? buf<double>(k - 1) : nullptr;
+            e.t_new = buf<double>(k + 1);
+            e.x0 = buf<double>(0);
+            e.stats = ctx_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
+            e.acc = acc_, e.acc_coef = acc_coef;
+            launched(ctx_, launch_epilogue_f64(e, ctx_.stream()), "epilogue");
+        }
+        ++k_done_;
+    }
+
+    // dots for passes [p0, p1] (inclusive), [p][3][s]; synchronizes
+    std::vector<double> dots(int p0, int p1) {
+        const int np = p1 - p0 + 1;
+        const size_t s = static_cast<size_t>(s_);
+        launched(ctx_,
+                 launch_reduce_stats(ctx_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
+                                     ctx_.red.as<double>(), ctx_.stream()),
+                 "reduce_stats");
+        std::vector<double> out(static_cast<size_t>(np) * 3 * s);
+        cuda_check(cudaMemcpyAsync(out.data(), ctx_.red.as<double>(), out.size() * sizeof(double),
+                                   cudaMemcpyDeviceToHost, ctx_.stream()),
+                   "download stats");
+        ctx_.sync();
+        return out;
+    }
+
+    void state_f64(int k, double* out, int64_t ldo) {
+        launched(ctx_,
+                 launch_state_to_f64(k_.prec == kF32 ? static_cast<const void*>(buf<float>(k))
+                                                     : static_cast<const void*>(buf<double>(k)),
+                                     k_.prec == kF32, rows_, s_, ld_, out, ldo, ctx_.stream()),
+                 "state_to_f64");
+    }
+
+    int passes() const { return k_done_; }
+    int64_t ld() const { return ld_; }
+
+private:
+    template <typename T>
+    T* buf(int k) const {
+        if (k == 0) return ctx_.state[0].as<T>();
+        return ctx_.state[1 + (k - 1) % 3].as<T>();
+    }
+
+    Context& ctx_;
+    const KernelMatrix& k_;
+    int s_;
+    int max_passes_;
+    double* acc_;
+    int64_t rows_ = 0, ld_ = 0;
+    int R_ = 0;
+    int npad_ = 0;
+    int k_done_ = 0;
+    StreamKPlan plan_;
+};
+
+}  // namespace
+
+PanelResult run_panel(Context& ctx, const KernelMatrix& k, const double* x, int64_t ldx, int s,
+                      const std::vector<std::array<double, 3>>& coeffs, const std::vector<double>* acc_coef,
+                      double* acc_out, double* last_out, int64_t ldo) {
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int P = static_cast<int>(coeffs.size());
+    PanelSession ps(ctx, k, x, ldx, s, std::max(P, 1), acc_out, acc_coef ? (*acc_coef)[0] : 0.0);
+    for (int p = 0; p < P; ++p)
+        ps.step(coeffs[p][0], coeffs[p][1], coeffs[p][2], acc_coef ? (*acc_coef)[p + 1] : 0.0);
+    if (last_out) ps.state_f64(P, last_out, ldo);
+    PanelResult r;
+    r.passes = P;
+    r.s = s;
+    r.dots = ps.dots(0, P);
+    return r;
+}
+
+namespace {
+
+std::vector<std::array<double, 3>> schedule(const MatFun& f) {
+    std::vector<std::array<double, 3>> c(f.degree);
+    for (int k = 0; k < f.degree; ++k) f.pass_coeffs(k, &c[k][0], &c[k][1], &c[k][2]);
+    return c;
+}
+
+// upload a host column-major panel (n x s) into a device fp64 buffer [s][ld]
+void upload_panel(Context& ctx, DevBuf& dst, const double* host, int64_t n, int s, int64_t ld) {
+    dst.ensure(static_cast<size_t>(s) * ld * sizeof(double));
+    cuda_check(cudaMemcpy2DAsync(dst.as<double>(), ld * sizeof(double), host, n * sizeof(double),
+                                 n * sizeof(double), s, cudaMemcpyHostToDevice, ctx.stream()),
+               "upload panel");
+}
+
+void download_panel(Context& ctx, const double* dev, int64_t ld, int64_t n, int s, double* host) {
+    cuda_check(cudaMemcpy2DAsync(host, n * sizeof(double), dev, ld * sizeof(double), n * sizeof(double), s,
+                                 cudaMemcpyDeviceToHost, ctx.stream()),
+               "download panel");
+    ctx.sync();
+}
+
+void require_single_rank(Context& ctx, const char* what) {
+    if (ctx.exchange && ctx.exchange->world() > 1)
+        fail(kInvalidArgument, std::string(what) + " is a single-rank parity seam");
+}
+
+}  // namespace
+
+void block_product(Context& ctx, const KernelMatrix& k, const double* v, int s, double* y) {
+    require_single_rank(ctx, "matmul_panel");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int64_t n = k.n, ld = round_up(n, 8);
+    for (int j0 = 0; j0 < s; j0 += kMaxPanelCols) {
+        const int w = std::min(kMaxPanelCols, s - j0);
+        upload_panel(ctx, ctx.x0, v + j0 * n, n, w, ld);
+        ctx.work.ensure(static_cast<size_t>(w) * ld * sizeof(double));
+        run_panel(ctx, k, ctx.x0.as<double>(), ld, w, {{1.0, 0.0, 0.0}}, nullptr, nullptr, ctx.work.as<double>(),
+                  ld);
+        download_panel(ctx, ctx.work.as<double>(), ld, n, w, y + j0 * n);
+    }
+}
+
+void apply_panel(Context& ctx, const KernelMatrix& k, const MatFun& f, const double* v, int s, double* y) {
+    require_single_rank(ctx, "apply_panel");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int64_t n = k.n, ld = round_up(n, 8);
+    std::vector<double> coef(f.degree + 1, 0.0);
+    double post = 1.0;
+    if (f.kind == kTaylor) {
+        for (int i = 0; i <= f.degree; ++i) coef[i] = f.coeffs[i];
+        post = std::pow(f.v, f.alpha);
+    } else if (f.kind == kChebyshev) {
+        coef[0] = 0.5 * f.coeffs[0];
+        for (int i = 1; i <= f.degree; ++i) coef[i] = f.coeffs[i];
+    }
+    for (int j0 = 0; j0 < s; j0 += kMaxPanelCols) {
+        const int w = std::min(kMaxPanelCols, s - j0);
+        upload_panel(ctx, ctx.x0, v + j0 * n, n, w, ld);
+        ctx.acc.ensure(static_cast<size_t>(w) * ld * sizeof(double));
+        if (f.kind == kIntPower) {
+            run_panel(ctx, k, ctx.x0.as<double>(), ld, w, schedule(f), nullptr, nullptr, ctx.acc.as<double>(), ld);
+        } else {
+            run_panel(ctx, k, ctx.x0.as<double>(), ld, w, schedule(f), &coef, ctx.acc.as<double>(), nullptr, 0);
+        }
+        download_panel(ctx, ctx.acc.as<double>(), ld, n, w, y + j0 * n);
+        if (post != 1.0)
+            for (int64_t i = 0; i < n * w; ++i) y[j0 * n + i] *= post;
+    }
+}
+
+namespace {
+
+// per-column traces x_j^T f(A) x_j for a device panel [s][ldx], in groups of <= 128 columns
+std::vector<double> panel_traces(Context& ctx, const KernelMatrix& k, const MatFun& f, const double* x, int64_t ldx,
+                                 int s) {
+    std::vector<double> tr(s, 0.0);
+    const auto sched = schedule(f);
+    for (int j0 = 0; j0 < s; j0 += kMaxPanelCols) {
+        const int w = std::min(kMaxPanelCols, s - j0);
+        PanelResult r = run_panel(ctx, k, x + static_cast<int64_t>(j0) * ldx, ldx, w, sched);
+        std::vector<double> d(f.degree + 1);
+        for (int j = 0; j < w; ++j) {
+            for (int p = 0; p <= f.degree; ++p) d[p] = r.dot(p, 0, j);
+            tr[j0 + j] = f.combine(d.data(), 1);
+        }
+    }
+    return tr;
+}
+
+}  // namespace
+
+void matfun_traces(Context& ctx, const KernelMatrix& k, const MatFun& f, const double* x, int s, double* out) {
+    require_single_rank(ctx, "matfun_traces");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int64_t n = k.n, ld = round_up(n, 8);
+    DevBuf xs;
+    upload_panel(ctx, xs, x, n, s, ld);
+    std::vector<double> tr = panel_traces(ctx, k, f, xs.as<double>(), ld, s);
+    std::copy(tr.begin(), tr.end(), out);
+}
+
+// ---------------------------------------------------------------- spectrum
+PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, double shift) {
+    // proj/src/spectrum.cpp:13-49; shift > 0 runs on (shift·I − A) without forming it
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int64_t n = k.n, ld = round_up(n, 8);
+    ctx.x0.ensure(static_cast<size_t>(ld) * sizeof(double));
+    cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
+    const uint64_t key = derive_key(o.seed, hash_name("power-start"));
+    launched(ctx,
+             launch_rng_panel(key, false, kProbeGaussian, n, 1, 0, ctx.x0.as<double>(), ld, ctx.probe_err.as<int>(),
+                              ctx.stream()),
+             "rng_panel");
+    PowerRes res;
+    const int iters = std::max(o.max_iters, 0);
+    PanelSession ps(ctx, k, ctx.x0.as<double>(), ld, 1, std::max(iters, 1), nullptr, 0.0);
+    std::vector<double> d0 = ps.dots(0, 0);
+    double norm = std::sqrt(d0[2]);
+    if (norm == 0.0) fail(kInternal, "power-start vector is zero");
+    double g = 1.0 / norm;  // x = T/||T||
+    double prev = 0.0;
+    for (int it = 1; it <= iters; ++it) {
+        if (shift != 0.0)
+            ps.step(-g, shift * g, 0.0, 0.0);
+        else
+            ps.step(g, 0.0, 0.0, 0.0);
+        std::vector<double> d = ps.dots(it, it);
+        const double quotient = g * d[1];
+        res.rayleigh = quotient;
+        res.iterations = it;
+        if (it > 1 && std::abs(quotient - prev) <= o.tol * std::abs(quotient)) {
+            res.converged = true;
+            break;
+        }
+        prev = quotient;
+        const double ny = std::sqrt(d[2]);
+        if (ny == 0.0) {
+            res.converged = true;
+            break;
+        }
+        g = 1.0 / ny;
+    }
+    return res;
+}
+
+SpectrumBoundsH estimate_bounds(Context& ctx, const KernelMatrix& k, const PowerOpts& o) {
+    // proj/src/spectrum.cpp:80-103
+    SpectrumBoundsH b;
+    const PowerRes rv = power_method(ctx, k, o, 0.0);
+    const double inv_n = 1.0 / static_cast<double>(k.n);
+    b.v = std::clamp(rv.rayleigh * (1.0 + o.tol), inv_n, 1.0);
+    b.v_converged = rv.converged;
+    PowerOpts so = o;
+    so.seed = derive_key(o.seed, hash_name("shifted"));
+    const PowerRes ru = power_method(ctx, k, so, b.v);
+    b.u_converged = ru.converged;
+    double u = (b.v - ru.rayleigh) * (1.0 - o.tol);
+    const double floor = std::max(o.rank_floor, b.v * o.tol * 100.0);
+    if (u < floor) {
+        u = 0.0;
+        b.rank_deficient = true;
+    }
+    b.u = std::min(u, inv_n);
+    b.kappa = b.u > 0.0 ? b.v / b.u : std::numeric_limits<double>::infinity();
+    b.iterations_used = rv.iterations + ru.iterations;
+    return b;
+}
+
+// ---------------------------------------------------------------- Hutch++
+namespace {
+
+// fp64 probe panel on the device [cols][ld]: injected host panel or the reference stream
+void make_probes(Context& ctx, DevBuf& dst, int64_t n, int cols, int64_t ld, const double* host, uint64_t seed,
+                 const char* label, int kind) {
+    dst.ensure(static_cast<size_t>(cols) * ld * sizeof(double));
+    if (host) {
+        upload_panel(ctx, dst, host, n, cols, ld);
+        return;
+    }
+    cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
+    launched(ctx,
+             launch_rng_panel(derive_key(seed, hash_name(label)), true, kind, n, cols, 0, dst.as<double>(), ld,
+                              ctx.probe_err.as<int>(), ctx.stream()),
+             "rng_panel");
+    int err = 0;
+    cuda_check(cudaMemcpyAsync(&err, ctx.probe_err.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()),
+               "probe flag");
+    ctx.sync();
+    if (err) fail(kInternal, "probe stream hit the 2^-53 Box-Muller redraw; pass the probes explicitly");
+}
+
+std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx, const double* z, int q,
+                              int64_t ldz, int64_t rows) {
+    std::vector<double> out(static_cast<size_t>(p) * q);
+    const int grid = std::min<int64_t>(ctx.sms(), std::max<int64_t>(1, (rows + 31) / 32));
+    // column blocks of z so p * qb <= 2048
+    const int qb_max = std::max(1, 2048 / std::max(p, 1));
+    ctx.small.ensure(static_cast<size_t>(p) * q * sizeof(double));
+    for (int b0 = 0; b0 < q; b0 += qb_max) {
+        const int qb = std::min(qb_max, q - b0);
+        ctx.gram_partial.ensure(static_cast<size_t>(grid) * p * qb * sizeof(double));
+        launched(ctx,
+                 launch_panel_gram(x, p, ldx, z + static_cast<int64_t>(b0) * ldz, qb, ldz, rows,
+                                   ctx.gram_partial.as<double>(), grid, ctx.small.as<double>() + static_cast<size_t>(b0) * p,
+                                   ctx.stream()),
+                 "panel_gram");
+    }
+    cuda_check(cudaMemcpyAsync(out.data(), ctx.small.as<double>(), out.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx.stream()),
+               "download gram");
+    ctx.sync();
+    return out;
+}
+
+// W = beta*G + X*C on the device; C is a host p x q column-major matrix
+void update(Context& ctx, double beta, const double* g, int64_t ldg, const double* x, int p, int64_t ldx,
+            const std::vector<double>& c, int q, int64_t rows, double* w, int64_t ldw) {
+    DevBuf cd;
+    cd.alloc(c.size() * sizeof(double));
+    cuda_check(cudaMemcpyAsync(cd.as<double>(), c.data(), c.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx.stream()),
+               "upload coefficients");
+    // smem limit: split q
+    const int qb_max = std::max(1, (48 * 1024 / 8) / std::max(p, 1));
+    for (int b0 = 0; b0 < q; b0 += qb_max) {
+        const int qb = std::min(qb_max, q - b0);
+        launched(ctx,
+                 launch_panel_update(beta, g ? g + static_cast<int64_t>(b0) * ldg : nullptr, ldg, x, p, ldx,
+                                     cd.as<double>() + static_cast<size_t>(b0) * p, qb, rows,
+                                     w + static_cast<int64_t>(b0) * ldw, ldw, ctx.stream()),
+                 "panel_update");
+    }
+    ctx.sync();
+}
+
+// Orthonormal basis of range(Y) (Y device [p][ld], n rows) by CholeskyQR2 with an
+// eigen-based first step (rank-revealing); returns the rank and writes Q [rank][ld].
+// Replaces Eigen::ColPivHouseholderQR + setThreshold(1e-12) (proj/src/hutchpp.cpp:91-108):
+// tr(Q^T f Q) and I - QQ^T are basis-invariant, so only the kept subspace matters.
+int orthonormal_range(Context& ctx, const double* y, int p, int64_t ld, int64_t n, DevBuf& q_out) {
+    std::vector<double> g = gram_host(ctx, y, p, ld, y, p, ld, n);
+    std::vector<double> w, v;
+    sym_eig_desc(p, g, w, v);
+    if (!(w.size() > 0 && w[0] > 0.0)) return 0;
+    const double tau = 1e-13;
+    int k = 0;
+    while (k < p && w[k] > tau * w[0]) ++k;
+    if (k == 0) return 0;
+    std::vector<double> m1(static_cast<size_t>(p) * k);
+    for (int c = 0; c < k; ++c) {
+        const double s = 1.0 / std::sqrt(w[c]);
+        for (int r = 0; r < p; ++r) m1[r + static_cast<size_t>(c) * p] = v[r + static_cast<size_t>(c) * p] * s;
+    }
+    DevBuf q1;
+    q1.alloc(static_cast<size_t>(k) * ld * sizeof(double));
+    update(ctx, 0.0, nullptr, ld, y, p, ld, m1, k, n, q1.as<double>(), ld);
+    // second (Cholesky) pass for orthogonality to working precision
+    std::vector<double> g2 = gram_host(ctx, q1.as<double>(), k, ld, q1.as<double>(), k, ld, n);
+    std::vector<double> r2;
+    q_out.ensure(static_cast<size_t>(k) * ld * sizeof(double));
+    if (cholesky_upper(k, g2, r2)) {
+        update(ctx, 0.0, nullptr, ld, q1.as<double>(), k, ld, upper_inverse(k, r2), k, n, q_out.as<double>(), ld);
+    } else {
+        std::vector<double> w2, v2;
+        sym_eig_desc(k, g2, w2, v2);
+        std::vector<double> m2(static_cast<size_t>(k) * k);
+        for (int c = 0; c < k; ++c)
+            for (int r = 0; r < k; ++r)
+                m2[r + static_cast<size_t>(c) * k] = v2[r + static_cast<size_t>(c) * k] / std::sqrt(w2[c]);
+        update(ctx, 0.0, nullptr, ld, q1.as<double>(), k, ld, m2, k, n, q_out.as<double>(), ld);
+    }
+    return k;
+}
+
+double exact_trace(Context& ctx, const KernelMatrix& k, const MatFun& f) {
+    // proj/src/hutchpp.cpp:53-65: identity panels
+    const int64_t n = k.n, ld = round_up(n, 8);
+    double sum = 0.0;
+    DevBuf eye;
+    for (int64_t j0 = 0; j0 < n; j0 += kMaxPanelCols) {
+        const int w = static_cast<int>(std::min<int64_t>(kMaxPanelCols, n - j0));
+        std::vector<double> h(static_cast<size_t>(n) * w, 0.0);
+        for (int j = 0; j < w; ++j) h[(j0 + j) + static_cast<size_t>(j) * n] = 1.0;
+        upload_panel(ctx, eye, h.data(), n, w, ld);
+        std::vector<double> tr = panel_traces(ctx, k, f, eye.as<double>(), ld, w);
+        for (double t : tr) sum += t;
+    }
+    return sum;
+}
+
+}  // namespace
+
+TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const SketchCfg& cfg) {
+    // proj/src/hutchpp.cpp:69-115, with probe injection / explicit split / Q-empty Hutchinson
+    require_single_rank(ctx, "hutchpp");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int64_t n = k.n, ld = round_up(n, 8);
+    const int s_q = cfg.s_q, s_g = cfg.s_g;
+    const int cost = f.query_cost();
+    if (s_q < 0 || s_g < 0 || s_q + s_g < 1) fail(kInvalidArgument, "hutchpp needs a positive query budget");
+    TraceEst est;
+    if (s_q >= n) {
+        est.value = est.low_rank_part = exact_trace(ctx, k, f);
+        est.residual_part = 0.0;
+        est.sketch_rank = static_cast<int>(n);
+        est.queries_used = static_cast<int>(n) * cost;
+        est.exact = true;
+        return est;
+    }
+    DevBuf qbuf;
+    int rank = 0;
+    if (s_q > 0) {
+        DevBuf sk;
+        make_probes(ctx, sk, n, s_q, ld, cfg.sketch, cfg.seed, "hutchpp-sketch", cfg.probe_kind);
+        DevBuf y;
+        y.alloc(static_cast<size_t>(s_q) * ld * sizeof(double));
+        for (int j0 = 0; j0 < s_q; j0 += kMaxPanelCols) {
+            const int w = std::min(kMaxPanelCols, s_q - j0);
+            run_panel(ctx, k, sk.as<double>() + j0 * ld, ld, w, {{1.0, 0.0, 0.0}}, nullptr, nullptr,
+                      y.as<double>() + j0 * ld, ld);
+        }
+        rank = orthonormal_range(ctx, y.as<double>(), s_q, ld, n, qbuf);
+        if (rank == 0) fail(kRankCollapse, "hutchpp sketch A*S is numerically zero");
+        est.sketch_rank = rank;
+        est.queries_used = s_q + rank * cost;
+    }
+    const int64_t codim = n - rank;
+    if (s_q > 0 && s_g >= codim) {
+        // trace the complement exactly (proj/src/hutchpp.cpp:100-106)
+        std::vector<double> qh(static_cast<size_t>(n) * rank);
+        download_panel(ctx, qbuf.as<double>(), ld, n, rank, qh.data());
+        std::vector<double> full = complete_basis(n, rank, qh);
+        DevBuf fb;
+        upload_panel(ctx, fb, full.data(), n, static_cast<int>(n), ld);
+        std::vector<double> tr = panel_traces(ctx, k, f, fb.as<double>(), ld, static_cast<int>(n));
+        double low = 0.0, res = 0.0;
+        for (int j = 0; j < rank; ++j) low += tr[j];
+        for (int64_t j = rank; j < n; ++j) res += tr[j];
+        est.low_rank_part = low;
+        est.residual_part = res;
+        est.queries_used += static_cast<int>(codim) * cost;
+        est.exact = true;
+    } else {
+        // X0 = [Q | W],  W = G - Q (Q^T G)
+        const int cols = rank + s_g;
+        DevBuf x0;
+        x0.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
+        if (rank > 0)
+            cuda_check(cudaMemcpyAsync(x0.as<double>(), qbuf.as<double>(), static_cast<size_t>(rank) * ld * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, ctx.stream()),
+                       "copy Q");
+        if (s_g > 0) {
+            double* wdst = x0.as<double>() + static_cast<int64_t>(rank) * ld;
+            DevBuf gp;
+            make_probes(ctx, gp, n, s_g, ld, cfg.probes, cfg.seed, "hutchpp-probe", cfg.probe_kind);
+            if (rank > 0) {
+                std::vector<double> c = gram_host(ctx, qbuf.as<double>(), rank, ld, gp.as<double>(), s_g, ld, n);
+                for (double& v : c) v = -v;
+                update(ctx, 1.0, gp.as<double>(), ld, qbuf.as<double>(), rank, ld, c, s_g, n, wdst, ld);
+            } else {
+                cuda_check(cudaMemcpyAsync(wdst, gp.as<double>(), static_cast<size_t>(s_g) * ld * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, ctx.stream()),
+                           "copy probes");
+            }
+        }
+        std::vector<double> tr = panel_traces(ctx, k, f, x0.as<double>(), ld, cols);
+        double low = 0.0, res = 0.0;
+        for (int j = 0; j < rank; ++j) low += tr[j];
+        for (int j = rank; j < cols; ++j) res += tr[j];
+        est.low_rank_part = low;
+        est.residual_part = s_g > 0 ? res / s_g : 0.0;
+        est.queries_used += s_g * cost;
+    }
+    est.value = est.low_rank_part + est.residual_part;
+    return est;
+}
+
+// ---------------------------------------------------------------- estimators
+namespace {
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+EntropyEst from_hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, double alpha, int s, const EstParams& p,
+                        int method, int m_used) {
+    const auto t0 = std::chrono::steady_clock::now();
+    SketchCfg cfg;
+    if (p.s_q >= 0 || p.s_g >= 0) {
+        cfg.s_q = std::max(p.s_q, 0);
+        cfg.s_g = std::max(p.s_g, 0);
+    } else {
+        if (s < 8) fail(kInvalidArgument, "hutchpp needs a query budget s >= 8");
+        cfg.s_q = s / 4;
+        cfg.s_g = s - 2 * (s / 4);
+    }
+    cfg.seed = p.seed;
+    cfg.probe_kind = p.probe_kind;
+    const TraceEst tr = hutchpp(ctx, k, f, cfg);
+    EntropyEst est;
+    est.trace = tr;
+    est.trace_estimate = tr.value;
+    est.entropy = entropy_from_trace(tr.value, alpha);
+    est.method_used = method;
+    est.s_used = s;
+    est.m_used = m_used;
+    est.deterministic = tr.exact;
+    est.elapsed = seconds_since(t0);
+    return est;
+}
+
+}  // namespace
+
+EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p) {
+    // proj/src/entropy.cpp:201-275
+    validate_alpha(p.alpha);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t n = k.n;
+    int alpha_int = 0;
+    const bool is_int = integer_alpha(p.alpha, &alpha_int);
+    bool have = p.has_bounds;
+    SpectrumBoundsH bounds = p.bounds;
+    auto ensure_bounds = [&]() -> const SpectrumBoundsH& {
+        if (!have) {
+            PowerOpts o = p.power;
+            o.seed = derive_key(p.seed, hash_name("bounds"));
+            bounds = estimate_bounds(ctx, k, o);
+            have = true;
+        }
+        return bounds;
+    };
+    int method = p.method;
+    if (method == kMethodAuto) {
+        if (is_int) {
+            method = kMethodInt;
+        } else {
+            const SpectrumBoundsH& b = ensure_bounds();
+            const bool flat_full_rank = b.u > 0.0 && b.kappa <= 50.0;
+            const bool flat_deficient = b.u == 0.0 && b.v * static_cast<double>(n) <= 50.0;
+            method = (flat_full_rank || flat_deficient) ? kMethodTaylor : kMethodChebyshev;
+        }
+    }
+    EntropyEst est;
+    switch (method) {
+        case kMethodExact:
+            fail(kInvalidArgument,
+                 "method=exact is the O(n^3) eigendecomposition check oracle; it is not a device path");
+        case kMethodInt: {
+            if (!is_int) fail(kInvalidArgument, "method=int needs an integer alpha >= 2");
+            const int s = p.s > 0 ? p.s
+                                  : select_params(p.alpha, p.epsilon, p.delta, SpectrumBoundsH{}, n, kMethodInt).s;
+            if (alpha_int < 2) fail(kInvalidArgument, "entropy_int needs integer alpha >= 2");
+            est = from_hutchpp(ctx, k, MatFun::int_power(alpha_int), alpha_int, s, p, kMethodInt, 0);
+            break;
+        }
+        case kMethodTaylor:
+        case kMethodChebyshev: {
+            const SpectrumBoundsH& b = ensure_bounds();
+            SelectedParams sel;
+            if (p.s > 0 && p.m > 0) {
+                sel = {p.s, p.m};
+            } else {
+                sel = select_params(p.alpha, p.epsilon, p.delta, b, n, method);
+                if (p.s > 0) sel.s = p.s;
+                if (p.m > 0) sel.m = p.m;
+            }
+            validate_alpha(p.alpha);
+            if (method == kMethodTaylor) {
+                require_non_integer(p.alpha, "entropy_taylor");
+                const int m = std::max(sel.m, static_cast<int>(std::ceil(p.alpha)) + 1);
+                const int m_min = static_cast<int>(std::ceil(p.alpha)) + 1;
+                if (m < m_min) fail(kInvalidArgument, "entropy_taylor needs m >= ceil(alpha)+1");
+                est = from_hutchpp(ctx, k, MatFun::taylor(p.alpha, m, b.v), p.alpha, sel.s, p, kMethodTaylor, m);
+            } else {
+                require_non_integer(p.alpha, "entropy_chebyshev");
+                est = from_hutchpp(ctx, k, MatFun::chebyshev(p.alpha, sel.m, b.u, b.v), p.alpha, sel.s, p,
+                                   kMethodChebyshev, sel.m);
+            }
+            break;
+        }
+        default:
+            fail(kInvalidArgument, "unresolved auto method");
+    }
+    est.has_bounds = have;
+    est.bounds_used = bounds;
+    est.elapsed = seconds_since(t0);
+    return est;
+}
+
+EstParams with_seed(const EstParams& p, const char* term) {
+    EstParams q = p;
+    q.seed = derive_key(p.seed, hash_name(term));
+    return q;
+}
+
+MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelMatrix& b, const EstParams& p) {
+    // proj/src/measures.cpp:36-46 (single-variable set: vars_joint = a)
+    KernelPtr joint = hadamard_joint(ctx, a, b);
+    MutualInfo mi;
+    mi.vars_entropy = estimate(ctx, a, with_seed(p, "term:vars")).entropy;
+    mi.target_entropy = estimate(ctx, b, with_seed(p, "term:target")).entropy;
+    mi.joint_entropy = estimate(ctx, *joint, with_seed(p, "term:joint")).entropy;
+    mi.value = mi.vars_entropy + mi.target_entropy - mi.joint_entropy;
+    return mi;
+}
+
+MutualInfo mutual_information_samples(Context& ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                      double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                      const EstParams& p, int prec) {
+    MutualInfo mi;
+    {
+        KernelPtr a = build_gaussian(ctx, x, n, dx, ldx, sigma_x, prec);
+        mi.vars_entropy = estimate(ctx, *a, with_seed(p, "term:vars")).entropy;
+    }
+    {
+        KernelPtr b = build_gaussian(ctx, y, n, dy, ldy, sigma_y, prec);
+        mi.target_entropy = estimate(ctx, *b, with_seed(p, "term:target")).entropy;
+    }
+    {
+        KernelPtr j = build_gaussian(ctx, x, n, dx, ldx, sigma_x, prec, y, dy, ldy, sigma_y);
+        mi.joint_entropy = estimate(ctx, *j, with_seed(p, "term:joint")).entropy;
+    }
+    mi.value = mi.vars_entropy + mi.target_entropy - mi.joint_entropy;
+    return mi;
+}
+
+}  // namespace rb

@@ -1,0 +1,202 @@
+// Host engine: device context, device-resident kernel matrices, and the
+// estimator pipeline (recurrence passes, power iteration, Hutch++, estimate,
+// mutual information) driving the sm_100a kernels. This is the C++ host surface
+// that mirrors the reference library (proj/include/renyi/*.hpp); the C ABI in
+// include/renyi_b200.h wraps it.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <array>
+#include <memory>
+#include <vector>
+
+#include "host_math.h"
+#include "kernels.h"
+
+namespace rb {
+
+enum Precision : int { kF64 = 0, kF32 = 1 };
+
+void cuda_check(cudaError_t e, const char* what);
+
+class DevBuf {
+public:
+    DevBuf() = default;
+    ~DevBuf();
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept;
+    void alloc(size_t bytes);
+    void ensure(size_t bytes);  // grow-only
+    void release();
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p_);
+    }
+    size_t bytes() const { return n_; }
+
+private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// Multi-rank exchange hooks (row-sharded A). nullptr = single rank.
+struct Exchange {
+    virtual ~Exchange() = default;
+    virtual int rank() const = 0;
+    virtual int world() const = 0;
+    // gather equal-size row shards: each rank contributes `count` bytes at `send`
+    // into `recv` laid out [world][count] — used per column plane.
+    virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+    virtual void allreduce_sum_f64(double* buf, size_t count, cudaStream_t s) = 0;
+    virtual void allreduce_max_u32(unsigned* buf, size_t count, cudaStream_t s) = 0;
+};
+
+class Context {
+public:
+    explicit Context(int device);
+    ~Context();
+    int device() const { return device_; }
+    cudaStream_t stream() const { return stream_; }
+    int sms() const { return sms_; }
+    void sync();
+
+    // tuning knobs of the block product
+    int grid = 0;  // CTAs of the persistent stream-K kernel (0 = SM count)
+    int kc = 16;   // k tiles (x64 columns) per TMEM accumulation chunk
+
+    // instrumentation: CUDA-event timing of every block-product launch
+    void prof_enable(bool on);
+    void prof_begin();
+    void prof_end();
+    // synchronizes; returns launches and summed device milliseconds since enable
+    void prof_read(int* launches, double* ms);
+    long launches = 0;  // kernels launched by the engine (all kinds)
+
+    Exchange* exchange = nullptr;
+
+    // scratch (grow-only)
+    DevBuf partial, stats, red, cmax, eexp, gram_partial, small, probe_err;
+    DevBuf state[4], vhi, vlo, x0, work, acc;
+
+private:
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    int sms_ = 148;
+    bool prof_ = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;
+    size_t prof_used_ = 0;
+};
+
+struct KernelMatrix {
+    int64_t n = 0;      // samples (columns)
+    int64_t row0 = 0;   // first row held by this rank
+    int64_t rows = 0;   // rows held by this rank
+    int64_t ld = 0;     // row pitch (elements)
+    int prec = kF32;
+    double unscale = 1.0;  // A = stored * unscale (split planes)
+    double a_norm = 1.0;   // >= max_i sum_j |A_ij|
+    bool normalized = true;
+    DevBuf a64, hi, lo;
+};
+
+using KernelPtr = std::unique_ptr<KernelMatrix>;
+
+// ---- kernel construction (proj/src/kernel.cpp) ----
+// x: host column-major n x d (Eigen layout of the reference), ld >= n.
+KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
+                         const double* y = nullptr, int64_t dy = 0, int64_t ldy = 0, double sigma_y = 1.0);
+KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec);
+KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix& b);
+void download(Context& ctx, const KernelMatrix& k, double* out_colmajor);
+
+// ---- passes ----
+struct PanelResult {
+    int passes = 0;
+    int s = 0;
+    std::vector<double> dots;  // [(passes+1)][3][s]: x0·T_k, T_{k-1}·T_k, T_k·T_k
+    double dot(int k, int q, int j) const { return dots[(static_cast<size_t>(k) * 3 + q) * s + j]; }
+};
+
+// Runs T_0 = X (device fp64 [s][ldx]) through `coeffs.size()` passes.
+// acc_coef (optional, size passes+1): acc = sum_k acc_coef[k] T_k into acc_out (device fp64 [s][ldo]).
+// last_out (optional): T_passes as fp64 [s][ldo].
+PanelResult run_panel(Context& ctx, const KernelMatrix& k, const double* x, int64_t ldx, int s,
+                      const std::vector<std::array<double, 3>>& coeffs, const std::vector<double>* acc_coef = nullptr,
+                      double* acc_out = nullptr, double* last_out = nullptr, int64_t ldo = 0);
+
+// Y = A V for host panels (ops::matmul_panel seam)
+void block_product(Context& ctx, const KernelMatrix& k, const double* v, int s, double* y);
+// f(A) V for host panels (apply_panel seam)
+void apply_panel(Context& ctx, const KernelMatrix& k, const MatFun& f, const double* v, int s, double* y);
+// per-column x_j^T f(A) x_j, host panel
+void matfun_traces(Context& ctx, const KernelMatrix& k, const MatFun& f, const double* x, int s, double* out);
+
+// ---- spectrum (proj/src/spectrum.cpp) ----
+struct PowerOpts {
+    int max_iters = 100;
+    double tol = 1e-6;
+    uint64_t seed = 0;
+    double rank_floor = 1e-12;
+};
+struct PowerRes {
+    double rayleigh = 0.0;
+    int iterations = 0;
+    bool converged = false;
+};
+PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, double shift);
+SpectrumBoundsH estimate_bounds(Context& ctx, const KernelMatrix& k, const PowerOpts& o);
+
+// ---- Hutch++ (proj/src/hutchpp.cpp) ----
+struct SketchCfg {
+    int s_q = 0, s_g = 0;
+    uint64_t seed = 0;
+    int probe_kind = kProbeGaussian;
+    const double* sketch = nullptr;  // optional host n x s_q
+    const double* probes = nullptr;  // optional host n x s_g
+};
+struct TraceEst {
+    double value = 0.0, low_rank_part = 0.0, residual_part = 0.0;
+    int queries_used = 0, sketch_rank = 0;
+    bool exact = false;
+};
+TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const SketchCfg& cfg);
+
+// ---- estimators (proj/src/entropy.cpp, proj/src/measures.cpp) ----
+struct EstParams {
+    double alpha = 2.0;
+    int method = kMethodAuto;
+    int s = 0, m = 0;
+    double epsilon = 1e-2, delta = 1e-2;
+    uint64_t seed = 0;
+    PowerOpts power;
+    bool has_bounds = false;
+    SpectrumBoundsH bounds;
+    int probe_kind = kProbeGaussian;
+    int s_q = -1, s_g = -1;  // explicit split; -1 = reference split floor(s/4), s-2floor(s/4)
+};
+struct EntropyEst {
+    double entropy = 0.0, trace_estimate = 0.0;
+    int method_used = kMethodExact, s_used = 0, m_used = 0;
+    bool has_bounds = false;
+    SpectrumBoundsH bounds_used;
+    double elapsed = 0.0;
+    bool deterministic = false;
+    TraceEst trace;
+};
+EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p);
+
+struct MutualInfo {
+    double value = 0.0, vars_entropy = 0.0, target_entropy = 0.0, joint_entropy = 0.0;
+};
+MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelMatrix& b, const EstParams& p);
+// memory-lean MI straight from samples: one n x n matrix resident at a time
+MutualInfo mutual_information_samples(Context& ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                      double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                      const EstParams& p, int prec);
+EstParams with_seed(const EstParams& p, const char* term);
+
+}  // namespace rb

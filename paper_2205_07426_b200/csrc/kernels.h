@@ -1,0 +1,168 @@
+// Host-side declarations of the device kernels (launch wrappers). Layout
+// conventions, shared by every kernel:
+//   * kernel matrix A (n_local x n): row-major, pitch `ld` elements. The fp32
+//     configurations store A as two fp16 planes (hi, lo) of A·n·2^14; the fp64
+//     configuration stores A itself.
+//   * panels (iterates, probes): column-major n x cols, column j at j*ld.
+//   * product partials: [slot][npad][128] (tile-column-major) in fp32 / fp64.
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace rb {
+
+constexpr double kSplitScale = 16384.0;  // 2^14: A·n lies in [0,1]; stored planes hold A·n·2^14
+constexpr int kSplitScaleLog2 = 14;
+constexpr int kPanelTarget = 15;  // iterate planes are scaled so max|v| < 2^15 (fp16 max 65504)
+constexpr int kMaxPanelCols = 128;
+
+struct SplitMatrixView {
+    const __half* hi;
+    const __half* lo;
+    int64_t rows, cols, ld;
+};
+
+struct SplitPanelView {
+    const __half* hi;
+    const __half* lo;
+    int64_t n;
+    int cols;
+    int64_t ld;
+};
+
+struct StreamKPlan {
+    int row_blocks = 0;
+    int k_tiles = 0;
+    int64_t total_iters = 0;
+    int grid = 1;
+    int kc = 16;
+    int slots = 0;
+};
+
+// ---- block product -------------------------------------------------------
+int tc_block_rows();
+int tc_block_k();
+int tc_npad(int cols);
+StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc);
+cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
+                               float* partial, cudaStream_t stream);
+
+StreamKPlan make_f64_plan(int64_t rows, int64_t cols);
+int f64_npad(int cols);
+cudaError_t launch_block_av_f64(const double* a, int64_t rows, int64_t cols, int64_t lda, const double* v, int s,
+                                int64_t ldv, double* partial, cudaStream_t stream);
+
+// ---- pass epilogue (recurrence + fused fp64 trace partials) --------------
+template <typename PT, typename ST>
+struct EpiArgs {
+    const PT* partial;
+    int npad;
+    int64_t total_iters;
+    int k_tiles;
+    int grid;
+    int64_t rows;  // local rows (product rows)
+    int s;
+    int64_t ld;
+    const int* e_cur;  // split only
+    int* e_next;       // split only
+    double unscale;    // product scale: 2^-14/n (split) or 1
+    const unsigned* cmax_cur;
+    const unsigned* cmax_prev;  // may be null when a3 == 0
+    unsigned* cmax_new;
+    double a1, a2, a3;
+    double a_norm;  // bound on max_i sum_j |A_ij|
+    const ST* t_cur;
+    const ST* t_prev;
+    ST* t_new;
+    const ST* x0;
+    __half* vhi;
+    __half* vlo;
+    double* stats;  // [3][row_blocks][s]
+    double* acc;    // optional vector accumulator (fp64, [s][ld])
+    double acc_coef;
+};
+
+cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream);
+cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t stream);
+
+// T0 <- X0 (fp64 input); stats[0] and cmax[0]; then planes with exponent e0.
+template <typename ST>
+struct PrepArgs {
+    const double* x;  // [s][ldx]
+    int64_t ldx;
+    int64_t rows;
+    int s;
+    int64_t ld;
+    ST* t0;
+    unsigned* cmax0;
+    double* stats;  // [3][row_blocks][s]
+    int* e0;
+    __half* vhi;
+    __half* vlo;
+    double* acc;  // optional: acc = acc_coef * t0
+    double acc_coef;
+};
+cudaError_t launch_prepare_split(const PrepArgs<float>& a, cudaStream_t stream);
+cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream);
+
+// out[p][q][j] = sum_r stats[p][q][r][j] (fixed order)
+cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks, int s, double* out,
+                                cudaStream_t stream);
+
+// state (fp32/fp64, [s][ld]) -> fp64 [s][ldo]
+cudaError_t launch_state_to_f64(const void* state, bool is_f32, int64_t rows, int s, int64_t ld, double* out,
+                                int64_t ldo, cudaStream_t stream);
+
+// ---- small dense panel algebra (fp64) ------------------------------------
+// C[p x q] = X^T Z over rows; partial buffer must hold grid*p*q doubles.
+cudaError_t launch_panel_gram(const double* x, int p, int64_t ldx, const double* z, int q, int64_t ldz,
+                              int64_t rows, double* partial, int grid, double* out, cudaStream_t stream);
+// W = beta*G + X*C   (X: rows x p, C: p x q column-major, W/G: rows x q)
+cudaError_t launch_panel_update(double beta, const double* g, int64_t ldg, const double* x, int p, int64_t ldx,
+                                const double* c, int q, int64_t rows, double* w, int64_t ldw, cudaStream_t stream);
+
+// ---- probes ----------------------------------------------------------------
+// Column j of the panel draws from RandomStream(derive_key(base_key, j0 + j)),
+// or from RandomStream(base_key) itself when derive == false (single column).
+// kind 0 = Gaussian (Box-Muller, reference stream order), 1 = Rademacher.
+cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t rows, int cols, int j0, double* out,
+                             int64_t ld, int* err_flag, cudaStream_t stream);
+
+// ---- kernel-matrix construction --------------------------------------------
+// Gaussian Gram + trace normalisation (reference build_kernel for sigma):
+// A_ij = fl(1/n) * exp(-max(0, |x_i|^2+|x_j|^2-2 x_i.x_j) / (2 sigma^2)), A_ii = 1/n.
+// Optional second sample set (Y) gives the normalised Hadamard joint
+// n * A^X_ij * A^Y_ij with diag 1/n.
+struct GramArgs {
+    const double* x;  // samples, row-major n x dx (fp64; fp32 configs pass fp32-rounded values)
+    int dx;
+    double inv_two_sigma2_x;
+    const double* y;  // optional second variable (nullptr)
+    int dy;
+    double inv_two_sigma2_y;
+    int64_t n;        // samples (= columns of A)
+    int64_t row0;     // first row of this shard
+    int64_t rows;     // rows in this shard
+    int64_t ld;       // pitch of the output
+    double inv_n;
+    int f32_compute;  // 1: distances/exponentials in fp32 (fp32 configs); 0: fp64
+};
+cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStream_t stream);
+cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream);
+
+// A (fp64 row-major) -> planes holding A*scale.
+cudaError_t launch_matrix_to_split(const double* a, int64_t rows, int64_t cols, int64_t lda, double scale,
+                                   __half* hi, __half* lo, int64_t ld, cudaStream_t stream);
+// Elementwise normalised Hadamard on split planes: stored C = factor*sA*sB, diagonal = diag_value.
+cudaError_t launch_hadamard_split(const __half* ahi, const __half* alo, const __half* bhi, const __half* blo,
+                                  int64_t rows, int64_t cols, int64_t ld, int64_t row0, double factor,
+                                  double diag_value, __half* chi, __half* clo, cudaStream_t stream);
+cudaError_t launch_hadamard_f64(const double* a, const double* b, int64_t rows, int64_t cols, int64_t ld,
+                                int64_t row0, double n, double* c, cudaStream_t stream);
+// split planes -> fp64 (A = (hi+lo) * unscale)
+cudaError_t launch_split_to_f64(const __half* hi, const __half* lo, int64_t rows, int64_t cols, int64_t ld,
+                                double unscale, double* out, int64_t ldo, cudaStream_t stream);
+
+}  // namespace rb

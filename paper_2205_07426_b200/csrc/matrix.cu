@@ -1,0 +1,281 @@
+// Kernel-matrix construction on the device.
+//
+// K1+K2 (+K4): Gaussian Gram, trace normalisation and the normalised
+// Hadamard joint, fused into one pass that writes A straight into its HBM
+// storage format. Reference: ops::gaussian_gram / gaussian_row
+// (proj/src/ops.cpp:9-20,39-47), build_kernel (proj/src/kernel.cpp:35-72),
+// hadamard_joint / hadamard_scaled (proj/src/kernel.cpp:74-101,
+// proj/src/ops.cpp:116-122).
+//
+// Arithmetic per entry follows the reference: d2 = (|x_i|^2 + |x_j|^2) − 2·x_i·x_j,
+// clamp at 0, K = exp(−d2 · 1/(2σ²)), K_ii = 1 exactly; A = fl(1/n)·K. The
+// fp32 configurations compute d2 and exp in fp32 (inputs are fp32 samples) and
+// store K·2^14 (= A·n·2^14) as an fp16 hi/lo pair; the fp64 configuration
+// stores fl(1/n)·K in fp64. Both are exactly symmetric (the formula is).
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rb {
+
+namespace {
+
+constexpr int TM = 64;  // output tile rows
+constexpr int TN = 64;  // output tile cols
+constexpr int TKd = 32; // feature chunk
+
+template <typename T>
+struct GramTile {
+    // accumulates dot products and squared norms of one 64x64 tile over a feature block
+    __device__ static void accumulate(const double* __restrict__ x, int d, int64_t n, int64_t row0, int64_t col0,
+                                      T (&dot)[4][4], T (&sqr)[4], T (&sqc)[4], T (*xr)[TM + 1],
+                                      T (*xc)[TN + 4]) {
+        const int tid = threadIdx.x;
+        const int tx = tid % 16, ty = tid / 16;
+        for (int k0 = 0; k0 < d; k0 += TKd) {
+            const int kc = min(TKd, d - k0);
+            for (int idx = tid; idx < TM * TKd; idx += blockDim.x) {
+                const int rr = idx / TKd, kk = idx % TKd;
+                const int64_t gr = row0 + rr;
+                xr[kk][rr] = (kk < kc && gr < n) ? static_cast<T>(x[gr * d + k0 + kk]) : T(0);
+                const int64_t gc = col0 + rr;
+                xc[kk][rr] = (kk < kc && gc < n) ? static_cast<T>(x[gc * d + k0 + kk]) : T(0);
+            }
+            __syncthreads();
+            for (int kk = 0; kk < kc; ++kk) {
+                T a[4], b[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = xr[kk][ty + 16 * u];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) b[v] = xc[kk][4 * tx + v];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    sqr[u] = fma(a[u], a[u], sqr[u]);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) dot[u][v] = fma(a[u], b[v], dot[u][v]);
+                }
+#pragma unroll
+                for (int v = 0; v < 4; ++v) sqc[v] = fma(b[v], b[v], sqc[v]);
+            }
+            __syncthreads();
+        }
+    }
+};
+
+__device__ __forceinline__ float kexp(float x) { return expf(x); }
+__device__ __forceinline__ double kexp(double x) { return exp(x); }
+
+template <typename T, bool SPLIT>
+__global__ void __launch_bounds__(256) gram_kernel(GramArgs g, __half* __restrict__ hi, __half* __restrict__ lo,
+                                                   double* __restrict__ a64) {
+    __shared__ T xr[TKd][TM + 1];
+    __shared__ T xc[TKd][TN + 4];
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t row0 = g.row0 + static_cast<int64_t>(blockIdx.y) * TM;  // global sample index of tile rows
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * TN;
+
+    T dot[4][4], sqr[4], sqc[4];
+    T kval[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        sqr[u] = sqc[u] = T(0);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dot[u][v] = T(0);
+    }
+    GramTile<T>::accumulate(g.x, g.dx, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+    const T ax = static_cast<T>(g.inv_two_sigma2_x);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            T d2 = (sqr[u] + sqc[v]) - T(2) * dot[u][v];
+            if (d2 < T(0)) d2 = T(0);
+            kval[u][v] = kexp(-d2 * ax);
+        }
+    if (g.y) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sqr[u] = sqc[u] = T(0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dot[u][v] = T(0);
+        }
+        GramTile<T>::accumulate(g.y, g.dy, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+        const T ay = static_cast<T>(g.inv_two_sigma2_y);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                T d2 = (sqr[u] + sqc[v]) - T(2) * dot[u][v];
+                if (d2 < T(0)) d2 = T(0);
+                const T ky = kexp(-d2 * ay);
+                if (SPLIT) {
+                    kval[u][v] = kval[u][v] * ky;
+                } else {
+                    // reference op order: n * ((inv_n*Kx) * (inv_n*Ky)); finished below
+                    kval[u][v] = kval[u][v];
+                    dot[u][v] = ky;  // stash Ky
+                }
+            }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t gi = row0 + ty + 16 * u;  // sample index
+        if (gi >= g.row0 + g.rows || gi >= g.n) continue;
+        const int64_t li = gi - g.row0;         // local row
+        const int64_t gj0 = col0 + 4 * tx;
+        if (SPLIT) {
+            __half h[4], l[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                float kv = static_cast<float>(kval[u][v]);
+                if (gi == gj0 + v) kv = 1.0f;
+                const float s = kv * static_cast<float>(kSplitScale);
+                h[v] = __float2half_rn(s);
+                l[v] = __float2half_rn(s - __half2float(h[v]));
+            }
+            __half* ph = hi + li * g.ld + gj0;
+            __half* pl = lo + li * g.ld + gj0;
+            if (gj0 + 3 < g.n) {
+                *reinterpret_cast<uint2*>(ph) = make_uint2(
+                    (static_cast<uint32_t>(__half_as_ushort(h[1])) << 16) | __half_as_ushort(h[0]),
+                    (static_cast<uint32_t>(__half_as_ushort(h[3])) << 16) | __half_as_ushort(h[2]));
+                *reinterpret_cast<uint2*>(pl) = make_uint2(
+                    (static_cast<uint32_t>(__half_as_ushort(l[1])) << 16) | __half_as_ushort(l[0]),
+                    (static_cast<uint32_t>(__half_as_ushort(l[3])) << 16) | __half_as_ushort(l[2]));
+            } else {
+                for (int v = 0; v < 4; ++v)
+                    if (gj0 + v < g.n) {
+                        ph[v] = h[v];
+                        pl[v] = l[v];
+                    }
+            }
+        } else {
+            double* pa = a64 + li * g.ld + gj0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int64_t gj = gj0 + v;
+                if (gj >= g.n) continue;
+                double val;
+                if (gi == gj) {
+                    val = g.inv_n;
+                } else if (g.y) {
+                    const double ax_ = g.inv_n * static_cast<double>(kval[u][v]);
+                    const double ay_ = g.inv_n * static_cast<double>(dot[u][v]);
+                    val = static_cast<double>(g.n) * (ax_ * ay_);
+                } else {
+                    val = g.inv_n * static_cast<double>(kval[u][v]);
+                }
+                pa[v] = val;
+            }
+        }
+    }
+}
+
+__global__ void matrix_to_split_kernel(const double* __restrict__ a, int64_t rows, int64_t cols, int64_t lda,
+                                       double scale, __half* __restrict__ hi, __half* __restrict__ lo, int64_t ld) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = a[i * lda + j] * scale;
+        const __half h = __double2half(v);
+        hi[i * ld + j] = h;
+        lo[i * ld + j] = __double2half(v - static_cast<double>(__half2float(h)));
+    }
+}
+
+__global__ void split_to_f64_kernel(const __half* __restrict__ hi, const __half* __restrict__ lo, int64_t rows,
+                                    int64_t cols, int64_t ld, double unscale, double* __restrict__ out,
+                                    int64_t ldo) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i * ldo + j] = (static_cast<double>(__half2float(hi[i * ld + j])) +
+                            static_cast<double>(__half2float(lo[i * ld + j]))) *
+                           unscale;
+}
+
+__global__ void hadamard_split_kernel(const __half* __restrict__ ahi, const __half* __restrict__ alo,
+                                      const __half* __restrict__ bhi, const __half* __restrict__ blo, int64_t rows,
+                                      int64_t cols, int64_t ld, int64_t row0, double factor, double diag_value,
+                                      __half* __restrict__ chi, __half* __restrict__ clo) {
+    const int64_t i = blockIdx.y;
+    // stored values S = X / unscale_X; stored C = n·uA·uB/uC · Sa·Sb = factor · Sa·Sb
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = i * ld + j;
+        double v;
+        if (row0 + i == j) {
+            v = diag_value;
+        } else {
+            const double sa = static_cast<double>(__half2float(ahi[k])) + static_cast<double>(__half2float(alo[k]));
+            const double sb = static_cast<double>(__half2float(bhi[k])) + static_cast<double>(__half2float(blo[k]));
+            v = factor * (sa * sb);
+        }
+        const __half h = __double2half(v);
+        chi[k] = h;
+        clo[k] = __double2half(v - static_cast<double>(__half2float(h)));
+    }
+}
+
+__global__ void hadamard_f64_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t rows,
+                                    int64_t cols, int64_t ld, int64_t row0, double n, double* __restrict__ c) {
+    const int64_t i = blockIdx.y;
+    const double inv_n = 1.0 / n;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = i * ld + j;
+        c[k] = (row0 + i == j) ? inv_n : n * (a[k] * b[k]);
+    }
+}
+
+inline dim3 row_grid(int64_t rows, int64_t cols) {
+    const int64_t bx = (cols + 255) / 256;
+    return dim3(static_cast<unsigned>(bx > 64 ? 64 : bx), static_cast<unsigned>(rows));
+}
+
+}  // namespace
+
+cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStream_t stream) {
+    dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
+    if (g.f32_compute)
+        gram_kernel<float, true><<<grid, 256, 0, stream>>>(g, hi, lo, nullptr);
+    else
+        gram_kernel<double, true><<<grid, 256, 0, stream>>>(g, hi, lo, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream) {
+    dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
+    gram_kernel<double, false><<<grid, 256, 0, stream>>>(g, nullptr, nullptr, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_matrix_to_split(const double* a, int64_t rows, int64_t cols, int64_t lda, double scale,
+                                   __half* hi, __half* lo, int64_t ld, cudaStream_t stream) {
+    matrix_to_split_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(a, rows, cols, lda, scale, hi, lo, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_to_f64(const __half* hi, const __half* lo, int64_t rows, int64_t cols, int64_t ld,
+                                double unscale, double* out, int64_t ldo, cudaStream_t stream) {
+    split_to_f64_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(hi, lo, rows, cols, ld, unscale, out, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hadamard_split(const __half* ahi, const __half* alo, const __half* bhi, const __half* blo,
+                                  int64_t rows, int64_t cols, int64_t ld, int64_t row0, double factor,
+                                  double diag_value, __half* chi, __half* clo, cudaStream_t stream) {
+    hadamard_split_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(ahi, alo, bhi, blo, rows, cols, ld, row0, factor,
+                                                                      diag_value, chi, clo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hadamard_f64(const double* a, const double* b, int64_t rows, int64_t cols, int64_t ld,
+                                int64_t row0, double n, double* c, cudaStream_t stream) {
+    hadamard_f64_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(a, b, rows, cols, ld, row0, n, c);
+    return cudaGetLastError();
+}
+
+}  // namespace rb

@@ -1,0 +1,364 @@
+// Pass epilogue and small panel kernels.
+//
+// The pass epilogue is where the reference's recurrence arithmetic
+// (proj/src/poly.cpp:97-134) and trace dots (proj/src/hutchpp.cpp:33-51) go:
+//   T_new = a1·(A·T_cur) + a2·T_cur + a3·T_prev
+// covers IntPower (1,0,0), Taylor (1/v,-1,0), Chebyshev first step
+// (scale,-center,0) and later steps (2·scale,-2·center,-1), and the shifted
+// power iteration (−g, v·g, 0). Per probe column it accumulates, in fp64,
+// x0·T_new (trace form), T_cur·T_new (Rayleigh) and T_new·T_new, and the
+// column max |T_new| that sets the next pass's fp16 plane scale.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rb {
+
+namespace {
+
+constexpr int ER = 128;  // rows per epilogue CTA (= product row block)
+
+__device__ __forceinline__ int64_t streamk_owner(int64_t i, int64_t total, int grid) {
+    return ((i + 1) * grid + total - 1) / total - 1;
+}
+
+__device__ __forceinline__ double cm_value(const unsigned* cm, int j) {
+    return cm ? static_cast<double>(__uint_as_float(cm[j])) : 0.0;
+}
+
+// exponent e with bound * 2^e < 2^kPanelTarget
+__device__ __forceinline__ int plane_exponent(double bound) {
+    if (!(bound > 0.0) || !isfinite(bound)) return 0;
+    int E;
+    frexp(bound, &E);  // bound < 2^E
+    int e = kPanelTarget - E;
+    e = max(-120, min(120, e));
+    return e;
+}
+
+__device__ __forceinline__ void split_store(double v, __half* hi, __half* lo, int64_t idx) {
+    const __half h = __double2half(v);
+    const double r = v - static_cast<double>(__half2float(h));
+    hi[idx] = h;
+    lo[idx] = __double2half(r);
+}
+
+template <typename PT, typename ST, bool SPLIT>
+__global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
+    __shared__ double red[3][4][kMaxPanelCols];
+    const int r = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int warp = tid / 32, lane = tid % 32;
+    const int64_t i = static_cast<int64_t>(r) * ER + tid;
+    const bool valid = i < p.rows;
+    const int64_t KT = p.k_tiles;
+    const int64_t c_lo = streamk_owner(static_cast<int64_t>(r) * KT, p.total_iters, p.grid);
+    const int64_t c_hi = streamk_owner(static_cast<int64_t>(r + 1) * KT - 1, p.total_iters, p.grid);
+    const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
+
+    for (int j = 0; j < p.s; ++j) {
+        double y = 0.0;
+        for (int64_t c = c_lo; c <= c_hi; ++c)
+            y += static_cast<double>(p.partial[((r + c) * p.npad + j) * ER + tid]);
+        if (SPLIT) y = ldexp(y * p.unscale, -p.e_cur[j]);
+        double tc = 0.0, tp = 0.0, x0 = 0.0;
+        const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
+        if (valid) {
+            tc = static_cast<double>(p.t_cur[idx]);
+            if (p.t_prev) tp = static_cast<double>(p.t_prev[idx]);
+            x0 = static_cast<double>(p.x0[idx]);
+        }
+        double tn = p.a1 * y + p.a2 * tc + p.a3 * tp;
+        const ST tns = static_cast<ST>(tn);
+        tn = static_cast<double>(tns);
+        if (!valid) tn = 0.0;
+        if (valid) {
+            p.t_new[idx] = tns;
+            if (p.acc) p.acc[idx] += p.acc_coef * tn;
+        }
+        if (SPLIT) {
+            const double bound = growth * cm_value(p.cmax_cur, j) + fabs(p.a3) * cm_value(p.cmax_prev, j);
+            const int e = plane_exponent(bound);
+            if (r == 0 && tid == 0) p.e_next[j] = e;
+            if (valid) split_store(ldexp(tn, e), p.vhi, p.vlo, idx);
+        }
+        const double d1 = warp_sum(x0 * tn);
+        const double d2 = warp_sum(tc * tn);
+        const double d3 = warp_sum(tn * tn);
+        const float mx = warp_max(static_cast<float>(fabs(tn)));
+        if (lane == 0) {
+            red[0][warp][j] = d1;
+            red[1][warp][j] = d2;
+            red[2][warp][j] = d3;
+            atomicMax(p.cmax_new + j, __float_as_uint(mx));
+        }
+    }
+    __syncthreads();
+    const int R = gridDim.x;
+    for (int t = tid; t < 3 * p.s; t += blockDim.x) {
+        const int q = t / p.s, j = t % p.s;
+        const double v = ((red[q][0][j] + red[q][1][j]) + red[q][2][j]) + red[q][3][j];
+        p.stats[(static_cast<int64_t>(q) * R + r) * p.s + j] = v;
+    }
+}
+
+template <typename ST, bool SPLIT>
+__global__ void __launch_bounds__(ER) prep_stats_kernel(PrepArgs<ST> p) {
+    __shared__ double red[4][kMaxPanelCols];
+    const int r = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int64_t i = static_cast<int64_t>(r) * ER + tid;
+    const bool valid = i < p.rows;
+    for (int j = 0; j < p.s; ++j) {
+        double v = 0.0;
+        if (valid) {
+            const ST vs = static_cast<ST>(p.x[static_cast<int64_t>(j) * p.ldx + i]);
+            v = static_cast<double>(vs);
+            p.t0[static_cast<int64_t>(j) * p.ld + i] = vs;
+            if (p.acc) p.acc[static_cast<int64_t>(j) * p.ld + i] = p.acc_coef * v;
+        }
+        const double d = warp_sum(v * v);
+        const float mx = warp_max(static_cast<float>(fabs(v)));
+        if (lane == 0) {
+            red[warp][j] = d;
+            atomicMax(p.cmax0 + j, __float_as_uint(mx));
+        }
+    }
+    __syncthreads();
+    const int R = gridDim.x;
+    for (int j = tid; j < p.s; j += blockDim.x) {
+        const double v = ((red[0][j] + red[1][j]) + red[2][j]) + red[3][j];
+        // q = 0 (x0·T0), 1 (T0·T0 as "Rayleigh" slot), 2 (T0·T0)
+        p.stats[(0 * static_cast<int64_t>(R) + r) * p.s + j] = v;
+        p.stats[(1 * static_cast<int64_t>(R) + r) * p.s + j] = v;
+        p.stats[(2 * static_cast<int64_t>(R) + r) * p.s + j] = v;
+    }
+}
+
+__global__ void prep_planes_kernel(PrepArgs<float> p) {
+    const int j = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int e = plane_exponent(static_cast<double>(__uint_as_float(p.cmax0[j])));
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.e0[j] = e;
+    if (i >= p.rows) return;
+    const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
+    split_store(ldexp(static_cast<double>(p.t0[idx]), e), p.vhi, p.vlo, idx);
+}
+
+__global__ void reduce_stats_kernel(const double* __restrict__ stats, int passes, int R, int s,
+                                    double* __restrict__ out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(passes) * 3 * s;
+    if (t >= total) return;
+    const int64_t j = t % s;
+    const int64_t pq = t / s;  // pass*3 + q
+    const double* src = stats + pq * R * s + j;
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += src[static_cast<int64_t>(r) * s];
+    out[t] = acc;
+}
+
+template <typename ST>
+__global__ void state_to_f64_kernel(const ST* __restrict__ st, int64_t rows, int64_t ld, double* __restrict__ out,
+                                    int64_t ldo) {
+    const int j = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < rows) out[static_cast<int64_t>(j) * ldo + i] = static_cast<double>(st[static_cast<int64_t>(j) * ld + i]);
+}
+
+// ---- panel gram: partial[cta][a][b] = sum_{rows of cta} X[i][a] Z[i][b] ----
+constexpr int GR = 32;  // rows per smem chunk
+__global__ void __launch_bounds__(256) panel_gram_kernel(const double* __restrict__ x, int p, int64_t ldx,
+                                                         const double* __restrict__ z, int q, int64_t ldz,
+                                                         int64_t rows, double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    double* xs = sm;            // [GR][p]
+    double* zs = sm + GR * p;   // [GR][q]
+    const int G = gridDim.x;
+    const int64_t per = (rows + G - 1) / G;
+    const int64_t r0 = per * blockIdx.x;
+    const int64_t r1 = min(rows, r0 + per);
+    const int outs = p * q;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int64_t c0 = r0; c0 < r1; c0 += GR) {
+        for (int idx = threadIdx.x; idx < GR * p; idx += blockDim.x) {
+            const int a = idx / GR, rr = idx % GR;
+            const int64_t gi = c0 + rr;
+            xs[rr * p + a] = gi < r1 ? x[static_cast<int64_t>(a) * ldx + gi] : 0.0;
+        }
+        for (int idx = threadIdx.x; idx < GR * q; idx += blockDim.x) {
+            const int b = idx / GR, rr = idx % GR;
+            const int64_t gi = c0 + rr;
+            zs[rr * q + b] = gi < r1 ? z[static_cast<int64_t>(b) * ldz + gi] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int o = threadIdx.x + u * blockDim.x;
+            if (o < outs) {
+                const int a = o % p, b = o / p;
+                double t = acc[u];
+                for (int rr = 0; rr < GR; ++rr) t = fma(xs[rr * p + a], zs[rr * q + b], t);
+                acc[u] = t;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int o = threadIdx.x + u * blockDim.x;
+        if (o < outs) partial[static_cast<int64_t>(blockIdx.x) * outs + o] = acc[u];
+    }
+}
+
+__global__ void panel_gram_reduce_kernel(const double* __restrict__ partial, int G, int outs,
+                                         double* __restrict__ out) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= outs) return;
+    double acc = 0.0;
+    for (int c = 0; c < G; ++c) acc += partial[static_cast<int64_t>(c) * outs + o];
+    out[o] = acc;
+}
+
+__global__ void panel_update_kernel(double beta, const double* __restrict__ g, int64_t ldg,
+                                    const double* __restrict__ x, int p, int64_t ldx, const double* __restrict__ c,
+                                    int q, int64_t rows, double* __restrict__ w, int64_t ldw) {
+    extern __shared__ double cs[];  // [p][q] column-major c[a + b*p]
+    for (int t = threadIdx.x; t < p * q; t += blockDim.x) cs[t] = c[t];
+    __syncthreads();
+    const int b = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double acc = 0.0;
+    for (int a = 0; a < p; ++a) acc = fma(x[static_cast<int64_t>(a) * ldx + i], cs[a + b * p], acc);
+    const double base = (beta != 0.0 && g) ? beta * g[static_cast<int64_t>(b) * ldg + i] : 0.0;
+    w[static_cast<int64_t>(b) * ldw + i] = base + acc;
+}
+
+// ---- reference RNG (proj/src/rng.cpp:8-54) on the device ----
+__device__ __forceinline__ uint64_t dmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t dderive(uint64_t seed, uint64_t tag) {
+    return dmix64(seed ^ dmix64(tag + 0x6a09e667f3bcc909ULL));
+}
+
+__global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64_t rows, int j0,
+                                 double* __restrict__ out, int64_t ld, int* err) {
+    const int j = blockIdx.y;
+    const uint64_t key = derive ? dderive(base_key, static_cast<uint64_t>(j0 + j)) : base_key;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double* col = out + static_cast<int64_t>(j) * ld;
+    if (kind == 1) {
+        if (t >= rows) return;
+        const uint64_t u = dmix64(key ^ dmix64(static_cast<uint64_t>(t)));
+        col[t] = (u >> 63) ? -1.0 : 1.0;
+        return;
+    }
+    // Gaussian: pair t covers elements 2t (cos) and 2t+1 (sin); counters 2t, 2t+1.
+    const int64_t i0 = 2 * t;
+    if (i0 >= rows) return;
+    const uint64_t w1 = dmix64(key ^ dmix64(static_cast<uint64_t>(2 * t)));
+    const uint64_t w2 = dmix64(key ^ dmix64(static_cast<uint64_t>(2 * t + 1)));
+    const double u1 = static_cast<double>(w1 >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(w2 >> 11) * 0x1.0p-53;
+    if (u1 <= 0.0) atomicExch(err, 1);  // the reference would redraw (p = 2^-53 per pair)
+    const double rr = sqrt(-2.0 * log(u1));
+    const double theta = 2.0 * 3.141592653589793 * u2;
+    col[i0] = rr * cos(theta);
+    if (i0 + 1 < rows) col[i0 + 1] = rr * sin(theta);
+}
+
+}  // namespace
+
+cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream) {
+    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + ER - 1) / ER);
+    epilogue_kernel<float, float, true><<<R, ER, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t stream) {
+    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + ER - 1) / ER);
+    epilogue_kernel<double, double, false><<<R, ER, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepare_split(const PrepArgs<float>& a, cudaStream_t stream) {
+    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + ER - 1) / ER);
+    prep_stats_kernel<float, true><<<R, ER, 0, stream>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 grid(static_cast<unsigned>((a.rows + 255) / 256), a.s);
+    prep_planes_kernel<<<grid, 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream) {
+    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + ER - 1) / ER);
+    prep_stats_kernel<double, false><<<R, ER, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks, int s, double* out,
+                                cudaStream_t stream) {
+    const int64_t total = static_cast<int64_t>(passes) * 3 * s;
+    if (total == 0) return cudaSuccess;
+    reduce_stats_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, stream>>>(stats, passes, row_blocks,
+                                                                                        s, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_state_to_f64(const void* state, bool is_f32, int64_t rows, int s, int64_t ld, double* out,
+                                int64_t ldo, cudaStream_t stream) {
+    dim3 grid(static_cast<unsigned>((rows + 255) / 256), s);
+    if (is_f32)
+        state_to_f64_kernel<float><<<grid, 256, 0, stream>>>(static_cast<const float*>(state), rows, ld, out, ldo);
+    else
+        state_to_f64_kernel<double><<<grid, 256, 0, stream>>>(static_cast<const double*>(state), rows, ld, out, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_panel_gram(const double* x, int p, int64_t ldx, const double* z, int q, int64_t ldz,
+                              int64_t rows, double* partial, int grid, double* out, cudaStream_t stream) {
+    if (p <= 0 || q <= 0) return cudaSuccess;
+    if (p * q > 8 * 256) return cudaErrorInvalidValue;
+    const size_t smem = static_cast<size_t>(GR) * (p + q) * sizeof(double);
+    if (smem > 48 * 1024) return cudaErrorInvalidValue;
+    panel_gram_kernel<<<grid, 256, smem, stream>>>(x, p, ldx, z, q, ldz, rows, partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int outs = p * q;
+    panel_gram_reduce_kernel<<<(outs + 127) / 128, 128, 0, stream>>>(partial, grid, outs, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_panel_update(double beta, const double* g, int64_t ldg, const double* x, int p, int64_t ldx,
+                                const double* c, int q, int64_t rows, double* w, int64_t ldw, cudaStream_t stream) {
+    if (q <= 0) return cudaSuccess;
+    const size_t smem = static_cast<size_t>(p) * q * sizeof(double);
+    if (smem > 48 * 1024) return cudaErrorInvalidValue;
+    dim3 grid(static_cast<unsigned>((rows + 255) / 256), q);
+    panel_update_kernel<<<grid, 256, smem, stream>>>(beta, g, ldg, x, p, ldx, c, q, rows, w, ldw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t rows, int cols, int j0, double* out,
+                             int64_t ld, int* err_flag, cudaStream_t stream) {
+    if (cols <= 0 || rows <= 0) return cudaSuccess;
+    const int64_t work = kind == 1 ? rows : (rows + 1) / 2;
+    dim3 grid(static_cast<unsigned>((work + 255) / 256), cols);
+    rng_panel_kernel<<<grid, 256, 0, stream>>>(base_key, derive, kind, rows, j0, out, ld, err_flag);
+    return cudaGetLastError();
+}
+
+}  // namespace rb
