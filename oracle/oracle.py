@@ -1,0 +1,367 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes binding of the fp64 CPU check oracle
+(oracle/renyi_oracle.cpp). Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module; the product
+(paper_2205_07426_b200) never does.
+
+Parity status: pinned by the reference's own analytic known-answer tests
+(tests/test_oracle_kats.py); the reference itself is unbuildable here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "_build" / "librenyi_oracle.so"
+
+_D = C.POINTER(C.c_double)
+_I64 = C.c_int64
+
+
+class CParams(C.Structure):
+    _fields_ = [
+        ("alpha", C.c_double), ("method", C.c_int), ("s", C.c_int), ("m", C.c_int),
+        ("epsilon", C.c_double), ("delta", C.c_double), ("seed", C.c_uint64),
+        ("power_max_iters", C.c_int), ("power_tol", C.c_double), ("power_seed", C.c_uint64),
+        ("power_rank_floor", C.c_double), ("has_bounds", C.c_int), ("bu", C.c_double), ("bv", C.c_double),
+        ("probe_kind", C.c_int), ("s_q", C.c_int), ("s_g", C.c_int),
+    ]
+
+
+class COut(C.Structure):
+    _fields_ = [
+        ("entropy", C.c_double), ("trace", C.c_double), ("low", C.c_double), ("residual", C.c_double),
+        ("method", C.c_int), ("s", C.c_int), ("m", C.c_int), ("queries", C.c_int), ("rank", C.c_int),
+        ("exact", C.c_int), ("deterministic", C.c_int), ("has_bounds", C.c_int),
+        ("bu", C.c_double), ("bv", C.c_double), ("kappa", C.c_double),
+        ("iterations_used", C.c_int), ("v_converged", C.c_int), ("u_converged", C.c_int),
+        ("rank_deficient", C.c_int),
+    ]
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+KINDS = {"int": 0, "int_power": 0, "taylor": 1, "chebyshev": 2}
+METHODS = {"exact": 0, "int": 1, "taylor": 2, "chebyshev": 3, "auto": 4}
+PROBES = {"gaussian": 0, "rademacher": 1}
+
+
+def build() -> Path:
+    """Compiles the oracle (make, g++ -O3 -fopenmp) if needed."""
+    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            build()
+        h = C.CDLL(str(LIB))
+        h.oracle_last_error.restype = C.c_char_p
+        for name in ("oracle_mix64", "oracle_derive_key", "oracle_hash_name"):
+            getattr(h, name).restype = C.c_uint64
+        h.oracle_mix64.argtypes = [C.c_uint64]
+        h.oracle_derive_key.argtypes = [C.c_uint64, C.c_uint64]
+        h.oracle_hash_name.argtypes = [C.c_char_p]
+        h.oracle_taylor_tail_constant.restype = C.c_double
+        h.oracle_taylor_tail_constant.argtypes = [C.c_double, C.c_int]
+        h.oracle_safeguard.restype = C.c_double
+        h.oracle_safeguard.argtypes = [C.c_double, C.c_double]
+        h.oracle_expected_queries.restype = C.c_long
+        h.oracle_expected_queries.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, C.c_int]
+        h.oracle_slab_sample.restype = C.c_double
+        h.oracle_slab_sample.argtypes = [_D, _I64, _I64, C.c_double, _I64, _I64, C.c_int, C.c_int, C.c_int]
+        h.oracle_probe_panel.argtypes = [_I64, C.c_int, C.c_uint64, C.c_char_p, C.c_int, _D]
+        h.oracle_stream_gaussian.argtypes = [C.c_uint64, _I64, _D]
+        h.oracle_mixture_samples.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, _D]
+        h.oracle_gaussian_gram.argtypes = [_D, _I64, _I64, C.c_double, _D]
+        h.oracle_build_kernel.argtypes = [_D, _I64, _I64, C.c_double, _D]
+        h.oracle_hadamard_joint.argtypes = [_D, _I64, _D, _I64, _D]
+        h.oracle_matvec.argtypes = [_D, _I64, _D, _D]
+        h.oracle_matmul_panel.argtypes = [_D, _I64, _D, C.c_int, _D]
+        h.oracle_apply_panel.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, _D, _I64, _D,
+                                         C.c_int, _D]
+        h.oracle_scalar_value.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, C.c_double, _D]
+        h.oracle_spec_coeffs.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, _D, _D]
+        h.oracle_binomial_coeffs.argtypes = [C.c_double, C.c_int, _D]
+        h.oracle_chebyshev_coeffs.argtypes = [C.c_double, C.c_int, C.c_double, C.c_double, _D]
+        h.oracle_power_method.argtypes = [_D, _I64, C.c_int, C.c_double, C.c_uint64, _D, C.POINTER(C.c_int),
+                                          C.POINTER(C.c_int)]
+        h.oracle_estimate_bounds.argtypes = [_D, _I64, C.c_int, C.c_double, C.c_uint64, C.c_double,
+                                             C.POINTER(COut)]
+        h.oracle_colpiv_rank.argtypes = [_D, _I64, C.c_int, C.c_double, C.POINTER(C.c_int), _D]
+        h.oracle_hutchpp.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, _D, _I64, C.c_int,
+                                     C.c_int, C.c_uint64, C.c_int, _D, _D, C.POINTER(COut)]
+        h.oracle_estimate.argtypes = [_D, _I64, C.POINTER(CParams), C.POINTER(COut)]
+        h.oracle_eigvals.argtypes = [_D, _I64, _D]
+        h.oracle_entropy_from_trace.argtypes = [C.c_double, C.c_double, _D]
+        h.oracle_select_params.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                           _I64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        h.oracle_mu_bound.argtypes = [C.c_double, C.c_double, C.c_double, _I64, _D, _D, _D]
+        h.oracle_threads.restype = C.c_int
+        h.oracle_set_threads.argtypes = [C.c_int]
+        _lib = h
+    return _lib
+
+
+def _chk(code: int):
+    if code != 0:
+        raise OracleError(code, lib().oracle_last_error().decode())
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+def _f(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _u64(x: int) -> int:
+    return x & (2**64 - 1)
+
+
+# ---- rng ----
+def mix64(x): return int(lib().oracle_mix64(_u64(x)))
+def derive_key(s, t): return int(lib().oracle_derive_key(_u64(s), _u64(t)))
+def hash_name(s: str): return int(lib().oracle_hash_name(s.encode()))
+
+
+def probe_panel(n, cols, seed, label, kind="gaussian"):
+    out = np.empty((n, cols), order="F")
+    _chk(lib().oracle_probe_panel(n, cols, _u64(seed), label.encode(), PROBES[kind], _p(out)))
+    return out
+
+
+gaussian_panel = probe_panel
+
+
+def stream_gaussian(key, count):
+    out = np.empty(count)
+    _chk(lib().oracle_stream_gaussian(_u64(key), count, _p(out)))
+    return out
+
+
+def fill_gaussian(key, rows, cols):
+    """RandomStream(key).fill_gaussian(Matrix(rows, cols)) — column-wise (rng.cpp:60-64)."""
+    return stream_gaussian(key, rows * cols).reshape((rows, cols), order="F")
+
+
+def mixture_samples(n, d, seed, center=1.0):
+    out = np.empty((n, d), order="F")
+    _chk(lib().oracle_mixture_samples(n, d, _u64(seed), center, _p(out)))
+    return out
+
+
+# ---- ops / kernel ----
+def gaussian_gram(x, sigma):
+    x = _f(x)
+    out = np.empty((x.shape[0], x.shape[0]), order="F")
+    _chk(lib().oracle_gaussian_gram(_p(x), x.shape[0], x.shape[1], sigma, _p(out)))
+    return out
+
+
+def build_kernel(x, sigma):
+    x = _f(x)
+    out = np.empty((x.shape[0], x.shape[0]), order="F")
+    _chk(lib().oracle_build_kernel(_p(x), x.shape[0], x.shape[1], sigma, _p(out)))
+    return out
+
+
+def hadamard_joint(a, b):
+    a, b = _f(a), _f(b)
+    out = np.empty_like(a, order="F")
+    _chk(lib().oracle_hadamard_joint(_p(a), a.shape[0], _p(b), b.shape[0], _p(out)))
+    return out
+
+
+def matvec(a, x):
+    a = _f(a)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(a.shape[0])
+    _chk(lib().oracle_matvec(_p(a), a.shape[0], _p(x), _p(y)))
+    return y
+
+
+def matmul_panel(a, x):
+    a, x = _f(a), _f(x)
+    y = np.empty((a.shape[0], x.shape[1]), order="F")
+    _chk(lib().oracle_matmul_panel(_p(a), a.shape[0], _p(x), x.shape[1], _p(y)))
+    return y
+
+
+# ---- poly ----
+@dataclass
+class Spec:
+    kind: str
+    alpha: float
+    m: int = 0
+    u: float = 0.0
+    v: float = 1.0
+
+    def args(self):
+        return (KINDS[self.kind], float(self.alpha), int(self.m), float(self.u), float(self.v))
+
+
+def apply_panel(spec: Spec, a, x):
+    a, x = _f(a), _f(x)
+    if x.ndim == 1:
+        x = x.reshape(-1, 1, order="F")
+    y = np.empty_like(x, order="F")
+    _chk(lib().oracle_apply_panel(*spec.args(), _p(a), a.shape[0], _p(x), x.shape[1], _p(y)))
+    return y
+
+
+def scalar_value(spec: Spec, lam):
+    out = C.c_double()
+    _chk(lib().oracle_scalar_value(*spec.args(), lam, C.byref(out)))
+    return out.value
+
+
+def spec_coeffs(spec: Spec):
+    n = max(spec.m, 0) + 1
+    c = np.empty(n)
+    sv = C.c_double()
+    _chk(lib().oracle_spec_coeffs(*spec.args(), _p(c), C.byref(sv)))
+    return c, sv.value
+
+
+def binomial_coeffs(alpha, m):
+    out = np.empty(m + 1)
+    _chk(lib().oracle_binomial_coeffs(alpha, m, _p(out)))
+    return out
+
+
+def chebyshev_coeffs(alpha, m, u, v):
+    out = np.empty(m + 1)
+    _chk(lib().oracle_chebyshev_coeffs(alpha, m, u, v, _p(out)))
+    return out
+
+
+def taylor_tail_constant(alpha, k_max=10000):
+    return lib().oracle_taylor_tail_constant(alpha, k_max)
+
+
+def safeguard(u, v):
+    return lib().oracle_safeguard(u, v)
+
+
+def expected_queries(spec: Spec, s):
+    return int(lib().oracle_expected_queries(*spec.args(), s))
+
+
+# ---- spectrum ----
+def power_method(a, max_iters=100, tol=1e-6, seed=0):
+    a = _f(a)
+    r, it, cv = C.c_double(), C.c_int(), C.c_int()
+    _chk(lib().oracle_power_method(_p(a), a.shape[0], max_iters, tol, _u64(seed), C.byref(r), C.byref(it),
+                                   C.byref(cv)))
+    return r.value, it.value, bool(cv.value)
+
+
+def estimate_bounds(a, max_iters=100, tol=1e-6, seed=0, rank_floor=1e-12):
+    a = _f(a)
+    o = COut()
+    _chk(lib().oracle_estimate_bounds(_p(a), a.shape[0], max_iters, tol, _u64(seed), rank_floor, C.byref(o)))
+    return dict(u=o.bu, v=o.bv, kappa=o.kappa, iterations_used=o.iterations_used, v_converged=bool(o.v_converged),
+                u_converged=bool(o.u_converged), rank_deficient=bool(o.rank_deficient))
+
+
+def colpiv_rank(y, threshold=1e-12, want_q=False):
+    y = _f(y)
+    r = C.c_int()
+    q = np.empty(y.shape, order="F") if want_q else None
+    _chk(lib().oracle_colpiv_rank(_p(y), y.shape[0], y.shape[1], threshold, C.byref(r),
+                                  _p(q) if want_q else None))
+    return (r.value, q[:, :r.value]) if want_q else r.value
+
+
+# ---- hutchpp / entropy ----
+def _out(o: COut):
+    return dict(entropy=o.entropy, value=o.trace, trace=o.trace, low_rank_part=o.low, residual_part=o.residual,
+                method=o.method, s=o.s, m=o.m, queries_used=o.queries, sketch_rank=o.rank, exact=bool(o.exact),
+                deterministic=bool(o.deterministic), has_bounds=bool(o.has_bounds), u=o.bu, v=o.bv,
+                kappa=o.kappa, iterations_used=o.iterations_used)
+
+
+def hutchpp(spec: Spec, a, s_q, s_g, seed=0, probe_kind="gaussian", sketch=None, probes=None):
+    a = _f(a)
+    S = _f(sketch) if sketch is not None else None
+    G = _f(probes) if probes is not None else None
+    o = COut()
+    _chk(lib().oracle_hutchpp(*spec.args(), _p(a), a.shape[0], s_q, s_g, _u64(seed), PROBES[probe_kind],
+                              _p(S) if S is not None else None, _p(G) if G is not None else None, C.byref(o)))
+    return _out(o)
+
+
+def estimate(a, alpha=2.0, method="auto", s=0, m=0, epsilon=1e-2, delta=1e-2, seed=0, bounds=None,
+             probe_kind="gaussian", s_q=None, s_g=None, power_max_iters=100, power_tol=1e-6):
+    a = _f(a)
+    p = CParams(alpha, METHODS[method], s, m, epsilon, delta, _u64(seed), power_max_iters, power_tol, 0, 1e-12,
+                1 if bounds is not None else 0, bounds[0] if bounds else 0.0, bounds[1] if bounds else 1.0,
+                PROBES[probe_kind], -1 if s_q is None else s_q, -1 if s_g is None else s_g)
+    o = COut()
+    _chk(lib().oracle_estimate(_p(a), a.shape[0], C.byref(p), C.byref(o)))
+    return _out(o)
+
+
+def eigvals(a):
+    a = _f(a)
+    out = np.empty(a.shape[0])
+    _chk(lib().oracle_eigvals(_p(a), a.shape[0], _p(out)))
+    return out
+
+
+def entropy_from_trace(trace, alpha):
+    out = C.c_double()
+    _chk(lib().oracle_entropy_from_trace(trace, alpha, C.byref(out)))
+    return out.value
+
+
+def entropy_exact(a, alpha):
+    return estimate(a, alpha=alpha, method="exact")["entropy"]
+
+
+def select_params(alpha, epsilon, delta, u, v, kappa, n, method):
+    s, m = C.c_int(), C.c_int()
+    _chk(lib().oracle_select_params(alpha, epsilon, delta, u, v, kappa, n, METHODS[method], C.byref(s), C.byref(m)))
+    return s.value, m.value
+
+
+def mu_bound(u, v, alpha, n):
+    mu, lo, hi = C.c_double(), C.c_double(), C.c_double()
+    _chk(lib().oracle_mu_bound(u, v, alpha, n, C.byref(mu), C.byref(lo), C.byref(hi)))
+    return mu.value, lo.value, hi.value
+
+
+def mutual_information(a, b, **params):
+    """measures.cpp:36-46 with per-term seeds."""
+    seed = params.pop("seed", 0)
+    j = hadamard_joint(a, b)
+    sv = estimate(a, seed=derive_key(seed, hash_name("term:vars")), **params)["entropy"]
+    st = estimate(b, seed=derive_key(seed, hash_name("term:target")), **params)["entropy"]
+    sj = estimate(j, seed=derive_key(seed, hash_name("term:joint")), **params)["entropy"]
+    return dict(value=sv + st - sj, vars_entropy=sv, target_entropy=st, joint_entropy=sj)
+
+
+def threads():
+    return lib().oracle_threads()
+
+
+def set_threads(t):
+    lib().oracle_set_threads(t)
+
+
+def slab_sample_seconds(x, sigma, r0, h, passes, cols_q, cols_w):
+    x = _f(x)
+    return lib().oracle_slab_sample(_p(x), x.shape[0], x.shape[1], sigma, r0, h, passes, cols_q, cols_w)

@@ -1,0 +1,1276 @@
+// TEST INFRASTRUCTURE ONLY — the parity checker and the CPU baseline, never
+// part of the product. Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs may load this library.
+//
+// Eigen-free fp64 CPU restatement of the reference estimator path
+// (arxiv 2205.07426 artifact, /root/reference/proj). The reference itself cannot
+// be compiled here (Eigen 3, doctest and CLI11 are absent), so this
+// file restates its algorithms function by function, each citing the reference
+// file:line it follows, with the reference's cost structure (8-column panels that
+// re-stream A, Q and W applied separately, OpenMP where the reference has it).
+// Column-major storage throughout, like Eigen::MatrixXd.
+//
+// Pinned by the reference's own known-answer tests (tests/test_oracle_kats.py).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <numbers>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace orc {
+
+using Vec = std::vector<double>;
+
+struct Mat {  // column-major n x m
+    int64_t r = 0, c = 0;
+    Vec d;
+    Mat() = default;
+    Mat(int64_t rows, int64_t cols, double v = 0.0) : r(rows), c(cols), d(static_cast<size_t>(rows) * cols, v) {}
+    double& operator()(int64_t i, int64_t j) { return d[i + j * r]; }
+    double operator()(int64_t i, int64_t j) const { return d[i + j * r]; }
+    double* col(int64_t j) { return d.data() + j * r; }
+    const double* col(int64_t j) const { return d.data() + j * r; }
+};
+
+// errc (proj/include/renyi/common.hpp:14-25) + 1
+enum { kInvalidArgument = 1, kZeroDiagonal, kNonFinite, kSizeMismatch, kDomainError, kRankCollapse,
+       kNonPositiveTrace, kAlphaIsOne, kDegenerateBounds, kParseError };
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+[[noreturn]] void fail(int c, const std::string& w) { throw Error(c, w); }
+
+// ---------------------------------------------------------------- rng.cpp:8-64
+uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+uint64_t derive_key(uint64_t seed, uint64_t tag) { return mix64(seed ^ mix64(tag + 0x6a09e667f3bcc909ULL)); }
+uint64_t hash_name(const char* name) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (const char* p = name; *p; ++p) {
+        h ^= static_cast<unsigned char>(*p);
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+struct Stream {
+    uint64_t key, counter = 0;
+    bool have_spare = false;
+    double spare = 0.0;
+    explicit Stream(uint64_t k) : key(k) {}
+    uint64_t next_u64() { return mix64(key ^ mix64(counter++)); }
+    double next_uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+    double next_gaussian() {
+        if (have_spare) {
+            have_spare = false;
+            return spare;
+        }
+        double u1 = next_uniform();
+        while (u1 <= 0.0) u1 = next_uniform();
+        const double u2 = next_uniform();
+        const double rr = std::sqrt(-2.0 * std::log(u1));
+        const double theta = 2.0 * std::numbers::pi * u2;
+        spare = rr * std::sin(theta);
+        have_spare = true;
+        return rr * std::cos(theta);
+    }
+    double next_rademacher() { return (next_u64() >> 63) ? -1.0 : 1.0; }
+    void fill_gaussian(Mat& m) {  // column-wise (rng.cpp:60-64)
+        for (int64_t j = 0; j < m.c; ++j)
+            for (int64_t i = 0; i < m.r; ++i) m(i, j) = next_gaussian();
+    }
+};
+
+// detail::gaussian_panel (hutchpp.cpp:13-22); kind 1 = Rademacher (extension)
+Mat probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind) {
+    Mat g(n, cols);
+    const uint64_t base = derive_key(seed, hash_name(label));
+#pragma omp parallel for schedule(static)
+    for (int j = 0; j < cols; ++j) {
+        Stream s(derive_key(base, static_cast<uint64_t>(j)));
+        for (int64_t i = 0; i < n; ++i) g(i, j) = kind == 1 ? s.next_rademacher() : s.next_gaussian();
+    }
+    return g;
+}
+
+// ---------------------------------------------------------------- ops.cpp
+// gaussian_row / gaussian_gram (ops.cpp:9-20,39-47)
+Mat gaussian_gram(const Mat& x, double sigma) {
+    const int64_t n = x.r, d = x.c;
+    Vec sq(n, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t k = 0; k < d; ++k) s += x(i, k) * x(i, k);
+        sq[i] = s;
+    }
+    const double inv_two_sigma2 = 1.0 / (2.0 * sigma * sigma);
+    Mat k(n, n);
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t i = 0; i < n; ++i) {
+        k(i, i) = 1.0;
+        for (int64_t j = i + 1; j < n; ++j) {
+            double dot = 0.0;
+            for (int64_t t = 0; t < d; ++t) dot += x(i, t) * x(j, t);
+            double d2 = sq[i] + sq[j] - 2.0 * dot;
+            if (d2 < 0.0) d2 = 0.0;
+            const double v = std::exp(-d2 * inv_two_sigma2);
+            k(i, j) = v;
+            k(j, i) = v;
+        }
+    }
+    return k;
+}
+
+// y = A x in 64-row blocks (ops.cpp:73-85)
+Vec matvec(const Mat& a, const Vec& x) {
+    const int64_t n = a.r;
+    Vec y(n, 0.0);
+    const int64_t nb = (n + 63) / 64;
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t i0 = b * 64, i1 = std::min(n, i0 + 64);
+        for (int64_t k = 0; k < a.c; ++k) {
+            const double xk = x[k];
+            const double* ak = a.col(k);
+            for (int64_t i = i0; i < i1; ++i) y[i] += ak[i] * xk;
+        }
+    }
+    return y;
+}
+
+// Y = A X as 8-column panels, each panel streaming all of A (ops.cpp:30-35,98-107)
+Mat matmul_panel(const Mat& a, const Mat& x) {
+    Mat y(a.r, x.c);
+    const int64_t nb = (x.c + 7) / 8;
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t j0 = b * 8, j1 = std::min<int64_t>(x.c, j0 + 8);
+        for (int64_t k = 0; k < a.c; ++k) {
+            const double* ak = a.col(k);
+            for (int64_t j = j0; j < j1; ++j) {
+                const double xkj = x(k, j);
+                double* yj = y.col(j);
+                for (int64_t i = 0; i < a.r; ++i) yj[i] += ak[i] * xkj;
+            }
+        }
+    }
+    return y;
+}
+
+// C = scale * (A o B) (ops.cpp:116-122)
+Mat hadamard_scaled(const Mat& a, const Mat& b, double scale) {
+    Mat c(a.r, a.c);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < a.c; ++j)
+        for (int64_t i = 0; i < a.r; ++i) c(i, j) = scale * (a(i, j) * b(i, j));
+    return c;
+}
+
+// ---------------------------------------------------------------- kernel.cpp
+uint64_t matrix_hash(const Mat& m) {  // kernel.cpp:13-23
+    uint64_t h = 0xcbf29ce484222325ULL;
+    const auto* bytes = reinterpret_cast<const unsigned char*>(m.d.data());
+    const size_t len = sizeof(double) * m.d.size();
+    for (size_t i = 0; i < len; ++i) {
+        h ^= bytes[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+bool all_finite(const Mat& m) {
+    for (double v : m.d)
+        if (!std::isfinite(v)) return false;
+    return true;
+}
+
+Mat build_kernel(const Mat& x, double sigma) {  // kernel.cpp:35-72 (Gaussian branch)
+    if (x.r < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(x.r));
+    if (!all_finite(x)) fail(kNonFinite, "sample matrix contains non-finite values");
+    if (sigma <= 0.0) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
+    Mat k = gaussian_gram(x, sigma);
+    const int64_t n = k.r;
+    if (!all_finite(k)) fail(kNonFinite, "kernel evaluation produced non-finite values");
+    Vec isd(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (k(i, i) <= 0.0) fail(kZeroDiagonal, "kernel diagonal entry " + std::to_string(i) + " is not positive");
+        isd[i] = 1.0 / std::sqrt(k(i, i));
+    }
+    const double inv_n = 1.0 / static_cast<double>(n);
+    Mat a(n, n);
+    for (int64_t i = 0; i < n; ++i) {
+        a(i, i) = inv_n;
+        for (int64_t j = i + 1; j < n; ++j) {
+            const double v = inv_n * k(i, j) * isd[i] * isd[j];
+            a(i, j) = v;
+            a(j, i) = v;
+        }
+    }
+    return a;
+}
+
+Mat hadamard_joint(std::vector<const Mat*> ks) {  // kernel.cpp:74-101
+    if (ks.size() < 2) fail(kInvalidArgument, "hadamard_joint needs at least 2 kernels");
+    const int64_t n = ks.front()->r;
+    for (const Mat* k : ks)
+        if (k->r != n) fail(kSizeMismatch, "hadamard_joint kernel sizes differ");
+    std::vector<std::pair<uint64_t, const Mat*>> order;
+    for (const Mat* k : ks) order.push_back({matrix_hash(*k), k});
+    std::sort(order.begin(), order.end(), [](const auto& x, const auto& y) {
+        if (x.first != y.first) return x.first < y.first;
+        return std::memcmp(x.second->d.data(), y.second->d.data(), sizeof(double) * x.second->d.size()) < 0;
+    });
+    double scale = 1.0;
+    for (size_t l = 1; l < order.size(); ++l) scale *= static_cast<double>(n);
+    Mat prod = *order[0].second;
+    for (size_t l = 1; l + 1 < order.size(); ++l) prod = hadamard_scaled(prod, *order[l].second, 1.0);
+    prod = hadamard_scaled(prod, *order.back().second, scale);
+    const double inv_n = 1.0 / static_cast<double>(n);
+    for (int64_t i = 0; i < n; ++i) prod(i, i) = inv_n;
+    return prod;
+}
+
+// ---------------------------------------------------------------- spectrum.cpp
+struct PowerOptions {
+    int max_iters = 100;
+    double tol = 1e-6;
+    uint64_t seed = 0;
+    double rank_floor = 1e-12;
+};
+struct PowerResult {
+    double rayleigh = 0.0;
+    int iterations = 0;
+    bool converged = false;
+};
+struct Bounds {
+    double u = 0.0, v = 1.0, kappa = std::numeric_limits<double>::infinity();
+    int iterations_used = 0;
+    bool v_converged = true, u_converged = true, rank_deficient = false;
+};
+
+double dot(const Vec& a, const Vec& b) {
+    double s = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+    return s;
+}
+
+Vec seeded_start(int64_t n, uint64_t seed) {  // spectrum.cpp:13-21
+    Stream s(derive_key(seed, hash_name("power-start")));
+    Vec x(n);
+    for (auto& v : x) v = s.next_gaussian();
+    const double norm = std::sqrt(dot(x, x));
+    if (norm == 0.0) std::fill(x.begin(), x.end(), 1.0 / std::sqrt(static_cast<double>(n)));
+    else
+        for (auto& v : x) v /= norm;
+    return x;
+}
+
+PowerResult power_method(const Mat& a, const PowerOptions& o) {  // spectrum.cpp:25-49
+    Vec x = seeded_start(a.r, o.seed);
+    PowerResult res;
+    double prev = 0.0;
+    for (int it = 1; it <= o.max_iters; ++it) {
+        Vec y = matvec(a, x);
+        const double q = dot(x, y);
+        res.rayleigh = q;
+        res.iterations = it;
+        if (it > 1 && std::abs(q - prev) <= o.tol * std::abs(q)) {
+            res.converged = true;
+            break;
+        }
+        prev = q;
+        const double norm = std::sqrt(dot(y, y));
+        if (norm == 0.0) {
+            res.converged = true;
+            break;
+        }
+        for (size_t i = 0; i < y.size(); ++i) x[i] = y[i] / norm;
+    }
+    return res;
+}
+
+Bounds estimate_bounds(const Mat& a, const PowerOptions& o) {  // spectrum.cpp:80-103
+    Bounds b;
+    const PowerResult rv = power_method(a, o);
+    const double inv_n = 1.0 / static_cast<double>(a.r);
+    b.v = std::clamp(rv.rayleigh * (1.0 + o.tol), inv_n, 1.0);
+    b.v_converged = rv.converged;
+    Mat shifted(a.r, a.c);
+    for (size_t i = 0; i < a.d.size(); ++i) shifted.d[i] = -a.d[i];
+    for (int64_t i = 0; i < a.r; ++i) shifted(i, i) += b.v;
+    PowerOptions so = o;
+    so.seed = derive_key(o.seed, hash_name("shifted"));
+    const PowerResult ru = power_method(shifted, so);
+    b.u_converged = ru.converged;
+    double u = (b.v - ru.rayleigh) * (1.0 - o.tol);
+    const double floor = std::max(o.rank_floor, b.v * o.tol * 100.0);
+    if (u < floor) {
+        u = 0.0;
+        b.rank_deficient = true;
+    }
+    b.u = std::min(u, inv_n);
+    b.kappa = b.u > 0.0 ? b.v / b.u : std::numeric_limits<double>::infinity();
+    b.iterations_used = rv.iterations + ru.iterations;
+    return b;
+}
+
+// ---------------------------------------------------------------- poly.cpp
+Vec binomial_coeffs(double alpha, int m) {  // poly.cpp:10-16
+    if (m < 0) fail(kInvalidArgument, "binomial_coeffs needs m >= 0");
+    Vec b(m + 1);
+    b[0] = 1.0;
+    for (int k = 0; k < m; ++k) b[k + 1] = b[k] * (alpha - k) / (k + 1);
+    return b;
+}
+
+Vec chebyshev_coeffs(double alpha, int m, double a, double b) {  // poly.cpp:18-46
+    if (a < 0.0 || b <= a) fail(kDomainError, "chebyshev_coeffs needs 0 <= u < v");
+    if (m < 1) fail(kInvalidArgument, "chebyshev_node_coeffs needs m >= 1");
+    const int n_nodes = m + 1;
+    Vec c(m + 1, 0.0);
+    for (int i = 0; i < n_nodes; ++i) {
+        const double theta = std::numbers::pi * (i + 0.5) / n_nodes;
+        const double x = std::cos(theta);
+        const double fx = std::pow(a + 0.5 * (b - a) * (x + 1.0), alpha);
+        double t_prev = 1.0, t_cur = x;
+        c[0] += fx;
+        if (m >= 1) c[1] += fx * x;
+        for (int k = 2; k <= m; ++k) {
+            const double t_next = 2.0 * x * t_cur - t_prev;
+            c[k] += fx * t_next;
+            t_prev = t_cur;
+            t_cur = t_next;
+        }
+    }
+    for (auto& v : c) v *= 2.0 / n_nodes;
+    return c;
+}
+
+double safeguard(double u, double v) {  // poly.hpp:27-30
+    const double widened = u + 2.0 * std::sqrt(std::max(0.0, 2.0 * u - u * u));
+    return std::max(v, widened);
+}
+
+double taylor_tail_constant(double alpha, int k_max) {  // poly.cpp:48-58
+    const int shift = static_cast<int>(std::ceil(alpha)) + 1;
+    double best = 0.0;
+    for (int k = 0; k <= k_max; ++k) {
+        double ratio = 1.0;
+        for (int i = k; i < k + shift; ++i) ratio *= std::abs(alpha - i) / (i + 1);
+        best = std::max(best, ratio);
+    }
+    return best;
+}
+
+struct Spec {  // MatrixFunctionSpec (poly.hpp:32-70)
+    int kind = 0;  // 0 int, 1 taylor, 2 chebyshev
+    double alpha = 2.0;
+    int degree = 2;
+    double u = 0.0, v = 1.0;
+    Vec coeffs;
+    int query_cost() const { return degree; }
+};
+
+Spec make_spec(int kind, double alpha, int m, double u, double v) {  // poly.cpp:60-80
+    Spec s;
+    s.kind = kind;
+    s.alpha = alpha;
+    if (kind == 0) {
+        const int ai = static_cast<int>(std::lround(alpha));
+        if (ai < 1) fail(kInvalidArgument, "int_power needs alpha >= 1");
+        s.degree = ai;
+    } else if (kind == 1) {
+        if (m < 1) fail(kInvalidArgument, "taylor spec needs m >= 1");
+        if (v <= 0.0 || v > 1.0) fail(kDomainError, "taylor spec needs v in (0, 1]");
+        if (alpha <= 0.0) fail(kInvalidArgument, "taylor spec needs alpha > 0");
+        s.degree = m;
+        s.v = v;
+        s.coeffs = binomial_coeffs(alpha, m);
+    } else {
+        if (m < 1) fail(kInvalidArgument, "chebyshev spec needs m >= 1");
+        if (alpha <= 0.0) fail(kInvalidArgument, "chebyshev spec needs alpha > 0");
+        if (u < 0.0) fail(kDomainError, "chebyshev spec needs u >= 0");
+        const double sv = safeguard(u, v);
+        if (sv <= u) fail(kDomainError, "chebyshev spec needs v > u after safeguard");
+        s.degree = m;
+        s.u = u;
+        s.v = sv;
+        s.coeffs = chebyshev_coeffs(alpha, m, u, sv);
+    }
+    return s;
+}
+
+// apply_int_power / apply_taylor / apply_chebyshev over panels (poly.cpp:97-134)
+Mat axpby(double a, const Mat& x, double b, const Mat& y) {  // a*x + b*y
+    Mat z(x.r, x.c);
+    for (size_t i = 0; i < z.d.size(); ++i) z.d[i] = a * x.d[i] + b * y.d[i];
+    return z;
+}
+void add_scaled(Mat& acc, double c, const Mat& t) {
+    for (size_t i = 0; i < acc.d.size(); ++i) acc.d[i] += c * t.d[i];
+}
+
+Mat apply_panel(const Spec& s, const Mat& a, const Mat& x) {
+    if (a.r != a.c || a.c != x.r) fail(kSizeMismatch, "apply_panel: size mismatch");
+    if (s.kind == 0) {
+        Mat y = x;
+        for (int k = 0; k < s.degree; ++k) y = matmul_panel(a, y);
+        return y;
+    }
+    if (s.kind == 1) {
+        const double inv_v = 1.0 / s.v;
+        Mat term = x;
+        Mat acc(x.r, x.c);
+        for (size_t i = 0; i < acc.d.size(); ++i) acc.d[i] = s.coeffs[0] * x.d[i];
+        for (int k = 1; k <= s.degree; ++k) {
+            Mat at = matmul_panel(a, term);
+            term = axpby(inv_v, at, -1.0, term);  // inv_v * mul(term) - term
+            add_scaled(acc, s.coeffs[k], term);
+        }
+        const double p = std::pow(s.v, s.alpha);
+        for (auto& v : acc.d) v *= p;
+        return acc;
+    }
+    const double scale = 2.0 / (s.v - s.u);
+    const double center = (s.v + s.u) / (s.v - s.u);
+    auto mapped = [&](const Mat& w) { return axpby(scale, matmul_panel(a, w), -center, w); };
+    Mat t_prev = x;
+    Mat acc(x.r, x.c);
+    for (size_t i = 0; i < acc.d.size(); ++i) acc.d[i] = (0.5 * s.coeffs[0]) * x.d[i];
+    if (s.degree >= 1) {
+        Mat t_cur = mapped(x);
+        add_scaled(acc, s.coeffs[1], t_cur);
+        for (int k = 2; k <= s.degree; ++k) {
+            Mat mt = mapped(t_cur);
+            Mat t_next(x.r, x.c);
+            for (size_t i = 0; i < t_next.d.size(); ++i) t_next.d[i] = 2.0 * mt.d[i] - t_prev.d[i];
+            add_scaled(acc, s.coeffs[k], t_next);
+            t_prev = std::move(t_cur);
+            t_cur = std::move(t_next);
+        }
+    }
+    return acc;
+}
+
+double scalar_value(const Spec& s, double lam) {  // poly.cpp:166-168
+    Mat a(1, 1, lam), x(1, 1, 1.0);
+    return apply_panel(s, a, x)(0, 0);
+}
+
+// ---------------------------------------------------------------- QR (Eigen ColPivHouseholderQR restated)
+// Householder QR with column pivoting; rank = #{|R_ii| > thr * max pivot}.
+struct PivQR {
+    Mat qr;        // R in the upper triangle, Householder vectors below
+    Vec hcoeffs;   // tau
+    int rank = 0;
+};
+
+PivQR colpiv_qr(const Mat& y, double threshold) {
+    PivQR f;
+    f.qr = y;
+    const int64_t m = y.r, n = y.c;
+    const int64_t size = std::min(m, n);
+    f.hcoeffs.assign(size, 0.0);
+    Vec colnorm(n), colnorm_upd(n);
+    for (int64_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int64_t i = 0; i < m; ++i) s += f.qr(i, j) * f.qr(i, j);
+        colnorm[j] = colnorm_upd[j] = std::sqrt(s);
+    }
+    double maxpivot = 0.0;
+    int64_t nonzero = size;
+    for (int64_t k = 0; k < size; ++k) {
+        int64_t best = k;
+        for (int64_t j = k + 1; j < n; ++j)
+            if (colnorm_upd[j] > colnorm_upd[best]) best = j;
+        if (colnorm_upd[best] == 0.0 && nonzero == size) nonzero = k;
+        if (best != k) {
+            for (int64_t i = 0; i < m; ++i) std::swap(f.qr(i, k), f.qr(i, best));
+            std::swap(colnorm[k], colnorm[best]);
+            std::swap(colnorm_upd[k], colnorm_upd[best]);
+        }
+        // Householder reflector for column k, rows k..m-1
+        double sig = 0.0;
+        for (int64_t i = k + 1; i < m; ++i) sig += f.qr(i, k) * f.qr(i, k);
+        const double c0 = f.qr(k, k);
+        double beta, tau;
+        if (sig == 0.0) {
+            tau = 0.0;
+            beta = c0;
+            for (int64_t i = k + 1; i < m; ++i) f.qr(i, k) = 0.0;
+        } else {
+            beta = std::sqrt(c0 * c0 + sig);
+            if (c0 >= 0.0) beta = -beta;
+            for (int64_t i = k + 1; i < m; ++i) f.qr(i, k) /= (c0 - beta);
+            tau = (beta - c0) / beta;
+        }
+        f.qr(k, k) = beta;
+        f.hcoeffs[k] = tau;
+        maxpivot = std::max(maxpivot, std::abs(beta));
+        // apply H = I - tau v v^T (v = [1; qr(k+1:,k)]) to the trailing columns
+        for (int64_t j = k + 1; j < n; ++j) {
+            double s = f.qr(k, j);
+            for (int64_t i = k + 1; i < m; ++i) s += f.qr(i, k) * f.qr(i, j);
+            s *= tau;
+            f.qr(k, j) -= s;
+            for (int64_t i = k + 1; i < m; ++i) f.qr(i, j) -= s * f.qr(i, k);
+        }
+        // downdate column norms (LAPACK dlaqp2 style)
+        for (int64_t j = k + 1; j < n; ++j) {
+            if (colnorm_upd[j] != 0.0) {
+                double t = std::abs(f.qr(k, j)) / colnorm_upd[j];
+                t = 1.0 - t * t;
+                t = t < 0.0 ? 0.0 : t;
+                const double t2 = t * (colnorm_upd[j] / colnorm[j]) * (colnorm_upd[j] / colnorm[j]);
+                if (t2 <= std::sqrt(std::numeric_limits<double>::epsilon())) {
+                    double s = 0.0;
+                    for (int64_t i = k + 1; i < m; ++i) s += f.qr(i, j) * f.qr(i, j);
+                    colnorm[j] = colnorm_upd[j] = std::sqrt(s);
+                } else {
+                    colnorm_upd[j] *= std::sqrt(t);
+                }
+            }
+        }
+    }
+    const double thr = std::abs(maxpivot) * threshold;
+    int rank = 0;
+    for (int64_t i = 0; i < nonzero; ++i) rank += std::abs(f.qr(i, i)) > thr ? 1 : 0;
+    f.rank = rank;
+    return f;
+}
+
+// householderQ() * Identity(m, cols)
+Mat householder_q(const PivQR& f, int64_t cols) {
+    const int64_t m = f.qr.r;
+    Mat q(m, cols);
+    for (int64_t j = 0; j < std::min(m, cols); ++j) q(j, j) = 1.0;
+    for (int64_t k = static_cast<int64_t>(f.hcoeffs.size()) - 1; k >= 0; --k) {
+        const double tau = f.hcoeffs[k];
+        if (tau == 0.0) continue;
+        for (int64_t j = 0; j < cols; ++j) {
+            double s = q(k, j);
+            for (int64_t i = k + 1; i < m; ++i) s += f.qr(i, k) * q(i, j);
+            s *= tau;
+            q(k, j) -= s;
+            for (int64_t i = k + 1; i < m; ++i) q(i, j) -= s * f.qr(i, k);
+        }
+    }
+    return q;
+}
+
+// ---------------------------------------------------------------- hutchpp.cpp
+struct Trace {
+    double value = 0.0, low = 0.0, residual = 0.0;
+    int queries = 0, rank = 0;
+    bool exact = false;
+};
+
+double col_dot_sum(const Mat& a, const Mat& b) {
+    double sum = 0.0;
+    for (int64_t j = 0; j < a.c; ++j) {
+        double s = 0.0;
+        for (int64_t i = 0; i < a.r; ++i) s += a(i, j) * b(i, j);
+        sum += s;
+    }
+    return sum;
+}
+
+Mat mul_t(const Mat& q, const Mat& w) {  // q^T w
+    Mat c(q.c, w.c);
+    for (int64_t j = 0; j < w.c; ++j)
+        for (int64_t a = 0; a < q.c; ++a) {
+            double s = 0.0;
+            for (int64_t i = 0; i < q.r; ++i) s += q(i, a) * w(i, j);
+            c(a, j) = s;
+        }
+    return c;
+}
+void sub_mul(Mat& w, const Mat& q, const Mat& c) {  // w -= q c
+    for (int64_t j = 0; j < w.c; ++j)
+        for (int64_t a = 0; a < q.c; ++a) {
+            const double cj = c(a, j);
+            for (int64_t i = 0; i < w.r; ++i) w(i, j) -= q(i, a) * cj;
+        }
+}
+
+double projected_trace(const Spec& f, const Mat& a, const Mat& q) {  // hutchpp.cpp:33-39
+    if (q.c == 0) return 0.0;
+    return col_dot_sum(q, apply_panel(f, a, q));
+}
+
+double residual_probe_trace(const Spec& f, const Mat& a, const Mat& q, Mat w) {  // hutchpp.cpp:41-51
+    const int64_t s_g = w.c;
+    if (q.c > 0) sub_mul(w, q, mul_t(q, w));
+    Mat fw = apply_panel(f, a, w);
+    if (q.c > 0) sub_mul(fw, q, mul_t(q, fw));
+    return col_dot_sum(w, fw) / static_cast<double>(s_g);
+}
+
+double exact_trace(const Spec& f, const Mat& a) {  // hutchpp.cpp:53-65
+    const int64_t n = a.r;
+    double sum = 0.0;
+    for (int64_t j0 = 0; j0 < n; j0 += 256) {
+        const int64_t len = std::min<int64_t>(256, n - j0);
+        Mat basis(n, len);
+        for (int64_t j = 0; j < len; ++j) basis(j0 + j, j) = 1.0;
+        const Mat fb = apply_panel(f, a, basis);
+        for (int64_t j = 0; j < len; ++j) sum += fb(j0 + j, j);
+    }
+    return sum;
+}
+
+// hutchpp (hutchpp.cpp:69-115); S / G may be injected; s_q = 0 gives plain Hutchinson
+Trace hutchpp(const Spec& f, const Mat& a, int s_q, int s_g, uint64_t seed, int kind, const Mat* S, const Mat* G) {
+    if (a.r != a.c) fail(kSizeMismatch, "hutchpp needs a square matrix");
+    const int64_t n = a.r;
+    const int cost = f.query_cost();
+    Trace est;
+    if (s_q >= n) {
+        est.value = est.low = exact_trace(f, a);
+        est.rank = static_cast<int>(n);
+        est.queries = static_cast<int>(n) * cost;
+        est.exact = true;
+        return est;
+    }
+    Mat q(n, 0);
+    PivQR qr;
+    if (s_q > 0) {
+        const Mat sketch = S ? *S : probe_panel(n, s_q, seed, "hutchpp-sketch", kind);
+        const Mat y = matmul_panel(a, sketch);
+        qr = colpiv_qr(y, 1e-12);
+        if (qr.rank == 0) fail(kRankCollapse, "hutchpp sketch A*S is numerically zero");
+        est.rank = qr.rank;
+        est.queries = s_q + qr.rank * cost;
+        const int64_t codim = n - qr.rank;
+        if (s_g >= codim) {
+            const Mat full = householder_q(qr, n);
+            Mat lo(n, qr.rank), hi(n, codim);
+            std::copy(full.d.begin(), full.d.begin() + n * qr.rank, lo.d.begin());
+            std::copy(full.d.begin() + n * qr.rank, full.d.end(), hi.d.begin());
+            est.low = projected_trace(f, a, lo);
+            est.residual = projected_trace(f, a, hi);
+            est.queries += static_cast<int>(codim) * cost;
+            est.exact = true;
+            est.value = est.low + est.residual;
+            return est;
+        }
+        q = householder_q(qr, qr.rank);
+    }
+    est.low = projected_trace(f, a, q);
+    const Mat w = G ? *G : probe_panel(n, s_g, seed, "hutchpp-probe", kind);
+    est.residual = s_g > 0 ? residual_probe_trace(f, a, q, w) : 0.0;
+    est.queries += s_g * cost;
+    est.value = est.low + est.residual;
+    return est;
+}
+
+// ---------------------------------------------------------------- entropy.cpp
+void validate_alpha(double alpha) {  // entropy.cpp:16-22
+    if (!(alpha > 0.0)) fail(kInvalidArgument, "alpha must be positive");
+    if (std::abs(alpha - 1.0) <= 1e-9) fail(kAlphaIsOne, "alpha within 1e-9 of 1 is rejected");
+}
+bool integer_alpha(double alpha, int* value) {
+    const double r = std::round(alpha);
+    if (std::abs(alpha - r) <= 1e-9 && r >= 2.0) {
+        if (value) *value = static_cast<int>(r);
+        return true;
+    }
+    return false;
+}
+double entropy_from_trace(double trace, double alpha) {  // entropy.cpp:62-69
+    validate_alpha(alpha);
+    if (!(trace > 0.0)) fail(kNonPositiveTrace, "trace estimate is not positive");
+    return std::log(trace) / (1.0 - alpha);
+}
+
+// symmetric eigenvalues: Householder tridiagonalisation + implicit QL (textbook tred2/tqli)
+Vec sym_eigvals(Mat a) {
+    const int64_t n = a.r;
+    Vec d(n), e(n);
+    for (int64_t i = n - 1; i > 0; --i) {
+        const int64_t l = i - 1;
+        double h = 0.0, scale = 0.0;
+        if (l > 0) {
+            for (int64_t k = 0; k <= l; ++k) scale += std::abs(a(i, k));
+            if (scale == 0.0) {
+                e[i] = a(i, l);
+            } else {
+                for (int64_t k = 0; k <= l; ++k) {
+                    a(i, k) /= scale;
+                    h += a(i, k) * a(i, k);
+                }
+                double f = a(i, l);
+                double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
+                e[i] = scale * g;
+                h -= f * g;
+                a(i, l) = f - g;
+                f = 0.0;
+                for (int64_t j = 0; j <= l; ++j) {
+                    g = 0.0;
+                    for (int64_t k = 0; k <= j; ++k) g += a(j, k) * a(i, k);
+                    for (int64_t k = j + 1; k <= l; ++k) g += a(k, j) * a(i, k);
+                    e[j] = g / h;
+                    f += e[j] * a(i, j);
+                }
+                const double hh = f / (h + h);
+                for (int64_t j = 0; j <= l; ++j) {
+                    f = a(i, j);
+                    e[j] = g = e[j] - hh * f;
+                    for (int64_t k = 0; k <= j; ++k) a(j, k) -= (f * e[k] + g * a(i, k));
+                }
+            }
+        } else {
+            e[i] = a(i, l);
+        }
+        d[i] = h;
+    }
+    for (int64_t i = 0; i < n; ++i) d[i] = a(i, i);
+    for (int64_t i = 1; i < n; ++i) e[i - 1] = e[i];
+    if (n > 0) e[n - 1] = 0.0;
+    for (int64_t l = 0; l < n; ++l) {
+        int iter = 0;
+        int64_t m;
+        do {
+            for (m = l; m < n - 1; ++m) {
+                const double dd = std::abs(d[m]) + std::abs(d[m + 1]);
+                if (std::abs(e[m]) <= std::numeric_limits<double>::epsilon() * dd) break;
+            }
+            if (m != l) {
+                if (iter++ == 200) fail(kInvalidArgument, "eigenvalue iteration did not converge");
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = std::hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::abs(r) : -std::abs(r)));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int64_t i;
+                for (i = m - 1; i >= l; --i) {
+                    double f = s * e[i], b = c * e[i];
+                    e[i + 1] = (r = std::hypot(f, g));
+                    if (r == 0.0) {
+                        d[i + 1] -= p;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    s = f / r;
+                    c = g / r;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    d[i + 1] = g + (p = s * r);
+                    g = c * r - b;
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= p;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
+    }
+    std::sort(d.begin(), d.end());
+    return d;
+}
+
+double exact_trace_power(const Mat& a, double alpha) {  // entropy.cpp:71-90 body
+    const Vec lam = sym_eigvals(a);
+    double trace = 0.0;
+    for (double l : lam) {
+        const double c = std::clamp(l, 0.0, 1.0);
+        if (c > 0.0) trace += std::pow(c, alpha);
+    }
+    return trace;
+}
+
+struct Params {
+    double alpha = 2.0;
+    int method = 4;  // 0 exact 1 int 2 taylor 3 chebyshev 4 auto
+    int s = 0, m = 0;
+    double epsilon = 1e-2, delta = 1e-2;
+    uint64_t seed = 0;
+    PowerOptions power;
+    bool has_bounds = false;
+    Bounds bounds;
+    int probe_kind = 0;
+    int s_q = -1, s_g = -1;
+};
+
+struct Estimate {
+    double entropy = 0.0, trace = 0.0;
+    int method = 0, s = 0, m = 0;
+    bool has_bounds = false;
+    Bounds bounds;
+    bool deterministic = false;
+    Trace tr;
+};
+
+int round_up4(double x) {
+    const long c = static_cast<long>(std::ceil(x));
+    return static_cast<int>((c + 3) / 4 * 4);
+}
+
+void select_params(double alpha, double eps, double delta, const Bounds& b, int64_t n, int method, int* s,
+                   int* m) {  // entropy.cpp:137-176
+    validate_alpha(alpha);
+    if (!(eps > 0.0 && eps < 1.0)) fail(kInvalidArgument, "epsilon must be in (0,1)");
+    if (!(delta > 0.0 && delta < 1.0)) fail(kInvalidArgument, "delta must be in (0,1)");
+    const double gap = std::abs(alpha - 1.0);
+    const double lid = std::log(1.0 / delta);
+    *s = round_up4(std::sqrt(lid) / (eps * gap) + lid);
+    const double ieg = 1.0 / (eps * gap);
+    if (method == 2) {
+        if (b.u > 0.0) *m = static_cast<int>(std::ceil(b.kappa * std::log(ieg)));
+        else
+            *m = static_cast<int>(std::ceil(std::pow(b.v * static_cast<double>(n), 1.0 / std::min(1.0, alpha)) *
+                                            std::pow(ieg, 1.0 / alpha)));
+        *m = std::max(*m, static_cast<int>(std::ceil(alpha)) + 1);
+    } else if (method == 3) {
+        if (b.u > 0.0) *m = static_cast<int>(std::ceil(std::sqrt(b.kappa) * std::log(b.kappa * ieg)));
+        else
+            *m = static_cast<int>(std::ceil(std::pow(b.v * static_cast<double>(n), 0.5 / std::min(1.0, alpha)) *
+                                            std::pow(ieg, 0.5 / alpha)));
+        *m = std::max(*m, 1);
+    } else {
+        *m = 0;
+    }
+}
+
+Estimate from_hutchpp(const Mat& a, const Spec& f, double alpha, int s, const Params& p, int method, int m_used) {
+    int s_q, s_g;
+    if (p.s_q >= 0 || p.s_g >= 0) {
+        s_q = std::max(p.s_q, 0);
+        s_g = std::max(p.s_g, 0);
+    } else {
+        if (s < 8) fail(kInvalidArgument, "hutchpp needs a query budget s >= 8");
+        s_q = s / 4;
+        s_g = s - 2 * (s / 4);
+    }
+    Estimate e;
+    e.tr = hutchpp(f, a, s_q, s_g, p.seed, p.probe_kind, nullptr, nullptr);
+    e.trace = e.tr.value;
+    e.entropy = entropy_from_trace(e.tr.value, alpha);
+    e.method = method;
+    e.s = s;
+    e.m = m_used;
+    e.deterministic = e.tr.exact;
+    return e;
+}
+
+Estimate estimate(const Mat& a, const Params& p) {  // entropy.cpp:201-275
+    validate_alpha(p.alpha);
+    if (a.r != a.c) fail(kSizeMismatch, "estimate needs a square matrix");
+    const int64_t n = a.r;
+    int ai = 0;
+    const bool is_int = integer_alpha(p.alpha, &ai);
+    bool have = p.has_bounds;
+    Bounds bounds = p.bounds;
+    auto ensure = [&]() -> const Bounds& {
+        if (!have) {
+            PowerOptions o = p.power;
+            o.seed = derive_key(p.seed, hash_name("bounds"));
+            bounds = estimate_bounds(a, o);
+            have = true;
+        }
+        return bounds;
+    };
+    int method = p.method;
+    if (method == 4) {
+        if (is_int) method = 1;
+        else {
+            const Bounds& b = ensure();
+            const bool ffr = b.u > 0.0 && b.kappa <= 50.0;
+            const bool fdf = b.u == 0.0 && b.v * static_cast<double>(n) <= 50.0;
+            method = (ffr || fdf) ? 2 : 3;
+        }
+    }
+    Estimate est;
+    if (method == 0) {
+        if (n > 20000) fail(kInvalidArgument, "entropy_exact is guarded at n <= 20000");
+        est.trace = exact_trace_power(a, p.alpha);
+        est.entropy = entropy_from_trace(est.trace, p.alpha);
+        est.method = 0;
+        est.deterministic = true;
+    } else if (method == 1) {
+        if (!is_int) fail(kInvalidArgument, "method=int needs an integer alpha >= 2");
+        int s = p.s, m = 0;
+        if (s <= 0) select_params(p.alpha, p.epsilon, p.delta, Bounds{}, n, 1, &s, &m);
+        est = from_hutchpp(a, make_spec(0, ai, 0, 0, 0), ai, s, p, 1, 0);
+    } else {
+        const Bounds& b = ensure();
+        int s = p.s, m = p.m;
+        if (!(p.s > 0 && p.m > 0)) {
+            select_params(p.alpha, p.epsilon, p.delta, b, n, method, &s, &m);
+            if (p.s > 0) s = p.s;
+            if (p.m > 0) m = p.m;
+        }
+        if (std::abs(p.alpha - std::round(p.alpha)) <= 1e-9)
+            fail(kInvalidArgument, "entropy_taylor/chebyshev handle non-integer alpha");
+        if (method == 2) {
+            const int mm = std::max(m, static_cast<int>(std::ceil(p.alpha)) + 1);
+            est = from_hutchpp(a, make_spec(1, p.alpha, mm, 0, b.v), p.alpha, s, p, 2, mm);
+        } else {
+            est = from_hutchpp(a, make_spec(2, p.alpha, m, b.u, b.v), p.alpha, s, p, 3, m);
+        }
+    }
+    est.has_bounds = have;
+    est.bounds = bounds;
+    return est;
+}
+
+void mu_bound(double u, double v, double alpha, int64_t n, double* mu, double* lower, double* upper) {
+    validate_alpha(alpha);
+    const double inv_n = 1.0 / static_cast<double>(n);
+    if (u < 0.0 || v > 1.0 || u > inv_n + 1e-12 || v < inv_n - 1e-12)
+        fail(kInvalidArgument, "mu_bound needs 0 <= u <= 1/n <= v <= 1");
+    const double flat = std::pow(static_cast<double>(n), 1.0 - alpha);
+    double m;
+    if (v > u) {
+        const double nd = static_cast<double>(n);
+        const double w_v = (1.0 - u * nd) / (v - u);
+        const double w_u = (v * nd - 1.0) / (v - u);
+        m = w_v * std::pow(v, alpha) + w_u * (u > 0.0 ? std::pow(u, alpha) : 0.0);
+    } else if (v == u && std::abs(v - inv_n) <= 1e-12) {
+        m = flat;
+    } else {
+        fail(kDegenerateBounds, "mu_bound needs v > u (or the degenerate v = u = 1/n)");
+    }
+    *mu = m;
+    *lower = std::min(m, flat);
+    *upper = std::max(m, flat);
+}
+
+// simulate.cpp:9-17
+Mat mixture_samples(int n, int d, uint64_t seed, double center) {
+    Mat x(n, d);
+    Stream s(derive_key(seed, hash_name("mixture")));
+    for (int i = 0; i < n; ++i) {
+        const double mu = (s.next_u64() & 1) ? center : -center;
+        for (int j = 0; j < d; ++j) x(i, j) = mu + s.next_gaussian();
+    }
+    return x;
+}
+
+}  // namespace orc
+
+// =====================================================================================
+// extern "C" surface for ctypes (tests/ and bench.py only)
+// =====================================================================================
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const orc::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 24;
+    }
+}
+
+orc::Mat wrap(const double* p, int64_t r, int64_t c) {
+    orc::Mat m(r, c);
+    std::memcpy(m.d.data(), p, sizeof(double) * r * c);
+    return m;
+}
+void unwrap(const orc::Mat& m, double* out) { std::memcpy(out, m.d.data(), sizeof(double) * m.d.size()); }
+
+struct CParams {
+    double alpha;
+    int method, s, m;
+    double epsilon, delta;
+    uint64_t seed;
+    int power_max_iters;
+    double power_tol;
+    uint64_t power_seed;
+    double power_rank_floor;
+    int has_bounds;
+    double bu, bv;
+    int probe_kind, s_q, s_g;
+};
+
+struct COut {  // estimate result
+    double entropy, trace, low, residual;
+    int method, s, m, queries, rank, exact, deterministic, has_bounds;
+    double bu, bv, kappa;
+    int iterations_used, v_converged, u_converged, rank_deficient;
+};
+
+orc::Params to_params(const CParams* c) {
+    orc::Params p;
+    p.alpha = c->alpha;
+    p.method = c->method;
+    p.s = c->s;
+    p.m = c->m;
+    p.epsilon = c->epsilon;
+    p.delta = c->delta;
+    p.seed = c->seed;
+    p.power.max_iters = c->power_max_iters;
+    p.power.tol = c->power_tol;
+    p.power.seed = c->power_seed;
+    p.power.rank_floor = c->power_rank_floor;
+    p.has_bounds = c->has_bounds != 0;
+    p.bounds.u = c->bu;
+    p.bounds.v = c->bv;
+    p.bounds.kappa = c->bu > 0 ? c->bv / c->bu : std::numeric_limits<double>::infinity();
+    p.probe_kind = c->probe_kind;
+    p.s_q = c->s_q;
+    p.s_g = c->s_g;
+    return p;
+}
+
+void to_out(const orc::Estimate& e, COut* o) {
+    o->entropy = e.entropy;
+    o->trace = e.trace;
+    o->low = e.tr.low;
+    o->residual = e.tr.residual;
+    o->method = e.method;
+    o->s = e.s;
+    o->m = e.m;
+    o->queries = e.tr.queries;
+    o->rank = e.tr.rank;
+    o->exact = e.tr.exact;
+    o->deterministic = e.deterministic;
+    o->has_bounds = e.has_bounds;
+    o->bu = e.bounds.u;
+    o->bv = e.bounds.v;
+    o->kappa = e.bounds.kappa;
+    o->iterations_used = e.bounds.iterations_used;
+    o->v_converged = e.bounds.v_converged;
+    o->u_converged = e.bounds.u_converged;
+    o->rank_deficient = e.bounds.rank_deficient;
+}
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error() { return g_err.c_str(); }
+int oracle_threads() {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+void oracle_set_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}
+
+uint64_t oracle_mix64(uint64_t x) { return orc::mix64(x); }
+uint64_t oracle_derive_key(uint64_t s, uint64_t t) { return orc::derive_key(s, t); }
+uint64_t oracle_hash_name(const char* n) { return orc::hash_name(n); }
+
+int oracle_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out) {
+    return guard([&] { unwrap(orc::probe_panel(n, cols, seed, label, kind), out); });
+}
+int oracle_stream_gaussian(uint64_t key, int64_t count, double* out) {
+    return guard([&] {
+        orc::Stream s(key);
+        for (int64_t i = 0; i < count; ++i) out[i] = s.next_gaussian();
+    });
+}
+int oracle_mixture_samples(int n, int d, uint64_t seed, double center, double* out) {
+    return guard([&] { unwrap(orc::mixture_samples(n, d, seed, center), out); });
+}
+int oracle_gaussian_gram(const double* x, int64_t n, int64_t d, double sigma, double* out) {
+    return guard([&] { unwrap(orc::gaussian_gram(wrap(x, n, d), sigma), out); });
+}
+int oracle_build_kernel(const double* x, int64_t n, int64_t d, double sigma, double* out) {
+    return guard([&] { unwrap(orc::build_kernel(wrap(x, n, d), sigma), out); });
+}
+int oracle_hadamard_joint(const double* a, int64_t na, const double* b, int64_t nb, double* out) {
+    return guard([&] {
+        const orc::Mat ma = wrap(a, na, na), mb = wrap(b, nb, nb);
+        unwrap(orc::hadamard_joint({&ma, &mb}), out);
+    });
+}
+int oracle_matvec(const double* a, int64_t n, const double* x, double* y) {
+    return guard([&] {
+        orc::Vec xv(x, x + n);
+        const orc::Vec r = orc::matvec(wrap(a, n, n), xv);
+        std::copy(r.begin(), r.end(), y);
+    });
+}
+int oracle_matmul_panel(const double* a, int64_t n, const double* x, int s, double* y) {
+    return guard([&] { unwrap(orc::matmul_panel(wrap(a, n, n), wrap(x, n, s)), y); });
+}
+int oracle_apply_panel(int kind, double alpha, int m, double u, double v, const double* a, int64_t n,
+                       const double* x, int s, double* y) {
+    return guard([&] { unwrap(orc::apply_panel(orc::make_spec(kind, alpha, m, u, v), wrap(a, n, n), wrap(x, n, s)), y); });
+}
+int oracle_scalar_value(int kind, double alpha, int m, double u, double v, double lam, double* out) {
+    return guard([&] { *out = orc::scalar_value(orc::make_spec(kind, alpha, m, u, v), lam); });
+}
+int oracle_spec_coeffs(int kind, double alpha, int m, double u, double v, double* coeffs, double* safe_v) {
+    return guard([&] {
+        const orc::Spec s = orc::make_spec(kind, alpha, m, u, v);
+        std::copy(s.coeffs.begin(), s.coeffs.end(), coeffs);
+        *safe_v = s.v;
+    });
+}
+int oracle_binomial_coeffs(double alpha, int m, double* out) {
+    return guard([&] {
+        const auto b = orc::binomial_coeffs(alpha, m);
+        std::copy(b.begin(), b.end(), out);
+    });
+}
+int oracle_chebyshev_coeffs(double alpha, int m, double u, double v, double* out) {
+    return guard([&] {
+        const auto c = orc::chebyshev_coeffs(alpha, m, u, v);
+        std::copy(c.begin(), c.end(), out);
+    });
+}
+double oracle_taylor_tail_constant(double alpha, int k_max) { return orc::taylor_tail_constant(alpha, k_max); }
+double oracle_safeguard(double u, double v) { return orc::safeguard(u, v); }
+
+int oracle_power_method(const double* a, int64_t n, int max_iters, double tol, uint64_t seed, double* rayleigh,
+                        int* iterations, int* converged) {
+    return guard([&] {
+        orc::PowerOptions o;
+        o.max_iters = max_iters, o.tol = tol, o.seed = seed;
+        const orc::PowerResult r = orc::power_method(wrap(a, n, n), o);
+        *rayleigh = r.rayleigh, *iterations = r.iterations, *converged = r.converged;
+    });
+}
+int oracle_estimate_bounds(const double* a, int64_t n, int max_iters, double tol, uint64_t seed, double rank_floor,
+                           COut* out) {
+    return guard([&] {
+        orc::PowerOptions o;
+        o.max_iters = max_iters, o.tol = tol, o.seed = seed, o.rank_floor = rank_floor;
+        const orc::Bounds b = orc::estimate_bounds(wrap(a, n, n), o);
+        orc::Estimate e;
+        e.bounds = b;
+        e.has_bounds = true;
+        to_out(e, out);
+    });
+}
+int oracle_colpiv_rank(const double* y, int64_t n, int c, double threshold, int* rank, double* q) {
+    return guard([&] {
+        const orc::PivQR f = orc::colpiv_qr(wrap(y, n, c), threshold);
+        *rank = f.rank;
+        if (q) unwrap(orc::householder_q(f, f.rank), q);
+    });
+}
+int oracle_hutchpp(int kind, double alpha, int m, double u, double v, const double* a, int64_t n, int s_q, int s_g,
+                   uint64_t seed, int probe_kind, const double* S, const double* G, COut* out) {
+    return guard([&] {
+        const orc::Mat ma = wrap(a, n, n);
+        orc::Mat ms, mg;
+        if (S) ms = wrap(S, n, s_q);
+        if (G) mg = wrap(G, n, s_g);
+        orc::Estimate e;
+        e.tr = orc::hutchpp(orc::make_spec(kind, alpha, m, u, v), ma, s_q, s_g, seed, probe_kind, S ? &ms : nullptr,
+                            G ? &mg : nullptr);
+        e.trace = e.tr.value;
+        to_out(e, out);
+    });
+}
+long oracle_expected_queries(int kind, double alpha, int m, double u, double v, int s) {
+    const orc::Spec f = orc::make_spec(kind, alpha, m, u, v);
+    const long s_q = s / 4, s_g = s - 2 * (s / 4);
+    return s_q + static_cast<long>(f.query_cost()) * (s_q + s_g) + 2 * s_g;
+}
+int oracle_estimate(const double* a, int64_t n, const CParams* p, COut* out) {
+    return guard([&] { to_out(orc::estimate(wrap(a, n, n), to_params(p)), out); });
+}
+int oracle_eigvals(const double* a, int64_t n, double* out) {
+    return guard([&] {
+        const orc::Vec l = orc::sym_eigvals(wrap(a, n, n));
+        std::copy(l.begin(), l.end(), out);
+    });
+}
+int oracle_entropy_from_trace(double trace, double alpha, double* out) {
+    return guard([&] { *out = orc::entropy_from_trace(trace, alpha); });
+}
+int oracle_select_params(double alpha, double eps, double delta, double u, double v, double kappa, int64_t n,
+                         int method, int* s, int* m) {
+    return guard([&] {
+        orc::Bounds b;
+        b.u = u, b.v = v, b.kappa = kappa;
+        orc::select_params(alpha, eps, delta, b, n, method, s, m);
+    });
+}
+int oracle_mu_bound(double u, double v, double alpha, int64_t n, double* mu, double* lo, double* hi) {
+    return guard([&] { orc::mu_bound(u, v, alpha, n, mu, lo, hi); });
+}
+
+// --- CPU-baseline sample: one row slab of the estimator's cost structure ---------
+// Builds rows [r0, r0+h) of A from X exactly as build_kernel does (gaussian_row +
+// normalisation), then runs `passes` block products of that slab with a random
+// n x s panel split into the reference's separately-applied groups (cols_q, then
+// cols_w), each as 8-column panels re-streaming the slab. Returns seconds.
+double oracle_slab_sample(const double* x, int64_t n, int64_t d, double sigma, int64_t r0, int64_t h, int passes,
+                          int cols_q, int cols_w) {
+    const auto t0 = std::chrono::steady_clock::now();
+    orc::Vec sq(n, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t k = 0; k < d; ++k) s += x[i + k * n] * x[i + k * n];
+        sq[i] = s;
+    }
+    const double inv2 = 1.0 / (2.0 * sigma * sigma), inv_n = 1.0 / static_cast<double>(n);
+    orc::Mat slab(h, n);  // rows r0.. of A, column-major h x n
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t ii = 0; ii < h; ++ii) {
+        const int64_t i = r0 + ii;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) {
+                slab(ii, j) = inv_n;
+                continue;
+            }
+            double dt = 0.0;
+            for (int64_t t = 0; t < d; ++t) dt += x[i + t * n] * x[j + t * n];
+            double d2 = sq[i] + sq[j] - 2.0 * dt;
+            if (d2 < 0.0) d2 = 0.0;
+            slab(ii, j) = inv_n * std::exp(-d2 * inv2);
+        }
+    }
+    orc::Mat v(n, std::max(cols_q, cols_w));
+    orc::Stream st(7);
+    st.fill_gaussian(v);
+    double sink = 0.0;
+    for (int p = 0; p < passes; ++p) {
+        for (int grp = 0; grp < 2; ++grp) {
+            const int cols = grp == 0 ? cols_q : cols_w;
+            if (cols <= 0) continue;
+            orc::Mat y(h, cols);
+            const int64_t nb = (cols + 7) / 8;
+#pragma omp parallel for schedule(dynamic)
+            for (int64_t b = 0; b < nb; ++b) {
+                const int64_t j0 = b * 8, j1 = std::min<int64_t>(cols, j0 + 8);
+                for (int64_t k = 0; k < n; ++k) {
+                    const double* ak = slab.col(k);
+                    for (int64_t j = j0; j < j1; ++j) {
+                        const double vkj = v(k, j);
+                        double* yj = y.col(j);
+                        for (int64_t i = 0; i < h; ++i) yj[i] += ak[i] * vkj;
+                    }
+                }
+            }
+            sink += y.d[0];
+        }
+    }
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return dt + (sink == 12345.678 ? 1e-30 : 0.0);
+}
+
+}  // extern "C"

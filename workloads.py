@@ -1,0 +1,99 @@
+"""Seeded synthetic inputs for the five BASELINE.json configurations.
+
+All randomness comes from the reference's counter-based RNG
+(proj/src/rng.cpp) through per-column substreams, so the GPU path, the oracle
+and the CPU baseline see identical arrays. The reference measures no public
+dataset for this path; these stand in with the shapes and distributions
+BASELINE.json names.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def mix64_np(x: np.ndarray) -> np.ndarray:
+    """Vectorised splitmix64 finalizer (rng.cpp:8-14), bitwise identical."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def stream_u64(key: int, count: int) -> np.ndarray:
+    """RandomStream(key).next_u64() for counters 0..count-1."""
+    k = np.uint64(key & 0xFFFFFFFFFFFFFFFF)
+    return mix64_np(k ^ mix64_np(np.arange(count, dtype=np.uint64)))
+
+
+def _R():
+    import paper_2205_07426_b200 as R
+
+    return R
+
+
+def gaussian(n: int, d: int, seed: int, label: str) -> np.ndarray:
+    """n x d, column j from RandomStream(derive_key(derive_key(seed, hash(label)), j)) (gaussian_panel)."""
+    return _R().gaussian_panel(n, d, seed, label)
+
+
+def iid(n: int, d: int, seed: int) -> np.ndarray:
+    return gaussian(n, d, seed, "X")
+
+
+def mixture10(n: int, d: int, seed: int) -> np.ndarray:
+    """Config 3: 10 isotropic unit-variance Gaussians, means ~ N(0, 4I), component = next_u64() % 10."""
+    R = _R()
+    means = 2.0 * gaussian(d, 10, seed, "means")
+    comp = (stream_u64(R.derive_key(seed, R.hash_name("component")), n) % np.uint64(10)).astype(np.int64)
+    return means[:, comp].T + gaussian(n, d, seed, "noise")
+
+
+def mi_inputs(n: int, seed: int, dx: int = 16, dy: int = 8):
+    """Config 4: X ~ N(0, I_16); Y = X W + 0.5 noise with W ~ N(0,1)^{16x8}."""
+    x = gaussian(n, dx, seed, "X")
+    w = gaussian(dx, dy, seed, "W")
+    y = x @ w + 0.5 * gaussian(n, dy, seed, "noise")
+    return x, y
+
+
+def f32(x: np.ndarray) -> np.ndarray:
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    n: int
+    d: int
+    precision: str
+    alpha: float
+    method: str
+    s: int
+    m: int
+    s_q: int
+    s_g: int
+    probe_kind: str
+    note: str
+
+
+CONFIGS = {
+    "c1": Config("c1", 2000, 10, "fp64", 2.0, "int", 30, 0, 0, 30, "rademacher",
+                 "n=2000 d=10 fp64, alpha=2 Hutchinson s=30 Rademacher"),
+    "c2": Config("c2", 20000, 32, "fp32", 1.5, "chebyshev", 60, 40, 20, 40, "rademacher",
+                 "n=20000 d=32 fp32, alpha=1.5 Chebyshev[0,1] m=40, Hutch++ 20+40 Rademacher"),
+    "c3": Config("c3", 50000, 64, "fp32", 0.5, "taylor", 100, 30, 0, 100, "gaussian",
+                 "n=50000 d=64 fp32 10-mixture, alpha=0.5 Taylor m=30, Hutchinson s=100 Gaussian"),
+    "c4": Config("c4", 100000, 16, "fp32", 1.01, "chebyshev", 90, 60, 22, 46, "gaussian",
+                 "MI n=100000 d=16/8 fp32, alpha=1.01 Chebyshev[0,1] m=60, Hutch++ s=90 (reference split 22+46)"),
+}
+
+
+def sigma_for(d: int) -> float:
+    return math.sqrt(d)
