@@ -132,10 +132,16 @@ int renyi_ctx_create(int device, renyi_ctx** out);
 int renyi_ctx_destroy(renyi_ctx* ctx);
 int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc);
 int renyi_ctx_sync(renyi_ctx* ctx);
-/* CUDA-event timing of block-product launches (bench instrumentation) */
+/* CUDA-event timing of block-product launches with their algorithmic bytes and
+ * flops (SURVEY §8d accounting); bench instrumentation */
 int renyi_ctx_profile(renyi_ctx* ctx, int enable);
-int renyi_ctx_profile_read(renyi_ctx* ctx, int* launches, double* milliseconds);
+int renyi_ctx_profile_read(renyi_ctx* ctx, int* launches, double* milliseconds, double* bytes, double* flops);
 int renyi_ctx_launch_count(renyi_ctx* ctx, long* launches);
+/* host<->device bytes issued by the engine since creation */
+int renyi_ctx_io_bytes(renyi_ctx* ctx, long long* h2d, long long* d2h);
+/* CUDA-event region timer on the engine stream */
+int renyi_ctx_timer_begin(renyi_ctx* ctx);
+int renyi_ctx_timer_end(renyi_ctx* ctx, double* milliseconds);
 
 /* ---- kernel matrices (proj/include/renyi/kernel.hpp:45-56) --------------- */
 /* build_kernel(X, GaussianKernel{sigma}) — proj/src/kernel.cpp:35-72 + ops.cpp:39-47 */
@@ -145,6 +151,10 @@ int renyi_kernel_build_gaussian(renyi_ctx* ctx, const double* x, int64_t n, int6
 int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
                                       double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                       int precision, renyi_kernel** out);
+/* the same from device-resident samples (column-major, leading dimension ldx; y may be NULL) */
+int renyi_kernel_build_gaussian_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx,
+                                    double sigma, const double* d_y, int64_t dy, int64_t ldy, double sigma_y,
+                                    int precision, renyi_kernel** out);
 /* NormalizedKernel(Matrix) — kernel.hpp:33 (caller asserts the invariants) */
 int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int precision, renyi_kernel** out);
 /* hadamard_joint({a, b}) — kernel.cpp:74-101 */
@@ -192,9 +202,14 @@ int renyi_mutual_information(renyi_ctx* ctx, const renyi_kernel* a, const renyi_
 int renyi_mutual_information_samples(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
                                      double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                      const renyi_estimator_params* p, int precision, renyi_mi_estimate* out);
+int renyi_mutual_information_samples_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t dx, int64_t ldx,
+                                         double sigma_x, const double* d_y, int64_t dy, int64_t ldy, double sigma_y,
+                                         const renyi_estimator_params* p, int precision, renyi_mi_estimate* out);
 /* north star: build_kernel(X, sigma) + estimate(A, params) (cmd_entropy, renyi_cli.cpp:144-154) */
 int renyi_entropy(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
                   const renyi_estimator_params* p, int precision, renyi_entropy_estimate* out);
+int renyi_entropy_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                      const renyi_estimator_params* p, int precision, renyi_entropy_estimate* out);
 
 /* ---- host-side arithmetic (no device) ------------------------------------------ */
 void renyi_default_params(renyi_estimator_params* p);      /* EstimatorParams{} defaults */

@@ -80,7 +80,7 @@ def lib():
         h.oracle_expected_queries.restype = C.c_long
         h.oracle_expected_queries.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, C.c_int]
         h.oracle_slab_sample.restype = C.c_double
-        h.oracle_slab_sample.argtypes = [_D, _I64, _I64, C.c_double, _I64, _I64, C.c_int, C.c_int, C.c_int]
+        h.oracle_slab_sample.argtypes = [_D, _I64, _I64, C.c_double, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_int]
         h.oracle_probe_panel.argtypes = [_I64, C.c_int, C.c_uint64, C.c_char_p, C.c_int, _D]
         h.oracle_stream_gaussian.argtypes = [C.c_uint64, _I64, _D]
         h.oracle_mixture_samples.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, _D]
@@ -362,6 +362,7 @@ def set_threads(t):
     lib().oracle_set_threads(t)
 
 
-def slab_sample_seconds(x, sigma, r0, h, passes, cols_q, cols_w):
+def slab_sample_seconds(x, sigma, r0, h, sketch_cols, passes, cols_q, cols_w):
+    """Seconds for rows [r0, r0+h) of one estimate: Gram rows + sketch pass + `passes` (Q, W) passes."""
     x = _f(x)
-    return lib().oracle_slab_sample(_p(x), x.shape[0], x.shape[1], sigma, r0, h, passes, cols_q, cols_w)
+    return lib().oracle_slab_sample(_p(x), x.shape[0], x.shape[1], sigma, r0, h, sketch_cols, passes, cols_q, cols_w)

@@ -1215,11 +1215,12 @@ int oracle_mu_bound(double u, double v, double alpha, int64_t n, double* mu, dou
 
 // --- CPU-baseline sample: one row slab of the estimator's cost structure ---------
 // Builds rows [r0, r0+h) of A from X exactly as build_kernel does (gaussian_row +
-// normalisation), then runs `passes` block products of that slab with a random
-// n x s panel split into the reference's separately-applied groups (cols_q, then
-// cols_w), each as 8-column panels re-streaming the slab. Returns seconds.
-double oracle_slab_sample(const double* x, int64_t n, int64_t d, double sigma, int64_t r0, int64_t h, int passes,
-                          int cols_q, int cols_w) {
+// normalisation), runs the sketch product (sketch_cols columns), then `passes`
+// block products of that slab with a random n x s panel split into the
+// reference's separately-applied groups (cols_q, then cols_w), each as 8-column
+// panels re-streaming the slab (ops.cpp:98-107, hutchpp.cpp:33-51). Returns seconds.
+double oracle_slab_sample(const double* x, int64_t n, int64_t d, double sigma, int64_t r0, int64_t h,
+                          int sketch_cols, int passes, int cols_q, int cols_w) {
     const auto t0 = std::chrono::steady_clock::now();
     orc::Vec sq(n, 0.0);
     for (int64_t i = 0; i < n; ++i) {
@@ -1228,45 +1229,59 @@ double oracle_slab_sample(const double* x, int64_t n, int64_t d, double sigma, i
         sq[i] = s;
     }
     const double inv2 = 1.0 / (2.0 * sigma * sigma), inv_n = 1.0 / static_cast<double>(n);
-    orc::Mat slab(h, n);  // rows r0.. of A, column-major h x n
+    // rows r0.. of A (row-major slab: row ii contiguous), gaussian_row + normalisation arithmetic
+    std::vector<double> slab(static_cast<size_t>(h) * n);
 #pragma omp parallel for schedule(dynamic, 8)
     for (int64_t ii = 0; ii < h; ++ii) {
         const int64_t i = r0 + ii;
+        double* row = slab.data() + ii * n;
         for (int64_t j = 0; j < n; ++j) {
             if (j == i) {
-                slab(ii, j) = inv_n;
+                row[j] = inv_n;
                 continue;
             }
             double dt = 0.0;
             for (int64_t t = 0; t < d; ++t) dt += x[i + t * n] * x[j + t * n];
             double d2 = sq[i] + sq[j] - 2.0 * dt;
             if (d2 < 0.0) d2 = 0.0;
-            slab(ii, j) = inv_n * std::exp(-d2 * inv2);
+            row[j] = inv_n * std::exp(-d2 * inv2);
         }
     }
-    orc::Mat v(n, std::max(cols_q, cols_w));
+    const int cmax = std::max(std::max(cols_q, cols_w), sketch_cols);
+    orc::Mat v(n, cmax);
     orc::Stream st(7);
     st.fill_gaussian(v);
     double sink = 0.0;
-    for (int p = 0; p < passes; ++p) {
+    constexpr int64_t KB = 256;
+    for (int p = -1; p < passes; ++p) {
         for (int grp = 0; grp < 2; ++grp) {
-            const int cols = grp == 0 ? cols_q : cols_w;
+            const int cols = p < 0 ? (grp == 0 ? sketch_cols : 0) : (grp == 0 ? cols_q : cols_w);
             if (cols <= 0) continue;
-            orc::Mat y(h, cols);
+            std::vector<double> y(static_cast<size_t>(h) * cols, 0.0);
             const int64_t nb = (cols + 7) / 8;
+            // one task per 8-column panel (ops.cpp:98-107); each streams the whole slab once,
+            // Eigen-style: the panel's k-block is packed (L1) and reused by every row
 #pragma omp parallel for schedule(dynamic)
             for (int64_t b = 0; b < nb; ++b) {
-                const int64_t j0 = b * 8, j1 = std::min<int64_t>(cols, j0 + 8);
-                for (int64_t k = 0; k < n; ++k) {
-                    const double* ak = slab.col(k);
-                    for (int64_t j = j0; j < j1; ++j) {
-                        const double vkj = v(k, j);
-                        double* yj = y.col(j);
-                        for (int64_t i = 0; i < h; ++i) yj[i] += ak[i] * vkj;
+                const int64_t j0 = b * 8;
+                const int w = static_cast<int>(std::min<int64_t>(cols, j0 + 8) - j0);
+                double pack[KB * 8];
+                for (int64_t k0 = 0; k0 < n; k0 += KB) {
+                    const int64_t kb = std::min(KB, n - k0);
+                    for (int64_t k = 0; k < kb; ++k)
+                        for (int c = 0; c < 8; ++c) pack[k * 8 + c] = c < w ? v(k0 + k, j0 + c) : 0.0;
+                    for (int64_t ii = 0; ii < h; ++ii) {
+                        const double* a = slab.data() + ii * n + k0;
+                        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        for (int64_t k = 0; k < kb; ++k) {
+                            const double ak = a[k];
+                            for (int c = 0; c < 8; ++c) acc[c] += ak * pack[k * 8 + c];
+                        }
+                        for (int c = 0; c < w; ++c) y[(j0 + c) * h + ii] += acc[c];
                     }
                 }
             }
-            sink += y.d[0];
+            sink += y[0];
         }
     }
     const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -146,12 +146,20 @@ SIGNATURES = {
     "renyi_ctx_set_tuning": (C.c_int, [_P, C.c_int, C.c_int]),
     "renyi_ctx_sync": (C.c_int, [_P]),
     "renyi_ctx_profile": (C.c_int, [_P, C.c_int]),
-    "renyi_ctx_profile_read": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+    "renyi_ctx_profile_read": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
+    "renyi_ctx_io_bytes": (C.c_int, [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "renyi_ctx_timer_begin": (C.c_int, [_P]),
+    "renyi_ctx_timer_end": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "renyi_ctx_launch_count": (C.c_int, [_P, C.POINTER(C.c_long)]),
     "renyi_kernel_build_gaussian": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)]),
     "renyi_kernel_build_gaussian_joint": (
         C.c_int,
         [_P, _D, _I64, _I64, _I64, C.c_double, _D, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)],
+    ),
+    "renyi_kernel_build_gaussian_dev": (
+        C.c_int,
+        [_P, C.c_void_p, _I64, _I64, _I64, C.c_double, C.c_void_p, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)],
     ),
     "renyi_kernel_from_matrix": (C.c_int, [_P, _D, _I64, C.c_int, C.POINTER(_P)]),
     "renyi_kernel_hadamard_joint": (C.c_int, [_P, _P, _P, C.POINTER(_P)]),
@@ -180,6 +188,16 @@ SIGNATURES = {
         C.c_int,
         [_P, _D, _I64, _I64, _I64, C.c_double, _D, _I64, _I64, C.c_double, C.POINTER(EstimatorParamsC), C.c_int,
          C.POINTER(MiEstimateC)],
+    ),
+    "renyi_mutual_information_samples_dev": (
+        C.c_int,
+        [_P, C.c_void_p, _I64, _I64, _I64, C.c_double, C.c_void_p, _I64, _I64, C.c_double,
+         C.POINTER(EstimatorParamsC), C.c_int, C.POINTER(MiEstimateC)],
+    ),
+    "renyi_entropy_dev": (
+        C.c_int,
+        [_P, C.c_void_p, _I64, _I64, _I64, C.c_double, C.POINTER(EstimatorParamsC), C.c_int,
+         C.POINTER(EntropyEstimateC)],
     ),
     "renyi_entropy": (
         C.c_int,

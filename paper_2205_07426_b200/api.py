@@ -61,10 +61,24 @@ class Context:
         check(L.lib().renyi_ctx_profile(self._h, 1 if enable else 0))
 
     def profile_read(self):
+        """(launches, device ms, algorithmic bytes, flops) of block products since profile(True)."""
         n = C.c_int()
+        ms, b, f = C.c_double(), C.c_double(), C.c_double()
+        check(L.lib().renyi_ctx_profile_read(self._h, C.byref(n), C.byref(ms), C.byref(b), C.byref(f)))
+        return n.value, ms.value, b.value, f.value
+
+    def io_bytes(self):
+        h, d = C.c_longlong(), C.c_longlong()
+        check(L.lib().renyi_ctx_io_bytes(self._h, C.byref(h), C.byref(d)))
+        return h.value, d.value
+
+    def timer_begin(self) -> None:
+        check(L.lib().renyi_ctx_timer_begin(self._h))
+
+    def timer_end(self) -> float:
         ms = C.c_double()
-        check(L.lib().renyi_ctx_profile_read(self._h, C.byref(n), C.byref(ms)))
-        return n.value, ms.value
+        check(L.lib().renyi_ctx_timer_end(self._h, C.byref(ms)))
+        return ms.value
 
     def launch_count(self) -> int:
         n = C.c_long()
@@ -636,6 +650,37 @@ def mutual_information_samples(x, sx: GaussianKernel, y, sy: GaussianKernel, par
                                                    sx.sigma, _dptr(ya), ya.shape[1], ya.shape[0], sy.sigma,
                                                    C.byref(params._c()), PRECISIONS[precision], C.byref(out)))
     return MutualInformation(out.value, out.vars_entropy, out.target_entropy, out.joint_entropy)
+
+
+def mutual_information_samples_dev(d_x: int, n: int, dx: int, ldx: int, sx: GaussianKernel, d_y: int, dy: int,
+                                   ldy: int, sy: GaussianKernel, params: EstimatorParams, precision="fp32",
+                                   ctx: Optional[Context] = None) -> MutualInformation:
+    """MI from device-resident column-major samples (raw device pointers, e.g. torch data_ptr())."""
+    ctx = ctx or default_context()
+    out = L.MiEstimateC()
+    check(L.lib().renyi_mutual_information_samples_dev(ctx.handle, C.c_void_p(d_x), n, dx, ldx, sx.sigma,
+                                                       C.c_void_p(d_y), dy, ldy, sy.sigma, C.byref(params._c()),
+                                                       PRECISIONS[precision], C.byref(out)))
+    return MutualInformation(out.value, out.vars_entropy, out.target_entropy, out.joint_entropy)
+
+
+def entropy_dev(d_x: int, n: int, d: int, ldx: int, sigma: float, params: EstimatorParams, precision="fp32",
+                ctx: Optional[Context] = None) -> EntropyEstimate:
+    """North-star composition from device-resident column-major samples."""
+    ctx = ctx or default_context()
+    out = L.EntropyEstimateC()
+    check(L.lib().renyi_entropy_dev(ctx.handle, C.c_void_p(d_x), n, d, ldx, sigma, C.byref(params._c()),
+                                    PRECISIONS[precision], C.byref(out)))
+    return EntropyEstimate._from(out)
+
+
+def build_kernel_dev(d_x: int, n: int, d: int, ldx: int, spec: GaussianKernel, precision="fp32",
+                     ctx: Optional[Context] = None) -> NormalizedKernel:
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    check(L.lib().renyi_kernel_build_gaussian_dev(ctx.handle, C.c_void_p(d_x), n, d, ldx, spec.sigma, None, 0, 0,
+                                                  1.0, PRECISIONS[precision], C.byref(h)))
+    return NormalizedKernel(h, ctx, PRECISIONS[precision])
 
 
 def entropy(x, sigma: float, params: EstimatorParams, precision="fp32",

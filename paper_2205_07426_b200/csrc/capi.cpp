@@ -172,12 +172,38 @@ int renyi_ctx_profile(renyi_ctx* ctx, int enable) {
     });
 }
 
-int renyi_ctx_profile_read(renyi_ctx* ctx, int* launches, double* ms) {
+int renyi_ctx_profile_read(renyi_ctx* ctx, int* launches, double* ms, double* bytes, double* flops) {
     return guarded([&] {
         need(ctx, "ctx");
         need(launches, "launches");
         need(ms, "milliseconds");
-        ctx->ctx.prof_read(launches, ms);
+        double b = 0.0, f = 0.0;
+        ctx->ctx.prof_read(launches, ms, &b, &f);
+        if (bytes) *bytes = b;
+        if (flops) *flops = f;
+    });
+}
+
+int renyi_ctx_io_bytes(renyi_ctx* ctx, long long* h2d, long long* d2h) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        if (h2d) *h2d = ctx->ctx.h2d_bytes;
+        if (d2h) *d2h = ctx->ctx.d2h_bytes;
+    });
+}
+
+int renyi_ctx_timer_begin(renyi_ctx* ctx) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        ctx->ctx.timer_begin();
+    });
+}
+
+int renyi_ctx_timer_end(renyi_ctx* ctx, double* ms) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        need(ms, "milliseconds");
+        *ms = ctx->ctx.timer_end_ms();
     });
 }
 
@@ -214,6 +240,24 @@ int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n
         auto* k = new renyi_kernel;
         try {
             k->k = rb::build_gaussian(ctx->ctx, x, n, dx, ldx, sigma_x, precision, y, dy, ldy, sigma_y);
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int renyi_kernel_build_gaussian_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx,
+                                    double sigma, const double* d_y, int64_t dy, int64_t ldy, double sigma_y,
+                                    int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(d_x, "samples"), need(out, "out");
+        check_precision(precision);
+        auto* k = new renyi_kernel;
+        try {
+            k->k = rb::build_gaussian_dev(ctx->ctx, d_x, n, d, ldx, sigma, precision, d_y, dy, ldy, sigma_y);
+            ctx->ctx.sync();
         } catch (...) {
             delete k;
             throw;
@@ -404,6 +448,29 @@ int renyi_mutual_information_samples(renyi_ctx* ctx, const double* x, int64_t n,
                                                                  sigma_y, to_params(p), precision);
         out->value = mi.value, out->vars_entropy = mi.vars_entropy;
         out->target_entropy = mi.target_entropy, out->joint_entropy = mi.joint_entropy;
+    });
+}
+
+int renyi_mutual_information_samples_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t dx, int64_t ldx,
+                                         double sigma_x, const double* d_y, int64_t dy, int64_t ldy, double sigma_y,
+                                         const renyi_estimator_params* p, int precision, renyi_mi_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(d_x, "samples"), need(d_y, "target samples"), need(out, "out");
+        check_precision(precision);
+        const rb::MutualInfo mi = rb::mutual_information_samples_dev(ctx->ctx, d_x, n, dx, ldx, sigma_x, d_y, dy, ldy,
+                                                                     sigma_y, to_params(p), precision);
+        out->value = mi.value, out->vars_entropy = mi.vars_entropy;
+        out->target_entropy = mi.target_entropy, out->joint_entropy = mi.joint_entropy;
+    });
+}
+
+int renyi_entropy_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                      const renyi_estimator_params* p, int precision, renyi_entropy_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(d_x, "samples"), need(out, "out");
+        check_precision(precision);
+        rb::KernelPtr k = rb::build_gaussian_dev(ctx->ctx, d_x, n, d, ldx, sigma, precision);
+        from_entropy(rb::estimate(ctx->ctx, *k, to_params(p)), out);
     });
 }
 

@@ -20,6 +20,29 @@ void cuda_check(cudaError_t e, const char* what) {
     fail(kCudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+void h2d(Context& ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx.stream()), "host->device copy");
+    ctx.h2d_bytes += static_cast<long long>(bytes);
+}
+void d2h(Context& ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx.stream()), "device->host copy");
+    ctx.d2h_bytes += static_cast<long long>(bytes);
+}
+void h2d_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height) {
+    if (width == 0 || height == 0) return;
+    cuda_check(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, ctx.stream()),
+               "host->device copy");
+    ctx.h2d_bytes += static_cast<long long>(width * height);
+}
+void d2h_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height) {
+    if (width == 0 || height == 0) return;
+    cuda_check(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, ctx.stream()),
+               "device->host copy");
+    ctx.d2h_bytes += static_cast<long long>(width * height);
+}
+
 // ---------------------------------------------------------------- DevBuf
 DevBuf::~DevBuf() { release(); }
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
@@ -63,6 +86,8 @@ Context::Context(int device) : device_(device) {
 
 Context::~Context() {
     cudaSetDevice(device_);
+    if (t0_) cudaEventDestroy(t0_);
+    if (t1_) cudaEventDestroy(t1_);
     for (auto& e : events_) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -75,6 +100,27 @@ void Context::sync() { cuda_check(cudaStreamSynchronize(stream_), "stream synchr
 void Context::prof_enable(bool on) {
     prof_ = on;
     prof_used_ = 0;
+    prof_bytes_ = prof_flops_ = 0.0;
+}
+void Context::prof_account(double bytes, double flops) {
+    if (!prof_) return;
+    prof_bytes_ += bytes;
+    prof_flops_ += flops;
+}
+void Context::timer_begin() {
+    if (!t0_) {
+        cuda_check(cudaEventCreate(&t0_), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&t1_), "cudaEventCreate");
+    }
+    cuda_check(cudaEventRecord(t0_, stream_), "cudaEventRecord");
+}
+double Context::timer_end_ms() {
+    if (!t0_) fail(kInvalidArgument, "timer_end without timer_begin");
+    cuda_check(cudaEventRecord(t1_, stream_), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(t1_), "cudaEventSynchronize");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, t0_, t1_), "cudaEventElapsedTime");
+    return ms;
 }
 void Context::prof_begin() {
     if (!prof_) return;
@@ -91,8 +137,11 @@ void Context::prof_end() {
     cuda_check(cudaEventRecord(events_[prof_used_].second, stream_), "cudaEventRecord");
     ++prof_used_;
 }
-void Context::prof_read(int* n, double* ms) {
+void Context::prof_read(int* n, double* ms, double* bytes, double* flops) {
     sync();
+    *bytes = prof_bytes_;
+    *flops = prof_flops_;
+    prof_bytes_ = prof_flops_ = 0.0;
     double total = 0.0;
     for (size_t i = 0; i < prof_used_; ++i) {
         float t = 0.f;
@@ -141,21 +190,50 @@ void shard_rows(Context& ctx, int64_t n, int64_t* row0, int64_t* rows) {
 // ---------------------------------------------------------------- kernel matrices
 KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
                          const double* y, int64_t dy, int64_t ldy, double sigma_y) {
-    // validate_samples (proj/src/kernel.cpp:25-29) + sigma check (kernel.cpp:42)
+    // validate_samples (proj/src/kernel.cpp:25-29) on the host copy, then upload column-major as given
+    if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
+    if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
+    if (ldx < n || (y && ldy < n)) fail(kInvalidArgument, "leading dimension smaller than the sample count");
+    double mx = 0.0, my = 0.0;
+    check_finite(x, n, d, ldx, &mx);
+    if (y) check_finite(y, n, dy, ldy, &my);
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    DevBuf xs;
+    const int64_t dt = d + (y ? dy : 0);
+    xs.alloc(static_cast<size_t>(n) * dt * sizeof(double));
+    h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), d);
+    if (y) h2d_2d(ctx, xs.as<double>() + n * d, n * sizeof(double), y, ldy * sizeof(double), n * sizeof(double), dy);
+    KernelPtr k = build_gaussian_dev(ctx, xs.as<double>(), n, d, n, sigma, prec, y ? xs.as<double>() + n * d : nullptr,
+                                     dy, n, sigma_y);
+    ctx.sync();  // xs goes out of scope
+    return k;
+}
+
+KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
+                             const double* y, int64_t dy, int64_t ldy, double sigma_y) {
+    // build_kernel(X, GaussianKernel{sigma}) (proj/src/kernel.cpp:35-72), samples resident on the device
     if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
     if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
     if (!(sigma > 0.0)) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
-    double mx = 0.0, my = 0.0;
-    check_finite(x, n, d, ldx, &mx);
     if (y) {
         if (dy < 1) fail(kInvalidArgument, "second variable needs at least one feature");
         if (!(sigma_y > 0.0)) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
-        check_finite(y, n, dy, ldy, &my);
     }
-    if (prec == kF32 && std::max(mx, my) > 1e18)
-        fail(kNonFinite, "sample values exceed the fp32 range of the fp32 configuration");
-
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    // finiteness (kernel.cpp:27) and, for fp32, representability of the squared norms
+    ctx.small.ensure(4 * sizeof(unsigned));
+    unsigned* flags = ctx.small.as<unsigned>();
+    cuda_check(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned), ctx.stream()), "memset");
+    launched(ctx, launch_check_samples(x, n, static_cast<int>(d), 1, ldx, flags, ctx.stream()), "check_samples");
+    if (y) launched(ctx, launch_check_samples(y, n, static_cast<int>(dy), 1, ldy, flags, ctx.stream()), "check_samples");
+    unsigned hf[2];
+    d2h(ctx, hf, flags, sizeof(hf));
+    ctx.sync();
+    if (hf[0]) fail(kNonFinite, "sample matrix contains non-finite values");
+    float mx;
+    std::memcpy(&mx, &hf[1], sizeof(float));
+    if (prec == kF32 && mx > 1e18f) fail(kNonFinite, "sample values exceed the fp32 range of the fp32 configuration");
+
     auto k = std::make_unique<KernelMatrix>();
     k->n = n;
     k->prec = prec;
@@ -164,30 +242,14 @@ KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, in
     const double inv_n = 1.0 / static_cast<double>(n);
     k->normalized = true;
     k->a_norm = 1.0;
-
-    // samples, row-major on the device
-    const int64_t dtot = d + (y ? dy : 0);
-    std::vector<double> xr(static_cast<size_t>(n) * dtot);
-    for (int64_t i = 0; i < n; ++i) {
-        for (int64_t j = 0; j < d; ++j) xr[i * d + j] = x[i + j * ldx];
-    }
-    double* yr_host = nullptr;
-    if (y) {
-        yr_host = xr.data() + n * d;
-        for (int64_t i = 0; i < n; ++i)
-            for (int64_t j = 0; j < dy; ++j) yr_host[i * dy + j] = y[i + j * ldy];
-    }
-    DevBuf xs;
-    xs.alloc(xr.size() * sizeof(double));
-    cuda_check(cudaMemcpyAsync(xs.as<double>(), xr.data(), xr.size() * sizeof(double), cudaMemcpyHostToDevice,
-                               ctx.stream()),
-               "upload samples");
     GramArgs g;
-    g.x = xs.as<double>();
+    g.x = x;
     g.dx = static_cast<int>(d);
+    g.x_rs = 1, g.x_cs = ldx;
     g.inv_two_sigma2_x = 1.0 / (2.0 * sigma * sigma);
-    g.y = y ? xs.as<double>() + n * d : nullptr;
+    g.y = y;
     g.dy = static_cast<int>(dy);
+    g.y_rs = 1, g.y_cs = ldy;
     g.inv_two_sigma2_y = y ? 1.0 / (2.0 * sigma_y * sigma_y) : 0.0;
     g.n = n;
     g.row0 = k->row0;
@@ -206,7 +268,6 @@ KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, in
         k->unscale = 1.0;
         launched(ctx, launch_gram_f64(g, k->a64.as<double>(), ctx.stream()), "gram_f64");
     }
-    ctx.sync();  // xs goes out of scope
     return k;
 }
 
@@ -236,9 +297,7 @@ KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
     k->a_norm = norm;
     DevBuf up;
     up.alloc(rm.size() * sizeof(double));
-    cuda_check(cudaMemcpyAsync(up.as<double>(), rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice,
-                               ctx.stream()),
-               "upload matrix");
+    h2d(ctx, up.as<double>(), rm.data(), rm.size() * sizeof(double));
     if (prec == kF32) {
         int e = 0;
         if (mx > 0.0) {
@@ -315,14 +374,11 @@ void download(Context& ctx, const KernelMatrix& k, double* out) {
                  launch_split_to_f64(k.hi.as<__half>(), k.lo.as<__half>(), k.rows, k.n, k.ld, k.unscale,
                                      tmp.as<double>(), k.n, ctx.stream()),
                  "split_to_f64");
-        cuda_check(cudaMemcpyAsync(rm.data(), tmp.as<double>(), rm.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                                   ctx.stream()),
-                   "download");
+        d2h(ctx, rm.data(), tmp.as<double>(), rm.size() * sizeof(double));
         ctx.sync();
     } else {
-        cuda_check(cudaMemcpy2DAsync(rm.data(), k.n * sizeof(double), k.a64.as<double>(), k.ld * sizeof(double),
-                                     k.n * sizeof(double), k.rows, cudaMemcpyDeviceToHost, ctx.stream()),
-                   "download");
+        d2h_2d(ctx, rm.data(), k.n * sizeof(double), k.a64.as<double>(), k.ld * sizeof(double), k.n * sizeof(double),
+               k.rows);
         ctx.sync();
     }
     for (int64_t i = 0; i < k.rows; ++i)
@@ -393,6 +449,8 @@ public:
             ctx_.prof_begin();
             launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()), "block_av_tc");
             ctx_.prof_end();
+            // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
+            ctx_.prof_account(4.0 * rows_ * k_.n + 4.0 * k_.n * s_ + 4.0 * rows_ * s_, 2.0 * rows_ * k_.n * s_);
             EpiArgs<float, float> e{};
             e.partial = ctx_.partial.as<float>();
             e.npad = npad_;
@@ -420,6 +478,7 @@ public:
                                          ctx_.partial.as<double>(), ctx_.stream()),
                      "block_av_f64");
             ctx_.prof_end();
+            ctx_.prof_account(8.0 * rows_ * k_.n + 8.0 * k_.n * s_ + 8.0 * rows_ * s_, 2.0 * rows_ * k_.n * s_);
             EpiArgs<double, double> e{};
             e.partial = ctx_.partial.as<double>();
             e.npad = npad_;
@@ -450,9 +509,7 @@ public:
                                      ctx_.red.as<double>(), ctx_.stream()),
                  "reduce_stats");
         std::vector<double> out(static_cast<size_t>(np) * 3 * s);
-        cuda_check(cudaMemcpyAsync(out.data(), ctx_.red.as<double>(), out.size() * sizeof(double),
-                                   cudaMemcpyDeviceToHost, ctx_.stream()),
-                   "download stats");
+        d2h(ctx_, out.data(), ctx_.red.as<double>(), out.size() * sizeof(double));
         ctx_.sync();
         return out;
     }
@@ -516,15 +573,11 @@ std::vector<std::array<double, 3>> schedule(const MatFun& f) {
 // upload a host column-major panel (n x s) into a device fp64 buffer [s][ld]
 void upload_panel(Context& ctx, DevBuf& dst, const double* host, int64_t n, int s, int64_t ld) {
     dst.ensure(static_cast<size_t>(s) * ld * sizeof(double));
-    cuda_check(cudaMemcpy2DAsync(dst.as<double>(), ld * sizeof(double), host, n * sizeof(double),
-                                 n * sizeof(double), s, cudaMemcpyHostToDevice, ctx.stream()),
-               "upload panel");
+    h2d_2d(ctx, dst.as<double>(), ld * sizeof(double), host, n * sizeof(double), n * sizeof(double), s);
 }
 
 void download_panel(Context& ctx, const double* dev, int64_t ld, int64_t n, int s, double* host) {
-    cuda_check(cudaMemcpy2DAsync(host, n * sizeof(double), dev, ld * sizeof(double), n * sizeof(double), s,
-                                 cudaMemcpyDeviceToHost, ctx.stream()),
-               "download panel");
+    d2h_2d(ctx, host, n * sizeof(double), dev, ld * sizeof(double), n * sizeof(double), s);
     ctx.sync();
 }
 
@@ -692,8 +745,7 @@ void make_probes(Context& ctx, DevBuf& dst, int64_t n, int cols, int64_t ld, con
                               ctx.probe_err.as<int>(), ctx.stream()),
              "rng_panel");
     int err = 0;
-    cuda_check(cudaMemcpyAsync(&err, ctx.probe_err.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()),
-               "probe flag");
+    d2h(ctx, &err, ctx.probe_err.as<int>(), sizeof(int));
     ctx.sync();
     if (err) fail(kInternal, "probe stream hit the 2^-53 Box-Muller redraw; pass the probes explicitly");
 }
@@ -714,9 +766,7 @@ std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx,
                                    ctx.stream()),
                  "panel_gram");
     }
-    cuda_check(cudaMemcpyAsync(out.data(), ctx.small.as<double>(), out.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                               ctx.stream()),
-               "download gram");
+    d2h(ctx, out.data(), ctx.small.as<double>(), out.size() * sizeof(double));
     ctx.sync();
     return out;
 }
@@ -726,9 +776,7 @@ void update(Context& ctx, double beta, const double* g, int64_t ldg, const doubl
             const std::vector<double>& c, int q, int64_t rows, double* w, int64_t ldw) {
     DevBuf cd;
     cd.alloc(c.size() * sizeof(double));
-    cuda_check(cudaMemcpyAsync(cd.as<double>(), c.data(), c.size() * sizeof(double), cudaMemcpyHostToDevice,
-                               ctx.stream()),
-               "upload coefficients");
+    h2d(ctx, cd.as<double>(), c.data(), c.size() * sizeof(double));
     // smem limit: split q
     const int qb_max = std::max(1, (48 * 1024 / 8) / std::max(p, 1));
     for (int b0 = 0; b0 < q; b0 += qb_max) {
@@ -1016,17 +1064,38 @@ MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelM
 MutualInfo mutual_information_samples(Context& ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
                                       double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                       const EstParams& p, int prec) {
+    // host buffers: validate, upload X and Y once (column-major as given), then the device path
+    if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
+    if (dx < 1 || dy < 1) fail(kInvalidArgument, "samples need at least one feature");
+    if (ldx < n || ldy < n) fail(kInvalidArgument, "leading dimension smaller than the sample count");
+    double mx = 0.0;
+    check_finite(x, n, dx, ldx, &mx);
+    check_finite(y, n, dy, ldy, &mx);
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    DevBuf xs;
+    xs.alloc(static_cast<size_t>(n) * (dx + dy) * sizeof(double));
+    h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), dx);
+    h2d_2d(ctx, xs.as<double>() + n * dx, n * sizeof(double), y, ldy * sizeof(double), n * sizeof(double), dy);
+    MutualInfo mi = mutual_information_samples_dev(ctx, xs.as<double>(), n, dx, n, sigma_x, xs.as<double>() + n * dx,
+                                                   dy, n, sigma_y, p, prec);
+    ctx.sync();
+    return mi;
+}
+
+MutualInfo mutual_information_samples_dev(Context& ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
+                                          double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
+                                          const EstParams& p, int prec) {
     MutualInfo mi;
     {
-        KernelPtr a = build_gaussian(ctx, x, n, dx, ldx, sigma_x, prec);
+        KernelPtr a = build_gaussian_dev(ctx, x, n, dx, ldx, sigma_x, prec);
         mi.vars_entropy = estimate(ctx, *a, with_seed(p, "term:vars")).entropy;
     }
     {
-        KernelPtr b = build_gaussian(ctx, y, n, dy, ldy, sigma_y, prec);
+        KernelPtr b = build_gaussian_dev(ctx, y, n, dy, ldy, sigma_y, prec);
         mi.target_entropy = estimate(ctx, *b, with_seed(p, "term:target")).entropy;
     }
     {
-        KernelPtr j = build_gaussian(ctx, x, n, dx, ldx, sigma_x, prec, y, dy, ldy, sigma_y);
+        KernelPtr j = build_gaussian_dev(ctx, x, n, dx, ldx, sigma_x, prec, y, dy, ldy, sigma_y);
         mi.joint_entropy = estimate(ctx, *j, with_seed(p, "term:joint")).entropy;
     }
     mi.value = mi.vars_entropy + mi.target_entropy - mi.joint_entropy;

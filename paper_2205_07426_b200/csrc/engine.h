@@ -72,9 +72,15 @@ public:
     void prof_enable(bool on);
     void prof_begin();
     void prof_end();
-    // synchronizes; returns launches and summed device milliseconds since enable
-    void prof_read(int* launches, double* ms);
+    void prof_account(double bytes, double flops);
+    // synchronizes; returns launches, summed device milliseconds, algorithmic bytes and flops since enable
+    void prof_read(int* launches, double* ms, double* bytes, double* flops);
     long launches = 0;  // kernels launched by the engine (all kinds)
+    long long h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic issued by the engine
+
+    // region timer (CUDA events on the engine stream)
+    void timer_begin();
+    double timer_end_ms();  // synchronizes
 
     Exchange* exchange = nullptr;
 
@@ -89,6 +95,8 @@ private:
     bool prof_ = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;
     size_t prof_used_ = 0;
+    double prof_bytes_ = 0.0, prof_flops_ = 0.0;
+    cudaEvent_t t0_ = nullptr, t1_ = nullptr;
 };
 
 struct KernelMatrix {
@@ -109,6 +117,10 @@ using KernelPtr = std::unique_ptr<KernelMatrix>;
 // x: host column-major n x d (Eigen layout of the reference), ld >= n.
 KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
                          const double* y = nullptr, int64_t dy = 0, int64_t ldy = 0, double sigma_y = 1.0);
+// device-resident samples (column-major, leading dimension ld)
+KernelPtr build_gaussian_dev(Context& ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                             int prec, const double* d_y = nullptr, int64_t dy = 0, int64_t ldy = 0,
+                             double sigma_y = 1.0);
 KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec);
 KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix& b);
 void download(Context& ctx, const KernelMatrix& k, double* out_colmajor);
@@ -197,6 +209,15 @@ MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelM
 MutualInfo mutual_information_samples(Context& ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
                                       double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                       const EstParams& p, int prec);
+MutualInfo mutual_information_samples_dev(Context& ctx, const double* d_x, int64_t n, int64_t dx, int64_t ldx,
+                                          double sigma_x, const double* d_y, int64_t dy, int64_t ldy,
+                                          double sigma_y, const EstParams& p, int prec);
 EstParams with_seed(const EstParams& p, const char* term);
+
+// counted host<->device copies on the engine stream
+void h2d(Context& ctx, void* dst, const void* src, size_t bytes);
+void d2h(Context& ctx, void* dst, const void* src, size_t bytes);
+void h2d_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height);
+void d2h_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height);
 
 }  // namespace rb

@@ -136,11 +136,13 @@ cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t r
 // Optional second sample set (Y) gives the normalised Hadamard joint
 // n * A^X_ij * A^Y_ij with diag 1/n.
 struct GramArgs {
-    const double* x;  // samples, row-major n x dx (fp64; fp32 configs pass fp32-rounded values)
+    const double* x;  // samples n x dx (fp64; fp32 configs pass fp32-rounded values), element (i,k) at x[i*x_rs + k*x_cs]
     int dx;
+    int64_t x_rs, x_cs;
     double inv_two_sigma2_x;
     const double* y;  // optional second variable (nullptr)
     int dy;
+    int64_t y_rs, y_cs;
     double inv_two_sigma2_y;
     int64_t n;        // samples (= columns of A)
     int64_t row0;     // first row of this shard
@@ -161,6 +163,9 @@ cudaError_t launch_hadamard_split(const __half* ahi, const __half* alo, const __
                                   double diag_value, __half* chi, __half* clo, cudaStream_t stream);
 cudaError_t launch_hadamard_f64(const double* a, const double* b, int64_t rows, int64_t cols, int64_t ld,
                                 int64_t row0, double n, double* c, cudaStream_t stream);
+// samples check: flag[0] |= non-finite, flag[1] = float bits of max |x| (atomic max)
+cudaError_t launch_check_samples(const double* x, int64_t n, int d, int64_t rs, int64_t cs, unsigned* flags,
+                                 cudaStream_t stream);
 // split planes -> fp64 (A = (hi+lo) * unscale)
 cudaError_t launch_split_to_f64(const __half* hi, const __half* lo, int64_t rows, int64_t cols, int64_t ld,
                                 double unscale, double* out, int64_t ldo, cudaStream_t stream);

@@ -14,6 +14,8 @@
 // stores fl(1/n)·K in fp64. Both are exactly symmetric (the formula is).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -28,19 +30,19 @@ constexpr int TKd = 32; // feature chunk
 template <typename T>
 struct GramTile {
     // accumulates dot products and squared norms of one 64x64 tile over a feature block
-    __device__ static void accumulate(const double* __restrict__ x, int d, int64_t n, int64_t row0, int64_t col0,
-                                      T (&dot)[4][4], T (&sqr)[4], T (&sqc)[4], T (*xr)[TM + 1],
-                                      T (*xc)[TN + 4]) {
+    __device__ static void accumulate(const double* __restrict__ x, int d, int64_t rs, int64_t cs, int64_t n,
+                                      int64_t row0, int64_t col0, T (&dot)[4][4], T (&sqr)[4], T (&sqc)[4],
+                                      T (*xr)[TM + 1], T (*xc)[TN + 4]) {
         const int tid = threadIdx.x;
         const int tx = tid % 16, ty = tid / 16;
         for (int k0 = 0; k0 < d; k0 += TKd) {
             const int kc = min(TKd, d - k0);
             for (int idx = tid; idx < TM * TKd; idx += blockDim.x) {
-                const int rr = idx / TKd, kk = idx % TKd;
+                const int rr = idx % TM, kk = idx / TM;  // consecutive threads: consecutive samples
                 const int64_t gr = row0 + rr;
-                xr[kk][rr] = (kk < kc && gr < n) ? static_cast<T>(x[gr * d + k0 + kk]) : T(0);
+                xr[kk][rr] = (kk < kc && gr < n) ? static_cast<T>(x[gr * rs + (k0 + kk) * cs]) : T(0);
                 const int64_t gc = col0 + rr;
-                xc[kk][rr] = (kk < kc && gc < n) ? static_cast<T>(x[gc * d + k0 + kk]) : T(0);
+                xc[kk][rr] = (kk < kc && gc < n) ? static_cast<T>(x[gc * rs + (k0 + kk) * cs]) : T(0);
             }
             __syncthreads();
             for (int kk = 0; kk < kc; ++kk) {
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g, __half* __restric
 #pragma unroll
         for (int v = 0; v < 4; ++v) dot[u][v] = T(0);
     }
-    GramTile<T>::accumulate(g.x, g.dx, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+    GramTile<T>::accumulate(g.x, g.dx, g.x_rs, g.x_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
     const T ax = static_cast<T>(g.inv_two_sigma2_x);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g, __half* __restric
 #pragma unroll
             for (int v = 0; v < 4; ++v) dot[u][v] = T(0);
         }
-        GramTile<T>::accumulate(g.y, g.dy, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+        GramTile<T>::accumulate(g.y, g.dy, g.y_rs, g.y_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
         const T ay = static_cast<T>(g.inv_two_sigma2_y);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -230,6 +232,26 @@ __global__ void hadamard_f64_kernel(const double* __restrict__ a, const double* 
     }
 }
 
+__global__ void check_samples_kernel(const double* __restrict__ x, int64_t n, int d, int64_t rs, int64_t cs,
+                                     unsigned* flags) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = n * d;
+    float mx = 0.f;
+    bool bad = false;
+    for (int64_t e = t; e < total; e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e % n, k = e / n;
+        const double v = x[i * rs + k * cs];
+        if (!isfinite(v)) bad = true;
+        else mx = fmaxf(mx, static_cast<float>(fabs(v)));
+    }
+    mx = warp_max(mx);
+    const unsigned b = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+        if (b) atomicOr(flags, 1u);
+        atomicMax(flags + 1, __float_as_uint(mx));
+    }
+}
+
 inline dim3 row_grid(int64_t rows, int64_t cols) {
     const int64_t bx = (cols + 255) / 256;
     return dim3(static_cast<unsigned>(bx > 64 ? 64 : bx), static_cast<unsigned>(rows));
@@ -249,6 +271,14 @@ cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStr
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream) {
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
     gram_kernel<double, false><<<grid, 256, 0, stream>>>(g, nullptr, nullptr, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_samples(const double* x, int64_t n, int d, int64_t rs, int64_t cs, unsigned* flags,
+                                 cudaStream_t stream) {
+    const int64_t total = n * d;
+    const int64_t blocks = std::min<int64_t>(1184, (total + 255) / 256);
+    check_samples_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), 256, 0, stream>>>(x, n, d, rs, cs, flags);
     return cudaGetLastError();
 }
 
