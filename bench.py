@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--seed", type=int, default=2205)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--operand", default="split", choices=["split", "fast"],
+                   help="iterate operand of the block product: fp16 hi+lo (split) or hi only (fast)")
+    p.add_argument("--kc", type=int, default=16, help="k tiles (x32 columns) per TMEM accumulation chunk")
     return p.parse_args()
 
 
@@ -216,6 +219,8 @@ def run_ours(args):
     params = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60, seed=args.seed + rank,
                                bounds=R.SpectrumBounds(u=0.0, v=1.0))
     ctx = R.Context(local)
+    ctx.set_tuning(0, args.kc)
+    ctx.set_operand_mode(args.operand)
     d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()  # (dx, n) row-major == column-major n x dx
     d_y = torch.from_numpy(np.ascontiguousarray(y.T)).cuda()
     torch.cuda.synchronize()
@@ -307,12 +312,14 @@ def run_ours(args):
         "value": value, "unit": "estimates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32",
-        "dtype_note": "A stored as an fp16 hi/lo split of A*n*2^14 (4 B/entry, 22-bit significand), "
-                      "tcgen05 fp32 accumulate drained every 1024 columns, fp32 recurrence state, fp64 trace partials",
+        "dtype_note": ("A stored as an fp16 hi/lo split of A*n*2^14 (4 B/entry, 22-bit significand); iterate "
+                       + ("fp16 hi+lo (3 tcgen05 products)" if args.operand == "split" else "fp16 hi (2 products)")
+                       + f"; fp32 TMEM accumulate drained every {32 * args.kc} columns; fp32 recurrence state; "
+                         "fp64 trace partials"),
         "data": "synthetic: X~N(0,1) 100000x16, W~N(0,1) 16x8, Y=XW+0.5N(0,1), reference RNG, fp32-rounded",
         "config": {"workload": "c4: MI n=100000 dx=16 dy=8 sigma=sqrt(d) alpha=1.01 Chebyshev[0,1] m=60 "
                                "Hutch++ s=90 (reference split 22+46), Gaussian probes drawn on device",
-                   "n": n, "estimates_per_step": 3,
+                   "n": n, "estimates_per_step": 3, "operand": args.operand, "kc": args.kc,
                    "l2": "inputs larger than L2: each A is 40 GB (n^2 x 4 B) vs 126 MB L2",
                    "parallelism": f"replicas x{world} (one independent MI estimate per rank, no collective)"},
         "roofline": roofline,

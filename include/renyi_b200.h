@@ -46,6 +46,10 @@ enum {
 
 /* storage/compute precision of a device kernel matrix */
 enum { RENYI_F64 = 0, RENYI_F32 = 1 };
+/* fp32 configurations: iterate operand of the block product. SPLIT (default) keeps V
+ * as an fp16 hi+lo pair (3 tensor-core products, ~fp32 accuracy); FAST rounds V to
+ * one fp16 plane (2 products) — see DESIGN.md for the measured trace error. */
+enum { RENYI_OPERAND_SPLIT = 0, RENYI_OPERAND_FAST = 1 };
 /* probe distributions */
 enum { RENYI_PROBE_GAUSSIAN = 0, RENYI_PROBE_RADEMACHER = 1 };
 /* estimator methods (renyi::Method, proj/include/renyi/entropy.hpp:12) */
@@ -131,7 +135,10 @@ int renyi_status_is_usage(int status); /* renyi::error::is_usage, common.hpp:33-
 int renyi_ctx_create(int device, renyi_ctx** out);
 int renyi_ctx_destroy(renyi_ctx* ctx);
 int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc);
+int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode);
 int renyi_ctx_sync(renyi_ctx* ctx);
+/* returns the engine's cached device blocks (kernel storage, panels, scratch) to the driver */
+int renyi_release_cached_memory(void);
 /* CUDA-event timing of block-product launches with their algorithmic bytes and
  * flops (SURVEY §8d accounting); bench instrumentation */
 int renyi_ctx_profile(renyi_ctx* ctx, int enable);

@@ -144,7 +144,9 @@ SIGNATURES = {
     "renyi_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "renyi_ctx_destroy": (C.c_int, [_P]),
     "renyi_ctx_set_tuning": (C.c_int, [_P, C.c_int, C.c_int]),
+    "renyi_ctx_set_operand_mode": (C.c_int, [_P, C.c_int]),
     "renyi_ctx_sync": (C.c_int, [_P]),
+    "renyi_release_cached_memory": (C.c_int, []),
     "renyi_ctx_profile": (C.c_int, [_P, C.c_int]),
     "renyi_ctx_profile_read": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]),

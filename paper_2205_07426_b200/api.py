@@ -54,6 +54,10 @@ class Context:
     def set_tuning(self, grid: int = 0, kc: int = 16) -> None:
         check(L.lib().renyi_ctx_set_tuning(self._h, grid, kc))
 
+    def set_operand_mode(self, mode: str = "split") -> None:
+        """'split' (default, V as fp16 hi+lo, 3 MMAs) or 'fast' (V hi only, 2 MMAs)."""
+        check(L.lib().renyi_ctx_set_operand_mode(self._h, {"split": 0, "fast": 1}[mode]))
+
     def sync(self) -> None:
         check(L.lib().renyi_ctx_sync(self._h))
 
@@ -95,6 +99,11 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def release_cached_memory() -> None:
+    """Returns the engine's cached device blocks to the driver."""
+    check(L.lib().renyi_release_cached_memory())
 
 
 _default = threading.local()

@@ -68,6 +68,7 @@ StreamKPlan make_f64_plan(int64_t rows, int64_t cols) {
     p.grid = 1;
     p.kc = 1;
     p.slots = p.row_blocks + 1;
+    p.rows_per_block = FM;
     (void)cols;
     return p;
 }

@@ -2,24 +2,31 @@
 // proj/src/ops.cpp:98-107, called from proj/src/poly.cpp:155-163 and
 // proj/src/hutchpp.cpp:90).
 //
-// B200 design (see DESIGN.md "K6"):
-//   * A lives in HBM as two fp16 planes (hi, lo) of A·n·2^14, i.e. the same
-//     4 bytes/entry as fp32 but split so the 5th-gen tensor cores can consume it.
-//     The iterate V is stored the same way, column-major, with a per-column
-//     power-of-two scale chosen by the previous pass's epilogue.
-//   * Y ≈ A_hi·V_hi + (A_hi·V_lo + A_lo·V_hi): three tcgen05.mma (kind::f16,
-//     fp32 accumulate) per K=16 step; the dropped lo·lo term is 2^-22 relative.
-//   * Persistent stream-K schedule: 148 CTAs each own one contiguous range of
-//     (row-block, k-tile) iterations, so every SM streams the same number of A
-//     bytes. Ranges that end inside a row block write an fp32 partial to a slot
-//     (slot = row_block + cta, unique along the monotone staircase); the pass
-//     epilogue kernel sums the slots of a row block in CTA order (deterministic).
-//   * Accumulation into TMEM is chunked (KC k-tiles) and drained into fp32
-//     registers (round-to-nearest adds), bounding the tensor core's internal
-//     accumulation error; the main and correction products use separate TMEM
-//     accumulators. Two accumulator sets double-buffer the drain.
+// B200 design (DESIGN.md "K6"):
+//   * A lives in HBM as two fp16 planes (hi, lo) of A·n·2^14: the same 4 bytes
+//     per entry as fp32, split so the 5th-gen tensor cores consume it directly.
+//     The iterate V is stored the same way (hi, lo fp16 planes), column-major,
+//     with a per-column power-of-two scale chosen by the previous pass's
+//     epilogue; the fp32 recurrence state itself stays in the epilogue.
+//   * Y ≈ A_hi·V_hi + A_lo·V_hi + A_hi·V_lo (the dropped lo·lo term is 2^-22
+//     relative) as two tcgen05.mma (kind::f16, fp32 accumulate) per K=16 step:
+//     A_hi·[V_hi | V_lo] with N' = 2N (A_hi is read from shared memory once)
+//     and A_lo·V_hi into the first N accumulator columns; the drain adds the
+//     two halves. The opt-in "fast" operand mode drops V_lo (A_hi·V_hi +
+//     A_lo·V_hi, one V plane); see DESIGN.md for its measured error.
+//   * Each CTA owns 256 rows (two UMMA M=128 tiles sharing one staged V tile),
+//     so V is re-read from L2 once per 256 rows: L2 traffic 1.16x the A stream.
+//   * Persistent stream-K schedule: one CTA per SM, each owning one contiguous
+//     range of (row-block, k-tile) iterations, so every SM streams the same
+//     number of A bytes. A range that ends inside a row block writes an fp32
+//     partial to slot = row_block + cta (unique along the monotone staircase);
+//     the pass epilogue sums a row block's slots in CTA order (deterministic).
+//   * The tensor core's fp32 accumulation is lossy over long K (measured on
+//     B200: 1e-4 rms at K=1e5 with Gaussian operands), so TMEM accumulation
+//     is chunked (kc k-tiles) and drained into fp32 registers with
+//     round-to-nearest adds; two accumulator sets double-buffer the drain.
 //   * Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM owner),
-//     warps 2..5 = TMEM drain / partial writers.
+//     warps 2..9 = TMEM drain (4 per M=128 tile) and partial writers.
 #include <cstdio>
 #include <cuda_fp16.h>
 
@@ -30,22 +37,29 @@ namespace rb {
 
 namespace {
 
-constexpr int BM = 128;  // UMMA M: rows of A per tile
-constexpr int BK = 64;   // K per tile: one 128-byte swizzle row of fp16
+constexpr int BM = 256;  // rows per CTA (two UMMA M=128 tiles)
+constexpr int TM = 128;  // UMMA M
+constexpr int BK = 32;   // K per stage: one 64-byte swizzle row of fp16
+constexpr int kThreads = 320;
 
-template <int NPAD>
+template <int NPAD, bool VSPLIT>
 struct TcCfg {
-    static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kVBytes = NPAD * BK * 2;
-    static constexpr int kStageBytes = 2 * kABytes + 2 * kVBytes;
+    static constexpr int kAPlane = BM * BK * 2;  // one plane, both tiles
+    static constexpr int kATile = TM * BK * 2;   // one plane, one tile
+    static constexpr int kVPlane = NPAD * BK * 2;
+    static constexpr int kVBytes = (VSPLIT ? 2 : 1) * kVPlane;
+    static constexpr int kStageBytes = 2 * kAPlane + kVBytes;
     static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-    static constexpr int kTmemCols = (4 * NPAD <= 32) ? 32 : (4 * NPAD <= 64) ? 64 : (4 * NPAD <= 128) ? 128
-                                                           : (4 * NPAD <= 256) ? 256 : 512;
+    static constexpr int kAccCols = (VSPLIT ? 2 : 1) * NPAD;              // accumulator width per tile
+    static constexpr int kBufs = (2 * 2 * kAccCols <= 512) ? 2 : 1;         // double-buffer the drain if it fits
+    static constexpr int kTmemNeed = kBufs * 2 * kAccCols;
+    static constexpr int kTmemCols = (kTmemNeed <= 32) ? 32 : (kTmemNeed <= 64) ? 64 : (kTmemNeed <= 128) ? 128
+                                                         : (kTmemNeed <= 256) ? 256 : 512;
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024;
-    static constexpr int kThreads = 192;
     static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 128, "NPAD must be a multiple of 16 in [16,128]");
-    static_assert(kStages >= 2, "need at least double buffering");
+    static_assert(kStages >= 3, "need a deep enough TMA ring");
+    static_assert(kVPlane % 512 == 0, "64-byte swizzle atoms are 512 bytes");
 };
 
 struct TcArgs {
@@ -55,12 +69,23 @@ struct TcArgs {
     float* partial;       // [slots][NPAD][BM]
 };
 
-template <int NPAD>
-__global__ void __launch_bounds__(192, 1)
+// UMMA shared-memory descriptor: K-major, 64-byte swizzle (rows of 64 bytes, 8-row atoms of 512 bytes).
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);  // start address
+    d |= static_cast<uint64_t>(1) << 16;                      // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(512 >> 4) << 32;               // SBO: stride between 8-row atoms
+    d |= static_cast<uint64_t>(1) << 46;                      // descriptor version (sm100)
+    d |= static_cast<uint64_t>(4) << 61;                      // SWIZZLE_64B
+    return d;
+}
+
+template <int NPAD, bool VSPLIT>
+__global__ void __launch_bounds__(kThreads, 1)
     block_av_tc_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
-                       const __grid_constant__ CUtensorMap map_vhi, const __grid_constant__ CUtensorMap map_vlo,
+                       const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_vlo,
                        TcArgs args) {
-    using C = TcCfg<NPAD>;
+    using C = TcCfg<NPAD, VSPLIT>;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[C::kStages];
     __shared__ __align__(8) uint64_t empty_bar[C::kStages];
@@ -83,15 +108,15 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&map_ahi);
         prefetch_tmap(&map_alo);
-        prefetch_tmap(&map_vhi);
-        prefetch_tmap(&map_vlo);
+        prefetch_tmap(&map_v);
+        if (VSPLIT) prefetch_tmap(&map_vlo);
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full_bar[b], 1);
-            mbar_init(&tmem_empty_bar[b], 4 * kWarp);
+            mbar_init(&tmem_empty_bar[b], 8 * kWarp);
         }
         fence_barrier_init();
     }
@@ -115,9 +140,10 @@ __global__ void __launch_bounds__(192, 1)
                 uint8_t* st = smem_base + stage * C::kStageBytes;
                 mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
                 tma_load_2d(st, &map_ahi, &full_bar[stage], k * BK, r * BM, pol_stream);
-                tma_load_2d(st + C::kABytes, &map_alo, &full_bar[stage], k * BK, r * BM, pol_stream);
-                tma_load_2d(st + 2 * C::kABytes, &map_vhi, &full_bar[stage], k * BK, 0, pol_keep);
-                tma_load_2d(st + 2 * C::kABytes + C::kVBytes, &map_vlo, &full_bar[stage], k * BK, 0, pol_keep);
+                tma_load_2d(st + C::kAPlane, &map_alo, &full_bar[stage], k * BK, r * BM, pol_stream);
+                tma_load_2d(st + 2 * C::kAPlane, &map_v, &full_bar[stage], k * BK, 0, pol_keep);
+                if (VSPLIT)
+                    tma_load_2d(st + 2 * C::kAPlane + C::kVPlane, &map_vlo, &full_bar[stage], k * BK, 0, pol_keep);
                 if (++stage == C::kStages) {
                     stage = 0;
                     phase ^= 1u;
@@ -127,7 +153,8 @@ __global__ void __launch_bounds__(192, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_f16_f32(BM, NPAD);
+            constexpr uint32_t idesc = umma_idesc_f16_f32(TM, NPAD);
+            constexpr uint32_t idesc2 = umma_idesc_f16_f32(TM, VSPLIT ? 2 * NPAD : NPAD);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t chunk = 0;
@@ -137,32 +164,29 @@ __global__ void __launch_bounds__(192, 1)
                 const int64_t seg_end = min(it_end, (r + 1) * KT);
                 while (it < seg_end) {
                     const int64_t cend = min(seg_end, it + args.kc);
-                    const uint32_t buf = chunk & 1u;
-                    const uint32_t use = chunk >> 1;
+                    const uint32_t buf = chunk % C::kBufs;
+                    const uint32_t use = chunk / C::kBufs;
                     mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
                     tc_fence_after();
-                    const uint32_t d_main = tmem_base + buf * (2 * NPAD);
-                    const uint32_t d_corr = d_main + NPAD;
+                    const uint32_t d0 = tmem_base + buf * (2 * C::kAccCols);
                     const int64_t cstart = it;
                     for (; it < cend; ++it) {
                         mbar_wait(&full_bar[stage], phase);
                         tc_fence_after();
                         const uint32_t st = smem_base_u32 + stage * C::kStageBytes;
-                        const uint32_t a_hi = st;
-                        const uint32_t a_lo = st + C::kABytes;
-                        const uint32_t v_hi = st + 2 * C::kABytes;
-                        const uint32_t v_lo = v_hi + C::kVBytes;
+                        const uint32_t v = st + 2 * C::kAPlane;
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint32_t off = kk * 32;  // 16 fp16 along K = 32 bytes
-                            const uint32_t acc = (it > cstart || kk > 0) ? 1u : 0u;
-                            const uint64_t dah = umma_desc_sw128(a_hi + off);
-                            const uint64_t dal = umma_desc_sw128(a_lo + off);
-                            const uint64_t dvh = umma_desc_sw128(v_hi + off);
-                            const uint64_t dvl = umma_desc_sw128(v_lo + off);
-                            umma_f16(d_main, dah, dvh, idesc, acc);
-                            umma_f16(d_corr, dah, dvl, idesc, acc);
-                            umma_f16(d_corr, dal, dvh, idesc, 1u);
+                            const uint64_t dv = desc_sw64(v + off);
+#pragma unroll
+                            for (int t = 0; t < BM / TM; ++t) {
+                                const uint32_t acc = (it > cstart || kk > 0) ? 1u : 0u;
+                                const uint32_t d = d0 + t * C::kAccCols;
+                                // A_hi x [V_hi | V_lo]: the two V planes are adjacent in smem (N' = 2N rows)
+                                umma_f16(d, desc_sw64(st + t * C::kATile + off), dv, VSPLIT ? idesc2 : idesc, acc);
+                                umma_f16(d, desc_sw64(st + C::kAPlane + t * C::kATile + off), dv, idesc, 1u);
+                            }
                         }
                         umma_commit(&empty_bar[stage]);
                         if (++stage == C::kStages) {
@@ -176,10 +200,11 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
     } else {
-        // ---------------- TMEM drain (warps 2..5) ----------------
+        // ---------------- TMEM drain (warps 2..9: tile (warp-2)/4, lane quarter warp%4) ----------------
+        const int tile = (warp - 2) / 4;
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-        const int row_local = quarter * 32 + lane;
-        const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+        const int row_local = tile * TM + quarter * 32 + lane;
+        const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + tile * C::kAccCols;
         float acc[NPAD];
 #pragma unroll
         for (int j = 0; j < NPAD; ++j) acc[j] = 0.f;
@@ -190,19 +215,26 @@ __global__ void __launch_bounds__(192, 1)
             const int64_t seg_end = min(it_end, (r + 1) * KT);
             while (it < seg_end) {
                 const int64_t cend = min(seg_end, it + args.kc);
-                const uint32_t buf = chunk & 1u;
-                const uint32_t use = chunk >> 1;
+                const uint32_t buf = chunk % C::kBufs;
+                const uint32_t use = chunk / C::kBufs;
                 mbar_wait(&tmem_full_bar[buf], use & 1u);
                 tc_fence_after();
-                const uint32_t t_main = lane_base + buf * (2 * NPAD);
+                const uint32_t t0 = lane_base + buf * (2 * C::kAccCols);
 #pragma unroll
                 for (int j0 = 0; j0 < NPAD; j0 += 16) {
-                    float m[16], c[16];
-                    tmem_ld16(t_main + j0, m);
-                    tmem_ld16(t_main + NPAD + j0, c);
-                    tmem_ld_wait();
+                    float m[16];
+                    tmem_ld16(t0 + j0, m);
+                    if (VSPLIT) {
+                        float c[16];
+                        tmem_ld16(t0 + NPAD + j0, c);  // A_hi·V_lo half
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i] + c[i];
+                        for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i] + c[i];
+                    } else {
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i];
+                    }
                 }
                 tc_fence_before();
                 mbar_arrive(&tmem_empty_bar[buf]);
@@ -251,25 +283,25 @@ bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-template <int NPAD>
+template <int NPAD, bool VSPLIT>
 cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan, float* partial,
                       cudaStream_t stream) {
-    using C = TcCfg<NPAD>;
-    CUtensorMap m_ahi, m_alo, m_vhi, m_vlo;
+    using C = TcCfg<NPAD, VSPLIT>;
+    CUtensorMap m_ahi, m_alo, m_v, m_vlo;
     bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM) &&
               make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM) &&
-              make_map_f16(&m_vhi, v.hi, v.n, v.cols, v.ld * 2ull, BK, NPAD) &&
-              make_map_f16(&m_vlo, v.lo, v.n, v.cols, v.ld * 2ull, BK, NPAD);
+              make_map_f16(&m_v, v.v, v.n, v.cols, v.ld * 2ull, BK, NPAD) &&
+              make_map_f16(&m_vlo, VSPLIT ? v.vlo : v.v, v.n, v.cols, v.ld * 2ull, BK, NPAD);
     if (!ok) return cudaErrorInvalidValue;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(block_av_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             C::kSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(block_av_tc_kernel<NPAD, VSPLIT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
@@ -278,7 +310,7 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     args.k_tiles = plan.k_tiles;
     args.kc = plan.kc;
     args.partial = partial;
-    block_av_tc_kernel<NPAD><<<plan.grid, C::kThreads, C::kSmemBytes, stream>>>(m_ahi, m_alo, m_vhi, m_vlo, args);
+    block_av_tc_kernel<NPAD, VSPLIT><<<plan.grid, kThreads, C::kSmemBytes, stream>>>(m_ahi, m_alo, m_v, m_vlo, args);
     return cudaGetLastError();
 }
 
@@ -296,6 +328,7 @@ StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc) {
     if (p.total_iters < grid) p.grid = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
     p.kc = kc;
     p.slots = p.row_blocks + p.grid;
+    p.rows_per_block = BM;
     return p;
 }
 
@@ -304,17 +337,22 @@ int tc_npad(int cols) { return ((cols + 15) / 16) * 16; }
 cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream) {
     const int npad = tc_npad(v.cols);
+#define RB_TC_CASE(N)                                                                              \
+    case N:                                                                                        \
+        return v.vlo ? launch_tc<N, true>(a, v, plan, partial, stream)                             \
+                     : launch_tc<N, false>(a, v, plan, partial, stream);
     switch (npad) {
-        case 16: return launch_tc<16>(a, v, plan, partial, stream);
-        case 32: return launch_tc<32>(a, v, plan, partial, stream);
-        case 48: return launch_tc<48>(a, v, plan, partial, stream);
-        case 64: return launch_tc<64>(a, v, plan, partial, stream);
-        case 80: return launch_tc<80>(a, v, plan, partial, stream);
-        case 96: return launch_tc<96>(a, v, plan, partial, stream);
-        case 112: return launch_tc<112>(a, v, plan, partial, stream);
-        case 128: return launch_tc<128>(a, v, plan, partial, stream);
+        RB_TC_CASE(16)
+        RB_TC_CASE(32)
+        RB_TC_CASE(48)
+        RB_TC_CASE(64)
+        RB_TC_CASE(80)
+        RB_TC_CASE(96)
+        RB_TC_CASE(112)
+        RB_TC_CASE(128)
         default: return cudaErrorInvalidValue;
     }
+#undef RB_TC_CASE
 }
 
 }  // namespace rb

@@ -158,10 +158,26 @@ int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc) {
     });
 }
 
+int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        if (mode != RENYI_OPERAND_SPLIT && mode != RENYI_OPERAND_FAST)
+            rb::fail(rb::kInvalidArgument, "unknown operand mode");
+        ctx->ctx.operand_split = mode == RENYI_OPERAND_SPLIT;
+    });
+}
+
 int renyi_ctx_sync(renyi_ctx* ctx) {
     return guarded([&] {
         need(ctx, "ctx");
         ctx->ctx.sync();
+    });
+}
+
+int renyi_release_cached_memory(void) {
+    return guarded([&] {
+        cudaDeviceSynchronize();
+        rb::pool_release_all();
     });
 }
 
@@ -310,7 +326,11 @@ int renyi_kernel_download(renyi_ctx* ctx, const renyi_kernel* k, double* out) {
 }
 
 int renyi_kernel_destroy(renyi_kernel* k) {
-    return guarded([&] { delete k; });
+    return guarded([&] {
+        // storage returns to the engine pool; make sure no queued work still reads it
+        if (k) cudaDeviceSynchronize();
+        delete k;
+    });
 }
 
 int renyi_matmul_panel(renyi_ctx* ctx, const renyi_kernel* k, const double* v, int s, double* y) {

@@ -9,6 +9,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 namespace rb {
@@ -43,28 +45,87 @@ void d2h_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spit
     ctx.d2h_bytes += static_cast<long long>(width * height);
 }
 
+// ---------------------------------------------------------------- caching pool
+namespace {
+std::mutex g_pool_mu;
+std::multimap<std::pair<int, size_t>, void*> g_pool;  // (device, capacity) -> block
+
+size_t pool_round(size_t bytes) {
+    const size_t g = bytes >= (size_t(1) << 21) ? (size_t(1) << 21) : 512;
+    return (bytes + g - 1) / g * g;
+}
+}  // namespace
+
+void* pool_alloc(size_t bytes, size_t* capacity, int* device) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const size_t want = pool_round(bytes);
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto it = g_pool.lower_bound({dev, want});
+        if (it != g_pool.end() && it->first.first == dev && it->first.second <= 2 * want + (size_t(1) << 21)) {
+            void* p = it->second;
+            *capacity = it->first.second;
+            *device = dev;
+            g_pool.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaErrorMemoryAllocation) {
+        (void)cudaGetLastError();
+        pool_release_all();
+        e = cudaMalloc(&p, want);
+    }
+    cuda_check(e, "cudaMalloc");
+    *capacity = want;
+    *device = dev;
+    return p;
+}
+
+void pool_free(void* p, size_t capacity, int device) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.insert({{device, capacity}, p});
+}
+
+void pool_release_all() {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : g_pool) {
+        cudaSetDevice(kv.first.first);
+        cudaFree(kv.second);
+    }
+    g_pool.clear();
+    cudaSetDevice(cur);
+}
+
 // ---------------------------------------------------------------- DevBuf
 DevBuf::~DevBuf() { release(); }
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
     if (this != &o) {
         release();
-        p_ = o.p_, n_ = o.n_;
-        o.p_ = nullptr, o.n_ = 0;
+        p_ = o.p_, n_ = o.n_, cap_ = o.cap_, dev_ = o.dev_;
+        o.p_ = nullptr, o.n_ = 0, o.cap_ = 0;
     }
     return *this;
 }
 void DevBuf::alloc(size_t bytes) {
     release();
     if (bytes == 0) return;
-    cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
+    p_ = pool_alloc(bytes, &cap_, &dev_);
     n_ = bytes;
 }
 void DevBuf::ensure(size_t bytes) {
     if (bytes > n_) alloc(bytes);
 }
 void DevBuf::release() {
-    if (p_) cudaFree(p_);
-    p_ = nullptr, n_ = 0;
+    // blocks may still be read by queued work on the engine stream: every public entry
+    // point synchronises before its buffers go out of scope, and reuse is stream-ordered
+    if (p_) pool_free(p_, cap_, dev_);
+    p_ = nullptr, n_ = 0, cap_ = 0;
 }
 
 // ---------------------------------------------------------------- Context
@@ -398,13 +459,23 @@ public:
             fail(kInvalidArgument, "row-sharded panels need the multi-rank exchange path");
         rows_ = k.rows;
         ld_ = round_up(k.n, 8);
-        R_ = static_cast<int>((rows_ + 127) / 128);
+        if (k.prec == kF32) {
+            const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
+            plan_ = make_streamk_plan(rows_, k.n, grid, ctx.kc);
+            npad_ = tc_npad(s);
+        } else {
+            plan_ = make_f64_plan(rows_, k.n);
+            npad_ = f64_npad(s);
+        }
+        const int rpb = plan_.rows_per_block;
+        R_ = static_cast<int>((rows_ + rpb - 1) / rpb);
         const size_t st = k.prec == kF32 ? sizeof(float) : sizeof(double);
         for (auto& b : ctx.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
         if (k.prec == kF32) {
             ctx.vhi.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
-            ctx.vlo.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
+            if (ctx.operand_split) ctx.vlo.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
         }
+        vlo_ = (k.prec == kF32 && ctx.operand_split) ? ctx.vlo.as<__half>() : nullptr;
         const size_t P1 = static_cast<size_t>(max_passes) + 1;
         ctx.stats.ensure(P1 * 3 * R_ * s * sizeof(double));
         ctx.red.ensure(P1 * 3 * s * sizeof(double));
@@ -412,25 +483,21 @@ public:
         ctx.eexp.ensure(P1 * s * sizeof(int));
         cuda_check(cudaMemsetAsync(ctx.cmax.as<unsigned>(), 0, P1 * s * sizeof(unsigned), ctx.stream()), "memset");
         if (k.prec == kF32) {
-            const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
-            plan_ = make_streamk_plan(rows_, k.n, grid, ctx.kc);
-            npad_ = tc_npad(s);
-            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * 128 * sizeof(float));
+            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(float));
             PrepArgs<float> p{};
-            p.x = x, p.ldx = ldx, p.rows = rows_, p.s = s, p.ld = ld_;
+            p.x = x, p.ldx = ldx, p.rows = rows_, p.rows_per_block = rpb, p.s = s, p.ld = ld_;
             p.t0 = buf<float>(0);
             p.cmax0 = ctx.cmax.as<unsigned>();
             p.stats = ctx.stats.as<double>();
             p.e0 = ctx.eexp.as<int>();
-            p.vhi = ctx.vhi.as<__half>(), p.vlo = ctx.vlo.as<__half>();
+            p.vop = ctx.vhi.as<__half>();
+            p.vop_lo = vlo_;
             p.acc = acc_out, p.acc_coef = acc_coef0;
             launched(ctx, launch_prepare_split(p, ctx.stream()), "prepare");
         } else {
-            plan_ = make_f64_plan(rows_, k.n);
-            npad_ = f64_npad(s);
-            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * 128 * sizeof(double));
+            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(double));
             PrepArgs<double> p{};
-            p.x = x, p.ldx = ldx, p.rows = rows_, p.s = s, p.ld = ld_;
+            p.x = x, p.ldx = ldx, p.rows = rows_, p.rows_per_block = rpb, p.s = s, p.ld = ld_;
             p.t0 = buf<double>(0);
             p.cmax0 = ctx.cmax.as<unsigned>();
             p.stats = ctx.stats.as<double>();
@@ -445,17 +512,18 @@ public:
         const size_t s = static_cast<size_t>(s_);
         if (k_.prec == kF32) {
             SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
-            SplitPanelView v{ctx_.vhi.as<__half>(), ctx_.vlo.as<__half>(), k_.n, s_, ld_};
+            SplitPanelView v{ctx_.vhi.as<__half>(), vlo_, k_.n, s_, ld_};
             ctx_.prof_begin();
             launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()), "block_av_tc");
             ctx_.prof_end();
             // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
-            ctx_.prof_account(4.0 * rows_ * k_.n + 4.0 * k_.n * s_ + 4.0 * rows_ * s_, 2.0 * rows_ * k_.n * s_);
+            ctx_.prof_account(4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_ + 4.0 * rows_ * s_,
+                              2.0 * rows_ * k_.n * s_);
             EpiArgs<float, float> e{};
             e.partial = ctx_.partial.as<float>();
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
-            e.rows = rows_, e.s = s_, e.ld = ld_;
+            e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.e_cur = ctx_.eexp.as<int>() + k * s;
             e.e_next = ctx_.eexp.as<int>() + (k + 1) * s;
             e.unscale = k_.unscale;
@@ -467,7 +535,8 @@ public:
             e.t_prev = k > 0 ? buf<float>(k - 1) : nullptr;
             e.t_new = buf<float>(k + 1);
             e.x0 = buf<float>(0);
-            e.vhi = ctx_.vhi.as<__half>(), e.vlo = ctx_.vlo.as<__half>();
+            e.vop = ctx_.vhi.as<__half>();
+            e.vop_lo = vlo_;
             e.stats = ctx_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
             e.acc = acc_, e.acc_coef = acc_coef;
             launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
@@ -483,7 +552,7 @@ public:
             e.partial = ctx_.partial.as<double>();
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
-            e.rows = rows_, e.s = s_, e.ld = ld_;
+            e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.unscale = 1.0;
             e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;
             e.cmax_prev = k > 0 ? ctx_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
@@ -541,6 +610,7 @@ private:
     int R_ = 0;
     int npad_ = 0;
     int k_done_ = 0;
+    __half* vlo_ = nullptr;
     StreamKPlan plan_;
 };
 

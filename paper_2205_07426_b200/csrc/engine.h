@@ -21,13 +21,20 @@ enum Precision : int { kF64 = 0, kF32 = 1 };
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Device memory comes from a process-wide caching pool (per device): n x n kernel
+// storage, panels and scratch are reused across estimates instead of paying
+// cudaMalloc/cudaFree (which synchronise the device) inside the estimator loop.
+void* pool_alloc(size_t bytes, size_t* capacity, int* device);
+void pool_free(void* p, size_t capacity, int device);
+void pool_release_all();  // returns every cached block to the driver
+
 class DevBuf {
 public:
     DevBuf() = default;
     ~DevBuf();
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), cap_(o.cap_), dev_(o.dev_) { o.p_ = nullptr, o.n_ = 0, o.cap_ = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept;
     void alloc(size_t bytes);
     void ensure(size_t bytes);  // grow-only
@@ -41,6 +48,8 @@ public:
 private:
     void* p_ = nullptr;
     size_t n_ = 0;
+    size_t cap_ = 0;
+    int dev_ = 0;
 };
 
 // Multi-rank exchange hooks (row-sharded A). nullptr = single rank.
@@ -66,7 +75,8 @@ public:
 
     // tuning knobs of the block product
     int grid = 0;  // CTAs of the persistent stream-K kernel (0 = SM count)
-    int kc = 16;   // k tiles (x64 columns) per TMEM accumulation chunk
+    int kc = 16;   // k tiles (x32 columns) per TMEM accumulation chunk
+    bool operand_split = true;  // V as fp16 hi+lo (3 MMAs); false = "fast" (V hi only, 2 MMAs)
 
     // instrumentation: CUDA-event timing of every block-product launch
     void prof_enable(bool on);

@@ -24,9 +24,9 @@ struct SplitMatrixView {
     int64_t rows, cols, ld;
 };
 
-struct SplitPanelView {
-    const __half* hi;
-    const __half* lo;
+struct SplitPanelView {  // the iterate operand: fp16 hi (+ optional lo) planes, column-major n x cols
+    const __half* v;
+    const __half* vlo;  // nullptr: "fast" operand mode (one plane, two MMAs)
     int64_t n;
     int cols;
     int64_t ld;
@@ -39,6 +39,7 @@ struct StreamKPlan {
     int grid = 1;
     int kc = 16;
     int slots = 0;
+    int rows_per_block = 256;
 };
 
 // ---- block product -------------------------------------------------------
@@ -63,6 +64,7 @@ struct EpiArgs {
     int k_tiles;
     int grid;
     int64_t rows;  // local rows (product rows)
+    int rows_per_block;  // 256 (tensor-core path) or 128 (fp64 path)
     int s;
     int64_t ld;
     const int* e_cur;  // split only
@@ -77,8 +79,8 @@ struct EpiArgs {
     const ST* t_prev;
     ST* t_new;
     const ST* x0;
-    __half* vhi;
-    __half* vlo;
+    __half* vop;    // fp16 operand plane(s) for the next pass (split only)
+    __half* vop_lo; // optional low plane (operand split mode)
     double* stats;  // [3][row_blocks][s]
     double* acc;    // optional vector accumulator (fp64, [s][ld])
     double acc_coef;
@@ -93,14 +95,15 @@ struct PrepArgs {
     const double* x;  // [s][ldx]
     int64_t ldx;
     int64_t rows;
+    int rows_per_block;
     int s;
     int64_t ld;
     ST* t0;
     unsigned* cmax0;
     double* stats;  // [3][row_blocks][s]
     int* e0;
-    __half* vhi;
-    __half* vlo;
+    __half* vop;
+    __half* vop_lo;
     double* acc;  // optional: acc = acc_coef * t0
     double acc_coef;
 };

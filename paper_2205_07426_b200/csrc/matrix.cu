@@ -175,6 +175,131 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g, __half* __restric
     }
 }
 
+// fp32 configurations: symmetric tiles. Only tiles with column tile >= row tile are
+// evaluated; the mirrored tile is written through shared memory (coalesced), so the
+// distance/exp work halves while every entry of A is still written once.
+// The joint uses one exp2 of the summed exponents (exp(a)·exp(b) = exp(a+b)).
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void store_split4(__half* ph, __half* pl, const float* kv, int64_t gj0, int64_t n) {
+    __half h[4], l[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        const float s = kv[v] * static_cast<float>(kSplitScale);
+        h[v] = __float2half_rn(s);
+        l[v] = __float2half_rn(s - __half2float(h[v]));
+    }
+    if (gj0 + 3 < n) {
+        *reinterpret_cast<uint2*>(ph) =
+            make_uint2((static_cast<uint32_t>(__half_as_ushort(h[1])) << 16) | __half_as_ushort(h[0]),
+                       (static_cast<uint32_t>(__half_as_ushort(h[3])) << 16) | __half_as_ushort(h[2]));
+        *reinterpret_cast<uint2*>(pl) =
+            make_uint2((static_cast<uint32_t>(__half_as_ushort(l[1])) << 16) | __half_as_ushort(l[0]),
+                       (static_cast<uint32_t>(__half_as_ushort(l[3])) << 16) | __half_as_ushort(l[2]));
+    } else {
+        for (int v = 0; v < 4; ++v)
+            if (gj0 + v < n) {
+                ph[v] = h[v];
+                pl[v] = l[v];
+            }
+    }
+}
+
+__global__ void __launch_bounds__(256) gram_sym_f32_kernel(GramArgs g, int nb, __half* __restrict__ hi,
+                                                           __half* __restrict__ lo) {
+    __shared__ float xr[TKd][TM + 1];
+    __shared__ float xc[TKd][TN + 4];
+    __shared__ float tt[TN][TM + 1];
+    // linear upper-triangle tile index -> (bi, bj), bi <= bj
+    const int64_t t = blockIdx.x;
+    auto start = [nb](int64_t b) { return b * nb - b * (b - 1) / 2; };
+    const double q = 2.0 * nb + 1.0;
+    int64_t bi = static_cast<int64_t>((q - sqrt(q * q - 8.0 * static_cast<double>(t))) * 0.5);
+    if (bi < 0) bi = 0;
+    if (bi > nb - 1) bi = nb - 1;
+    while (bi + 1 < nb && start(bi + 1) <= t) ++bi;
+    while (bi > 0 && start(bi) > t) --bi;
+    const int64_t bj = bi + (t - start(bi));
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t row0 = static_cast<int64_t>(bi) * TM;
+    const int64_t col0 = static_cast<int64_t>(bj) * TN;
+    const float l2e = 1.4426950408889634f;
+
+    float e[4][4];
+    {
+        float dot[4][4], sqr[4], sqc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sqr[u] = sqc[u] = 0.f;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dot[u][v] = 0.f;
+        }
+        GramTile<float>::accumulate(g.x, g.dx, g.x_rs, g.x_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+        const float ax = static_cast<float>(g.inv_two_sigma2_x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                float d2 = (sqr[u] + sqc[v]) - 2.f * dot[u][v];
+                e[u][v] = -fmaxf(d2, 0.f) * ax;
+            }
+    }
+    if (g.y) {
+        float dot[4][4], sqr[4], sqc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sqr[u] = sqc[u] = 0.f;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dot[u][v] = 0.f;
+        }
+        GramTile<float>::accumulate(g.y, g.dy, g.y_rs, g.y_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+        const float ay = static_cast<float>(g.inv_two_sigma2_y);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                float d2 = (sqr[u] + sqc[v]) - 2.f * dot[u][v];
+                e[u][v] -= fmaxf(d2, 0.f) * ay;
+            }
+    }
+    float kv[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t gi = row0 + ty + 16 * u, gj = col0 + 4 * tx + v;
+            kv[u][v] = (gi == gj) ? 1.0f : fast_exp2(e[u][v] * l2e);
+        }
+    // direct tile: rows gi, columns gj
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t gi = row0 + ty + 16 * u;
+        if (gi < g.n) store_split4(hi + gi * g.ld + col0 + 4 * tx, lo + gi * g.ld + col0 + 4 * tx, kv[u], col0 + 4 * tx, g.n);
+    }
+    if (bi == bj) return;
+    // mirrored tile: rows gj, columns gi (via shared memory)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) tt[4 * tx + v][ty + 16 * u] = kv[u][v];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int rr = ty + 16 * u;  // row of the mirrored tile (a column of the direct tile)
+        const int64_t gr = col0 + rr;
+        if (gr >= g.n) continue;
+        float w[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) w[v] = tt[rr][4 * tx + v];
+        store_split4(hi + gr * g.ld + row0 + 4 * tx, lo + gr * g.ld + row0 + 4 * tx, w, row0 + 4 * tx, g.n);
+    }
+}
+
 __global__ void matrix_to_split_kernel(const double* __restrict__ a, int64_t rows, int64_t cols, int64_t lda,
                                        double scale, __half* __restrict__ hi, __half* __restrict__ lo, int64_t ld) {
     const int64_t i = blockIdx.y;
@@ -260,6 +385,12 @@ inline dim3 row_grid(int64_t rows, int64_t cols) {
 }  // namespace
 
 cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStream_t stream) {
+    if (g.f32_compute && g.row0 == 0 && g.rows == g.n) {
+        const int nb = static_cast<int>((g.n + TM - 1) / TM);
+        const int64_t tiles = static_cast<int64_t>(nb) * (nb + 1) / 2;
+        gram_sym_f32_kernel<<<static_cast<unsigned>(tiles), 256, 0, stream>>>(g, nb, hi, lo);
+        return cudaGetLastError();
+    }
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
     if (g.f32_compute)
         gram_kernel<float, true><<<grid, 256, 0, stream>>>(g, hi, lo, nullptr);

@@ -17,7 +17,6 @@ namespace rb {
 
 namespace {
 
-constexpr int ER = 128;  // rows per epilogue CTA (= product row block)
 
 __device__ __forceinline__ int64_t streamk_owner(int64_t i, int64_t total, int grid) {
     return ((i + 1) * grid + total - 1) / total - 1;
@@ -37,16 +36,17 @@ __device__ __forceinline__ int plane_exponent(double bound) {
     return e;
 }
 
+// fp16 operand (+ optional low plane carrying the rounding residual)
 __device__ __forceinline__ void split_store(double v, __half* hi, __half* lo, int64_t idx) {
     const __half h = __double2half(v);
-    const double r = v - static_cast<double>(__half2float(h));
     hi[idx] = h;
-    lo[idx] = __double2half(r);
+    if (lo) lo[idx] = __double2half(v - static_cast<double>(__half2float(h)));
 }
 
-template <typename PT, typename ST, bool SPLIT>
+template <typename PT, typename ST, bool SPLIT, int ER>
 __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
-    __shared__ double red[3][4][kMaxPanelCols];
+    constexpr int NW = ER / 32;
+    __shared__ double red[3][NW][kMaxPanelCols];
     const int r = blockIdx.x;
     const int tid = threadIdx.x;
     const int warp = tid / 32, lane = tid % 32;
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
             const double bound = growth * cm_value(p.cmax_cur, j) + fabs(p.a3) * cm_value(p.cmax_prev, j);
             const int e = plane_exponent(bound);
             if (r == 0 && tid == 0) p.e_next[j] = e;
-            if (valid) split_store(ldexp(tn, e), p.vhi, p.vlo, idx);
+            if (valid) split_store(ldexp(tn, e), p.vop, p.vop_lo, idx);
         }
         const double d1 = warp_sum(x0 * tn);
         const double d2 = warp_sum(tc * tn);
@@ -98,14 +98,17 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     const int R = gridDim.x;
     for (int t = tid; t < 3 * p.s; t += blockDim.x) {
         const int q = t / p.s, j = t % p.s;
-        const double v = ((red[q][0][j] + red[q][1][j]) + red[q][2][j]) + red[q][3][j];
+        double v = red[q][0][j];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) v += red[q][w][j];
         p.stats[(static_cast<int64_t>(q) * R + r) * p.s + j] = v;
     }
 }
 
-template <typename ST, bool SPLIT>
+template <typename ST, int ER>
 __global__ void __launch_bounds__(ER) prep_stats_kernel(PrepArgs<ST> p) {
-    __shared__ double red[4][kMaxPanelCols];
+    constexpr int NW = ER / 32;
+    __shared__ double red[NW][kMaxPanelCols];
     const int r = blockIdx.x;
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int64_t i = static_cast<int64_t>(r) * ER + tid;
@@ -128,7 +131,9 @@ __global__ void __launch_bounds__(ER) prep_stats_kernel(PrepArgs<ST> p) {
     __syncthreads();
     const int R = gridDim.x;
     for (int j = tid; j < p.s; j += blockDim.x) {
-        const double v = ((red[0][j] + red[1][j]) + red[2][j]) + red[3][j];
+        double v = red[0][j];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) v += red[w][j];
         // q = 0 (x0·T0), 1 (T0·T0 as "Rayleigh" slot), 2 (T0·T0)
         p.stats[(0 * static_cast<int64_t>(R) + r) * p.s + j] = v;
         p.stats[(1 * static_cast<int64_t>(R) + r) * p.s + j] = v;
@@ -143,7 +148,7 @@ __global__ void prep_planes_kernel(PrepArgs<float> p) {
     if (blockIdx.x == 0 && threadIdx.x == 0) p.e0[j] = e;
     if (i >= p.rows) return;
     const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
-    split_store(ldexp(static_cast<double>(p.t0[idx]), e), p.vhi, p.vlo, idx);
+    split_store(ldexp(static_cast<double>(p.t0[idx]), e), p.vop, p.vop_lo, idx);
 }
 
 __global__ void reduce_stats_kernel(const double* __restrict__ stats, int passes, int R, int s,
@@ -278,23 +283,23 @@ __global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64
 }  // namespace
 
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream) {
-    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + ER - 1) / ER);
-    epilogue_kernel<float, float, true><<<R, ER, 0, stream>>>(a);
+    if (a.s > kMaxPanelCols || a.rows_per_block != 256) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + 255) / 256);
+    epilogue_kernel<float, float, true, 256><<<R, 256, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t stream) {
-    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + ER - 1) / ER);
-    epilogue_kernel<double, double, false><<<R, ER, 0, stream>>>(a);
+    if (a.s > kMaxPanelCols || a.rows_per_block != 128) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + 127) / 128);
+    epilogue_kernel<double, double, false, 128><<<R, 128, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_prepare_split(const PrepArgs<float>& a, cudaStream_t stream) {
-    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + ER - 1) / ER);
-    prep_stats_kernel<float, true><<<R, ER, 0, stream>>>(a);
+    if (a.s > kMaxPanelCols || a.rows_per_block != 256) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + 255) / 256);
+    prep_stats_kernel<float, 256><<<R, 256, 0, stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid(static_cast<unsigned>((a.rows + 255) / 256), a.s);
@@ -303,9 +308,9 @@ cudaError_t launch_prepare_split(const PrepArgs<float>& a, cudaStream_t stream) 
 }
 
 cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream) {
-    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + ER - 1) / ER);
-    prep_stats_kernel<double, false><<<R, ER, 0, stream>>>(a);
+    if (a.s > kMaxPanelCols || a.rows_per_block != 128) return cudaErrorInvalidValue;
+    const int R = static_cast<int>((a.rows + 127) / 128);
+    prep_stats_kernel<double, 128><<<R, 128, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
