@@ -74,9 +74,10 @@ def measured_peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per block-product launch from the committed ncu capture, if any."""
-    f = ROOT / "profiles" / "ncu_block_av.json"
+def ncu_traffic(operand: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one block-product launch (68-column pass at
+    n=100k) from the committed ncu --set full capture, if present."""
+    f = ROOT / "profiles" / f"r1_ncu_block_av_{operand}.json"
     if f.exists():
         try:
             return json.loads(f.read_text()).get("dram_bytes_per_launch")
@@ -284,7 +285,7 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     achieved = prof_bytes / (prof_ms / 1e3) / 1e9 if prof_ms > 0 else 0.0
     per_launch_bytes = prof_bytes / max(nprof, 1)
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.operand)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "kernel": "block_av_tc_kernel (tcgen05 split-fp16)",
                 "launches": nprof, "avg_launch_ms": prof_ms / max(nprof, 1),

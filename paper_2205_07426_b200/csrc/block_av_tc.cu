@@ -16,17 +16,24 @@
 //     A_lo·V_hi, one V plane); see DESIGN.md for its measured error.
 //   * Each CTA owns 256 rows (two UMMA M=128 tiles sharing one staged V tile),
 //     so V is re-read from L2 once per 256 rows: L2 traffic 1.16x the A stream.
-//   * Persistent stream-K schedule: one CTA per SM, each owning one contiguous
-//     range of (row-block, k-tile) iterations, so every SM streams the same
-//     number of A bytes. A range that ends inside a row block writes an fp32
-//     partial to slot = row_block + cta (unique along the monotone staircase);
-//     the pass epilogue sums a row block's slots in CTA order (deterministic).
+//   * CTA pairs (thread-block clusters of 2) own adjacent 256-row blocks and walk
+//     the same k-tiles in lockstep: each CTA TMA-loads half of the V tile and
+//     multicasts it to both, so V leaves L2 once per 512 rows (L2 traffic
+//     ~1.08x the A stream in fast mode, ~1.16x in split mode). A stage is
+//     released only when both CTAs' MMAs are done (multicast commit, count 2).
+//   * Persistent stream-K schedule over pairs: one CTA per SM, each pair owning
+//     one contiguous range of (row-block-pair, k-tile) iterations, so every SM
+//     streams the same number of A bytes. A range that ends inside a row block
+//     writes an fp32 partial to slot = 2·(pair_block + pair) + rank (unique
+//     along the monotone staircase); the pass epilogue sums a row block's slots
+//     in pair order (deterministic).
 //   * The tensor core's fp32 accumulation is lossy over long K (measured on
 //     B200: 1e-4 rms at K=1e5 with Gaussian operands), so TMEM accumulation
 //     is chunked (kc k-tiles) and drained into fp32 registers with
 //     round-to-nearest adds; two accumulator sets double-buffer the drain.
 //   * Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM owner),
 //     warps 2..9 = TMEM drain (4 per M=128 tile) and partial writers.
+#include <algorithm>
 #include <cstdio>
 #include <cuda_fp16.h>
 
@@ -41,6 +48,10 @@ constexpr int BM = 256;  // rows per CTA (two UMMA M=128 tiles)
 constexpr int TM = 128;  // UMMA M
 constexpr int BK = 32;   // K per stage: one 64-byte swizzle row of fp16
 constexpr int kThreads = 320;
+#ifndef RB_SMEM_BUDGET_KB
+#define RB_SMEM_BUDGET_KB 220
+#endif
+constexpr int kSmemBudget = RB_SMEM_BUDGET_KB;  // KB of dynamic smem for the TMA ring
 
 template <int NPAD, bool VSPLIT>
 struct TcCfg {
@@ -49,7 +60,7 @@ struct TcCfg {
     static constexpr int kVPlane = NPAD * BK * 2;
     static constexpr int kVBytes = (VSPLIT ? 2 : 1) * kVPlane;
     static constexpr int kStageBytes = 2 * kAPlane + kVBytes;
-    static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+    static constexpr int kStagesRaw = (kSmemBudget * 1024) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kAccCols = (VSPLIT ? 2 : 1) * NPAD;              // accumulator width per tile
     static constexpr int kBufs = (2 * 2 * kAccCols <= 512) ? 2 : 1;         // double-buffer the drain if it fits
@@ -67,6 +78,7 @@ struct TcArgs {
     int k_tiles;          // k tiles per row block
     int kc;               // k tiles per TMEM chunk
     float* partial;       // [slots][NPAD][BM]
+    int a_policy;         // 0: evict_first for the A stream, 1: evict_normal
 };
 
 // UMMA shared-memory descriptor: K-major, 64-byte swizzle (rows of 64 bytes, 8-row atoms of 512 bytes).
@@ -81,7 +93,7 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t smem_addr) {
 }
 
 template <int NPAD, bool VSPLIT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     block_av_tc_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                        const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_vlo,
                        TcArgs args) {
@@ -95,14 +107,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
-    const int G = gridDim.x;
-    const int cta = blockIdx.x;
+    const int G = gridDim.x / 2;  // CTA pairs
+    const int pair = blockIdx.x / 2;
+    const int rank = static_cast<int>(cluster_ctarank());
 
     const uint32_t smem_base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem_base = smem_raw + (smem_base_u32 - smem_u32(smem_raw));
 
-    const int64_t it_begin = (args.total_iters * cta) / G;
-    const int64_t it_end = (args.total_iters * (cta + 1)) / G;
+    // iterations are (row-block-pair, k-tile); this CTA serves row block 2*rp + rank
+    const int64_t it_begin = (args.total_iters * pair) / G;
+    const int64_t it_end = (args.total_iters * (pair + 1)) / G;
     const int KT = args.k_tiles;
 
     if (warp == 0 && lane == 0) {
@@ -112,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (VSPLIT) prefetch_tmap(&map_vlo);
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
+            mbar_init(&empty_bar[s], 2);  // released by both CTAs' MMAs
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full_bar[b], 1);
@@ -123,27 +137,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_alloc(&tmem_base_smem, C::kTmemCols);
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // peer barriers are initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = tmem_base_smem;
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            const uint64_t pol_stream = policy_evict_first();
+            const uint64_t pol_stream = args.a_policy ? policy_evict_normal() : policy_evict_first();
             const uint64_t pol_keep = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t it = it_begin; it < it_end; ++it) {
-                const int r = static_cast<int>(it / KT);
-                const int k = static_cast<int>(it - static_cast<int64_t>(r) * KT);
-                mbar_wait(&empty_bar[stage], phase ^ 1u);
+                const int rp = static_cast<int>(it / KT);
+                const int k = static_cast<int>(it - static_cast<int64_t>(rp) * KT);
+                const int r = 2 * rp + rank;
+                mbar_wait(&empty_bar[stage], phase ^ 1u);  // both CTAs released this stage
                 uint8_t* st = smem_base + stage * C::kStageBytes;
                 mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
                 tma_load_2d(st, &map_ahi, &full_bar[stage], k * BK, r * BM, pol_stream);
                 tma_load_2d(st + C::kAPlane, &map_alo, &full_bar[stage], k * BK, r * BM, pol_stream);
-                tma_load_2d(st + 2 * C::kAPlane, &map_v, &full_bar[stage], k * BK, 0, pol_keep);
-                if (VSPLIT)
-                    tma_load_2d(st + 2 * C::kAPlane + C::kVPlane, &map_vlo, &full_bar[stage], k * BK, 0, pol_keep);
+                if (VSPLIT) {  // rank 0 multicasts V_hi, rank 1 V_lo
+                    tma_load_2d_mc(st + 2 * C::kAPlane + rank * C::kVPlane, rank ? &map_vlo : &map_v,
+                                   &full_bar[stage], k * BK, 0, 0x3, pol_keep);
+                } else {  // each rank multicasts half of the V rows
+                    tma_load_2d_mc(st + 2 * C::kAPlane + rank * (C::kVPlane / 2), &map_v, &full_bar[stage], k * BK,
+                                   rank * (NPAD / 2), 0x3, pol_keep);
+                }
                 if (++stage == C::kStages) {
                     stage = 0;
                     phase ^= 1u;
@@ -160,8 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t chunk = 0;
             int64_t it = it_begin;
             while (it < it_end) {
-                const int64_t r = it / KT;
-                const int64_t seg_end = min(it_end, (r + 1) * KT);
+                const int64_t rp = it / KT;
+                const int64_t seg_end = min(it_end, (rp + 1) * KT);
                 while (it < seg_end) {
                     const int64_t cend = min(seg_end, it + args.kc);
                     const uint32_t buf = chunk % C::kBufs;
@@ -188,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 umma_f16(d, desc_sw64(st + C::kAPlane + t * C::kATile + off), dv, idesc, 1u);
                             }
                         }
-                        umma_commit(&empty_bar[stage]);
+                        umma_commit_mc(&empty_bar[stage], 0x3);  // release the stage in both CTAs
                         if (++stage == C::kStages) {
                             stage = 0;
                             phase ^= 1u;
@@ -211,8 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t chunk = 0;
         int64_t it = it_begin;
         while (it < it_end) {
-            const int64_t r = it / KT;
-            const int64_t seg_end = min(it_end, (r + 1) * KT);
+            const int64_t rp = it / KT;
+            const int64_t seg_end = min(it_end, (rp + 1) * KT);
             while (it < seg_end) {
                 const int64_t cend = min(seg_end, it + args.kc);
                 const uint32_t buf = chunk % C::kBufs;
@@ -241,8 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 it = cend;
                 ++chunk;
             }
-            // segment finished: publish the partial for row block r
-            const int64_t slot = r + cta;
+            // segment finished: publish the partial for row block 2*rp + rank
+            const int64_t slot = 2 * (rp + pair) + rank;
             float* dst = args.partial + (slot * NPAD) * BM + row_local;
 #pragma unroll
             for (int j = 0; j < NPAD; ++j) {
@@ -254,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
     if (warp == 1) tmem_dealloc(tmem_base, C::kTmemCols);
 }
 
@@ -275,7 +296,8 @@ EncodeFn get_encode() {
 }
 
 bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
-                  uint32_t box_inner, uint32_t box_outer) {
+                  uint32_t box_inner, uint32_t box_outer,
+                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
     EncodeFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
@@ -283,7 +305,7 @@ bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -293,10 +315,15 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
                       cudaStream_t stream) {
     using C = TcCfg<NPAD, VSPLIT>;
     CUtensorMap m_ahi, m_alo, m_v, m_vlo;
-    bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM) &&
-              make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM) &&
-              make_map_f16(&m_v, v.v, v.n, v.cols, v.ld * 2ull, BK, NPAD) &&
-              make_map_f16(&m_vlo, VSPLIT ? v.vlo : v.v, v.n, v.cols, v.ld * 2ull, BK, NPAD);
+    // split: one CTA of the pair loads V_hi, the other V_lo; fast: each loads half of V's rows
+    const uint32_t vbox = VSPLIT ? NPAD : NPAD / 2;
+    // measured on B200 (r1): 256-byte L2 promotion + evict_first for the A stream beats no/128-byte
+    // promotion and evict_normal by 1-2%
+    const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM, promo) &&
+              make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM, promo) &&
+              make_map_f16(&m_v, v.v, v.n, v.cols, v.ld * 2ull, BK, vbox) &&
+              make_map_f16(&m_vlo, VSPLIT ? v.vlo : v.v, v.n, v.cols, v.ld * 2ull, BK, vbox);
     if (!ok) return cudaErrorInvalidValue;
     static bool attr_done = false;
     if (!attr_done) {
@@ -310,7 +337,9 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     args.k_tiles = plan.k_tiles;
     args.kc = plan.kc;
     args.partial = partial;
-    block_av_tc_kernel<NPAD, VSPLIT><<<plan.grid, kThreads, C::kSmemBytes, stream>>>(m_ahi, m_alo, m_v, m_vlo, args);
+    args.a_policy = 0;
+    block_av_tc_kernel<NPAD, VSPLIT><<<2 * plan.grid, kThreads, C::kSmemBytes, stream>>>(m_ahi, m_alo, m_v, m_vlo,
+                                                                                       args);
     return cudaGetLastError();
 }
 
@@ -320,14 +349,18 @@ int tc_block_rows() { return BM; }
 int tc_block_k() { return BK; }
 
 StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc) {
+    // grid = CTAs (rounded down to pairs); iterations are (row-block-pair, k-tile)
     StreamKPlan p;
     p.row_blocks = static_cast<int>((rows + BM - 1) / BM);
     p.k_tiles = static_cast<int>((cols + BK - 1) / BK);
-    p.total_iters = static_cast<int64_t>(p.row_blocks) * p.k_tiles;
-    p.grid = grid;
-    if (p.total_iters < grid) p.grid = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
+    const int64_t pair_blocks = (p.row_blocks + 1) / 2;
+    p.total_iters = pair_blocks * p.k_tiles;
+    int pairs = std::max(1, grid / 2);
+    if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
+    p.grid = pairs;  // stream-K participants (pairs)
+    p.cluster = 2;
     p.kc = kc;
-    p.slots = p.row_blocks + p.grid;
+    p.slots = static_cast<int>(2 * (pair_blocks + pairs));
     p.rows_per_block = BM;
     return p;
 }

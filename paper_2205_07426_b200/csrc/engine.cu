@@ -523,6 +523,7 @@ public:
             e.partial = ctx_.partial.as<float>();
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
+            e.cluster = plan_.cluster;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.e_cur = ctx_.eexp.as<int>() + k * s;
             e.e_next = ctx_.eexp.as<int>() + (k + 1) * s;
@@ -552,6 +553,7 @@ public:
             e.partial = ctx_.partial.as<double>();
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
+            e.cluster = plan_.cluster;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.unscale = 1.0;
             e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;

@@ -40,6 +40,7 @@ struct StreamKPlan {
     int kc = 16;
     int slots = 0;
     int rows_per_block = 256;
+    int cluster = 1;  // row blocks per stream-K participant (2: CTA pairs)
 };
 
 // ---- block product -------------------------------------------------------
@@ -63,6 +64,7 @@ struct EpiArgs {
     int64_t total_iters;
     int k_tiles;
     int grid;
+    int cluster;   // slot(r, p) = cluster*(r/cluster + p) + r%cluster
     int64_t rows;  // local rows (product rows)
     int rows_per_block;  // 256 (tensor-core path) or 128 (fp64 path)
     int s;

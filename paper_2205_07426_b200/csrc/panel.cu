@@ -53,14 +53,15 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     const int64_t i = static_cast<int64_t>(r) * ER + tid;
     const bool valid = i < p.rows;
     const int64_t KT = p.k_tiles;
-    const int64_t c_lo = streamk_owner(static_cast<int64_t>(r) * KT, p.total_iters, p.grid);
-    const int64_t c_hi = streamk_owner(static_cast<int64_t>(r + 1) * KT - 1, p.total_iters, p.grid);
+    const int64_t cl = p.cluster, rb = r / cl, rr = r % cl;
+    const int64_t c_lo = streamk_owner(rb * KT, p.total_iters, p.grid);
+    const int64_t c_hi = streamk_owner((rb + 1) * KT - 1, p.total_iters, p.grid);
     const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
 
     for (int j = 0; j < p.s; ++j) {
         double y = 0.0;
         for (int64_t c = c_lo; c <= c_hi; ++c)
-            y += static_cast<double>(p.partial[((r + c) * p.npad + j) * ER + tid]);
+            y += static_cast<double>(p.partial[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
         if (SPLIT) y = ldexp(y * p.unscale, -p.e_cur[j]);
         double tc = 0.0, tp = 0.0, x0 = 0.0;
         const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
