@@ -107,3 +107,17 @@ def test_spec_validation(R):  # poly.cpp:60-80
         R.MatrixFunctionSpec.chebyshev(0.5, 0, 0.0, 1.0)
     with pytest.raises(R.RenyiError):
         R.MatrixFunctionSpec.int_power(0)
+
+
+def test_cpp_mirror_compiles_links_and_runs(tmp_path):
+    """include/renyi_b200.hpp builds against the C ABI with plain g++ (reference toolchain)."""
+    import subprocess
+
+    exe = tmp_path / "example_host"
+    lib_dir = ROOT / "paper_2205_07426_b200"
+    r = subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{ROOT / 'include'}",
+                        str(ROOT / "tests" / "cpp" / "example_host.cpp"), f"-L{lib_dir}", "-lrenyi_b200",
+                        f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
