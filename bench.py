@@ -17,7 +17,7 @@ roofline: dominant kernel = the tcgen05 block product Y = A·V; algorithmic
           itself is unbuildable here) on a bounded row-slab sample of the same
           workload, extrapolated per estimate
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n N]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--samples N]
 """
 from __future__ import annotations
 
@@ -46,13 +46,16 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=0, help="override n (default: config 4's 100000)")
+    p.add_argument("--samples", type=int, default=0, help="override n (default: config 4 n = 100000)")
     p.add_argument("--seed", type=int, default=2205)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--operand", default="split", choices=["split", "fast"],
                    help="iterate operand of the block product: fp16 hi+lo (split) or hi only (fast)")
     p.add_argument("--kc", type=int, default=16, help="k tiles (x32 columns) per TMEM accumulation chunk")
+    p.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                   help="N > 1: row-shard one estimate over all ranks (NCCL, strong scaling) or run "
+                        "independent replicas (weak scaling)")
     return p.parse_args()
 
 
@@ -165,7 +168,7 @@ def run_reference(args):
     from workloads import f32, mi_inputs
 
     oracle.build()
-    n = args.n or 100000
+    n = args.samples or 100000
     x, y = mi_inputs(n, args.seed)
     x, y = f32(x), f32(y)
     sx, sy = 4.0, math.sqrt(8.0)
@@ -211,17 +214,28 @@ def run_ours(args):
     import paper_2205_07426_b200 as R
     from workloads import f32, mi_inputs
 
-    n = args.n or 100000
+    n = args.samples or 100000
     dx, dy = 16, 8
     sx, sy = R.GaussianKernel(4.0), R.GaussianKernel(math.sqrt(8.0))
-    # each rank owns independent MI estimates (its own seeded X, Y): weak scaling
-    x, y = mi_inputs(n, args.seed + 7919 * rank)
+    sharded = world > 1 and args.mode == "sharded"
+    # sharded: every rank holds the same X, Y and rows [row0, row0+rows) of each A (one estimate
+    # per step over all ranks, strong scaling); replicas: each rank its own seeded X, Y (weak scaling)
+    salt = 0 if sharded else 7919 * rank
+    x, y = mi_inputs(n, args.seed + salt)
     x, y = f32(x), f32(y)
-    params = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60, seed=args.seed + rank,
+    params = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60, seed=args.seed + (0 if sharded else rank),
                                bounds=R.SpectrumBounds(u=0.0, v=1.0))
     ctx = R.Context(local)
     ctx.set_tuning(0, args.kc)
     ctx.set_operand_mode(args.operand)
+    if sharded:
+        import torch
+
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0)
+        ctx.init_nccl(rank, world, bytes(uid.cpu().numpy().tobytes()))
     d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()  # (dx, n) row-major == column-major n x dx
     d_y = torch.from_numpy(np.ascontiguousarray(y.T)).cuda()
     torch.cuda.synchronize()
@@ -257,7 +271,8 @@ def run_ours(args):
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = 3.0 * args.steps * world / (ms / 1e3)
+    units = 1 if sharded else world  # MI estimates completed per step over the whole job
+    value = 3.0 * args.steps * units / (ms / 1e3)
 
     # ---- end to end through the public C-ABI call with host buffers ----
     e2e = None
@@ -275,7 +290,7 @@ def run_ours(args):
             t = torch.tensor([wall], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        e2e = {"value": 3.0 * args.steps * world / wall, "unit": "estimates/s",
+        e2e = {"value": 3.0 * args.steps * units / wall, "unit": "estimates/s",
                "h2d_bytes_per_step": (h1 - h0) // args.steps, "d2h_bytes_per_step": (d1 - d0) // args.steps,
                "ms_per_step": wall * 1e3 / args.steps}
 
@@ -311,7 +326,8 @@ def run_ours(args):
     line = {
         "metric": "entropy estimates/sec at n=100k (config 4 MI: 3 estimates per step)",
         "value": value, "unit": "estimates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None,
         "dtype": "f32",
         "dtype_note": ("A stored as an fp16 hi/lo split of A*n*2^14 (4 B/entry, 22-bit significand); iterate "
                        + ("fp16 hi+lo (3 tcgen05 products)" if args.operand == "split" else "fp16 hi (2 products)")
@@ -322,7 +338,10 @@ def run_ours(args):
                                "Hutch++ s=90 (reference split 22+46), Gaussian probes drawn on device",
                    "n": n, "estimates_per_step": 3, "operand": args.operand, "kc": args.kc,
                    "l2": "inputs larger than L2: each A is 40 GB (n^2 x 4 B) vs 126 MB L2",
-                   "parallelism": f"replicas x{world} (one independent MI estimate per rank, no collective)"},
+                   "parallelism": (f"rowshard x{world}: A split by rows, NCCL all-gather of the operand planes "
+                                   "per pass, fp64 trace partials all-reduced per estimate") if sharded else
+                                  (f"replicas x{world} (one independent MI estimate per rank, no collective)"
+                                   if world > 1 else "single GPU")},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

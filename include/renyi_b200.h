@@ -60,6 +60,7 @@ enum { RENYI_MATFUN_INT_POWER = 0, RENYI_MATFUN_TAYLOR = 1, RENYI_MATFUN_CHEBYSH
 
 typedef struct renyi_ctx renyi_ctx;
 typedef struct renyi_kernel renyi_kernel;
+typedef struct renyi_local_group renyi_local_group;
 
 /* MatrixFunctionSpec::{int_power,taylor,chebyshev} arguments; coefficients
  * (binomials, Chebyshev node sums, safeguard) are derived inside exactly as the
@@ -149,6 +150,19 @@ int renyi_ctx_io_bytes(renyi_ctx* ctx, long long* h2d, long long* d2h);
 /* CUDA-event region timer on the engine stream */
 int renyi_ctx_timer_begin(renyi_ctx* ctx);
 int renyi_ctx_timer_end(renyi_ctx* ctx, double* milliseconds);
+
+/* ---- multi-rank (row-sharded A) -------------------------------
+ * One context per rank. After joining, kernel matrices built on the context hold
+ * rows [row0, row0+rows) of A and every estimator call is collective over the
+ * group (same arguments on every rank; results identical on every rank). */
+int renyi_shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* rows_per_rank);
+int renyi_nccl_unique_id(unsigned char id[128]);
+int renyi_ctx_init_nccl(renyi_ctx* ctx, int rank, int world, const unsigned char id[128]);
+/* ranks as threads of one process (host-driven collectives; any devices) */
+int renyi_local_group_create(int world, renyi_local_group** out);
+int renyi_local_group_destroy(renyi_local_group* g);
+int renyi_ctx_join_local_group(renyi_ctx* ctx, renyi_local_group* g, int rank);
+int renyi_ctx_rank(renyi_ctx* ctx, int* rank, int* world);
 
 /* ---- kernel matrices (proj/include/renyi/kernel.hpp:45-56) --------------- */
 /* build_kernel(X, GaussianKernel{sigma}) — proj/src/kernel.cpp:35-72 + ops.cpp:39-47 */

@@ -154,6 +154,13 @@ SIGNATURES = {
     "renyi_ctx_timer_begin": (C.c_int, [_P]),
     "renyi_ctx_timer_end": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "renyi_ctx_launch_count": (C.c_int, [_P, C.POINTER(C.c_long)]),
+    "renyi_shard_rows": (C.c_int, [_I64, C.c_int, C.c_int, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64)]),
+    "renyi_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "renyi_ctx_init_nccl": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
+    "renyi_local_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "renyi_local_group_destroy": (C.c_int, [_P]),
+    "renyi_ctx_join_local_group": (C.c_int, [_P, _P, C.c_int]),
+    "renyi_ctx_rank": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "renyi_kernel_build_gaussian": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)]),
     "renyi_kernel_build_gaussian_joint": (
         C.c_int,

@@ -84,6 +84,20 @@ class Context:
         check(L.lib().renyi_ctx_timer_end(self._h, C.byref(ms)))
         return ms.value
 
+    def init_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
+        """Join an NCCL group (one process per GPU); unique_id from nccl_unique_id() on rank 0."""
+        if len(unique_id) != 128:
+            raise RenyiError(1, "NCCL unique id must be 128 bytes")
+        check(L.lib().renyi_ctx_init_nccl(self._h, rank, world, unique_id))
+
+    def join_local_group(self, group: "LocalGroup", rank: int) -> None:
+        check(L.lib().renyi_ctx_join_local_group(self._h, group.handle, rank))
+
+    def rank_world(self):
+        r, w = C.c_int(), C.c_int()
+        check(L.lib().renyi_ctx_rank(self._h, C.byref(r), C.byref(w)))
+        return r.value, w.value
+
     def launch_count(self) -> int:
         n = C.c_long()
         check(L.lib().renyi_ctx_launch_count(self._h, C.byref(n)))
@@ -99,6 +113,41 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class LocalGroup:
+    """Ranks as threads of this process (host-driven collectives), e.g. to validate the sharded path."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(L.lib().renyi_local_group_create(world, C.byref(h)))
+        self._h = h
+        self.world = world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                L.lib().renyi_local_group_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(L.lib().renyi_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """(row0, rows, rows_per_rank) of this rank's row block of A."""
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    check(L.lib().renyi_shard_rows(n, world, rank, C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, c.value
 
 
 def release_cached_memory() -> None:

@@ -76,6 +76,7 @@ struct TcCfg {
 struct TcArgs {
     int64_t total_iters;  // row_blocks * k_tiles
     int k_tiles;          // k tiles per row block
+    int kt_chunk;         // k tiles per V chunk (rpr / BK)
     int kc;               // k tiles per TMEM chunk
     float* partial;       // [slots][NPAD][BM]
     int a_policy;         // 0: evict_first for the A stream, 1: evict_normal
@@ -157,12 +158,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
                 tma_load_2d(st, &map_ahi, &full_bar[stage], k * BK, r * BM, pol_stream);
                 tma_load_2d(st + C::kAPlane, &map_alo, &full_bar[stage], k * BK, r * BM, pol_stream);
+                const int vz = k / args.kt_chunk;               // V chunk (shard) holding these K rows
+                const int vx = (k - vz * args.kt_chunk) * BK;   // offset inside the chunk
                 if (VSPLIT) {  // rank 0 multicasts V_hi, rank 1 V_lo
-                    tma_load_2d_mc(st + 2 * C::kAPlane + rank * C::kVPlane, rank ? &map_vlo : &map_v,
-                                   &full_bar[stage], k * BK, 0, 0x3, pol_keep);
+                    tma_load_3d_mc(st + 2 * C::kAPlane + rank * C::kVPlane, rank ? &map_vlo : &map_v,
+                                   &full_bar[stage], vx, 0, vz, 0x3, pol_keep);
                 } else {  // each rank multicasts half of the V rows
-                    tma_load_2d_mc(st + 2 * C::kAPlane + rank * (C::kVPlane / 2), &map_v, &full_bar[stage], k * BK,
-                                   rank * (NPAD / 2), 0x3, pol_keep);
+                    tma_load_3d_mc(st + 2 * C::kAPlane + rank * (C::kVPlane / 2), &map_v, &full_bar[stage], vx,
+                                   rank * (NPAD / 2), vz, 0x3, pol_keep);
                 }
                 if (++stage == C::kStages) {
                     stage = 0;
@@ -310,6 +313,19 @@ bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
     return r == CUDA_SUCCESS;
 }
 
+bool make_map_v3(CUtensorMap* m, const void* base, uint64_t rpr, uint64_t cols, uint64_t world, uint32_t box_rows) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {rpr, cols, world};
+    cuuint64_t strides[2] = {rpr * 2ull, rpr * cols * 2ull};
+    cuuint32_t box[3] = {BK, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <int NPAD, bool VSPLIT>
 cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan, float* partial,
                       cudaStream_t stream) {
@@ -322,8 +338,9 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM, promo) &&
               make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM, promo) &&
-              make_map_f16(&m_v, v.v, v.n, v.cols, v.ld * 2ull, BK, vbox) &&
-              make_map_f16(&m_vlo, VSPLIT ? v.vlo : v.v, v.n, v.cols, v.ld * 2ull, BK, vbox);
+              make_map_v3(&m_v, v.v, v.rpr, v.cols, v.world, vbox) &&
+              make_map_v3(&m_vlo, VSPLIT ? v.vlo : v.v, v.rpr, v.cols, v.world, vbox);
+    if (v.rpr % BK != 0) return cudaErrorInvalidValue;
     if (!ok) return cudaErrorInvalidValue;
     static bool attr_done = false;
     if (!attr_done) {
@@ -335,6 +352,7 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     TcArgs args;
     args.total_iters = plan.total_iters;
     args.k_tiles = plan.k_tiles;
+    args.kt_chunk = static_cast<int>(v.rpr / BK);
     args.kc = plan.kc;
     args.partial = partial;
     args.a_policy = 0;

@@ -21,6 +21,10 @@ struct renyi_kernel {
     rb::KernelPtr k;
 };
 
+struct renyi_local_group {
+    std::shared_ptr<rb::LocalGroup> g;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -155,6 +159,56 @@ int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc) {
         if (grid < 0 || kc < 1) rb::fail(rb::kInvalidArgument, "grid >= 0 and kc >= 1 required");
         ctx->ctx.grid = grid;
         ctx->ctx.kc = kc;
+    });
+}
+
+int renyi_shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* rpr) {
+    return guarded([&] {
+        need(row0, "row0"), need(rows, "rows"), need(rpr, "rows_per_rank");
+        rb::shard_rows(n, world, rank, row0, rows, rpr);
+    });
+}
+
+int renyi_nccl_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        need(id, "id");
+        rb::nccl_unique_id(id);
+    });
+}
+
+int renyi_ctx_init_nccl(renyi_ctx* ctx, int rank, int world, const unsigned char id[128]) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(id, "id");
+        cudaSetDevice(ctx->ctx.device());
+        ctx->ctx.exchange = rb::make_nccl_exchange(rank, world, id);
+    });
+}
+
+int renyi_local_group_create(int world, renyi_local_group** out) {
+    return guarded([&] {
+        need(out, "out");
+        auto* g = new renyi_local_group;
+        g->g = rb::make_local_group(world);
+        *out = g;
+    });
+}
+
+int renyi_local_group_destroy(renyi_local_group* g) {
+    return guarded([&] { delete g; });
+}
+
+int renyi_ctx_join_local_group(renyi_ctx* ctx, renyi_local_group* g, int rank) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(g, "group");
+        ctx->ctx.exchange = rb::make_local_exchange(g->g, rank);
+    });
+}
+
+int renyi_ctx_rank(renyi_ctx* ctx, int* rank, int* world) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        if (rank) *rank = ctx->ctx.rank();
+        if (world) *world = ctx->ctx.world();
     });
 }
 

@@ -234,19 +234,23 @@ void check_finite(const double* x, int64_t n, int64_t d, int64_t ld, double* max
     *max_abs = mx;
 }
 
-void shard_rows(Context& ctx, int64_t n, int64_t* row0, int64_t* rows) {
-    if (!ctx.exchange || ctx.exchange->world() == 1) {
-        *row0 = 0, *rows = n;
-        return;
-    }
-    const int r = ctx.exchange->rank(), w = ctx.exchange->world();
-    // equal shards (multiple of 128 rows except the last) so the all-gather is uniform
-    const int64_t per = round_up((n + w - 1) / w, 128);
-    *row0 = std::min<int64_t>(n, per * r);
-    *rows = std::min<int64_t>(n, per * (r + 1)) - *row0;
+void assign_shard(Context& ctx, KernelMatrix& k) {
+    k.world = ctx.world();
+    k.rank = ctx.rank();
+    shard_rows(k.n, k.world, k.rank, &k.row0, &k.rows, &k.rpr);
 }
 
 }  // namespace
+
+void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* rpr) {
+    if (world < 1 || rank < 0 || rank >= world) fail(kInvalidArgument, "bad rank/world");
+    // equal chunks (a multiple of 256 rows = one block-product row block; the last chunk shorter)
+    // so the per-pass all-gather of the operand planes is uniform
+    const int64_t per = round_up((n + world - 1) / world, 256);
+    *rpr = per;
+    *row0 = std::min<int64_t>(n, per * rank);
+    *rows = std::min<int64_t>(n, per * (rank + 1)) - *row0;
+}
 
 // ---------------------------------------------------------------- kernel matrices
 KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
@@ -298,7 +302,8 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
     auto k = std::make_unique<KernelMatrix>();
     k->n = n;
     k->prec = prec;
-    shard_rows(ctx, n, &k->row0, &k->rows);
+    assign_shard(ctx, *k);
+    if (prec == kF64 && k->world > 1) fail(kInvalidArgument, "the fp64 configuration is single-rank");
     k->ld = round_up(n, 8);
     const double inv_n = 1.0 / static_cast<double>(n);
     k->normalized = true;
@@ -338,7 +343,8 @@ KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
     auto k = std::make_unique<KernelMatrix>();
     k->n = n;
     k->prec = prec;
-    shard_rows(ctx, n, &k->row0, &k->rows);
+    assign_shard(ctx, *k);
+    if (prec == kF64 && k->world > 1) fail(kInvalidArgument, "the fp64 configuration is single-rank");
     k->ld = round_up(n, 8);
     k->normalized = false;
     std::vector<double> rm(static_cast<size_t>(k->rows) * k->ld, 0.0);
@@ -396,6 +402,7 @@ KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     auto c = std::make_unique<KernelMatrix>();
     c->n = a.n, c->row0 = a.row0, c->rows = a.rows, c->ld = a.ld, c->prec = a.prec;
+    c->rpr = a.rpr, c->world = a.world, c->rank = a.rank;
     const double nd = static_cast<double>(a.n);
     const double inv_n = 1.0 / nd;
     // |n A_ij B_ij| row sums: <= n * max|B| * ||A||_inf (<= 1 for normalised factors)
@@ -455,10 +462,10 @@ public:
                  double* acc_out, double acc_coef0)
         : ctx_(ctx), k_(k), s_(s), max_passes_(max_passes), acc_(acc_out) {
         if (s < 1 || s > kMaxPanelCols) fail(kInternal, "panel width must be in [1,128]");
-        if (ctx.exchange && ctx.exchange->world() > 1 && k.rows != k.n)
-            fail(kInvalidArgument, "row-sharded panels need the multi-rank exchange path");
+        if (k.world != ctx.world() || k.rank != ctx.rank())
+            fail(kInvalidArgument, "kernel matrix was built for a different rank layout");
         rows_ = k.rows;
-        ld_ = round_up(k.n, 8);
+        ld_ = k.rpr;  // state [s][rpr] (local rows); operand planes [world][s][rpr]
         if (k.prec == kF32) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
             plan_ = make_streamk_plan(rows_, k.n, grid, ctx.kc);
@@ -472,12 +479,20 @@ public:
         const size_t st = k.prec == kF32 ? sizeof(float) : sizeof(double);
         for (auto& b : ctx.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
         if (k.prec == kF32) {
-            ctx.vhi.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
-            if (ctx.operand_split) ctx.vlo.ensure(static_cast<size_t>(s) * ld_ * sizeof(__half));
+            const size_t plane = static_cast<size_t>(k.world) * s * ld_ * sizeof(__half);
+            ctx.vhi.ensure(plane);
+            // rows past n in the last chunk are never written: keep them zero (A's columns there are
+            // TMA-zero, but 0 x garbage could be NaN)
+            cuda_check(cudaMemsetAsync(ctx.vhi.as<__half>(), 0, plane, ctx.stream()), "memset");
+            if (ctx.operand_split) {
+                ctx.vlo.ensure(plane);
+                cuda_check(cudaMemsetAsync(ctx.vlo.as<__half>(), 0, plane, ctx.stream()), "memset");
+            }
+            slice_ = static_cast<size_t>(k.rank) * s * ld_;
         }
         vlo_ = (k.prec == kF32 && ctx.operand_split) ? ctx.vlo.as<__half>() : nullptr;
         const size_t P1 = static_cast<size_t>(max_passes) + 1;
-        ctx.stats.ensure(P1 * 3 * R_ * s * sizeof(double));
+        ctx.stats.ensure(P1 * 3 * std::max(R_, 1) * s * sizeof(double));
         ctx.red.ensure(P1 * 3 * s * sizeof(double));
         ctx.cmax.ensure(P1 * s * sizeof(unsigned));
         ctx.eexp.ensure(P1 * s * sizeof(int));
@@ -490,10 +505,13 @@ public:
             p.cmax0 = ctx.cmax.as<unsigned>();
             p.stats = ctx.stats.as<double>();
             p.e0 = ctx.eexp.as<int>();
-            p.vop = ctx.vhi.as<__half>();
-            p.vop_lo = vlo_;
+            p.vop = ctx.vhi.as<__half>() + slice_;
+            p.vop_lo = vlo_ ? vlo_ + slice_ : nullptr;
             p.acc = acc_out, p.acc_coef = acc_coef0;
-            launched(ctx, launch_prepare_split(p, ctx.stream()), "prepare");
+            if (rows_ > 0) launched(ctx, launch_prepare_split_stats(p, ctx.stream()), "prepare");
+            if (ctx.exchange) ctx.exchange->allreduce_max_u32(ctx.cmax.as<unsigned>(), s, ctx.stream());
+            launched(ctx, launch_prepare_split_planes(p, ctx.stream()), "prepare");  // also writes e0
+            gather_planes();
         } else {
             ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(double));
             PrepArgs<double> p{};
@@ -506,15 +524,25 @@ public:
         }
     }
 
+    // all ranks' operand slices -> full planes (in place)
+    void gather_planes() {
+        if (!ctx_.exchange || k_.prec != kF32) return;
+        const size_t chunk = static_cast<size_t>(s_) * ld_ * sizeof(__half);
+        ctx_.exchange->allgather_inplace(ctx_.vhi.as<__half>(), chunk, ctx_.stream());
+        if (vlo_) ctx_.exchange->allgather_inplace(vlo_, chunk, ctx_.stream());
+    }
+
     void step(double a1, double a2, double a3, double acc_coef) {
         if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
         const int k = k_done_;
         const size_t s = static_cast<size_t>(s_);
         if (k_.prec == kF32) {
             SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
-            SplitPanelView v{ctx_.vhi.as<__half>(), vlo_, k_.n, s_, ld_};
+            SplitPanelView v{ctx_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world};
             ctx_.prof_begin();
-            launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()), "block_av_tc");
+            if (rows_ > 0)
+                launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
+                         "block_av_tc");
             ctx_.prof_end();
             // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
             ctx_.prof_account(4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_ + 4.0 * rows_ * s_,
@@ -536,11 +564,15 @@ public:
             e.t_prev = k > 0 ? buf<float>(k - 1) : nullptr;
             e.t_new = buf<float>(k + 1);
             e.x0 = buf<float>(0);
-            e.vop = ctx_.vhi.as<__half>();
-            e.vop_lo = vlo_;
+            e.vop = ctx_.vhi.as<__half>() + slice_;
+            e.vop_lo = vlo_ ? vlo_ + slice_ : nullptr;
             e.stats = ctx_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
             e.acc = acc_, e.acc_coef = acc_coef;
-            launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
+            if (rows_ > 0) launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
+            if (ctx_.exchange) {
+                ctx_.exchange->allreduce_max_u32(ctx_.cmax.as<unsigned>() + (k + 1) * s, s, ctx_.stream());
+                gather_planes();
+            }
         } else {
             ctx_.prof_begin();
             launched(ctx_,
@@ -575,10 +607,17 @@ public:
     std::vector<double> dots(int p0, int p1) {
         const int np = p1 - p0 + 1;
         const size_t s = static_cast<size_t>(s_);
-        launched(ctx_,
-                 launch_reduce_stats(ctx_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
-                                     ctx_.red.as<double>(), ctx_.stream()),
-                 "reduce_stats");
+        if (R_ > 0) {
+            launched(ctx_,
+                     launch_reduce_stats(ctx_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
+                                         ctx_.red.as<double>(), ctx_.stream()),
+                     "reduce_stats");
+        } else {
+            cuda_check(cudaMemsetAsync(ctx_.red.as<double>(), 0, np * 3 * s * sizeof(double), ctx_.stream()),
+                       "memset");
+        }
+        // row-separable trace partials: one sum over ranks
+        if (ctx_.exchange) ctx_.exchange->allreduce_sum_f64(ctx_.red.as<double>(), np * 3 * s, ctx_.stream());
         std::vector<double> out(static_cast<size_t>(np) * 3 * s);
         d2h(ctx_, out.data(), ctx_.red.as<double>(), out.size() * sizeof(double));
         ctx_.sync();
@@ -613,6 +652,7 @@ private:
     int npad_ = 0;
     int k_done_ = 0;
     __half* vlo_ = nullptr;
+    size_t slice_ = 0;  // this rank's chunk offset in the operand planes
     StreamKPlan plan_;
 };
 
@@ -690,13 +730,15 @@ void apply_panel(Context& ctx, const KernelMatrix& k, const MatFun& f, const dou
     for (int j0 = 0; j0 < s; j0 += kMaxPanelCols) {
         const int w = std::min(kMaxPanelCols, s - j0);
         upload_panel(ctx, ctx.x0, v + j0 * n, n, w, ld);
-        ctx.acc.ensure(static_cast<size_t>(w) * ld * sizeof(double));
+        // the vector accumulator shares the state layout [s][rpr]
+        ctx.acc.ensure(static_cast<size_t>(w) * k.rpr * sizeof(double));
         if (f.kind == kIntPower) {
-            run_panel(ctx, k, ctx.x0.as<double>(), ld, w, schedule(f), nullptr, nullptr, ctx.acc.as<double>(), ld);
+            run_panel(ctx, k, ctx.x0.as<double>(), ld, w, schedule(f), nullptr, nullptr, ctx.acc.as<double>(),
+                      k.rpr);
         } else {
             run_panel(ctx, k, ctx.x0.as<double>(), ld, w, schedule(f), &coef, ctx.acc.as<double>(), nullptr, 0);
         }
-        download_panel(ctx, ctx.acc.as<double>(), ld, n, w, y + j0 * n);
+        download_panel(ctx, ctx.acc.as<double>(), k.rpr, n, w, y + j0 * n);
         if (post != 1.0)
             for (int64_t i = 0; i < n * w; ++i) y[j0 * n + i] *= post;
     }
@@ -726,7 +768,7 @@ std::vector<double> panel_traces(Context& ctx, const KernelMatrix& k, const MatF
 void matfun_traces(Context& ctx, const KernelMatrix& k, const MatFun& f, const double* x, int s, double* out) {
     require_single_rank(ctx, "matfun_traces");
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
-    const int64_t n = k.n, ld = round_up(n, 8);
+    const int64_t n = k.n, ld = k.rpr;
     DevBuf xs;
     upload_panel(ctx, xs, x, n, s, ld);
     std::vector<double> tr = panel_traces(ctx, k, f, xs.as<double>(), ld, s);
@@ -737,13 +779,13 @@ void matfun_traces(Context& ctx, const KernelMatrix& k, const MatFun& f, const d
 PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, double shift) {
     // proj/src/spectrum.cpp:13-49; shift > 0 runs on (shift·I − A) without forming it
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
-    const int64_t n = k.n, ld = round_up(n, 8);
+    const int64_t ld = k.rpr;  // local rows of the start vector (row-sharded: counters from row0)
     ctx.x0.ensure(static_cast<size_t>(ld) * sizeof(double));
     cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
     const uint64_t key = derive_key(o.seed, hash_name("power-start"));
     launched(ctx,
-             launch_rng_panel(key, false, kProbeGaussian, n, 1, 0, ctx.x0.as<double>(), ld, ctx.probe_err.as<int>(),
-                              ctx.stream()),
+             launch_rng_panel(key, false, kProbeGaussian, k.row0, k.rows, 1, 0, ctx.x0.as<double>(), ld,
+                              ctx.probe_err.as<int>(), ctx.stream()),
              "rng_panel");
     PowerRes res;
     const int iters = std::max(o.max_iters, 0);
@@ -804,17 +846,19 @@ SpectrumBoundsH estimate_bounds(Context& ctx, const KernelMatrix& k, const Power
 namespace {
 
 // fp64 probe panel on the device [cols][ld]: injected host panel or the reference stream
-void make_probes(Context& ctx, DevBuf& dst, int64_t n, int cols, int64_t ld, const double* host, uint64_t seed,
-                 const char* label, int kind) {
+void make_probes(Context& ctx, const KernelMatrix& k, DevBuf& dst, int cols, int64_t ld, const double* host,
+                 uint64_t seed, const char* label, int kind) {
+    // this rank's rows [row0, row0 + rows) of the n x cols probe panel
     dst.ensure(static_cast<size_t>(cols) * ld * sizeof(double));
     if (host) {
-        upload_panel(ctx, dst, host, n, cols, ld);
+        h2d_2d(ctx, dst.as<double>(), ld * sizeof(double), host + k.row0, k.n * sizeof(double),
+               k.rows * sizeof(double), cols);
         return;
     }
     cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
     launched(ctx,
-             launch_rng_panel(derive_key(seed, hash_name(label)), true, kind, n, cols, 0, dst.as<double>(), ld,
-                              ctx.probe_err.as<int>(), ctx.stream()),
+             launch_rng_panel(derive_key(seed, hash_name(label)), true, kind, k.row0, k.rows, cols, 0,
+                              dst.as<double>(), ld, ctx.probe_err.as<int>(), ctx.stream()),
              "rng_panel");
     int err = 0;
     d2h(ctx, &err, ctx.probe_err.as<int>(), sizeof(int));
@@ -838,6 +882,8 @@ std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx,
                                    ctx.stream()),
                  "panel_gram");
     }
+    // Grams over row-sharded panels: one sum over ranks (CholeskyQR2 / projection)
+    if (ctx.exchange) ctx.exchange->allreduce_sum_f64(ctx.small.as<double>(), out.size(), ctx.stream());
     d2h(ctx, out.data(), ctx.small.as<double>(), out.size() * sizeof(double));
     ctx.sync();
     return out;
@@ -902,8 +948,8 @@ int orthonormal_range(Context& ctx, const double* y, int p, int64_t ld, int64_t 
 }
 
 double exact_trace(Context& ctx, const KernelMatrix& k, const MatFun& f) {
-    // proj/src/hutchpp.cpp:53-65: identity panels
-    const int64_t n = k.n, ld = round_up(n, 8);
+    // proj/src/hutchpp.cpp:53-65: identity panels (single rank)
+    const int64_t n = k.n, ld = k.rpr;
     double sum = 0.0;
     DevBuf eye;
     for (int64_t j0 = 0; j0 < n; j0 += kMaxPanelCols) {
@@ -920,15 +966,17 @@ double exact_trace(Context& ctx, const KernelMatrix& k, const MatFun& f) {
 }  // namespace
 
 TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const SketchCfg& cfg) {
-    // proj/src/hutchpp.cpp:69-115, with probe injection / explicit split / Q-empty Hutchinson
-    require_single_rank(ctx, "hutchpp");
+    // proj/src/hutchpp.cpp:69-115, with probe injection / explicit split / Q-empty Hutchinson.
+    // Row-sharded: every panel below holds this rank's rows; Grams are summed over ranks.
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
-    const int64_t n = k.n, ld = round_up(n, 8);
+    const int64_t n = k.n, ld = k.rpr, rows = k.rows;
+    const bool single = ctx.world() == 1;
     const int s_q = cfg.s_q, s_g = cfg.s_g;
     const int cost = f.query_cost();
     if (s_q < 0 || s_g < 0 || s_q + s_g < 1) fail(kInvalidArgument, "hutchpp needs a positive query budget");
     TraceEst est;
     if (s_q >= n) {
+        if (!single) fail(kInvalidArgument, "the exact-degeneration branch (s/4 >= n) is single-rank");
         est.value = est.low_rank_part = exact_trace(ctx, k, f);
         est.residual_part = 0.0;
         est.sketch_rank = static_cast<int>(n);
@@ -940,7 +988,7 @@ TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const Ske
     int rank = 0;
     if (s_q > 0) {
         DevBuf sk;
-        make_probes(ctx, sk, n, s_q, ld, cfg.sketch, cfg.seed, "hutchpp-sketch", cfg.probe_kind);
+        make_probes(ctx, k, sk, s_q, ld, cfg.sketch, cfg.seed, "hutchpp-sketch", cfg.probe_kind);
         DevBuf y;
         y.alloc(static_cast<size_t>(s_q) * ld * sizeof(double));
         for (int j0 = 0; j0 < s_q; j0 += kMaxPanelCols) {
@@ -948,7 +996,7 @@ TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const Ske
             run_panel(ctx, k, sk.as<double>() + j0 * ld, ld, w, {{1.0, 0.0, 0.0}}, nullptr, nullptr,
                       y.as<double>() + j0 * ld, ld);
         }
-        rank = orthonormal_range(ctx, y.as<double>(), s_q, ld, n, qbuf);
+        rank = orthonormal_range(ctx, y.as<double>(), s_q, ld, rows, qbuf);
         if (rank == 0) fail(kRankCollapse, "hutchpp sketch A*S is numerically zero");
         est.sketch_rank = rank;
         est.queries_used = s_q + rank * cost;
@@ -956,6 +1004,7 @@ TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const Ske
     const int64_t codim = n - rank;
     if (s_q > 0 && s_g >= codim) {
         // trace the complement exactly (proj/src/hutchpp.cpp:100-106)
+        if (!single) fail(kInvalidArgument, "the exact-complement branch (s_g >= n - rank) is single-rank");
         std::vector<double> qh(static_cast<size_t>(n) * rank);
         download_panel(ctx, qbuf.as<double>(), ld, n, rank, qh.data());
         std::vector<double> full = complete_basis(n, rank, qh);
@@ -981,11 +1030,11 @@ TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const Ske
         if (s_g > 0) {
             double* wdst = x0.as<double>() + static_cast<int64_t>(rank) * ld;
             DevBuf gp;
-            make_probes(ctx, gp, n, s_g, ld, cfg.probes, cfg.seed, "hutchpp-probe", cfg.probe_kind);
+            make_probes(ctx, k, gp, s_g, ld, cfg.probes, cfg.seed, "hutchpp-probe", cfg.probe_kind);
             if (rank > 0) {
-                std::vector<double> c = gram_host(ctx, qbuf.as<double>(), rank, ld, gp.as<double>(), s_g, ld, n);
+                std::vector<double> c = gram_host(ctx, qbuf.as<double>(), rank, ld, gp.as<double>(), s_g, ld, rows);
                 for (double& v : c) v = -v;
-                update(ctx, 1.0, gp.as<double>(), ld, qbuf.as<double>(), rank, ld, c, s_g, n, wdst, ld);
+                update(ctx, 1.0, gp.as<double>(), ld, qbuf.as<double>(), rank, ld, c, s_g, rows, wdst, ld);
             } else {
                 cuda_check(cudaMemcpyAsync(wdst, gp.as<double>(), static_cast<size_t>(s_g) * ld * sizeof(double),
                                            cudaMemcpyDeviceToDevice, ctx.stream()),

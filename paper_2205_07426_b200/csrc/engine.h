@@ -52,17 +52,26 @@ private:
     int dev_ = 0;
 };
 
-// Multi-rank exchange hooks (row-sharded A). nullptr = single rank.
+// Multi-rank exchange (row-sharded A). Context::exchange == nullptr: one rank.
 struct Exchange {
     virtual ~Exchange() = default;
     virtual int rank() const = 0;
     virtual int world() const = 0;
-    // gather equal-size row shards: each rank contributes `count` bytes at `send`
-    // into `recv` laid out [world][count] — used per column plane.
-    virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+    // buf holds `world` chunks of chunk_bytes; this rank's chunk (index rank) is in place
+    virtual void allgather_inplace(void* buf, size_t chunk_bytes, cudaStream_t s) = 0;
     virtual void allreduce_sum_f64(double* buf, size_t count, cudaStream_t s) = 0;
     virtual void allreduce_max_u32(unsigned* buf, size_t count, cudaStream_t s) = 0;
 };
+
+struct LocalGroup;
+std::shared_ptr<LocalGroup> make_local_group(int world);
+std::unique_ptr<Exchange> make_local_exchange(std::shared_ptr<LocalGroup> g, int rank);
+void nccl_unique_id(unsigned char* out128);
+std::unique_ptr<Exchange> make_nccl_exchange(int rank, int world, const unsigned char* id128);
+
+// Row shard of rank `rank` out of `world` for n rows: chunks of rpr rows (rpr a multiple of 256),
+// the last chunk shorter. world == 1: row0 = 0, rows = n, rpr = round_up(n, 256).
+void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* rpr);
 
 class Context {
 public:
@@ -92,7 +101,9 @@ public:
     void timer_begin();
     double timer_end_ms();  // synchronizes
 
-    Exchange* exchange = nullptr;
+    std::unique_ptr<Exchange> exchange;
+    int rank() const { return exchange ? exchange->rank() : 0; }
+    int world() const { return exchange ? exchange->world() : 1; }
 
     // scratch (grow-only)
     DevBuf partial, stats, red, cmax, eexp, gram_partial, small, probe_err;
@@ -113,6 +124,8 @@ struct KernelMatrix {
     int64_t n = 0;      // samples (columns)
     int64_t row0 = 0;   // first row held by this rank
     int64_t rows = 0;   // rows held by this rank
+    int64_t rpr = 0;    // rows per rank chunk (multiple of 256)
+    int world = 1, rank = 0;
     int64_t ld = 0;     // row pitch (elements)
     int prec = kF32;
     double unscale = 1.0;  // A = stored * unscale (split planes)

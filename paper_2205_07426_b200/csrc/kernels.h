@@ -24,12 +24,16 @@ struct SplitMatrixView {
     int64_t rows, cols, ld;
 };
 
-struct SplitPanelView {  // the iterate operand: fp16 hi (+ optional lo) planes, column-major n x cols
+// The iterate operand: fp16 hi (+ optional lo) planes laid out [world][cols][rpr]: rank w's
+// rows of every column are contiguous (the all-gather output layout); global row k lives
+// at chunk k / rpr, offset k % rpr. Single rank: [1][cols][rpr] = column-major with ld rpr.
+struct SplitPanelView {
     const __half* v;
     const __half* vlo;  // nullptr: "fast" operand mode (one plane, two MMAs)
     int64_t n;
     int cols;
-    int64_t ld;
+    int64_t rpr;  // rows per rank chunk (multiple of 256)
+    int world;
 };
 
 struct StreamKPlan {
@@ -109,7 +113,9 @@ struct PrepArgs {
     double* acc;  // optional: acc = acc_coef * t0
     double acc_coef;
 };
-cudaError_t launch_prepare_split(const PrepArgs<float>& a, cudaStream_t stream);
+// split into stats (T0, cmax0, dots) and planes (exponent from the — possibly all-reduced — cmax0)
+cudaError_t launch_prepare_split_stats(const PrepArgs<float>& a, cudaStream_t stream);
+cudaError_t launch_prepare_split_planes(const PrepArgs<float>& a, cudaStream_t stream);
 cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream);
 
 // out[p][q][j] = sum_r stats[p][q][r][j] (fixed order)
@@ -132,8 +138,9 @@ cudaError_t launch_panel_update(double beta, const double* g, int64_t ldg, const
 // Column j of the panel draws from RandomStream(derive_key(base_key, j0 + j)),
 // or from RandomStream(base_key) itself when derive == false (single column).
 // kind 0 = Gaussian (Box-Muller, reference stream order), 1 = Rademacher.
-cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t rows, int cols, int j0, double* out,
-                             int64_t ld, int* err_flag, cudaStream_t stream);
+// Rows [row0, row0 + rows) of the panel (row0 even: Gaussian draws come in Box-Muller pairs).
+cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t row0, int64_t rows, int cols, int j0,
+                             double* out, int64_t ld, int* err_flag, cudaStream_t stream);
 
 // ---- kernel-matrix construction --------------------------------------------
 // Gaussian Gram + trace normalisation (reference build_kernel for sigma):

@@ -10,6 +10,8 @@
 // column max |T_new| that sets the next pass's fp16 plane scale.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -255,7 +257,7 @@ __device__ __forceinline__ uint64_t dderive(uint64_t seed, uint64_t tag) {
     return dmix64(seed ^ dmix64(tag + 0x6a09e667f3bcc909ULL));
 }
 
-__global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64_t rows, int j0,
+__global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64_t row0, int64_t rows, int j0,
                                  double* __restrict__ out, int64_t ld, int* err) {
     const int j = blockIdx.y;
     const uint64_t key = derive ? dderive(base_key, static_cast<uint64_t>(j0 + j)) : base_key;
@@ -263,15 +265,15 @@ __global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64
     double* col = out + static_cast<int64_t>(j) * ld;
     if (kind == 1) {
         if (t >= rows) return;
-        const uint64_t u = dmix64(key ^ dmix64(static_cast<uint64_t>(t)));
+        const uint64_t u = dmix64(key ^ dmix64(static_cast<uint64_t>(row0 + t)));
         col[t] = (u >> 63) ? -1.0 : 1.0;
         return;
     }
-    // Gaussian: pair t covers elements 2t (cos) and 2t+1 (sin); counters 2t, 2t+1.
+    // Gaussian: local pair t covers elements 2t (cos) and 2t+1 (sin); global counters row0+2t, row0+2t+1.
     const int64_t i0 = 2 * t;
     if (i0 >= rows) return;
-    const uint64_t w1 = dmix64(key ^ dmix64(static_cast<uint64_t>(2 * t)));
-    const uint64_t w2 = dmix64(key ^ dmix64(static_cast<uint64_t>(2 * t + 1)));
+    const uint64_t w1 = dmix64(key ^ dmix64(static_cast<uint64_t>(row0 + 2 * t)));
+    const uint64_t w2 = dmix64(key ^ dmix64(static_cast<uint64_t>(row0 + 2 * t + 1)));
     const double u1 = static_cast<double>(w1 >> 11) * 0x1.0p-53;
     const double u2 = static_cast<double>(w2 >> 11) * 0x1.0p-53;
     if (u1 <= 0.0) atomicExch(err, 1);  // the reference would redraw (p = 2^-53 per pair)
@@ -297,13 +299,15 @@ cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t s
     return cudaGetLastError();
 }
 
-cudaError_t launch_prepare_split(const PrepArgs<float>& a, cudaStream_t stream) {
+cudaError_t launch_prepare_split_stats(const PrepArgs<float>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols || a.rows_per_block != 256) return cudaErrorInvalidValue;
     const int R = static_cast<int>((a.rows + 255) / 256);
-    prep_stats_kernel<float, 256><<<R, 256, 0, stream>>>(a);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    dim3 grid(static_cast<unsigned>((a.rows + 255) / 256), a.s);
+    if (R > 0) prep_stats_kernel<float, 256><<<R, 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepare_split_planes(const PrepArgs<float>& a, cudaStream_t stream) {
+    dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, (a.rows + 255) / 256)), a.s);
     prep_planes_kernel<<<grid, 256, 0, stream>>>(a);
     return cudaGetLastError();
 }
@@ -358,12 +362,13 @@ cudaError_t launch_panel_update(double beta, const double* g, int64_t ldg, const
     return cudaGetLastError();
 }
 
-cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t rows, int cols, int j0, double* out,
-                             int64_t ld, int* err_flag, cudaStream_t stream) {
+cudaError_t launch_rng_panel(uint64_t base_key, bool derive, int kind, int64_t row0, int64_t rows, int cols, int j0,
+                             double* out, int64_t ld, int* err_flag, cudaStream_t stream) {
     if (cols <= 0 || rows <= 0) return cudaSuccess;
+    if (kind != 1 && (row0 & 1)) return cudaErrorInvalidValue;
     const int64_t work = kind == 1 ? rows : (rows + 1) / 2;
     dim3 grid(static_cast<unsigned>((work + 255) / 256), cols);
-    rng_panel_kernel<<<grid, 256, 0, stream>>>(base_key, derive, kind, rows, j0, out, ld, err_flag);
+    rng_panel_kernel<<<grid, 256, 0, stream>>>(base_key, derive, kind, row0, rows, j0, out, ld, err_flag);
     return cudaGetLastError();
 }
 
