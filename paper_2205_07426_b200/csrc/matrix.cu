@@ -209,11 +209,78 @@ __device__ __forceinline__ void store_split4(__half* ph, __half* pl, const float
     }
 }
 
-__global__ void __launch_bounds__(256) gram_sym_f32_kernel(GramArgs g, int nb, __half* __restrict__ hi,
-                                                           __half* __restrict__ lo) {
-    __shared__ float xr[TKd][TM + 1];
-    __shared__ float xc[TKd][TN + 4];
-    __shared__ float tt[TN][TM + 1];
+// 128x128 output tile per CTA (256 threads, 8x8 entries each); samples pre-converted to fp32
+// column-major [d][n] (xf, yf) so each tile reads 2·128·d·4 bytes from L2 (d/16 B per entry).
+// 128x128 output tile per CTA (512 threads, 4x8 entries each); samples pre-converted to fp32
+// column-major [d][n] (xf, yf) so each tile reads 2·128·d·4 bytes from L2 (d/16 B per entry).
+constexpr int ST = 128;  // symmetric tile
+constexpr int SK = 16;   // feature chunk
+
+__device__ __forceinline__ void store_split8(__half* ph, __half* pl, const float* kv, int64_t gj0, int64_t n) {
+    __align__(16) __half h[8];
+    __align__(16) __half l[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+        const float s = kv[v] * static_cast<float>(kSplitScale);
+        h[v] = __float2half_rn(s);
+        l[v] = __float2half_rn(s - __half2float(h[v]));
+    }
+    if (gj0 + 7 < n && ((reinterpret_cast<uintptr_t>(ph) | reinterpret_cast<uintptr_t>(pl)) & 15) == 0) {
+        *reinterpret_cast<uint4*>(ph) = *reinterpret_cast<const uint4*>(h);
+        *reinterpret_cast<uint4*>(pl) = *reinterpret_cast<const uint4*>(l);
+    } else {
+        for (int v = 0; v < 8; ++v)
+            if (gj0 + v < n) {
+                ph[v] = h[v];
+                pl[v] = l[v];
+            }
+    }
+}
+
+constexpr int SU = 4;      // rows per thread (rows ty + 32u)
+constexpr int SThreads = 512;
+
+__device__ __forceinline__ void sym_accumulate(const float* __restrict__ xf, int d, int64_t n, int64_t row0,
+                                               int64_t col0, float (&dot)[SU][8], float (&sqr)[SU], float (&sqc)[8],
+                                               float (*xr)[ST], float (*xc)[ST]) {
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    for (int k0 = 0; k0 < d; k0 += SK) {
+        const int kc = min(SK, d - k0);
+        for (int idx = tid; idx < SK * ST; idx += blockDim.x) {
+            const int kk = idx / ST, rr = idx % ST;  // consecutive threads: consecutive samples (coalesced)
+            const int64_t gr = row0 + rr, gc = col0 + rr;
+            xr[kk][rr] = (kk < kc && gr < n) ? xf[static_cast<int64_t>(k0 + kk) * n + gr] : 0.f;
+            xc[kk][rr] = (kk < kc && gc < n) ? xf[static_cast<int64_t>(k0 + kk) * n + gc] : 0.f;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            float a[SU], b[8];
+#pragma unroll
+            for (int u = 0; u < SU; ++u) a[u] = xr[kk][ty + 32 * u];
+            const float4 b0 = *reinterpret_cast<const float4*>(&xc[kk][8 * tx]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&xc[kk][8 * tx + 4]);
+            b[0] = b0.x, b[1] = b0.y, b[2] = b0.z, b[3] = b0.w, b[4] = b1.x, b[5] = b1.y, b[6] = b1.z, b[7] = b1.w;
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                sqr[u] = fmaf(a[u], a[u], sqr[u]);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) dot[u][v] = fmaf(a[u], b[v], dot[u][v]);
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v) sqc[v] = fmaf(b[v], b[v], sqc[v]);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(SThreads) gram_sym_f32_kernel(GramArgs g, const float* __restrict__ xf,
+                                                           const float* __restrict__ yf, int nb,
+                                                           __half* __restrict__ hi, __half* __restrict__ lo) {
+    extern __shared__ float gsm[];
+    float(*xr)[ST] = reinterpret_cast<float(*)[ST]>(gsm);             // [SK][ST]
+    float(*xc)[ST] = reinterpret_cast<float(*)[ST]>(gsm + SK * ST);    // [SK][ST]
+    float(*tt)[ST + 1] = reinterpret_cast<float(*)[ST + 1]>(gsm + 2 * SK * ST);  // [ST][ST+1]
     // linear upper-triangle tile index -> (bi, bj), bi <= bj
     const int64_t t = blockIdx.x;
     auto start = [nb](int64_t b) { return b * nb - b * (b - 1) / 2; };
@@ -226,78 +293,82 @@ __global__ void __launch_bounds__(256) gram_sym_f32_kernel(GramArgs g, int nb, _
     const int64_t bj = bi + (t - start(bi));
     const int tid = threadIdx.x;
     const int tx = tid % 16, ty = tid / 16;
-    const int64_t row0 = static_cast<int64_t>(bi) * TM;
-    const int64_t col0 = static_cast<int64_t>(bj) * TN;
+    const int64_t row0 = bi * ST, col0 = bj * ST;
     const float l2e = 1.4426950408889634f;
 
-    float e[4][4];
+    float e[SU][8];
     {
-        float dot[4][4], sqr[4], sqc[4];
+        float dot[SU][8], sqr[SU], sqc[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            sqr[u] = sqc[u] = 0.f;
+        for (int u = 0; u < SU; ++u) {
+            sqr[u] = 0.f;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) dot[u][v] = 0.f;
+            for (int v = 0; v < 8; ++v) dot[u][v] = 0.f;
         }
-        GramTile<float>::accumulate(g.x, g.dx, g.x_rs, g.x_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
-        const float ax = static_cast<float>(g.inv_two_sigma2_x);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int v = 0; v < 8; ++v) sqc[v] = 0.f;
+        sym_accumulate(xf, g.dx, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+        const float ax = static_cast<float>(g.inv_two_sigma2_x) * l2e;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                float d2 = (sqr[u] + sqc[v]) - 2.f * dot[u][v];
-                e[u][v] = -fmaxf(d2, 0.f) * ax;
-            }
+        for (int u = 0; u < SU; ++u)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) e[u][v] = -fmaxf((sqr[u] + sqc[v]) - 2.f * dot[u][v], 0.f) * ax;
     }
-    if (g.y) {
-        float dot[4][4], sqr[4], sqc[4];
+    if (yf) {
+        float dot[SU][8], sqr[SU], sqc[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            sqr[u] = sqc[u] = 0.f;
+        for (int u = 0; u < SU; ++u) {
+            sqr[u] = 0.f;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) dot[u][v] = 0.f;
+            for (int v = 0; v < 8; ++v) dot[u][v] = 0.f;
         }
-        GramTile<float>::accumulate(g.y, g.dy, g.y_rs, g.y_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
-        const float ay = static_cast<float>(g.inv_two_sigma2_y);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int v = 0; v < 8; ++v) sqc[v] = 0.f;
+        sym_accumulate(yf, g.dy, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+        const float ay = static_cast<float>(g.inv_two_sigma2_y) * l2e;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                float d2 = (sqr[u] + sqc[v]) - 2.f * dot[u][v];
-                e[u][v] -= fmaxf(d2, 0.f) * ay;
-            }
+        for (int u = 0; u < SU; ++u)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) e[u][v] -= fmaxf((sqr[u] + sqc[v]) - 2.f * dot[u][v], 0.f) * ay;
     }
-    float kv[4][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < SU; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int64_t gi = row0 + ty + 16 * u, gj = col0 + 4 * tx + v;
-            kv[u][v] = (gi == gj) ? 1.0f : fast_exp2(e[u][v] * l2e);
+        for (int v = 0; v < 8; ++v) {
+            const int64_t gi = row0 + ty + 32 * u, gj = col0 + 8 * tx + v;
+            e[u][v] = (gi == gj) ? 1.0f : fast_exp2(e[u][v]);  // e now holds K
         }
     // direct tile: rows gi, columns gj
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int64_t gi = row0 + ty + 16 * u;
-        if (gi < g.n) store_split4(hi + gi * g.ld + col0 + 4 * tx, lo + gi * g.ld + col0 + 4 * tx, kv[u], col0 + 4 * tx, g.n);
+    for (int u = 0; u < SU; ++u) {
+        const int64_t gi = row0 + ty + 32 * u;
+        if (gi < g.n) store_split8(hi + gi * g.ld + col0 + 8 * tx, lo + gi * g.ld + col0 + 8 * tx, e[u], col0 + 8 * tx, g.n);
     }
     if (bi == bj) return;
-    // mirrored tile: rows gj, columns gi (via shared memory)
+    // mirrored tile: rows gj, columns gi (transposed through shared memory)
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < SU; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) tt[4 * tx + v][ty + 16 * u] = kv[u][v];
+        for (int v = 0; v < 8; ++v) tt[8 * tx + v][ty + 32 * u] = e[u][v];
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int rr = ty + 16 * u;  // row of the mirrored tile (a column of the direct tile)
+    for (int u = 0; u < SU; ++u) {
+        const int rr = ty + 32 * u;
         const int64_t gr = col0 + rr;
         if (gr >= g.n) continue;
-        float w[4];
+        float w[8];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) w[v] = tt[rr][4 * tx + v];
-        store_split4(hi + gr * g.ld + row0 + 4 * tx, lo + gr * g.ld + row0 + 4 * tx, w, row0 + 4 * tx, g.n);
+        for (int v = 0; v < 8; ++v) w[v] = tt[rr][8 * tx + v];
+        store_split8(hi + gr * g.ld + row0 + 8 * tx, lo + gr * g.ld + row0 + 8 * tx, w, row0 + 8 * tx, g.n);
     }
+}
+
+__global__ void to_f32_colmajor_kernel(const double* __restrict__ x, int64_t n, int d, int64_t rs, int64_t cs,
+                                       float* __restrict__ out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n * d) return;
+    const int64_t i = t % n, k = t / n;
+    out[t] = static_cast<float>(x[i * rs + k * cs]);
 }
 
 __global__ void matrix_to_split_kernel(const double* __restrict__ a, int64_t rows, int64_t cols, int64_t lda,
@@ -385,11 +456,37 @@ inline dim3 row_grid(int64_t rows, int64_t cols) {
 }  // namespace
 
 cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStream_t stream) {
-    if (g.f32_compute && g.row0 == 0 && g.rows == g.n) {
-        const int nb = static_cast<int>((g.n + TM - 1) / TM);
+    if (g.f32_compute && g.row0 == 0 && g.rows == g.n && g.ld % 8 == 0) {
+        // fp32 copies of the samples, column-major [d][n], for the symmetric tiles
+        float* xf = nullptr;
+        const int64_t dt = g.dx + (g.y ? g.dy : 0);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&xf), static_cast<size_t>(g.n) * dt * sizeof(float),
+                                        stream);
+        if (e != cudaSuccess) return e;
+        const int64_t nx = g.n * g.dx;
+        to_f32_colmajor_kernel<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, stream>>>(g.x, g.n, g.dx, g.x_rs,
+                                                                                         g.x_cs, xf);
+        float* yf = nullptr;
+        if (g.y) {
+            yf = xf + nx;
+            const int64_t ny = g.n * g.dy;
+            to_f32_colmajor_kernel<<<static_cast<unsigned>((ny + 255) / 256), 256, 0, stream>>>(
+                g.y, g.n, g.dy, g.y_rs, g.y_cs, yf);
+        }
+        const int nb = static_cast<int>((g.n + ST - 1) / ST);
         const int64_t tiles = static_cast<int64_t>(nb) * (nb + 1) / 2;
-        gram_sym_f32_kernel<<<static_cast<unsigned>(tiles), 256, 0, stream>>>(g, nb, hi, lo);
-        return cudaGetLastError();
+        const size_t smem = (2 * SK * ST + ST * (ST + 1)) * sizeof(float);
+        static bool attr = false;
+        if (!attr) {
+            e = cudaFuncSetAttribute(gram_sym_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        gram_sym_f32_kernel<<<static_cast<unsigned>(tiles), SThreads, smem, stream>>>(g, xf, yf, nb, hi, lo);
+        e = cudaGetLastError();
+        cudaFreeAsync(xf, stream);
+        return e;
     }
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
     if (g.f32_compute)
