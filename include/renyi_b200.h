@@ -44,8 +44,12 @@ enum {
     RENYI_E_INTERNAL = 24
 };
 
-/* storage/compute precision of a device kernel matrix */
-enum { RENYI_F64 = 0, RENYI_F32 = 1 };
+/* storage/compute precision of a device kernel matrix. RENYI_MF ("matrix-free") never
+ * stores A: each pass recomputes K(x_i, x_j) from bf16 samples on the tensor cores
+ * (fp32 accumulation, fp16 kernel values into an fp32-accumulated product). It is built
+ * from samples only (renyi_kernel_build_gaussian*, the *_samples and entropy entry
+ * points); renyi_kernel_from_matrix / _hadamard_joint / _download reject it. */
+enum { RENYI_F64 = 0, RENYI_F32 = 1, RENYI_MF = 2 };
 /* fp32 configurations: iterate operand of the block product. SPLIT (default) keeps V
  * as an fp16 hi+lo pair (3 tensor-core products, ~fp32 accuracy); FAST rounds V to
  * one fp16 plane (2 products) — see DESIGN.md for the measured trace error. */

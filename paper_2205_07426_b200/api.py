@@ -22,7 +22,9 @@ from ._lib import RenyiError, check
 
 F64 = 0
 F32 = 1
-PRECISIONS = {"fp64": F64, "f64": F64, "float64": F64, F64: F64, "fp32": F32, "f32": F32, "float32": F32, F32: F32}
+MF = 2  # matrix-free: bf16 samples, kernel entries recomputed per pass, A never stored
+PRECISIONS = {"fp64": F64, "f64": F64, "float64": F64, F64: F64, "fp32": F32, "f32": F32, "float32": F32, F32: F32,
+              "mf": MF, "matrix_free": MF, "bf16_mf": MF, MF: MF}
 
 METHODS = {"exact": 0, "int": 1, "int_power": 1, "taylor": 2, "chebyshev": 3, "auto": 4}
 METHOD_NAMES = {0: "exact", 1: "int", 2: "taylor", 3: "chebyshev", 4: "auto"}

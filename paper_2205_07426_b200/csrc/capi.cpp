@@ -128,7 +128,7 @@ void from_entropy(const rb::EntropyEst& e, renyi_entropy_estimate* o) {
 }
 
 void check_precision(int precision) {
-    if (precision != RENYI_F64 && precision != RENYI_F32) rb::fail(rb::kInvalidArgument, "unknown precision");
+    if (precision != RENYI_F64 && precision != RENYI_F32 && precision != RENYI_MF) rb::fail(rb::kInvalidArgument, "unknown precision");
 }
 
 }  // namespace

@@ -297,7 +297,7 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
     if (hf[0]) fail(kNonFinite, "sample matrix contains non-finite values");
     float mx;
     std::memcpy(&mx, &hf[1], sizeof(float));
-    if (prec == kF32 && mx > 1e18f) fail(kNonFinite, "sample values exceed the fp32 range of the fp32 configuration");
+    if (prec != kF64 && mx > 1e18f) fail(kNonFinite, "sample values exceed the fp32 range of the fp32 configuration");
 
     auto k = std::make_unique<KernelMatrix>();
     k->n = n;
@@ -308,6 +308,46 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
     const double inv_n = 1.0 / static_cast<double>(n);
     k->normalized = true;
     k->a_norm = 1.0;
+    if (prec == kMF) {
+        // matrix-free: keep bf16 samples and the per-sample bias; kernel entries are recomputed per pass.
+        // One variable: exp(-|x_i-x_j|^2/(2σ^2)) from bf16(x). Joint (x, y): the normalised Hadamard
+        // product is the Gaussian of the concatenated features [x/σx, y/σy] with σ = 1.
+        const int64_t dt = d + (y ? dy : 0);
+        if (dt > 128) fail(kInvalidArgument, "the matrix-free path supports up to 128 features");
+        k->dp = dt <= 64 ? 64 : 128;
+        const double l2e = 1.4426950408889634;
+        const int64_t npad = round_up(n, 128);
+        k->xb.alloc(static_cast<size_t>(npad) * k->dp * sizeof(__nv_bfloat16));
+        k->bias.alloc(static_cast<size_t>(npad) * sizeof(float));
+        cuda_check(cudaMemsetAsync(k->xb.as<void>(), 0, k->xb.bytes(), ctx.stream()), "memset");
+        cuda_check(cudaMemsetAsync(k->bias.as<void>(), 0, k->bias.bytes(), ctx.stream()), "memset");
+        if (!y) {
+            const double c = l2e / (2.0 * sigma * sigma);
+            k->c2 = 2.0 * c;
+            launched(ctx,
+                     launch_mf_prepare(x, n, static_cast<int>(d), 1, ldx, k->dp, c, k->xb.as<__nv_bfloat16>(),
+                                       k->bias.as<float>(), ctx.stream()),
+                     "mf_prepare");
+        } else {
+            DevBuf cat;
+            cat.alloc(static_cast<size_t>(n) * dt * sizeof(double));
+            launched(ctx, launch_scale_columns(x, n, static_cast<int>(d), 1, ldx, 1.0 / sigma, cat.as<double>(),
+                                               ctx.stream()),
+                     "scale_columns");
+            launched(ctx, launch_scale_columns(y, n, static_cast<int>(dy), 1, ldy, 1.0 / sigma_y,
+                                               cat.as<double>() + n * d, ctx.stream()),
+                     "scale_columns");
+            const double c = l2e / 2.0;
+            k->c2 = 2.0 * c;
+            launched(ctx,
+                     launch_mf_prepare(cat.as<double>(), n, static_cast<int>(dt), 1, n, k->dp, c,
+                                       k->xb.as<__nv_bfloat16>(), k->bias.as<float>(), ctx.stream()),
+                     "mf_prepare");
+            ctx.sync();
+        }
+        k->unscale = inv_n;
+        return k;
+    }
     GramArgs g;
     g.x = x;
     g.dx = static_cast<int>(d);
@@ -339,6 +379,7 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
 
 KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
     if (n < 1) fail(kInvalidArgument, "matrix must be non-empty");
+    if (prec == kMF) fail(kInvalidArgument, "the matrix-free precision builds from samples only");
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     auto k = std::make_unique<KernelMatrix>();
     k->n = n;
@@ -399,6 +440,8 @@ KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix
         fail(kSizeMismatch,
              "hadamard_joint kernel sizes differ: " + std::to_string(a.n) + " vs " + std::to_string(b.n));
     if (a.prec != b.prec) fail(kInvalidArgument, "hadamard_joint needs kernels of the same precision");
+    if (a.prec == kMF)
+        fail(kInvalidArgument, "matrix-free joints are built from samples (renyi_kernel_build_gaussian_joint)");
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     auto c = std::make_unique<KernelMatrix>();
     c->n = a.n, c->row0 = a.row0, c->rows = a.rows, c->ld = a.ld, c->prec = a.prec;
@@ -434,6 +477,7 @@ KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix
 
 void download(Context& ctx, const KernelMatrix& k, double* out) {
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    if (k.prec == kMF) fail(kInvalidArgument, "matrix-free kernels are never materialised");
     std::vector<double> rm(static_cast<size_t>(k.rows) * k.n);
     if (k.prec == kF32) {
         DevBuf tmp;
@@ -466,9 +510,14 @@ public:
             fail(kInvalidArgument, "kernel matrix was built for a different rank layout");
         rows_ = k.rows;
         ld_ = k.rpr;  // state [s][rpr] (local rows); operand planes [world][s][rpr]
+        mf_ = k.prec == kMF;
         if (k.prec == kF32) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
             plan_ = make_streamk_plan(rows_, k.n, grid, ctx.kc);
+            npad_ = tc_npad(s);
+        } else if (mf_) {
+            const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
+            plan_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.kc / 4));  // same K per TMEM chunk (512)
             npad_ = tc_npad(s);
         } else {
             plan_ = make_f64_plan(rows_, k.n);
@@ -476,20 +525,22 @@ public:
         }
         const int rpb = plan_.rows_per_block;
         R_ = static_cast<int>((rows_ + rpb - 1) / rpb);
-        const size_t st = k.prec == kF32 ? sizeof(float) : sizeof(double);
+        const bool f32 = k.prec != kF64;  // fp32 state for the split and matrix-free paths
+        const size_t st = f32 ? sizeof(float) : sizeof(double);
         for (auto& b : ctx.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
-        if (k.prec == kF32) {
+        if (f32) {
             const size_t plane = static_cast<size_t>(k.world) * s * ld_ * sizeof(__half);
             ctx.vhi.ensure(plane);
             // rows past n in the last chunk are never written: keep them zero (A's columns there are
             // TMA-zero, but 0 x garbage could be NaN)
             cuda_check(cudaMemsetAsync(ctx.vhi.as<__half>(), 0, plane, ctx.stream()), "memset");
-            if (ctx.operand_split) {
+            if (ctx.operand_split && !mf_) {
                 ctx.vlo.ensure(plane);
                 cuda_check(cudaMemsetAsync(ctx.vlo.as<__half>(), 0, plane, ctx.stream()), "memset");
             }
             slice_ = static_cast<size_t>(k.rank) * s * ld_;
         }
+        // the matrix-free P·V product takes one fp16 operand plane (P itself is fp16)
         vlo_ = (k.prec == kF32 && ctx.operand_split) ? ctx.vlo.as<__half>() : nullptr;
         const size_t P1 = static_cast<size_t>(max_passes) + 1;
         ctx.stats.ensure(P1 * 3 * std::max(R_, 1) * s * sizeof(double));
@@ -497,7 +548,7 @@ public:
         ctx.cmax.ensure(P1 * s * sizeof(unsigned));
         ctx.eexp.ensure(P1 * s * sizeof(int));
         cuda_check(cudaMemsetAsync(ctx.cmax.as<unsigned>(), 0, P1 * s * sizeof(unsigned), ctx.stream()), "memset");
-        if (k.prec == kF32) {
+        if (f32) {
             ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(float));
             PrepArgs<float> p{};
             p.x = x, p.ldx = ldx, p.rows = rows_, p.rows_per_block = rpb, p.s = s, p.ld = ld_;
@@ -526,7 +577,7 @@ public:
 
     // all ranks' operand slices -> full planes (in place)
     void gather_planes() {
-        if (!ctx_.exchange || k_.prec != kF32) return;
+        if (!ctx_.exchange || k_.prec == kF64) return;
         const size_t chunk = static_cast<size_t>(s_) * ld_ * sizeof(__half);
         ctx_.exchange->allgather_inplace(ctx_.vhi.as<__half>(), chunk, ctx_.stream());
         if (vlo_) ctx_.exchange->allgather_inplace(vlo_, chunk, ctx_.stream());
@@ -536,17 +587,28 @@ public:
         if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
         const int k = k_done_;
         const size_t s = static_cast<size_t>(s_);
-        if (k_.prec == kF32) {
-            SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
+        if (k_.prec != kF64) {
             SplitPanelView v{ctx_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world};
             ctx_.prof_begin();
-            if (rows_ > 0)
-                launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
-                         "block_av_tc");
-            ctx_.prof_end();
-            // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
-            ctx_.prof_account(4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_ + 4.0 * rows_ * s_,
-                              2.0 * rows_ * k_.n * s_);
+            if (mf_) {
+                MfMatrixView a{k_.xb.as<__nv_bfloat16>(), k_.bias.as<float>(), k_.n, k_.dp, k_.row0, k_.c2};
+                if (rows_ > 0)
+                    launched(ctx_, launch_block_av_mf(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
+                             "block_av_mf");
+                ctx_.prof_end();
+                // algorithmic flops (SURVEY §8d matrix-free): 2·n_local·n·(d + s); bytes: X, V, Y
+                ctx_.prof_account(2.0 * k_.n * k_.dp + 2.0 * k_.n * s_ + 4.0 * rows_ * s_,
+                                  2.0 * rows_ * k_.n * (k_.dp + s_));
+            } else {
+                SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
+                if (rows_ > 0)
+                    launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
+                             "block_av_tc");
+                ctx_.prof_end();
+                // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
+                ctx_.prof_account(4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_ + 4.0 * rows_ * s_,
+                                  2.0 * rows_ * k_.n * s_);
+            }
             EpiArgs<float, float> e{};
             e.partial = ctx_.partial.as<float>();
             e.npad = npad_;
@@ -625,10 +687,11 @@ public:
     }
 
     void state_f64(int k, double* out, int64_t ldo) {
+        const bool f32 = k_.prec != kF64;
         launched(ctx_,
-                 launch_state_to_f64(k_.prec == kF32 ? static_cast<const void*>(buf<float>(k))
-                                                     : static_cast<const void*>(buf<double>(k)),
-                                     k_.prec == kF32, rows_, s_, ld_, out, ldo, ctx_.stream()),
+                 launch_state_to_f64(f32 ? static_cast<const void*>(buf<float>(k))
+                                         : static_cast<const void*>(buf<double>(k)),
+                                     f32, rows_, s_, ld_, out, ldo, ctx_.stream()),
                  "state_to_f64");
     }
 
@@ -651,6 +714,7 @@ private:
     int R_ = 0;
     int npad_ = 0;
     int k_done_ = 0;
+    bool mf_ = false;
     __half* vlo_ = nullptr;
     size_t slice_ = 0;  // this rank's chunk offset in the operand planes
     StreamKPlan plan_;

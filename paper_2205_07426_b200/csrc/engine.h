@@ -17,7 +17,8 @@
 
 namespace rb {
 
-enum Precision : int { kF64 = 0, kF32 = 1 };
+// kF64: fp64 A; kF32: A as fp16 hi/lo planes (fp32-class); kMF: matrix-free (bf16 samples, A never stored)
+enum Precision : int { kF64 = 0, kF32 = 1, kMF = 2 };
 
 void cuda_check(cudaError_t e, const char* what);
 
@@ -132,6 +133,10 @@ struct KernelMatrix {
     double a_norm = 1.0;   // >= max_i sum_j |A_ij|
     bool normalized = true;
     DevBuf a64, hi, lo;
+    // matrix-free storage
+    DevBuf xb, bias;  // bf16 [n][dp], fp32 −b = −c·|x|² [round_up(n,128)]
+    int dp = 0;
+    double c2 = 0.0;  // 2c = log2(e)/σ²
 };
 
 using KernelPtr = std::unique_ptr<KernelMatrix>;

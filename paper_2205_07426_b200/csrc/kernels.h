@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -54,6 +55,22 @@ int tc_npad(int cols);
 StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc);
 cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream);
+
+// matrix-free: bf16 samples [n][dp] (dp = 64 or 128, zero padded) and negated bias −b = −c·|x|² [n_pad]
+struct MfMatrixView {
+    const __nv_bfloat16* x;
+    const float* bias;
+    int64_t n;
+    int dp;
+    int64_t row0;
+    double c2;  // 2c = log2(e)/σ²
+};
+StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc);
+cudaError_t launch_block_av_mf(const MfMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
+                               float* partial, cudaStream_t stream);
+// x (fp64, element (i,k) at x[i*rs + k*cs]) -> bf16 [n][dp] and negated bias −c·|bf16(x)|²
+cudaError_t launch_mf_prepare(const double* x, int64_t n, int d, int64_t rs, int64_t cs, int dp, double c,
+                              __nv_bfloat16* xb, float* bias, cudaStream_t stream);
 
 StreamKPlan make_f64_plan(int64_t rows, int64_t cols);
 int f64_npad(int cols);
@@ -175,6 +192,9 @@ cudaError_t launch_hadamard_split(const __half* ahi, const __half* alo, const __
                                   double diag_value, __half* chi, __half* clo, cudaStream_t stream);
 cudaError_t launch_hadamard_f64(const double* a, const double* b, int64_t rows, int64_t cols, int64_t ld,
                                 int64_t row0, double n, double* c, cudaStream_t stream);
+// out (column-major [d][n]) = scale * x
+cudaError_t launch_scale_columns(const double* x, int64_t n, int d, int64_t rs, int64_t cs, double scale, double* out,
+                                 cudaStream_t stream);
 // samples check: flag[0] |= non-finite, flag[1] = float bits of max |x| (atomic max)
 cudaError_t launch_check_samples(const double* x, int64_t n, int d, int64_t rs, int64_t cs, unsigned* flags,
                                  cudaStream_t stream);

@@ -502,6 +502,22 @@ cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+__global__ void scale_columns_kernel(const double* __restrict__ x, int64_t n, int d, int64_t rs, int64_t cs,
+                                     double scale, double* __restrict__ out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n * d) return;
+    const int64_t i = t % n, k = t / n;
+    out[t] = x[i * rs + k * cs] * scale;
+}
+
+cudaError_t launch_scale_columns(const double* x, int64_t n, int d, int64_t rs, int64_t cs, double scale, double* out,
+                                 cudaStream_t stream) {
+    const int64_t total = n * d;
+    if (total == 0) return cudaSuccess;
+    scale_columns_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(x, n, d, rs, cs, scale, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_samples(const double* x, int64_t n, int d, int64_t rs, int64_t cs, unsigned* flags,
                                  cudaStream_t stream) {
     const int64_t total = n * d;

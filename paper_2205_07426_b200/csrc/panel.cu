@@ -286,9 +286,16 @@ __global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64
 }  // namespace
 
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream) {
-    if (a.s > kMaxPanelCols || a.rows_per_block != 256) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + 255) / 256);
-    epilogue_kernel<float, float, true, 256><<<R, 256, 0, stream>>>(a);
+    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    if (a.rows_per_block == 256) {
+        const int R = static_cast<int>((a.rows + 255) / 256);
+        epilogue_kernel<float, float, true, 256><<<R, 256, 0, stream>>>(a);
+    } else if (a.rows_per_block == 128) {
+        const int R = static_cast<int>((a.rows + 127) / 128);
+        epilogue_kernel<float, float, true, 128><<<R, 128, 0, stream>>>(a);
+    } else {
+        return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
@@ -300,9 +307,16 @@ cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t s
 }
 
 cudaError_t launch_prepare_split_stats(const PrepArgs<float>& a, cudaStream_t stream) {
-    if (a.s > kMaxPanelCols || a.rows_per_block != 256) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + 255) / 256);
-    if (R > 0) prep_stats_kernel<float, 256><<<R, 256, 0, stream>>>(a);
+    if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    if (a.rows_per_block == 256) {
+        const int R = static_cast<int>((a.rows + 255) / 256);
+        if (R > 0) prep_stats_kernel<float, 256><<<R, 256, 0, stream>>>(a);
+    } else if (a.rows_per_block == 128) {
+        const int R = static_cast<int>((a.rows + 127) / 128);
+        if (R > 0) prep_stats_kernel<float, 128><<<R, 128, 0, stream>>>(a);
+    } else {
+        return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
