@@ -1,18 +1,24 @@
 // Matrix-free block product (config 5; SURVEY §8(a5) "matrix-free variant", §7 step 6):
-//   Y_i = Σ_j K(x_i, x_j) · V_j,   K = exp(−(|x_i|² + |x_j|² − 2 x_i·x_j) / (2σ²)),  K_ii = 1,
+//   Y_i = Σ_j K(x_i, x_j) · V_j,   K = exp(−|x_i − x_j|² / (2σ²)),  K_ii = 1,
 // with the kernel entries recomputed from bf16 X on the tensor cores and never stored
 // (the reference materialises A: proj/src/kernel.cpp:35-72 + ops.cpp:98-107).
 //
 // FlashAttention-shaped, without the softmax bookkeeping (kernel values are already in (0, 1]):
-//   S  = X_i · X_jᵀ            tcgen05.mma kind::f16 (bf16 in, fp32 accumulate) → TMEM
-//   P  = exp2(2c·S − b_i − b_j) exp warps: TMEM → registers → MUFU ex2 → fp16 → SW128 smem
-//   O += P · V_j               tcgen05.mma kind::f16 (fp16 in, fp32 accumulate) → TMEM
-// where b = c·|x|², c = log2(e)/(2σ²). One CTA owns 128 rows (UMMA M); j-blocks of 128.
-// Warp roles: 0 TMA (X_i once per row block, X_j + V_j ring), 1 MMA issuer, 2-5 exp,
-// 6-9 O drain (fp32 register accumulation every kc j-blocks — the tensor core's long-K
-// accumulation is lossy, see block_av_tc.cu). S and O are double-buffered in TMEM, P in smem.
-// Persistent stream-K over (row block, j-block) with the same partial-slot protocol and pass
-// epilogue as the materialised path.
+//   S  = [X_i | a_i] · [X_j | a'_j]ᵀ = x_i·x_j − |x_i|²/2 − |x_j|²/2 = −|x_i − x_j|²/2
+//        tcgen05.mma kind::f16 (bf16 in, fp32 accumulate) → TMEM. The squared norms ride in 16
+//        augmented K columns: a_i = [h_i, m_i, l_i, 1, 1, 1, 0…], a'_j = [1, 1, 1, h_j, m_j, l_j, 0…]
+//        with h + m + l = −|x|²/2 split over three bf16 (24-bit significand), so the exp warps
+//        do no bias arithmetic at all.
+//   P  = exp2(c2·S)             exp warps: TMEM → registers → MUFU ex2 → fp16 → back into TMEM
+//                               (over the S columns just read; c2 = log2(e)/σ²)
+//   O += P · V_j                tcgen05.mma kind::f16 with A = P from TMEM, B = V_j from smem
+// One CTA owns 128 rows (UMMA M); j-blocks of 128. Warp roles: 0 TMA (X_i once per row block,
+// X_j + V_j + a'_j ring), 1 MMA issuer, 2-9 two exp warpgroups (columns [64h, 64h+64) of each
+// S tile) that also drain half of O each into fp32 registers every kc j-blocks (the tensor
+// core's long-K accumulation is lossy, see block_av_tc.cu). S/P and O are double-buffered in
+// TMEM. Persistent schedule: whole row blocks in data-parallel waves (L2 reuse of X_j / V_j across
+// the wave) plus a stream-K split of the tail; partial slots and the pass epilogue are shared with
+// the materialised path.
 #include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -24,27 +30,30 @@ namespace rb {
 
 namespace {
 
-constexpr int MB = 128;  // rows per CTA (UMMA M)
-constexpr int JB = 128;  // j-block: S tile N and P·V K
-constexpr int kMfThreads = 320;
-constexpr int kBiasBytes = JB * 4;
+constexpr int MB = 128;   // rows per CTA (UMMA M)
+constexpr int JB = 128;   // j-block: S tile N and P·V K
+constexpr int kAug = 16;  // augmented K columns carrying −|x|²/2
+constexpr int kMfThreads = 352;  // TMA(X), MMA, 8 exp/drain warps, TMA(V)
 
 template <int DP, int NPAD>
 struct MfCfg {
-    static constexpr int kXTile = MB * DP * 2;      // X tile, bf16, [128][DP] as DP/64 SW128 sub-tiles
-    static constexpr int kXSub = MB * 64 * 2;       // one 64-feature sub-tile (16 KB)
-    static constexpr int kVTile = NPAD * JB * 2;    // V_j tile, fp16, [NPAD][128] as two SW128 sub-tiles
+    static constexpr int kXTile = MB * DP * 2;    // X tile, bf16, [128][DP] as DP/64 SW128 sub-tiles
+    static constexpr int kXSub = MB * 64 * 2;     // one 64-feature sub-tile (16 KB)
+    static constexpr int kATile = MB * kAug * 2;  // augmented columns, bf16 [128][16], SW32
+    static constexpr int kVTile = NPAD * JB * 2;  // V_j tile, fp16, [NPAD][128] as two SW128 sub-tiles
     static constexpr int kVSub = NPAD * 64 * 2;
-    static constexpr int kPTile = MB * JB * 2;      // P tile, fp16, [128][128] as two SW128 sub-tiles
-    static constexpr int kStage = kXTile + kVTile;  // X_j + V_j (1024-aligned); the j-block bias rides in a ring
-    static constexpr int kStagesRaw = (226 * 1024 - kXTile - 2 * kPTile - 1024) / (kStage + kBiasBytes);
-    static constexpr int kStages = kStagesRaw > 4 ? 4 : kStagesRaw;
-    static constexpr int kSmem = kXTile + 2 * kPTile + kStages * (kStage + kBiasBytes) + 1024;
-    static constexpr int kOCol = 2 * JB;  // O buffers after the two S buffers
+    static constexpr int kXSlot = kXTile + kATile;  // X_j | a'_j (1024-aligned); also X_i | a_i
+    static constexpr int kBudget = 226 * 1024 - 1024 - kXSlot;
+    // two rings: X_j (released when S(j) completes) and V_j (released when P·V(j) completes)
+    static constexpr int kVStages = (kBudget - 3 * kVTile) / kXSlot >= 3 ? 3 : 2;
+    static constexpr int kXStagesRaw = (kBudget - kVStages * kVTile) / kXSlot;
+    static constexpr int kXStages = kXStagesRaw > 4 ? 4 : kXStagesRaw;
+    static constexpr int kSmem = kXSlot * (1 + kXStages) + kVTile * kVStages + 1024;
+    static constexpr int kOCol = 2 * JB;    // O buffers after the two S/P buffers
     static constexpr int kHalf = NPAD / 2;  // O columns drained by each exp warpgroup
     static_assert(DP == 64 || DP == 128, "feature dimension is padded to 64 or 128");
     static_assert(NPAD % 16 == 0 && NPAD <= 128, "NPAD must be a multiple of 16 in [16,128]");
-    static_assert(kStages >= 2, "need a double-buffered X_j/V_j ring");
+    static_assert(kXStages >= 2, "need a double-buffered X_j ring");
     static_assert(kOCol + 2 * NPAD <= 512, "TMEM budget");
 };
 
@@ -53,14 +62,43 @@ struct MfArgs {
     int j_blocks;
     int kc;               // j-blocks per O accumulation chunk
     int64_t row0;         // first global row of this rank
-    int64_t n;            // samples
     int kt_chunk;         // j-blocks per V chunk (rpr / 128)
-    float c2;             // 2c = log2(e)/σ²
-    const float* nbias;   // −b = −c·|x|², [n_pad], zero padded
+    float c2;             // log2(e)/σ²
+    int64_t dp_blocks;    // row blocks owned whole (waves of gridDim.x); stream-K over the rest
     float* partial;       // [slots][NPAD][128]
 };
 
-__device__ __forceinline__ uint64_t desc_sw128_k(uint32_t addr) { return umma_desc_sw128(addr); }
+// The (row block, j-range) segments one CTA processes: whole row blocks in data-parallel waves
+// (all CTAs walk the same j-blocks at about the same time, so X_j / V_j are fetched from HBM once
+// per wave and served from L2 to the other CTAs), then an even stream-K share of the tail.
+struct MfSegments {
+    int64_t waves, grid, cta, J, dp_rows, it, it_end, w = 0;
+    __device__ MfSegments(const MfArgs& a, int c, int G) : grid(G), cta(c), J(a.j_blocks), dp_rows(a.dp_blocks) {
+        waves = a.dp_blocks / G;
+        const int64_t tail = a.total_iters - a.dp_blocks * J;
+        it = tail * c / G;
+        it_end = tail * (c + 1) / G;
+    }
+    __device__ bool next(int64_t& r, int& j0, int& j1) {
+        if (w < waves) {
+            r = w * grid + cta;
+            j0 = 0;
+            j1 = static_cast<int>(J);
+            ++w;
+            return true;
+        }
+        if (it >= it_end) return false;
+        const int64_t rt = it / J;
+        const int64_t e = min(it_end, (rt + 1) * J);
+        r = dp_rows + rt;
+        j0 = static_cast<int>(it - rt * J);
+        j1 = static_cast<int>(e - rt * J);
+        it = e;
+        return true;
+    }
+    // partial slot of row block r for this CTA (epilogue: panel.cu)
+    __device__ int64_t slot(int64_t r) const { return r < dp_rows ? r : r + cta; }
+};
 
 __device__ __forceinline__ uint32_t pack_f16x2_clamp1(float lo, float hi) {
     // fp16 pair, clamped to <= 1 (K <= 1; guards exp2 of a rounding-positive argument)
@@ -77,26 +115,12 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
-                 : "memory");
-}
-
-__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-    return v;
-}
-
-// 8 kernel values of one row: p = exp2(2c·s − b_i − b_j), packed to fp16 (16 bytes of P)
+// 64 kernel values of one row: p = exp2(c2·s), packed to 32 fp16 pairs (K order)
 template <bool DIAG>
-__device__ __forceinline__ void exp8(const float* sv, float2 c2v, float2 nbv, float4 b0, float4 b1, int col0,
-                                     int row, uint32_t* pk) {
-    const float bj[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+__device__ __forceinline__ void exp64(const float* sv, float2 c2v, int col0, int row, uint32_t* pk) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        float2 a = __ffma2_rn(make_float2(sv[2 * e], sv[2 * e + 1]), c2v, nbv);
-        a = __fadd2_rn(a, make_float2(bj[2 * e], bj[2 * e + 1]));
+    for (int e = 0; e < 32; ++e) {
+        const float2 a = __fmul2_rn(make_float2(sv[2 * e], sv[2 * e + 1]), c2v);
         float p0 = ex2(a.x), p1 = ex2(a.y);
         if (DIAG) {  // K_ii = 1 exactly (proj/src/ops.cpp:12)
             if (col0 + 2 * e == row) p0 = 1.0f;
@@ -108,13 +132,15 @@ __device__ __forceinline__ void exp8(const float* sv, float2 c2v, float2 nbv, fl
 
 template <int DP, int NPAD>
 __global__ void __launch_bounds__(kMfThreads, 1)
-    block_av_mf_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_v,
+    block_av_mf_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_ar,
+                       const __grid_constant__ CUtensorMap map_ac, const __grid_constant__ CUtensorMap map_v,
                        MfArgs args) {
     using C = MfCfg<DP, NPAD>;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t xi_full, xi_empty;
-    __shared__ __align__(8) uint64_t st_full[C::kStages], st_empty[C::kStages];
-    __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_full[2], o_empty[2];
+    __shared__ __align__(8) uint64_t x_full[C::kXStages], x_empty[C::kXStages];
+    __shared__ __align__(8) uint64_t v_full[C::kVStages], v_empty[C::kVStages];
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
     __shared__ uint32_t tmem_base_smem;
 
     const int warp = threadIdx.x / kWarp;
@@ -122,29 +148,30 @@ __global__ void __launch_bounds__(kMfThreads, 1)
     const int G = gridDim.x, cta = blockIdx.x;
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
-    const uint32_t xi_smem = base_u32;
-    const uint32_t p_smem = xi_smem + C::kXTile;                // two P buffers
-    const uint32_t st_smem = p_smem + 2 * C::kPTile;            // ring of X_j + V_j
-    const uint32_t bias_smem = st_smem + C::kStages * C::kStage;  // ring of −b_j (128 floats per stage)
-    const int64_t it_begin = (args.total_iters * cta) / G;
-    const int64_t it_end = (args.total_iters * (cta + 1)) / G;
-    const int JBn = args.j_blocks;
+    const uint32_t xi_smem = base_u32;                        // X_i | a_i
+    const uint32_t xs_smem = xi_smem + C::kXSlot;             // ring of X_j | a'_j
+    const uint32_t vs_smem = xs_smem + C::kXStages * C::kXSlot;  // ring of V_j
     constexpr uint32_t kExpThreads = 8 * kWarp;
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&map_x);
+        prefetch_tmap(&map_ar);
+        prefetch_tmap(&map_ac);
         prefetch_tmap(&map_v);
         mbar_init(&xi_full, 1);
         mbar_init(&xi_empty, 1);
-        for (int s = 0; s < C::kStages; ++s) {
-            mbar_init(&st_full[s], 1);
-            mbar_init(&st_empty[s], 1);
+        for (int s = 0; s < C::kXStages; ++s) {
+            mbar_init(&x_full[s], 1);
+            mbar_init(&x_empty[s], 1);
+        }
+        for (int s = 0; s < C::kVStages; ++s) {
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&s_full[b], 1);
-            mbar_init(&s_empty[b], kExpThreads);
+            mbar_init(&s_empty[b], 1);
             mbar_init(&p_full[b], kExpThreads);
-            mbar_init(&p_empty[b], 1);
             mbar_init(&o_full[b], 1);
             mbar_init(&o_empty[b], kExpThreads);
         }
@@ -157,33 +184,28 @@ __global__ void __launch_bounds__(kMfThreads, 1)
     const uint32_t tmem = tmem_base_smem;
 
     if (warp == 0) {
-        // ---------------- TMA producer ----------------
+        // ---------------- TMA producer: X_i, X_j | a'_j ----------------
         if (lane == 0) {
-            const uint64_t pol = policy_evict_last();  // X, V and b are re-read by every row block
+            const uint64_t pol = policy_evict_normal();  // the wave re-reads X_j / a'_j from L2 (LRU)
             int stage = 0;
             uint32_t phase = 0, seg = 0;
-            int64_t it = it_begin;
-            while (it < it_end) {
-                const int64_t r = it / JBn;
-                const int64_t seg_end = min(it_end, (r + 1) * JBn);
+            MfSegments sg(args, cta, G);
+            int64_t r;
+            int j0, j1;
+            while (sg.next(r, j0, j1)) {
+                const int gi0 = static_cast<int>(args.row0 + r * MB);
                 mbar_wait(&xi_empty, (seg & 1u) ^ 1u);
-                mbar_arrive_expect_tx(&xi_full, C::kXTile);
-                for (int h = 0; h < DP / 64; ++h)
-                    tma_load_2d(base + h * C::kXSub, &map_x, &xi_full, h * 64, static_cast<int>(args.row0 + r * MB),
-                                pol);
-                for (; it < seg_end; ++it) {
-                    const int jb = static_cast<int>(it - r * JBn);
-                    mbar_wait(&st_empty[stage], phase ^ 1u);
-                    uint8_t* st = base + (st_smem - base_u32) + stage * C::kStage;
-                    mbar_arrive_expect_tx(&st_full[stage], C::kStage + kBiasBytes);
+                mbar_arrive_expect_tx(&xi_full, C::kXSlot);
+                for (int h = 0; h < DP / 64; ++h) tma_load_2d(base + h * C::kXSub, &map_x, &xi_full, h * 64, gi0, pol);
+                tma_load_2d(base + C::kXTile, &map_ar, &xi_full, 0, gi0, pol);
+                for (int jb = j0; jb < j1; ++jb) {
+                    mbar_wait(&x_empty[stage], phase ^ 1u);
+                    uint8_t* st = base + (xs_smem - base_u32) + stage * C::kXSlot;
+                    mbar_arrive_expect_tx(&x_full[stage], C::kXSlot);
                     for (int h = 0; h < DP / 64; ++h)
-                        tma_load_2d(st + h * C::kXSub, &map_x, &st_full[stage], h * 64, jb * JB, pol);
-                    const int vz = jb / args.kt_chunk, vx = (jb - vz * args.kt_chunk) * JB;
-                    for (int h = 0; h < 2; ++h)
-                        tma_load_3d(st + C::kXTile + h * C::kVSub, &map_v, &st_full[stage], vx + h * 64, 0, vz, pol);
-                    bulk_load_1d(base + (bias_smem - base_u32) + stage * kBiasBytes, args.nbias + jb * JB,
-                                 kBiasBytes, &st_full[stage], pol);
-                    if (++stage == C::kStages) {
+                        tma_load_2d(st + h * C::kXSub, &map_x, &x_full[stage], h * 64, jb * JB, pol);
+                    tma_load_2d(st + C::kXTile, &map_ac, &x_full[stage], 0, jb * JB, pol);
+                    if (++stage == C::kXStages) {
                         stage = 0;
                         phase ^= 1u;
                     }
@@ -191,16 +213,38 @@ __global__ void __launch_bounds__(kMfThreads, 1)
                 ++seg;
             }
         }
+    } else if (warp == 10) {
+        // ---------------- TMA producer: V_j ----------------
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            MfSegments sg(args, cta, G);
+            int64_t r;
+            int j0, j1;
+            while (sg.next(r, j0, j1)) for (int jb = j0; jb < j1; ++jb) {
+                mbar_wait(&v_empty[stage], phase ^ 1u);
+                uint8_t* st = base + (vs_smem - base_u32) + stage * C::kVTile;
+                mbar_arrive_expect_tx(&v_full[stage], C::kVTile);
+                const int vz = jb / args.kt_chunk, vx = (jb - vz * args.kt_chunk) * JB;
+                for (int h = 0; h < 2; ++h)
+                    tma_load_3d(st + h * C::kVSub, &map_v, &v_full[stage], vx + h * 64, 0, vz, pol);
+                if (++stage == C::kVStages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             constexpr uint32_t idesc_s = umma_idesc_bf16_f32(MB, JB);
             constexpr uint32_t idesc_o = umma_idesc_f16_f32(MB, NPAD);
-            int stage = 0;
-            uint32_t phase = 0, seg = 0, jc = 0, chunk = 0, in_chunk = 0;
-            int prev_stage = -1;
-            auto pv = [&](int st_idx, uint32_t jprev, bool last_of_segment) {
+            int xs = 0, vs = 0;
+            uint32_t xph = 0, vph = 0, seg = 0, jc = 0, chunk = 0, in_chunk = 0;
+            auto pv = [&](uint32_t jprev, bool last_of_segment) {
                 const uint32_t pb = jprev & 1u;
+                mbar_wait(&v_full[vs], vph);
                 mbar_wait(&p_full[pb], (jprev >> 1) & 1u);
                 tc_fence_after();
                 const uint32_t ob = chunk & 1u;
@@ -209,16 +253,19 @@ __global__ void __launch_bounds__(kMfThreads, 1)
                     tc_fence_after();
                 }
                 const uint32_t d = tmem + C::kOCol + ob * NPAD;
-                const uint32_t pa = p_smem + pb * C::kPTile;
-                const uint32_t vb = st_smem + st_idx * C::kStage + C::kXTile;
+                const uint32_t pa = tmem + pb * JB;  // P: K 0-63 at columns 0-31, K 64-127 at 64-95
+                const uint32_t vb = vs_smem + vs * C::kVTile;
 #pragma unroll
-                for (int k = 0; k < JB / 16; ++k) {
-                    const uint32_t off = (k & 3) * 32;  // 16 K-elements = 32 bytes inside a 128-byte row
-                    umma_f16(d, desc_sw128_k(pa + (k >> 2) * (MB * 128) + off),
-                             desc_sw128_k(vb + (k >> 2) * C::kVSub + off), idesc_o, (in_chunk > 0 || k > 0) ? 1u : 0u);
+                for (int k = 0; k < JB / 16; ++k)
+                    umma_f16_ts(d, pa + (k >> 2) * 64 + (k & 3) * 8,
+                                umma_desc_sw128(vb + (k >> 2) * C::kVSub + (k & 3) * 32), idesc_o,
+                                (in_chunk > 0 || k > 0) ? 1u : 0u);
+                umma_commit(&s_empty[pb]);  // S/P buffer reusable
+                umma_commit(&v_empty[vs]);  // V_j consumed
+                if (++vs == C::kVStages) {
+                    vs = 0;
+                    vph ^= 1u;
                 }
-                umma_commit(&p_empty[pb]);
-                umma_commit(&st_empty[st_idx]);
                 ++in_chunk;
                 if (in_chunk == static_cast<uint32_t>(args.kc) || last_of_segment) {
                     umma_commit(&o_full[ob]);
@@ -226,44 +273,49 @@ __global__ void __launch_bounds__(kMfThreads, 1)
                     in_chunk = 0;
                 }
             };
-            int64_t it = it_begin;
-            while (it < it_end) {
-                const int64_t r = it / JBn;
-                const int64_t seg_end = min(it_end, (r + 1) * JBn);
+            MfSegments sg(args, cta, G);
+            int64_t r;
+            int j0, j1;
+            while (sg.next(r, j0, j1)) {
                 mbar_wait(&xi_full, seg & 1u);
                 tc_fence_after();
-                for (; it < seg_end; ++it) {
-                    mbar_wait(&st_full[stage], phase);
+                bool first = true;
+                for (int jb = j0; jb < j1; ++jb) {
+                    mbar_wait(&x_full[xs], xph);
                     const uint32_t sb = jc & 1u;
-                    mbar_wait(&s_empty[sb], ((jc >> 1) & 1u) ^ 1u);
+                    mbar_wait(&s_empty[sb], ((jc >> 1) & 1u) ^ 1u);  // P·V of j-2 done with this buffer
                     tc_fence_after();
-                    const uint32_t xj = st_smem + stage * C::kStage;
+                    const uint32_t xj = xs_smem + xs * C::kXSlot;
+                    const uint32_t d = tmem + sb * JB;
 #pragma unroll
                     for (int k = 0; k < DP / 16; ++k) {
                         const uint32_t off = (k >> 2) * C::kXSub + (k & 3) * 32;
-                        umma_f16(tmem + sb * JB, desc_sw128_k(xi_smem + off), desc_sw128_k(xj + off), idesc_s,
+                        umma_f16(d, umma_desc_sw128(xi_smem + off), umma_desc_sw128(xj + off), idesc_s,
                                  k > 0 ? 1u : 0u);
                     }
+                    umma_f16(d, umma_desc_kmajor(xi_smem + C::kXTile, 6, 256),
+                             umma_desc_kmajor(xj + C::kXTile, 6, 256), idesc_s, 1u);
                     umma_commit(&s_full[sb]);
-                    if (it + 1 == seg_end) umma_commit(&xi_empty);  // X_i free once the segment's S MMAs finish
-                    if (prev_stage >= 0) pv(prev_stage, jc - 1, false);
-                    prev_stage = stage;
-                    ++jc;
-                    if (++stage == C::kStages) {
-                        stage = 0;
-                        phase ^= 1u;
+                    umma_commit(&x_empty[xs]);  // X_j consumed
+                    if (++xs == C::kXStages) {
+                        xs = 0;
+                        xph ^= 1u;
                     }
+                    if (jb + 1 == j1) umma_commit(&xi_empty);  // X_i free once the segment's S MMAs finish
+                    if (!first) pv(jc - 1, false);
+                    first = false;
+                    ++jc;
                 }
-                pv(prev_stage, jc - 1, true);  // last P·V of the segment closes the O chunk
-                prev_stage = -1;
+                pv(jc - 1, true);  // last P·V of the segment closes the O chunk
                 ++seg;
             }
         }
-    } else {
-        // ---------------- exp + O drain: two warpgroups, columns [64h, 64h+64) of S / P ----------------
-        // Each thread owns one row (its TMEM lane) and half of the j-block's columns; it also drains
-        // half of the O columns into fp32 registers (lazily, one j-block after the chunk closes, so
-        // the exp work of the next j-block overlaps the last P·V of the chunk).
+    } else if (warp >= 2 && warp < 10) {
+        // ---------------- exp + O drain: two warpgroups, columns [64h, 64h+64) of S ----------------
+        // Each thread owns one row (its TMEM lane) and half of the j-block's columns; it writes its
+        // P values back over the S columns it has just read (so the two halves never race) and
+        // drains half of the O columns into fp32 registers, lazily one j-block after the chunk
+        // closes so the exp work of the next j-block overlaps the chunk's last P·V.
         const int h = (warp - 2) >> 2;
         const int q = warp & 3;  // TMEM lane quarter
         const int row = q * 32 + lane;
@@ -295,56 +347,38 @@ __global__ void __launch_bounds__(kMfThreads, 1)
             tc_fence_before();
             mbar_arrive(&o_empty[ob]);
         };
-        uint32_t jc = 0, chunk = 0, phase = 0;
-        int stage = 0;
-        int64_t it = it_begin;
-        while (it < it_end) {
-            const int64_t r = it / JBn;
-            const int64_t seg_end = min(it_end, (r + 1) * JBn);
-            const int64_t g0 = args.row0 + r * MB;  // first global row of the block (a multiple of 128)
-            const float2 nbv = make_float2(__ldg(args.nbias + g0 + row), __ldg(args.nbias + g0 + row));
-            const int64_t diag_jb = g0 / JB;
+        uint32_t jc = 0, chunk = 0;
+        MfSegments sg(args, cta, G);
+        int64_t r;
+        int j0, j1;
+        while (sg.next(r, j0, j1)) {
+            const int64_t diag_jb = (args.row0 + r * MB) / JB;  // row blocks start at multiples of 128
             uint32_t in_chunk = 0, pend = 0;
             bool pending = false;
-            for (; it < seg_end; ++it, ++jc) {
-                const int64_t jb = it - r * JBn;
+            for (int jb = j0; jb < j1; ++jb, ++jc) {
                 const uint32_t sb = jc & 1u;
                 mbar_wait(&s_full[sb], (jc >> 1) & 1u);
                 tc_fence_after();
+                const uint32_t taddr = tmem + lane_off + sb * JB + h * 64;
                 float sv[64];
-                tmem_ld32(tmem + lane_off + sb * JB + h * 64, sv);
-                tmem_ld32(tmem + lane_off + sb * JB + h * 64 + 32, sv + 32);
+                tmem_ld32(taddr, sv);
+                tmem_ld32(taddr + 32, sv + 32);
                 tmem_ld_wait();
+                uint32_t pk[32];
+                if (jb == diag_jb)
+                    exp64<true>(sv, c2v, h * 64, row, pk);
+                else
+                    exp64<false>(sv, c2v, h * 64, row, pk);
+                tmem_st32(taddr, pk);  // P over the first 32 of the 64 S columns this thread read
+                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&s_empty[sb]);  // S buffer free for the MMA of j+2
-                mbar_wait(&st_full[stage], phase);  // −b_j landed (already implied by s_full)
-                mbar_wait(&p_empty[sb], ((jc >> 1) & 1u) ^ 1u);
-                const uint32_t bsm = bias_smem + stage * kBiasBytes + h * 64 * 4;
-                const uint32_t prow = p_smem + sb * C::kPTile + h * (MB * 128) + row * 128;
-                const bool diag = jb == diag_jb;
-#pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    const float4 b0 = ld_shared_f4(bsm + g * 32);
-                    const float4 b1 = ld_shared_f4(bsm + g * 32 + 16);
-                    uint32_t pk[4];
-                    if (diag)
-                        exp8<true>(sv + 8 * g, c2v, nbv, b0, b1, h * 64 + 8 * g, row, pk);
-                    else
-                        exp8<false>(sv + 8 * g, c2v, nbv, b0, b1, h * 64 + 8 * g, row, pk);
-                    st_shared_v4(prow + ((g ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
-                }
-                fence_proxy_async_smem();  // P visible to the tensor core
                 mbar_arrive(&p_full[sb]);
-                if (++stage == C::kStages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
                 if (pending) {
                     drain(pend);
                     pending = false;
                 }
-                if (++in_chunk == static_cast<uint32_t>(args.kc) || it + 1 == seg_end) {
-                    if (it + 1 == seg_end) {
+                if (++in_chunk == static_cast<uint32_t>(args.kc) || jb + 1 == j1) {
+                    if (jb + 1 == j1) {
                         drain(chunk);
                     } else {
                         pending = true;
@@ -354,7 +388,7 @@ __global__ void __launch_bounds__(kMfThreads, 1)
                     in_chunk = 0;
                 }
             }
-            const int64_t slot = r + cta;
+            const int64_t slot = sg.slot(r);
             float* dst = args.partial + (slot * NPAD + h * C::kHalf) * MB + row;
 #pragma unroll
             for (int j = 0; j < C::kHalf; ++j) {
@@ -391,14 +425,25 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     using C = MfCfg<DP, NPAD>;
     EncodeFn enc = encoder();
     if (!enc) return cudaErrorInvalidValue;
-    CUtensorMap mx, mv;
+    if (v.rpr % JB != 0) return cudaErrorInvalidValue;
+    CUtensorMap mx, mar, mac, mv;
+    const cuuint32_t estr[3] = {1, 1, 1};
     {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.dp), static_cast<cuuint64_t>(a.n)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.dp) * 2};
         cuuint32_t box[2] = {64, MB};
-        cuuint32_t estr[2] = {1, 1};
         if (enc(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(a.x), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    for (int side = 0; side < 2; ++side) {
+        cuuint64_t dims[2] = {kAug, static_cast<cuuint64_t>(a.npad)};
+        cuuint64_t strides[1] = {kAug * 2};
+        cuuint32_t box[2] = {kAug, MB};
+        if (enc(side == 0 ? &mar : &mac, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                const_cast<__nv_bfloat16*>(a.xa) + static_cast<size_t>(side) * a.npad * kAug, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
@@ -407,13 +452,11 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
                               static_cast<cuuint64_t>(v.world)};
         cuuint64_t strides[2] = {static_cast<cuuint64_t>(v.rpr) * 2, static_cast<cuuint64_t>(v.rpr) * v.cols * 2};
         cuuint32_t box[3] = {64, NPAD, 1};
-        cuuint32_t estr[3] = {1, 1, 1};
         if (enc(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(v.v), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    if (v.rpr % JB != 0) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
@@ -426,27 +469,40 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     args.j_blocks = plan.k_tiles;
     args.kc = plan.kc;
     args.row0 = a.row0;
-    args.n = a.n;
     args.kt_chunk = static_cast<int>(v.rpr / JB);
+    args.dp_blocks = plan.dp_blocks;
     args.c2 = static_cast<float>(a.c2);
-    args.nbias = a.bias;
     args.partial = partial;
-    block_av_mf_kernel<DP, NPAD><<<plan.grid, kMfThreads, C::kSmem, stream>>>(mx, mv, args);
+    block_av_mf_kernel<DP, NPAD><<<plan.grid, kMfThreads, C::kSmem, stream>>>(mx, mar, mac, mv, args);
     return cudaGetLastError();
 }
 
+// x (fp64) -> bf16 samples [n][dp] and the augmented columns [2][npad][16]:
+// row side a = [h, m, l, 1, 1, 1, 0…], column side a' = [1, 1, 1, h, m, l, 0…], h + m + l = −|bf16(x)|²/2
 __global__ void mf_prepare_kernel(const double* __restrict__ x, int64_t n, int d, int64_t rs, int64_t cs, int dp,
-                                  double c, __nv_bfloat16* __restrict__ xb, float* __restrict__ bias) {
+                                  int64_t npad, __nv_bfloat16* __restrict__ xb, __nv_bfloat16* __restrict__ xa) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float sq = 0.f;
+    double sq = 0.0;
     for (int k = 0; k < dp; ++k) {
         const __nv_bfloat16 v = __float2bfloat16_rn(k < d ? static_cast<float>(x[i * rs + k * cs]) : 0.f);
         xb[i * dp + k] = v;
-        const float f = __bfloat162float(v);
-        sq = fmaf(f, f, sq);
+        const double f = static_cast<double>(__bfloat162float(v));
+        sq += f * f;
     }
-    bias[i] = static_cast<float>(-c * static_cast<double>(sq));  // −b
+    double v = -0.5 * sq;
+    __nv_bfloat16 part[3];
+    for (int t = 0; t < 3; ++t) {
+        part[t] = __double2bfloat16(v);
+        v -= static_cast<double>(__bfloat162float(part[t]));
+    }
+    const __nv_bfloat16 one = __float2bfloat16_rn(1.f), zero = __float2bfloat16_rn(0.f);
+    __nv_bfloat16* ar = xa + i * kAug;
+    __nv_bfloat16* ac = xa + (npad + i) * kAug;
+    for (int k = 0; k < kAug; ++k) {
+        ar[k] = k < 3 ? part[k] : (k < 6 ? one : zero);
+        ac[k] = k < 3 ? one : (k < 6 ? part[k - 3] : zero);
+    }
 }
 
 }  // namespace
@@ -462,8 +518,11 @@ StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc) {
     p.slots = p.row_blocks + p.grid;
     p.rows_per_block = MB;
     p.cluster = 1;
+    p.dp_blocks = (p.row_blocks / p.grid) * p.grid;  // whole waves; the remainder goes stream-K
     return p;
 }
+
+int mf_aug_cols() { return kAug; }
 
 cudaError_t launch_block_av_mf(const MfMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream) {
@@ -486,10 +545,10 @@ cudaError_t launch_block_av_mf(const MfMatrixView& a, const SplitPanelView& v, c
 #undef RB_MF_CASE
 }
 
-cudaError_t launch_mf_prepare(const double* x, int64_t n, int d, int64_t rs, int64_t cs, int dp, double c,
-                              __nv_bfloat16* xb, float* bias, cudaStream_t stream) {
+cudaError_t launch_mf_prepare(const double* x, int64_t n, int d, int64_t rs, int64_t cs, int dp, int64_t npad,
+                              __nv_bfloat16* xb, __nv_bfloat16* xa, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
-    mf_prepare_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(x, n, d, rs, cs, dp, c, xb, bias);
+    mf_prepare_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(x, n, d, rs, cs, dp, npad, xb, xa);
     return cudaGetLastError();
 }
 

@@ -318,15 +318,14 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
         const double l2e = 1.4426950408889634;
         const int64_t npad = round_up(n, 128);
         k->xb.alloc(static_cast<size_t>(npad) * k->dp * sizeof(__nv_bfloat16));
-        k->bias.alloc(static_cast<size_t>(npad) * sizeof(float));
+        k->xa.alloc(static_cast<size_t>(2) * npad * mf_aug_cols() * sizeof(__nv_bfloat16));
         cuda_check(cudaMemsetAsync(k->xb.as<void>(), 0, k->xb.bytes(), ctx.stream()), "memset");
-        cuda_check(cudaMemsetAsync(k->bias.as<void>(), 0, k->bias.bytes(), ctx.stream()), "memset");
+        cuda_check(cudaMemsetAsync(k->xa.as<void>(), 0, k->xa.bytes(), ctx.stream()), "memset");
         if (!y) {
-            const double c = l2e / (2.0 * sigma * sigma);
-            k->c2 = 2.0 * c;
+            k->c2 = l2e / (sigma * sigma);
             launched(ctx,
-                     launch_mf_prepare(x, n, static_cast<int>(d), 1, ldx, k->dp, c, k->xb.as<__nv_bfloat16>(),
-                                       k->bias.as<float>(), ctx.stream()),
+                     launch_mf_prepare(x, n, static_cast<int>(d), 1, ldx, k->dp, npad, k->xb.as<__nv_bfloat16>(),
+                                       k->xa.as<__nv_bfloat16>(), ctx.stream()),
                      "mf_prepare");
         } else {
             DevBuf cat;
@@ -337,11 +336,10 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
             launched(ctx, launch_scale_columns(y, n, static_cast<int>(dy), 1, ldy, 1.0 / sigma_y,
                                                cat.as<double>() + n * d, ctx.stream()),
                      "scale_columns");
-            const double c = l2e / 2.0;
-            k->c2 = 2.0 * c;
+            k->c2 = l2e;
             launched(ctx,
-                     launch_mf_prepare(cat.as<double>(), n, static_cast<int>(dt), 1, n, k->dp, c,
-                                       k->xb.as<__nv_bfloat16>(), k->bias.as<float>(), ctx.stream()),
+                     launch_mf_prepare(cat.as<double>(), n, static_cast<int>(dt), 1, n, k->dp, npad,
+                                       k->xb.as<__nv_bfloat16>(), k->xa.as<__nv_bfloat16>(), ctx.stream()),
                      "mf_prepare");
             ctx.sync();
         }
@@ -591,7 +589,8 @@ public:
             SplitPanelView v{ctx_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world};
             ctx_.prof_begin();
             if (mf_) {
-                MfMatrixView a{k_.xb.as<__nv_bfloat16>(), k_.bias.as<float>(), k_.n, k_.dp, k_.row0, k_.c2};
+                MfMatrixView a{k_.xb.as<__nv_bfloat16>(), k_.xa.as<__nv_bfloat16>(), k_.n, round_up(k_.n, 128), k_.dp,
+                               k_.row0, k_.c2};
                 if (rows_ > 0)
                     launched(ctx_, launch_block_av_mf(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
                              "block_av_mf");
@@ -614,6 +613,7 @@ public:
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
             e.cluster = plan_.cluster;
+            e.dp_blocks = plan_.dp_blocks;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.e_cur = ctx_.eexp.as<int>() + k * s;
             e.e_next = ctx_.eexp.as<int>() + (k + 1) * s;
@@ -648,6 +648,7 @@ public:
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
             e.cluster = plan_.cluster;
+            e.dp_blocks = plan_.dp_blocks;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.unscale = 1.0;
             e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;

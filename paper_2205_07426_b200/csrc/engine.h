@@ -134,9 +134,9 @@ struct KernelMatrix {
     bool normalized = true;
     DevBuf a64, hi, lo;
     // matrix-free storage
-    DevBuf xb, bias;  // bf16 [n][dp], fp32 −b = −c·|x|² [round_up(n,128)]
+    DevBuf xb, xa;  // bf16 [npad][dp] samples, bf16 [2][npad][16] augmented columns (−|x|²/2)
     int dp = 0;
-    double c2 = 0.0;  // 2c = log2(e)/σ²
+    double c2 = 0.0;  // log2(e)/σ²
 };
 
 using KernelPtr = std::unique_ptr<KernelMatrix>;

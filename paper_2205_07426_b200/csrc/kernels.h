@@ -46,6 +46,9 @@ struct StreamKPlan {
     int slots = 0;
     int rows_per_block = 256;
     int cluster = 1;  // row blocks per stream-K participant (2: CTA pairs)
+    // row blocks [0, dp_blocks) are owned whole, block r by CTA r % grid (data-parallel waves, slot r);
+    // the remaining row blocks' iterations are split stream-K over the grid (slot r + CTA)
+    int dp_blocks = 0;
 };
 
 // ---- block product -------------------------------------------------------
@@ -58,19 +61,22 @@ cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v
 
 // matrix-free: bf16 samples [n][dp] (dp = 64 or 128, zero padded) and negated bias −b = −c·|x|² [n_pad]
 struct MfMatrixView {
-    const __nv_bfloat16* x;
-    const float* bias;
+    const __nv_bfloat16* x;   // bf16 samples [n][dp] (dp = 64 or 128, zero padded)
+    const __nv_bfloat16* xa;  // augmented columns [2][npad][16]: row side, column side (block_av_mf.cu)
     int64_t n;
+    int64_t npad;             // round_up(n, 128)
     int dp;
     int64_t row0;
-    double c2;  // 2c = log2(e)/σ²
+    double c2;  // log2(e)/σ²
 };
 StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc);
+int mf_aug_cols();
 cudaError_t launch_block_av_mf(const MfMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream);
-// x (fp64, element (i,k) at x[i*rs + k*cs]) -> bf16 [n][dp] and negated bias −c·|bf16(x)|²
-cudaError_t launch_mf_prepare(const double* x, int64_t n, int d, int64_t rs, int64_t cs, int dp, double c,
-                              __nv_bfloat16* xb, float* bias, cudaStream_t stream);
+// x (fp64, element (i,k) at x[i*rs + k*cs]) -> bf16 [n][dp] and the augmented columns
+// carrying −|bf16(x)|²/2 as three bf16 terms
+cudaError_t launch_mf_prepare(const double* x, int64_t n, int d, int64_t rs, int64_t cs, int dp, int64_t npad,
+                              __nv_bfloat16* xb, __nv_bfloat16* xa, cudaStream_t stream);
 
 StreamKPlan make_f64_plan(int64_t rows, int64_t cols);
 int f64_npad(int cols);
@@ -86,6 +92,7 @@ struct EpiArgs {
     int k_tiles;
     int grid;
     int cluster;   // slot(r, p) = cluster*(r/cluster + p) + r%cluster
+    int dp_blocks;  // row blocks owned whole (slot r); stream-K over the rest (StreamKPlan)
     int64_t rows;  // local rows (product rows)
     int rows_per_block;  // 256 (tensor-core path) or 128 (fp64 path)
     int s;

@@ -56,8 +56,12 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     const bool valid = i < p.rows;
     const int64_t KT = p.k_tiles;
     const int64_t cl = p.cluster, rb = r / cl, rr = r % cl;
-    const int64_t c_lo = streamk_owner(rb * KT, p.total_iters, p.grid);
-    const int64_t c_hi = streamk_owner((rb + 1) * KT - 1, p.total_iters, p.grid);
+    int64_t c_lo = 0, c_hi = 0;  // whole row block owned by one CTA: slot rb
+    if (rb >= p.dp_blocks) {
+        const int64_t rt = rb - p.dp_blocks, tail = p.total_iters - static_cast<int64_t>(p.dp_blocks) * KT;
+        c_lo = streamk_owner(rt * KT, tail, p.grid);
+        c_hi = streamk_owner((rt + 1) * KT - 1, tail, p.grid);
+    }
     const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
 
     for (int j = 0; j < p.s; ++j) {
