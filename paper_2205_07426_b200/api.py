@@ -56,6 +56,10 @@ class Context:
     def set_tuning(self, grid: int = 0, kc: int = 16) -> None:
         check(L.lib().renyi_ctx_set_tuning(self._h, grid, kc))
 
+    def set_matrix_free_chunk(self, jblocks: int = 4) -> None:
+        """Matrix-free product: j-blocks of 128 samples accumulated in TMEM between fp32 drains."""
+        check(L.lib().renyi_ctx_set_matrix_free_chunk(self._h, jblocks))
+
     def set_operand_mode(self, mode: str = "split") -> None:
         """'split' (default, V as fp16 hi+lo, 3 MMAs) or 'fast' (V hi only, 2 MMAs)."""
         check(L.lib().renyi_ctx_set_operand_mode(self._h, {"split": 0, "fast": 1}[mode]))

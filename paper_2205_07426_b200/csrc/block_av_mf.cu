@@ -12,13 +12,18 @@
 //   P  = exp2(c2·S)             exp warps: TMEM → registers → MUFU ex2 → fp16 → back into TMEM
 //                               (over the S columns just read; c2 = log2(e)/σ²)
 //   O += P · V_j                tcgen05.mma kind::f16 with A = P from TMEM, B = V_j from smem
-// One CTA owns 128 rows (UMMA M); j-blocks of 128. Warp roles: 0 TMA (X_i once per row block,
-// X_j + V_j + a'_j ring), 1 MMA issuer, 2-9 two exp warpgroups (columns [64h, 64h+64) of each
-// S tile) that also drain half of O each into fp32 registers every kc j-blocks (the tensor
-// core's long-K accumulation is lossy, see block_av_tc.cu). S/P and O are double-buffered in
-// TMEM. Persistent schedule: whole row blocks in data-parallel waves (L2 reuse of X_j / V_j across
-// the wave) plus a stream-K split of the tail; partial slots and the pass epilogue are shared with
-// the materialised path.
+//
+// CTA pairs (tcgen05 cta_group::2): a cluster of two CTAs owns 256 rows (128 each, UMMA M=256);
+// the leader issues every MMA for the pair. Each CTA stages only HALF of the shared operands —
+// 64 of the 128 j-rows of X_j / a'_j and NPAD/2 of the V_j columns — so the L2→SMEM traffic and
+// the shared-memory operand reads per row are halved against one CTA per 128 rows.
+// Warp roles per CTA: 0 TMA (X_i, X_j half), 1 S issuer and 11 P·V issuer (leader), 2-9 two exp warpgroups
+// (columns [64h, 64h+64) of each S tile) that also drain half of O each into fp32 registers
+// every kc j-blocks (the tensor core's long-K accumulation is lossy, see block_av_tc.cu),
+// 10 TMA (V_j half). S/P are triple-buffered in TMEM, O double-buffered for NPAD <= 64.
+// Persistent schedule: whole 256-row blocks in data-parallel waves of pairs (L2 reuse of X_j /
+// V_j across the wave) plus a stream-K split of the tail; partial slots and the pass epilogue
+// are shared with the materialised path (cluster = 2).
 #include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -30,58 +35,66 @@ namespace rb {
 
 namespace {
 
-constexpr int MB = 128;   // rows per CTA (UMMA M)
+constexpr int MB = 128;   // rows per CTA (the pair's UMMA M is 256)
 constexpr int JB = 128;   // j-block: S tile N and P·V K
 constexpr int kAug = 16;  // augmented K columns carrying −|x|²/2
-constexpr int kMfThreads = 352;  // TMA(X), MMA, 8 exp/drain warps, TMA(V)
+constexpr int kMfThreads = 384;  // TMA(X), S issuer, 8 exp/drain warps, TMA(V), P·V issuer
+constexpr uint32_t kExpWarps = 8;
 
 template <int DP, int NPAD>
 struct MfCfg {
-    static constexpr int kXTile = MB * DP * 2;    // X tile, bf16, [128][DP] as DP/64 SW128 sub-tiles
-    static constexpr int kXSub = MB * 64 * 2;     // one 64-feature sub-tile (16 KB)
-    static constexpr int kATile = MB * kAug * 2;  // augmented columns, bf16 [128][16], SW32
-    static constexpr int kVTile = NPAD * JB * 2;  // V_j tile, fp16, [NPAD][128] as two SW128 sub-tiles
-    static constexpr int kVSub = NPAD * 64 * 2;
-    static constexpr int kXSlot = kXTile + kATile;  // X_j | a'_j (1024-aligned); also X_i | a_i
-    static constexpr int kBudget = 226 * 1024 - 1024 - kXSlot;
-    // two rings: X_j (released when S(j) completes) and V_j (released when P·V(j) completes)
-    static constexpr int kVStages = (kBudget - 3 * kVTile) / kXSlot >= 3 ? 3 : 2;
+    static constexpr int kXTile = MB * DP * 2;          // X_i, bf16, [128][DP] as DP/64 SW128 sub-tiles
+    static constexpr int kXSub = MB * 64 * 2;           // 16 KB
+    static constexpr int kATile = MB * kAug * 2;        // a_i, bf16 [128][16], SW32
+    static constexpr int kFixed = kXTile + kATile;
+    static constexpr int kXjTile = (JB / 2) * DP * 2;   // this CTA's half of X_j: [64][DP]
+    static constexpr int kXjSub = (JB / 2) * 64 * 2;    // 8 KB
+    static constexpr int kAjTile = (JB / 2) * kAug * 2; // half of a'_j: [64][16]
+    static constexpr int kXSlot = kXjTile + kAjTile;    // 1024-aligned
+    static constexpr int kNH = NPAD / 2;                // V_j columns staged by this CTA
+    static constexpr int kVTile = kNH * JB * 2;         // [kNH][128] as two SW128 sub-tiles
+    static constexpr int kVSub = kNH * 64 * 2;
+    static constexpr int kBudget = 226 * 1024 - 1024 - kFixed;
+    static constexpr int kVStages = 4;
     static constexpr int kXStagesRaw = (kBudget - kVStages * kVTile) / kXSlot;
     static constexpr int kXStages = kXStagesRaw > 4 ? 4 : kXStagesRaw;
-    static constexpr int kSmem = kXSlot * (1 + kXStages) + kVTile * kVStages + 1024;
-    static constexpr int kOCol = 2 * JB;    // O buffers after the two S/P buffers
+    static constexpr int kSmem = kFixed + kXStages * kXSlot + kVStages * kVTile + 1024;
+    static constexpr int kNS = 3;           // S/P buffers in TMEM (S(j+3) never waits on P·V(j))
+    static constexpr int kOCol = kNS * JB;  // O buffers after the S/P buffers
+    static constexpr int kNO = (512 - kOCol) / NPAD >= 2 ? 2 : 1;
     static constexpr int kHalf = NPAD / 2;  // O columns drained by each exp warpgroup
     static_assert(DP == 64 || DP == 128, "feature dimension is padded to 64 or 128");
     static_assert(NPAD % 16 == 0 && NPAD <= 128, "NPAD must be a multiple of 16 in [16,128]");
     static_assert(kXStages >= 2, "need a double-buffered X_j ring");
-    static_assert(kOCol + 2 * NPAD <= 512, "TMEM budget");
+    static_assert(kXSlot % 1024 == 0 && kVTile % 1024 == 0 && kFixed % 1024 == 0, "SW128 alignment");
+    static_assert(kOCol + kNO * NPAD <= 512, "TMEM budget");
 };
 
 struct MfArgs {
-    int64_t total_iters;  // row_blocks * j_blocks
+    int64_t total_iters;  // pair_blocks * j_blocks
     int j_blocks;
     int kc;               // j-blocks per O accumulation chunk
     int64_t row0;         // first global row of this rank
     int kt_chunk;         // j-blocks per V chunk (rpr / 128)
     float c2;             // log2(e)/σ²
-    int64_t dp_blocks;    // row blocks owned whole (waves of gridDim.x); stream-K over the rest
+    int64_t dp_blocks;    // 256-row blocks owned whole (waves of pairs); stream-K over the rest
     float* partial;       // [slots][NPAD][128]
 };
 
-// The (row block, j-range) segments one CTA processes: whole row blocks in data-parallel waves
-// (all CTAs walk the same j-blocks at about the same time, so X_j / V_j are fetched from HBM once
-// per wave and served from L2 to the other CTAs), then an even stream-K share of the tail.
+// The (256-row block, j-range) segments one CTA pair processes: whole blocks in data-parallel
+// waves (all pairs walk the same j-blocks at about the same time, so X_j / V_j are fetched from
+// HBM once per wave and served from L2 to the other pairs), then an even stream-K share of the tail.
 struct MfSegments {
-    int64_t waves, grid, cta, J, dp_rows, it, it_end, w = 0;
-    __device__ MfSegments(const MfArgs& a, int c, int G) : grid(G), cta(c), J(a.j_blocks), dp_rows(a.dp_blocks) {
-        waves = a.dp_blocks / G;
+    int64_t waves, grid, pair, J, dp_rows, it, it_end, w = 0;
+    __device__ MfSegments(const MfArgs& a, int p, int P) : grid(P), pair(p), J(a.j_blocks), dp_rows(a.dp_blocks) {
+        waves = a.dp_blocks / P;
         const int64_t tail = a.total_iters - a.dp_blocks * J;
-        it = tail * c / G;
-        it_end = tail * (c + 1) / G;
+        it = tail * p / P;
+        it_end = tail * (p + 1) / P;
     }
     __device__ bool next(int64_t& r, int& j0, int& j1) {
         if (w < waves) {
-            r = w * grid + cta;
+            r = w * grid + pair;
             j0 = 0;
             j1 = static_cast<int>(J);
             ++w;
@@ -96,8 +109,10 @@ struct MfSegments {
         it = e;
         return true;
     }
-    // partial slot of row block r for this CTA (epilogue: panel.cu)
-    __device__ int64_t slot(int64_t r) const { return r < dp_rows ? r : r + cta; }
+    // partial slot of 128-row block 2r + rank (epilogue: panel.cu, cluster = 2)
+    __device__ int64_t slot(int64_t r, uint32_t rank) const {
+        return r < dp_rows ? 2 * r + rank : 2 * (r + pair) + rank;
+    }
 };
 
 __device__ __forceinline__ uint32_t pack_f16x2_clamp1(float lo, float hi) {
@@ -115,11 +130,11 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-// 64 kernel values of one row: p = exp2(c2·s), packed to 32 fp16 pairs (K order)
+// 16 kernel values of one row: p = exp2(c2·s), packed to 8 fp16 pairs (K order)
 template <bool DIAG>
-__device__ __forceinline__ void exp64(const float* sv, float2 c2v, int col0, int row, uint32_t* pk) {
+__device__ __forceinline__ void exp16(const float* sv, float2 c2v, int col0, int row, uint32_t* pk) {
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
+    for (int e = 0; e < 8; ++e) {
         const float2 a = __fmul2_rn(make_float2(sv[2 * e], sv[2 * e + 1]), c2v);
         float p0 = ex2(a.x), p1 = ex2(a.y);
         if (DIAG) {  // K_ii = 1 exactly (proj/src/ops.cpp:12)
@@ -130,31 +145,53 @@ __device__ __forceinline__ void exp64(const float* sv, float2 c2v, int col0, int
     }
 }
 
+// One thread's 64 columns of S -> P, with the TMEM reads pipelined against the exp work
+template <bool DIAG>
+__device__ __forceinline__ void exp_row64(uint32_t taddr, float2 c2v, int col0, int row, uint32_t* pk) {
+    float s0[16], s1[16];
+    tmem_ld16(taddr, s0);
+    tmem_ld_wait();
+    tmem_ld16(taddr + 16, s1);
+    exp16<DIAG>(s0, c2v, col0, row, pk);
+    tmem_ld_wait();
+    tmem_ld16(taddr + 32, s0);
+    exp16<DIAG>(s1, c2v, col0 + 16, row, pk + 8);
+    tmem_ld_wait();
+    tmem_ld16(taddr + 48, s1);
+    exp16<DIAG>(s0, c2v, col0 + 32, row, pk + 16);
+    tmem_ld_wait();
+    exp16<DIAG>(s1, c2v, col0 + 48, row, pk + 24);
+}
+
 template <int DP, int NPAD>
-__global__ void __launch_bounds__(kMfThreads, 1)
-    block_av_mf_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_ar,
-                       const __grid_constant__ CUtensorMap map_ac, const __grid_constant__ CUtensorMap map_v,
-                       MfArgs args) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
+    block_av_mf_kernel(const __grid_constant__ CUtensorMap map_xi, const __grid_constant__ CUtensorMap map_xj,
+                       const __grid_constant__ CUtensorMap map_ar, const __grid_constant__ CUtensorMap map_ac,
+                       const __grid_constant__ CUtensorMap map_v, MfArgs args) {
     using C = MfCfg<DP, NPAD>;
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t xi_full, xi_empty;
     __shared__ __align__(8) uint64_t x_full[C::kXStages], x_empty[C::kXStages];
     __shared__ __align__(8) uint64_t v_full[C::kVStages], v_empty[C::kVStages];
-    __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
+    __shared__ __align__(8) uint64_t s_full[C::kNS], s_empty[C::kNS], p_full[C::kNS];
+    __shared__ __align__(8) uint64_t o_full[C::kNO], o_empty[C::kNO];
     __shared__ uint32_t tmem_base_smem;
 
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
-    const int G = gridDim.x, cta = blockIdx.x;
+    const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the pair's MMAs)
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, P = gridDim.x >> 1;
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
-    const uint32_t xi_smem = base_u32;                        // X_i | a_i
-    const uint32_t xs_smem = xi_smem + C::kXSlot;             // ring of X_j | a'_j
-    const uint32_t vs_smem = xs_smem + C::kXStages * C::kXSlot;  // ring of V_j
-    constexpr uint32_t kExpThreads = 8 * kWarp;
+    const uint32_t xi_smem = base_u32;                            // X_i | a_i
+    const uint32_t xs_smem = xi_smem + C::kFixed;                 // ring of X_j half | a'_j half
+    const uint32_t vs_smem = xs_smem + C::kXStages * C::kXSlot;   // ring of V_j halves
+    constexpr uint16_t kBoth = 0b11, kLead = 0b01;
 
     if (warp == 0 && lane == 0) {
-        prefetch_tmap(&map_x);
+        prefetch_tmap(&map_xi);
+        prefetch_tmap(&map_xj);
         prefetch_tmap(&map_ar);
         prefetch_tmap(&map_ac);
         prefetch_tmap(&map_v);
@@ -168,43 +205,48 @@ __global__ void __launch_bounds__(kMfThreads, 1)
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < C::kNS; ++b) {
             mbar_init(&s_full[b], 1);
             mbar_init(&s_empty[b], 1);
-            mbar_init(&p_full[b], kExpThreads);
+            mbar_init(&p_full[b], 2 * kExpWarps);  // one arrival per exp warp of both CTAs
+        }
+        for (int b = 0; b < C::kNO; ++b) {
             mbar_init(&o_full[b], 1);
-            mbar_init(&o_empty[b], kExpThreads);
+            mbar_init(&o_empty[b], 2 * kExpWarps);
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(&tmem_base_smem, 512);
+    if (warp == 1) tmem_alloc_2sm(&tmem_base_smem, 512);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers initialised and the pair's TMEM allocated
     tc_fence_after();
     const uint32_t tmem = tmem_base_smem;
 
     if (warp == 0) {
-        // ---------------- TMA producer: X_i, X_j | a'_j ----------------
+        // ---------------- TMA producer: X_i | a_i (own rows), X_j | a'_j (own half) ----------------
         if (lane == 0) {
             const uint64_t pol = policy_evict_normal();  // the wave re-reads X_j / a'_j from L2 (LRU)
+            const uint32_t xi_full_l = mapa_shared(&xi_full, 0);
             int stage = 0;
             uint32_t phase = 0, seg = 0;
-            MfSegments sg(args, cta, G);
+            MfSegments sg(args, pair, P);
             int64_t r;
             int j0, j1;
             while (sg.next(r, j0, j1)) {
-                const int gi0 = static_cast<int>(args.row0 + r * MB);
+                const int gi0 = static_cast<int>(args.row0 + (2 * r + rank) * MB);
                 mbar_wait(&xi_empty, (seg & 1u) ^ 1u);
-                mbar_arrive_expect_tx(&xi_full, C::kXSlot);
-                for (int h = 0; h < DP / 64; ++h) tma_load_2d(base + h * C::kXSub, &map_x, &xi_full, h * 64, gi0, pol);
-                tma_load_2d(base + C::kXTile, &map_ar, &xi_full, 0, gi0, pol);
+                if (leader) mbar_arrive_expect_tx(&xi_full, 2 * C::kFixed);
+                for (int h = 0; h < DP / 64; ++h)
+                    tma_load_2d_2sm(base + h * C::kXSub, &map_xi, xi_full_l, h * 64, gi0, pol);
+                tma_load_2d_2sm(base + C::kXTile, &map_ar, xi_full_l, 0, gi0, pol);
                 for (int jb = j0; jb < j1; ++jb) {
+                    const int jr = jb * JB + static_cast<int>(rank) * (JB / 2);
                     mbar_wait(&x_empty[stage], phase ^ 1u);
+                    if (leader) mbar_arrive_expect_tx(&x_full[stage], 2 * C::kXSlot);
+                    const uint32_t bar = mapa_shared(&x_full[stage], 0);
                     uint8_t* st = base + (xs_smem - base_u32) + stage * C::kXSlot;
-                    mbar_arrive_expect_tx(&x_full[stage], C::kXSlot);
-                    for (int h = 0; h < DP / 64; ++h)
-                        tma_load_2d(st + h * C::kXSub, &map_x, &x_full[stage], h * 64, jb * JB, pol);
-                    tma_load_2d(st + C::kXTile, &map_ac, &x_full[stage], 0, jb * JB, pol);
+                    for (int h = 0; h < DP / 64; ++h) tma_load_2d_2sm(st + h * C::kXjSub, &map_xj, bar, h * 64, jr, pol);
+                    tma_load_2d_2sm(st + C::kXjTile, &map_ac, bar, 0, jr, pol);
                     if (++stage == C::kXStages) {
                         stage = 0;
                         phase ^= 1u;
@@ -214,100 +256,107 @@ __global__ void __launch_bounds__(kMfThreads, 1)
             }
         }
     } else if (warp == 10) {
-        // ---------------- TMA producer: V_j ----------------
+        // ---------------- TMA producer: V_j, columns [rank·NPAD/2, +NPAD/2) ----------------
         if (lane == 0) {
             const uint64_t pol = policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            MfSegments sg(args, cta, G);
+            MfSegments sg(args, pair, P);
             int64_t r;
             int j0, j1;
-            while (sg.next(r, j0, j1)) for (int jb = j0; jb < j1; ++jb) {
-                mbar_wait(&v_empty[stage], phase ^ 1u);
-                uint8_t* st = base + (vs_smem - base_u32) + stage * C::kVTile;
-                mbar_arrive_expect_tx(&v_full[stage], C::kVTile);
-                const int vz = jb / args.kt_chunk, vx = (jb - vz * args.kt_chunk) * JB;
-                for (int h = 0; h < 2; ++h)
-                    tma_load_3d(st + h * C::kVSub, &map_v, &v_full[stage], vx + h * 64, 0, vz, pol);
-                if (++stage == C::kVStages) {
-                    stage = 0;
-                    phase ^= 1u;
+            while (sg.next(r, j0, j1)) {
+                for (int jb = j0; jb < j1; ++jb) {
+                    mbar_wait(&v_empty[stage], phase ^ 1u);
+                    if (leader) mbar_arrive_expect_tx(&v_full[stage], 2 * C::kVTile);
+                    const uint32_t bar = mapa_shared(&v_full[stage], 0);
+                    uint8_t* st = base + (vs_smem - base_u32) + stage * C::kVTile;
+                    const int vz = jb / args.kt_chunk, vx = (jb - vz * args.kt_chunk) * JB;
+                    for (int h = 0; h < 2; ++h)
+                        tma_load_3d_2sm(st + h * C::kVSub, &map_v, bar, vx + h * 64, static_cast<int>(rank) * C::kNH,
+                                        vz, pol);
+                    if (++stage == C::kVStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            constexpr uint32_t idesc_s = umma_idesc_bf16_f32(MB, JB);
-            constexpr uint32_t idesc_o = umma_idesc_f16_f32(MB, NPAD);
-            int xs = 0, vs = 0;
-            uint32_t xph = 0, vph = 0, seg = 0, jc = 0, chunk = 0, in_chunk = 0;
-            auto pv = [&](uint32_t jprev, bool last_of_segment) {
-                const uint32_t pb = jprev & 1u;
-                mbar_wait(&v_full[vs], vph);
-                mbar_wait(&p_full[pb], (jprev >> 1) & 1u);
-                tc_fence_after();
-                const uint32_t ob = chunk & 1u;
-                if (in_chunk == 0) {
-                    mbar_wait(&o_empty[ob], ((chunk >> 1) & 1u) ^ 1u);
-                    tc_fence_after();
-                }
-                const uint32_t d = tmem + C::kOCol + ob * NPAD;
-                const uint32_t pa = tmem + pb * JB;  // P: K 0-63 at columns 0-31, K 64-127 at 64-95
-                const uint32_t vb = vs_smem + vs * C::kVTile;
-#pragma unroll
-                for (int k = 0; k < JB / 16; ++k)
-                    umma_f16_ts(d, pa + (k >> 2) * 64 + (k & 3) * 8,
-                                umma_desc_sw128(vb + (k >> 2) * C::kVSub + (k & 3) * 32), idesc_o,
-                                (in_chunk > 0 || k > 0) ? 1u : 0u);
-                umma_commit(&s_empty[pb]);  // S/P buffer reusable
-                umma_commit(&v_empty[vs]);  // V_j consumed
-                if (++vs == C::kVStages) {
-                    vs = 0;
-                    vph ^= 1u;
-                }
-                ++in_chunk;
-                if (in_chunk == static_cast<uint32_t>(args.kc) || last_of_segment) {
-                    umma_commit(&o_full[ob]);
-                    ++chunk;
-                    in_chunk = 0;
-                }
-            };
-            MfSegments sg(args, cta, G);
+        // ---------------- S issuer (leader CTA only): S(j) = [X_i|a_i]·[X_j|a'_j]ᵀ ----------------
+        // S and P·V are issued from two threads so that neither chain's barrier waits stall the
+        // other's MMAs (tcgen05.commit tracks the MMAs of the issuing thread only).
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc_s = umma_idesc_bf16_f32(2 * MB, JB);
+            int xs = 0;
+            uint32_t xph = 0, seg = 0, jc = 0;
+            MfSegments sg(args, pair, P);
             int64_t r;
             int j0, j1;
             while (sg.next(r, j0, j1)) {
                 mbar_wait(&xi_full, seg & 1u);
                 tc_fence_after();
-                bool first = true;
-                for (int jb = j0; jb < j1; ++jb) {
+                for (int jb = j0; jb < j1; ++jb, ++jc) {
+                    const uint32_t sb = jc % C::kNS;
+                    mbar_wait(&s_empty[sb], ((jc / C::kNS) & 1u) ^ 1u);  // P·V of j-3 done with this buffer
                     mbar_wait(&x_full[xs], xph);
-                    const uint32_t sb = jc & 1u;
-                    mbar_wait(&s_empty[sb], ((jc >> 1) & 1u) ^ 1u);  // P·V of j-2 done with this buffer
                     tc_fence_after();
                     const uint32_t xj = xs_smem + xs * C::kXSlot;
                     const uint32_t d = tmem + sb * JB;
 #pragma unroll
-                    for (int k = 0; k < DP / 16; ++k) {
-                        const uint32_t off = (k >> 2) * C::kXSub + (k & 3) * 32;
-                        umma_f16(d, umma_desc_sw128(xi_smem + off), umma_desc_sw128(xj + off), idesc_s,
-                                 k > 0 ? 1u : 0u);
-                    }
-                    umma_f16(d, umma_desc_kmajor(xi_smem + C::kXTile, 6, 256),
-                             umma_desc_kmajor(xj + C::kXTile, 6, 256), idesc_s, 1u);
-                    umma_commit(&s_full[sb]);
-                    umma_commit(&x_empty[xs]);  // X_j consumed
+                    for (int k = 0; k < DP / 16; ++k)
+                        umma2_f16(d, umma_desc_sw128(xi_smem + (k >> 2) * C::kXSub + (k & 3) * 32),
+                                  umma_desc_sw128(xj + (k >> 2) * C::kXjSub + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
+                    umma2_f16(d, umma_desc_kmajor(xi_smem + C::kXTile, 6, 256),
+                              umma_desc_kmajor(xj + C::kXjTile, 6, 256), idesc_s, 1u);
+                    umma2_commit_mc(&s_full[sb], kBoth);
+                    umma2_commit_mc(&x_empty[xs], kBoth);  // X_j halves consumed
                     if (++xs == C::kXStages) {
                         xs = 0;
                         xph ^= 1u;
                     }
-                    if (jb + 1 == j1) umma_commit(&xi_empty);  // X_i free once the segment's S MMAs finish
-                    if (!first) pv(jc - 1, false);
-                    first = false;
-                    ++jc;
                 }
-                pv(jc - 1, true);  // last P·V of the segment closes the O chunk
+                umma2_commit_mc(&xi_empty, kBoth);  // X_i free after the segment's S MMAs
                 ++seg;
+            }
+        }
+    } else if (warp == 11) {
+        // ---------------- P·V issuer (leader CTA only): O += P(j)·V_j ----------------
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc_o = umma_idesc_f16_f32(2 * MB, NPAD);
+            int vs = 0;
+            uint32_t vph = 0, jc = 0, chunk = 0;
+            MfSegments sg(args, pair, P);
+            int64_t r;
+            int j0, j1;
+            while (sg.next(r, j0, j1)) {
+                uint32_t in_chunk = 0;
+                for (int jb = j0; jb < j1; ++jb, ++jc) {
+                    const uint32_t pb = jc % C::kNS;
+                    const uint32_t ob = chunk % C::kNO;
+                    if (in_chunk == 0) mbar_wait(&o_empty[ob], ((chunk / C::kNO) & 1u) ^ 1u);
+                    mbar_wait(&v_full[vs], vph);
+                    mbar_wait(&p_full[pb], (jc / C::kNS) & 1u);
+                    tc_fence_after();
+                    const uint32_t d = tmem + C::kOCol + ob * NPAD;
+                    const uint32_t pa = tmem + pb * JB;  // P: K 0-63 at columns 0-31, K 64-127 at 64-95
+                    const uint32_t vb = vs_smem + vs * C::kVTile;
+#pragma unroll
+                    for (int k = 0; k < JB / 16; ++k)
+                        umma2_f16_ts(d, pa + (k >> 2) * 64 + (k & 3) * 8,
+                                     umma_desc_sw128(vb + (k >> 2) * C::kVSub + (k & 3) * 32), idesc_o,
+                                     (in_chunk > 0 || k > 0) ? 1u : 0u);
+                    umma2_commit_mc(&s_empty[pb], kLead);  // S/P buffer reusable
+                    umma2_commit_mc(&v_empty[vs], kBoth);  // V_j halves consumed
+                    if (++vs == C::kVStages) {
+                        vs = 0;
+                        vph ^= 1u;
+                    }
+                    if (++in_chunk == static_cast<uint32_t>(args.kc) || jb + 1 == j1) {
+                        umma2_commit_mc(&o_full[ob], kBoth);
+                        ++chunk;
+                        in_chunk = 0;
+                    }
+                }
             }
         }
     } else if (warp >= 2 && warp < 10) {
@@ -325,8 +374,8 @@ __global__ void __launch_bounds__(kMfThreads, 1)
 #pragma unroll
         for (int j = 0; j < C::kHalf; ++j) acc[j] = 0.f;
         auto drain = [&](uint32_t c) {
-            const uint32_t ob = c & 1u;
-            mbar_wait(&o_full[ob], (c >> 1) & 1u);
+            const uint32_t ob = c % C::kNO;
+            mbar_wait(&o_full[ob], (c / C::kNO) & 1u);
             tc_fence_after();
             const uint32_t t0 = tmem + lane_off + C::kOCol + ob * NPAD + h * C::kHalf;
 #pragma unroll
@@ -345,34 +394,32 @@ __global__ void __launch_bounds__(kMfThreads, 1)
                 for (int i = 0; i < 8; ++i) acc[C::kHalf - 8 + i] += m[i];
             }
             tc_fence_before();
-            mbar_arrive(&o_empty[ob]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(&o_empty[ob], 0));
         };
         uint32_t jc = 0, chunk = 0;
-        MfSegments sg(args, cta, G);
+        MfSegments sg(args, pair, P);
         int64_t r;
         int j0, j1;
         while (sg.next(r, j0, j1)) {
-            const int64_t diag_jb = (args.row0 + r * MB) / JB;  // row blocks start at multiples of 128
+            const int64_t diag_jb = (args.row0 + (2 * r + rank) * MB) / JB;  // blocks start at multiples of 128
             uint32_t in_chunk = 0, pend = 0;
             bool pending = false;
             for (int jb = j0; jb < j1; ++jb, ++jc) {
-                const uint32_t sb = jc & 1u;
-                mbar_wait(&s_full[sb], (jc >> 1) & 1u);
+                const uint32_t sb = jc % C::kNS;
+                mbar_wait(&s_full[sb], (jc / C::kNS) & 1u);
                 tc_fence_after();
                 const uint32_t taddr = tmem + lane_off + sb * JB + h * 64;
-                float sv[64];
-                tmem_ld32(taddr, sv);
-                tmem_ld32(taddr + 32, sv + 32);
-                tmem_ld_wait();
                 uint32_t pk[32];
                 if (jb == diag_jb)
-                    exp64<true>(sv, c2v, h * 64, row, pk);
+                    exp_row64<true>(taddr, c2v, h * 64, row, pk);
                 else
-                    exp64<false>(sv, c2v, h * 64, row, pk);
+                    exp_row64<false>(taddr, c2v, h * 64, row, pk);
                 tmem_st32(taddr, pk);  // P over the first 32 of the 64 S columns this thread read
                 tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&p_full[sb]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa_shared(&p_full[sb], 0));
                 if (pending) {
                     drain(pend);
                     pending = false;
@@ -388,7 +435,7 @@ __global__ void __launch_bounds__(kMfThreads, 1)
                     in_chunk = 0;
                 }
             }
-            const int64_t slot = sg.slot(r);
+            const int64_t slot = sg.slot(r, rank);
             float* dst = args.partial + (slot * NPAD + h * C::kHalf) * MB + row;
 #pragma unroll
             for (int j = 0; j < C::kHalf; ++j) {
@@ -400,7 +447,8 @@ __global__ void __launch_bounds__(kMfThreads, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 512);
+    cluster_sync_all();  // the peer is done with the pair's TMEM and barriers
+    if (warp == 1) tmem_dealloc_2sm(tmem, 512);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -426,21 +474,21 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     EncodeFn enc = encoder();
     if (!enc) return cudaErrorInvalidValue;
     if (v.rpr % JB != 0) return cudaErrorInvalidValue;
-    CUtensorMap mx, mar, mac, mv;
+    CUtensorMap mxi, mxj, mar, mac, mv;
     const cuuint32_t estr[3] = {1, 1, 1};
-    {
+    for (int t = 0; t < 2; ++t) {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.dp), static_cast<cuuint64_t>(a.n)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.dp) * 2};
-        cuuint32_t box[2] = {64, MB};
-        if (enc(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(a.x), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        cuuint32_t box[2] = {64, t == 0 ? static_cast<cuuint32_t>(MB) : static_cast<cuuint32_t>(JB / 2)};
+        if (enc(t == 0 ? &mxi : &mxj, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(a.x), dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
     for (int side = 0; side < 2; ++side) {
         cuuint64_t dims[2] = {kAug, static_cast<cuuint64_t>(a.npad)};
         cuuint64_t strides[1] = {kAug * 2};
-        cuuint32_t box[2] = {kAug, MB};
+        cuuint32_t box[2] = {kAug, side == 0 ? static_cast<cuuint32_t>(MB) : static_cast<cuuint32_t>(JB / 2)};
         if (enc(side == 0 ? &mar : &mac, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                 const_cast<__nv_bfloat16*>(a.xa) + static_cast<size_t>(side) * a.npad * kAug, dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -451,7 +499,7 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
         cuuint64_t dims[3] = {static_cast<cuuint64_t>(v.rpr), static_cast<cuuint64_t>(v.cols),
                               static_cast<cuuint64_t>(v.world)};
         cuuint64_t strides[2] = {static_cast<cuuint64_t>(v.rpr) * 2, static_cast<cuuint64_t>(v.rpr) * v.cols * 2};
-        cuuint32_t box[3] = {64, NPAD, 1};
+        cuuint32_t box[3] = {64, static_cast<cuuint32_t>(C::kNH), 1};
         if (enc(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(v.v), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -470,10 +518,10 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     args.kc = plan.kc;
     args.row0 = a.row0;
     args.kt_chunk = static_cast<int>(v.rpr / JB);
-    args.dp_blocks = plan.dp_blocks;
     args.c2 = static_cast<float>(a.c2);
+    args.dp_blocks = plan.dp_blocks;
     args.partial = partial;
-    block_av_mf_kernel<DP, NPAD><<<plan.grid, kMfThreads, C::kSmem, stream>>>(mx, mar, mac, mv, args);
+    block_av_mf_kernel<DP, NPAD><<<2 * plan.grid, kMfThreads, C::kSmem, stream>>>(mxi, mxj, mar, mac, mv, args);
     return cudaGetLastError();
 }
 
@@ -508,17 +556,20 @@ __global__ void mf_prepare_kernel(const double* __restrict__ x, int64_t n, int d
 }  // namespace
 
 StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc) {
+    // CTA pairs over 256-row blocks; the epilogue reads 128-row blocks with cluster = 2
     StreamKPlan p;
+    const int64_t pair_blocks = (rows + 2 * MB - 1) / (2 * MB);
     p.row_blocks = static_cast<int>((rows + MB - 1) / MB);
     p.k_tiles = static_cast<int>((n + JB - 1) / JB);  // j-blocks
-    p.total_iters = static_cast<int64_t>(p.row_blocks) * p.k_tiles;
-    p.grid = grid;
-    if (p.total_iters < grid) p.grid = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
+    p.total_iters = pair_blocks * p.k_tiles;
+    int pairs = std::max(1, grid / 2);
+    if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
+    p.grid = pairs;
     p.kc = kc;
-    p.slots = p.row_blocks + p.grid;
+    p.cluster = 2;
+    p.slots = static_cast<int>(2 * (pair_blocks + pairs));
     p.rows_per_block = MB;
-    p.cluster = 1;
-    p.dp_blocks = (p.row_blocks / p.grid) * p.grid;  // whole waves; the remainder goes stream-K
+    p.dp_blocks = static_cast<int>((pair_blocks / pairs) * pairs);  // whole waves; the remainder goes stream-K
     return p;
 }
 

@@ -162,6 +162,14 @@ int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc) {
     });
 }
 
+int renyi_ctx_set_matrix_free_chunk(renyi_ctx* ctx, int jblocks) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        if (jblocks < 1) rb::fail(rb::kInvalidArgument, "jblocks >= 1 required");
+        ctx->ctx.mf_kc = jblocks;
+    });
+}
+
 int renyi_shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* rpr) {
     return guarded([&] {
         need(row0, "row0"), need(rows, "rows"), need(rpr, "rows_per_rank");

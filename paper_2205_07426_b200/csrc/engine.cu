@@ -515,7 +515,7 @@ public:
             npad_ = tc_npad(s);
         } else if (mf_) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
-            plan_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.kc / 4));  // same K per TMEM chunk (512)
+            plan_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.mf_kc));
             npad_ = tc_npad(s);
         } else {
             plan_ = make_f64_plan(rows_, k.n);

@@ -86,6 +86,7 @@ public:
     // tuning knobs of the block product
     int grid = 0;  // CTAs of the persistent stream-K kernel (0 = SM count)
     int kc = 16;   // k tiles (x32 columns) per TMEM accumulation chunk
+    int mf_kc = 8;  // matrix-free: j-blocks (x128 samples) per TMEM accumulation chunk
     bool operand_split = true;  // V as fp16 hi+lo (3 MMAs); false = "fast" (V hi only, 2 MMAs)
 
     // instrumentation: CUDA-event timing of every block-product launch
