@@ -17,6 +17,8 @@ LIB = PKG / "librenyi_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
+# developer builds only (e.g. -DRB_MF_TRACE for the matrix-free kernel's clock64 timeline)
+COMMON += os.environ.get("RB_EXTRA_NVCC_FLAGS", "").split()
 
 SOURCES = sorted(list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cpp")))
 HEADERS = sorted(list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "renyi_b200.h"])

@@ -25,6 +25,7 @@
 // V_j across the wave) plus a stream-K split of the tail; partial slots and the pass epilogue
 // are shared with the materialised path (cluster = 2).
 #include <algorithm>
+#include <cstdio>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -79,7 +80,20 @@ struct MfArgs {
     float c2;             // log2(e)/σ²
     int64_t dp_blocks;    // 256-row blocks owned whole (waves of pairs); stream-K over the rest
     float* partial;       // [slots][NPAD][128]
+    unsigned long long* trace;  // RB_MF_TRACE builds only: clock64 stamps of CTA 0's first 256 j-blocks
 };
+
+#ifdef RB_MF_TRACE
+__device__ __forceinline__ unsigned long long clock_now() {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    return c;
+}
+#define MF_STAMP(slot, j) \
+    if (args.trace && blockIdx.x == 0 && (j) < 256) args.trace[(j) * 16 + (slot)] = clock_now();
+#else
+#define MF_STAMP(slot, j)
+#endif
 
 // The (256-row block, j-range) segments one CTA pair processes: whole blocks in data-parallel
 // waves (all pairs walk the same j-blocks at about the same time, so X_j / V_j are fetched from
@@ -130,13 +144,38 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// exp2 of a pair on the FMA pipe (offloads the MUFU): 2^x = 2^n · 2^f, n = rint(x), f ∈ [-½, ½],
+// 2^f by a degree-4 near-minimax polynomial (max relative error 2.7e-6, far below the fp16
+// rounding of P), 2^n added into the exponent bits.
+__device__ __forceinline__ float2 exp2_poly(float2 a) {
+    const float2 x = make_float2(fmaxf(a.x, -125.f), fmaxf(a.y, -125.f));  // keeps 2^n·p a normal float
+    const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5·2^23: rint into the low mantissa bits
+    const float2 t = __fadd2_rn(x, magic);
+    const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), x);
+    float2 p = __ffma2_rn(make_float2(0.0095701f, 0.0095701f), f, make_float2(0.05591786f, 0.05591786f));
+    p = __ffma2_rn(p, f, make_float2(0.24024744f, 0.24024744f));
+    p = __ffma2_rn(p, f, make_float2(0.6931218f, 0.6931218f));
+    p = __ffma2_rn(p, f, make_float2(0.9999993f, 0.9999993f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
+constexpr int kEmuPairs = 0;  // of every 8 pairs, this many go to the FMA pipe (0: measured fastest on B200)
+
 // 16 kernel values of one row: p = exp2(c2·s), packed to 8 fp16 pairs (K order)
 template <bool DIAG>
 __device__ __forceinline__ void exp16(const float* sv, float2 c2v, int col0, int row, uint32_t* pk) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const float2 a = __fmul2_rn(make_float2(sv[2 * e], sv[2 * e + 1]), c2v);
-        float p0 = ex2(a.x), p1 = ex2(a.y);
+        float p0, p1;
+        if (e % 4 >= 4 - kEmuPairs / 2) {
+            const float2 q = exp2_poly(a);
+            p0 = q.x, p1 = q.y;
+        } else {
+            p0 = ex2(a.x), p1 = ex2(a.y);
+        }
         if (DIAG) {  // K_ii = 1 exactly (proj/src/ops.cpp:12)
             if (col0 + 2 * e == row) p0 = 1.0f;
             if (col0 + 2 * e + 1 == row) p1 = 1.0f;
@@ -297,8 +336,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 tc_fence_after();
                 for (int jb = j0; jb < j1; ++jb, ++jc) {
                     const uint32_t sb = jc % C::kNS;
+                    MF_STAMP(0, jc)
                     mbar_wait(&s_empty[sb], ((jc / C::kNS) & 1u) ^ 1u);  // P·V of j-3 done with this buffer
+                    MF_STAMP(1, jc)
                     mbar_wait(&x_full[xs], xph);
+                    MF_STAMP(2, jc)
                     tc_fence_after();
                     const uint32_t xj = xs_smem + xs * C::kXSlot;
                     const uint32_t d = tmem + sb * JB;
@@ -310,6 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                               umma_desc_kmajor(xj + C::kXjTile, 6, 256), idesc_s, 1u);
                     umma2_commit_mc(&s_full[sb], kBoth);
                     umma2_commit_mc(&x_empty[xs], kBoth);  // X_j halves consumed
+                    MF_STAMP(3, jc)
                     if (++xs == C::kXStages) {
                         xs = 0;
                         xph ^= 1u;
@@ -333,9 +376,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 for (int jb = j0; jb < j1; ++jb, ++jc) {
                     const uint32_t pb = jc % C::kNS;
                     const uint32_t ob = chunk % C::kNO;
+                    MF_STAMP(4, jc)
                     if (in_chunk == 0) mbar_wait(&o_empty[ob], ((chunk / C::kNO) & 1u) ^ 1u);
                     mbar_wait(&v_full[vs], vph);
+                    MF_STAMP(5, jc)
                     mbar_wait(&p_full[pb], (jc / C::kNS) & 1u);
+                    MF_STAMP(6, jc)
                     tc_fence_after();
                     const uint32_t d = tmem + C::kOCol + ob * NPAD;
                     const uint32_t pa = tmem + pb * JB;  // P: K 0-63 at columns 0-31, K 64-127 at 64-95
@@ -347,6 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                                      (in_chunk > 0 || k > 0) ? 1u : 0u);
                     umma2_commit_mc(&s_empty[pb], kLead);  // S/P buffer reusable
                     umma2_commit_mc(&v_empty[vs], kBoth);  // V_j halves consumed
+                    MF_STAMP(7, jc)
                     if (++vs == C::kVStages) {
                         vs = 0;
                         vph ^= 1u;
@@ -407,7 +454,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
             bool pending = false;
             for (int jb = j0; jb < j1; ++jb, ++jc) {
                 const uint32_t sb = jc % C::kNS;
+                if (warp == 2 && lane == 0) { MF_STAMP(8, jc) }
                 mbar_wait(&s_full[sb], (jc / C::kNS) & 1u);
+                if (warp == 2 && lane == 0) { MF_STAMP(9, jc) }
                 tc_fence_after();
                 const uint32_t taddr = tmem + lane_off + sb * JB + h * 64;
                 uint32_t pk[32];
@@ -415,15 +464,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                     exp_row64<true>(taddr, c2v, h * 64, row, pk);
                 else
                     exp_row64<false>(taddr, c2v, h * 64, row, pk);
+                if (warp == 2 && lane == 0) { MF_STAMP(12, jc) }
                 tmem_st32(taddr, pk);  // P over the first 32 of the 64 S columns this thread read
                 tmem_st_wait();
+                if (warp == 2 && lane == 0) { MF_STAMP(13, jc) }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(mapa_shared(&p_full[sb], 0));
+                if (warp == 2 && lane == 0) { MF_STAMP(10, jc) }
+                if (warp == 6 && lane == 0) { MF_STAMP(11, jc) }
                 if (pending) {
                     drain(pend);
                     pending = false;
                 }
+                if (warp == 2 && lane == 0) { MF_STAMP(14, jc) }
                 if (++in_chunk == static_cast<uint32_t>(args.kc) || jb + 1 == j1) {
                     if (jb + 1 == j1) {
                         drain(chunk);
@@ -521,7 +575,27 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     args.c2 = static_cast<float>(a.c2);
     args.dp_blocks = plan.dp_blocks;
     args.partial = partial;
+    args.trace = nullptr;
+#ifdef RB_MF_TRACE
+    static unsigned long long* trace = nullptr;
+    if (!trace) cudaMalloc(&trace, 256 * 16 * 8);
+    cudaMemsetAsync(trace, 0, 256 * 16 * 8, stream);
+    args.trace = trace;
+#endif
     block_av_mf_kernel<DP, NPAD><<<2 * plan.grid, kMfThreads, C::kSmem, stream>>>(mxi, mxj, mar, mac, mv, args);
+#ifdef RB_MF_TRACE
+    if (NPAD == 128) {
+        cudaStreamSynchronize(stream);
+        static unsigned long long h[256 * 16];
+        cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+        const unsigned long long t0 = h[100 * 16];
+        for (int j = 100; j < 116; ++j) {
+            fprintf(stderr, "j=%3d", j);
+            for (int k = 0; k < 15; ++k) fprintf(stderr, " %7lld", static_cast<long long>(h[j * 16 + k] - t0));
+            fprintf(stderr, "\n");
+        }
+    }
+#endif
     return cudaGetLastError();
 }
 

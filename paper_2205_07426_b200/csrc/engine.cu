@@ -223,17 +223,6 @@ inline void launched(Context& ctx, cudaError_t e, const char* what) {
     ++ctx.launches;
 }
 
-void check_finite(const double* x, int64_t n, int64_t d, int64_t ld, double* max_abs) {
-    double mx = 0.0;
-    for (int64_t j = 0; j < d; ++j)
-        for (int64_t i = 0; i < n; ++i) {
-            const double v = x[i + j * ld];
-            if (!std::isfinite(v)) fail(kNonFinite, "sample matrix contains non-finite values");
-            mx = std::max(mx, std::abs(v));
-        }
-    *max_abs = mx;
-}
-
 void assign_shard(Context& ctx, KernelMatrix& k) {
     k.world = ctx.world();
     k.rank = ctx.rank();
@@ -255,13 +244,10 @@ void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, in
 // ---------------------------------------------------------------- kernel matrices
 KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
                          const double* y, int64_t dy, int64_t ldy, double sigma_y) {
-    // validate_samples (proj/src/kernel.cpp:25-29) on the host copy, then upload column-major as given
+    // upload column-major as given; validate_samples (proj/src/kernel.cpp:25-29) runs on the device copy
     if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
     if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
     if (ldx < n || (y && ldy < n)) fail(kInvalidArgument, "leading dimension smaller than the sample count");
-    double mx = 0.0, my = 0.0;
-    check_finite(x, n, d, ldx, &mx);
-    if (y) check_finite(y, n, dy, ldy, &my);
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     DevBuf xs;
     const int64_t dt = d + (y ? dy : 0);
@@ -315,6 +301,7 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
         const int64_t dt = d + (y ? dy : 0);
         if (dt > 128) fail(kInvalidArgument, "the matrix-free path supports up to 128 features");
         k->dp = dt <= 64 ? 64 : 128;
+        k->dfeat = static_cast<int>(dt);
         const double l2e = 1.4426950408889634;
         const int64_t npad = round_up(n, 128);
         k->xb.alloc(static_cast<size_t>(npad) * k->dp * sizeof(__nv_bfloat16));
@@ -596,8 +583,8 @@ public:
                              "block_av_mf");
                 ctx_.prof_end();
                 // algorithmic flops (SURVEY §8d matrix-free): 2·n_local·n·(d + s); bytes: X, V, Y
-                ctx_.prof_account(2.0 * k_.n * k_.dp + 2.0 * k_.n * s_ + 4.0 * rows_ * s_,
-                                  2.0 * rows_ * k_.n * (k_.dp + s_));
+                ctx_.prof_account(2.0 * k_.n * k_.dfeat + 2.0 * k_.n * s_ + 4.0 * rows_ * s_,
+                                  2.0 * rows_ * k_.n * (k_.dfeat + s_));
             } else {
                 SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
                 if (rows_ > 0)
@@ -1250,13 +1237,10 @@ MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelM
 MutualInfo mutual_information_samples(Context& ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
                                       double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                       const EstParams& p, int prec) {
-    // host buffers: validate, upload X and Y once (column-major as given), then the device path
+    // host buffers: upload X and Y once (column-major as given), then the device path (which validates)
     if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
     if (dx < 1 || dy < 1) fail(kInvalidArgument, "samples need at least one feature");
     if (ldx < n || ldy < n) fail(kInvalidArgument, "leading dimension smaller than the sample count");
-    double mx = 0.0;
-    check_finite(x, n, dx, ldx, &mx);
-    check_finite(y, n, dy, ldy, &mx);
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     DevBuf xs;
     xs.alloc(static_cast<size_t>(n) * (dx + dy) * sizeof(double));

@@ -137,6 +137,7 @@ struct KernelMatrix {
     // matrix-free storage
     DevBuf xb, xa;  // bf16 [npad][dp] samples, bf16 [2][npad][16] augmented columns (−|x|²/2)
     int dp = 0;
+    int dfeat = 0;  // true feature count (algorithmic flops)
     double c2 = 0.0;  // log2(e)/σ²
 };
 

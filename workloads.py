@@ -67,6 +67,13 @@ def f32(x: np.ndarray) -> np.ndarray:
     return np.asarray(x, dtype=np.float32).astype(np.float64)
 
 
+def bf16(x: np.ndarray) -> np.ndarray:
+    """Round to bf16 (round-to-nearest-even) and widen back to fp64."""
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).double().numpy()
+
+
 @dataclass(frozen=True)
 class Config:
     name: str
@@ -92,6 +99,8 @@ CONFIGS = {
                  "n=50000 d=64 fp32 10-mixture, alpha=0.5 Taylor m=30, Hutchinson s=100 Gaussian"),
     "c4": Config("c4", 100000, 16, "fp32", 1.01, "chebyshev", 90, 60, 22, 46, "gaussian",
                  "MI n=100000 d=16/8 fp32, alpha=1.01 Chebyshev[0,1] m=60, Hutch++ s=90 (reference split 22+46)"),
+    "c5": Config("c5", 400000, 128, "mf", 3.0, "int", 120, 0, 30, 60, "gaussian",
+                 "n=400000 d=128 bf16 matrix-free, alpha=3 integer power, Hutch++ s=120 (reference split 30+60)"),
 }
 
 
