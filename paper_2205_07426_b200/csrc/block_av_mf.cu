@@ -17,10 +17,11 @@
 // the leader issues every MMA for the pair. Each CTA stages only HALF of the shared operands —
 // 64 of the 128 j-rows of X_j / a'_j and NPAD/2 of the V_j columns — so the L2→SMEM traffic and
 // the shared-memory operand reads per row are halved against one CTA per 128 rows.
-// Warp roles per CTA: 0 TMA (X_i, X_j half), 1 S issuer and 11 P·V issuer (leader), 2-9 two exp warpgroups
-// (columns [64h, 64h+64) of each S tile) that also drain half of O each into fp32 registers
-// every kc j-blocks (the tensor core's long-K accumulation is lossy, see block_av_tc.cu),
-// 10 TMA (V_j half). S/P are triple-buffered in TMEM, O double-buffered for NPAD <= 64.
+// Warp roles per CTA: 0 TMA (X_i, X_j half), 1 S issuer and 3 P·V issuer (leader only; two issuing
+// threads so neither chain's barrier waits stall the other's MMAs), 2 TMA (V_j half), 4-19 four exp
+// warpgroups (columns [32h, 32h+32) of each S tile) that also drain a quarter of O each into fp32
+// registers every kc j-blocks (the tensor core's long-K accumulation is lossy, see block_av_tc.cu).
+// S/P are triple-buffered in TMEM, O double-buffered for NPAD <= 64.
 // Persistent schedule: whole 256-row blocks in data-parallel waves of pairs (L2 reuse of X_j /
 // V_j across the wave) plus a stream-K split of the tail; partial slots and the pass epilogue
 // are shared with the materialised path (cluster = 2).
@@ -39,8 +40,10 @@ namespace {
 constexpr int MB = 128;   // rows per CTA (the pair's UMMA M is 256)
 constexpr int JB = 128;   // j-block: S tile N and P·V K
 constexpr int kAug = 16;  // augmented K columns carrying −|x|²/2
-constexpr int kMfThreads = 384;  // TMA(X), S issuer, 8 exp/drain warps, TMA(V), P·V issuer
-constexpr uint32_t kExpWarps = 8;
+constexpr int kEG = 4;               // exp/drain warpgroups; group h owns S columns [h·CW, (h+1)·CW)
+constexpr int CW = JB / kEG;         // S columns per exp thread and j-block
+constexpr uint32_t kExpWarps = 4 * kEG;
+constexpr int kMfThreads = 32 * (4 + kExpWarps);  // warps 0-3: TMA(X), S issuer, TMA(V), P·V issuer
 
 template <int DP, int NPAD>
 struct MfCfg {
@@ -63,12 +66,13 @@ struct MfCfg {
     static constexpr int kNS = 3;           // S/P buffers in TMEM (S(j+3) never waits on P·V(j))
     static constexpr int kOCol = kNS * JB;  // O buffers after the S/P buffers
     static constexpr int kNO = (512 - kOCol) / NPAD >= 2 ? 2 : 1;
-    static constexpr int kHalf = NPAD / 2;  // O columns drained by each exp warpgroup
+    static constexpr int kOW = NPAD / kEG;  // O columns drained by each exp warpgroup
     static_assert(DP == 64 || DP == 128, "feature dimension is padded to 64 or 128");
     static_assert(NPAD % 16 == 0 && NPAD <= 128, "NPAD must be a multiple of 16 in [16,128]");
     static_assert(kXStages >= 2, "need a double-buffered X_j ring");
     static_assert(kXSlot % 1024 == 0 && kVTile % 1024 == 0 && kFixed % 1024 == 0, "SW128 alignment");
     static_assert(kOCol + kNO * NPAD <= 512, "TMEM budget");
+    static_assert(kOW % 4 == 0, "O drain granularity");
 };
 
 struct MfArgs {
@@ -184,22 +188,25 @@ __device__ __forceinline__ void exp16(const float* sv, float2 c2v, int col0, int
     }
 }
 
-// One thread's 64 columns of S -> P, with the TMEM reads pipelined against the exp work
+// 32 columns of S (TMEM, two pipelined x16 reads) -> 16 fp16 pairs of P written back to TMEM at wr
 template <bool DIAG>
-__device__ __forceinline__ void exp_row64(uint32_t taddr, float2 c2v, int col0, int row, uint32_t* pk) {
+__device__ __forceinline__ void exp_store32(uint32_t rd, uint32_t wr, float2 c2v, int col0, int row) {
     float s0[16], s1[16];
-    tmem_ld16(taddr, s0);
+    uint32_t pk[16];
+    tmem_ld16(rd, s0);
     tmem_ld_wait();
-    tmem_ld16(taddr + 16, s1);
+    tmem_ld16(rd + 16, s1);
     exp16<DIAG>(s0, c2v, col0, row, pk);
     tmem_ld_wait();
-    tmem_ld16(taddr + 32, s0);
     exp16<DIAG>(s1, c2v, col0 + 16, row, pk + 8);
-    tmem_ld_wait();
-    tmem_ld16(taddr + 48, s1);
-    exp16<DIAG>(s0, c2v, col0 + 32, row, pk + 16);
-    tmem_ld_wait();
-    exp16<DIAG>(s1, c2v, col0 + 48, row, pk + 24);
+    tmem_st16(wr, pk);
+}
+
+// One thread's CW columns of S -> P (P over the first CW/2 of the columns it read)
+template <bool DIAG>
+__device__ __forceinline__ void exp_cols(uint32_t taddr, float2 c2v, int col0, int row) {
+#pragma unroll
+    for (int c = 0; c < CW; c += 32) exp_store32<DIAG>(taddr + c, taddr + c / 2, c2v, col0 + c, row);
 }
 
 template <int DP, int NPAD>
@@ -294,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 ++seg;
             }
         }
-    } else if (warp == 10) {
+    } else if (warp == 2) {
         // ---------------- TMA producer: V_j, columns [rank·NPAD/2, +NPAD/2) ----------------
         if (lane == 0) {
             const uint64_t pol = policy_evict_normal();
@@ -362,7 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 ++seg;
             }
         }
-    } else if (warp == 11) {
+    } else if (warp == 3) {
         // ---------------- P·V issuer (leader CTA only): O += P(j)·V_j ----------------
         if (leader && lane == 0) {
             constexpr uint32_t idesc_o = umma_idesc_f16_f32(2 * MB, NPAD);
@@ -384,11 +391,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                     MF_STAMP(6, jc)
                     tc_fence_after();
                     const uint32_t d = tmem + C::kOCol + ob * NPAD;
-                    const uint32_t pa = tmem + pb * JB;  // P: K 0-63 at columns 0-31, K 64-127 at 64-95
+                    // P of exp group g (K in [g·CW, (g+1)·CW)) sits at columns [g·CW, g·CW + CW/2)
+                    const uint32_t pa = tmem + pb * JB;
                     const uint32_t vb = vs_smem + vs * C::kVTile;
 #pragma unroll
                     for (int k = 0; k < JB / 16; ++k)
-                        umma2_f16_ts(d, pa + (k >> 2) * 64 + (k & 3) * 8,
+                        umma2_f16_ts(d, pa + (k / (CW / 16)) * CW + (k % (CW / 16)) * 8,
                                      umma_desc_sw128(vb + (k >> 2) * C::kVSub + (k & 3) * 32), idesc_o,
                                      (in_chunk > 0 || k > 0) ? 1u : 0u);
                     umma2_commit_mc(&s_empty[pb], kLead);  // S/P buffer reusable
@@ -406,39 +414,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 }
             }
         }
-    } else if (warp >= 2 && warp < 10) {
+    } else if (warp >= 4) {
         // ---------------- exp + O drain: two warpgroups, columns [64h, 64h+64) of S ----------------
         // Each thread owns one row (its TMEM lane) and half of the j-block's columns; it writes its
         // P values back over the S columns it has just read (so the two halves never race) and
         // drains half of the O columns into fp32 registers, lazily one j-block after the chunk
         // closes so the exp work of the next j-block overlaps the chunk's last P·V.
-        const int h = (warp - 2) >> 2;
+        const int h = (warp - 4) >> 2;  // exp warpgroup: S columns [h·CW, (h+1)·CW), O columns [h·OW, (h+1)·OW)
         const int q = warp & 3;  // TMEM lane quarter
         const int row = q * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         const float2 c2v = make_float2(args.c2, args.c2);
-        float acc[C::kHalf];
+        float acc[C::kOW];
 #pragma unroll
-        for (int j = 0; j < C::kHalf; ++j) acc[j] = 0.f;
+        for (int j = 0; j < C::kOW; ++j) acc[j] = 0.f;
         auto drain = [&](uint32_t c) {
             const uint32_t ob = c % C::kNO;
             mbar_wait(&o_full[ob], (c / C::kNO) & 1u);
             tc_fence_after();
-            const uint32_t t0 = tmem + lane_off + C::kOCol + ob * NPAD + h * C::kHalf;
+            const uint32_t t0 = tmem + lane_off + C::kOCol + ob * NPAD + h * C::kOW;
+            constexpr int n16 = C::kOW / 16, r8 = (C::kOW % 16) / 8, r4 = (C::kOW % 8) / 4;
 #pragma unroll
-            for (int j0 = 0; j0 + 16 <= C::kHalf; j0 += 16) {
+            for (int j0 = 0; j0 < 16 * n16; j0 += 16) {
                 float m[16];
                 tmem_ld16(t0 + j0, m);
                 tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i];
             }
-            if constexpr (C::kHalf % 16 != 0) {
+            if constexpr (r8) {
                 float m[8];
-                tmem_ld8(t0 + C::kHalf - 8, m);
+                tmem_ld8(t0 + 16 * n16, m);
                 tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[C::kHalf - 8 + i] += m[i];
+                for (int i = 0; i < 8; ++i) acc[16 * n16 + i] += m[i];
+            }
+            if constexpr (r4) {
+                float m[4];
+                tmem_ld4(t0 + 16 * n16 + 8 * r8, m);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[16 * n16 + 8 * r8 + i] += m[i];
             }
             tc_fence_before();
             __syncwarp();
@@ -454,30 +470,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
             bool pending = false;
             for (int jb = j0; jb < j1; ++jb, ++jc) {
                 const uint32_t sb = jc % C::kNS;
-                if (warp == 2 && lane == 0) { MF_STAMP(8, jc) }
+                if (warp == 4 && lane == 0) { MF_STAMP(8, jc) }
                 mbar_wait(&s_full[sb], (jc / C::kNS) & 1u);
-                if (warp == 2 && lane == 0) { MF_STAMP(9, jc) }
+                if (warp == 4 && lane == 0) { MF_STAMP(9, jc) }
                 tc_fence_after();
-                const uint32_t taddr = tmem + lane_off + sb * JB + h * 64;
-                uint32_t pk[32];
+                const uint32_t taddr = tmem + lane_off + sb * JB + h * CW;
                 if (jb == diag_jb)
-                    exp_row64<true>(taddr, c2v, h * 64, row, pk);
+                    exp_cols<true>(taddr, c2v, h * CW, row);
                 else
-                    exp_row64<false>(taddr, c2v, h * 64, row, pk);
-                if (warp == 2 && lane == 0) { MF_STAMP(12, jc) }
-                tmem_st32(taddr, pk);  // P over the first 32 of the 64 S columns this thread read
+                    exp_cols<false>(taddr, c2v, h * CW, row);
                 tmem_st_wait();
-                if (warp == 2 && lane == 0) { MF_STAMP(13, jc) }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(mapa_shared(&p_full[sb], 0));
-                if (warp == 2 && lane == 0) { MF_STAMP(10, jc) }
-                if (warp == 6 && lane == 0) { MF_STAMP(11, jc) }
-                if (pending) {
+                if (warp == 4 && lane == 0) { MF_STAMP(10, jc) }
+                if (pending) {  // chunk closed one j-block ago; its last P·V has had time to finish
                     drain(pend);
                     pending = false;
                 }
-                if (warp == 2 && lane == 0) { MF_STAMP(14, jc) }
                 if (++in_chunk == static_cast<uint32_t>(args.kc) || jb + 1 == j1) {
                     if (jb + 1 == j1) {
                         drain(chunk);
@@ -490,9 +500,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 }
             }
             const int64_t slot = sg.slot(r, rank);
-            float* dst = args.partial + (slot * NPAD + h * C::kHalf) * MB + row;
+            float* dst = args.partial + (slot * NPAD + h * C::kOW) * MB + row;
 #pragma unroll
-            for (int j = 0; j < C::kHalf; ++j) {
+            for (int j = 0; j < C::kOW; ++j) {
                 dst[j * MB] = acc[j];
                 acc[j] = 0.f;
             }

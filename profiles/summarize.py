@@ -24,6 +24,10 @@ KEYS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "launch__cluster_dim_x": "cluster_x",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_active_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_mufu_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
 }
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "msecond": 1e-3, "usecond": 1e-6,
          "us": 1e-6, "ns": 1e-9, "nsecond": 1e-9, "Ghz": 1e9, "Mhz": 1e6}
