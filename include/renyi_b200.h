@@ -130,6 +130,13 @@ typedef struct { /* EntropyEstimate, proj/include/renyi/entropy.hpp:32-41 */
     renyi_trace_estimate trace;
 } renyi_entropy_estimate;
 
+typedef struct { /* MreCell, proj/include/renyi/simulate.hpp:27-37 (oracle_elapsed stays with the caller) */
+    double alpha;
+    int s, m, method;
+    double mre, sd, mean_elapsed; /* mean_elapsed: batched wall time / trials */
+    int trials;
+} renyi_mre_cell;
+
 typedef struct { /* MutualInformation, proj/include/renyi/measures.hpp:24-29 */
     double value, vars_entropy, target_entropy, joint_entropy;
 } renyi_mi_estimate;
@@ -141,6 +148,8 @@ int renyi_ctx_create(int device, renyi_ctx** out);
 int renyi_ctx_destroy(renyi_ctx* ctx);
 int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc);
 int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode);
+/* matrix-free product: j-blocks (of 128 samples) accumulated in TMEM before each fp32 drain */
+int renyi_ctx_set_matrix_free_chunk(renyi_ctx* ctx, int jblocks);
 int renyi_ctx_sync(renyi_ctx* ctx);
 /* returns the engine's cached device blocks (kernel storage, panels, scratch) to the driver */
 int renyi_release_cached_memory(void);
@@ -213,6 +222,16 @@ int renyi_hutchpp(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, 
 /* estimate — proj/src/entropy.cpp:201-275 */
 int renyi_estimate(renyi_ctx* ctx, const renyi_kernel* k, const renyi_estimator_params* p,
                    renyi_entropy_estimate* out);
+/* K trials of estimate() with seeds derive_key(p->seed, t), bounds resolved once, as measure_cell
+ * runs them (proj/src/simulate.cpp:19-51); the probes of all trials share the passes over A.
+ * out[trials]. */
+int renyi_estimate_trials(renyi_ctx* ctx, const renyi_kernel* k, const renyi_estimator_params* p, int trials,
+                          renyi_entropy_estimate* out);
+/* measure_cell — proj/src/simulate.cpp:19-72 (MRE/SD over K trials against a known exact entropy) */
+int renyi_measure_cell(renyi_ctx* ctx, const renyi_kernel* k, double exact_entropy,
+                       const renyi_estimator_params* p, int trials, renyi_mre_cell* out);
+/* mixture_samples — proj/src/simulate.cpp:9-17 (host; out column-major n x d) */
+int renyi_mixture_samples(int n, int d, uint64_t seed, double center, double* out);
 /* entropy_int / entropy_taylor / entropy_chebyshev — proj/src/entropy.cpp:111-135 */
 int renyi_entropy_int(renyi_ctx* ctx, const renyi_kernel* k, int alpha, int s, uint64_t seed,
                       renyi_entropy_estimate* out);

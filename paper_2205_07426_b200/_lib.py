@@ -109,6 +109,19 @@ class EstimatorParamsC(C.Structure):
     ]
 
 
+class MreCellC(C.Structure):
+    _fields_ = [
+        ("alpha", C.c_double),
+        ("s", C.c_int),
+        ("m", C.c_int),
+        ("method", C.c_int),
+        ("mre", C.c_double),
+        ("sd", C.c_double),
+        ("mean_elapsed", C.c_double),
+        ("trials", C.c_int),
+    ]
+
+
 class EntropyEstimateC(C.Structure):
     _fields_ = [
         ("entropy", C.c_double),
@@ -184,6 +197,9 @@ SIGNATURES = {
     "renyi_estimate_bounds": (C.c_int, [_P, _P, C.POINTER(PowerOptionsC), C.POINTER(SpectrumBoundsC)]),
     "renyi_hutchpp": (C.c_int, [_P, _P, C.POINTER(Matfun), C.POINTER(Sketch), C.POINTER(TraceEstimateC)]),
     "renyi_estimate": (C.c_int, [_P, _P, C.POINTER(EstimatorParamsC), C.POINTER(EntropyEstimateC)]),
+    "renyi_estimate_trials": (C.c_int, [_P, _P, C.POINTER(EstimatorParamsC), C.c_int, C.POINTER(EntropyEstimateC)]),
+    "renyi_measure_cell": (C.c_int, [_P, _P, C.c_double, C.POINTER(EstimatorParamsC), C.c_int, C.POINTER(MreCellC)]),
+    "renyi_mixture_samples": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_double, C.POINTER(C.c_double)]),
     "renyi_entropy_int": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_uint64, C.POINTER(EntropyEstimateC)]),
     "renyi_entropy_taylor": (
         C.c_int,

@@ -579,6 +579,85 @@ def estimate(a: NormalizedKernel, params: EstimatorParams) -> EntropyEstimate:
     return EntropyEstimate._from(out)
 
 
+def estimate_trials(a: NormalizedKernel, params: EstimatorParams, trials: int) -> list:
+    """K trials of estimate() with seeds derive_key(params.seed, t), bounds resolved once (the
+    measure_cell protocol, proj/src/simulate.cpp:19-51); all trials' probes share the passes over A."""
+    if params.method == "exact":
+        raise RenyiError(1, "method=exact has no trials")
+    out = (L.EntropyEstimateC * max(int(trials), 1))()
+    check(L.lib().renyi_estimate_trials(a.ctx.handle, a.handle, C.byref(params._c()), int(trials), out))
+    return [EntropyEstimate._from(out[t]) for t in range(int(trials))]
+
+
+@dataclass
+class MreCell:
+    alpha: float
+    s: int
+    m: int
+    method: str
+    mre: float
+    sd: float
+    mean_elapsed: float
+    trials: int
+    oracle_elapsed: float = 0.0
+
+
+def measure_cell(a: NormalizedKernel, exact_entropy: float, params: EstimatorParams, trials: int) -> MreCell:
+    """measure_cell (proj/src/simulate.cpp:19-72): MRE / SD of K batched trials against exact_entropy."""
+    out = L.MreCellC()
+    check(L.lib().renyi_measure_cell(a.ctx.handle, a.handle, float(exact_entropy), C.byref(params._c()),
+                                     int(trials), C.byref(out)))
+    return MreCell(out.alpha, out.s, out.m, METHOD_NAMES.get(out.method, "?"), out.mre, out.sd, out.mean_elapsed,
+                   out.trials)
+
+
+def mixture_samples(n: int, d: int, seed: int, center: float = 1.0) -> np.ndarray:
+    """(1/2) N(-center, I_d) + (1/2) N(+center, I_d) from the reference stream (proj/src/simulate.cpp:9-17)."""
+    out = np.empty((n, d), order="F")
+    check(L.lib().renyi_mixture_samples(int(n), int(d), seed & (2**64 - 1), float(center), _dptr(out)))
+    return out
+
+
+@dataclass
+class SimulationSpec:
+    """proj/include/renyi/simulate.hpp:13-25."""
+    n: int = 1000
+    d: int = 10
+    center: float = 1.0
+    sigma: float = 1.0
+    alphas: Sequence[float] = (2.0,)
+    s_list: Sequence[int] = (64,)
+    m_list: Sequence[int] = (0,)
+    trials: int = 100
+    seed: int = 0
+    method: str = "auto"
+    precision: str = "fp64"
+
+
+def run_simulation(spec: SimulationSpec, ctx: Optional["Context"] = None) -> list:
+    """run_simulation (proj/src/simulate.cpp:74-104): mixture samples, one kernel, the exact entropy
+    per alpha (eigendecomposition on the GPU), then measure_cell for every (alpha, s, m)."""
+    if spec.trials < 1:
+        raise RenyiError(1, "K must be >= 1")
+    if spec.n < 16:
+        raise RenyiError(1, "simulation needs n >= 16")
+    x = mixture_samples(spec.n, spec.d, spec.seed, spec.center)
+    k = build_kernel(x, GaussianKernel(spec.sigma), spec.precision, ctx=ctx)
+    cells = []
+    for alpha in spec.alphas:
+        oracle = entropy_exact(k, alpha)
+        for s in spec.s_list:
+            for m in spec.m_list:
+                p = EstimatorParams(alpha=alpha, method=spec.method, s=s, m=m, seed=spec.seed)
+                try:
+                    cell = measure_cell(k, oracle.entropy, p, spec.trials)
+                except RenyiError as e:
+                    raise RenyiError(e.status, f"cell alpha={alpha} s={s} m={m}: {e}") from None
+                cell.oracle_elapsed = oracle.elapsed
+                cells.append(cell)
+    return cells
+
+
 def entropy_int(a: NormalizedKernel, alpha: int, s: int, seed: int) -> EntropyEstimate:
     out = L.EntropyEstimateC()
     check(L.lib().renyi_entropy_int(a.ctx.handle, a.handle, int(alpha), s, seed & (2**64 - 1), C.byref(out)))

@@ -461,6 +461,25 @@ int renyi_estimate(renyi_ctx* ctx, const renyi_kernel* k, const renyi_estimator_
     });
 }
 
+int renyi_estimate_trials(renyi_ctx* ctx, const renyi_kernel* k, const renyi_estimator_params* p, int trials,
+                          renyi_entropy_estimate* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        const std::vector<rb::EntropyEst> est = rb::estimate_trials(ctx->ctx, *k->k, to_params(p), trials);
+        for (int t = 0; t < trials; ++t) from_entropy(est[t], out + t);
+    });
+}
+
+int renyi_measure_cell(renyi_ctx* ctx, const renyi_kernel* k, double exact_entropy,
+                       const renyi_estimator_params* p, int trials, renyi_mre_cell* out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(k, "kernel"), need(out, "out");
+        const rb::MreCell c = rb::measure_cell(ctx->ctx, *k->k, exact_entropy, to_params(p), trials);
+        out->alpha = c.alpha, out->s = c.s, out->m = c.m, out->method = c.method;
+        out->mre = c.mre, out->sd = c.sd, out->mean_elapsed = c.mean_elapsed, out->trials = c.trials;
+    });
+}
+
 int renyi_entropy_int(renyi_ctx* ctx, const renyi_kernel* k, int alpha, int s, uint64_t seed,
                       renyi_entropy_estimate* out) {
     renyi_estimator_params p;
@@ -599,6 +618,19 @@ int renyi_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int
         need(label, "label"), need(out, "out");
         if (n < 0 || cols < 0) rb::fail(rb::kInvalidArgument, "negative panel size");
         rb::probe_panel(n, cols, seed, label, kind, out);
+    });
+}
+
+int renyi_mixture_samples(int n, int d, uint64_t seed, double center, double* out) {
+    // proj/src/simulate.cpp:9-17: one stream, row by row; out column-major n x d
+    return guarded([&] {
+        need(out, "out");
+        if (n < 0 || d < 0) rb::fail(rb::kInvalidArgument, "negative sample size");
+        rb::RandomStream st(rb::derive_key(seed, rb::hash_name("mixture")));
+        for (int i = 0; i < n; ++i) {
+            const double mu = (st.next_u64() & 1) ? center : -center;
+            for (int j = 0; j < d; ++j) out[i + static_cast<int64_t>(j) * n] = mu + st.next_gaussian();
+        }
     });
 }
 

@@ -1112,9 +1112,7 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-EntropyEst from_hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, double alpha, int s, const EstParams& p,
-                        int method, int m_used) {
-    const auto t0 = std::chrono::steady_clock::now();
+SketchCfg sketch_cfg(const EstParams& p, int s) {
     SketchCfg cfg;
     if (p.s_q >= 0 || p.s_g >= 0) {
         cfg.s_q = std::max(p.s_q, 0);
@@ -1126,7 +1124,10 @@ EntropyEst from_hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, do
     }
     cfg.seed = p.seed;
     cfg.probe_kind = p.probe_kind;
-    const TraceEst tr = hutchpp(ctx, k, f, cfg);
+    return cfg;
+}
+
+EntropyEst entropy_of(const TraceEst& tr, double alpha, int method, int s, int m_used) {
     EntropyEst est;
     est.trace = tr;
     est.trace_estimate = tr.value;
@@ -1135,29 +1136,37 @@ EntropyEst from_hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, do
     est.s_used = s;
     est.m_used = m_used;
     est.deterministic = tr.exact;
-    est.elapsed = seconds_since(t0);
     return est;
 }
 
-}  // namespace
+// Everything estimate() decides before the trace estimator runs (proj/src/entropy.cpp:201-275):
+// routing, bounds, (s, m) selection and the matrix function. Seed-independent except for the
+// bounds' power iteration, which uses derive_key(p.seed, "bounds").
+struct Resolved {
+    int method = kMethodInt;
+    MatFun f;
+    double alpha = 2.0;
+    int s = 0, m_used = 0;
+    bool has_bounds = false;
+    SpectrumBoundsH bounds;
+};
 
-EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p) {
-    // proj/src/entropy.cpp:201-275
+Resolved resolve(Context& ctx, const KernelMatrix& k, const EstParams& p) {
     validate_alpha(p.alpha);
-    const auto t0 = std::chrono::steady_clock::now();
     const int64_t n = k.n;
     int alpha_int = 0;
     const bool is_int = integer_alpha(p.alpha, &alpha_int);
-    bool have = p.has_bounds;
-    SpectrumBoundsH bounds = p.bounds;
+    Resolved r;
+    r.has_bounds = p.has_bounds;
+    r.bounds = p.bounds;
     auto ensure_bounds = [&]() -> const SpectrumBoundsH& {
-        if (!have) {
+        if (!r.has_bounds) {
             PowerOpts o = p.power;
             o.seed = derive_key(p.seed, hash_name("bounds"));
-            bounds = estimate_bounds(ctx, k, o);
-            have = true;
+            r.bounds = estimate_bounds(ctx, k, o);
+            r.has_bounds = true;
         }
-        return bounds;
+        return r.bounds;
     };
     int method = p.method;
     if (method == kMethodAuto) {
@@ -1170,17 +1179,18 @@ EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p) {
             method = (flat_full_rank || flat_deficient) ? kMethodTaylor : kMethodChebyshev;
         }
     }
-    EntropyEst est;
+    r.method = method;
     switch (method) {
         case kMethodExact:
             fail(kInvalidArgument,
                  "method=exact is the O(n^3) eigendecomposition check oracle; it is not a device path");
         case kMethodInt: {
             if (!is_int) fail(kInvalidArgument, "method=int needs an integer alpha >= 2");
-            const int s = p.s > 0 ? p.s
-                                  : select_params(p.alpha, p.epsilon, p.delta, SpectrumBoundsH{}, n, kMethodInt).s;
+            r.s = p.s > 0 ? p.s : select_params(p.alpha, p.epsilon, p.delta, SpectrumBoundsH{}, n, kMethodInt).s;
             if (alpha_int < 2) fail(kInvalidArgument, "entropy_int needs integer alpha >= 2");
-            est = from_hutchpp(ctx, k, MatFun::int_power(alpha_int), alpha_int, s, p, kMethodInt, 0);
+            r.f = MatFun::int_power(alpha_int);
+            r.alpha = alpha_int;
+            r.m_used = 0;
             break;
         }
         case kMethodTaylor:
@@ -1194,27 +1204,193 @@ EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p) {
                 if (p.s > 0) sel.s = p.s;
                 if (p.m > 0) sel.m = p.m;
             }
-            validate_alpha(p.alpha);
+            r.s = sel.s;
+            r.alpha = p.alpha;
             if (method == kMethodTaylor) {
                 require_non_integer(p.alpha, "entropy_taylor");
                 const int m = std::max(sel.m, static_cast<int>(std::ceil(p.alpha)) + 1);
-                const int m_min = static_cast<int>(std::ceil(p.alpha)) + 1;
-                if (m < m_min) fail(kInvalidArgument, "entropy_taylor needs m >= ceil(alpha)+1");
-                est = from_hutchpp(ctx, k, MatFun::taylor(p.alpha, m, b.v), p.alpha, sel.s, p, kMethodTaylor, m);
+                r.f = MatFun::taylor(p.alpha, m, b.v);
+                r.m_used = m;
             } else {
                 require_non_integer(p.alpha, "entropy_chebyshev");
-                est = from_hutchpp(ctx, k, MatFun::chebyshev(p.alpha, sel.m, b.u, b.v), p.alpha, sel.s, p,
-                                   kMethodChebyshev, sel.m);
+                r.f = MatFun::chebyshev(p.alpha, sel.m, b.u, b.v);
+                r.m_used = sel.m;
             }
             break;
         }
         default:
             fail(kInvalidArgument, "unresolved auto method");
     }
-    est.has_bounds = have;
-    est.bounds_used = bounds;
+    return r;
+}
+
+}  // namespace
+
+EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p) {
+    // proj/src/entropy.cpp:201-275
+    const auto t0 = std::chrono::steady_clock::now();
+    const Resolved r = resolve(ctx, k, p);
+    EntropyEst est = entropy_of(hutchpp(ctx, k, r.f, sketch_cfg(p, r.s)), r.alpha, r.method, r.s, r.m_used);
+    est.has_bounds = r.has_bounds;
+    est.bounds_used = r.bounds;
     est.elapsed = seconds_since(t0);
     return est;
+}
+
+// ---------------------------------------------------------------- batched trials
+namespace {
+
+// Hutch++ for several probe seeds at once: the sketch products and the
+// f(A)·[Q_t | W_t] recurrences of all trials share the same passes over A as extra panel columns
+// (up to 128 per pass), so K trials cost ~ceil(K·cols/128) passes instead of K. Each column's
+// arithmetic is the same as in a single-trial run.
+std::vector<TraceEst> hutchpp_batch(Context& ctx, const KernelMatrix& k, const MatFun& f, const SketchCfg& base,
+                                    const std::vector<uint64_t>& seeds) {
+    const int K = static_cast<int>(seeds.size());
+    const int64_t n = k.n, ld = k.rpr, rows = k.rows;
+    const int s_q = base.s_q, s_g = base.s_g, cost = f.query_cost();
+    std::vector<TraceEst> out(K);
+    if (s_q < 0 || s_g < 0 || s_q + s_g < 1) fail(kInvalidArgument, "hutchpp needs a positive query budget");
+    if (s_q >= n || base.sketch || base.probes) {  // exact branch or injected probes: one trial at a time
+        for (int t = 0; t < K; ++t) {
+            SketchCfg c = base;
+            c.seed = seeds[t];
+            out[t] = hutchpp(ctx, k, f, c);
+        }
+        return out;
+    }
+    // sketch products of every trial: Y = A·[S_0 | S_1 | ...]
+    std::vector<DevBuf> q(K);
+    std::vector<int> rank(K, 0);
+    if (s_q > 0) {
+        const int cols = K * s_q;
+        DevBuf sk, y;
+        sk.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
+        y.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
+        for (int t = 0; t < K; ++t) {
+            DevBuf one;
+            make_probes(ctx, k, one, s_q, ld, nullptr, seeds[t], "hutchpp-sketch", base.probe_kind);
+            cuda_check(cudaMemcpyAsync(sk.as<double>() + static_cast<int64_t>(t) * s_q * ld, one.as<double>(),
+                                       static_cast<size_t>(s_q) * ld * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       ctx.stream()),
+                       "copy sketch");
+        }
+        for (int j0 = 0; j0 < cols; j0 += kMaxPanelCols) {
+            const int w = std::min(kMaxPanelCols, cols - j0);
+            run_panel(ctx, k, sk.as<double>() + static_cast<int64_t>(j0) * ld, ld, w, {{1.0, 0.0, 0.0}}, nullptr,
+                      nullptr, y.as<double>() + static_cast<int64_t>(j0) * ld, ld);
+        }
+        for (int t = 0; t < K; ++t) {
+            rank[t] = orthonormal_range(ctx, y.as<double>() + static_cast<int64_t>(t) * s_q * ld, s_q, ld, rows, q[t]);
+            if (rank[t] == 0) fail(kRankCollapse, "trial " + std::to_string(t) + ": hutchpp sketch A*S is numerically zero");
+            if (s_g >= n - rank[t]) {  // exact-complement branch for this trial: run it on its own
+                SketchCfg c = base;
+                c.seed = seeds[t];
+                out[t] = hutchpp(ctx, k, f, c);
+                rank[t] = -1;
+            }
+        }
+    }
+    // X0 = [Q_0 | W_0 | Q_1 | W_1 | ...],  W_t = G_t - Q_t (Q_tᵀ G_t)
+    std::vector<int64_t> off(K, 0);
+    int64_t total = 0;
+    for (int t = 0; t < K; ++t) {
+        off[t] = total;
+        if (rank[t] >= 0) total += rank[t] + s_g;
+    }
+    if (total == 0) return out;
+    DevBuf x0;
+    x0.alloc(static_cast<size_t>(total) * ld * sizeof(double));
+    for (int t = 0; t < K; ++t) {
+        if (rank[t] < 0) continue;
+        double* dst = x0.as<double>() + off[t] * ld;
+        if (rank[t] > 0)
+            cuda_check(cudaMemcpyAsync(dst, q[t].as<double>(), static_cast<size_t>(rank[t]) * ld * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, ctx.stream()),
+                       "copy Q");
+        if (s_g > 0) {
+            double* wdst = dst + static_cast<int64_t>(rank[t]) * ld;
+            DevBuf gp;
+            make_probes(ctx, k, gp, s_g, ld, nullptr, seeds[t], "hutchpp-probe", base.probe_kind);
+            if (rank[t] > 0) {
+                std::vector<double> c = gram_host(ctx, q[t].as<double>(), rank[t], ld, gp.as<double>(), s_g, ld, rows);
+                for (double& v : c) v = -v;
+                update(ctx, 1.0, gp.as<double>(), ld, q[t].as<double>(), rank[t], ld, c, s_g, rows, wdst, ld);
+            } else {
+                cuda_check(cudaMemcpyAsync(wdst, gp.as<double>(), static_cast<size_t>(s_g) * ld * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, ctx.stream()),
+                           "copy probes");
+                ctx.sync();
+            }
+        }
+    }
+    const std::vector<double> tr = panel_traces(ctx, k, f, x0.as<double>(), ld, static_cast<int>(total));
+    for (int t = 0; t < K; ++t) {
+        if (rank[t] < 0) continue;
+        TraceEst& e = out[t];
+        double low = 0.0, res = 0.0;
+        for (int j = 0; j < rank[t]; ++j) low += tr[off[t] + j];
+        for (int j = 0; j < s_g; ++j) res += tr[off[t] + rank[t] + j];
+        e.sketch_rank = rank[t];
+        e.low_rank_part = low;
+        e.residual_part = s_g > 0 ? res / s_g : 0.0;
+        e.queries_used = (s_q > 0 ? s_q + rank[t] * cost : 0) + s_g * cost;
+        e.value = e.low_rank_part + e.residual_part;
+    }
+    return out;
+}
+
+}  // namespace
+
+std::vector<EntropyEst> estimate_trials(Context& ctx, const KernelMatrix& k, const EstParams& p, int trials) {
+    // K trials of estimate() with seeds derive_key(p.seed, t) and the bounds resolved once, as
+    // measure_cell does them (proj/src/simulate.cpp:19-51), batched over shared passes.
+    if (trials < 1) fail(kInvalidArgument, "need at least one trial");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const auto t0 = std::chrono::steady_clock::now();
+    const Resolved r = resolve(ctx, k, p);
+    std::vector<uint64_t> seeds(trials);
+    for (int t = 0; t < trials; ++t) seeds[t] = derive_key(p.seed, static_cast<uint64_t>(t));
+    const SketchCfg base = sketch_cfg(p, r.s);
+    const std::vector<TraceEst> tr = hutchpp_batch(ctx, k, r.f, base, seeds);
+    const double per = seconds_since(t0) / trials;
+    std::vector<EntropyEst> out(trials);
+    for (int t = 0; t < trials; ++t) {
+        try {
+            out[t] = entropy_of(tr[t], r.alpha, r.method, r.s, r.m_used);
+        } catch (const Error& e) {
+            fail(e.code(), "trial " + std::to_string(t) + ": " + e.what());
+        }
+        out[t].has_bounds = r.has_bounds;
+        out[t].bounds_used = r.bounds;
+        out[t].elapsed = per;
+    }
+    return out;
+}
+
+MreCell measure_cell(Context& ctx, const KernelMatrix& k, double exact_entropy, const EstParams& p, int trials) {
+    // proj/src/simulate.cpp:19-72
+    if (trials < 1) fail(kInvalidArgument, "need at least one trial");
+    const std::vector<EntropyEst> est = estimate_trials(ctx, k, p, trials);
+    MreCell cell;
+    cell.alpha = p.alpha;
+    cell.s = p.s;
+    cell.m = p.m;
+    cell.method = p.method;
+    cell.trials = trials;
+    double sum = 0.0, tsum = 0.0;
+    std::vector<double> rel(trials);
+    for (int t = 0; t < trials; ++t) {
+        rel[t] = std::abs(est[t].entropy - exact_entropy) / std::abs(exact_entropy);
+        sum += rel[t];
+        tsum += est[t].elapsed;
+    }
+    cell.mre = sum / trials;
+    double var = 0.0;
+    for (double x : rel) var += (x - cell.mre) * (x - cell.mre);
+    cell.sd = trials > 1 ? std::sqrt(var / (trials - 1)) : 0.0;
+    cell.mean_elapsed = tsum / trials;
+    return cell;
 }
 
 EstParams with_seed(const EstParams& p, const char* term) {

@@ -231,6 +231,18 @@ struct EntropyEst {
 };
 EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p);
 
+// ---- batched trials (proj/src/simulate.cpp:19-72) ----
+// trials of estimate() with seeds derive_key(p.seed, t), bounds resolved once, probes of all
+// trials sharing the passes over A
+std::vector<EntropyEst> estimate_trials(Context& ctx, const KernelMatrix& k, const EstParams& p, int trials);
+struct MreCell {
+    double alpha = 0.0;
+    int s = 0, m = 0, method = kMethodExact;
+    double mre = 0.0, sd = 0.0, mean_elapsed = 0.0;
+    int trials = 0;
+};
+MreCell measure_cell(Context& ctx, const KernelMatrix& k, double exact_entropy, const EstParams& p, int trials);
+
 struct MutualInfo {
     double value = 0.0, vars_entropy = 0.0, target_entropy = 0.0, joint_entropy = 0.0;
 };

@@ -45,10 +45,13 @@ __device__ __forceinline__ void split_store(double v, __half* hi, __half* lo, in
     if (lo) lo[idx] = __double2half(v - static_cast<double>(__half2float(h)));
 }
 
+constexpr int kEpiCols = 8;  // columns per epilogue CTA (grid = row blocks x column groups)
+
 template <typename PT, typename ST, bool SPLIT, int ER>
 __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     constexpr int NW = ER / 32;
-    __shared__ double red[3][NW][kMaxPanelCols];
+    __shared__ double red[3][NW][kEpiCols];
+    const int jb0 = blockIdx.y * kEpiCols, jb1 = min(p.s, jb0 + kEpiCols);
     const int r = blockIdx.x;
     const int tid = threadIdx.x;
     const int warp = tid / 32, lane = tid % 32;
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     }
     const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
 
-    for (int j = 0; j < p.s; ++j) {
+    for (int j = jb0; j < jb1; ++j) {
         double y = 0.0;
         for (int64_t c = c_lo; c <= c_hi; ++c)
             y += static_cast<double>(p.partial[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
@@ -95,20 +98,20 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
         const double d3 = warp_sum(tn * tn);
         const float mx = warp_max(static_cast<float>(fabs(tn)));
         if (lane == 0) {
-            red[0][warp][j] = d1;
-            red[1][warp][j] = d2;
-            red[2][warp][j] = d3;
+            red[0][warp][j - jb0] = d1;
+            red[1][warp][j - jb0] = d2;
+            red[2][warp][j - jb0] = d3;
             atomicMax(p.cmax_new + j, __float_as_uint(mx));
         }
     }
     __syncthreads();
-    const int R = gridDim.x;
-    for (int t = tid; t < 3 * p.s; t += blockDim.x) {
-        const int q = t / p.s, j = t % p.s;
-        double v = red[q][0][j];
+    const int R = gridDim.x, w = jb1 - jb0;
+    for (int t = tid; t < 3 * w; t += blockDim.x) {
+        const int q = t / w, jj = t % w;
+        double v = red[q][0][jj];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) v += red[q][w][j];
-        p.stats[(static_cast<int64_t>(q) * R + r) * p.s + j] = v;
+        for (int ww = 1; ww < NW; ++ww) v += red[q][ww][jj];
+        p.stats[(static_cast<int64_t>(q) * R + r) * p.s + jb0 + jj] = v;
     }
 }
 
@@ -291,12 +294,13 @@ __global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64
 
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    const unsigned groups = static_cast<unsigned>((a.s + kEpiCols - 1) / kEpiCols);
     if (a.rows_per_block == 256) {
-        const int R = static_cast<int>((a.rows + 255) / 256);
-        epilogue_kernel<float, float, true, 256><<<R, 256, 0, stream>>>(a);
+        const unsigned R = static_cast<unsigned>((a.rows + 255) / 256);
+        epilogue_kernel<float, float, true, 256><<<dim3(R, groups), 256, 0, stream>>>(a);
     } else if (a.rows_per_block == 128) {
-        const int R = static_cast<int>((a.rows + 127) / 128);
-        epilogue_kernel<float, float, true, 128><<<R, 128, 0, stream>>>(a);
+        const unsigned R = static_cast<unsigned>((a.rows + 127) / 128);
+        epilogue_kernel<float, float, true, 128><<<dim3(R, groups), 128, 0, stream>>>(a);
     } else {
         return cudaErrorInvalidValue;
     }
@@ -305,8 +309,9 @@ cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t s
 
 cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols || a.rows_per_block != 128) return cudaErrorInvalidValue;
-    const int R = static_cast<int>((a.rows + 127) / 128);
-    epilogue_kernel<double, double, false, 128><<<R, 128, 0, stream>>>(a);
+    const unsigned R = static_cast<unsigned>((a.rows + 127) / 128);
+    const unsigned groups = static_cast<unsigned>((a.s + kEpiCols - 1) / kEpiCols);
+    epilogue_kernel<double, double, false, 128><<<dim3(R, groups), 128, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

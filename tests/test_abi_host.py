@@ -121,3 +121,10 @@ def test_cpp_mirror_compiles_links_and_runs(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_mixture_samples_match_oracle(R, orc):
+    """mixture_samples (proj/src/simulate.cpp:9-17): one stream, bitwise."""
+    x = R.mixture_samples(50, 3, 11, 1.5)
+    y = orc.mixture_samples(50, 3, 11, 1.5)
+    assert np.array_equal(x, y)
