@@ -71,6 +71,11 @@ def lib():
         for name in ("oracle_mix64", "oracle_derive_key", "oracle_hash_name"):
             getattr(h, name).restype = C.c_uint64
         h.oracle_mix64.argtypes = [C.c_uint64]
+        _PD = C.POINTER(C.c_double)
+        for name in ("oracle_rank_features", "oracle_select_features"):
+            getattr(h, name).argtypes = [_PD, C.c_int64, C.c_int64, C.POINTER(C.c_char_p), C.c_int64,
+                                         C.POINTER(C.c_char_p), C.c_double, C.c_void_p, C.c_int, C.POINTER(C.c_int),
+                                         _PD]
         h.oracle_derive_key.argtypes = [C.c_uint64, C.c_uint64]
         h.oracle_hash_name.argtypes = [C.c_char_p]
         h.oracle_taylor_tail_constant.restype = C.c_double
@@ -313,6 +318,45 @@ def estimate(a, alpha=2.0, method="auto", s=0, m=0, epsilon=1e-2, delta=1e-2, se
     o = COut()
     _chk(lib().oracle_estimate(_p(a), a.shape[0], C.byref(p), C.byref(o)))
     return _out(o)
+
+
+def _params(alpha=2.0, method="auto", s=0, m=0, epsilon=1e-2, delta=1e-2, seed=0, bounds=None,
+            probe_kind="gaussian", s_q=None, s_g=None, power_max_iters=100, power_tol=1e-6):
+    return CParams(alpha, METHODS[method], s, m, epsilon, delta, _u64(seed), power_max_iters, power_tol, 0, 1e-12,
+                   1 if bounds is not None else 0, bounds[0] if bounds else 0.0, bounds[1] if bounds else 1.0,
+                   PROBES[probe_kind], -1 if s_q is None else s_q, -1 if s_g is None else s_g)
+
+
+def _cstrs(items):
+    if items is None:
+        return None
+    arr = (C.c_char_p * len(items))()
+    arr[:] = [str(v).encode() for v in items]
+    return arr
+
+
+def rank_features(x, labels, sigma, k, names=None, **params):
+    """rank_features (features.cpp:95-123) -> (columns, scores) of the top k."""
+    x = _f(x)
+    cols = (C.c_int * k)()
+    scores = np.empty(k)
+    prm = _params(**params)
+    _chk(lib().oracle_rank_features(_p(x), x.shape[0], x.shape[1], _cstrs(labels), len(labels or []), _cstrs(names),
+                                    float(sigma),
+                                    C.cast(C.byref(prm), C.c_void_p), k, cols, _p(scores)))
+    return list(cols), scores
+
+
+def select_features(x, labels, sigma, k, names=None, **params):
+    """select_features (features.cpp:125-162) -> (columns in pick order, objective after each pick)."""
+    x = _f(x)
+    cols = (C.c_int * k)()
+    obj = np.empty(k)
+    prm = _params(**params)
+    _chk(lib().oracle_select_features(_p(x), x.shape[0], x.shape[1], _cstrs(labels), len(labels or []),
+                                      _cstrs(names), float(sigma),
+                                      C.cast(C.byref(prm), C.c_void_p), k, cols, _p(obj)))
+    return list(cols), obj
 
 
 def eigvals(a):

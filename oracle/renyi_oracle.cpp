@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <numbers>
 #include <stdexcept>
 #include <string>
@@ -698,9 +699,16 @@ double entropy_from_trace(double trace, double alpha) {  // entropy.cpp:62-69
     return std::log(trace) / (1.0 - alpha);
 }
 
-// symmetric eigenvalues: Householder tridiagonalisation + implicit QL (textbook tred2/tqli)
+// symmetric eigenvalues: Householder tridiagonalisation + implicit QL (textbook tred2/tqli), with
+// Eigen's SelfAdjointEigenSolver conventions: the matrix is scaled by its largest |entry| and an
+// off-diagonal entry is deflated when (e/eps)^2 <= |d_i| + |d_i+1| (or |e| < DBL_MIN), which also
+// converges on the large null spaces of low-rank kernels (e.g. a feature with 3 distinct values)
 Vec sym_eigvals(Mat a) {
     const int64_t n = a.r;
+    double amax = 0.0;
+    for (double v : a.d) amax = std::max(amax, std::abs(v));
+    if (amax == 0.0) return Vec(n, 0.0);
+    for (double& v : a.d) v /= amax;
     Vec d(n), e(n);
     for (int64_t i = n - 1; i > 0; --i) {
         const int64_t l = i - 1;
@@ -748,7 +756,8 @@ Vec sym_eigvals(Mat a) {
         do {
             for (m = l; m < n - 1; ++m) {
                 const double dd = std::abs(d[m]) + std::abs(d[m + 1]);
-                if (std::abs(e[m]) <= std::numeric_limits<double>::epsilon() * dd) break;
+                const double se = e[m] / std::numeric_limits<double>::epsilon();
+                if (std::abs(e[m]) < std::numeric_limits<double>::min() || se * se <= dd) break;
             }
             if (m != l) {
                 if (iter++ == 200) fail(kInvalidArgument, "eigenvalue iteration did not converge");
@@ -779,6 +788,7 @@ Vec sym_eigvals(Mat a) {
             }
         } while (m != l);
     }
+    for (double& v : d) v *= amax;
     std::sort(d.begin(), d.end());
     return d;
 }
@@ -961,6 +971,127 @@ Mat mixture_samples(int n, int d, uint64_t seed, double center) {
     return x;
 }
 
+// ---------------------------------------------------------------- features.cpp
+// one_hot_labels (features.cpp:83-93): distinct labels in sorted (std::map) order
+Mat one_hot_labels(const std::vector<std::string>& labels) {
+    std::map<std::string, int> classes;
+    for (const auto& l : labels) classes.emplace(l, 0);
+    int idx = 0;
+    for (auto& kv : classes) kv.second = idx++;
+    Mat e(static_cast<int64_t>(labels.size()), static_cast<int64_t>(classes.size()));
+    for (size_t i = 0; i < labels.size(); ++i) e(static_cast<int64_t>(i), classes[labels[i]]) = 1.0;
+    return e;
+}
+
+struct FeatureData {
+    Mat x;  // n x d
+    std::vector<std::string> labels, names;
+    std::string name(int j) const {
+        return j < static_cast<int>(names.size()) ? names[j] : "feature_" + std::to_string(j);
+    }
+};
+
+void validate_features(const FeatureData& data, int k) {  // features.cpp:18-26
+    if (data.labels.empty()) fail(kInvalidArgument, "dataset has no label column");
+    if (static_cast<int64_t>(data.labels.size()) != data.x.r)
+        fail(kSizeMismatch, "label count does not match sample count");
+    if (k < 1 || k > data.x.c)
+        fail(kInvalidArgument,
+             "k must be in [1, d]; got k=" + std::to_string(k) + " with d=" + std::to_string(data.x.c));
+}
+
+Mat feature_kernel(const FeatureData& data, double sigma, int j) {  // features.cpp:33-39
+    Mat col(data.x.r, 1);
+    for (int64_t i = 0; i < data.x.r; ++i) col(i, 0) = data.x(i, j);
+    try {
+        return build_kernel(col, sigma);
+    } catch (const Error& e) {
+        fail(e.code, "feature '" + data.name(j) + "': " + e.what());
+    }
+}
+
+// StepScorer (features.cpp:44-75): the label entropy once per step, then per candidate
+// S(F) + S(Y) - S(F∘Y) with the mutual_information seed schedule
+struct StepScorer {
+    const Mat* label;
+    Params step;
+    double label_entropy = 0.0;
+    StepScorer(const Mat& label_kernel, const Params& params, uint64_t step_seed) : label(&label_kernel), step(params) {
+        step.seed = step_seed;
+        Params p = step;
+        p.seed = derive_key(step_seed, hash_name("term:target"));
+        label_entropy = estimate(label_kernel, p).entropy;
+    }
+    double score(const Mat& feats, const std::string& name) const {
+        try {
+            Params pv = step;
+            pv.seed = derive_key(step.seed, hash_name("term:vars"));
+            const double s_f = estimate(feats, pv).entropy;
+            Params pj = step;
+            pj.seed = derive_key(step.seed, hash_name("term:joint"));
+            const Mat joint = hadamard_joint({&feats, label});
+            const double s_fy = estimate(joint, pj).entropy;
+            return s_f + label_entropy - s_fy;
+        } catch (const Error& e) {
+            fail(e.code, "feature '" + name + "': " + e.what());
+        }
+    }
+};
+
+// rank_features (features.cpp:95-123): top-k by score, ties by ascending column
+void rank_features(const FeatureData& data, double sigma, const Params& params, int k, std::vector<int>& cols,
+                   std::vector<double>& scores_out) {
+    validate_features(data, k);
+    const int d = static_cast<int>(data.x.c);
+    const Mat label_kernel = build_kernel(one_hot_labels(data.labels), sigma);
+    const StepScorer scorer(label_kernel, params, derive_key(params.seed, 0));
+    std::vector<double> scores(d);
+    for (int j = 0; j < d; ++j) scores[j] = scorer.score(feature_kernel(data, sigma, j), data.name(j));
+    std::vector<int> order(d);
+    for (int j = 0; j < d; ++j) order[j] = j;
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        if (scores[a] != scores[b]) return scores[a] > scores[b];
+        return a < b;
+    });
+    cols.assign(order.begin(), order.begin() + k);
+    scores_out.clear();
+    for (int r = 0; r < k; ++r) scores_out.push_back(scores[order[r]]);
+}
+
+// select_features (features.cpp:125-162): greedy forward selection over Hadamard joints
+void select_features(const FeatureData& data, double sigma, const Params& params, int k, std::vector<int>& cols,
+                     std::vector<double>& objective) {
+    validate_features(data, k);
+    const int d = static_cast<int>(data.x.c);
+    const Mat label_kernel = build_kernel(one_hot_labels(data.labels), sigma);
+    std::vector<Mat> kernels;
+    for (int j = 0; j < d; ++j) kernels.push_back(feature_kernel(data, sigma, j));
+    std::vector<bool> taken(d, false);
+    Mat selected;
+    cols.clear();
+    objective.clear();
+    for (int step = 0; step < k; ++step) {
+        const StepScorer scorer(label_kernel, params, derive_key(params.seed, static_cast<uint64_t>(step)));
+        int best = -1;
+        double best_score = 0.0;
+        Mat best_joint;
+        for (int j = 0; j < d; ++j) {
+            if (taken[j]) continue;
+            Mat cand = step == 0 ? kernels[j] : hadamard_joint({&selected, &kernels[j]});
+            const double sc = scorer.score(cand, data.name(j));
+            if (best < 0 || sc > best_score) {
+                best = j;
+                best_score = sc;
+                best_joint = std::move(cand);
+            }
+        }
+        taken[best] = true;
+        selected = std::move(best_joint);
+        cols.push_back(best);
+        objective.push_back(best_score);
+    }
+}
+
 }  // namespace orc
 
 // =====================================================================================
@@ -1088,6 +1219,40 @@ int oracle_stream_gaussian(uint64_t key, int64_t count, double* out) {
         for (int64_t i = 0; i < count; ++i) out[i] = s.next_gaussian();
     });
 }
+static orc::FeatureData feature_data(const double* x, int64_t n, int64_t d, const char* const* labels,
+                                     int64_t n_labels, const char* const* names) {
+    orc::FeatureData data;
+    data.x = wrap(x, n, d);
+    if (labels)
+        for (int64_t i = 0; i < n_labels; ++i) data.labels.push_back(labels[i]);
+    if (names)
+        for (int64_t j = 0; j < d; ++j) data.names.push_back(names[j]);
+    return data;
+}
+
+int oracle_rank_features(const double* x, int64_t n, int64_t d, const char* const* labels, int64_t n_labels,
+                         const char* const* names, double sigma, const CParams* p, int k, int* cols, double* scores) {
+    return guard([&] {
+        std::vector<int> c;
+        std::vector<double> sc;
+        orc::rank_features(feature_data(x, n, d, labels, n_labels, names), sigma, to_params(p), k, c, sc);
+        std::copy(c.begin(), c.end(), cols);
+        std::copy(sc.begin(), sc.end(), scores);
+    });
+}
+
+int oracle_select_features(const double* x, int64_t n, int64_t d, const char* const* labels, int64_t n_labels,
+                           const char* const* names, double sigma, const CParams* p, int k, int* cols,
+                           double* objective) {
+    return guard([&] {
+        std::vector<int> c;
+        std::vector<double> ob;
+        orc::select_features(feature_data(x, n, d, labels, n_labels, names), sigma, to_params(p), k, c, ob);
+        std::copy(c.begin(), c.end(), cols);
+        std::copy(ob.begin(), ob.end(), objective);
+    });
+}
+
 int oracle_mixture_samples(int n, int d, uint64_t seed, double center, double* out) {
     return guard([&] { unwrap(orc::mixture_samples(n, d, seed, center), out); });
 }
