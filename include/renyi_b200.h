@@ -230,6 +230,17 @@ int renyi_estimate_trials(renyi_ctx* ctx, const renyi_kernel* k, const renyi_est
 /* measure_cell — proj/src/simulate.cpp:19-72 (MRE/SD over K trials against a known exact entropy) */
 int renyi_measure_cell(renyi_ctx* ctx, const renyi_kernel* k, double exact_entropy,
                        const renyi_estimator_params* p, int trials, renyi_mre_cell* out);
+/* rank_features / select_features — proj/src/features.cpp:95-162 (Gaussian kernel of width sigma
+ * for every feature and for the one-hot labels; names may be NULL -> "feature_<j>").
+ * rank: columns[k], scores[k], elapsed[d]. select: columns[k], objective[k], elapsed[k]. */
+int renyi_rank_features(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                        const char* const* labels, int64_t n_labels, const char* const* names, double sigma,
+                        const renyi_estimator_params* p, int precision, int k, int* columns, double* scores,
+                        double* elapsed);
+int renyi_select_features(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                          const char* const* labels, int64_t n_labels, const char* const* names, double sigma,
+                          const renyi_estimator_params* p, int precision, int k, int* columns, double* objective,
+                          double* elapsed);
 /* mixture_samples — proj/src/simulate.cpp:9-17 (host; out column-major n x d) */
 int renyi_mixture_samples(int n, int d, uint64_t seed, double center, double* out);
 /* entropy_int / entropy_taylor / entropy_chebyshev — proj/src/entropy.cpp:111-135 */

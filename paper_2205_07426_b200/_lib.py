@@ -200,6 +200,14 @@ SIGNATURES = {
     "renyi_estimate_trials": (C.c_int, [_P, _P, C.POINTER(EstimatorParamsC), C.c_int, C.POINTER(EntropyEstimateC)]),
     "renyi_measure_cell": (C.c_int, [_P, _P, C.c_double, C.POINTER(EstimatorParamsC), C.c_int, C.POINTER(MreCellC)]),
     "renyi_mixture_samples": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_double, C.POINTER(C.c_double)]),
+    "renyi_rank_features": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_int64,
+                                      C.POINTER(C.c_char_p), C.c_int64, C.POINTER(C.c_char_p), C.c_double,
+                                      C.POINTER(EstimatorParamsC), C.c_int, C.c_int, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "renyi_select_features": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_char_p), C.c_int64, C.POINTER(C.c_char_p), C.c_double,
+                                        C.POINTER(EstimatorParamsC), C.c_int, C.c_int, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "renyi_entropy_int": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_uint64, C.POINTER(EntropyEstimateC)]),
     "renyi_entropy_taylor": (
         C.c_int,

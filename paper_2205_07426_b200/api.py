@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import threading
+import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -656,6 +657,129 @@ def run_simulation(spec: SimulationSpec, ctx: Optional["Context"] = None) -> lis
                 cell.oracle_elapsed = oracle.elapsed
                 cells.append(cell)
     return cells
+
+
+# ---------------------------------------------------------------- feature tools (features.hpp)
+@dataclass
+class RankingResult:
+    names: list
+    columns: list
+    scores: list
+    elapsed: list
+
+
+@dataclass
+class SelectionResult:
+    names: list
+    columns: list
+    objective: list
+    elapsed: list
+
+
+def _cstrs(items):
+    arr = (C.c_char_p * max(len(items), 1))()
+    arr[:len(items)] = [str(v).encode() for v in items]
+    return arr
+
+
+def _feature_names(d, names):
+    return [names[j] if names is not None and j < len(names) else f"feature_{j}" for j in range(d)]
+
+
+def one_hot_labels(labels) -> np.ndarray:
+    """one_hot_labels (proj/src/features.cpp:83-93): distinct labels in sorted order."""
+    classes = {c: i for i, c in enumerate(sorted(set(labels)))}
+    out = np.zeros((len(labels), len(classes)))
+    for i, l in enumerate(labels):
+        out[i, classes[l]] = 1.0
+    return out
+
+
+def _exact_score_fn(ctx, label_k, params, step_seed, precision):
+    """The reference's scorer with method=exact (entropy_exact on the device matrices)."""
+    h_y = entropy_exact(label_k, params.alpha).entropy
+
+    def score(feats):
+        h_f = entropy_exact(feats, params.alpha).entropy
+        return h_f + h_y - entropy_exact(hadamard_joint([feats, label_k]), params.alpha).entropy
+
+    return score
+
+
+def rank_features(x, labels, spec: GaussianKernel, params: EstimatorParams, k: int, names=None,
+                  precision="fp64", ctx: Optional[Context] = None) -> RankingResult:
+    """rank_features (proj/src/features.cpp:95-123): top k features by I_alpha(X_j; Y), ties by column."""
+    ctx = ctx or default_context()
+    xa = _colmajor(x)
+    n, d = xa.shape
+    fnames = _feature_names(d, names)
+    if params.method == "exact":  # eigendecomposition check path (entropy_exact on the device)
+        _validate_features(n, d, labels, k)
+        score = _exact_score_fn(ctx, build_kernel(one_hot_labels(labels), spec, precision, ctx), params, 0, precision)
+        scores, elapsed = [], []
+        for j in range(d):
+            t0 = time.time()
+            scores.append(score(build_kernel(xa[:, j:j + 1], spec, precision, ctx)))
+            elapsed.append(time.time() - t0)
+        order = sorted(range(d), key=lambda j: (-scores[j], j))[:k]
+        return RankingResult([fnames[j] for j in order], order, [scores[j] for j in order], elapsed)
+    cols = (C.c_int * k)()
+    scores = np.empty(k)
+    elapsed = np.empty(d)
+    check(L.lib().renyi_rank_features(ctx.handle, _dptr(xa), n, d, n, _cstrs(list(labels)), len(labels),
+                                      _cstrs(fnames), spec.sigma, C.byref(params._c()), PRECISIONS[precision], k,
+                                      cols, _dptr(scores), _dptr(elapsed)))
+    order = list(cols)
+    return RankingResult([fnames[j] for j in order], order, list(scores), list(elapsed))
+
+
+def select_features(x, labels, spec: GaussianKernel, params: EstimatorParams, k: int, names=None,
+                    precision="fp64", ctx: Optional[Context] = None) -> SelectionResult:
+    """select_features (proj/src/features.cpp:125-162): greedy forward selection over Hadamard joints."""
+    ctx = ctx or default_context()
+    xa = _colmajor(x)
+    n, d = xa.shape
+    fnames = _feature_names(d, names)
+    if params.method == "exact":
+        _validate_features(n, d, labels, k)
+        label_k = build_kernel(one_hot_labels(labels), spec, precision, ctx)
+        kernels = [build_kernel(xa[:, j:j + 1], spec, precision, ctx) for j in range(d)]
+        score = _exact_score_fn(ctx, label_k, params, 0, precision)
+        taken, selected, res = set(), None, SelectionResult([], [], [], [])
+        for step in range(k):
+            t0 = time.time()
+            best, best_score, best_joint = -1, 0.0, None
+            for j in range(d):
+                if j in taken:
+                    continue
+                cand = kernels[j] if step == 0 else hadamard_joint([selected, kernels[j]])
+                sc = score(cand)
+                if best < 0 or sc > best_score:
+                    best, best_score, best_joint = j, sc, cand
+            taken.add(best)
+            selected = best_joint
+            res.names.append(fnames[best])
+            res.columns.append(best)
+            res.objective.append(best_score)
+            res.elapsed.append(time.time() - t0)
+        return res
+    cols = (C.c_int * k)()
+    obj = np.empty(k)
+    elapsed = np.empty(k)
+    check(L.lib().renyi_select_features(ctx.handle, _dptr(xa), n, d, n, _cstrs(list(labels)), len(labels),
+                                        _cstrs(fnames), spec.sigma, C.byref(params._c()), PRECISIONS[precision], k,
+                                        cols, _dptr(obj), _dptr(elapsed)))
+    order = list(cols)
+    return SelectionResult([fnames[j] for j in order], order, list(obj), list(elapsed))
+
+
+def _validate_features(n, d, labels, k):  # features.cpp:18-26
+    if not labels:
+        raise RenyiError(1, "dataset has no label column")
+    if len(labels) != n:
+        raise RenyiError(4, "label count does not match sample count")
+    if k < 1 or k > d:
+        raise RenyiError(1, f"k must be in [1, d]; got k={k} with d={d}")
 
 
 def entropy_int(a: NormalizedKernel, alpha: int, s: int, seed: int) -> EntropyEstimate:

@@ -621,6 +621,53 @@ int renyi_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int
     });
 }
 
+namespace {
+rb::FeatureData feature_data(const double* x, int64_t n, int64_t d, int64_t ldx, const char* const* labels,
+                             int64_t n_labels, const char* const* names) {
+    need(x, "x");
+    if (n_labels > 0) need(labels, "labels");
+    rb::FeatureData data;
+    data.x = x, data.n = n, data.d = d, data.ldx = ldx;
+    for (int64_t i = 0; i < n_labels; ++i) {
+        need(labels[i], "label");
+        data.labels.emplace_back(labels[i]);
+    }
+    if (names)
+        for (int64_t j = 0; j < d; ++j) data.names.emplace_back(names[j] ? names[j] : "");
+    return data;
+}
+}  // namespace
+
+int renyi_rank_features(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                        const char* const* labels, int64_t n_labels, const char* const* names, double sigma,
+                        const renyi_estimator_params* p, int precision, int k, int* columns, double* scores,
+                        double* elapsed) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(columns, "columns"), need(scores, "scores");
+        check_precision(precision);
+        const rb::FeatureRanking r = rb::rank_features(
+            ctx->ctx, feature_data(x, n, d, ldx, labels, n_labels, names), sigma, to_params(p), precision, k);
+        std::copy(r.columns.begin(), r.columns.end(), columns);
+        std::copy(r.scores.begin(), r.scores.end(), scores);
+        if (elapsed) std::copy(r.elapsed.begin(), r.elapsed.end(), elapsed);
+    });
+}
+
+int renyi_select_features(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                          const char* const* labels, int64_t n_labels, const char* const* names, double sigma,
+                          const renyi_estimator_params* p, int precision, int k, int* columns, double* objective,
+                          double* elapsed) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(columns, "columns"), need(objective, "objective");
+        check_precision(precision);
+        const rb::FeatureSelection r = rb::select_features(
+            ctx->ctx, feature_data(x, n, d, ldx, labels, n_labels, names), sigma, to_params(p), precision, k);
+        std::copy(r.columns.begin(), r.columns.end(), columns);
+        std::copy(r.objective.begin(), r.objective.end(), objective);
+        if (elapsed) std::copy(r.elapsed.begin(), r.elapsed.end(), elapsed);
+    });
+}
+
 int renyi_mixture_samples(int n, int d, uint64_t seed, double center, double* out) {
     // proj/src/simulate.cpp:9-17: one stream, row by row; out column-major n x d
     return guarded([&] {

@@ -960,43 +960,82 @@ void update(Context& ctx, double beta, const double* g, int64_t ldg, const doubl
     ctx.sync();
 }
 
-// Orthonormal basis of range(Y) (Y device [p][ld], n rows) by CholeskyQR2 with an
-// eigen-based first step (rank-revealing); returns the rank and writes Q [rank][ld].
+// Orthonormal basis of range(Y) (Y device [p][ld], n rows) by CholeskyQR2 with an eigen-based,
+// rank-revealing first step, plus one residual pass; returns the rank and writes Q [rank][ld].
 // Replaces Eigen::ColPivHouseholderQR + setThreshold(1e-12) (proj/src/hutchpp.cpp:91-108):
-// tr(Q^T f Q) and I - QQ^T are basis-invariant, so only the kept subspace matters.
+// tr(Q^T f Q) and I - QQ^T are basis-invariant, so only the kept subspace matters. The Gram's
+// eigenvalues resolve singular values only down to ~1e-7 of the largest, so the directions
+// between 1e-12 and 1e-7 (fast-decaying spectra, e.g. 1-D feature kernels) are recovered from
+// the residual Y - Q Q^T Y, whose own Gram resolves them; the kept set is then
+// { sigma_i > 1e-12 sigma_0 }, the reference's rank rule stated on singular values.
 int orthonormal_range(Context& ctx, const double* y, int p, int64_t ld, int64_t n, DevBuf& q_out) {
     std::vector<double> g = gram_host(ctx, y, p, ld, y, p, ld, n);
     std::vector<double> w, v;
     sym_eig_desc(p, g, w, v);
     if (!(w.size() > 0 && w[0] > 0.0)) return 0;
-    const double tau = 1e-13;
+    const double w0 = w[0];
     int k = 0;
-    while (k < p && w[k] > tau * w[0]) ++k;
+    while (k < p && w[k] > 1e-13 * w0) ++k;
     if (k == 0) return 0;
-    std::vector<double> m1(static_cast<size_t>(p) * k);
-    for (int c = 0; c < k; ++c) {
-        const double s = 1.0 / std::sqrt(w[c]);
-        for (int r = 0; r < p; ++r) m1[r + static_cast<size_t>(c) * p] = v[r + static_cast<size_t>(c) * p] * s;
-    }
-    DevBuf q1;
-    q1.alloc(static_cast<size_t>(k) * ld * sizeof(double));
-    update(ctx, 0.0, nullptr, ld, y, p, ld, m1, k, n, q1.as<double>(), ld);
-    // second (Cholesky) pass for orthogonality to working precision
-    std::vector<double> g2 = gram_host(ctx, q1.as<double>(), k, ld, q1.as<double>(), k, ld, n);
-    std::vector<double> r2;
-    q_out.ensure(static_cast<size_t>(k) * ld * sizeof(double));
-    if (cholesky_upper(k, g2, r2)) {
-        update(ctx, 0.0, nullptr, ld, q1.as<double>(), k, ld, upper_inverse(k, r2), k, n, q_out.as<double>(), ld);
-    } else {
+    // orthonormalise X·M with CholeskyQR (eigen fallback), X [cols][ld]
+    auto chol_qr = [&](const double* x, int cols, double* out) {
+        std::vector<double> g2 = gram_host(ctx, x, cols, ld, x, cols, ld, n);
+        std::vector<double> r2;
+        if (cholesky_upper(cols, g2, r2)) {
+            update(ctx, 0.0, nullptr, ld, x, cols, ld, upper_inverse(cols, r2), cols, n, out, ld);
+        } else {
+            std::vector<double> w2, v2;
+            sym_eig_desc(cols, g2, w2, v2);
+            std::vector<double> m2(static_cast<size_t>(cols) * cols);
+            for (int c = 0; c < cols; ++c)
+                for (int r = 0; r < cols; ++r)
+                    m2[r + static_cast<size_t>(c) * cols] = v2[r + static_cast<size_t>(c) * cols] / std::sqrt(w2[c]);
+            update(ctx, 0.0, nullptr, ld, x, cols, ld, m2, cols, n, out, ld);
+        }
+    };
+    auto scaled_vectors = [&](const std::vector<double>& ww, const std::vector<double>& vv, int cols) {
+        std::vector<double> m(static_cast<size_t>(p) * cols);
+        for (int c = 0; c < cols; ++c) {
+            const double sc = 1.0 / std::sqrt(ww[c]);
+            for (int r = 0; r < p; ++r) m[r + static_cast<size_t>(c) * p] = vv[r + static_cast<size_t>(c) * p] * sc;
+        }
+        return m;
+    };
+    DevBuf q1, qa;
+    q1.alloc(static_cast<size_t>(p) * ld * sizeof(double));
+    qa.alloc(static_cast<size_t>(p) * ld * sizeof(double));
+    update(ctx, 0.0, nullptr, ld, y, p, ld, scaled_vectors(w, v, k), k, n, q1.as<double>(), ld);
+    chol_qr(q1.as<double>(), k, qa.as<double>());  // second pass: orthogonal to working precision
+    int rank = k;
+    if (k < p) {
+        // residual pass: Y2 = Y - Q (Q^T Y); keep sigma(Y2) > 1e-12 sigma_0(Y)
+        std::vector<double> c = gram_host(ctx, qa.as<double>(), k, ld, y, p, ld, n);
+        for (double& x : c) x = -x;
+        DevBuf y2;
+        y2.alloc(static_cast<size_t>(p) * ld * sizeof(double));
+        update(ctx, 1.0, y, ld, qa.as<double>(), k, ld, c, p, n, y2.as<double>(), ld);
+        std::vector<double> g2 = gram_host(ctx, y2.as<double>(), p, ld, y2.as<double>(), p, ld, n);
         std::vector<double> w2, v2;
-        sym_eig_desc(k, g2, w2, v2);
-        std::vector<double> m2(static_cast<size_t>(k) * k);
-        for (int c = 0; c < k; ++c)
-            for (int r = 0; r < k; ++r)
-                m2[r + static_cast<size_t>(c) * k] = v2[r + static_cast<size_t>(c) * k] / std::sqrt(w2[c]);
-        update(ctx, 0.0, nullptr, ld, q1.as<double>(), k, ld, m2, k, n, q_out.as<double>(), ld);
+        sym_eig_desc(p, g2, w2, v2);
+        int k2 = 0;
+        while (k2 < p - k && w2[k2] > 1e-24 * w0) ++k2;
+        if (k2 > 0) {
+            double* dst = qa.as<double>() + static_cast<int64_t>(k) * ld;
+            update(ctx, 0.0, nullptr, ld, y2.as<double>(), p, ld, scaled_vectors(w2, v2, k2), k2, n, q1.as<double>(),
+                   ld);
+            // re-orthogonalise against the first block, then CholeskyQR
+            std::vector<double> c2 = gram_host(ctx, qa.as<double>(), k, ld, q1.as<double>(), k2, ld, n);
+            for (double& x : c2) x = -x;
+            update(ctx, 1.0, q1.as<double>(), ld, qa.as<double>(), k, ld, c2, k2, n, y2.as<double>(), ld);
+            chol_qr(y2.as<double>(), k2, dst);
+            rank += k2;
+        }
     }
-    return k;
+    q_out.ensure(static_cast<size_t>(rank) * ld * sizeof(double));
+    cuda_check(cudaMemcpyAsync(q_out.as<double>(), qa.as<double>(), static_cast<size_t>(rank) * ld * sizeof(double),
+                               cudaMemcpyDeviceToDevice, ctx.stream()),
+               "copy Q");
+    return rank;
 }
 
 double exact_trace(Context& ctx, const KernelMatrix& k, const MatFun& f) {
@@ -1446,6 +1485,162 @@ MutualInfo mutual_information_samples_dev(Context& ctx, const double* x, int64_t
     }
     mi.value = mi.vars_entropy + mi.target_entropy - mi.joint_entropy;
     return mi;
+}
+
+// ---------------------------------------------------------------- feature tools
+// proj/src/features.cpp: every score is S(F) + S(Y) - S(F∘Y) with the mutual_information seed
+// schedule; kernels stay resident on the device (select keeps all d feature kernels).
+std::string FeatureData::name(int j) const {
+    return j < static_cast<int>(names.size()) ? names[j] : "feature_" + std::to_string(j);
+}
+
+namespace {
+
+void validate_features(const FeatureData& data, int k) {  // features.cpp:18-26
+    if (data.labels.empty()) fail(kInvalidArgument, "dataset has no label column");
+    if (static_cast<int64_t>(data.labels.size()) != data.n) fail(kSizeMismatch, "label count does not match sample count");
+    if (k < 1 || k > data.d)
+        fail(kInvalidArgument, "k must be in [1, d]; got k=" + std::to_string(k) + " with d=" + std::to_string(data.d));
+    if (data.ldx < data.n) fail(kInvalidArgument, "leading dimension smaller than the sample count");
+}
+
+// one_hot_labels (features.cpp:83-93): distinct labels in sorted order, column-major n x C
+std::vector<double> one_hot(const std::vector<std::string>& labels, int* classes_out) {
+    std::map<std::string, int> classes;
+    for (const auto& l : labels) classes.emplace(l, 0);
+    int idx = 0;
+    for (auto& kv : classes) kv.second = idx++;
+    const size_t n = labels.size();
+    std::vector<double> e(n * classes.size(), 0.0);
+    for (size_t i = 0; i < n; ++i) e[i + static_cast<size_t>(classes[labels[i]]) * n] = 1.0;
+    *classes_out = idx;
+    return e;
+}
+
+KernelPtr label_kernel(Context& ctx, const FeatureData& data, double sigma, int prec) {
+    int c = 0;
+    const std::vector<double> e = one_hot(data.labels, &c);
+    return build_gaussian(ctx, e.data(), data.n, c, data.n, sigma, prec);
+}
+
+KernelPtr feature_kernel(Context& ctx, const FeatureData& data, const double* d_x, double sigma, int prec, int j) {
+    try {  // features.cpp:33-39
+        return build_gaussian_dev(ctx, d_x + static_cast<int64_t>(j) * data.n, data.n, 1, data.n, sigma, prec);
+    } catch (const Error& e) {
+        fail(e.code(), "feature '" + data.name(j) + "': " + e.what());
+    }
+}
+
+struct StepScorer {  // features.cpp:44-75
+    Context& ctx;
+    const KernelMatrix& label;
+    EstParams step;
+    double label_entropy = 0.0;
+    StepScorer(Context& c, const KernelMatrix& l, const EstParams& p, uint64_t step_seed) : ctx(c), label(l), step(p) {
+        step.seed = step_seed;
+        EstParams q = step;
+        q.seed = derive_key(step_seed, hash_name("term:target"));
+        label_entropy = estimate(ctx, label, q).entropy;
+    }
+    double score(const KernelMatrix& feats, const std::string& name) const {
+        try {
+            EstParams pv = step;
+            pv.seed = derive_key(step.seed, hash_name("term:vars"));
+            const double s_f = estimate(ctx, feats, pv).entropy;
+            EstParams pj = step;
+            pj.seed = derive_key(step.seed, hash_name("term:joint"));
+            KernelPtr joint = hadamard_joint(ctx, feats, label);
+            const double s_fy = estimate(ctx, *joint, pj).entropy;
+            return s_f + label_entropy - s_fy;
+        } catch (const Error& e) {
+            fail(e.code(), "feature '" + name + "': " + e.what());
+        }
+    }
+};
+
+DevBuf upload_features(Context& ctx, const FeatureData& data) {
+    DevBuf xs;
+    xs.alloc(static_cast<size_t>(data.n) * data.d * sizeof(double));
+    h2d_2d(ctx, xs.as<double>(), data.n * sizeof(double), data.x, data.ldx * sizeof(double), data.n * sizeof(double),
+           data.d);
+    return xs;
+}
+
+}  // namespace
+
+FeatureRanking rank_features(Context& ctx, const FeatureData& data, double sigma, const EstParams& p, int prec, int k) {
+    // features.cpp:95-123
+    validate_features(data, k);
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int d = static_cast<int>(data.d);
+    KernelPtr label = label_kernel(ctx, data, sigma, prec);
+    DevBuf xs = upload_features(ctx, data);
+    const StepScorer scorer(ctx, *label, p, derive_key(p.seed, 0));
+    std::vector<double> scores(d), elapsed(d);
+    for (int j = 0; j < d; ++j) {
+        const auto t0 = std::chrono::steady_clock::now();
+        KernelPtr f = feature_kernel(ctx, data, xs.as<double>(), sigma, prec, j);
+        scores[j] = scorer.score(*f, data.name(j));
+        elapsed[j] = seconds_since(t0);
+    }
+    std::vector<int> order(d);
+    for (int j = 0; j < d; ++j) order[j] = j;
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        if (scores[a] != scores[b]) return scores[a] > scores[b];
+        return a < b;
+    });
+    FeatureRanking res;
+    res.elapsed = std::move(elapsed);
+    for (int r = 0; r < k; ++r) {
+        res.columns.push_back(order[r]);
+        res.scores.push_back(scores[order[r]]);
+    }
+    return res;
+}
+
+FeatureSelection select_features(Context& ctx, const FeatureData& data, double sigma, const EstParams& p, int prec,
+                                 int k) {
+    // features.cpp:125-162
+    validate_features(data, k);
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    const int d = static_cast<int>(data.d);
+    KernelPtr label = label_kernel(ctx, data, sigma, prec);
+    std::vector<KernelPtr> kernels;
+    {
+        DevBuf xs = upload_features(ctx, data);
+        for (int j = 0; j < d; ++j) kernels.push_back(feature_kernel(ctx, data, xs.as<double>(), sigma, prec, j));
+        ctx.sync();
+    }
+    FeatureSelection res;
+    std::vector<bool> taken(d, false);
+    KernelPtr selected;  // running Hadamard product of the picks
+    for (int step = 0; step < k; ++step) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const StepScorer scorer(ctx, *label, p, derive_key(p.seed, static_cast<uint64_t>(step)));
+        int best = -1;
+        double best_score = 0.0;
+        KernelPtr best_joint;
+        for (int j = 0; j < d; ++j) {
+            if (taken[j]) continue;
+            KernelPtr cand = step == 0 ? nullptr : hadamard_joint(ctx, *selected, *kernels[j]);
+            const KernelMatrix& cm = step == 0 ? *kernels[j] : *cand;
+            const double sc = scorer.score(cm, data.name(j));
+            if (best < 0 || sc > best_score) {
+                best = j;
+                best_score = sc;
+                best_joint = std::move(cand);
+            }
+        }
+        taken[best] = true;
+        if (step == 0)
+            selected = std::move(kernels[best]);  // the first pick's own kernel (no longer a candidate)
+        else
+            selected = std::move(best_joint);
+        res.columns.push_back(best);
+        res.objective.push_back(best_score);
+        res.elapsed.push_back(seconds_since(t0));
+    }
+    return res;
 }
 
 }  // namespace rb

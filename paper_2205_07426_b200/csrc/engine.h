@@ -10,6 +10,7 @@
 
 #include <array>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "host_math.h"
@@ -242,6 +243,27 @@ struct MreCell {
     int trials = 0;
 };
 MreCell measure_cell(Context& ctx, const KernelMatrix& k, double exact_entropy, const EstParams& p, int trials);
+
+// ---- feature tools (proj/src/features.cpp) ----
+struct FeatureData {
+    const double* x = nullptr;  // host n x d, column-major, leading dimension ldx
+    int64_t n = 0, d = 0, ldx = 0;
+    std::vector<std::string> labels, names;
+    std::string name(int j) const;
+};
+struct FeatureRanking {
+    std::vector<int> columns;       // top-k, scores non-increasing, ties by ascending column
+    std::vector<double> scores;     // I_alpha(X_j; Y)
+    std::vector<double> elapsed;    // seconds per scored feature (all d)
+};
+struct FeatureSelection {
+    std::vector<int> columns;       // greedy pick order
+    std::vector<double> objective;  // I_alpha(S; Y) after each addition
+    std::vector<double> elapsed;    // seconds per greedy step
+};
+FeatureRanking rank_features(Context& ctx, const FeatureData& data, double sigma, const EstParams& p, int prec, int k);
+FeatureSelection select_features(Context& ctx, const FeatureData& data, double sigma, const EstParams& p, int prec,
+                                 int k);
 
 struct MutualInfo {
     double value = 0.0, vars_entropy = 0.0, target_entropy = 0.0, joint_entropy = 0.0;

@@ -1,0 +1,105 @@
+"""Feature tools on the device (proj/src/features.cpp): parity with the
+oracle restatement on identical inputs (randomized methods through the C ABI), and the
+reference's own known-answer tests (proj/tests/test_features.cpp) on the device mirror."""
+import numpy as np
+import pytest
+
+from fixtures import correlated_dataset, duplicate_dataset, label_leak_dataset, parity_dataset
+
+pytestmark = pytest.mark.gpu
+
+EXACT = dict(alpha=2.0, method="exact")
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-4)])
+@pytest.mark.parametrize("params", [dict(alpha=2.0, method="int", s=32, seed=9),
+                                    dict(alpha=1.5, method="chebyshev", s=40, m=30, seed=4, bounds=(0.0, 1.0))])
+def test_rank_and_select_match_oracle(R, orc, prec, tol, params):
+    x, labels, names = correlated_dataset(200, 94, [0.1, 0.6, 0.3, 0.0, 0.45])
+    if prec == "fp32":
+        x = x.astype(np.float32).astype(np.float64)
+    rp = dict(params)
+    if "bounds" in rp:
+        rp["bounds"] = R.SpectrumBounds(u=rp["bounds"][0], v=rp["bounds"][1])
+    p = R.EstimatorParams(**rp)
+    cols, scores = orc.rank_features(x, labels, 1.0, 5, names, **params)
+    got = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 5, names, precision=prec)
+    # a score is a difference of three entropies (each within tol relative, |S| <= log n), so the
+    # bound on it is absolute: tol * log(n)
+    atol = tol * np.log(len(labels))
+    assert got.columns == cols
+    assert np.allclose(got.scores, scores, rtol=0, atol=atol)
+    assert got.names == [names[c] for c in cols] and len(got.elapsed) == 5
+    scols, obj = orc.select_features(x, labels, 1.0, 3, names, **params)
+    sel = R.select_features(x, labels, R.GaussianKernel(1.0), p, 3, names, precision=prec)
+    assert sel.columns == scols
+    assert np.allclose(sel.objective, obj, rtol=0, atol=atol)
+
+
+def test_label_leak_first(R):  # test_features.cpp:59-68
+    x, labels, names = label_leak_dataset(300, 91)
+    p = R.EstimatorParams(**EXACT)
+    rank = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 5, names)
+    assert rank.names[0] == "leak" and rank.scores[0] > 3.0 * abs(rank.scores[1])
+    sel = R.select_features(x, labels, R.GaussianKernel(1.0), p, 2, names)
+    assert sel.names[0] == "leak"
+    # randomized device path agrees on the leak
+    rank2 = R.rank_features(x, labels, R.GaussianKernel(1.0), R.EstimatorParams(alpha=2.0, method="int", s=64,
+                                                                                 seed=3), 5, names)
+    assert rank2.names[0] == "leak"
+
+
+def test_duplicates_identical_scores_index_tie_break(R):  # test_features.cpp:78-99
+    x, labels, names = duplicate_dataset(120, 93)
+    for p in (R.EstimatorParams(**EXACT), R.EstimatorParams(alpha=2.0, method="int", s=32, seed=5)):
+        rank = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 3, names)
+        assert rank.scores[0] == rank.scores[1]  # bitwise-identical computation
+        assert rank.names[:2] == ["a", "b"] and rank.columns[:2] == [0, 1]
+
+
+def test_k1_selection_equals_ranking_argmax(R):  # test_features.cpp:101-114
+    x, labels, names = correlated_dataset(200, 94, [0.1, 0.6, 0.3, 0.0, 0.45])
+    for seed in (0, 7, 123):
+        p = R.EstimatorParams(alpha=2.0, method="int", s=64, seed=seed)
+        rank = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 1, names)
+        sel = R.select_features(x, labels, R.GaussianKernel(1.0), p, 1, names)
+        assert rank.names[0] == sel.names[0] and rank.scores[0] == sel.objective[0]
+
+
+def test_parity_pair(R):  # test_features.cpp:116-141
+    x, labels, names = parity_dataset(400, 95)
+    p = R.EstimatorParams(**EXACT)
+    rank = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 4, names)
+    assert all(abs(s) <= 0.02 for s in rank.scores)
+    sel = R.select_features(x, labels, R.GaussianKernel(1.0), p, 2, names)
+    assert sorted(sel.names) == ["p1", "p2"] and sel.objective[1] >= 0.1
+
+
+def test_fixed_seeds_identical(R):  # test_features.cpp:160-175
+    x, labels, names = correlated_dataset(150, 96, [0.7, 0.2, 0.0])
+    p = R.EstimatorParams(alpha=2.0, method="int", s=32, seed=9)
+    r1 = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 3, names)
+    r2 = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 3, names)
+    assert r1.names == r2.names and r1.scores == r2.scores
+    s1 = R.select_features(x, labels, R.GaussianKernel(1.0), p, 3, names)
+    s2 = R.select_features(x, labels, R.GaussianKernel(1.0), p, 3, names)
+    assert s1.names == s2.names and s1.objective == s2.objective
+
+
+def test_validation(R):  # test_features.cpp:177-183
+    x, labels, names = correlated_dataset(50, 97, [0.5, 0.1])
+    p = R.EstimatorParams(alpha=2.0, method="int", s=16, seed=1)
+    with pytest.raises(R.RenyiError):
+        R.rank_features(x, labels, R.GaussianKernel(1.0), p, 3, names)
+    with pytest.raises(R.RenyiError):
+        R.select_features(x, labels, R.GaussianKernel(1.0), p, 0, names)
+    with pytest.raises(R.RenyiError) as e:
+        R.rank_features(x, labels[:10], R.GaussianKernel(1.0), p, 1, names)
+    assert e.value.kind == "size_mismatch"
+    with pytest.raises(R.RenyiError):
+        R.rank_features(x, [], R.GaussianKernel(1.0), p, 1, names)
+
+
+def test_one_hot_labels(R):  # test_features.cpp:185-192
+    oh = R.one_hot_labels(["b", "a", "b", "c"])
+    assert oh.shape == (4, 3) and np.all(oh.sum(axis=1) == 1.0) and oh[1, 0] == 1.0
