@@ -217,22 +217,26 @@ constexpr int ST = 128;  // symmetric tile
 constexpr int SK = 16;   // feature chunk
 
 __device__ __forceinline__ void store_split8(__half* ph, __half* pl, const float* kv, int64_t gj0, int64_t n) {
-    __align__(16) __half h[8];
-    __align__(16) __half l[8];
+    __align__(16) __half2 h[4];
+    __align__(16) __half2 l[4];
+    const float2 sc = make_float2(static_cast<float>(kSplitScale), static_cast<float>(kSplitScale));
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-        const float s = kv[v] * static_cast<float>(kSplitScale);
-        h[v] = __float2half_rn(s);
-        l[v] = __float2half_rn(s - __half2float(h[v]));
+    for (int v = 0; v < 4; ++v) {  // packed: cvt.rn.f16x2.f32 for hi, the residual in fp32 pairs, cvt again
+        const float2 s2 = __fmul2_rn(make_float2(kv[2 * v], kv[2 * v + 1]), sc);
+        h[v] = __float22half2_rn(s2);
+        const float2 back = __half22float2(h[v]);
+        l[v] = __float22half2_rn(__fadd2_rn(s2, make_float2(-back.x, -back.y)));
     }
     if (gj0 + 7 < n && ((reinterpret_cast<uintptr_t>(ph) | reinterpret_cast<uintptr_t>(pl)) & 15) == 0) {
         *reinterpret_cast<uint4*>(ph) = *reinterpret_cast<const uint4*>(h);
         *reinterpret_cast<uint4*>(pl) = *reinterpret_cast<const uint4*>(l);
     } else {
+        const __half* hh = reinterpret_cast<const __half*>(h);
+        const __half* ll = reinterpret_cast<const __half*>(l);
         for (int v = 0; v < 8; ++v)
             if (gj0 + v < n) {
-                ph[v] = h[v];
-                pl[v] = l[v];
+                ph[v] = hh[v];
+                pl[v] = ll[v];
             }
     }
 }
@@ -264,8 +268,12 @@ __device__ __forceinline__ void sym_accumulate(const float* __restrict__ xf, int
 #pragma unroll
             for (int u = 0; u < SU; ++u) {
                 sqr[u] = fmaf(a[u], a[u], sqr[u]);
+                const float2 au = make_float2(a[u], a[u]);
 #pragma unroll
-                for (int v = 0; v < 8; ++v) dot[u][v] = fmaf(a[u], b[v], dot[u][v]);
+                for (int v = 0; v < 8; v += 2) {  // packed FFMA2: two columns per instruction
+                    const float2 r = __ffma2_rn(au, make_float2(b[v], b[v + 1]), make_float2(dot[u][v], dot[u][v + 1]));
+                    dot[u][v] = r.x, dot[u][v + 1] = r.y;
+                }
             }
 #pragma unroll
             for (int v = 0; v < 8; ++v) sqc[v] = fmaf(b[v], b[v], sqc[v]);
@@ -334,10 +342,14 @@ __global__ void __launch_bounds__(SThreads) gram_sym_f32_kernel(GramArgs g, cons
 #pragma unroll
     for (int u = 0; u < SU; ++u)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            const int64_t gi = row0 + ty + 32 * u, gj = col0 + 8 * tx + v;
-            e[u][v] = (gi == gj) ? 1.0f : fast_exp2(e[u][v]);  // e now holds K
-        }
+        for (int v = 0; v < 8; ++v) e[u][v] = fast_exp2(e[u][v]);  // e now holds K
+    if (bi == bj) {  // K_ii = 1 exactly (ops.cpp:12) on the diagonal tiles only
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+                if (ty + 32 * u == 8 * tx + v) e[u][v] = 1.0f;
+    }
     // direct tile: rows gi, columns gj
 #pragma unroll
     for (int u = 0; u < SU; ++u) {
