@@ -192,14 +192,15 @@ __device__ __forceinline__ void exp16(const float* sv, float2 c2v, int col0, int
 template <bool DIAG>
 __device__ __forceinline__ void exp_store32(uint32_t rd, uint32_t wr, float2 c2v, int col0, int row) {
     float s0[16], s1[16];
-    uint32_t pk[16];
+    uint32_t pk0[8], pk1[8];
     tmem_ld16(rd, s0);
     tmem_ld_wait();
     tmem_ld16(rd + 16, s1);
-    exp16<DIAG>(s0, c2v, col0, row, pk);
+    exp16<DIAG>(s0, c2v, col0, row, pk0);
+    tmem_st8(wr, pk0);  // over columns already read; overlaps the second half's exp work
     tmem_ld_wait();
-    exp16<DIAG>(s1, c2v, col0 + 16, row, pk + 8);
-    tmem_st16(wr, pk);
+    exp16<DIAG>(s1, c2v, col0 + 16, row, pk1);
+    tmem_st8(wr + 8, pk1);
 }
 
 // One thread's CW columns of S -> P (P over the first CW/2 of the columns it read)
@@ -569,13 +570,9 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(block_av_mf_kernel<DP, NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(block_av_mf_kernel<DP, NPAD>), C::kSmem);
+        e != cudaSuccess)
+        return e;
     MfArgs args;
     args.total_iters = plan.total_iters;
     args.j_blocks = plan.k_tiles;

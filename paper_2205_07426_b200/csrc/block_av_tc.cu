@@ -342,13 +342,10 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
               make_map_v3(&m_vlo, VSPLIT ? v.vlo : v.v, v.rpr, v.cols, v.world, vbox);
     if (v.rpr % BK != 0) return cudaErrorInvalidValue;
     if (!ok) return cudaErrorInvalidValue;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(block_av_tc_kernel<NPAD, VSPLIT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    if (cudaError_t e =
+            ensure_smem_attr(reinterpret_cast<const void*>(block_av_tc_kernel<NPAD, VSPLIT>), C::kSmemBytes);
+        e != cudaSuccess)
+        return e;
     TcArgs args;
     args.total_iters = plan.total_iters;
     args.k_tiles = plan.k_tiles;

@@ -37,6 +37,10 @@ struct SplitPanelView {
     int world;
 };
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device, once per (fn, device);
+// thread-safe (ranks may drive different devices from different host threads)
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
+
 struct StreamKPlan {
     int row_blocks = 0;
     int k_tiles = 0;

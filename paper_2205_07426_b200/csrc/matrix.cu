@@ -488,13 +488,8 @@ cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStr
         const int nb = static_cast<int>((g.n + ST - 1) / ST);
         const int64_t tiles = static_cast<int64_t>(nb) * (nb + 1) / 2;
         const size_t smem = (2 * SK * ST + ST * (ST + 1)) * sizeof(float);
-        static bool attr = false;
-        if (!attr) {
-            e = cudaFuncSetAttribute(gram_sym_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
+        e = ensure_smem_attr(reinterpret_cast<const void*>(gram_sym_f32_kernel), static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
         gram_sym_f32_kernel<<<static_cast<unsigned>(tiles), SThreads, smem, stream>>>(g, xf, yf, nb, hi, lo);
         e = cudaGetLastError();
         cudaFreeAsync(xf, stream);

@@ -12,6 +12,10 @@
 
 #include <algorithm>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -291,6 +295,19 @@ __global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64
 }
 
 }  // namespace
+
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({fn, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({fn, dev});
+    return e;
+}
 
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;

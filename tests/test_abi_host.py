@@ -128,3 +128,13 @@ def test_mixture_samples_match_oracle(R, orc):
     x = R.mixture_samples(50, 3, 11, 1.5)
     y = orc.mixture_samples(50, 3, 11, 1.5)
     assert np.array_equal(x, y)
+
+
+def test_nccl_unique_id_without_gpu(R):
+    """The NCCL transport opens libnccl.so.2 at run time; creating the bootstrap id needs no GPU."""
+    try:
+        uid = R.nccl_unique_id()
+    except R.RenyiError as e:  # no libnccl on this host: the error is the NCCL kind, not a crash
+        assert e.kind == "nccl_error"
+        return
+    assert isinstance(uid, (bytes, bytearray)) and len(uid) == 128 and any(uid)
