@@ -58,6 +58,7 @@ def parse():
                    help="c4 (default, BASELINE headline): MI at n=100k, materialised fp32 A; "
                         "c5: entropy at n=400k d=128, bf16 matrix-free (tensor-pipe bound)")
     p.add_argument("--mf-kc", type=int, default=8, help="c5: j-blocks (x128) per TMEM accumulation chunk")
+    p.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period during the timed region")
     p.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                    help="N > 1: row-shard one estimate over all ranks (NCCL, strong scaling) or run "
                         "independent replicas (weak scaling)")
@@ -114,8 +115,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 200):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
         self.path = None
 
@@ -125,7 +127,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", str(self.period_ms)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
@@ -272,7 +274,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, args.clock_ms)
     clocks.start()
     ctx.profile(True)
     l0 = ctx.launch_count()
@@ -472,7 +474,7 @@ def run_ours_c5(args):
         torch.cuda.synchronize()
 
     barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, args.clock_ms)
     clocks.start()
     ctx.profile(True)
     l0 = ctx.launch_count()

@@ -165,6 +165,17 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64
         : "memory");
 }
 
+// D (TMEM) [+]= A · B, tf32 operands (fp32 storage, K = 8 per instruction)
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // D (TMEM) [+]= A (TMEM, 16-bit, 2 K-elements per 32-bit column, lane = row) · B (smem descriptor)
 __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -297,6 +308,12 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_
     d |= static_cast<uint64_t>(1) << 46;
     d |= static_cast<uint64_t>(layout) << 61;
     return d;
+}
+
+// Instruction descriptor: tf32 x tf32 -> fp32 (kind::tf32), both operands K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_tf32_f32(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
 }
 
 // Instruction descriptor: bf16 x bf16 -> fp32, both operands K-major.

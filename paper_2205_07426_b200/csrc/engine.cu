@@ -353,7 +353,10 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
         k->hi.alloc(elems * sizeof(__half));
         k->lo.alloc(elems * sizeof(__half));
         k->unscale = inv_n / kSplitScale;
-        launched(ctx, launch_gram_split(g, k->hi.as<__half>(), k->lo.as<__half>(), ctx.stream()), "gram_split");
+        DevBuf scratch;
+        scratch.alloc(gram_split_scratch_bytes(g));
+        launched(ctx, launch_gram_split(g, k->hi.as<__half>(), k->lo.as<__half>(), scratch.as<void>(), ctx.stream()),
+                 "gram_split");  // scratch goes back to the pool: reuse is stream-ordered
     } else {
         k->a64.alloc(elems * sizeof(double));
         k->unscale = 1.0;

@@ -191,7 +191,14 @@ struct GramArgs {
     double inv_n;
     int f32_compute;  // 1: distances/exponentials in fp32 (fp32 configs); 0: fp64
 };
-cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStream_t stream);
+// scratch (device bytes) the split Gram needs for staged operands; the caller provides it from its
+// caching pool (no allocation on the launch path: stream-ordered allocations stalled up to 150 ms)
+size_t gram_split_scratch_bytes(const GramArgs& g);
+cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, void* scratch, cudaStream_t stream);
+// tensor-core (3xTF32) Gram for single-rank fp32 builds with at most 128 features (gram_tc.cu)
+bool gram_tc_supported(const GramArgs& g);
+size_t gram_tc_scratch_bytes(const GramArgs& g);
+cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scratch, cudaStream_t stream);
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream);
 
 // A (fp64 row-major) -> planes holding A*scale.

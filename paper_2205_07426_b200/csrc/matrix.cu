@@ -467,14 +467,19 @@ inline dim3 row_grid(int64_t rows, int64_t cols) {
 
 }  // namespace
 
-cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStream_t stream) {
+size_t gram_split_scratch_bytes(const GramArgs& g) {
+    if (gram_tc_supported(g)) return gram_tc_scratch_bytes(g);
+    if (g.f32_compute && g.row0 == 0 && g.rows == g.n && g.ld % 8 == 0)
+        return static_cast<size_t>(g.n) * (g.dx + (g.y ? g.dy : 0)) * sizeof(float);
+    return 0;
+}
+
+cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, void* scratch, cudaStream_t stream) {
+    if (gram_tc_supported(g)) return launch_gram_tc(g, hi, lo, scratch, stream);
     if (g.f32_compute && g.row0 == 0 && g.rows == g.n && g.ld % 8 == 0) {
         // fp32 copies of the samples, column-major [d][n], for the symmetric tiles
-        float* xf = nullptr;
-        const int64_t dt = g.dx + (g.y ? g.dy : 0);
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&xf), static_cast<size_t>(g.n) * dt * sizeof(float),
-                                        stream);
-        if (e != cudaSuccess) return e;
+        float* xf = static_cast<float*>(scratch);
+        cudaError_t e = cudaSuccess;
         const int64_t nx = g.n * g.dx;
         to_f32_colmajor_kernel<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, stream>>>(g.x, g.n, g.dx, g.x_rs,
                                                                                          g.x_cs, xf);
@@ -492,7 +497,6 @@ cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, cudaStr
         if (e != cudaSuccess) return e;
         gram_sym_f32_kernel<<<static_cast<unsigned>(tiles), SThreads, smem, stream>>>(g, xf, yf, nb, hi, lo);
         e = cudaGetLastError();
-        cudaFreeAsync(xf, stream);
         return e;
     }
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
