@@ -40,7 +40,9 @@ constexpr int kPlane = GT * kTT;   // one staged [128][128] fp16 plane
 constexpr int kGSmem = kGStages * 2 * kSub + 4 * kPlane + 1024;
 
 struct GtArgs {
-    int64_t nb, tiles;  // row blocks; upper-triangle tiles
+    int64_t nb, tiles;  // column blocks; tiles (upper triangle, or shard row blocks x nb)
+    int rect;           // 1: a row shard [row0, row0 + rows): all its tiles, no mirroring
+    int64_t row0, row_end;
     int ksub;           // K sub-tiles (KP / 32)
     int64_t n, ld;
     const float* sq;    // ‖z_i‖², [round_up(n,128)]
@@ -63,6 +65,15 @@ __device__ __forceinline__ float tf32_round(float v) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
     return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void map_tile(const GtArgs& a, int64_t t, int64_t* bi, int64_t* bj) {
+    if (a.rect) {
+        *bi = a.row0 / GT + t / a.nb;
+        *bj = t % a.nb;
+    } else {
+        tile_of(t, a.nb, bi, bj);
+    }
 }
 
 __device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -107,7 +118,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < args.tiles; t += gridDim.x) {
                 int64_t bi, bj;
-                tile_of(t, args.nb, &bi, &bj);
+                map_tile(args, t, &bi, &bj);
                 for (int ks = 0; ks < args.ksub; ++ks) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     mbar_arrive_expect_tx(&full[stage], 2 * kSub);
@@ -164,9 +175,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
             for (int qq = et; qq < GT * 16; qq += 256) {
                 const int r = qq >> 4, c = qq & 15;
                 const int64_t gr = grow0 + r, gc = gcol0 + 8 * c;
-                if (gr >= args.n) continue;
+                if (gr >= args.row_end) continue;
                 const uint4 v = *reinterpret_cast<const uint4*>(src + r * kTT + c * 16);
-                __half* out = dst + gr * args.ld + gc;
+                __half* out = dst + (gr - args.row0) * args.ld + gc;
                 if (gc + 8 <= args.n) {
                     st_global_v4(out, v.x, v.y, v.z, v.w);
                 } else {
@@ -177,7 +188,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         };
         for (int64_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++lt) {
             int64_t bi, bj;
-            tile_of(t, args.nb, &bi, &bj);
+            map_tile(args, t, &bi, &bj);
             const uint32_t buf = lt & 1u;
             const bool diag = bi == bj;
             const int64_t gi = bi * GT + row;
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM buffer free for the tile after next
             asm volatile("bar.sync 1, 256;" ::: "memory");
-            if (diag) {  // D[i][j] <- K(j, i) = T[i][j] below the diagonal
+            if (diag && !args.rect) {  // D[i][j] <- K(j, i) = T[i][j] below the diagonal
                 for (int idx = et; idx < GT * GT; idx += 256) {
                     const int i = idx >> 7, j = idx & 127;
                     if (j < i) {
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
             store_plane_rows(dd, args.hi, bi * GT, bj * GT);
             store_plane_rows(dd + kPlane, args.lo, bi * GT, bj * GT);
-            if (!diag) {
+            if (!diag && !args.rect) {
                 store_plane_rows(tt, args.hi, bj * GT, bi * GT);
                 store_plane_rows(tt + kPlane, args.lo, bj * GT, bi * GT);
             }
@@ -305,7 +316,7 @@ EncodeFn tmap_encoder() {
 }  // namespace
 
 bool gram_tc_supported(const GramArgs& g) {
-    return g.f32_compute && g.row0 == 0 && g.rows == g.n && g.ld % 8 == 0 && g.dx + (g.y ? g.dy : 0) <= 128;
+    return g.f32_compute && g.row0 % GT == 0 && g.ld % 8 == 0 && g.dx + (g.y ? g.dy : 0) <= 128;
 }
 
 namespace {
@@ -361,7 +372,10 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
     if (e == cudaSuccess) {
         GtArgs a;
         a.nb = npad / GT;
-        a.tiles = a.nb * (a.nb + 1) / 2;
+        a.rect = (g.row0 != 0 || g.rows != g.n) ? 1 : 0;
+        a.row0 = g.row0;
+        a.row_end = g.row0 + g.rows;
+        a.tiles = a.rect ? (g.rows + GT - 1) / GT * a.nb : a.nb * (a.nb + 1) / 2;
         a.ksub = kp / KS;
         a.n = g.n, a.ld = g.ld;
         a.sq = sq;
@@ -370,8 +384,10 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t grid = std::min<int64_t>(sms, a.tiles);
-        gram_tc_kernel<<<static_cast<unsigned>(grid), kGThreads, kGSmem, stream>>>(ma, mb, a);
-        e = cudaGetLastError();
+        if (grid > 0) {
+            gram_tc_kernel<<<static_cast<unsigned>(grid), kGThreads, kGSmem, stream>>>(ma, mb, a);
+            e = cudaGetLastError();
+        }
     }
     return e;
 }
