@@ -370,3 +370,24 @@ def test_estimates_deterministic(R, orc):
     e1 = R.entropy(x, 4.0, p, "fp32")
     e2 = R.entropy(x, 4.0, p, "fp32")
     assert e1.entropy == e2.entropy and e1.trace_estimate == e2.trace_estimate
+
+
+def test_out_of_memory_is_reported_and_recoverable(R):
+    """A materialised fp32 A at n = 250k needs 250 GB (> 180 GB of HBM): the build fails with the
+    out_of_memory kind, and the context keeps working afterwards."""
+    import torch
+
+    n, d = 250_000, 2
+    ctx = R.Context(0)
+    xd = torch.zeros(d, n, dtype=torch.float64, device="cuda")
+    xd[0] = torch.arange(n, dtype=torch.float64, device="cuda") * 1e-3
+    with pytest.raises(R.RenyiError) as e:
+        R.build_kernel_dev(xd.data_ptr(), n, d, n, R.GaussianKernel(1.0), "fp32", ctx=ctx)
+    assert e.value.kind == "out_of_memory"
+    # the matrix-free path handles the same samples without storing A
+    k = R.build_kernel_dev(xd.data_ptr(), n, d, n, R.GaussianKernel(1.0), "mf", ctx=ctx)
+    y = R.ops.matvec(k, np.ones(n))
+    # interior rows: (1/n) * sum_j exp(-(1e-3 (i-j))^2 / 2) = sqrt(2 pi) / 1e-3 / n (edges: half)
+    assert np.all(np.isfinite(y))
+    assert abs(y[n // 2] - math.sqrt(2 * math.pi) / 1e-3 / n) <= 1e-3 * y[n // 2]
+    assert abs(y[0] - 0.5 * math.sqrt(2 * math.pi) / 1e-3 / n) <= 2e-3 * y[0]

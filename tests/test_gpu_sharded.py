@@ -113,3 +113,24 @@ def test_sharded_matrix_free_matches_single_rank(R, orc):
         assert t.sketch_rank == ref.sketch_rank
         # different stream-K splits change the fp32 TMEM chunk boundaries: agreement to ~1e-6
         assert abs(t.value - ref.value) <= 1e-5 * abs(ref.value)
+
+
+def test_nccl_transport_single_rank(R):
+    """The NCCL transport end to end with a 1-rank communicator (no cross-rank waits on one GPU):
+    dlopen, comm init, in-place all-gather and the f64-sum / u32-max all-reduces on the estimator
+    path; results must equal the transport-free run bit for bit."""
+    n = 1500
+    x, y = mi_inputs(n, 23)
+    x, y = f32(x), f32(y)
+    sx, sy = R.GaussianKernel(4.0), R.GaussianKernel(math.sqrt(8))
+    p = R.EstimatorParams(alpha=1.5, method="chebyshev", s=40, m=30, seed=2, bounds=R.SpectrumBounds(u=0, v=1))
+    ref = R.mutual_information_samples(x, sx, y, sy, p, "fp32", R.Context(0))
+    try:
+        uid = R.nccl_unique_id()
+    except R.RenyiError as e:
+        pytest.skip(f"no NCCL: {e}")
+    ctx = R.Context(0)
+    ctx.init_nccl(0, 1, uid)
+    assert ctx.rank_world() == (0, 1)
+    got = R.mutual_information_samples(x, sx, y, sy, p, "fp32", ctx)
+    assert got.value == ref.value and got.joint_entropy == ref.joint_entropy
