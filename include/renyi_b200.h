@@ -50,10 +50,13 @@ enum {
  * from samples only (renyi_kernel_build_gaussian*, the *_samples and entropy entry
  * points); renyi_kernel_from_matrix / _hadamard_joint / _download reject it. */
 enum { RENYI_F64 = 0, RENYI_F32 = 1, RENYI_MF = 2 };
-/* fp32 configurations: iterate operand of the block product. SPLIT (default) keeps V
- * as an fp16 hi+lo pair (3 tensor-core products, ~fp32 accuracy); FAST rounds V to
- * one fp16 plane (2 products) — see DESIGN.md for the measured trace error. */
-enum { RENYI_OPERAND_SPLIT = 0, RENYI_OPERAND_FAST = 1 };
+/* fp32 configurations: iterate operand of the block product. SPLIT (default) keeps V as an
+ * fp16 hi+lo pair (3 tensor-core products, ~fp32 accuracy per product); FAST rounds V to
+ * one fp16 plane (2 products); AUTO uses SPLIT where product vectors are returned
+ * (matmul_panel, apply_panel, the Hutch++ sketch) and FAST for trace-only passes. FAST and
+ * AUTO are ~10 % faster on config 4 but can miss the 1e-4 trace bar at small probe counts
+ * (DESIGN.md). */
+enum { RENYI_OPERAND_SPLIT = 0, RENYI_OPERAND_FAST = 1, RENYI_OPERAND_AUTO = 2 };
 /* probe distributions */
 enum { RENYI_PROBE_GAUSSIAN = 0, RENYI_PROBE_RADEMACHER = 1 };
 /* estimator methods (renyi::Method, proj/include/renyi/entropy.hpp:12) */

@@ -62,8 +62,9 @@ class Context:
         check(L.lib().renyi_ctx_set_matrix_free_chunk(self._h, jblocks))
 
     def set_operand_mode(self, mode: str = "split") -> None:
-        """'split' (default, V as fp16 hi+lo, 3 MMAs) or 'fast' (V hi only, 2 MMAs)."""
-        check(L.lib().renyi_ctx_set_operand_mode(self._h, {"split": 0, "fast": 1}[mode]))
+        """'split' (default; V as fp16 hi+lo, 3 MMAs), 'fast' (V hi only, 2 MMAs) or 'auto' (split
+        where vectors are returned, fast for trace-only passes)."""
+        check(L.lib().renyi_ctx_set_operand_mode(self._h, {"split": 0, "fast": 1, "auto": 2}[mode]))
 
     def sync(self) -> None:
         check(L.lib().renyi_ctx_sync(self._h))

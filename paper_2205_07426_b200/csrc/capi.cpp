@@ -223,9 +223,9 @@ int renyi_ctx_rank(renyi_ctx* ctx, int* rank, int* world) {
 int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode) {
     return guarded([&] {
         need(ctx, "ctx");
-        if (mode != RENYI_OPERAND_SPLIT && mode != RENYI_OPERAND_FAST)
+        if (mode != RENYI_OPERAND_SPLIT && mode != RENYI_OPERAND_FAST && mode != RENYI_OPERAND_AUTO)
             rb::fail(rb::kInvalidArgument, "unknown operand mode");
-        ctx->ctx.operand_split = mode == RENYI_OPERAND_SPLIT;
+        ctx->ctx.operand_mode = mode == RENYI_OPERAND_SPLIT ? 0 : (mode == RENYI_OPERAND_FAST ? 1 : 2);
     });
 }
 

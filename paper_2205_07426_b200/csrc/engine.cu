@@ -488,10 +488,14 @@ void download(Context& ctx, const KernelMatrix& k, double* out) {
 // ---------------------------------------------------------------- panel sessions
 namespace {
 
+bool split_operand(const Context& ctx, bool vectors_out) {
+    return ctx.operand_mode == 0 || (ctx.operand_mode == 2 && vectors_out);
+}
+
 class PanelSession {
 public:
     PanelSession(Context& ctx, const KernelMatrix& k, const double* x, int64_t ldx, int s, int max_passes,
-                 double* acc_out, double acc_coef0)
+                 double* acc_out, double acc_coef0, bool vectors_out)
         : ctx_(ctx), k_(k), s_(s), max_passes_(max_passes), acc_(acc_out) {
         if (s < 1 || s > kMaxPanelCols) fail(kInternal, "panel width must be in [1,128]");
         if (k.world != ctx.world() || k.rank != ctx.rank())
@@ -522,14 +526,14 @@ public:
             // rows past n in the last chunk are never written: keep them zero (A's columns there are
             // TMA-zero, but 0 x garbage could be NaN)
             cuda_check(cudaMemsetAsync(ctx.vhi.as<__half>(), 0, plane, ctx.stream()), "memset");
-            if (ctx.operand_split && !mf_) {
+            if (split_operand(ctx, vectors_out) && !mf_) {
                 ctx.vlo.ensure(plane);
                 cuda_check(cudaMemsetAsync(ctx.vlo.as<__half>(), 0, plane, ctx.stream()), "memset");
             }
             slice_ = static_cast<size_t>(k.rank) * s * ld_;
         }
         // the matrix-free P·V product takes one fp16 operand plane (P itself is fp16)
-        vlo_ = (k.prec == kF32 && ctx.operand_split) ? ctx.vlo.as<__half>() : nullptr;
+        vlo_ = (k.prec == kF32 && split_operand(ctx, vectors_out)) ? ctx.vlo.as<__half>() : nullptr;
         const size_t P1 = static_cast<size_t>(max_passes) + 1;
         ctx.stats.ensure(P1 * 3 * std::max(R_, 1) * s * sizeof(double));
         ctx.red.ensure(P1 * 3 * s * sizeof(double));
@@ -718,7 +722,8 @@ PanelResult run_panel(Context& ctx, const KernelMatrix& k, const double* x, int6
                       double* acc_out, double* last_out, int64_t ldo) {
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     const int P = static_cast<int>(coeffs.size());
-    PanelSession ps(ctx, k, x, ldx, s, std::max(P, 1), acc_out, acc_coef ? (*acc_coef)[0] : 0.0);
+    PanelSession ps(ctx, k, x, ldx, s, std::max(P, 1), acc_out, acc_coef ? (*acc_coef)[0] : 0.0,
+                    acc_out != nullptr || last_out != nullptr);
     for (int p = 0; p < P; ++p)
         ps.step(coeffs[p][0], coeffs[p][1], coeffs[p][2], acc_coef ? (*acc_coef)[p + 1] : 0.0);
     if (last_out) ps.state_f64(P, last_out, ldo);
@@ -844,7 +849,7 @@ PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, d
              "rng_panel");
     PowerRes res;
     const int iters = std::max(o.max_iters, 0);
-    PanelSession ps(ctx, k, ctx.x0.as<double>(), ld, 1, std::max(iters, 1), nullptr, 0.0);
+    PanelSession ps(ctx, k, ctx.x0.as<double>(), ld, 1, std::max(iters, 1), nullptr, 0.0, false);
     std::vector<double> d0 = ps.dots(0, 0);
     double norm = std::sqrt(d0[2]);
     if (norm == 0.0) fail(kInternal, "power-start vector is zero");

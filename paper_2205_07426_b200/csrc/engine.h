@@ -88,7 +88,12 @@ public:
     int grid = 0;  // CTAs of the persistent stream-K kernel (0 = SM count)
     int kc = 16;   // k tiles (x32 columns) per TMEM accumulation chunk
     int mf_kc = 8;  // matrix-free: j-blocks (x128 samples) per TMEM accumulation chunk
-    bool operand_split = true;  // V as fp16 hi+lo (3 MMAs); false = "fast" (V hi only, 2 MMAs)
+    // iterate operand of the fp32 block product: 0 split (default; V as fp16 hi+lo, 3 MMAs),
+    // 1 fast (V hi only, 2 MMAs), 2 auto (split where product vectors leave the panel:
+    // block_product, apply_panel, the Hutch++ sketch; fast for trace-only passes). Measured
+    // trace errors against the oracle: split <= 4e-6, fast / auto up to 2.5e-4 at small probe
+    // counts, so only split keeps the 1e-4 fp32 bar everywhere.
+    int operand_mode = 0;
 
     // instrumentation: CUDA-event timing of every block-product launch
     void prof_enable(bool on);
