@@ -200,6 +200,31 @@ int renyi_kernel_size(const renyi_kernel* k, int64_t* n);
 int renyi_kernel_download(renyi_ctx* ctx, const renyi_kernel* k, double* out);
 int renyi_kernel_destroy(renyi_kernel* k);
 
+/* ---- CSV ingestion feeding device X -----------------------------------------
+ * renyi::load_csv(path, label_column) — proj/src/csv.cpp:63-115, proj/include/renyi/csv.hpp:8-15
+ * (Dataset: proj/include/renyi/features.hpp:12-19). The bytes are parsed on the device: a quote-aware
+ * structural scan (read_record, csv.cpp:13-47) and a strtod-exact cell parse (parse_cell, 49-60);
+ * the n x d features stay resident for renyi_kernel_build_gaussian_dataset. Errors and their texts
+ * are the reference's (RENYI_E_PARSE_ERROR): "cannot open 'p'", "'p': missing header row",
+ * "'p': no column named 'c'", "row R: expected H fields, got F", "row R, column C: 't' is not
+ * numeric", "'p': need at least 2 data rows, got K". label_column may be NULL. */
+typedef struct renyi_dataset renyi_dataset;
+int renyi_csv_load(renyi_ctx* ctx, const char* path, const char* label_column, renyi_dataset** out);
+/* the same from a host buffer; source names the input in messages (NULL: "<buffer>") */
+int renyi_csv_parse(renyi_ctx* ctx, const char* text, int64_t len, const char* label_column, const char* source,
+                    renyi_dataset** out);
+int renyi_dataset_shape(const renyi_dataset* ds, int64_t* n, int64_t* d, int* has_labels);
+/* features (column-major, leading dimension ldx >= n) to a host buffer */
+int renyi_dataset_features(renyi_ctx* ctx, const renyi_dataset* ds, double* x, int64_t ldx);
+/* names[j] (j < d) and labels[i] (i < n); NULL when out of range */
+const char* renyi_dataset_name(const renyi_dataset* ds, int64_t j);
+const char* renyi_dataset_label(const renyi_dataset* ds, int64_t i);
+/* build_kernel(data.features(:, columns), GaussianKernel{sigma}) from the resident features
+ * (columns NULL: all d columns) */
+int renyi_kernel_build_gaussian_dataset(renyi_ctx* ctx, const renyi_dataset* ds, const int64_t* columns,
+                                        int64_t ncols, double sigma, int precision, renyi_kernel** out);
+int renyi_dataset_destroy(renyi_dataset* ds);
+
 /* ---- hot-path seams ------------------------------------------------------- */
 /* ops::matmul_panel(a, x) — proj/src/ops.cpp:98-107: Y = A V, V n x s */
 int renyi_matmul_panel(renyi_ctx* ctx, const renyi_kernel* k, const double* v, int s, double* y);

@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -250,6 +251,50 @@ inline MutualInformation mutual_information(const Context& ctx, const Normalized
     MutualInformation mi{};
     check(renyi_mutual_information(ctx.get(), vars.get(), target.get(), &p, &mi));
     return mi;
+}
+
+// Dataset (proj/include/renyi/features.hpp:12-19); features resident on the device
+class Dataset {
+public:
+    explicit Dataset(renyi_dataset* d) : h_(d, Del{}) {
+        int hl = 0;
+        check(renyi_dataset_shape(d, &n_, &d_, &hl));
+        for (int64_t j = 0; j < d_; ++j) names.emplace_back(renyi_dataset_name(d, j));
+        if (hl)
+            for (int64_t i = 0; i < n_; ++i) labels.emplace_back(renyi_dataset_label(d, i));
+    }
+    int64_t n() const { return n_; }
+    int64_t d() const { return d_; }
+    Matrix features(const Context& ctx) const {
+        Matrix x(n_, d_);
+        check(renyi_dataset_features(ctx.get(), h_.get(), x.data.data(), n_ > 0 ? n_ : 1));
+        return x;
+    }
+    // build_kernel(features(:, columns), spec) without leaving the device
+    NormalizedKernel kernel(const Context& ctx, const GaussianKernel& spec, Precision prec = Precision::fp64,
+                            const std::vector<int64_t>& columns = {}) const {
+        renyi_kernel* k = nullptr;
+        check(renyi_kernel_build_gaussian_dataset(ctx.get(), h_.get(), columns.empty() ? nullptr : columns.data(),
+                                                  static_cast<int64_t>(columns.size()), spec.sigma,
+                                                  static_cast<int>(prec), &k));
+        return NormalizedKernel(k);
+    }
+    std::vector<std::string> names, labels;
+
+private:
+    struct Del {
+        void operator()(renyi_dataset* d) const { renyi_dataset_destroy(d); }
+    };
+    std::shared_ptr<renyi_dataset> h_;
+    int64_t n_ = 0, d_ = 0;
+};
+
+// load_csv (proj/include/renyi/csv.hpp:14-15), parsed on the device
+inline Dataset load_csv(const Context& ctx, const std::string& path,
+                        const std::optional<std::string>& label_column = std::nullopt) {
+    renyi_dataset* d = nullptr;
+    check(renyi_csv_load(ctx.get(), path.c_str(), label_column ? label_column->c_str() : nullptr, &d));
+    return Dataset(d);
 }
 
 // cmd_entropy's composition (proj/tools/renyi_cli.cpp:144-154): build_kernel + estimate

@@ -113,6 +113,12 @@ def lib():
         h.oracle_select_params.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                            _I64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         h.oracle_mu_bound.argtypes = [C.c_double, C.c_double, C.c_double, _I64, _D, _D, _D]
+        h.oracle_csv_parse.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+        h.oracle_csv_shape.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int)]
+        h.oracle_csv_features.argtypes = [C.c_void_p, _D]
+        h.oracle_csv_string.restype = C.c_int64
+        h.oracle_csv_string.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_char_p, C.c_int64]
+        h.oracle_csv_free.argtypes = [C.c_void_p]
         h.oracle_threads.restype = C.c_int
         h.oracle_set_threads.argtypes = [C.c_int]
         _lib = h
@@ -410,3 +416,32 @@ def slab_sample_seconds(x, sigma, r0, h, sketch_cols, passes, cols_q, cols_w):
     """Seconds for rows [r0, r0+h) of one estimate: Gram rows + sketch pass + `passes` (Q, W) passes."""
     x = _f(x)
     return lib().oracle_slab_sample(_p(x), x.shape[0], x.shape[1], sigma, r0, h, sketch_cols, passes, cols_q, cols_w)
+
+
+def load_csv(text, label_column=None, source=None):
+    """load_csv (proj/src/csv.cpp:63-115) restated over a buffer with glibc std::strtod.
+    Returns dict(n, d, features (n x d), names, labels) or raises OracleError(10, message)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    _chk(lib().oracle_csv_parse(data, len(data), label_column.encode() if label_column else None,
+                                source.encode() if source else None, C.byref(h)))
+    try:
+        n, d, hl = C.c_int64(), C.c_int64(), C.c_int()
+        lib().oracle_csv_shape(h, C.byref(n), C.byref(d), C.byref(hl))
+        x = np.empty((n.value, d.value), dtype=np.float64, order="F")
+        if x.size:
+            lib().oracle_csv_features(h, x.ctypes.data_as(_D))
+
+        def strings(which, count):
+            out = []
+            for i in range(count):
+                size = lib().oracle_csv_string(h, which, i, None, 0)
+                buf = C.create_string_buffer(max(size, 1))
+                lib().oracle_csv_string(h, which, i, buf, size)
+                out.append(buf.raw[:size].decode("utf-8", errors="surrogateescape"))
+            return out
+
+        return dict(n=n.value, d=d.value, features=x, names=strings(0, d.value),
+                    labels=strings(1, n.value) if hl.value else [])
+    finally:
+        lib().oracle_csv_free(h)

@@ -1092,6 +1092,102 @@ void select_features(const FeatureData& data, double sigma, const Params& params
     }
 }
 
+// ---- load_csv (proj/src/csv.cpp:63-115) over an in-memory buffer -----------------------------
+// read_record (csv.cpp:13-47): one record, quotes and "" escapes honoured, '\r' dropped outside
+// quotes; returns false at EOF with no data. pos/len stand in for the std::istream.
+bool csv_read_record(const std::string& in, size_t& pos, std::vector<std::string>& fields) {
+    fields.clear();
+    std::string field;
+    bool in_quotes = false;
+    bool any = false;
+    while (pos < in.size()) {
+        const char c = in[pos++];
+        any = true;
+        if (in_quotes) {
+            if (c == '"') {
+                if (pos < in.size() && in[pos] == '"') {
+                    field.push_back('"');
+                    ++pos;
+                } else {
+                    in_quotes = false;
+                }
+            } else {
+                field.push_back(c);
+            }
+        } else if (c == '"') {
+            in_quotes = true;
+        } else if (c == ',') {
+            fields.push_back(std::move(field));
+            field.clear();
+        } else if (c == '\n') {
+            break;
+        } else if (c != '\r') {
+            field.push_back(c);
+        }
+    }
+    if (!any) return false;
+    fields.push_back(std::move(field));
+    return true;
+}
+
+// parse_cell (csv.cpp:49-60): std::strtod, trailing spaces tolerated
+double csv_parse_cell(const std::string& text, size_t row, size_t col) {
+    const char* begin = text.c_str();
+    char* end = nullptr;
+    const double value = std::strtod(begin, &end);
+    while (end && *end == ' ') ++end;
+    if (end == begin || (end && *end != '\0'))
+        fail(kParseError, "row " + std::to_string(row) + ", column " + std::to_string(col) + ": '" + text +
+                              "' is not numeric");
+    return value;
+}
+
+struct CsvData {
+    int64_t n = 0, d = 0;
+    Vec x;  // column-major n x d
+    std::vector<std::string> names, labels;
+};
+
+CsvData load_csv(const std::string& in, const char* label_column, const std::string& path) {
+    size_t pos = 0;
+    std::vector<std::string> header;
+    if (!csv_read_record(in, pos, header) || header.empty()) fail(kParseError, "'" + path + "': missing header row");
+    int label_idx = -1;
+    if (label_column) {
+        for (size_t j = 0; j < header.size(); ++j)
+            if (header[j] == label_column) label_idx = static_cast<int>(j);
+        if (label_idx < 0) fail(kParseError, "'" + path + "': no column named '" + std::string(label_column) + "'");
+    }
+    CsvData data;
+    for (size_t j = 0; j < header.size(); ++j)
+        if (static_cast<int>(j) != label_idx) data.names.push_back(header[j]);
+    std::vector<std::vector<double>> rows;
+    std::vector<std::string> fields;
+    size_t row_no = 1;
+    while (csv_read_record(in, pos, fields)) {
+        ++row_no;
+        if (fields.size() == 1 && fields[0].empty()) continue;
+        if (fields.size() != header.size())
+            fail(kParseError, "row " + std::to_string(row_no) + ": expected " + std::to_string(header.size()) +
+                                  " fields, got " + std::to_string(fields.size()));
+        std::vector<double> row;
+        row.reserve(header.size());
+        for (size_t j = 0; j < fields.size(); ++j) {
+            if (static_cast<int>(j) == label_idx) data.labels.push_back(fields[j]);
+            else row.push_back(csv_parse_cell(fields[j], row_no, j + 1));
+        }
+        rows.push_back(std::move(row));
+    }
+    if (rows.size() < 2)
+        fail(kParseError, "'" + path + "': need at least 2 data rows, got " + std::to_string(rows.size()));
+    data.n = static_cast<int64_t>(rows.size());
+    data.d = static_cast<int64_t>(rows.front().size());
+    data.x.assign(static_cast<size_t>(data.n * data.d), 0.0);
+    for (int64_t i = 0; i < data.n; ++i)
+        for (int64_t j = 0; j < data.d; ++j) data.x[static_cast<size_t>(i + j * data.n)] = rows[i][j];
+    return data;
+}
+
 }  // namespace orc
 
 // =====================================================================================
@@ -1452,5 +1548,30 @@ double oracle_slab_sample(const double* x, int64_t n, int64_t d, double sigma, i
     const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return dt + (sink == 12345.678 ? 1e-30 : 0.0);
 }
+
+// CSV: handle-based so Python can read the variable-size result
+int oracle_csv_parse(const char* text, int64_t len, const char* label, const char* source, void** out) {
+    return guard([&] {
+        auto* d = new orc::CsvData(orc::load_csv(std::string(text ? text : "", static_cast<size_t>(len)), label,
+                                                 source ? source : "<buffer>"));
+        *out = d;
+    });
+}
+void oracle_csv_shape(void* h, int64_t* n, int64_t* d, int* has_labels) {
+    auto* c = static_cast<orc::CsvData*>(h);
+    *n = c->n, *d = c->d, *has_labels = c->labels.empty() ? 0 : 1;
+}
+void oracle_csv_features(void* h, double* out) {
+    auto* c = static_cast<orc::CsvData*>(h);
+    std::memcpy(out, c->x.data(), sizeof(double) * c->x.size());
+}
+// string accessors: length-prefixed copies (names/labels may hold NUL bytes)
+int64_t oracle_csv_string(void* h, int which, int64_t i, char* buf, int64_t cap) {
+    auto* c = static_cast<orc::CsvData*>(h);
+    const std::string& s = which == 0 ? c->names[static_cast<size_t>(i)] : c->labels[static_cast<size_t>(i)];
+    if (buf && cap >= static_cast<int64_t>(s.size())) std::memcpy(buf, s.data(), s.size());
+    return static_cast<int64_t>(s.size());
+}
+void oracle_csv_free(void* h) { delete static_cast<orc::CsvData*>(h); }
 
 }  // extern "C"

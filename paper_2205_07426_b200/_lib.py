@@ -176,6 +176,15 @@ SIGNATURES = {
     "renyi_ctx_join_local_group": (C.c_int, [_P, _P, C.c_int]),
     "renyi_ctx_rank": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "renyi_kernel_build_gaussian": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)]),
+    "renyi_csv_load": (C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
+    "renyi_csv_parse": (C.c_int, [_P, C.c_char_p, _I64, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
+    "renyi_dataset_shape": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(C.c_int)]),
+    "renyi_dataset_features": (C.c_int, [_P, _P, _D, _I64]),
+    "renyi_dataset_name": (C.c_char_p, [_P, _I64]),
+    "renyi_dataset_label": (C.c_char_p, [_P, _I64]),
+    "renyi_kernel_build_gaussian_dataset": (C.c_int, [_P, _P, C.POINTER(_I64), _I64, C.c_double, C.c_int,
+                                                      C.POINTER(_P)]),
+    "renyi_dataset_destroy": (C.c_int, [_P]),
     "renyi_kernel_build_gaussian_joint": (
         C.c_int,
         [_P, _D, _I64, _I64, _I64, C.c_double, _D, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)],

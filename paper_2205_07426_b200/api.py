@@ -960,3 +960,68 @@ def entropy(x, sigma: float, params: EstimatorParams, precision="fp32",
     check(L.lib().renyi_entropy(ctx.handle, _dptr(xa), xa.shape[0], xa.shape[1], xa.shape[0], sigma,
                                 C.byref(params._c()), PRECISIONS[precision], C.byref(out)))
     return EntropyEstimate._from(out)
+
+
+class Dataset:
+    """renyi::Dataset (proj/include/renyi/features.hpp:12-19) with the n x d features resident on the
+    device; names / labels are host strings. Built by load_csv / parse_csv."""
+
+    def __init__(self, handle, ctx: Context):
+        self._h = handle
+        self.ctx = ctx
+        n, d, hl = C.c_int64(), C.c_int64(), C.c_int()
+        check(L.lib().renyi_dataset_shape(handle, C.byref(n), C.byref(d), C.byref(hl)))
+        self.n, self.d = n.value, d.value
+        lib = L.lib()
+        self.names = [lib.renyi_dataset_name(handle, j).decode("utf-8", errors="surrogateescape")
+                      for j in range(self.d)]
+        self.labels = ([lib.renyi_dataset_label(handle, i).decode("utf-8", errors="surrogateescape")
+                        for i in range(self.n)] if hl.value else [])
+
+    @property
+    def features(self) -> np.ndarray:
+        """n x d fp64 copy of the device-resident features (column-major)."""
+        out = np.empty((self.n, self.d), dtype=np.float64, order="F")
+        if out.size:
+            check(L.lib().renyi_dataset_features(self.ctx.handle, self._h, _dptr(out), max(self.n, 1)))
+        return out
+
+    def kernel(self, spec: GaussianKernel, precision="fp64", columns=None) -> NormalizedKernel:
+        """build_kernel(features[:, columns], spec) straight from the device copy."""
+        h = C.c_void_p()
+        if columns is None:
+            cols, nc = None, 0
+        else:
+            arr = (C.c_int64 * len(columns))(*[int(c) for c in columns])
+            cols, nc = arr, len(columns)
+        check(L.lib().renyi_kernel_build_gaussian_dataset(self.ctx.handle, self._h, cols, nc, spec.sigma,
+                                                          PRECISIONS[precision], C.byref(h)))
+        return NormalizedKernel(h, self.ctx, PRECISIONS[precision])
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                L.lib().renyi_dataset_destroy(h)
+            except Exception:
+                pass
+
+
+def load_csv(path, label_column: Optional[str] = None, ctx: Optional[Context] = None) -> Dataset:
+    """load_csv (proj/src/csv.cpp:63-115): the file is parsed on the device."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    check(L.lib().renyi_csv_load(ctx.handle, str(path).encode(), label_column.encode() if label_column else None,
+                                 C.byref(h)))
+    return Dataset(h, ctx)
+
+
+def parse_csv(text, label_column: Optional[str] = None, source: Optional[str] = None,
+              ctx: Optional[Context] = None) -> Dataset:
+    """load_csv over an in-memory CSV (bytes or str); `source` names it in error messages."""
+    ctx = ctx or default_context()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    check(L.lib().renyi_csv_parse(ctx.handle, data, len(data), label_column.encode() if label_column else None,
+                                  source.encode() if source else None, C.byref(h)))
+    return Dataset(h, ctx)

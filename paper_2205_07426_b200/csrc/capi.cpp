@@ -21,6 +21,10 @@ struct renyi_kernel {
     rb::KernelPtr k;
 };
 
+struct renyi_dataset {
+    std::unique_ptr<rb::Dataset> d;
+};
+
 struct renyi_local_group {
     std::shared_ptr<rb::LocalGroup> g;
 };
@@ -342,6 +346,112 @@ int renyi_kernel_build_gaussian_dev(renyi_ctx* ctx, const double* d_x, int64_t n
         }
         *out = k;
     });
+}
+
+int renyi_csv_load(renyi_ctx* ctx, const char* path, const char* label_column, renyi_dataset** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(path, "path"), need(out, "out");
+        auto* ds = new renyi_dataset;
+        try {
+            ds->d = rb::load_csv_file(ctx->ctx, path, label_column);
+        } catch (...) {
+            delete ds;
+            throw;
+        }
+        *out = ds;
+    });
+}
+
+int renyi_csv_parse(renyi_ctx* ctx, const char* text, int64_t len, const char* label_column, const char* source,
+                    renyi_dataset** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(out, "out");
+        if (len < 0) rb::fail(rb::kInvalidArgument, "negative text length");
+        if (len > 0) need(text, "text");
+        auto* ds = new renyi_dataset;
+        try {
+            ds->d = rb::load_csv_text(ctx->ctx, text, static_cast<size_t>(len), label_column,
+                                      source ? source : "<buffer>");
+        } catch (...) {
+            delete ds;
+            throw;
+        }
+        *out = ds;
+    });
+}
+
+int renyi_dataset_shape(const renyi_dataset* ds, int64_t* n, int64_t* d, int* has_labels) {
+    return guarded([&] {
+        need(ds, "dataset");
+        if (n) *n = ds->d->n;
+        if (d) *d = ds->d->d;
+        if (has_labels) *has_labels = ds->d->labels.empty() ? 0 : 1;
+    });
+}
+
+int renyi_dataset_features(renyi_ctx* ctx, const renyi_dataset* ds, double* x, int64_t ldx) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(ds, "dataset");
+        const int64_t n = ds->d->n, d = ds->d->d;
+        if (n == 0 || d == 0) return;
+        need(x, "features");
+        if (ldx < n) rb::fail(rb::kInvalidArgument, "leading dimension smaller than the sample count");
+        cudaSetDevice(ctx->ctx.device());
+        rb::d2h_2d(ctx->ctx, x, static_cast<size_t>(ldx) * sizeof(double), ds->d->features.as<double>(),
+                   static_cast<size_t>(n) * sizeof(double), static_cast<size_t>(n) * sizeof(double),
+                   static_cast<size_t>(d));
+        ctx->ctx.sync();
+    });
+}
+
+const char* renyi_dataset_name(const renyi_dataset* ds, int64_t j) {
+    if (!ds || j < 0 || j >= static_cast<int64_t>(ds->d->names.size())) return nullptr;
+    return ds->d->names[static_cast<size_t>(j)].c_str();
+}
+
+const char* renyi_dataset_label(const renyi_dataset* ds, int64_t i) {
+    if (!ds || i < 0 || i >= static_cast<int64_t>(ds->d->labels.size())) return nullptr;
+    return ds->d->labels[static_cast<size_t>(i)].c_str();
+}
+
+int renyi_kernel_build_gaussian_dataset(renyi_ctx* ctx, const renyi_dataset* ds, const int64_t* columns,
+                                        int64_t ncols, double sigma, int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(ds, "dataset"), need(out, "out");
+        check_precision(precision);
+        const rb::Dataset& data = *ds->d;
+        auto* k = new renyi_kernel;
+        try {
+            cudaSetDevice(ctx->ctx.device());
+            if (!columns) {
+                k->k = rb::build_gaussian_dev(ctx->ctx, data.features.as<double>(), data.n, data.d, data.n, sigma,
+                                              precision);
+            } else {
+                if (ncols < 1) rb::fail(rb::kInvalidArgument, "need at least one column");
+                rb::DevBuf sel;
+                sel.alloc(static_cast<size_t>(data.n) * static_cast<size_t>(ncols) * sizeof(double));
+                for (int64_t c = 0; c < ncols; ++c) {
+                    if (columns[c] < 0 || columns[c] >= data.d)
+                        rb::fail(rb::kInvalidArgument, "column " + std::to_string(columns[c]) + " out of range");
+                    rb::cuda_check(cudaMemcpyAsync(sel.as<double>() + c * data.n,
+                                                   data.features.as<double>() + columns[c] * data.n,
+                                                   static_cast<size_t>(data.n) * sizeof(double),
+                                                   cudaMemcpyDeviceToDevice, ctx->ctx.stream()),
+                                   "column gather");
+                }
+                k->k = rb::build_gaussian_dev(ctx->ctx, sel.as<double>(), data.n, ncols, data.n, sigma, precision);
+            }
+            ctx->ctx.sync();
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int renyi_dataset_destroy(renyi_dataset* ds) {
+    return guarded([&] { delete ds; });
 }
 
 int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int precision, renyi_kernel** out) {

@@ -158,6 +158,18 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* d_x, int64_t n, int64_t
                              int prec, const double* d_y = nullptr, int64_t dy = 0, int64_t ldy = 0,
                              double sigma_y = 1.0);
 KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec);
+
+// ---- CSV ingestion (renyi::load_csv, proj/src/csv.cpp:63-115; csv.cu) ----
+// Dataset (proj/include/renyi/features.hpp:12-19) with the features resident on the device.
+struct Dataset {
+    int64_t n = 0, d = 0;
+    DevBuf features;  // n x d, column-major fp64
+    std::vector<std::string> names, labels;
+};
+// text: the file's bytes (host); source names the input in messages ('path': ...)
+std::unique_ptr<Dataset> load_csv_text(Context& ctx, const char* text, size_t len, const char* label_column,
+                                       const std::string& source);
+std::unique_ptr<Dataset> load_csv_file(Context& ctx, const std::string& path, const char* label_column);
 KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix& b);
 void download(Context& ctx, const KernelMatrix& k, double* out_colmajor);
 

@@ -27,6 +27,17 @@ int main() {
         p.bounds.v = 1.0;
         const EntropyEstimate e = estimate(ctx, k, p);
         std::printf("entropy %.12f trace %.12f\n", e.entropy, e.trace_estimate);
+        // load_csv on the device feeding build_kernel (proj/include/renyi/csv.hpp:14-15)
+        const std::string path = "/tmp/renyi_example_host.csv";
+        if (FILE* f = std::fopen(path.c_str(), "wb")) {
+            std::fprintf(f, "a,b,class\n");
+            for (int i = 0; i < 200; ++i) std::fprintf(f, "%g,%g,%s\n", std::sin(0.1 * i), std::cos(0.3 * i), i % 2 ? "x" : "y");
+            std::fclose(f);
+        }
+        const Dataset data = load_csv(ctx, path, std::string("class"));
+        if (data.n() != 200 || data.d() != 2 || data.labels.size() != 200 || data.names[1] != "b") return 3;
+        const EntropyEstimate e2 = estimate(ctx, data.kernel(ctx, GaussianKernel{1.0}, Precision::fp32), p);
+        std::printf("csv entropy %.12f\n", e2.entropy);
         return 0;
     } catch (const error& e) {
         std::printf("error kind=%d usage=%d: %s\n", static_cast<int>(e.kind()), e.is_usage(), e.what());
