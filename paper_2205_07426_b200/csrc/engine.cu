@@ -47,8 +47,14 @@ void d2h_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spit
 
 // ---------------------------------------------------------------- caching pool
 namespace {
+struct PoolBlock {
+    void* p;
+    cudaStream_t stream;  // stream of the thread that freed it (nullptr: idle when freed)
+    cudaEvent_t ready;    // recorded on `stream` at the free
+};
 std::mutex g_pool_mu;
-std::multimap<std::pair<int, size_t>, void*> g_pool;  // (device, capacity) -> block
+std::multimap<std::pair<int, size_t>, PoolBlock> g_pool;  // (device, capacity) -> block
+thread_local cudaStream_t t_stream = nullptr;
 
 size_t pool_round(size_t bytes) {
     const size_t g = bytes >= (size_t(1) << 21) ? (size_t(1) << 21) : 512;
@@ -56,19 +62,38 @@ size_t pool_round(size_t bytes) {
 }
 }  // namespace
 
+void set_current_stream(cudaStream_t s) { t_stream = s; }
+
 void* pool_alloc(size_t bytes, size_t* capacity, int* device) {
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     const size_t want = pool_round(bytes);
     {
         std::lock_guard<std::mutex> lk(g_pool_mu);
-        auto it = g_pool.lower_bound({dev, want});
-        if (it != g_pool.end() && it->first.first == dev && it->first.second <= 2 * want + (size_t(1) << 21)) {
-            void* p = it->second;
-            *capacity = it->first.second;
+        const size_t cap_max = 2 * want + (size_t(1) << 21);
+        auto first = g_pool.lower_bound({dev, want});
+        auto pick = g_pool.end();
+        // prefer a block this stream freed itself (stream order makes it reusable at once)
+        for (auto it = first; it != g_pool.end() && it->first.first == dev && it->first.second <= cap_max; ++it) {
+            if (pick == g_pool.end()) pick = it;
+            if (it->second.stream == t_stream) {
+                pick = it;
+                break;
+            }
+        }
+        if (pick != g_pool.end()) {
+            PoolBlock b = pick->second;
+            *capacity = pick->first.second;
             *device = dev;
-            g_pool.erase(it);
-            return p;
+            g_pool.erase(pick);
+            if (b.ready) {
+                if (b.stream != t_stream) {  // order this stream after the freeing stream's queued work
+                    if (t_stream) cudaStreamWaitEvent(t_stream, b.ready, 0);
+                    else cudaEventSynchronize(b.ready);
+                }
+                cudaEventDestroy(b.ready);
+            }
+            return b.p;
         }
     }
     void* p = nullptr;
@@ -86,8 +111,27 @@ void* pool_alloc(size_t bytes, size_t* capacity, int* device) {
 
 void pool_free(void* p, size_t capacity, int device) {
     if (!p) return;
+    PoolBlock b{p, t_stream, nullptr};
+    if (t_stream) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != device) cudaSetDevice(device);
+        if (cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming) != cudaSuccess) {
+            (void)cudaGetLastError();
+            b.ready = nullptr;
+        } else if (cudaEventRecord(b.ready, t_stream) != cudaSuccess) {
+            (void)cudaGetLastError();
+            cudaEventDestroy(b.ready);
+            b.ready = nullptr;
+        }
+        if (!b.ready) {  // could not tag the free: make the block idle before it can be reused
+            cudaDeviceSynchronize();
+            b.stream = nullptr;
+        }
+        if (cur != device) cudaSetDevice(cur);
+    }
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    g_pool.insert({{device, capacity}, p});
+    g_pool.insert({{device, capacity}, b});
 }
 
 void pool_release_all() {
@@ -96,7 +140,11 @@ void pool_release_all() {
     cudaGetDevice(&cur);
     for (auto& kv : g_pool) {
         cudaSetDevice(kv.first.first);
-        cudaFree(kv.second);
+        if (kv.second.ready) {
+            cudaEventSynchronize(kv.second.ready);
+            cudaEventDestroy(kv.second.ready);
+        }
+        cudaFree(kv.second.p);
     }
     g_pool.clear();
     cudaSetDevice(cur);
@@ -147,6 +195,10 @@ Context::Context(int device) : device_(device) {
 
 Context::~Context() {
     cudaSetDevice(device_);
+    // the members' scratch returns to the pool after this body: the stream is drained and no
+    // longer tags those frees
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (t_stream == stream_) t_stream = nullptr;
     if (t0_) cudaEventDestroy(t0_);
     if (t1_) cudaEventDestroy(t1_);
     for (auto& e : events_) {

@@ -26,9 +26,14 @@ void cuda_check(cudaError_t e, const char* what);
 // Device memory comes from a process-wide caching pool (per device): n x n kernel
 // storage, panels and scratch are reused across estimates instead of paying
 // cudaMalloc/cudaFree (which synchronise the device) inside the estimator loop.
+// Blocks are stream-ordered: a block freed while the thread's current engine stream may
+// still have queued work is handed to another stream only behind an event recorded at the
+// free (cudaStreamWaitEvent), so ranks / contexts on other streams never race on it.
 void* pool_alloc(size_t bytes, size_t* capacity, int* device);
 void pool_free(void* p, size_t capacity, int device);
 void pool_release_all();  // returns every cached block to the driver
+// the engine stream of the calling thread (set by Context::stream(); tags pool frees)
+void set_current_stream(cudaStream_t s);
 
 class DevBuf {
 public:
@@ -80,7 +85,10 @@ public:
     explicit Context(int device);
     ~Context();
     int device() const { return device_; }
-    cudaStream_t stream() const { return stream_; }
+    cudaStream_t stream() const {
+        set_current_stream(stream_);
+        return stream_;
+    }
     int sms() const { return sms_; }
     void sync();
 
