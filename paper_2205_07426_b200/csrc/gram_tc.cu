@@ -11,8 +11,9 @@
 // the K·2^14 hi/lo split, and writes the tile and (through shared memory) its mirror: only the
 // upper-triangle tiles are computed.
 //
-// Warp roles: 0 TMA (A/B K sub-tiles, 4-stage ring), 1 MMA issuer (M=128, N=128, K=8 tf32
-// steps into one of two TMEM accumulators), 2-9 epilogue (two warpgroups: column halves).
+// Warp roles: 0 TMA (A/B K sub-tiles, 2-stage ring), 1 MMA issuer (M=128, N=128, K=8 tf32
+// steps into one of two TMEM accumulators), 2-9 epilogue (two warpgroups: column halves) whose
+// staged tiles leave through TMA stores.
 // Persistent CTAs walk the upper-triangle tiles row-major (consecutive tiles share A in L2).
 #include <algorithm>
 #include <cmath>
@@ -34,10 +35,14 @@ constexpr int KS = 32;            // fp32 per K sub-tile: one 128-byte SW128 row
 constexpr int kGStages = 2;
 constexpr int kGThreads = 320;
 constexpr int kSub = GT * KS * 4;  // 16 KB per operand sub-tile
-constexpr int kTT = GT * 2 + 16;   // staged half tile: row pitch in bytes (padded)
-constexpr int kPlane = GT * kTT;   // one staged [128][128] fp16 plane
+constexpr int kPlane = GT * GT * 2;  // one staged [128][128] fp16 plane: two 128B-swizzled boxes of 64 columns
 // ring | D (tile, row-major: hi, lo) | T (transposed tile: hi, lo)
 constexpr int kGSmem = kGStages * 2 * kSub + 4 * kPlane + 1024;
+
+// byte offset of fp16 element (r, c) in a staged plane (TMA SWIZZLE_128B boxes of 128 rows x 64 columns)
+__device__ __forceinline__ uint32_t sw_off(int r, int c) {
+    return static_cast<uint32_t>((c >> 6) * (GT * 128) + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) + ((c & 7) << 1));
+}
 
 struct GtArgs {
     int64_t nb, tiles;  // column blocks; tiles (upper triangle, or shard row blocks x nb)
@@ -76,12 +81,10 @@ __device__ __forceinline__ void map_tile(const GtArgs& a, int64_t t, int64_t* bi
     }
 }
 
-__device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
 
 __global__ void __launch_bounds__(kGThreads, 1)
-    gram_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, GtArgs args) {
+    gram_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo, GtArgs args) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_base_smem;
@@ -89,12 +92,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
     const uint32_t ring = base_u32;                            // [stage][A | B]
-    uint8_t* dd = base + kGStages * 2 * kSub;                  // D: [hi | lo][128 rows][kTT]
-    uint8_t* tt = dd + 2 * kPlane;                             // T: [hi | lo][128 cols][kTT]
+    uint8_t* dd = base + kGStages * 2 * kSub;                  // D: [hi | lo] staged planes (sw_off layout)
+    uint8_t* tt = dd + 2 * kPlane;                             // T: [hi | lo], the transposed tile
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&map_a);
         prefetch_tmap(&map_b);
+        prefetch_tmap(&map_hi);
+        prefetch_tmap(&map_lo);
         for (int s = 0; s < kGStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -160,32 +165,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
     } else {
         // ---------------- epilogue: warps 2-9, columns [64h, 64h+64) of the tile ----------------
-        // Phase A: TMEM -> K -> fp16 hi/lo, staged row-major (D) and transposed (T) in shared memory.
-        // Phase B: coalesced 16-byte stores of D (rows of block bi) and T (rows of block bj, the
-        // mirror tile); on a diagonal tile the lower triangle of D is first replaced from T so A is
-        // exactly symmetric like the reference's mirrored Gram (ops.cpp:9-20).
+        // Phase A: TMEM -> K -> fp16 hi/lo, staged row-major (D) and transposed (T) in shared memory in
+        // the TMA 128B-swizzled box layout (conflict-free row writes and transposed 2-byte writes).
+        // Phase B: one thread stores the boxes with TMA (full-line writes; the global writes drain
+        // asynchronously while the next tile is computed). On a diagonal tile the lower triangle of D
+        // is first replaced from T so A is exactly symmetric like the reference's mirrored Gram
+        // (ops.cpp:9-20).
         const int h = (warp - 2) >> 2, q = warp & 3;
         const int row = q * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         const float l2e = 1.4426950408889634f, scale = static_cast<float>(kSplitScale);
         const int et = threadIdx.x - 2 * kWarp;  // 0..255
         uint32_t lt = 0;
-        auto store_plane_rows = [&](const uint8_t* src, __half* dst, int64_t grow0, int64_t gcol0) {
-            // 128 rows x 16 chunks of 16 bytes; consecutive threads take consecutive chunks of a row
-            for (int qq = et; qq < GT * 16; qq += 256) {
-                const int r = qq >> 4, c = qq & 15;
-                const int64_t gr = grow0 + r, gc = gcol0 + 8 * c;
-                if (gr >= args.row_end) continue;
-                const uint4 v = *reinterpret_cast<const uint4*>(src + r * kTT + c * 16);
-                __half* out = dst + (gr - args.row0) * args.ld + gc;
-                if (gc + 8 <= args.n) {
-                    st_global_v4(out, v.x, v.y, v.z, v.w);
-                } else {
-                    const __half* hv = reinterpret_cast<const __half*>(&v);
-                    for (int e = 0; e < 8 && gc + e < args.n; ++e) out[e] = hv[e];
-                }
-            }
-        };
         for (int64_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++lt) {
             int64_t bi, bj;
             map_tile(args, t, &bi, &bj);
@@ -223,20 +214,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         const __half2 ll = __floats2half2_rn(kk[0] - back.x, kk[1] - back.y);
                         ph[(e + u) / 2] = *reinterpret_cast<const uint32_t*>(&hh);
                         pl[(e + u) / 2] = *reinterpret_cast<const uint32_t*>(&ll);
-                        const int c = h * 64 + c0 + e + u;  // transposed copy
-                        __half* th = reinterpret_cast<__half*>(tt + c * kTT) + row;
-                        __half* tl = reinterpret_cast<__half*>(tt + kPlane + c * kTT) + row;
-                        th[0] = __low2half(hh);
-                        tl[0] = __low2half(ll);
-                        th[kTT / 2] = __high2half(hh);
-                        tl[kTT / 2] = __high2half(ll);
+                        const int c = h * 64 + c0 + e + u;  // transposed copy: T[c][row], T[c + 1][row]
+                        *reinterpret_cast<__half*>(tt + sw_off(c, row)) = __low2half(hh);
+                        *reinterpret_cast<__half*>(tt + kPlane + sw_off(c, row)) = __low2half(ll);
+                        *reinterpret_cast<__half*>(tt + sw_off(c + 1, row)) = __high2half(hh);
+                        *reinterpret_cast<__half*>(tt + kPlane + sw_off(c + 1, row)) = __high2half(ll);
                     }
                 }
-                uint8_t* drow = dd + row * kTT + (h * 64 + c0) * 2;
-                *reinterpret_cast<uint4*>(drow) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-                *reinterpret_cast<uint4*>(drow + 16) = make_uint4(ph[4], ph[5], ph[6], ph[7]);
-                *reinterpret_cast<uint4*>(drow + kPlane) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-                *reinterpret_cast<uint4*>(drow + kPlane + 16) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
+                const int cc = h * 64 + c0;
+                *reinterpret_cast<uint4*>(dd + sw_off(row, cc)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+                *reinterpret_cast<uint4*>(dd + sw_off(row, cc + 8)) = make_uint4(ph[4], ph[5], ph[6], ph[7]);
+                *reinterpret_cast<uint4*>(dd + kPlane + sw_off(row, cc)) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+                *reinterpret_cast<uint4*>(dd + kPlane + sw_off(row, cc + 8)) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
             }
             tc_fence_before();
             __syncwarp();
@@ -246,21 +235,35 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 for (int idx = et; idx < GT * GT; idx += 256) {
                     const int i = idx >> 7, j = idx & 127;
                     if (j < i) {
-                        reinterpret_cast<__half*>(dd + i * kTT)[j] = reinterpret_cast<const __half*>(tt + i * kTT)[j];
-                        reinterpret_cast<__half*>(dd + kPlane + i * kTT)[j] =
-                            reinterpret_cast<const __half*>(tt + kPlane + i * kTT)[j];
+                        const uint32_t o = sw_off(i, j);
+                        *reinterpret_cast<__half*>(dd + o) = *reinterpret_cast<const __half*>(tt + o);
+                        *reinterpret_cast<__half*>(dd + kPlane + o) = *reinterpret_cast<const __half*>(tt + kPlane + o);
                     }
                 }
                 asm volatile("bar.sync 1, 256;" ::: "memory");
             }
-            store_plane_rows(dd, args.hi, bi * GT, bj * GT);
-            store_plane_rows(dd + kPlane, args.lo, bi * GT, bj * GT);
-            if (!diag && !args.rect) {
-                store_plane_rows(tt, args.hi, bj * GT, bi * GT);
-                store_plane_rows(tt + kPlane, args.lo, bj * GT, bi * GT);
+            fence_proxy_async_smem();  // this thread's staging writes -> visible to the TMA engine
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (et == 0) {
+                const int ri = static_cast<int>(bi * GT - args.row0), ci = static_cast<int>(bj * GT);
+                for (int b = 0; b < 2; ++b) {
+                    tma_store_2d(&map_hi, dd + b * (GT * 128), ci + 64 * b, ri);
+                    tma_store_2d(&map_lo, dd + kPlane + b * (GT * 128), ci + 64 * b, ri);
+                }
+                if (!diag && !args.rect) {  // the mirror tile (bj, bi)
+                    for (int b = 0; b < 2; ++b) {
+                        tma_store_2d(&map_hi, tt + b * (GT * 128), static_cast<int>(bi * GT) + 64 * b,
+                                     static_cast<int>(bj * GT));
+                        tma_store_2d(&map_lo, tt + kPlane + b * (GT * 128), static_cast<int>(bi * GT) + 64 * b,
+                                     static_cast<int>(bj * GT));
+                    }
+                }
+                bulk_commit_group();
+                bulk_wait_read_all();  // staging reusable; the global writes complete in the background
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // D, T reusable by the next tile
         }
+        if (et == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -368,6 +371,17 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             e = cudaErrorInvalidValue;
     }
+    CUtensorMap mhi, mlo;  // outputs: fp16 [rows][ld] planes, 128-row x 64-column boxes, 128B swizzle
+    for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.rows)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ld) * 2};
+        cuuint32_t box[2] = {64, GT};
+        cuuint32_t estr[2] = {1, 1};
+        if (enc(s == 0 ? &mhi : &mlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, s == 0 ? static_cast<void*>(hi) : lo, dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            e = cudaErrorInvalidValue;
+    }
     if (e == cudaSuccess) e = ensure_smem_attr(reinterpret_cast<const void*>(gram_tc_kernel), kGSmem);
     if (e == cudaSuccess) {
         GtArgs a;
@@ -385,7 +399,7 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t grid = std::min<int64_t>(sms, a.tiles);
         if (grid > 0) {
-            gram_tc_kernel<<<static_cast<unsigned>(grid), kGThreads, kGSmem, stream>>>(ma, mb, a);
+            gram_tc_kernel<<<static_cast<unsigned>(grid), kGThreads, kGSmem, stream>>>(ma, mb, mhi, mlo, a);
             e = cudaGetLastError();
         }
     }
