@@ -12,7 +12,7 @@
 // upper-triangle tiles are computed.
 //
 // Warp roles: 0 TMA (A/B K sub-tiles, 2-stage ring), 1 MMA issuer (M=128, N=128, K=8 tf32
-// steps into one of two TMEM accumulators), 2-9 epilogue (two warpgroups: column halves) whose
+// steps into one of two TMEM accumulators), 2-17 epilogue (four warpgroups: column quarters) whose
 // staged tiles leave through TMA stores.
 // Persistent CTAs walk the upper-triangle tiles row-major (consecutive tiles share A in L2).
 #include <algorithm>
@@ -33,7 +33,8 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
 constexpr int GT = 128;           // tile (rows and columns)
 constexpr int KS = 32;            // fp32 per K sub-tile: one 128-byte SW128 row
 constexpr int kGStages = 2;
-constexpr int kGThreads = 320;
+constexpr int kGEpiWarps = 16;  // epilogue warps: 4 groups of 32 columns x 4 TMEM lane quarters
+constexpr int kGThreads = 32 * (2 + kGEpiWarps);
 constexpr int kSub = GT * KS * 4;  // 16 KB per operand sub-tile
 constexpr int kPlane = GT * GT * 2;  // one staged [128][128] fp16 plane: two 128B-swizzled boxes of 64 columns
 // ring | D (tile, row-major: hi, lo) | T (transposed tile: hi, lo)
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 8);  // one arrival per epilogue warp
+            mbar_init(&acc_empty[b], kGEpiWarps);  // one arrival per epilogue warp
         }
         fence_barrier_init();
     }
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
         }
     } else {
-        // ---------------- epilogue: warps 2-9, columns [64h, 64h+64) of the tile ----------------
+        // ---------------- epilogue: warps 2-17, columns [32h, 32h+32) of the tile ----------------
         // Phase A: TMEM -> K -> fp16 hi/lo, staged row-major (D) and transposed (T) in shared memory in
         // the TMA 128B-swizzled box layout (conflict-free row writes and transposed 2-byte writes).
         // Phase B: one thread stores the boxes with TMA (full-line writes; the global writes drain
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         const int row = q * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         const float l2e = 1.4426950408889634f, scale = static_cast<float>(kSplitScale);
-        const int et = threadIdx.x - 2 * kWarp;  // 0..255
+        const int et = threadIdx.x - 2 * kWarp;  // 0..511
         uint32_t lt = 0;
         for (int64_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++lt) {
             int64_t bi, bj;
@@ -187,11 +188,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
             mbar_wait(&acc_full[buf], (lt >> 1) & 1u);
             tc_fence_after();
 #pragma unroll 1
-            for (int c0 = 0; c0 < 64; c0 += 16) {
+            for (int c0 = 0; c0 < 32; c0 += 16) {
                 float sv[16];
-                tmem_ld16(tmem + lane_off + buf * GT + h * 64 + c0, sv);
+                tmem_ld16(tmem + lane_off + buf * GT + h * 32 + c0, sv);
                 tmem_ld_wait();
-                const float4* sqj4 = reinterpret_cast<const float4*>(args.sq + bj * GT + h * 64 + c0);
+                const float4* sqj4 = reinterpret_cast<const float4*>(args.sq + bj * GT + h * 32 + c0);
                 uint32_t ph[8], pl[8];
 #pragma unroll
                 for (int e = 0; e < 16; e += 4) {
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                             const float arg = fminf(l2e * (2.f * sv[e + u + w] - sqi - sjv[u + w]), 0.f);
                             float kv;
                             asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(kv) : "f"(arg));
-                            if (diag && h * 64 + c == row) kv = 1.0f;  // K_ii = 1 exactly (ops.cpp:12)
+                            if (diag && h * 32 + c == row) kv = 1.0f;  // K_ii = 1 exactly (ops.cpp:12)
                             kk[w] = kv * scale;
                         }
                         const __half2 hh = __floats2half2_rn(kk[0], kk[1]);
@@ -214,14 +215,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         const __half2 ll = __floats2half2_rn(kk[0] - back.x, kk[1] - back.y);
                         ph[(e + u) / 2] = *reinterpret_cast<const uint32_t*>(&hh);
                         pl[(e + u) / 2] = *reinterpret_cast<const uint32_t*>(&ll);
-                        const int c = h * 64 + c0 + e + u;  // transposed copy: T[c][row], T[c + 1][row]
+                        const int c = h * 32 + c0 + e + u;  // transposed copy: T[c][row], T[c + 1][row]
                         *reinterpret_cast<__half*>(tt + sw_off(c, row)) = __low2half(hh);
                         *reinterpret_cast<__half*>(tt + kPlane + sw_off(c, row)) = __low2half(ll);
                         *reinterpret_cast<__half*>(tt + sw_off(c + 1, row)) = __high2half(hh);
                         *reinterpret_cast<__half*>(tt + kPlane + sw_off(c + 1, row)) = __high2half(ll);
                     }
                 }
-                const int cc = h * 64 + c0;
+                const int cc = h * 32 + c0;
                 *reinterpret_cast<uint4*>(dd + sw_off(row, cc)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
                 *reinterpret_cast<uint4*>(dd + sw_off(row, cc + 8)) = make_uint4(ph[4], ph[5], ph[6], ph[7]);
                 *reinterpret_cast<uint4*>(dd + kPlane + sw_off(row, cc)) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
@@ -230,9 +231,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM buffer free for the tile after next
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, 512;" ::: "memory");
             if (diag && !args.rect) {  // D[i][j] <- K(j, i) = T[i][j] below the diagonal
-                for (int idx = et; idx < GT * GT; idx += 256) {
+                for (int idx = et; idx < GT * GT; idx += 32 * kGEpiWarps) {
                     const int i = idx >> 7, j = idx & 127;
                     if (j < i) {
                         const uint32_t o = sw_off(i, j);
@@ -240,10 +241,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         *reinterpret_cast<__half*>(dd + kPlane + o) = *reinterpret_cast<const __half*>(tt + kPlane + o);
                     }
                 }
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                asm volatile("bar.sync 1, 512;" ::: "memory");
             }
             fence_proxy_async_smem();  // this thread's staging writes -> visible to the TMA engine
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, 512;" ::: "memory");
             if (et == 0) {
                 const int ri = static_cast<int>(bi * GT - args.row0), ci = static_cast<int>(bj * GT);
                 for (int b = 0; b < 2; ++b) {
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 bulk_commit_group();
                 bulk_wait_read_all();  // staging reusable; the global writes complete in the background
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // D, T reusable by the next tile
+            asm volatile("bar.sync 1, 512;" ::: "memory");  // D, T reusable by the next tile
         }
         if (et == 0) bulk_wait_all();
     }
