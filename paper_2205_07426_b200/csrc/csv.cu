@@ -14,9 +14,10 @@
 //   K4 csv_records      one thread per record: blank-line rule and field-count check;
 //   K5                  exclusive scan of the data-row flags (cub);
 //   K6 csv_parse        one thread per cell: quote/CR removal on the fly and a strtod-exact parse
-//                       (grammar of glibc strtod in the C locale; decimal values through exact
-//                       big-decimal shifting, hex floats with round-to-nearest-even, inf/nan with
-//                       glibc's payload rule) straight into the column-major n x d fp64 matrix.
+//                       (grammar of glibc strtod in the C locale; decimal values by Clinger's exact
+//                       path, Eisel-Lemire, and exact big-decimal shifting for what those leave
+//                       undecided; hex floats with round-to-nearest-even; inf/nan with glibc's
+//                       payload rule) straight into the column-major n x d fp64 matrix.
 // Errors keep the reference's first-failure order: the smallest (row, column) key wins, a
 // row's field-count error (column 0) before its cells. Header names, the label column and error
 // texts are strings, cleaned on the host from the caller's buffer by the same state machine.
@@ -28,6 +29,7 @@
 #include <limits>
 
 #include "engine.h"
+#include "pow10_table.h"
 
 namespace rb {
 
@@ -444,10 +446,44 @@ __device__ __forceinline__ bool is_nchar(int c) {
     return (c >= '0' && c <= '9') || (c >= 'A' && c <= 'Z') || (c >= 'a' && c <= 'z') || c == '_';
 }
 
+// Eisel-Lemire: man x 10^e10 -> binary64 bits when the 128-bit product of the normalised mantissa and
+// the truncated 128-bit mantissa of 10^e10 (pow10_table.h) decides the rounding. Returns false on a
+// possible ambiguity, a subnormal or overflowing result, or e10 outside the table: the caller then
+// takes the exact big-decimal path.
+__device__ bool eisel_lemire(uint64_t man, int64_t e10, bool neg, uint64_t* bits) {
+    if (man == 0 || e10 < kPow10Min || e10 > kPow10Max) return false;
+    const int clz = __clzll(static_cast<long long>(man));
+    man <<= clz;
+    uint64_t ret_exp2 = static_cast<uint64_t>(((217706 * e10) >> 16) + 64 + 1023) - static_cast<uint64_t>(clz);
+    const uint64_t* p = kPow10[e10 - kPow10Min];
+    uint64_t x_hi = __umul64hi(man, p[1]), x_lo = man * p[1];
+    if ((x_hi & 0x1FF) == 0x1FF && x_lo + man < man) {  // the low product could carry into the top bits
+        const uint64_t y_hi = __umul64hi(man, p[0]), y_lo = man * p[0];
+        uint64_t m_hi = x_hi, m_lo = x_lo + y_hi;
+        if (m_lo < x_lo) ++m_hi;
+        if ((m_hi & 0x1FF) == 0x1FF && m_lo + 1 == 0 && y_lo + man < man) return false;
+        x_hi = m_hi, x_lo = m_lo;
+    }
+    const uint64_t msb = x_hi >> 63;
+    uint64_t mant = x_hi >> (msb + 9);
+    ret_exp2 -= 1 ^ msb;
+    if (x_lo == 0 && (x_hi & 0x1FF) == 0 && (mant & 3) == 1) return false;  // exactly halfway: undecided
+    mant += mant & 1;
+    mant >>= 1;
+    if (mant >> 53) {
+        mant >>= 1;
+        ++ret_exp2;
+    }
+    if (ret_exp2 - 1 >= 0x7FF - 1) return false;  // subnormal or overflow
+    *bits = (ret_exp2 << 52) | (mant & 0x000FFFFFFFFFFFFFull) | (neg ? (uint64_t(1) << 63) : 0);
+    return true;
+}
+
 // Decimal body (digits, optional '.', optional exponent) followed by trailing spaces and the end of the
 // cell. c is the current character; zero0 = a leading '0' was already consumed. Values with at most 15
-// significant digits and |e10| <= 22 are exact in one double operation (Clinger); everything else is
-// re-read into the big decimal and converted exactly.
+// significant digits and |e10| <= 22 are exact in one double operation (Clinger); up to 19 digits go
+// through Eisel-Lemire, longer ones through Eisel-Lemire on both truncation brackets (w, w + 1);
+// whatever stays undecided is re-read into the big decimal and converted exactly.
 __device__ bool parse_decimal(CStrReader& in, int c, bool zero0, bool neg, const uint8_t* text, int64_t s,
                               int64_t e, double* out, Dec& dec) {
     int64_t nd_all = 0, dp = 0, ex = 0;
@@ -470,7 +506,7 @@ __device__ bool parse_decimal(CStrReader& in, int c, bool zero0, bool neg, const
         if (c == '0') {
             ++pend;
         } else {
-            if (wd + pend + 1 > 19) {
+            if (many || wd + pend + 1 > 19) {  // w keeps the leading digits only; later ones are dropped
                 many = true;
             } else {
                 for (int z = 0; z < pend; ++z) w *= 10;
@@ -501,7 +537,9 @@ __device__ bool parse_decimal(CStrReader& in, int c, bool zero0, bool neg, const
         *out = neg ? -0.0 : 0.0;
         return true;
     }
-    const int64_t e10 = dp + ex - sig;  // value = w x 10^e10 when !many
+    // value = w x 10^e10 (w holds wd digits: all significant ones when !many, else the leading wd of them
+    // and the value lies strictly between w x 10^e10 and (w + 1) x 10^e10)
+    const int64_t e10 = dp + ex - wd;
     if (!many && sig <= 15 && e10 >= -22 && e10 <= 22) {
         constexpr double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                     1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
@@ -509,6 +547,15 @@ __device__ bool parse_decimal(CStrReader& in, int c, bool zero0, bool neg, const
         v = e10 >= 0 ? v * p10[e10] : v / p10[-e10];
         *out = neg ? -v : v;
         return true;
+    }
+    {
+        uint64_t b0 = 0, b1 = 1;
+        const bool ok0 = eisel_lemire(w, e10, neg, &b0);
+        const bool ok1 = many && ok0 && eisel_lemire(w + 1, e10, neg, &b1);
+        if (ok0 && (!many || (ok1 && b0 == b1))) {
+            memcpy(out, &b0, 8);
+            return true;
+        }
     }
     // exact path: the significant digits (first Dec::kMax kept, the rest only as a sticky flag)
     CStrReader in2{CleanReader{text, s, e, 0}};

@@ -140,3 +140,28 @@ def test_large_file_matches_oracle(R, orc):
     dev, ref = both(R, orc, text, "class")
     assert_same(dev, ref, "<large>")
     assert np.array_equal(dev[1]["features"], x)  # %.17g round-trips
+
+
+def test_decimal_paths_bit_exact_at_scale(R, orc):
+    """Clinger / Eisel-Lemire / bracketed Eisel-Lemire / big-decimal paths against glibc strtod on
+    ~300k decimal cells: random binary64 values printed with 15-25 significant digits, random
+    16-40 digit strings over the whole exponent range (subnormals, overflow), and near-ties."""
+    rng = np.random.default_rng(17)
+    bits = rng.integers(0, 2 ** 63, 120_000, dtype=np.uint64) | (rng.integers(0, 2, 120_000, dtype=np.uint64) << 63)
+    vals = bits.view(np.float64)
+    vals = vals[np.isfinite(vals)]
+    fmts = ["%.15g", "%.16g", "%.17g", "%.18g", "%.19g", "%.20g", "%.25e"]
+    cells = [fmts[i % len(fmts)] % v for i, v in enumerate(vals)]
+    digits = rng.integers(0, 10, (120_000, 40))
+    lens = rng.integers(16, 41, 120_000)
+    exps = rng.integers(-345, 320, 120_000)
+    for i in range(120_000):
+        ds = "".join(map(str, digits[i, : lens[i]])).lstrip("0") or "0"
+        cells.append(f"{ds[0]}.{ds[1:]}e{exps[i] - len(ds) + 1}")
+    g = random.Random(23)
+    from csv_cases import _midpoint_text
+    cells += [_midpoint_text(g) for _ in range(20_000)]
+    text = "v\n" + "\n".join(cells) + "\n"
+    dev, ref = both(R, orc, text)
+    assert_same(dev, ref, "<decimal paths>")
+    assert dev[1]["n"] == len(cells)
