@@ -85,3 +85,29 @@ def test_generated_files_parse(orc):
             continue
         assert d["features"].shape == (d["n"], d["d"])
     assert number_text(random.Random(1))  # generator smoke
+
+
+def test_pow10_table_matches_generator():
+    """csrc/pow10_table.h (Eisel-Lemire table of the device CSV reader) is exactly what
+    gen_pow10.py computes: floor of the top 128 bits of 10^e, leading bit set."""
+    import re
+    from pathlib import Path
+
+    from paper_2205_07426_b200.gen_pow10 import HI, LO, mantissa128
+
+    text = (Path(__file__).resolve().parents[1] / "paper_2205_07426_b200" / "csrc" / "pow10_table.h").read_text()
+    rows = re.findall(r"\{0x([0-9a-f]{16})ull, 0x([0-9a-f]{16})ull\},\s*// 1e(-?\d+)", text)
+    assert len(rows) == HI - LO + 1
+    for lo, hi, e in rows:
+        m = (int(hi, 16) << 64) | int(lo, 16)
+        e = int(e)
+        assert m == mantissa128(e)
+        # m = floor(10^e * 2^k) with k = 127 - floor(log2 10^e), checked in integers
+        if e >= 0:
+            v = 10 ** e
+            k = 127 - (v.bit_length() - 1)
+            assert (m << max(-k, 0)) <= (v << max(k, 0)) < ((m + 1) << max(-k, 0))
+        else:
+            d = 10 ** (-e)  # never a power of two: floor(log2(1/d)) = -bit_length(d)
+            k = 127 + d.bit_length()
+            assert m * d <= (1 << k) < (m + 1) * d
