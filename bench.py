@@ -125,7 +125,8 @@ class ClockSampler:
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "clocks.mem,temperature.gpu,temperature.memory")
 
     def __init__(self, index: int, period_ms: int = 200):
         self.index = index
@@ -171,8 +172,13 @@ class ClockSampler:
         under_load = [c for c in sm if c > 0.5 * mx] or sm
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(under_load), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(num(r[3]) for r in rows)}
+        out = {"sm_mhz": statistics.median(under_load), "sm_max_mhz": mx, "reasons": reasons,
+               "samples": len(rows), "power_w_max": max(num(r[3]) for r in rows)}
+        if all(len(r) >= 12 for r in rows):  # HBM clock and temperatures (context for bandwidth-bound runs)
+            out["mem_mhz"] = statistics.median(num(r[9]) for r in rows)
+            out["gpu_temp_c_max"] = max(num(r[10]) for r in rows)
+            out["mem_temp_c_max"] = max(num(r[11]) for r in rows)
+        return out
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle restatement)
