@@ -191,16 +191,13 @@ __device__ __forceinline__ void exp16(const float* sv, float2 c2v, int col0, int
 // 32 columns of S (TMEM, two pipelined x16 reads) -> 16 fp16 pairs of P written back to TMEM at wr
 template <bool DIAG>
 __device__ __forceinline__ void exp_store32(uint32_t rd, uint32_t wr, float2 c2v, int col0, int row) {
-    float s0[16], s1[16];
-    uint32_t pk0[8], pk1[8];
-    tmem_ld16(rd, s0);
+    float sv[32];
+    uint32_t pk[16];
+    tmem_ld32(rd, sv);  // one 32-column read
     tmem_ld_wait();
-    tmem_ld16(rd + 16, s1);
-    exp16<DIAG>(s0, c2v, col0, row, pk0);
-    tmem_st8(wr, pk0);  // over columns already read; overlaps the second half's exp work
-    tmem_ld_wait();
-    exp16<DIAG>(s1, c2v, col0 + 16, row, pk1);
-    tmem_st8(wr + 8, pk1);
+    exp16<DIAG>(sv, c2v, col0, row, pk);
+    exp16<DIAG>(sv + 16, c2v, col0 + 16, row, pk + 8);
+    tmem_st16(wr, pk);  // one 16-column write of the fp16 pairs, over columns already read
 }
 
 // One thread's CW columns of S -> P (P over the first CW/2 of the columns it read)
