@@ -79,3 +79,24 @@ def test_config5_full_size_matrix_free(R):
         assert np.max(np.abs(cols[:, c] - ref)) <= 1e-3 * ref.max(), j
         assert abs(cols[j, c] - 1.0 / n) <= 1e-3 / n
     check_properties(R, k, n, 1e-3, 9)
+
+
+def test_config4_mi_sharded_matches_single_rank_at_full_size(R):
+    """The whole config-4 MI estimate (three Chebyshev m = 60 Hutch++ 22 + 46 estimates at
+    n = 100k) row-sharded over two ranks (the NCCL rank code over the LocalGroup transport)
+    equals the single-rank result: the sharded protocol at the benchmark's size."""
+    from test_gpu_sharded import run_ranks
+
+    n = 100_000
+    x, y = mi_inputs(n, 1)
+    x, y = x.astype(np.float32).astype(np.float64), y.astype(np.float32).astype(np.float64)
+    sx, sy = R.GaussianKernel(4.0), R.GaussianKernel(math.sqrt(8.0))
+    p = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60, seed=1, s_q=22, s_g=46,
+                          bounds=R.SpectrumBounds(u=0, v=1))
+    ref = R.mutual_information_samples(x, sx, y, sy, p, precision="fp32", ctx=R.Context(0))
+    res = run_ranks(R, 2, lambda ctx, rank: R.mutual_information_samples(x, sx, y, sy, p, "fp32", ctx))
+    for r in res:
+        assert r.value == res[0].value
+        for key in ("vars_entropy", "target_entropy", "joint_entropy"):
+            a, b = getattr(r, key), getattr(ref, key)
+            assert abs(a - b) <= 1e-5 * abs(b), (key, a, b)
