@@ -513,27 +513,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
     if (warp == 1) tmem_dealloc_2sm(tmem, 512);
 }
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encoder() {
-    static EncodeFn fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(p);
-    }
-    return fn;
-}
-
 template <int DP, int NPAD>
 cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan, float* partial,
                       cudaStream_t stream) {
     using C = MfCfg<DP, NPAD>;
-    EncodeFn enc = encoder();
+    TensorMapEncodeFn enc = tensor_map_encoder();
     if (!enc) return cudaErrorInvalidValue;
     if (v.rpr % JB != 0) return cudaErrorInvalidValue;
     CUtensorMap mxi, mxj, mar, mac, mv;

@@ -26,10 +26,6 @@ namespace rb {
 
 namespace {
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 constexpr int GT = 128;           // tile (rows and columns)
 constexpr int KS = 32;            // fp32 per K sub-tile: one 128-byte SW128 row
 constexpr int kGStages = 2;
@@ -305,18 +301,6 @@ __global__ void gram_tc_norms_kernel(GramArgs g, double sx, double sy, int dt, f
     sq[i] = static_cast<float>(s2);
 }
 
-EncodeFn tmap_encoder() {
-    static EncodeFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            return reinterpret_cast<EncodeFn>(p);
-        return static_cast<EncodeFn>(nullptr);
-    }();
-    return fn;
-}
-
 }  // namespace
 
 bool gram_tc_supported(const GramArgs& g) {
@@ -359,7 +343,7 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
         gram_tc_norms_kernel<<<static_cast<unsigned>((g.n + 255) / 256), 256, 0, stream>>>(g, sx, sy, dt, sq);
         e = cudaGetLastError();
     }
-    EncodeFn enc = tmap_encoder();
+    TensorMapEncodeFn enc = tensor_map_encoder();
     if (e == cudaSuccess && !enc) e = cudaErrorInvalidValue;
     CUtensorMap ma, mb;
     for (int s = 0; s < 2 && e == cudaSuccess; ++s) {

@@ -296,6 +296,18 @@ __global__ void rng_panel_kernel(uint64_t base_key, bool derive, int kind, int64
 
 }  // namespace
 
+TensorMapEncodeFn tensor_map_encoder() {
+    static const TensorMapEncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<TensorMapEncodeFn>(p);
+        return static_cast<TensorMapEncodeFn>(nullptr);
+    }();
+    return fn;
+}
+
 cudaError_t ensure_smem_attr(const void* fn, int bytes) {
     static std::mutex mu;
     static std::set<std::pair<const void*, int>> done;
