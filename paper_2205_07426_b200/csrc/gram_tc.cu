@@ -162,8 +162,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
     } else {
         // ---------------- epilogue: warps 2-17, columns [32h, 32h+32) of the tile ----------------
-        // Phase A: TMEM -> K -> fp16 hi/lo, staged row-major (D) and transposed (T) in shared memory in
-        // the TMA 128B-swizzled box layout (conflict-free row writes and transposed 2-byte writes).
+        // Phase A: TMEM -> K -> fp16 hi/lo in registers (overlapping the previous tile's TMA stores),
+        // then staged row-major (D) and transposed (T) in shared memory in the TMA 128B-swizzled box
+        // layout (conflict-free row writes and transposed 2-byte writes).
         // Phase B: one thread stores the boxes with TMA (full-line writes; the global writes drain
         // asynchronously while the next tile is computed). On a diagonal tile the lower triangle of D
         // is first replaced from T so A is exactly symmetric like the reference's mirrored Gram
@@ -183,13 +184,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
             const float sqi = __ldg(args.sq + gi);
             mbar_wait(&acc_full[buf], (lt >> 1) & 1u);
             tc_fence_after();
-#pragma unroll 1
+            // (1) the tile's 32 columns of this thread's row -> fp16 hi/lo pairs in registers, while the
+            //     TMA engine may still be reading the previous tile's staging
+            uint32_t ph[16], pl[16];
+#pragma unroll
             for (int c0 = 0; c0 < 32; c0 += 16) {
                 float sv[16];
                 tmem_ld16(tmem + lane_off + buf * GT + h * 32 + c0, sv);
                 tmem_ld_wait();
                 const float4* sqj4 = reinterpret_cast<const float4*>(args.sq + bj * GT + h * 32 + c0);
-                uint32_t ph[8], pl[8];
 #pragma unroll
                 for (int e = 0; e < 16; e += 4) {
                     const float4 sj = __ldg(sqj4 + e / 4);
@@ -209,26 +212,37 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         const __half2 hh = __floats2half2_rn(kk[0], kk[1]);
                         const float2 back = __half22float2(hh);
                         const __half2 ll = __floats2half2_rn(kk[0] - back.x, kk[1] - back.y);
-                        ph[(e + u) / 2] = *reinterpret_cast<const uint32_t*>(&hh);
-                        pl[(e + u) / 2] = *reinterpret_cast<const uint32_t*>(&ll);
-                        const int c = h * 32 + c0 + e + u;  // transposed copy: T[c][row], T[c + 1][row]
-                        *reinterpret_cast<__half*>(tt + sw_off(c, row)) = __low2half(hh);
-                        *reinterpret_cast<__half*>(tt + kPlane + sw_off(c, row)) = __low2half(ll);
-                        *reinterpret_cast<__half*>(tt + sw_off(c + 1, row)) = __high2half(hh);
-                        *reinterpret_cast<__half*>(tt + kPlane + sw_off(c + 1, row)) = __high2half(ll);
+                        ph[(c0 + e + u) / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+                        pl[(c0 + e + u) / 2] = *reinterpret_cast<const uint32_t*>(&ll);
                     }
                 }
-                const int cc = h * 32 + c0;
-                *reinterpret_cast<uint4*>(dd + sw_off(row, cc)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-                *reinterpret_cast<uint4*>(dd + sw_off(row, cc + 8)) = make_uint4(ph[4], ph[5], ph[6], ph[7]);
-                *reinterpret_cast<uint4*>(dd + kPlane + sw_off(row, cc)) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-                *reinterpret_cast<uint4*>(dd + kPlane + sw_off(row, cc + 8)) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM buffer free for the tile after next
+            // (2) staging free (the previous tile's TMA stores have read it), then D rows and T columns
+            if (et == 0) bulk_wait_read_all();
             asm volatile("bar.sync 1, 512;" ::: "memory");
+#pragma unroll
+            for (int c8 = 0; c8 < 32; c8 += 8) {
+                const int cc = h * 32 + c8;
+                *reinterpret_cast<uint4*>(dd + sw_off(row, cc)) =
+                    make_uint4(ph[c8 / 2], ph[c8 / 2 + 1], ph[c8 / 2 + 2], ph[c8 / 2 + 3]);
+                *reinterpret_cast<uint4*>(dd + kPlane + sw_off(row, cc)) =
+                    make_uint4(pl[c8 / 2], pl[c8 / 2 + 1], pl[c8 / 2 + 2], pl[c8 / 2 + 3]);
+            }
+#pragma unroll
+            for (int p = 0; p < 16; ++p) {  // transposed copy: T[c][row], T[c + 1][row]
+                const int c = h * 32 + 2 * p;
+                const __half2 hh = *reinterpret_cast<const __half2*>(&ph[p]);
+                const __half2 ll = *reinterpret_cast<const __half2*>(&pl[p]);
+                *reinterpret_cast<__half*>(tt + sw_off(c, row)) = __low2half(hh);
+                *reinterpret_cast<__half*>(tt + kPlane + sw_off(c, row)) = __low2half(ll);
+                *reinterpret_cast<__half*>(tt + sw_off(c + 1, row)) = __high2half(hh);
+                *reinterpret_cast<__half*>(tt + kPlane + sw_off(c + 1, row)) = __high2half(ll);
+            }
             if (diag && !args.rect) {  // D[i][j] <- K(j, i) = T[i][j] below the diagonal
+                asm volatile("bar.sync 1, 512;" ::: "memory");
                 for (int idx = et; idx < GT * GT; idx += 32 * kGEpiWarps) {
                     const int i = idx >> 7, j = idx & 127;
                     if (j < i) {
@@ -237,7 +251,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         *reinterpret_cast<__half*>(dd + kPlane + o) = *reinterpret_cast<const __half*>(tt + kPlane + o);
                     }
                 }
-                asm volatile("bar.sync 1, 512;" ::: "memory");
             }
             fence_proxy_async_smem();  // this thread's staging writes -> visible to the TMA engine
             asm volatile("bar.sync 1, 512;" ::: "memory");
@@ -255,10 +268,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
                                      static_cast<int>(bj * GT));
                     }
                 }
-                bulk_commit_group();
-                bulk_wait_read_all();  // staging reusable; the global writes complete in the background
+                bulk_commit_group();  // read completion is awaited before the next tile's staging writes
             }
-            asm volatile("bar.sync 1, 512;" ::: "memory");  // D, T reusable by the next tile
         }
         if (et == 0) bulk_wait_all();
     }
