@@ -377,6 +377,7 @@ def run_ours(args):
         "config": {"workload": "c4: MI n=100000 dx=16 dy=8 sigma=sqrt(d) alpha=1.01 Chebyshev[0,1] m=60 "
                                "Hutch++ s=90 (reference split 22+46), Gaussian probes drawn on device",
                    "n": n, "estimates_per_step": 3, "operand": args.operand, "kc": args.kc,
+                   "passes_per_estimate": "1 sketch + 30 (degree-60 Chebyshev moments by doubling, DESIGN.md §8)",
                    "l2": "inputs larger than L2: each A is 40 GB (n^2 x 4 B) vs 126 MB L2",
                    "parallelism": (f"rowshard x{world}: A split by rows, NCCL all-gather of the operand planes "
                                    "per pass, fp64 trace partials all-reduced per estimate") if sharded else
@@ -573,6 +574,7 @@ def run_ours_c5(args):
         "config": {"workload": "c5: n=400000 d=128 sigma=sqrt(d) alpha=3 integer power, Hutch++ s=120 "
                                "(reference split 30+60), Gaussian probes drawn on device, A never stored",
                    "n": n, "estimates_per_step": 1, "mf_kc": args.mf_kc,
+                   "passes_per_estimate": "1 sketch + 2 (x.A^3 x = (Ax).A(Ax), DESIGN.md §8)",
                    "l2": "X (102 MB bf16) + operand planes (96 MB) exceed the 126 MB L2; the kernel streams them "
                          "in waves (HBM reads ~8 GB per pass per ncu)",
                    "parallelism": (f"rowshard x{world}: rows of K split by rank, NCCL all-gather of the operand "
