@@ -391,3 +391,27 @@ def test_out_of_memory_is_reported_and_recoverable(R):
     assert np.all(np.isfinite(y))
     assert abs(y[n // 2] - math.sqrt(2 * math.pi) / 1e-3 / n) <= 1e-3 * y[n // 2]
     assert abs(y[0] - 0.5 * math.sqrt(2 * math.pi) / 1e-3 / n) <= 2e-3 * y[0]
+
+
+@pytest.mark.parametrize("spec", [("int", 1, 0, 0.0, 1.0), ("int", 5, 0, 0.0, 1.0), ("taylor", 0.7, 2, 0.0, 1.0),
+                                  ("taylor", 2.5, 7, 0.0, 0.6), ("chebyshev", 1.5, 1, 0.0, 1.0),
+                                  ("chebyshev", 1.5, 2, 0.0, 1.0), ("chebyshev", 1.2, 7, 0.0, 1.0),
+                                  ("chebyshev", 2.0, 31, 0.02, 0.9)])
+def test_trace_moment_doubling_edge_degrees(R, orc, spec):
+    """Traces take ceil(m/2) passes by moment doubling: odd and even degrees,
+    m = 1 and 2, integer powers 1 and 5, narrow Chebyshev intervals — against the oracle's
+    sequential apply_panel (poly.cpp:97-134) and x.f(A)x."""
+    kind, alpha, m, u, v = spec
+    n, s = 700, 9
+    x = orc.fill_gaussian(41, n, 4)
+    p = orc.fill_gaussian(42, n, s)
+    ospec = orc.Spec(kind, alpha, m, u, v)
+    rspec = {"int": lambda: R.MatrixFunctionSpec.int_power(int(alpha)),
+             "taylor": lambda: R.MatrixFunctionSpec.taylor(alpha, m, v),
+             "chebyshev": lambda: R.MatrixFunctionSpec.chebyshev(alpha, m, u, v)}[kind]()
+    for prec in ("fp64", "fp32"):
+        xx = x if prec == "fp64" else f32(x)
+        a = orc.build_kernel(xx, 1.3)
+        ref_tr = np.einsum("ij,ij->j", p, orc.apply_panel(ospec, a, p))
+        tr = R.matfun_traces(rspec, R.build_kernel(xx, R.GaussianKernel(1.3), prec), p)
+        assert np.max(np.abs(tr - ref_tr) / np.abs(ref_tr)) <= (1e-10 if prec == "fp64" else TOL["fp32"]), prec
