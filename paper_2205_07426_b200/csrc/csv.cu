@@ -23,15 +23,10 @@
 // texts are strings, cleaned on the host from the caller's buffer by the same state machine.
 #include <cub/cub.cuh>
 
-#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <limits>
-#include <map>
-#include <mutex>
-#include <thread>
-#include <vector>
 
 #include "engine.h"
 #include "pow10_table.h"
@@ -820,79 +815,7 @@ std::string clean_host(const char* t, int64_t s, int64_t e) {
     return out;
 }
 
-// The text usually sits in pageable memory (a file read into a std::string). Large inputs go through
-// two page-locked 32 MB slots per device: several host threads fill one slot while the DMA engine
-// drains the other, instead of the driver's single-threaded pageable staging.
-struct PinnedStaging {
-    static constexpr size_t kSlot = size_t(32) << 20;
-    void* slot[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
-    std::mutex mu;  // one staged upload at a time per device
-};
 
-PinnedStaging* staging_for(int device) {
-    static std::mutex mu;
-    static std::map<int, PinnedStaging*> all;  // process lifetime (page-locked memory is reused)
-    std::lock_guard<std::mutex> lk(mu);
-    PinnedStaging*& st = all[device];
-    if (!st) {
-        auto* p = new PinnedStaging;
-        bool ok = true;
-        for (int i = 0; i < 2 && ok; ++i)
-            ok = cudaHostAlloc(&p->slot[i], PinnedStaging::kSlot, cudaHostAllocDefault) == cudaSuccess &&
-                 cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming) == cudaSuccess;
-        if (!ok) {
-            (void)cudaGetLastError();
-            for (int i = 0; i < 2; ++i) {
-                if (p->slot[i]) cudaFreeHost(p->slot[i]);
-                if (p->done[i]) cudaEventDestroy(p->done[i]);
-            }
-            delete p;
-            return nullptr;
-        }
-        st = p;
-    }
-    return st;
-}
-
-void parallel_memcpy(void* dst, const void* src, size_t n) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned T = std::min(8u, hw);
-    if (n < (size_t(4) << 20) || T == 1) {
-        memcpy(dst, src, n);
-        return;
-    }
-    std::vector<std::thread> th;
-    const size_t part = (n + T - 1) / T;
-    for (unsigned t = 0; t < T; ++t) {
-        const size_t a = t * part, b = std::min(n, a + part);
-        if (a < b)
-            th.emplace_back([=] { memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
-    }
-    for (auto& x : th) x.join();
-}
-
-void h2d_staged(Context& ctx, void* dst, const char* src, size_t len) {
-    PinnedStaging* st = len >= (size_t(8) << 20) ? staging_for(ctx.device()) : nullptr;
-    if (!st) {
-        h2d(ctx, dst, src, len);
-        return;
-    }
-    std::lock_guard<std::mutex> lk(st->mu);
-    size_t c = 0;
-    for (size_t off = 0; off < len; off += PinnedStaging::kSlot, ++c) {
-        const int i = static_cast<int>(c & 1);
-        const size_t b = std::min(PinnedStaging::kSlot, len - off);
-        cuda_check(cudaEventSynchronize(st->done[i]), "staging slot");  // its previous DMA has drained
-        parallel_memcpy(st->slot[i], src + off, b);
-        cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + off, st->slot[i], b, cudaMemcpyHostToDevice,
-                                   ctx.stream()),
-                   "host->device copy");
-        cuda_check(cudaEventRecord(st->done[i], ctx.stream()), "staging event");
-    }
-    ctx.h2d_bytes += static_cast<long long>(len);
-    // the slots are reused by the next upload only after these copies drain (event waits above)
-}
 
 }  // namespace
 
@@ -909,7 +832,7 @@ std::unique_ptr<Dataset> load_csv_text(Context& ctx, const char* text, size_t le
     dtext.alloc(static_cast<size_t>(chunks) * kCsvChunk);
     cuda_check(cudaMemsetAsync(dtext.as<uint8_t>() + L, 0, static_cast<size_t>(chunks) * kCsvChunk - L, st),
                "memset");
-    h2d_staged(ctx, dtext.as<void>(), text, len);
+    h2d_staged(ctx, dtext.as<void>(), text, len);  // engine.cu: page-locked double buffering
     dstats.alloc(static_cast<size_t>(chunks) * sizeof(ChunkStats));
     dstate.alloc(static_cast<size_t>(chunks));
     drec0.alloc(static_cast<size_t>(chunks) * sizeof(int64_t));

@@ -12,6 +12,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 
 namespace rb {
 
@@ -43,6 +44,88 @@ void d2h_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spit
     cuda_check(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, ctx.stream()),
                "device->host copy");
     ctx.d2h_bytes += static_cast<long long>(width * height);
+}
+
+namespace {
+// Host inputs usually sit in pageable memory (numpy arrays, a file read into a string). Large ones go through
+// two page-locked 32 MB slots per device: several host threads fill one slot while the DMA engine
+// drains the other, instead of the driver's single-threaded pageable staging.
+struct PinnedStaging {
+    static constexpr size_t kSlot = size_t(32) << 20;
+    void* slot[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    std::mutex mu;  // one staged upload at a time per device
+};
+
+PinnedStaging* staging_for(int device) {
+    static std::mutex mu;
+    static std::map<int, PinnedStaging*> all;  // process lifetime (page-locked memory is reused)
+    std::lock_guard<std::mutex> lk(mu);
+    PinnedStaging*& st = all[device];
+    if (!st) {
+        auto* p = new PinnedStaging;
+        bool ok = true;
+        for (int i = 0; i < 2 && ok; ++i)
+            ok = cudaHostAlloc(&p->slot[i], PinnedStaging::kSlot, cudaHostAllocDefault) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            (void)cudaGetLastError();
+            for (int i = 0; i < 2; ++i) {
+                if (p->slot[i]) cudaFreeHost(p->slot[i]);
+                if (p->done[i]) cudaEventDestroy(p->done[i]);
+            }
+            delete p;
+            return nullptr;
+        }
+        st = p;
+    }
+    return st;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t n) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned T = std::min(8u, hw);
+    if (n < (size_t(4) << 20) || T == 1) {
+        memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (n + T - 1) / T;
+    for (unsigned t = 0; t < T; ++t) {
+        const size_t a = t * part, b = std::min(n, a + part);
+        if (a < b)
+            th.emplace_back([=] { memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+    }
+    for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+void h2d_staged(Context& ctx, void* dst, const void* src_v, size_t len) {
+    const char* src = static_cast<const char*>(src_v);
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, src_v) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    // page-locked sources already copy at full link speed
+    PinnedStaging* st = (!pinned && len >= (size_t(8) << 20)) ? staging_for(ctx.device()) : nullptr;
+    if (!st) {
+        h2d(ctx, dst, src, len);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(st->mu);
+    size_t c = 0;
+    for (size_t off = 0; off < len; off += PinnedStaging::kSlot, ++c) {
+        const int i = static_cast<int>(c & 1);
+        const size_t b = std::min(PinnedStaging::kSlot, len - off);
+        cuda_check(cudaEventSynchronize(st->done[i]), "staging slot");  // its previous DMA has drained
+        parallel_memcpy(st->slot[i], src + off, b);
+        cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + off, st->slot[i], b, cudaMemcpyHostToDevice,
+                                   ctx.stream()),
+                   "host->device copy");
+        cuda_check(cudaEventRecord(st->done[i], ctx.stream()), "staging event");
+    }
+    ctx.h2d_bytes += static_cast<long long>(len);
+    // the slots are reused by the next upload only after these copies drain (event waits above)
 }
 
 // ---------------------------------------------------------------- caching pool
@@ -304,8 +387,11 @@ KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, in
     DevBuf xs;
     const int64_t dt = d + (y ? dy : 0);
     xs.alloc(static_cast<size_t>(n) * dt * sizeof(double));
-    h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), d);
-    if (y) h2d_2d(ctx, xs.as<double>() + n * d, n * sizeof(double), y, ldy * sizeof(double), n * sizeof(double), dy);
+    // contiguous panels (ld == n) take the page-locked staged path when large
+    if (ldx == n) h2d_staged(ctx, xs.as<double>(), x, static_cast<size_t>(n) * d * sizeof(double));
+    else h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), d);
+    if (y && ldy == n) h2d_staged(ctx, xs.as<double>() + n * d, y, static_cast<size_t>(n) * dy * sizeof(double));
+    else if (y) h2d_2d(ctx, xs.as<double>() + n * d, n * sizeof(double), y, ldy * sizeof(double), n * sizeof(double), dy);
     KernelPtr k = build_gaussian_dev(ctx, xs.as<double>(), n, d, n, sigma, prec, y ? xs.as<double>() + n * d : nullptr,
                                      dy, n, sigma_y);
     ctx.sync();  // xs goes out of scope
@@ -1548,8 +1634,10 @@ MutualInfo mutual_information_samples(Context& ctx, const double* x, int64_t n, 
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     DevBuf xs;
     xs.alloc(static_cast<size_t>(n) * (dx + dy) * sizeof(double));
-    h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), dx);
-    h2d_2d(ctx, xs.as<double>() + n * dx, n * sizeof(double), y, ldy * sizeof(double), n * sizeof(double), dy);
+    if (ldx == n) h2d_staged(ctx, xs.as<double>(), x, static_cast<size_t>(n) * dx * sizeof(double));
+    else h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), dx);
+    if (ldy == n) h2d_staged(ctx, xs.as<double>() + n * dx, y, static_cast<size_t>(n) * dy * sizeof(double));
+    else h2d_2d(ctx, xs.as<double>() + n * dx, n * sizeof(double), y, ldy * sizeof(double), n * sizeof(double), dy);
     MutualInfo mi = mutual_information_samples_dev(ctx, xs.as<double>(), n, dx, n, sigma_x, xs.as<double>() + n * dx,
                                                    dy, n, sigma_y, p, prec);
     ctx.sync();

@@ -305,6 +305,8 @@ EstParams with_seed(const EstParams& p, const char* term);
 
 // counted host<->device copies on the engine stream
 void h2d(Context& ctx, void* dst, const void* src, size_t bytes);
+// large contiguous uploads from pageable memory: page-locked double buffering, several host threads
+void h2d_staged(Context& ctx, void* dst, const void* src, size_t bytes);
 void d2h(Context& ctx, void* dst, const void* src, size_t bytes);
 void h2d_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height);
 void d2h_2d(Context& ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height);
