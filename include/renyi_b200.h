@@ -233,7 +233,10 @@ int renyi_matvec(renyi_ctx* ctx, const renyi_kernel* k, const double* x, double*
 /* apply_panel(spec, a, x) — proj/src/poly.cpp:158-164 */
 int renyi_apply_panel(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const double* v, int s,
                       double* y);
-/* fused x_j^T f(A) x_j per column (projected_trace without the vector) — hutchpp.cpp:33-39 */
+/* fused x_j^T f(A) x_j per column (projected_trace without the vector) — hutchpp.cpp:33-39.
+ * Every trace-only entry point (this, renyi_hutchpp, renyi_estimate, the entropy, MI, trials and
+ * feature entry points) forms the quadratic forms of a degree-m polynomial from ceil(m/2) passes
+ * over A by moment doubling (A symmetric); renyi_apply_panel runs all m. */
 int renyi_matfun_traces(renyi_ctx* ctx, const renyi_kernel* k, const renyi_matfun* f, const double* x, int s,
                         double* traces);
 
