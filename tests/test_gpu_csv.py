@@ -165,3 +165,21 @@ def test_decimal_paths_bit_exact_at_scale(R, orc):
     dev, ref = both(R, orc, text)
     assert_same(dev, ref, "<decimal paths>")
     assert dev[1]["n"] == len(cells)
+
+
+def test_golden_csv_fixtures_on_device(R):
+    """tests/golden: the reference tests' CSV inputs through load_csv(path) on the device."""
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent / "golden"
+    for name, want in json.loads((root / "expected.json").read_text()).items():
+        path = str(root / name)
+        if "error" in want:
+            with pytest.raises(R.RenyiError) as e:
+                R.load_csv(path)
+            assert e.value.status == 10 and want["error"] in str(e.value), name
+        else:
+            ds = R.load_csv(path)
+            assert (ds.n, ds.d, ds.names) == (want["n"], want["d"], want["names"])
+            assert np.array_equal(ds.features, np.array(want["features"], dtype=float))

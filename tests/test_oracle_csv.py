@@ -111,3 +111,21 @@ def test_pow10_table_matches_generator():
             d = 10 ** (-e)  # never a power of two: floor(log2(1/d)) = -bit_length(d)
             k = 127 + d.bit_length()
             assert m * d <= (1 << k) < (m + 1) * d
+
+
+def test_golden_csv_fixtures(orc):
+    """tests/golden: the reference tests' CSV inputs and their asserted outcomes."""
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent / "golden"
+    for name, want in json.loads((root / "expected.json").read_text()).items():
+        text = (root / name).read_bytes()
+        if "error" in want:
+            with pytest.raises(orc.OracleError) as e:
+                orc.load_csv(text, source=name)
+            assert e.value.code == 10 and want["error"] in str(e.value), name
+        else:
+            d = orc.load_csv(text, source=name)
+            assert (d["n"], d["d"], d["names"]) == (want["n"], want["d"], want["names"])
+            assert np.array_equal(d["features"], np.array(want["features"], dtype=float))
