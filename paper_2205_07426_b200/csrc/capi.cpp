@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <string>
 
@@ -52,6 +53,14 @@ int guarded(F&& f) {
         g_last_error = "unknown failure";
         return RENYI_E_INTERNAL;
     }
+}
+
+// Builds a handle and releases it to the caller only when construction succeeded.
+template <typename H, typename F>
+H* make_handle(F&& build) {
+    auto h = std::make_unique<H>();
+    build(*h);
+    return h.release();
 }
 
 void need(const void* p, const char* what) {
@@ -199,9 +208,7 @@ int renyi_ctx_init_nccl(renyi_ctx* ctx, int rank, int world, const unsigned char
 int renyi_local_group_create(int world, renyi_local_group** out) {
     return guarded([&] {
         need(out, "out");
-        auto* g = new renyi_local_group;
-        g->g = rb::make_local_group(world);
-        *out = g;
+        *out = make_handle<renyi_local_group>([&](renyi_local_group& h) { h.g = rb::make_local_group(world); });
     });
 }
 
@@ -302,14 +309,9 @@ int renyi_kernel_build_gaussian(renyi_ctx* ctx, const double* x, int64_t n, int6
     return guarded([&] {
         need(ctx, "ctx"), need(x, "samples"), need(out, "out");
         check_precision(precision);
-        auto* k = new renyi_kernel;
-        try {
-            k->k = rb::build_gaussian(ctx->ctx, x, n, d, ldx, sigma, precision);
-        } catch (...) {
-            delete k;
-            throw;
-        }
-        *out = k;
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::build_gaussian(ctx->ctx, x, n, d, ldx, sigma, precision);
+        });
     });
 }
 
@@ -319,14 +321,9 @@ int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n
     return guarded([&] {
         need(ctx, "ctx"), need(x, "samples"), need(y, "second samples"), need(out, "out");
         check_precision(precision);
-        auto* k = new renyi_kernel;
-        try {
-            k->k = rb::build_gaussian(ctx->ctx, x, n, dx, ldx, sigma_x, precision, y, dy, ldy, sigma_y);
-        } catch (...) {
-            delete k;
-            throw;
-        }
-        *out = k;
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::build_gaussian(ctx->ctx, x, n, dx, ldx, sigma_x, precision, y, dy, ldy, sigma_y);
+        });
     });
 }
 
@@ -336,29 +333,19 @@ int renyi_kernel_build_gaussian_dev(renyi_ctx* ctx, const double* d_x, int64_t n
     return guarded([&] {
         need(ctx, "ctx"), need(d_x, "samples"), need(out, "out");
         check_precision(precision);
-        auto* k = new renyi_kernel;
-        try {
-            k->k = rb::build_gaussian_dev(ctx->ctx, d_x, n, d, ldx, sigma, precision, d_y, dy, ldy, sigma_y);
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::build_gaussian_dev(ctx->ctx, d_x, n, d, ldx, sigma, precision, d_y, dy, ldy, sigma_y);
             ctx->ctx.sync();
-        } catch (...) {
-            delete k;
-            throw;
-        }
-        *out = k;
+        });
     });
 }
 
 int renyi_csv_load(renyi_ctx* ctx, const char* path, const char* label_column, renyi_dataset** out) {
     return guarded([&] {
         need(ctx, "ctx"), need(path, "path"), need(out, "out");
-        auto* ds = new renyi_dataset;
-        try {
-            ds->d = rb::load_csv_file(ctx->ctx, path, label_column);
-        } catch (...) {
-            delete ds;
-            throw;
-        }
-        *out = ds;
+        *out = make_handle<renyi_dataset>([&](renyi_dataset& h) {
+            h.d = rb::load_csv_file(ctx->ctx, path, label_column);
+        });
     });
 }
 
@@ -368,15 +355,10 @@ int renyi_csv_parse(renyi_ctx* ctx, const char* text, int64_t len, const char* l
         need(ctx, "ctx"), need(out, "out");
         if (len < 0) rb::fail(rb::kInvalidArgument, "negative text length");
         if (len > 0) need(text, "text");
-        auto* ds = new renyi_dataset;
-        try {
-            ds->d = rb::load_csv_text(ctx->ctx, text, static_cast<size_t>(len), label_column,
-                                      source ? source : "<buffer>");
-        } catch (...) {
-            delete ds;
-            throw;
-        }
-        *out = ds;
+        *out = make_handle<renyi_dataset>([&](renyi_dataset& h) {
+            h.d = rb::load_csv_text(ctx->ctx, text, static_cast<size_t>(len), label_column,
+                                    source ? source : "<buffer>");
+        });
     });
 }
 
@@ -420,12 +402,11 @@ int renyi_kernel_build_gaussian_dataset(renyi_ctx* ctx, const renyi_dataset* ds,
         need(ctx, "ctx"), need(ds, "dataset"), need(out, "out");
         check_precision(precision);
         const rb::Dataset& data = *ds->d;
-        auto* k = new renyi_kernel;
-        try {
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
             cudaSetDevice(ctx->ctx.device());
             if (!columns) {
-                k->k = rb::build_gaussian_dev(ctx->ctx, data.features.as<double>(), data.n, data.d, data.n, sigma,
-                                              precision);
+                h.k = rb::build_gaussian_dev(ctx->ctx, data.features.as<double>(), data.n, data.d, data.n, sigma,
+                                            precision);
             } else {
                 if (ncols < 1) rb::fail(rb::kInvalidArgument, "need at least one column");
                 rb::DevBuf sel;
@@ -439,14 +420,10 @@ int renyi_kernel_build_gaussian_dataset(renyi_ctx* ctx, const renyi_dataset* ds,
                                                    cudaMemcpyDeviceToDevice, ctx->ctx.stream()),
                                    "column gather");
                 }
-                k->k = rb::build_gaussian_dev(ctx->ctx, sel.as<double>(), data.n, ncols, data.n, sigma, precision);
+                h.k = rb::build_gaussian_dev(ctx->ctx, sel.as<double>(), data.n, ncols, data.n, sigma, precision);
             }
             ctx->ctx.sync();
-        } catch (...) {
-            delete k;
-            throw;
-        }
-        *out = k;
+        });
     });
 }
 
@@ -458,28 +435,18 @@ int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int pre
     return guarded([&] {
         need(ctx, "ctx"), need(a, "matrix"), need(out, "out");
         check_precision(precision);
-        auto* k = new renyi_kernel;
-        try {
-            k->k = rb::from_matrix(ctx->ctx, a, n, precision);
-        } catch (...) {
-            delete k;
-            throw;
-        }
-        *out = k;
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::from_matrix(ctx->ctx, a, n, precision);
+        });
     });
 }
 
 int renyi_kernel_hadamard_joint(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b, renyi_kernel** out) {
     return guarded([&] {
         need(ctx, "ctx"), need(a, "kernel a"), need(b, "kernel b"), need(out, "out");
-        auto* k = new renyi_kernel;
-        try {
-            k->k = rb::hadamard_joint(ctx->ctx, *a->k, *b->k);
-        } catch (...) {
-            delete k;
-            throw;
-        }
-        *out = k;
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::hadamard_joint(ctx->ctx, *a->k, *b->k);
+        });
     });
 }
 
