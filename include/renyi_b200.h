@@ -151,6 +151,10 @@ int renyi_ctx_create(int device, renyi_ctx** out);
 int renyi_ctx_destroy(renyi_ctx* ctx);
 int renyi_ctx_set_tuning(renyi_ctx* ctx, int grid, int kc);
 int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode);
+/* mutual information over fp32 kernels: 1 (default) runs the three terms' passes fused, one read of
+ * A and B per pass with the joint kernel n·A∘B formed on the fly (never stored); 0: three separate
+ * estimates over a materialised joint (proj/src/measures.cpp:36-46) */
+int renyi_ctx_set_fused_mi(renyi_ctx* ctx, int on);
 /* matrix-free product: j-blocks (of 128 samples) accumulated in TMEM before each fp32 drain */
 int renyi_ctx_set_matrix_free_chunk(renyi_ctx* ctx, int jblocks);
 int renyi_ctx_sync(renyi_ctx* ctx);

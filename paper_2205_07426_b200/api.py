@@ -66,6 +66,11 @@ class Context:
         where vectors are returned, fast for trace-only passes)."""
         check(L.lib().renyi_ctx_set_operand_mode(self._h, {"split": 0, "fast": 1, "auto": 2}[mode]))
 
+    def set_fused_mi(self, on: bool = True) -> None:
+        """Mutual information over fp32 kernels: one pass over A and B serves all three terms (the
+        joint kernel n·A∘B is formed on the fly, never stored); False: three separate estimates."""
+        check(L.lib().renyi_ctx_set_fused_mi(self._h, 1 if on else 0))
+
     def sync(self) -> None:
         check(L.lib().renyi_ctx_sync(self._h))
 
@@ -910,7 +915,8 @@ def mutual_information(vars_: Sequence[NormalizedKernel], target: NormalizedKern
 
 def mutual_information_samples(x, sx: GaussianKernel, y, sy: GaussianKernel, params: EstimatorParams,
                                precision="fp32", ctx: Optional[Context] = None) -> MutualInformation:
-    """MI from samples with one n x n matrix resident at a time (the bench path)."""
+    """MI from host samples (the bench path): fp32 kernels with bounds / integer alpha run the fused
+    pass (A and B resident, the joint formed on the fly), otherwise one n x n matrix at a time."""
     ctx = ctx or default_context()
     xa, ya = _colmajor(x), _colmajor(y)
     out = L.MiEstimateC()

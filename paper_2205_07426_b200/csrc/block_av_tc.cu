@@ -34,7 +34,9 @@
 //   * Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM owner),
 //     warps 2..9 = TMEM drain (4 per M=128 tile) and partial writers.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -341,6 +343,458 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ fused mutual-information pass
+// One pass over A and B computes the products of all three MI terms (proj/src/measures.cpp:36-46):
+//   Y_A = A·V_A,   Y_B = B·V_B,   Y_J = J·V_J,   J = n·(A∘B) with J_ii = 1/n (proj/src/kernel.cpp:74-108),
+// J formed tile by tile from the staged A and B planes and never stored: 8 B of HBM per entry instead
+// of 12 B for three separate passes over A, B and a materialised J. Each CTA owns 128 rows (one UMMA
+// M = 128 tile per operand, TMEM: 3 accumulators + the J operand); CTA pairs walk the same k-tiles and
+// multicast the V planes as in block_av_tc_kernel.
+//   warp 0      TMA: A_hi, A_lo, B_hi, B_lo (128 x 32 fp16 each) + this CTA's half of the six V planes
+//   warp 1      MMA issuer: A_hi·[V_A hi|lo] + A_lo·V_A hi, the same for B (operands in smem), then
+//               J_hi·[V_J hi|lo] + J_lo·V_J hi with J from TMEM
+//   warps 2-5   J builders: one row per thread, j = fl(a·b)·2^-14 (+ the FMA remainder) split into fp16
+//               hi/lo pairs and stored into TMEM (same values as hadamard_split_kernel up to the fp32 round)
+//   warps 6-17  TMEM drains: operand (warp-6)/4, lane quarter warp%4, fp32 register accumulation
+constexpr int TBM = 128;
+constexpr int kTriConv = 8;    // two warpgroups: lane quarter warp%4, K half (warp-4)/4
+constexpr int kTriDrain = 12;  // three warpgroups: operand (warp-12)/4
+constexpr int kTriConv0 = 4, kTriDrain0 = 12;
+#ifndef RB_TRI_AB_STAGES
+#define RB_TRI_AB_STAGES 3
+#endif
+#ifndef RB_TRI_SETMAXNREG
+#define RB_TRI_SETMAXNREG 1
+#endif
+constexpr int kTriThreads = 32 * 24;  // warpgroup 0: TMA (warp 0), MMA (warp 1); setmaxnreg per role
+
+template <int NPAD, bool VSPLIT>
+struct TriCfg {
+    static constexpr int kAPlane = TBM * BK * 2;              // 8 KB: one fp16 plane of 128 rows x 32
+    static constexpr int kABStage = 4 * kAPlane;              // A_hi, A_lo, B_hi, B_lo
+    static constexpr int kVPer = VSPLIT ? 2 : 1;               // V planes per operand
+    static constexpr int kVHalf = (NPAD / 2) * BK * 2;        // this CTA's half of one V plane's rows
+    static constexpr int kVStage = 3 * kVPer * kVHalf;
+    static constexpr int kABStages = RB_TRI_AB_STAGES;
+    static constexpr int kVStagesRaw = (kSmemBudget * 1024 - kABStages * kABStage) / kVStage;
+    static constexpr int kVStages = kVStagesRaw > 8 ? 8 : kVStagesRaw;
+    static constexpr int kOpCols = 6 * 8;                     // one K=16 slot: A, B, J hi/lo planes (8 cols each)
+    static constexpr int kBufs = (2 * 3 * NPAD + 4 * kOpCols <= 512) ? 2 : 1;  // accumulator buffers
+    static constexpr int kOpCol0 = kBufs * 3 * NPAD;          // operand slots after the accumulators
+    static constexpr int kSlotsRaw = (512 - kOpCol0) / kOpCols;
+    static constexpr int kSlots = kSlotsRaw > 8 ? 8 : kSlotsRaw;  // half-stage operand slots in flight
+    static constexpr int kSmemBytes = kABStages * kABStage + kVStages * kVStage + 1024;
+    static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 80, "fused MI pass: NPAD in [16, 80]");
+    static_assert(kSlots >= 4 && kOpCol0 + kSlots * kOpCols <= 512, "TMEM budget");
+    static_assert(kVStages >= 3, "need a deep enough V ring");
+    static_assert(kVHalf % 512 == 0, "64-byte swizzle atoms");
+};
+
+struct TriArgs {
+    int64_t total_iters;  // pair_blocks * k_tiles
+    int k_tiles;
+    int kt_chunk;         // k tiles per V chunk (rpr / BK)
+    int kc;               // k tiles per TMEM chunk
+    int64_t dp_blocks;    // pair blocks owned whole (waves of pairs); stream-K over the rest
+    float* partial[3];    // [slots][NPAD][128] per operand (A, B, J)
+    int64_t row0;         // global index of this rank's first row (J diagonal)
+    uint32_t scale_a;     // fp16x2 2^ea, 2^eb with ea + eb = log2(stored J / (stored A · stored B))
+    uint32_t scale_b;
+    float diag;           // stored J_ii
+    int a_policy;         // 0: evict_first for the A/B stream, 1: evict_normal
+};
+
+// The (pair block, k range) segments of one CTA pair: whole pair blocks in data-parallel waves (all
+// pairs walk the same k tiles at about the same time, so the three V tiles of a k tile leave HBM once
+// per wave and are served from L2 to the other pairs), then an even stream-K share of the tail.
+struct TriSegs {
+    int64_t waves, grid, pair, KT, dp, it, it_end, w = 0;
+    __device__ TriSegs(const TriArgs& a, int p, int P) : grid(P), pair(p), KT(a.k_tiles), dp(a.dp_blocks) {
+        waves = dp / P;
+        const int64_t tail = a.total_iters - dp * KT;
+        it = tail * p / P;
+        it_end = tail * (p + 1) / P;
+    }
+    __device__ bool next(int64_t& r, int& k0, int& k1) {
+        if (w < waves) {
+            r = w * grid + pair;
+            k0 = 0;
+            k1 = static_cast<int>(KT);
+            ++w;
+            return true;
+        }
+        if (it >= it_end) return false;
+        const int64_t rt = it / KT;
+        const int64_t e = min(it_end, (rt + 1) * KT);
+        r = dp + rt;
+        k0 = static_cast<int>(it - rt * KT);
+        k1 = static_cast<int>(e - rt * KT);
+        it = e;
+        return true;
+    }
+    // partial slot of 128-row block 2r + rank (same layout as the matrix-free path's epilogue)
+    __device__ int64_t slot(int64_t r, int rank) const { return r < dp ? 2 * r + rank : 2 * (r + pair) + rank; }
+};
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.b32 %0, 1, 0, e;\n\t}" : "=r"(p));
+    return p != 0;
+}
+
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// 2 entries of J from packed (hi, lo) fp16 pairs of A and B, as a (hi, lo) fp16 split, in packed
+// half2 arithmetic: with a = a_h + a_l and b = b_h + b_l prescaled by exact powers of two,
+//   j_h = fl16(a_h b_h),  r = a_h b_h - j_h (exact: an 11x11-bit product minus its rounding),
+//   j_l = fl16(a_h b_l + fl16(a_l b_h + r))   (a_l b_l ~ 2^-22 relative is dropped, as in the split product)
+// so J is carried to ~21 bits like the materialised split of hadamard_split_kernel (22 bits).
+__device__ __forceinline__ void joint_pair(uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl, uint32_t sa,
+                                           uint32_t sb, uint32_t& jh, uint32_t& jl) {
+    ah = hmul2(ah, sa), al = hmul2(al, sa), bh = hmul2(bh, sb), bl = hmul2(bl, sb);
+    jh = hmul2(ah, bh);
+    const uint32_t r = hfma2(ah, bh, jh ^ 0x80008000u);
+    jl = hfma2(ah, bl, hfma2(al, bh, r));
+}
+
+__device__ __forceinline__ uint32_t f2h(float2 f) {
+    const __half2 h = __float22half2_rn(f);
+    uint32_t u;
+    memcpy(&u, &h, 4);
+    return u;
+}
+
+template <int NPAD, bool VSPLIT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
+    block_av_tri_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                        const __grid_constant__ CUtensorMap map_va, const __grid_constant__ CUtensorMap map_valo,
+                        const __grid_constant__ CUtensorMap map_vb, const __grid_constant__ CUtensorMap map_vblo,
+                        const __grid_constant__ CUtensorMap map_vj, const __grid_constant__ CUtensorMap map_vjlo,
+                        TriArgs args) {
+    using C = TriCfg<NPAD, VSPLIT>;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t ab_full[C::kABStages], ab_empty[C::kABStages];
+    __shared__ __align__(8) uint64_t v_full[C::kVStages], v_empty[C::kVStages];
+    __shared__ __align__(8) uint64_t op_full[C::kSlots], op_empty[C::kSlots];
+    __shared__ __align__(8) uint64_t acc_full[C::kBufs], acc_empty[C::kBufs];
+    __shared__ uint32_t tmem_base_smem;
+
+    const int warp = threadIdx.x / kWarp;
+    const int lane = threadIdx.x % kWarp;
+    const int G = gridDim.x / 2;
+    const int pair = blockIdx.x / 2;
+    const uint32_t rank = cluster_ctarank();  // 0 = leader: issues the pair's MMAs
+    const bool leader = rank == 0;
+    constexpr uint16_t kBoth = 0b11;
+
+    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+    const uint32_t v_u32 = base_u32 + C::kABStages * C::kABStage;  // V ring after the A/B ring
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&map_ahi), prefetch_tmap(&map_alo), prefetch_tmap(&map_bhi), prefetch_tmap(&map_blo);
+        prefetch_tmap(&map_va), prefetch_tmap(&map_vb), prefetch_tmap(&map_vj);
+        if (VSPLIT) prefetch_tmap(&map_valo), prefetch_tmap(&map_vblo), prefetch_tmap(&map_vjlo);
+        for (int s = 0; s < C::kABStages; ++s) {
+            mbar_init(&ab_full[s], 1);
+            mbar_init(&ab_empty[s], kTriConv);  // this CTA's converters have read the tiles
+        }
+        for (int s = 0; s < C::kVStages; ++s) {
+            mbar_init(&v_full[s], 1);   // leader: both CTAs' V halves landed
+            mbar_init(&v_empty[s], 1);  // the pair's MMAs are done with the stage
+        }
+        for (int b = 0; b < C::kSlots; ++b) {
+            mbar_init(&op_full[b], 2 * (kTriConv / 2));  // leader: both CTAs' converters of this K half
+            mbar_init(&op_empty[b], 1);
+        }
+        for (int b = 0; b < C::kBufs; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 2 * kTriDrain);  // leader: both CTAs' drains
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_2sm(&tmem_base_smem, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_smem;
+
+    // registers move only between warpgroups of the CTA: 4x(80-40) + 8x(80-64) = 12x(104-80) per thread
+    if (RB_TRI_SETMAXNREG && warp < kTriConv0) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 || warp == 2) {
+        // ---------------- TMA: A/B tiles of this CTA's rows (warp 0, local ring); its half of the V planes
+        // (warp 2, completing on the leader's barriers). Separate issuers: neither ring's back-pressure
+        // delays the other's loads.
+        if (lane == 0) {
+            const uint64_t pol_stream = args.a_policy ? policy_evict_normal() : policy_evict_first();
+            const uint64_t pol_keep = policy_evict_last();
+            const CUtensorMap* vmap[3][2] = {{&map_va, &map_valo}, {&map_vb, &map_vblo}, {&map_vj, &map_vjlo}};
+            int as = 0, vs = 0;
+            uint32_t aph = 0, vph = 0;
+            TriSegs sg(args, pair, G);
+            int64_t rp;
+            int k0, k1;
+            while (sg.next(rp, k0, k1)) {
+                const int r = static_cast<int>(2 * rp + rank);
+                for (int k = k0; k < k1; ++k) {
+                    if (warp == 0) {
+                        mbar_wait(&ab_empty[as], aph ^ 1u);
+                        uint8_t* st = base + as * C::kABStage;
+                        mbar_arrive_expect_tx(&ab_full[as], C::kABStage);
+                        tma_load_2d(st, &map_ahi, &ab_full[as], k * BK, r * TBM, pol_stream);
+                        tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], k * BK, r * TBM, pol_stream);
+                        tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], k * BK, r * TBM, pol_stream);
+                        tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], k * BK, r * TBM, pol_stream);
+                        if (++as == C::kABStages) as = 0, aph ^= 1u;
+                    } else {
+                        mbar_wait(&v_empty[vs], vph ^ 1u);
+                        if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * C::kVStage);
+                        const uint32_t bar = mapa_shared(&v_full[vs], 0);
+                        uint8_t* vt = base + (v_u32 - base_u32) + vs * C::kVStage;
+                        const int vz = k / args.kt_chunk;
+                        const int vx = (k - vz * args.kt_chunk) * BK;
+#pragma unroll
+                        for (int q = 0; q < 3 * C::kVPer; ++q)  // rows [rank·NPAD/2, +NPAD/2) of every plane
+                            tma_load_3d_2sm(vt + q * C::kVHalf, vmap[q / C::kVPer][q % C::kVPer], bar, vx,
+                                            static_cast<int>(rank) * (NPAD / 2), vz, pol_keep);
+                        if (++vs == C::kVStages) vs = 0, vph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader): M = 256 over the pair, A operands from TMEM ----------------
+        if (leader) {
+            constexpr uint32_t idesc = umma_idesc_f16_f32(2 * TBM, NPAD);
+            const uint64_t dv0 = desc_sw64(v_u32);
+            int vs = 0;
+            uint32_t vph = 0, u = 0, chunk = 0;
+            TriSegs sg(args, pair, G);
+            int64_t rp;
+            int k0, k1;
+            while (sg.next(rp, k0, k1)) {
+                int it = k0;
+                while (it < k1) {
+                    const int cend = min(k1, it + args.kc);
+                    const uint32_t buf = chunk % C::kBufs;
+                    mbar_wait(&acc_empty[buf], ((chunk / C::kBufs) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t d0 = tmem + buf * (3 * NPAD);
+                    const int cstart = it;
+                    for (; it < cend; ++it, ++u) {
+                        mbar_wait(&v_full[vs], vph);
+                        const uint64_t dv = dv0 + static_cast<uint64_t>((vs * C::kVStage) >> 4);
+                        const uint32_t cont = it > cstart ? 1u : 0u;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk) {  // K half kk of the tile: its own operand slot
+                            const uint32_t q = 2 * u + kk, slot = q % C::kSlots;
+                            mbar_wait(&op_full[slot], (q / C::kSlots) & 1u);
+                            tc_fence_after();
+                            const uint32_t ta = tmem + C::kOpCol0 + slot * C::kOpCols;
+                            if (elect_one()) {
+#pragma unroll
+                                for (int o = 0; o < 3; ++o) {
+                                    const uint32_t d = d0 + o * NPAD;
+                                    const uint32_t th = ta + o * 16;  // operand o: hi at +0, lo at +8
+                                    const uint64_t vh = dv + (((o * C::kVPer) * C::kVHalf + kk * 32) >> 4);
+                                    umma2_f16_ts(d, th, vh, idesc, cont | kk);                   // hi·hi
+                                    umma2_f16_ts(d, th + 8, vh, idesc, 1u);                      // lo·hi
+                                    if (VSPLIT) umma2_f16_ts(d, th, vh + (C::kVHalf >> 4), idesc, 1u);  // hi·lo
+                                }
+                                umma2_commit_mc(&op_empty[slot], kBoth);
+                            }
+                            __syncwarp();
+                        }
+                        if (elect_one()) umma2_commit_mc(&v_empty[vs], kBoth);
+                        __syncwarp();
+                        if (++vs == C::kVStages) vs = 0, vph ^= 1u;
+                    }
+                    if (elect_one()) umma2_commit_mc(&acc_full[buf], kBoth);
+                    __syncwarp();
+                    ++chunk;
+                }
+            }
+        }
+    } else if (warp >= kTriConv0 && warp < kTriConv0 + kTriConv) {
+        // ---------------- operand builders: A, B and J = n·(A∘B) into TMEM ----------------
+        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+        const int half = (warp - kTriConv0) / 4;  // K columns [16·half, 16·half + 16) of the tile
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int sw = (row >> 1) & 3;  // 64-byte swizzle: 16-byte chunk c of row r sits at c ^ ((r >> 1) & 3)
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t op_full_l = mapa_shared(&op_full[0], 0);
+        int as = 0;
+        uint32_t aph = 0, u = 0;
+        TriSegs sg(args, pair, G);
+        int64_t rp;
+        int k0, k1;
+        while (sg.next(rp, k0, k1)) {
+            const int64_t grow = args.row0 + (2 * rp + rank) * TBM + row;  // global row (J diagonal)
+            for (int k = k0; k < k1; ++k, ++u) {
+                mbar_wait(&ab_full[as], aph);
+                const uint8_t* src = base + as * C::kABStage + row * 64;
+                uint32_t pa_h[8], pa_l[8], pb_h[8], pb_l[8], jh[8], jl[8];
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    const int po = ((2 * half + c2) ^ sw) * 16;
+                    const uint4 x0 = *reinterpret_cast<const uint4*>(src + po);
+                    const uint4 x1 = *reinterpret_cast<const uint4*>(src + C::kAPlane + po);
+                    const uint4 x2 = *reinterpret_cast<const uint4*>(src + 2 * C::kAPlane + po);
+                    const uint4 x3 = *reinterpret_cast<const uint4*>(src + 3 * C::kAPlane + po);
+                    pa_h[4 * c2] = x0.x, pa_h[4 * c2 + 1] = x0.y, pa_h[4 * c2 + 2] = x0.z, pa_h[4 * c2 + 3] = x0.w;
+                    pa_l[4 * c2] = x1.x, pa_l[4 * c2 + 1] = x1.y, pa_l[4 * c2 + 2] = x1.z, pa_l[4 * c2 + 3] = x1.w;
+                    pb_h[4 * c2] = x2.x, pb_h[4 * c2 + 1] = x2.y, pb_h[4 * c2 + 2] = x2.z, pb_h[4 * c2 + 3] = x2.w;
+                    pb_l[4 * c2] = x3.x, pb_l[4 * c2 + 1] = x3.y, pb_l[4 * c2 + 2] = x3.z, pb_l[4 * c2 + 3] = x3.w;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ab_empty[as]);  // the A/B stage can be refilled
+                if (++as == C::kABStages) as = 0, aph ^= 1u;
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
+                const int64_t e = grow - static_cast<int64_t>(k) * BK - 16 * half;  // J_ii = 1/n (kernel.cpp:98-99)
+                if (e >= 0 && e < 16) {
+                    const int q = static_cast<int>(e);
+                    const uint32_t dh = f2h(make_float2(args.diag, args.diag));
+                    const uint32_t mask = (q & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        if (t == q / 2) {
+                            jh[t] = (jh[t] & ~mask) | (dh & mask);
+                            jl[t] &= ~mask;
+                        }
+                    }
+                }
+                const uint32_t q = 2 * u + half, slot = q % C::kSlots;
+                mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
+                tc_fence_after();
+                const uint32_t ta = tmem + lane_off + C::kOpCol0 + slot * C::kOpCols;
+                tmem_st8(ta, pa_h);
+                tmem_st8(ta + 8, pa_l);
+                tmem_st8(ta + 16, pb_h);
+                tmem_st8(ta + 24, pb_l);
+                tmem_st8(ta + 32, jh);
+                tmem_st8(ta + 40, jl);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(op_full_l + slot * 8);
+            }
+        }
+    } else if (warp >= kTriDrain0) {
+        // ---------------- TMEM drains: operand (warp-12)/4, lane quarter warp%4 ----------------
+        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        const int op = (warp - kTriDrain0) / 4;
+        const int quarter = warp & 3;
+        const int row_local = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + op * NPAD;
+        const uint32_t acc_empty_l = mapa_shared(&acc_empty[0], 0);
+        float acc[NPAD];
+#pragma unroll
+        for (int j = 0; j < NPAD; ++j) acc[j] = 0.f;
+        uint32_t chunk = 0;
+        TriSegs sg(args, pair, G);
+        int64_t rp;
+        int k0, k1;
+        while (sg.next(rp, k0, k1)) {
+            for (int it = k0; it < k1; it += args.kc) {
+                const uint32_t buf = chunk % C::kBufs;
+                mbar_wait(&acc_full[buf], (chunk / C::kBufs) & 1u);
+                tc_fence_after();
+                const uint32_t t0 = lane_base + buf * (3 * NPAD);
+#pragma unroll
+                for (int j0 = 0; j0 < NPAD; j0 += 16) {
+                    float m[16];
+                    tmem_ld16(t0 + j0, m);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(acc_empty_l + buf * 8);
+                ++chunk;
+            }
+            const int64_t slot = sg.slot(rp, static_cast<int>(rank));
+            float* dst = args.partial[op] + (slot * NPAD) * TBM + row_local;
+#pragma unroll
+            for (int j = 0; j < NPAD; ++j) {
+                dst[j * TBM] = acc[j];
+                acc[j] = 0.f;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // the peer is done with the pair's TMEM and barriers
+    if (warp == 1) tmem_dealloc_2sm(tmem, 512);
+}
+
+template <int NPAD, bool VSPLIT>
+cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const SplitPanelView* v,
+                       const StreamKPlan& plan, float* const* partial, int64_t row0, float factor, float diag,
+                       cudaStream_t stream) {
+    using C = TriCfg<NPAD, VSPLIT>;
+    CUtensorMap ma[4], mv[6];
+    const uint32_t vbox = NPAD / 2;  // each CTA of the pair stages half of every V plane's rows
+    static const int promo_env = [] { const char* e = getenv("RB_TRI_PROMO"); return e ? atoi(e) : 128; }();
+    const CUtensorMapL2promotion promo = promo_env == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : promo_env == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                       : promo_env == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, BK, TBM, promo) &&
+              make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, BK, TBM, promo) &&
+              make_map_f16(&ma[2], b.hi, b.cols, b.rows, b.ld * 2ull, BK, TBM, promo) &&
+              make_map_f16(&ma[3], b.lo, b.cols, b.rows, b.ld * 2ull, BK, TBM, promo);
+    for (int o = 0; o < 3 && ok; ++o) {
+        if (VSPLIT != (v[o].vlo != nullptr) || v[o].rpr % BK != 0) return cudaErrorInvalidValue;
+        ok = make_map_v3(&mv[2 * o], v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox) &&
+             make_map_v3(&mv[2 * o + 1], VSPLIT ? v[o].vlo : v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox);
+    }
+    if (!ok) return cudaErrorInvalidValue;
+    if (cudaError_t e =
+            ensure_smem_attr(reinterpret_cast<const void*>(block_av_tri_kernel<NPAD, VSPLIT>), C::kSmemBytes);
+        e != cudaSuccess)
+        return e;
+    TriArgs args;
+    args.total_iters = plan.total_iters;
+    args.k_tiles = plan.k_tiles;
+    args.kt_chunk = static_cast<int>(v[0].rpr / BK);
+    args.kc = plan.kc;
+    args.dp_blocks = plan.dp_blocks;
+    for (int o = 0; o < 3; ++o) args.partial[o] = partial[o];
+    args.row0 = row0;
+    int e = 0;
+    if (!(factor > 0.0f) || std::frexp(factor, &e) != 0.5f) return cudaErrorInvalidValue;  // 2^(e-1)
+    const int ea = (e - 1) / 2, eb = (e - 1) - ea;  // each prescale a normal fp16 power of two
+    if (ea < -14 || eb < -14 || ea > 15 || eb > 15) return cudaErrorInvalidValue;
+    const __half ha = __float2half(std::ldexp(1.0f, ea)), hb = __float2half(std::ldexp(1.0f, eb));
+    const uint32_t ua = __half_as_ushort(ha), ub = __half_as_ushort(hb);
+    args.scale_a = ua | (ua << 16);
+    args.scale_b = ub | (ub << 16);
+    args.diag = diag;
+    static const int pol_env = [] { const char* e = getenv("RB_TRI_POLICY"); return e ? atoi(e) : 0; }();
+    args.a_policy = pol_env;
+    block_av_tri_kernel<NPAD, VSPLIT><<<2 * plan.grid, kTriThreads, C::kSmemBytes, stream>>>(
+        ma[0], ma[1], ma[2], ma[3], mv[0], mv[1], mv[2], mv[3], mv[4], mv[5], args);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int tc_block_rows() { return BM; }
@@ -384,6 +838,47 @@ cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v
         default: return cudaErrorInvalidValue;
     }
 #undef RB_TC_CASE
+}
+
+StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc) {
+    // 128-row blocks, CTA pairs walking the same k tiles (iterations: (row-block-pair, k-tile))
+    StreamKPlan p;
+    p.row_blocks = static_cast<int>((rows + TBM - 1) / TBM);
+    p.k_tiles = static_cast<int>((cols + BK - 1) / BK);
+    const int64_t pair_blocks = (p.row_blocks + 1) / 2;
+    p.total_iters = pair_blocks * p.k_tiles;
+    int pairs = std::max(1, grid / 2);
+    if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
+    p.grid = pairs;
+    p.cluster = 2;
+    p.kc = kc;
+    p.slots = static_cast<int>(2 * (pair_blocks + pairs));
+    p.rows_per_block = TBM;
+    p.dp_blocks = static_cast<int>((pair_blocks / pairs) * pairs);  // whole waves; the remainder stream-K
+    return p;
+}
+
+int tri_max_cols() { return 80; }
+
+cudaError_t launch_block_av_tri(const SplitMatrixView& a, const SplitMatrixView& b, const SplitPanelView* v,
+                                const StreamKPlan& plan, float* const* partial, int64_t row0, double factor,
+                                double diag, cudaStream_t stream) {
+    const int npad = tc_npad(v[0].cols);
+    if (v[1].cols != v[0].cols || v[2].cols != v[0].cols) return cudaErrorInvalidValue;
+    const float f = static_cast<float>(factor), dg = static_cast<float>(diag);
+#define RB_TRI_CASE(N)                                                                               \
+    case N:                                                                                          \
+        return v[0].vlo ? launch_tri<N, true>(a, b, v, plan, partial, row0, f, dg, stream)           \
+                        : launch_tri<N, false>(a, b, v, plan, partial, row0, f, dg, stream);
+    switch (npad) {
+        RB_TRI_CASE(16)
+        RB_TRI_CASE(32)
+        RB_TRI_CASE(48)
+        RB_TRI_CASE(64)
+        RB_TRI_CASE(80)
+        default: return cudaErrorInvalidValue;
+    }
+#undef RB_TRI_CASE
 }
 
 }  // namespace rb

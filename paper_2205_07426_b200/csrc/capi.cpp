@@ -240,6 +240,13 @@ int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode) {
     });
 }
 
+int renyi_ctx_set_fused_mi(renyi_ctx* ctx, int on) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        ctx->ctx.fused_mi = on != 0;
+    });
+}
+
 int renyi_ctx_sync(renyi_ctx* ctx) {
     return guarded([&] {
         need(ctx, "ctx");

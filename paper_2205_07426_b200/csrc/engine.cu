@@ -632,9 +632,11 @@ bool split_operand(const Context& ctx, bool vectors_out) {
 
 class PanelSession {
 public:
+    // ws: the session's buffers (default ctx.ws); tri: the panel is one operand of a fused
+    // mutual-information pass (128-row stream-K plan of launch_block_av_tri)
     PanelSession(Context& ctx, const KernelMatrix& k, const double* x, int64_t ldx, int s, int max_passes,
-                 double* acc_out, double acc_coef0, bool vectors_out)
-        : ctx_(ctx), k_(k), s_(s), max_passes_(max_passes), acc_(acc_out) {
+                 double* acc_out, double acc_coef0, bool vectors_out, PanelWorkspace* ws = nullptr, bool tri = false)
+        : ctx_(ctx), w_(ws ? *ws : ctx.ws), k_(k), s_(s), max_passes_(max_passes), acc_(acc_out) {
         if (s < 1 || s > kMaxPanelCols) fail(kInternal, "panel width must be in [1,128]");
         if (k.world != ctx.world() || k.rank != ctx.rank())
             fail(kInvalidArgument, "kernel matrix was built for a different rank layout");
@@ -643,7 +645,7 @@ public:
         mf_ = k.prec == kMF;
         if (k.prec == kF32) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
-            plan_ = make_streamk_plan(rows_, k.n, grid, ctx.kc);
+            plan_ = tri ? make_tri_plan(rows_, k.n, grid, ctx.kc) : make_streamk_plan(rows_, k.n, grid, ctx.kc);
             npad_ = tc_npad(s);
         } else if (mf_) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
@@ -657,49 +659,49 @@ public:
         R_ = static_cast<int>((rows_ + rpb - 1) / rpb);
         const bool f32 = k.prec != kF64;  // fp32 state for the split and matrix-free paths
         const size_t st = f32 ? sizeof(float) : sizeof(double);
-        for (auto& b : ctx.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
+        for (auto& b : w_.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
         if (f32) {
             const size_t plane = static_cast<size_t>(k.world) * s * ld_ * sizeof(__half);
-            ctx.vhi.ensure(plane);
+            w_.vhi.ensure(plane);
             // rows past n in the last chunk are never written: keep them zero (A's columns there are
             // TMA-zero, but 0 x garbage could be NaN)
-            cuda_check(cudaMemsetAsync(ctx.vhi.as<__half>(), 0, plane, ctx.stream()), "memset");
+            cuda_check(cudaMemsetAsync(w_.vhi.as<__half>(), 0, plane, ctx.stream()), "memset");
             if (split_operand(ctx, vectors_out) && !mf_) {
-                ctx.vlo.ensure(plane);
-                cuda_check(cudaMemsetAsync(ctx.vlo.as<__half>(), 0, plane, ctx.stream()), "memset");
+                w_.vlo.ensure(plane);
+                cuda_check(cudaMemsetAsync(w_.vlo.as<__half>(), 0, plane, ctx.stream()), "memset");
             }
             slice_ = static_cast<size_t>(k.rank) * s * ld_;
         }
         // the matrix-free P·V product takes one fp16 operand plane (P itself is fp16)
-        vlo_ = (k.prec == kF32 && split_operand(ctx, vectors_out)) ? ctx.vlo.as<__half>() : nullptr;
+        vlo_ = (k.prec == kF32 && split_operand(ctx, vectors_out)) ? w_.vlo.as<__half>() : nullptr;
         const size_t P1 = static_cast<size_t>(max_passes) + 1;
-        ctx.stats.ensure(P1 * 3 * std::max(R_, 1) * s * sizeof(double));
-        ctx.red.ensure(P1 * 3 * s * sizeof(double));
-        ctx.cmax.ensure(P1 * s * sizeof(unsigned));
-        ctx.eexp.ensure(P1 * s * sizeof(int));
-        cuda_check(cudaMemsetAsync(ctx.cmax.as<unsigned>(), 0, P1 * s * sizeof(unsigned), ctx.stream()), "memset");
+        w_.stats.ensure(P1 * 3 * std::max(R_, 1) * s * sizeof(double));
+        w_.red.ensure(P1 * 3 * s * sizeof(double));
+        w_.cmax.ensure(P1 * s * sizeof(unsigned));
+        w_.eexp.ensure(P1 * s * sizeof(int));
+        cuda_check(cudaMemsetAsync(w_.cmax.as<unsigned>(), 0, P1 * s * sizeof(unsigned), ctx.stream()), "memset");
         if (f32) {
-            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(float));
+            w_.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(float));
             PrepArgs<float> p{};
             p.x = x, p.ldx = ldx, p.rows = rows_, p.rows_per_block = rpb, p.s = s, p.ld = ld_;
             p.t0 = buf<float>(0);
-            p.cmax0 = ctx.cmax.as<unsigned>();
-            p.stats = ctx.stats.as<double>();
-            p.e0 = ctx.eexp.as<int>();
-            p.vop = ctx.vhi.as<__half>() + slice_;
+            p.cmax0 = w_.cmax.as<unsigned>();
+            p.stats = w_.stats.as<double>();
+            p.e0 = w_.eexp.as<int>();
+            p.vop = w_.vhi.as<__half>() + slice_;
             p.vop_lo = vlo_ ? vlo_ + slice_ : nullptr;
             p.acc = acc_out, p.acc_coef = acc_coef0;
             if (rows_ > 0) launched(ctx, launch_prepare_split_stats(p, ctx.stream()), "prepare");
-            if (ctx.exchange) ctx.exchange->allreduce_max_u32(ctx.cmax.as<unsigned>(), s, ctx.stream());
+            if (ctx.exchange) ctx.exchange->allreduce_max_u32(w_.cmax.as<unsigned>(), s, ctx.stream());
             launched(ctx, launch_prepare_split_planes(p, ctx.stream()), "prepare");  // also writes e0
             gather_planes();
         } else {
-            ctx.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(double));
+            w_.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(double));
             PrepArgs<double> p{};
             p.x = x, p.ldx = ldx, p.rows = rows_, p.rows_per_block = rpb, p.s = s, p.ld = ld_;
             p.t0 = buf<double>(0);
-            p.cmax0 = ctx.cmax.as<unsigned>();
-            p.stats = ctx.stats.as<double>();
+            p.cmax0 = w_.cmax.as<unsigned>();
+            p.stats = w_.stats.as<double>();
             p.acc = acc_out, p.acc_coef = acc_coef0;
             launched(ctx, launch_prepare_f64(p, ctx.stream()), "prepare");
         }
@@ -709,22 +711,36 @@ public:
     void gather_planes() {
         if (!ctx_.exchange || k_.prec == kF64) return;
         const size_t chunk = static_cast<size_t>(s_) * ld_ * sizeof(__half);
-        ctx_.exchange->allgather_inplace(ctx_.vhi.as<__half>(), chunk, ctx_.stream());
+        ctx_.exchange->allgather_inplace(w_.vhi.as<__half>(), chunk, ctx_.stream());
         if (vlo_) ctx_.exchange->allgather_inplace(vlo_, chunk, ctx_.stream());
     }
 
     void step(double a1, double a2, double a3, double acc_coef) {
-        if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
-        const int k = k_done_;
-        const size_t s = static_cast<size_t>(s_);
         if (k_.prec != kF64) {
-            SplitPanelView v{ctx_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world};
+            product();
+            finish(a1, a2, a3, acc_coef);
+        } else {
+            step_f64(a1, a2, a3, acc_coef);
+        }
+    }
+
+    // the operand planes of the next pass, the partial buffer and the plan (fused MI pass)
+    SplitPanelView operand() const { return SplitPanelView{w_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world}; }
+    float* partial() const { return w_.partial.as<float>(); }
+    const StreamKPlan& plan() const { return plan_; }
+    int64_t rows() const { return rows_; }
+
+    // block product of the current pass into the partials (split / matrix-free paths)
+    void product() {
+        if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
+        {
+            SplitPanelView v = operand();
             ctx_.prof_begin();
             if (mf_) {
                 MfMatrixView a{k_.xb.as<__nv_bfloat16>(), k_.xa.as<__nv_bfloat16>(), k_.n, round_up(k_.n, 128), k_.dp,
                                k_.row0, k_.c2};
                 if (rows_ > 0)
-                    launched(ctx_, launch_block_av_mf(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
+                    launched(ctx_, launch_block_av_mf(a, v, plan_, w_.partial.as<float>(), ctx_.stream()),
                              "block_av_mf");
                 ctx_.prof_end();
                 // algorithmic flops (SURVEY §8d matrix-free): 2·n_local·n·(d + s); bytes: X, V, Y
@@ -733,65 +749,82 @@ public:
             } else {
                 SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
                 if (rows_ > 0)
-                    launched(ctx_, launch_block_av_tc(a, v, plan_, ctx_.partial.as<float>(), ctx_.stream()),
+                    launched(ctx_, launch_block_av_tc(a, v, plan_, w_.partial.as<float>(), ctx_.stream()),
                              "block_av_tc");
                 ctx_.prof_end();
                 // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
                 ctx_.prof_account(4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_ + 4.0 * rows_ * s_,
                                   2.0 * rows_ * k_.n * s_);
             }
+        }
+    }
+
+    // pass epilogue over the partials the product left: T_new = a1·(A T) + a2·T + a3·T_prev, next planes
+    void finish(double a1, double a2, double a3, double acc_coef) {
+        if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
+        const int k = k_done_;
+        const size_t s = static_cast<size_t>(s_);
+        {
             EpiArgs<float, float> e{};
-            e.partial = ctx_.partial.as<float>();
+            e.partial = w_.partial.as<float>();
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
             e.cluster = plan_.cluster;
             e.dp_blocks = plan_.dp_blocks;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
-            e.e_cur = ctx_.eexp.as<int>() + k * s;
-            e.e_next = ctx_.eexp.as<int>() + (k + 1) * s;
+            e.e_cur = w_.eexp.as<int>() + k * s;
+            e.e_next = w_.eexp.as<int>() + (k + 1) * s;
             e.unscale = k_.unscale;
-            e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;
-            e.cmax_prev = k > 0 ? ctx_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
-            e.cmax_new = ctx_.cmax.as<unsigned>() + (k + 1) * s;
+            e.cmax_cur = w_.cmax.as<unsigned>() + k * s;
+            e.cmax_prev = k > 0 ? w_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
+            e.cmax_new = w_.cmax.as<unsigned>() + (k + 1) * s;
             e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm;
             e.t_cur = buf<float>(k);
             e.t_prev = k > 0 ? buf<float>(k - 1) : nullptr;
             e.t_new = buf<float>(k + 1);
             e.x0 = buf<float>(0);
-            e.vop = ctx_.vhi.as<__half>() + slice_;
+            e.vop = w_.vhi.as<__half>() + slice_;
             e.vop_lo = vlo_ ? vlo_ + slice_ : nullptr;
-            e.stats = ctx_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
+            e.stats = w_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
             e.acc = acc_, e.acc_coef = acc_coef;
             if (rows_ > 0) launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
             if (ctx_.exchange) {
-                ctx_.exchange->allreduce_max_u32(ctx_.cmax.as<unsigned>() + (k + 1) * s, s, ctx_.stream());
+                ctx_.exchange->allreduce_max_u32(w_.cmax.as<unsigned>() + (k + 1) * s, s, ctx_.stream());
                 gather_planes();
             }
-        } else {
+        }
+        ++k_done_;
+    }
+
+    void step_f64(double a1, double a2, double a3, double acc_coef) {
+        if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
+        const int k = k_done_;
+        const size_t s = static_cast<size_t>(s_);
+        {
             ctx_.prof_begin();
             launched(ctx_,
                      launch_block_av_f64(k_.a64.as<double>(), rows_, k_.n, k_.ld, buf<double>(k), s_, ld_,
-                                         ctx_.partial.as<double>(), ctx_.stream()),
+                                         w_.partial.as<double>(), ctx_.stream()),
                      "block_av_f64");
             ctx_.prof_end();
             ctx_.prof_account(8.0 * rows_ * k_.n + 8.0 * k_.n * s_ + 8.0 * rows_ * s_, 2.0 * rows_ * k_.n * s_);
             EpiArgs<double, double> e{};
-            e.partial = ctx_.partial.as<double>();
+            e.partial = w_.partial.as<double>();
             e.npad = npad_;
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
             e.cluster = plan_.cluster;
             e.dp_blocks = plan_.dp_blocks;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.unscale = 1.0;
-            e.cmax_cur = ctx_.cmax.as<unsigned>() + k * s;
-            e.cmax_prev = k > 0 ? ctx_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
-            e.cmax_new = ctx_.cmax.as<unsigned>() + (k + 1) * s;
+            e.cmax_cur = w_.cmax.as<unsigned>() + k * s;
+            e.cmax_prev = k > 0 ? w_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
+            e.cmax_new = w_.cmax.as<unsigned>() + (k + 1) * s;
             e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm;
             e.t_cur = buf<double>(k);
             e.t_prev = k > 0 ? buf<double>(k - 1) : nullptr;
             e.t_new = buf<double>(k + 1);
             e.x0 = buf<double>(0);
-            e.stats = ctx_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
+            e.stats = w_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
             e.acc = acc_, e.acc_coef = acc_coef;
             launched(ctx_, launch_epilogue_f64(e, ctx_.stream()), "epilogue");
         }
@@ -804,17 +837,17 @@ public:
         const size_t s = static_cast<size_t>(s_);
         if (R_ > 0) {
             launched(ctx_,
-                     launch_reduce_stats(ctx_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
-                                         ctx_.red.as<double>(), ctx_.stream()),
+                     launch_reduce_stats(w_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
+                                         w_.red.as<double>(), ctx_.stream()),
                      "reduce_stats");
         } else {
-            cuda_check(cudaMemsetAsync(ctx_.red.as<double>(), 0, np * 3 * s * sizeof(double), ctx_.stream()),
+            cuda_check(cudaMemsetAsync(w_.red.as<double>(), 0, np * 3 * s * sizeof(double), ctx_.stream()),
                        "memset");
         }
         // row-separable trace partials: one sum over ranks
-        if (ctx_.exchange) ctx_.exchange->allreduce_sum_f64(ctx_.red.as<double>(), np * 3 * s, ctx_.stream());
+        if (ctx_.exchange) ctx_.exchange->allreduce_sum_f64(w_.red.as<double>(), np * 3 * s, ctx_.stream());
         std::vector<double> out(static_cast<size_t>(np) * 3 * s);
-        d2h(ctx_, out.data(), ctx_.red.as<double>(), out.size() * sizeof(double));
+        d2h(ctx_, out.data(), w_.red.as<double>(), out.size() * sizeof(double));
         ctx_.sync();
         return out;
     }
@@ -834,11 +867,12 @@ public:
 private:
     template <typename T>
     T* buf(int k) const {
-        if (k == 0) return ctx_.state[0].as<T>();
-        return ctx_.state[1 + (k - 1) % 3].as<T>();
+        if (k == 0) return w_.state[0].as<T>();
+        return w_.state[1 + (k - 1) % 3].as<T>();
     }
 
     Context& ctx_;
+    PanelWorkspace& w_;
     const KernelMatrix& k_;
     int s_;
     int max_passes_;
@@ -1613,8 +1647,239 @@ EstParams with_seed(const EstParams& p, const char* term) {
     return q;
 }
 
+// ---------------------------------------------------------------- fused mutual information
+// The three terms of I(X;Y) = S(A) + S(B) - S(n·A∘B) (proj/src/measures.cpp:36-46) run their Hutch++
+// estimates in lockstep: every pass is one launch_block_av_tri over A and B that also forms the joint
+// kernel J = n·(A∘B) (proj/src/kernel.cpp:74-108) tile by tile, so J is never stored and each pass reads
+// 8 B per entry instead of 12 B. Per-term arithmetic (probes, recurrences, QR, traces) is unchanged.
+namespace {
+
+struct JointMeta {
+    KernelMatrix k;  // metadata only (no storage): what the sessions and resolve() read
+    double factor = 0.0, diag = 0.0;
+};
+
+JointMeta joint_meta(const KernelMatrix& a, const KernelMatrix& b) {
+    // the same stored representation hadamard_joint() materialises (split planes of J·n·2^14)
+    JointMeta m;
+    KernelMatrix& c = m.k;
+    c.n = a.n, c.row0 = a.row0, c.rows = a.rows, c.ld = a.ld, c.prec = a.prec;
+    c.rpr = a.rpr, c.world = a.world, c.rank = a.rank;
+    const double nd = static_cast<double>(a.n);
+    const double inv_n = 1.0 / nd;
+    c.a_norm = (a.normalized && b.normalized) ? 1.0 : std::max(1.0, a.a_norm * b.a_norm * nd);
+    c.normalized = a.normalized && b.normalized;
+    c.unscale = inv_n / kSplitScale;
+    m.factor = nd * a.unscale * b.unscale / c.unscale;
+    m.diag = inv_n / c.unscale;
+    // the fused kernel prescales A and B by exact powers of two: factor = 2^e up to rounding of n·fl(1/n)
+    int e = 0;
+    const double fr = std::frexp(m.factor, &e);
+    m.factor = std::abs(fr - 0.5) <= 1e-12 ? std::ldexp(1.0, e - 1) : 0.0;  // 0: not fusable
+    return m;
+}
+
+struct Tri {
+    const KernelMatrix* a;
+    const KernelMatrix* b;
+    JointMeta j;
+    const KernelMatrix* op(int i) const { return i == 0 ? a : (i == 1 ? b : &j.k); }
+};
+
+// P lockstep passes over three panels x_i of width s (<= tri_max_cols): sched[i][p] are operand i's
+// recurrence coefficients; last_out[i] (optional) receives T_P
+std::array<PanelResult, 3> run_panel3(Context& ctx, const Tri& t, const double* const* x, int64_t ldx, int s,
+                                      const std::array<std::vector<std::array<double, 3>>, 3>& sched,
+                                      double* const* last_out, int64_t ldo) {
+    const int P = static_cast<int>(sched[0].size());
+    PanelWorkspace* ws[3] = {&ctx.ws, &ctx.ws_aux[0], &ctx.ws_aux[1]};
+    std::array<std::unique_ptr<PanelSession>, 3> ps;
+    for (int i = 0; i < 3; ++i)
+        ps[i] = std::make_unique<PanelSession>(ctx, *t.op(i), x[i], ldx, s, std::max(P, 1), nullptr, 0.0,
+                                               last_out != nullptr, ws[i], true);
+    const KernelMatrix& a = *t.a;
+    const KernelMatrix& b = *t.b;
+    const SplitMatrixView av{a.hi.as<__half>(), a.lo.as<__half>(), a.rows, a.n, a.ld};
+    const SplitMatrixView bv{b.hi.as<__half>(), b.lo.as<__half>(), b.rows, b.n, b.ld};
+    for (int p = 0; p < P; ++p) {
+        const SplitPanelView v[3] = {ps[0]->operand(), ps[1]->operand(), ps[2]->operand()};
+        float* const part[3] = {ps[0]->partial(), ps[1]->partial(), ps[2]->partial()};
+        ctx.prof_begin();
+        if (a.rows > 0)
+            launched(ctx,
+                     launch_block_av_tri(av, bv, v, ps[0]->plan(), part, a.row0, t.j.factor, t.j.diag, ctx.stream()),
+                     "block_av_tri");
+        ctx.prof_end();
+        // algorithmic bytes: A and B (4 B/entry each) + three operand panels + three results
+        ctx.prof_account(8.0 * a.rows * a.n + 3.0 * ((v[0].vlo ? 4.0 : 2.0) * a.n * s + 4.0 * a.rows * s),
+                         3.0 * 2.0 * a.rows * a.n * s);
+        for (int i = 0; i < 3; ++i) ps[i]->finish(sched[i][p][0], sched[i][p][1], sched[i][p][2], 0.0);
+    }
+    std::array<PanelResult, 3> r;
+    for (int i = 0; i < 3; ++i) {
+        if (last_out) ps[i]->state_f64(P, last_out[i], ldo);
+        r[i].passes = P;
+        r[i].s = s;
+        r[i].dots = ps[i]->dots(0, P);
+    }
+    return r;
+}
+
+// per-column traces x_j^T f_i(M_i) x_j of three device panels [cols][ldx] (moment doubling, as panel_traces)
+std::array<std::vector<double>, 3> panel_traces3(Context& ctx, const Tri& t, const std::array<MatFun, 3>& f,
+                                                 const double* const* x, int64_t ldx, int cols) {
+    std::array<std::vector<double>, 3> tr;
+    std::array<std::vector<std::array<double, 3>>, 3> sched;
+    const int passes = (f[0].degree + 1) / 2;
+    for (int i = 0; i < 3; ++i) {
+        tr[i].assign(cols, 0.0);
+        const auto full = schedule(f[i]);
+        sched[i].assign(full.begin(), full.begin() + passes);
+    }
+    const int W = tri_max_cols();
+    for (int j0 = 0; j0 < cols; j0 += W) {
+        const int w = std::min(W, cols - j0);
+        const double* xs[3] = {x[0] + static_cast<int64_t>(j0) * ldx, x[1] + static_cast<int64_t>(j0) * ldx,
+                               x[2] + static_cast<int64_t>(j0) * ldx};
+        const auto r = run_panel3(ctx, t, xs, ldx, w, sched, nullptr, 0);
+        for (int i = 0; i < 3; ++i) {
+            std::vector<double> mu(f[i].degree + 1);
+            for (int j = 0; j < w; ++j) {
+                doubled_moments(f[i], r[i], j, mu.data());
+                tr[i][j0 + j] = f[i].combine(mu.data(), 1);
+            }
+        }
+    }
+    return tr;
+}
+
+// hutchpp() for the three terms in lockstep (main branch; the caller guarantees s_q + s_g < n)
+std::array<TraceEst, 3> hutchpp3(Context& ctx, const Tri& t, const std::array<MatFun, 3>& f,
+                                 const std::array<SketchCfg, 3>& cfg) {
+    const KernelMatrix& k0 = *t.a;
+    const int64_t ld = k0.rpr, rows = k0.rows;
+    const int s_q = cfg[0].s_q, s_g = cfg[0].s_g;
+    std::array<TraceEst, 3> est;
+    std::array<DevBuf, 3> qbuf;
+    std::array<int, 3> rank{0, 0, 0};
+    if (s_q > 0) {
+        std::array<DevBuf, 3> sk, y;
+        for (int i = 0; i < 3; ++i) {
+            make_probes(ctx, *t.op(i), sk[i], s_q, ld, cfg[i].sketch, cfg[i].seed, "hutchpp-sketch",
+                        cfg[i].probe_kind);
+            y[i].alloc(static_cast<size_t>(s_q) * ld * sizeof(double));
+        }
+        const std::array<std::vector<std::array<double, 3>>, 3> one{{{{1.0, 0.0, 0.0}}, {{1.0, 0.0, 0.0}},
+                                                                      {{1.0, 0.0, 0.0}}}};
+        const int W = tri_max_cols();
+        for (int j0 = 0; j0 < s_q; j0 += W) {
+            const int w = std::min(W, s_q - j0);
+            const double* xs[3];
+            double* ys[3];
+            for (int i = 0; i < 3; ++i) {
+                xs[i] = sk[i].as<double>() + j0 * ld;
+                ys[i] = y[i].as<double>() + j0 * ld;
+            }
+            run_panel3(ctx, t, xs, ld, w, one, ys, ld);
+        }
+        for (int i = 0; i < 3; ++i) {
+            rank[i] = orthonormal_range(ctx, y[i].as<double>(), s_q, ld, rows, qbuf[i]);
+            if (rank[i] == 0) fail(kRankCollapse, "hutchpp sketch A*S is numerically zero");
+            est[i].sketch_rank = rank[i];
+            est[i].queries_used = s_q + rank[i] * f[i].query_cost();
+        }
+    }
+    // X0_i = [Q_i | W_i | 0]: one width for the lockstep panels (zero columns trace to zero)
+    const int cols = *std::max_element(rank.begin(), rank.end()) + s_g;
+    std::array<DevBuf, 3> x0;
+    for (int i = 0; i < 3; ++i) {
+        x0[i].alloc(static_cast<size_t>(cols) * ld * sizeof(double));
+        cuda_check(cudaMemsetAsync(x0[i].as<double>(), 0, static_cast<size_t>(cols) * ld * sizeof(double),
+                                   ctx.stream()),
+                   "memset");
+        if (rank[i] > 0)
+            cuda_check(cudaMemcpyAsync(x0[i].as<double>(), qbuf[i].as<double>(),
+                                       static_cast<size_t>(rank[i]) * ld * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       ctx.stream()),
+                       "copy Q");
+        if (s_g > 0) {
+            double* wdst = x0[i].as<double>() + static_cast<int64_t>(rank[i]) * ld;
+            DevBuf gp;
+            make_probes(ctx, *t.op(i), gp, s_g, ld, cfg[i].probes, cfg[i].seed, "hutchpp-probe", cfg[i].probe_kind);
+            if (rank[i] > 0) {
+                std::vector<double> c =
+                    gram_host(ctx, qbuf[i].as<double>(), rank[i], ld, gp.as<double>(), s_g, ld, rows);
+                for (double& v : c) v = -v;
+                update(ctx, 1.0, gp.as<double>(), ld, qbuf[i].as<double>(), rank[i], ld, c, s_g, rows, wdst, ld);
+            } else {
+                cuda_check(cudaMemcpyAsync(wdst, gp.as<double>(), static_cast<size_t>(s_g) * ld * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, ctx.stream()),
+                           "copy probes");
+            }
+            ctx.sync();  // gp is released at scope end
+        }
+    }
+    const double* xs[3] = {x0[0].as<double>(), x0[1].as<double>(), x0[2].as<double>()};
+    const auto tr = panel_traces3(ctx, t, f, xs, ld, cols);
+    for (int i = 0; i < 3; ++i) {
+        double low = 0.0, res = 0.0;
+        for (int j = 0; j < rank[i]; ++j) low += tr[i][j];
+        for (int j = rank[i]; j < rank[i] + s_g; ++j) res += tr[i][j];
+        est[i].low_rank_part = low;
+        est[i].residual_part = s_g > 0 ? res / s_g : 0.0;
+        est[i].queries_used += s_g * f[i].query_cost();
+        est[i].value = est[i].low_rank_part + est[i].residual_part;
+    }
+    return est;
+}
+
+// the fused pass needs no spectrum bounds of J (J is never formed as a matrix)
+bool fused_mi_params(const EstParams& p) {
+    int ai = 0;
+    const bool is_int = integer_alpha(p.alpha, &ai);
+    if (p.method == kMethodExact) return false;
+    return p.has_bounds || (is_int && (p.method == kMethodAuto || p.method == kMethodInt));
+}
+
+bool mutual_information_fused(Context& ctx, const KernelMatrix& a, const KernelMatrix& b, const EstParams& p,
+                              MutualInfo* out) {
+    if (!ctx.fused_mi || !fused_mi_params(p)) return false;
+    if (a.prec != kF32 || b.prec != kF32 || a.n != b.n || a.rows != b.rows || a.row0 != b.row0 || a.ld != b.ld ||
+        a.rpr != b.rpr || a.world != b.world || a.rank != b.rank)
+        return false;
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    Tri t{&a, &b, joint_meta(a, b)};
+    if (t.j.factor == 0.0) return false;
+    const EstParams q[3] = {with_seed(p, "term:vars"), with_seed(p, "term:target"), with_seed(p, "term:joint")};
+    std::array<Resolved, 3> r;
+    std::array<MatFun, 3> f;
+    std::array<SketchCfg, 3> cfg;
+    for (int i = 0; i < 3; ++i) {
+        r[i] = resolve(ctx, *t.op(i), q[i]);
+        f[i] = r[i].f;
+        cfg[i] = sketch_cfg(q[i], r[i].s);
+    }
+    for (int i = 1; i < 3; ++i)
+        if (f[i].degree != f[0].degree || cfg[i].s_q != cfg[0].s_q || cfg[i].s_g != cfg[0].s_g) return false;
+    const int s_q = cfg[0].s_q, s_g = cfg[0].s_g;
+    if (s_q < 0 || s_g < 0 || s_q + s_g < 1) fail(kInvalidArgument, "hutchpp needs a positive query budget");
+    if (static_cast<int64_t>(s_q) + s_g >= a.n) return false;  // exact branches: the sequential path
+    const auto tr = hutchpp3(ctx, t, f, cfg);
+    double h[3];
+    for (int i = 0; i < 3; ++i) h[i] = entropy_of(tr[i], r[i].alpha, r[i].method, r[i].s, r[i].m_used).entropy;
+    out->vars_entropy = h[0];
+    out->target_entropy = h[1];
+    out->joint_entropy = h[2];
+    out->value = h[0] + h[1] - h[2];
+    return true;
+}
+
+}  // namespace
+
 MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelMatrix& b, const EstParams& p) {
     // proj/src/measures.cpp:36-46 (single-variable set: vars_joint = a)
+    MutualInfo fused;
+    if (mutual_information_fused(ctx, a, b, p, &fused)) return fused;
     KernelPtr joint = hadamard_joint(ctx, a, b);
     MutualInfo mi;
     mi.vars_entropy = estimate(ctx, a, with_seed(p, "term:vars")).entropy;
@@ -1648,6 +1913,12 @@ MutualInfo mutual_information_samples_dev(Context& ctx, const double* x, int64_t
                                           double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                           const EstParams& p, int prec) {
     MutualInfo mi;
+    if (prec == kF32 && ctx.fused_mi && fused_mi_params(p)) {
+        // A and B resident together; the joint term is formed inside the fused passes
+        KernelPtr a = build_gaussian_dev(ctx, x, n, dx, ldx, sigma_x, prec);
+        KernelPtr b = build_gaussian_dev(ctx, y, n, dy, ldy, sigma_y, prec);
+        if (mutual_information_fused(ctx, *a, *b, p, &mi)) return mi;
+    }
     {
         KernelPtr a = build_gaussian_dev(ctx, x, n, dx, ldx, sigma_x, prec);
         mi.vars_entropy = estimate(ctx, *a, with_seed(p, "term:vars")).entropy;

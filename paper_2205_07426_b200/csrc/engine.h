@@ -80,6 +80,12 @@ std::unique_ptr<Exchange> make_nccl_exchange(int rank, int world, const unsigned
 // the last chunk shorter. world == 1: row0 = 0, rows = n, rpr = round_up(n, 256).
 void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, int64_t* rpr);
 
+// device buffers of one panel session (recurrence state, operand planes, partials, reductions)
+struct PanelWorkspace {
+    DevBuf partial, stats, red, cmax, eexp;
+    DevBuf state[4], vhi, vlo;
+};
+
 class Context {
 public:
     explicit Context(int device);
@@ -122,8 +128,11 @@ public:
     int world() const { return exchange ? exchange->world() : 1; }
 
     // scratch (grow-only)
-    DevBuf partial, stats, red, cmax, eexp, gram_partial, small, probe_err;
-    DevBuf state[4], vhi, vlo, x0, work, acc;
+    PanelWorkspace ws;         // the panel session's buffers
+    PanelWorkspace ws_aux[2];  // the second and third operand of a fused mutual-information pass
+    bool fused_mi = true;      // mutual information: one pass over A and B for all three terms
+    DevBuf gram_partial, small, probe_err;
+    DevBuf x0, work, acc;
 
 private:
     int device_ = 0;

@@ -62,6 +62,14 @@ int tc_npad(int cols);
 StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc);
 cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream);
+// fused mutual-information pass: Y_A = A·V[0], Y_B = B·V[1], Y_J = J·V[2] with J = n·(A∘B) (J_ii = 1/n)
+// formed from the staged A and B tiles (stored J = factor·stored A·stored B, stored J_ii = diag);
+// 128-row blocks (make_tri_plan), all three panels of the same width <= tri_max_cols()
+StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc);
+int tri_max_cols();
+cudaError_t launch_block_av_tri(const SplitMatrixView& a, const SplitMatrixView& b, const SplitPanelView* v,
+                                const StreamKPlan& plan, float* const* partial, int64_t row0, double factor,
+                                double diag, cudaStream_t stream);
 
 // matrix-free: bf16 samples [n][dp] (dp = 64 or 128, zero padded) and negated bias −b = −c·|x|² [n_pad]
 struct MfMatrixView {
