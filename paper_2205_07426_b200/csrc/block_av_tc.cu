@@ -285,7 +285,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
                   uint32_t box_inner, uint32_t box_outer,
-                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B) {
     TensorMapEncodeFn enc = tensor_map_encoder();
     if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
@@ -293,20 +294,21 @@ bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, promo,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-bool make_map_v3(CUtensorMap* m, const void* base, uint64_t rpr, uint64_t cols, uint64_t world, uint32_t box_rows) {
+bool make_map_v3(CUtensorMap* m, const void* base, uint64_t rpr, uint64_t cols, uint64_t world, uint32_t box_rows,
+                 uint32_t box_k = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B) {
     TensorMapEncodeFn enc = tensor_map_encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {rpr, cols, world};
     cuuint64_t strides[2] = {rpr * 2ull, rpr * cols * 2ull};
-    cuuint32_t box[3] = {BK, box_rows, 1};
+    cuuint32_t box[3] = {box_k, box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -358,11 +360,12 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
 //               hi/lo pairs and stored into TMEM (same values as hadamard_split_kernel up to the fp32 round)
 //   warps 6-17  TMEM drains: operand (warp-6)/4, lane quarter warp%4, fp32 register accumulation
 constexpr int TBM = 128;
+constexpr int TBK = 64;  // k per stage: one 128-byte (SWIZZLE_128B) row of fp16 per TMA request
 constexpr int kTriConv = 8;    // two warpgroups: lane quarter warp%4, K half (warp-4)/4
 constexpr int kTriDrain = 12;  // three warpgroups: operand (warp-12)/4
 constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 #ifndef RB_TRI_AB_STAGES
-#define RB_TRI_AB_STAGES 3
+#define RB_TRI_AB_STAGES 2
 #endif
 #ifndef RB_TRI_SETMAXNREG
 #define RB_TRI_SETMAXNREG 1
@@ -371,10 +374,10 @@ constexpr int kTriThreads = 32 * 24;  // warpgroup 0: TMA (warp 0), MMA (warp 1)
 
 template <int NPAD, bool VSPLIT>
 struct TriCfg {
-    static constexpr int kAPlane = TBM * BK * 2;              // 8 KB: one fp16 plane of 128 rows x 32
+    static constexpr int kAPlane = TBM * TBK * 2;             // 16 KB: one fp16 plane of 128 rows x 64
     static constexpr int kABStage = 4 * kAPlane;              // A_hi, A_lo, B_hi, B_lo
     static constexpr int kVPer = VSPLIT ? 2 : 1;               // V planes per operand
-    static constexpr int kVHalf = (NPAD / 2) * BK * 2;        // this CTA's half of one V plane's rows
+    static constexpr int kVHalf = (NPAD / 2) * TBK * 2;       // this CTA's half of one V plane's rows
     static constexpr int kVStage = 3 * kVPer * kVHalf;
     static constexpr int kABStages = RB_TRI_AB_STAGES;
     static constexpr int kVStagesRaw = (kSmemBudget * 1024 - kABStages * kABStage) / kVStage;
@@ -387,8 +390,8 @@ struct TriCfg {
     static constexpr int kSmemBytes = kABStages * kABStage + kVStages * kVStage + 1024;
     static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 80, "fused MI pass: NPAD in [16, 80]");
     static_assert(kSlots >= 4 && kOpCol0 + kSlots * kOpCols <= 512, "TMEM budget");
-    static_assert(kVStages >= 3, "need a deep enough V ring");
-    static_assert(kVHalf % 512 == 0, "64-byte swizzle atoms");
+    static_assert(kVStages >= 2, "need a V ring");
+    static_assert(kVHalf % 1024 == 0, "128-byte swizzle atoms");
 };
 
 struct TriArgs {
@@ -554,10 +557,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         mbar_wait(&ab_empty[as], aph ^ 1u);
                         uint8_t* st = base + as * C::kABStage;
                         mbar_arrive_expect_tx(&ab_full[as], C::kABStage);
-                        tma_load_2d(st, &map_ahi, &ab_full[as], k * BK, r * TBM, pol_stream);
-                        tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], k * BK, r * TBM, pol_stream);
-                        tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], k * BK, r * TBM, pol_stream);
-                        tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], k * BK, r * TBM, pol_stream);
+                        tma_load_2d(st, &map_ahi, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], k * TBK, r * TBM, pol_stream);
                         if (++as == C::kABStages) as = 0, aph ^= 1u;
                     } else {
                         mbar_wait(&v_empty[vs], vph ^ 1u);
@@ -565,7 +568,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         const uint32_t bar = mapa_shared(&v_full[vs], 0);
                         uint8_t* vt = base + (v_u32 - base_u32) + vs * C::kVStage;
                         const int vz = k / args.kt_chunk;
-                        const int vx = (k - vz * args.kt_chunk) * BK;
+                        const int vx = (k - vz * args.kt_chunk) * TBK;
 #pragma unroll
                         for (int q = 0; q < 3 * C::kVPer; ++q)  // rows [rank·NPAD/2, +NPAD/2) of every plane
                             tma_load_3d_2sm(vt + q * C::kVHalf, vmap[q / C::kVPer][q % C::kVPer], bar, vx,
@@ -579,7 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         // ---------------- MMA issuer (leader): M = 256 over the pair, A operands from TMEM ----------------
         if (leader) {
             constexpr uint32_t idesc = umma_idesc_f16_f32(2 * TBM, NPAD);
-            const uint64_t dv0 = desc_sw64(v_u32);
+            const uint64_t dv0 = umma_desc_sw128(v_u32);
             int vs = 0;
             uint32_t vph = 0, u = 0, chunk = 0;
             TriSegs sg(args, pair, G);
@@ -599,8 +602,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         const uint64_t dv = dv0 + static_cast<uint64_t>((vs * C::kVStage) >> 4);
                         const uint32_t cont = it > cstart ? 1u : 0u;
 #pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk) {  // K half kk of the tile: its own operand slot
-                            const uint32_t q = 2 * u + kk, slot = q % C::kSlots;
+                        for (int kk = 0; kk < TBK / 16; ++kk) {  // K group kk of the tile: its own operand slot
+                            const uint32_t q = (TBK / 16) * u + kk, slot = q % C::kSlots;
                             mbar_wait(&op_full[slot], (q / C::kSlots) & 1u);
                             tc_fence_after();
                             const uint32_t ta = tmem + C::kOpCol0 + slot * C::kOpCols;
@@ -610,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                                     const uint32_t d = d0 + o * NPAD;
                                     const uint32_t th = ta + o * 16;  // operand o: hi at +0, lo at +8
                                     const uint64_t vh = dv + (((o * C::kVPer) * C::kVHalf + kk * 32) >> 4);
-                                    umma2_f16_ts(d, th, vh, idesc, cont | kk);                   // hi·hi
+                                    umma2_f16_ts(d, th, vh, idesc, cont | (kk > 0));             // hi·hi
                                     umma2_f16_ts(d, th + 8, vh, idesc, 1u);                      // lo·hi
                                     if (VSPLIT) umma2_f16_ts(d, th, vh + (C::kVHalf >> 4), idesc, 1u);  // hi·lo
                                 }
@@ -631,12 +634,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
     } else if (warp >= kTriConv0 && warp < kTriConv0 + kTriConv) {
         // ---------------- operand builders: A, B and J = n·(A∘B) into TMEM ----------------
         if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
-        const int half = (warp - kTriConv0) / 4;  // K columns [16·half, 16·half + 16) of the tile
+        const int half = (warp - kTriConv0) / 4;  // K groups {2·half, 2·half + 1} (16 columns each) of the tile
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
-        const int sw = (row >> 1) & 3;  // 64-byte swizzle: 16-byte chunk c of row r sits at c ^ ((r >> 1) & 3)
+        const int sw = row & 7;  // 128-byte swizzle: 16-byte chunk c of row r sits at c ^ (r & 7)
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const uint32_t op_full_l = mapa_shared(&op_full[0], 0);
+        const uint32_t dh = f2h(make_float2(args.diag, args.diag));
         int as = 0;
         uint32_t aph = 0, u = 0;
         TriSegs sg(args, pair, G);
@@ -646,53 +650,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
             const int64_t grow = args.row0 + (2 * rp + rank) * TBM + row;  // global row (J diagonal)
             for (int k = k0; k < k1; ++k, ++u) {
                 mbar_wait(&ab_full[as], aph);
-                const uint8_t* src = base + as * C::kABStage + row * 64;
-                uint32_t pa_h[8], pa_l[8], pb_h[8], pb_l[8], jh[8], jl[8];
+                const uint8_t* src = base + as * C::kABStage + row * 128;
 #pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2) {
-                    const int po = ((2 * half + c2) ^ sw) * 16;
-                    const uint4 x0 = *reinterpret_cast<const uint4*>(src + po);
-                    const uint4 x1 = *reinterpret_cast<const uint4*>(src + C::kAPlane + po);
-                    const uint4 x2 = *reinterpret_cast<const uint4*>(src + 2 * C::kAPlane + po);
-                    const uint4 x3 = *reinterpret_cast<const uint4*>(src + 3 * C::kAPlane + po);
-                    pa_h[4 * c2] = x0.x, pa_h[4 * c2 + 1] = x0.y, pa_h[4 * c2 + 2] = x0.z, pa_h[4 * c2 + 3] = x0.w;
-                    pa_l[4 * c2] = x1.x, pa_l[4 * c2 + 1] = x1.y, pa_l[4 * c2 + 2] = x1.z, pa_l[4 * c2 + 3] = x1.w;
-                    pb_h[4 * c2] = x2.x, pb_h[4 * c2 + 1] = x2.y, pb_h[4 * c2 + 2] = x2.z, pb_h[4 * c2 + 3] = x2.w;
-                    pb_l[4 * c2] = x3.x, pb_l[4 * c2 + 1] = x3.y, pb_l[4 * c2 + 2] = x3.z, pb_l[4 * c2 + 3] = x3.w;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&ab_empty[as]);  // the A/B stage can be refilled
-                if (++as == C::kABStages) as = 0, aph ^= 1u;
+                for (int sub = 0; sub < 2; ++sub) {
+                    const int g = 2 * half + sub;  // K group: columns [16g, 16g + 16) of the tile
+                    uint32_t pa_h[8], pa_l[8], pb_h[8], pb_l[8], jh[8], jl[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
-                const int64_t e = grow - static_cast<int64_t>(k) * BK - 16 * half;  // J_ii = 1/n (kernel.cpp:98-99)
-                if (e >= 0 && e < 16) {
-                    const int q = static_cast<int>(e);
-                    const uint32_t dh = f2h(make_float2(args.diag, args.diag));
-                    const uint32_t mask = (q & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+                    for (int c2 = 0; c2 < 2; ++c2) {
+                        const int po = ((2 * g + c2) ^ sw) * 16;
+                        const uint4 x0 = *reinterpret_cast<const uint4*>(src + po);
+                        const uint4 x1 = *reinterpret_cast<const uint4*>(src + C::kAPlane + po);
+                        const uint4 x2 = *reinterpret_cast<const uint4*>(src + 2 * C::kAPlane + po);
+                        const uint4 x3 = *reinterpret_cast<const uint4*>(src + 3 * C::kAPlane + po);
+                        pa_h[4 * c2] = x0.x, pa_h[4 * c2 + 1] = x0.y, pa_h[4 * c2 + 2] = x0.z, pa_h[4 * c2 + 3] = x0.w;
+                        pa_l[4 * c2] = x1.x, pa_l[4 * c2 + 1] = x1.y, pa_l[4 * c2 + 2] = x1.z, pa_l[4 * c2 + 3] = x1.w;
+                        pb_h[4 * c2] = x2.x, pb_h[4 * c2 + 1] = x2.y, pb_h[4 * c2 + 2] = x2.z, pb_h[4 * c2 + 3] = x2.w;
+                        pb_l[4 * c2] = x3.x, pb_l[4 * c2 + 1] = x3.y, pb_l[4 * c2 + 2] = x3.z, pb_l[4 * c2 + 3] = x3.w;
+                    }
+                    if (sub == 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&ab_empty[as]);  // this warp is done with the A/B stage
+                    }
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        if (t == q / 2) {
-                            jh[t] = (jh[t] & ~mask) | (dh & mask);
-                            jl[t] &= ~mask;
+                    for (int t = 0; t < 8; ++t)
+                        joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
+                    const int64_t e = grow - static_cast<int64_t>(k) * TBK - 16 * g;  // J_ii = 1/n (kernel.cpp:98-99)
+                    if (e >= 0 && e < 16) {
+                        const int q = static_cast<int>(e);
+                        const uint32_t mask = (q & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            if (t == q / 2) {
+                                jh[t] = (jh[t] & ~mask) | (dh & mask);
+                                jl[t] &= ~mask;
+                            }
                         }
                     }
+                    const uint32_t q = (TBK / 16) * u + g, slot = q % C::kSlots;
+                    mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
+                    tc_fence_after();
+                    const uint32_t ta = tmem + lane_off + C::kOpCol0 + slot * C::kOpCols;
+                    tmem_st8(ta, pa_h);
+                    tmem_st8(ta + 8, pa_l);
+                    tmem_st8(ta + 16, pb_h);
+                    tmem_st8(ta + 24, pb_l);
+                    tmem_st8(ta + 32, jh);
+                    tmem_st8(ta + 40, jl);
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(op_full_l + slot * 8);
                 }
-                const uint32_t q = 2 * u + half, slot = q % C::kSlots;
-                mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
-                tc_fence_after();
-                const uint32_t ta = tmem + lane_off + C::kOpCol0 + slot * C::kOpCols;
-                tmem_st8(ta, pa_h);
-                tmem_st8(ta + 8, pa_l);
-                tmem_st8(ta + 16, pb_h);
-                tmem_st8(ta + 24, pb_l);
-                tmem_st8(ta + 32, jh);
-                tmem_st8(ta + 40, jl);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(op_full_l + slot * 8);
+                if (++as == C::kABStages) as = 0, aph ^= 1u;
             }
         }
     } else if (warp >= kTriDrain0) {
@@ -757,14 +766,16 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
                                        : promo_env == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                        : promo_env == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                           : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, BK, TBM, promo) &&
-              make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, BK, TBM, promo) &&
-              make_map_f16(&ma[2], b.hi, b.cols, b.rows, b.ld * 2ull, BK, TBM, promo) &&
-              make_map_f16(&ma[3], b.lo, b.cols, b.rows, b.ld * 2ull, BK, TBM, promo);
+    constexpr CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
+    bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
+              make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
+              make_map_f16(&ma[2], b.hi, b.cols, b.rows, b.ld * 2ull, TBK, TBM, promo, swz) &&
+              make_map_f16(&ma[3], b.lo, b.cols, b.rows, b.ld * 2ull, TBK, TBM, promo, swz);
     for (int o = 0; o < 3 && ok; ++o) {
-        if (VSPLIT != (v[o].vlo != nullptr) || v[o].rpr % BK != 0) return cudaErrorInvalidValue;
-        ok = make_map_v3(&mv[2 * o], v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox) &&
-             make_map_v3(&mv[2 * o + 1], VSPLIT ? v[o].vlo : v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox);
+        if (VSPLIT != (v[o].vlo != nullptr) || v[o].rpr % TBK != 0) return cudaErrorInvalidValue;
+        ok = make_map_v3(&mv[2 * o], v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox, TBK, swz) &&
+             make_map_v3(&mv[2 * o + 1], VSPLIT ? v[o].vlo : v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox, TBK,
+                         swz);
     }
     if (!ok) return cudaErrorInvalidValue;
     if (cudaError_t e =
@@ -774,7 +785,7 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
     TriArgs args;
     args.total_iters = plan.total_iters;
     args.k_tiles = plan.k_tiles;
-    args.kt_chunk = static_cast<int>(v[0].rpr / BK);
+    args.kt_chunk = static_cast<int>(v[0].rpr / TBK);
     args.kc = plan.kc;
     args.dp_blocks = plan.dp_blocks;
     for (int o = 0; o < 3; ++o) args.partial[o] = partial[o];
@@ -844,14 +855,14 @@ StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc) {
     // 128-row blocks, CTA pairs walking the same k tiles (iterations: (row-block-pair, k-tile))
     StreamKPlan p;
     p.row_blocks = static_cast<int>((rows + TBM - 1) / TBM);
-    p.k_tiles = static_cast<int>((cols + BK - 1) / BK);
+    p.k_tiles = static_cast<int>((cols + TBK - 1) / TBK);
     const int64_t pair_blocks = (p.row_blocks + 1) / 2;
     p.total_iters = pair_blocks * p.k_tiles;
     int pairs = std::max(1, grid / 2);
     if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
     p.grid = pairs;
     p.cluster = 2;
-    p.kc = kc;
+    p.kc = std::max(1, kc * BK / TBK);  // the same TMEM accumulation length in columns as the split product
     p.slots = static_cast<int>(2 * (pair_blocks + pairs));
     p.rows_per_block = TBM;
     p.dp_blocks = static_cast<int>((pair_blocks / pairs) * pairs);  // whole waves; the remainder stream-K
