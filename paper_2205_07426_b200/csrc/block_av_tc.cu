@@ -364,6 +364,9 @@ constexpr int TBK = 64;  // k per stage: one 128-byte (SWIZZLE_128B) row of fp16
 constexpr int kTriConv = 8;    // two warpgroups: lane quarter warp%4, K half (warp-4)/4
 constexpr int kTriDrain = 12;  // three warpgroups: operand (warp-12)/4
 constexpr int kTriConv0 = 4, kTriDrain0 = 12;
+#ifndef RB_TRI_SMEM_KB
+#define RB_TRI_SMEM_KB 220
+#endif
 #ifndef RB_TRI_AB_STAGES
 #define RB_TRI_AB_STAGES 2
 #endif
@@ -380,7 +383,7 @@ struct TriCfg {
     static constexpr int kVHalf = (NPAD / 2) * TBK * 2;       // this CTA's half of one V plane's rows
     static constexpr int kVStage = 3 * kVPer * kVHalf;
     static constexpr int kABStages = RB_TRI_AB_STAGES;
-    static constexpr int kVStagesRaw = (kSmemBudget * 1024 - kABStages * kABStage) / kVStage;
+    static constexpr int kVStagesRaw = (RB_TRI_SMEM_KB * 1024 - kABStages * kABStage) / kVStage;
     static constexpr int kVStages = kVStagesRaw > 8 ? 8 : kVStagesRaw;
     static constexpr int kOpCols = 6 * 8;                     // one K=16 slot: A, B, J hi/lo planes (8 cols each)
     static constexpr int kBufs = (2 * 3 * NPAD + 4 * kOpCols <= 512) ? 2 : 1;  // accumulator buffers
@@ -390,7 +393,7 @@ struct TriCfg {
     static constexpr int kSmemBytes = kABStages * kABStage + kVStages * kVStage + 1024;
     static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 80, "fused MI pass: NPAD in [16, 80]");
     static_assert(kSlots >= 4 && kOpCol0 + kSlots * kOpCols <= 512, "TMEM budget");
-    static_assert(kVStages >= 2, "need a V ring");
+    static_assert(kVStages >= 1, "need a V ring");
     static_assert(kVHalf % 1024 == 0, "128-byte swizzle atoms");
 };
 
