@@ -38,20 +38,38 @@ def run_ranks(R, world, fn):
     return out
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_mutual_information_matches_single_rank(R, world):
+def test_sharded_mutual_information_matches_single_rank(R, orc, world, fused):
+    """Both MI paths (fused pass over A and B, or three estimates over a materialised joint)
+    row-sharded: every rank agrees bitwise, each term is within the fp32 contract (1e-4) of the
+    oracle, and within 2e-5 (fused: 5e-5) of the single-rank run. alpha = 1.01 turns trace
+    differences into x100 entropy differences; the fused pass accumulates all three split
+    products in one TMEM accumulator, so its fp32 accumulation order differs most between
+    shardings (measured: <= 4e-5 from the oracle at world 1, 2e-5 at world 2)."""
     n = 2600  # not a multiple of 256: the last shard is short
     x, y = mi_inputs(n, 21)
     x, y = f32(x), f32(y)
     sx, sy = R.GaussianKernel(4.0), R.GaussianKernel(math.sqrt(8.0))
     p = R.EstimatorParams(alpha=1.01, method="chebyshev", s=60, m=40, seed=5, bounds=R.SpectrumBounds(u=0, v=1))
-    ref = R.mutual_information_samples(x, sx, y, sy, p, precision="fp32", ctx=R.Context(0))
-    res = run_ranks(R, world, lambda ctx, rank: R.mutual_information_samples(x, sx, y, sy, p, "fp32", ctx))
+    oref = orc.mutual_information(orc.build_kernel(x, 4.0), orc.build_kernel(y, math.sqrt(8.0)), seed=5,
+                                  alpha=1.01, method="chebyshev", s=60, m=40, bounds=(0.0, 1.0))
+    ctx0 = R.Context(0)
+    ctx0.set_fused_mi(fused)
+    ref = R.mutual_information_samples(x, sx, y, sy, p, precision="fp32", ctx=ctx0)
+
+    def fn(ctx, rank):
+        ctx.set_fused_mi(fused)
+        return R.mutual_information_samples(x, sx, y, sy, p, "fp32", ctx)
+
+    res = run_ranks(R, world, fn)
+    tol = 5e-5 if fused else 2e-5
     for r in res:
         assert r.value == res[0].value  # identical on every rank
         for key in ("vars_entropy", "target_entropy", "joint_entropy"):
             a, b = getattr(r, key), getattr(ref, key)
-            assert abs(a - b) <= 2e-5 * abs(b), (key, a, b)
+            assert abs(a - b) <= tol * abs(b), (key, a, b)
+            assert abs(a - oref[key]) <= 1e-4 * abs(oref[key]), (key, a, oref[key])
 
 
 def test_sharded_hutchpp_and_bounds(R, orc):
