@@ -10,9 +10,12 @@ value   : device-timed throughput with X, Y resident in HBM (CUDA events on the
 e2e     : the same metric through the public C-ABI call with host buffers
           (renyi_mutual_information_samples): H2D of X, Y and the D2H of every
           result inside the timed region
-roofline: dominant kernel = the tcgen05 block product Y = A·V; algorithmic
-          bytes per launch 4·n_local·n + 4·n·s + 4·n_local·s over
-          its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+roofline: dominant kernel = the tcgen05 block product. Default (--fused-mi on):
+          the fused MI pass Y_A = A·V_A, Y_B = B·V_B, Y_J = (nA∘B)·V_J reading A
+          and B once, algorithmic bytes per launch 8·n_local·n + 3·(4·n·s +
+          4·n_local·s); --fused-mi off: one product per matrix, 4·n_local·n +
+          4·n·s + 4·n_local·s; over the launches' CUDA-event
+          durations, against MEASURED_PEAKS.json hbm_gbs
 --impl reference: the CPU restatement of the reference (oracle/, the reference
           itself is unbuildable here) on a bounded row-slab sample of the same
           workload, extrapolated per estimate
@@ -51,6 +54,9 @@ def parse():
     p.add_argument("--seed", type=int, default=2205)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--fused-mi", default="on", choices=["on", "off"],
+                   help="c4: one pass over A and B for all three MI terms (joint formed on the fly) or three "
+                        "separate estimates over a materialised joint")
     p.add_argument("--operand", default="split", choices=["split", "fast", "auto"],
                    help="iterate operand of the block product: fp16 hi+lo (split), hi only (fast), or auto "
                         "(split where vectors are returned, fast for the trace-only passes)")
@@ -266,6 +272,8 @@ def run_ours(args):
     ctx = R.Context(local)
     ctx.set_tuning(0, args.kc)
     ctx.set_operand_mode(args.operand)
+    fused = args.fused_mi == "on"
+    ctx.set_fused_mi(fused)
     if sharded:
         import torch
 
@@ -339,9 +347,11 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     achieved = prof_bytes / (prof_ms / 1e3) / 1e9 if prof_ms > 0 else 0.0
     per_launch_bytes = prof_bytes / max(nprof, 1)
-    traffic = ncu_traffic("fast" if args.operand == "auto" else args.operand)
+    traffic = ncu_traffic("tri" if fused else ("fast" if args.operand == "auto" else args.operand))
+    kernel = ("block_av_tri_kernel (fused MI pass: A, B read once, joint n·A∘B formed in TMEM; tcgen05 "
+              "cta_group::2, A operands from TMEM)" if fused else "block_av_tc_kernel (tcgen05, fp16 hi/lo A)")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "kernel": "block_av_tc_kernel (tcgen05, fp16 hi/lo A)",
+                "traffic": traffic, "peak_source": peak_src, "kernel": kernel,
                 "launches": nprof, "avg_launch_ms": prof_ms / max(nprof, 1),
                 "algorithmic_bytes_per_launch": per_launch_bytes,
                 "share_of_step": prof_ms / ms if ms > 0 else None,
@@ -378,6 +388,10 @@ def run_ours(args):
                                "Hutch++ s=90 (reference split 22+46), Gaussian probes drawn on device",
                    "n": n, "estimates_per_step": 3, "operand": args.operand, "kc": args.kc,
                    "passes_per_estimate": "1 sketch + 30 (degree-60 Chebyshev moments by doubling, DESIGN.md §8)",
+                   "mi_passes": ("fused: the three estimates' passes run in lockstep, each one launch over A and "
+                                 "B (80 GB) with the joint kernel formed on the fly; 31 launches per step"
+                                 if fused else "separate: 31 passes over each of A, B and the materialised joint "
+                                 "(40 GB each); 93 launches per step"),
                    "l2": "inputs larger than L2: each A is 40 GB (n^2 x 4 B) vs 126 MB L2",
                    "parallelism": (f"rowshard x{world}: A split by rows, NCCL all-gather of the operand planes "
                                    "per pass, fp64 trace partials all-reduced per estimate") if sharded else

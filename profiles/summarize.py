@@ -28,6 +28,8 @@ KEYS = {
     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_mufu_pct",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed": "sm_to_l2_request_path_pct",
+    "dram__cycles_active.avg.pct_of_peak_sustained_elapsed": "dram_cycles_active_pct",
 }
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "msecond": 1e-3, "usecond": 1e-6,
          "us": 1e-6, "ns": 1e-9, "nsecond": 1e-9, "Ghz": 1e9, "Mhz": 1e6}
