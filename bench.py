@@ -341,10 +341,31 @@ def run_ours(args):
                "h2d_bytes_per_step": (h1 - h0) // args.steps, "d2h_bytes_per_step": (d1 - d0) // args.steps,
                "ms_per_step": wall * 1e3 / args.steps}
 
+    # ---- the single-matrix product (block_av_tc) on A, when the fused pass is the dominant kernel ----
+    single = None
+    if world == 1 and fused and rank == 0:
+        k = R.build_kernel_dev(d_x.data_ptr(), n, dx, n, sx, "fp32", ctx)
+        v = np.random.default_rng(1).standard_normal((n, 68))
+        R.ops.matmul_panel(k, v)  # warm-up
+        ctx.profile(True)
+        for _ in range(3):
+            R.ops.matmul_panel(k, v)
+        cnt, pms, pbytes, _ = ctx.profile_read()
+        ctx.profile(False)
+        del k
+        single = {"kernel": "block_av_tc_kernel (one matrix, 68 columns, split operand)", "launches": cnt,
+                  "avg_launch_ms": pms / max(cnt, 1), "achieved": pbytes / (pms / 1e3) / 1e9 if pms > 0 else 0.0,
+                  "unit": "GB/s", "traffic": ncu_traffic("split"),
+                  "note": "measured after the timed region on the same A; the unfused MI path (--fused-mi off) "
+                          "runs this kernel 93 times per step"}
+
     if rank != 0:
         return 0
 
     peak, peak_src = measured_peaks()
+    if single:
+        single["peak"] = peak
+        single["frac"] = single["achieved"] / peak
     achieved = prof_bytes / (prof_ms / 1e3) / 1e9 if prof_ms > 0 else 0.0
     per_launch_bytes = prof_bytes / max(nprof, 1)
     traffic = ncu_traffic("tri" if fused else ("fast" if args.operand == "auto" else args.operand))
@@ -398,6 +419,7 @@ def run_ours(args):
                                   (f"replicas x{world} (one independent MI estimate per rank, no collective)"
                                    if world > 1 else "single GPU")},
         "roofline": roofline,
+        "roofline_single_matrix_product": single,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
