@@ -370,6 +370,11 @@ constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 #ifndef RB_TRI_AB_STAGES
 #define RB_TRI_AB_STAGES 2
 #endif
+#ifndef RB_TRI_CP
+// 1: A/B planes reach TMEM by tcgen05.cp.cta_group::2 issued with the MMAs, builders store only J. Measured
+// slower (22.7 vs 20.7 ms per config-4 pass): the A/B stage is then held until the MMAs complete
+#define RB_TRI_CP 0
+#endif
 #ifndef RB_TRI_SETMAXNREG
 #define RB_TRI_SETMAXNREG 1
 #endif
@@ -515,7 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (VSPLIT) prefetch_tmap(&map_valo), prefetch_tmap(&map_vblo), prefetch_tmap(&map_vjlo);
         for (int s = 0; s < C::kABStages; ++s) {
             mbar_init(&ab_full[s], 1);
-            mbar_init(&ab_empty[s], kTriConv);  // this CTA's converters have read the tiles
+            mbar_init(&ab_empty[s], kTriConv + RB_TRI_CP);  // converters read the tiles (+ the pair's copies)
         }
         for (int s = 0; s < C::kVStages; ++s) {
             mbar_init(&v_full[s], 1);   // leader: both CTAs' V halves landed
@@ -586,7 +591,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (leader) {
             constexpr uint32_t idesc = umma_idesc_f16_f32(2 * TBM, NPAD);
             const uint64_t dv0 = umma_desc_sw128(v_u32);
-            int vs = 0;
+            const uint64_t da0 = umma_desc_sw128(base_u32);
+            int vs = 0, as = 0;
             uint32_t vph = 0, u = 0, chunk = 0;
             TriSegs sg(args, pair, G);
             int64_t rp;
@@ -611,6 +617,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                             tc_fence_after();
                             const uint32_t ta = tmem + C::kOpCol0 + slot * C::kOpCols;
                             if (elect_one()) {
+                                if (RB_TRI_CP) {  // A_hi, A_lo, B_hi, B_lo slices of this K group into the slot
+                                    const uint64_t da = da0 + static_cast<uint64_t>((as * C::kABStage + kk * 32) >> 4);
+#pragma unroll
+                                    for (int pl = 0; pl < 4; ++pl)
+                                        tmem_cp2_128x256b(ta + pl * 8, da + ((pl * C::kAPlane) >> 4));
+                                }
 #pragma unroll
                                 for (int o = 0; o < 3; ++o) {
                                     const uint32_t d = d0 + o * NPAD;
@@ -624,9 +636,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                             }
                             __syncwarp();
                         }
-                        if (elect_one()) umma2_commit_mc(&v_empty[vs], kBoth);
+                        if (elect_one()) {
+                            umma2_commit_mc(&v_empty[vs], kBoth);
+                            if (RB_TRI_CP) umma2_commit_mc(&ab_empty[as], kBoth);  // copies done with the A/B stage
+                        }
                         __syncwarp();
                         if (++vs == C::kVStages) vs = 0, vph ^= 1u;
+                        if (++as == C::kABStages) as = 0;
                     }
                     if (elect_one()) umma2_commit_mc(&acc_full[buf], kBoth);
                     __syncwarp();
@@ -693,10 +709,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
                     tc_fence_after();
                     const uint32_t ta = tmem + lane_off + C::kOpCol0 + slot * C::kOpCols;
-                    tmem_st8(ta, pa_h);
-                    tmem_st8(ta + 8, pa_l);
-                    tmem_st8(ta + 16, pb_h);
-                    tmem_st8(ta + 24, pb_l);
+                    if (!RB_TRI_CP) {
+                        tmem_st8(ta, pa_h);
+                        tmem_st8(ta + 8, pa_l);
+                        tmem_st8(ta + 16, pb_h);
+                        tmem_st8(ta + 24, pb_l);
+                    }
                     tmem_st8(ta + 32, jh);
                     tmem_st8(ta + 40, jl);
                     tmem_st_wait();
