@@ -543,7 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_base_smem;
 
-    // registers move only between warpgroups of the CTA: 4x(80-40) + 8x(80-64) = 12x(104-80) per thread
+    // registers move only between warpgroups of the CTA: 4x(80-40) + 8x(80-72) >= 12x(96-80) per thread
     if (RB_TRI_SETMAXNREG && warp < kTriConv0) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 0 || warp == 2) {
         // ---------------- TMA: A/B tiles of this CTA's rows (warp 0, local ring); its half of the V planes
@@ -652,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         }
     } else if (warp >= kTriConv0 && warp < kTriConv0 + kTriConv) {
         // ---------------- operand builders: A, B and J = n·(A∘B) into TMEM ----------------
-        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
         const int half = (warp - kTriConv0) / 4;  // K groups {2·half, 2·half + 1} (16 columns each) of the tile
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
@@ -727,7 +727,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         }
     } else if (warp >= kTriDrain0) {
         // ---------------- TMEM drains: operand (warp-12)/4, lane quarter warp%4 ----------------
-        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");
         const int op = (warp - kTriDrain0) / 4;
         const int quarter = warp & 3;
         const int row_local = quarter * 32 + lane;
@@ -747,12 +747,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                 tc_fence_after();
                 const uint32_t t0 = lane_base + buf * (3 * NPAD);
 #pragma unroll
-                for (int j0 = 0; j0 < NPAD; j0 += 16) {
-                    float m[16];
-                    tmem_ld16(t0 + j0, m);
+                for (int j0 = 0; j0 < NPAD; j0 += 8) {
+                    float m[8];
+                    tmem_ld8(t0 + j0, m);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i];
+                    for (int i = 0; i < 8; ++i) acc[j0 + i] += m[i];
                 }
                 tc_fence_before();
                 __syncwarp();
