@@ -883,7 +883,10 @@ StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc) {
     if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
     p.grid = pairs;
     p.cluster = 2;
-    p.kc = std::max(1, kc * BK / TBK);  // the same TMEM accumulation length in columns as the split product
+    // half the split product's TMEM accumulation length: all three split products land in one accumulator,
+    // whose truncation bias grows with the chunk (config 4 vars entropy: +5e-6 from 256 to 512 columns,
+    // +1.6e-5 more at 1024; the drain cost is invisible in the pass time)
+    p.kc = std::max(1, kc * BK / TBK / 2);
     p.slots = static_cast<int>(2 * (pair_blocks + pairs));
     p.rows_per_block = TBM;
     p.dp_blocks = static_cast<int>((pair_blocks / pairs) * pairs);  // whole waves; the remainder stream-K
