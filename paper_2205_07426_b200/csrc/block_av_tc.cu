@@ -375,6 +375,9 @@ constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 // slower (22.7 vs 20.7 ms per config-4 pass): the A/B stage is then held until the MMAs complete
 #define RB_TRI_CP 0
 #endif
+#ifndef RB_TRI_ABLATE
+#define RB_TRI_ABLATE 0  // timing experiments only: 1 no J arithmetic, 2 no TMEM stores, 3 no MMAs
+#endif
 #ifndef RB_TRI_SETMAXNREG
 #define RB_TRI_SETMAXNREG 1
 #endif
@@ -628,6 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                                     const uint32_t d = d0 + o * NPAD;
                                     const uint32_t th = ta + o * 16;  // operand o: hi at +0, lo at +8
                                     const uint64_t vh = dv + (((o * C::kVPer) * C::kVHalf + kk * 32) >> 4);
+                                    if (RB_TRI_ABLATE == 3) continue;
                                     umma2_f16_ts(d, th, vh, idesc, cont | (kk > 0));             // hi·hi
                                     umma2_f16_ts(d, th + 8, vh, idesc, 1u);                      // lo·hi
                                     if (VSPLIT) umma2_f16_ts(d, th, vh + (C::kVHalf >> 4), idesc, 1u);  // hi·lo
@@ -691,8 +695,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         if (lane == 0) mbar_arrive(&ab_empty[as]);  // this warp is done with the A/B stage
                     }
 #pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
+                    for (int t = 0; t < 8; ++t) {
+                        if (RB_TRI_ABLATE == 1 && NPAD == 80) jh[t] = pa_h[t] ^ pb_h[t], jl[t] = pa_l[t] ^ pb_l[t];
+                        else joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
+                    }
                     const int64_t e = grow - static_cast<int64_t>(k) * TBK - 16 * g;  // J_ii = 1/n (kernel.cpp:98-99)
                     if (e >= 0 && e < 16) {
                         const int q = static_cast<int>(e);
@@ -709,6 +715,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
                     tc_fence_after();
                     const uint32_t ta = tmem + lane_off + C::kOpCol0 + slot * C::kOpCols;
+                    if (RB_TRI_ABLATE == 2 && NPAD == 80) {
+                        if (lane == 99) tmem_st8(ta, jh);  // never: no TMEM stores
+                    } else {
                     if (!RB_TRI_CP) {
                         tmem_st8(ta, pa_h);
                         tmem_st8(ta + 8, pa_l);
@@ -717,6 +726,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     }
                     tmem_st8(ta + 32, jh);
                     tmem_st8(ta + 40, jl);
+                    }
                     tmem_st_wait();
                     tc_fence_before();
                     __syncwarp();
