@@ -350,15 +350,17 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
 // One pass over A and B computes the products of all three MI terms (proj/src/measures.cpp:36-46):
 //   Y_A = A·V_A,   Y_B = B·V_B,   Y_J = J·V_J,   J = n·(A∘B) with J_ii = 1/n (proj/src/kernel.cpp:74-108),
 // J formed tile by tile from the staged A and B planes and never stored: 8 B of HBM per entry instead
-// of 12 B for three separate passes over A, B and a materialised J. Each CTA owns 128 rows (one UMMA
-// M = 128 tile per operand, TMEM: 3 accumulators + the J operand); CTA pairs walk the same k-tiles and
-// multicast the V planes as in block_av_tc_kernel.
-//   warp 0      TMA: A_hi, A_lo, B_hi, B_lo (128 x 32 fp16 each) + this CTA's half of the six V planes
-//   warp 1      MMA issuer: A_hi·[V_A hi|lo] + A_lo·V_A hi, the same for B (operands in smem), then
-//               J_hi·[V_J hi|lo] + J_lo·V_J hi with J from TMEM
-//   warps 2-5   J builders: one row per thread, j = fl(a·b)·2^-14 (+ the FMA remainder) split into fp16
-//               hi/lo pairs and stored into TMEM (same values as hadamard_split_kernel up to the fp32 round)
-//   warps 6-17  TMEM drains: operand (warp-6)/4, lane quarter warp%4, fp32 register accumulation
+// of 12 B for three separate passes over A, B and a materialised J.
+// CTA pairs (cluster of 2, tcgen05 cta_group::2): each CTA owns 128 rows; the leader issues M = 256
+// MMAs whose A operands (A, B and J hi/lo planes) come from each CTA's TMEM and whose B operand (the
+// iterate) is split by rows between the two CTAs' shared memory.
+//   warp 0       TMA: A_hi, A_lo, B_hi, B_lo tiles of this CTA's rows (128 x 64, SWIZZLE_128B, local ring)
+//   warp 1       MMA issuer (leader): per K=16 group and operand hi·hi, lo·hi, hi·lo into one accumulator
+//   warp 2       TMA: this CTA's half of the six V planes (completing on the leader's barriers)
+//   warps 4-11   operand builders (lane quarter warp%4, K half (warp-4)/4): shared memory -> registers ->
+//                A, B planes and J = n·(A∘B) (packed half2 split arithmetic) into a ring of TMEM slots
+//   warps 12-23  TMEM drains: operand (warp-12)/4, fp32 register accumulation every 256 columns
+// setmaxnreg moves registers from warpgroup 0 and the builders to the drains.
 constexpr int TBM = 128;
 constexpr int TBK = 64;  // k per stage: one 128-byte (SWIZZLE_128B) row of fp16 per TMA request
 constexpr int kTriConv = 8;    // two warpgroups: lane quarter warp%4, K half (warp-4)/4
@@ -792,11 +794,9 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
     using C = TriCfg<NPAD, VSPLIT>;
     CUtensorMap ma[4], mv[6];
     const uint32_t vbox = NPAD / 2;  // each CTA of the pair stages half of every V plane's rows
-    static const int promo_env = [] { const char* e = getenv("RB_TRI_PROMO"); return e ? atoi(e) : 128; }();
-    const CUtensorMapL2promotion promo = promo_env == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                                       : promo_env == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                       : promo_env == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    // measured on B200: 128-byte L2 promotion + evict_first for the A/B stream beats 256 B / none and
+    // evict_normal by 2-4 % (profiles/r1_microbench.md)
+    const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     constexpr CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
     bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
               make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
@@ -830,8 +830,7 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
     args.scale_a = ua | (ua << 16);
     args.scale_b = ub | (ub << 16);
     args.diag = diag;
-    static const int pol_env = [] { const char* e = getenv("RB_TRI_POLICY"); return e ? atoi(e) : 0; }();
-    args.a_policy = pol_env;
+    args.a_policy = 0;
     block_av_tri_kernel<NPAD, VSPLIT><<<2 * plan.grid, kTriThreads, C::kSmemBytes, stream>>>(
         ma[0], ma[1], ma[2], ma[3], mv[0], mv[1], mv[2], mv[3], mv[4], mv[5], args);
     return cudaGetLastError();
