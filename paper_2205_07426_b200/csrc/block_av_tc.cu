@@ -36,7 +36,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
-#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
