@@ -368,8 +368,13 @@ constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 #ifndef RB_TRI_SMEM_KB
 #define RB_TRI_SMEM_KB 220
 #endif
-#ifndef RB_TRI_AB_ENTRIES
-#define RB_TRI_AB_ENTRIES 5  // 64-row halves of the A/B tile in flight (32 KB each)
+#ifndef RB_TRI_AB_STAGES
+#define RB_TRI_AB_STAGES 2
+#endif
+#ifndef RB_TRI_CP
+// 1: A/B planes reach TMEM by tcgen05.cp.cta_group::2 issued with the MMAs, builders store only J. Measured
+// slower (22.7 vs 20.7 ms per config-4 pass): the A/B stage is then held until the MMAs complete
+#define RB_TRI_CP 0
 #endif
 #ifndef RB_TRI_ABLATE
 #define RB_TRI_ABLATE 0  // timing experiments only: 1 no J arithmetic, 2 no TMEM stores, 3 no MMAs
@@ -386,17 +391,15 @@ struct TriCfg {
     static constexpr int kVPer = VSPLIT ? 2 : 1;               // V planes per operand
     static constexpr int kVHalf = (NPAD / 2) * TBK * 2;       // this CTA's half of one V plane's rows
     static constexpr int kVStage = 3 * kVPer * kVHalf;
-    static constexpr int kABEntry = kABStage / 2;            // one 64-row half of the tile (4 planes)
-    static constexpr int kAPlaneH = kAPlane / 2;
-    static constexpr int kABStages = RB_TRI_AB_ENTRIES;      // ring of 64-row halves
-    static constexpr int kVStagesRaw = (RB_TRI_SMEM_KB * 1024 - kABStages * kABEntry) / kVStage;
+    static constexpr int kABStages = RB_TRI_AB_STAGES;
+    static constexpr int kVStagesRaw = (RB_TRI_SMEM_KB * 1024 - kABStages * kABStage) / kVStage;
     static constexpr int kVStages = kVStagesRaw > 8 ? 8 : kVStagesRaw;
     static constexpr int kOpCols = 6 * 8;                     // one K=16 slot: A, B, J hi/lo planes (8 cols each)
     static constexpr int kBufs = (2 * 3 * NPAD + 4 * kOpCols <= 512) ? 2 : 1;  // accumulator buffers
     static constexpr int kOpCol0 = kBufs * 3 * NPAD;          // operand slots after the accumulators
     static constexpr int kSlotsRaw = (512 - kOpCol0) / kOpCols;
     static constexpr int kSlots = kSlotsRaw > 8 ? 8 : kSlotsRaw;  // half-stage operand slots in flight
-    static constexpr int kSmemBytes = kABStages * kABEntry + kVStages * kVStage + 1024;
+    static constexpr int kSmemBytes = kABStages * kABStage + kVStages * kVStage + 1024;
     static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 80, "fused MI pass: NPAD in [16, 80]");
     static_assert(kSlots >= 4 && kOpCol0 + kSlots * kOpCols <= 512, "TMEM budget");
     static_assert(kVStages >= 1, "need a V ring");
@@ -513,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
 
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
-    const uint32_t v_u32 = base_u32 + C::kABStages * C::kABEntry;  // V ring after the A/B ring
+    const uint32_t v_u32 = base_u32 + C::kABStages * C::kABStage;  // V ring after the A/B ring
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&map_ahi), prefetch_tmap(&map_alo), prefetch_tmap(&map_bhi), prefetch_tmap(&map_blo);
@@ -521,7 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (VSPLIT) prefetch_tmap(&map_valo), prefetch_tmap(&map_vblo), prefetch_tmap(&map_vjlo);
         for (int s = 0; s < C::kABStages; ++s) {
             mbar_init(&ab_full[s], 1);
-            mbar_init(&ab_empty[s], kTriConv / 2);  // the builders of this half's lane quarters read it
+            mbar_init(&ab_empty[s], kTriConv + RB_TRI_CP);  // converters read the tiles (+ the pair's copies)
         }
         for (int s = 0; s < C::kVStages; ++s) {
             mbar_init(&v_full[s], 1);   // leader: both CTAs' V halves landed
@@ -563,18 +566,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                 const int r = static_cast<int>(2 * rp + rank);
                 for (int k = k0; k < k1; ++k) {
                     if (warp == 0) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {  // rows [64h, 64h + 64) of the tile: their own ring entry
-                            mbar_wait(&ab_empty[as], aph ^ 1u);
-                            uint8_t* st = base + as * C::kABEntry;
-                            const int y = r * TBM + 64 * h;
-                            mbar_arrive_expect_tx(&ab_full[as], C::kABEntry);
-                            tma_load_2d(st, &map_ahi, &ab_full[as], k * TBK, y, pol_stream);
-                            tma_load_2d(st + C::kAPlaneH, &map_alo, &ab_full[as], k * TBK, y, pol_stream);
-                            tma_load_2d(st + 2 * C::kAPlaneH, &map_bhi, &ab_full[as], k * TBK, y, pol_stream);
-                            tma_load_2d(st + 3 * C::kAPlaneH, &map_blo, &ab_full[as], k * TBK, y, pol_stream);
-                            if (++as == C::kABStages) as = 0, aph ^= 1u;
-                        }
+                        mbar_wait(&ab_empty[as], aph ^ 1u);
+                        uint8_t* st = base + as * C::kABStage;
+                        mbar_arrive_expect_tx(&ab_full[as], C::kABStage);
+                        tma_load_2d(st, &map_ahi, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        if (++as == C::kABStages) as = 0, aph ^= 1u;
                     } else {
                         mbar_wait(&v_empty[vs], vph ^ 1u);
                         if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * C::kVStage);
@@ -596,7 +595,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (leader) {
             constexpr uint32_t idesc = umma_idesc_f16_f32(2 * TBM, NPAD);
             const uint64_t dv0 = umma_desc_sw128(v_u32);
-            int vs = 0;
+            const uint64_t da0 = umma_desc_sw128(base_u32);
+            int vs = 0, as = 0;
             uint32_t vph = 0, u = 0, chunk = 0;
             TriSegs sg(args, pair, G);
             int64_t rp;
@@ -621,6 +621,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                             tc_fence_after();
                             const uint32_t ta = tmem + C::kOpCol0 + slot * C::kOpCols;
                             if (elect_one()) {
+                                if (RB_TRI_CP) {  // A_hi, A_lo, B_hi, B_lo slices of this K group into the slot
+                                    const uint64_t da = da0 + static_cast<uint64_t>((as * C::kABStage + kk * 32) >> 4);
+#pragma unroll
+                                    for (int pl = 0; pl < 4; ++pl)
+                                        tmem_cp2_128x256b(ta + pl * 8, da + ((pl * C::kAPlane) >> 4));
+                                }
 #pragma unroll
                                 for (int o = 0; o < 3; ++o) {
                                     const uint32_t d = d0 + o * NPAD;
@@ -635,9 +641,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                             }
                             __syncwarp();
                         }
-                        if (elect_one()) umma2_commit_mc(&v_empty[vs], kBoth);
+                        if (elect_one()) {
+                            umma2_commit_mc(&v_empty[vs], kBoth);
+                            if (RB_TRI_CP) umma2_commit_mc(&ab_empty[as], kBoth);  // copies done with the A/B stage
+                        }
                         __syncwarp();
                         if (++vs == C::kVStages) vs = 0, vph ^= 1u;
+                        if (++as == C::kABStages) as = 0;
                     }
                     if (elect_one()) umma2_commit_mc(&acc_full[buf], kBoth);
                     __syncwarp();
@@ -655,17 +665,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const uint32_t op_full_l = mapa_shared(&op_full[0], 0);
         const uint32_t dh = f2h(make_float2(args.diag, args.diag));
-        uint32_t u = 0;
+        int as = 0;
+        uint32_t aph = 0, u = 0;
         TriSegs sg(args, pair, G);
         int64_t rp;
         int k0, k1;
         while (sg.next(rp, k0, k1)) {
             const int64_t grow = args.row0 + (2 * rp + rank) * TBM + row;  // global row (J diagonal)
             for (int k = k0; k < k1; ++k, ++u) {
-                const uint32_t e = 2 * u + (quarter >> 1);  // ring entry of this lane quarter's 64-row half
-                const uint32_t as = e % C::kABStages;
-                mbar_wait(&ab_full[as], (e / C::kABStages) & 1u);
-                const uint8_t* src = base + as * C::kABEntry + (row & 63) * 128;
+                mbar_wait(&ab_full[as], aph);
+                const uint8_t* src = base + as * C::kABStage + row * 128;
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int g = 2 * half + sub;  // K group: columns [16g, 16g + 16) of the tile
@@ -674,9 +683,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     for (int c2 = 0; c2 < 2; ++c2) {
                         const int po = ((2 * g + c2) ^ sw) * 16;
                         const uint4 x0 = *reinterpret_cast<const uint4*>(src + po);
-                        const uint4 x1 = *reinterpret_cast<const uint4*>(src + C::kAPlaneH + po);
-                        const uint4 x2 = *reinterpret_cast<const uint4*>(src + 2 * C::kAPlaneH + po);
-                        const uint4 x3 = *reinterpret_cast<const uint4*>(src + 3 * C::kAPlaneH + po);
+                        const uint4 x1 = *reinterpret_cast<const uint4*>(src + C::kAPlane + po);
+                        const uint4 x2 = *reinterpret_cast<const uint4*>(src + 2 * C::kAPlane + po);
+                        const uint4 x3 = *reinterpret_cast<const uint4*>(src + 3 * C::kAPlane + po);
                         pa_h[4 * c2] = x0.x, pa_h[4 * c2 + 1] = x0.y, pa_h[4 * c2 + 2] = x0.z, pa_h[4 * c2 + 3] = x0.w;
                         pa_l[4 * c2] = x1.x, pa_l[4 * c2 + 1] = x1.y, pa_l[4 * c2 + 2] = x1.z, pa_l[4 * c2 + 3] = x1.w;
                         pb_h[4 * c2] = x2.x, pb_h[4 * c2 + 1] = x2.y, pb_h[4 * c2 + 2] = x2.z, pb_h[4 * c2 + 3] = x2.w;
@@ -710,10 +719,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     if (RB_TRI_ABLATE == 2 && NPAD == 80) {
                         if (lane == 99) tmem_st8(ta, jh);  // never: no TMEM stores
                     } else {
-                    tmem_st8(ta, pa_h);
-                    tmem_st8(ta + 8, pa_l);
-                    tmem_st8(ta + 16, pb_h);
-                    tmem_st8(ta + 24, pb_l);
+                    if (!RB_TRI_CP) {
+                        tmem_st8(ta, pa_h);
+                        tmem_st8(ta + 8, pa_l);
+                        tmem_st8(ta + 16, pb_h);
+                        tmem_st8(ta + 24, pb_l);
+                    }
                     tmem_st8(ta + 32, jh);
                     tmem_st8(ta + 40, jl);
                     }
@@ -722,6 +733,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(op_full_l + slot * 8);
                 }
+                if (++as == C::kABStages) as = 0, aph ^= 1u;
             }
         }
     } else if (warp >= kTriDrain0) {
@@ -785,10 +797,10 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
     // evict_normal by 2-4 % (profiles/r1_microbench.md)
     const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     constexpr CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
-    bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, TBK, TBM / 2, promo, swz) &&
-              make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, TBK, TBM / 2, promo, swz) &&
-              make_map_f16(&ma[2], b.hi, b.cols, b.rows, b.ld * 2ull, TBK, TBM / 2, promo, swz) &&
-              make_map_f16(&ma[3], b.lo, b.cols, b.rows, b.ld * 2ull, TBK, TBM / 2, promo, swz);
+    bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
+              make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
+              make_map_f16(&ma[2], b.hi, b.cols, b.rows, b.ld * 2ull, TBK, TBM, promo, swz) &&
+              make_map_f16(&ma[3], b.lo, b.cols, b.rows, b.ld * 2ull, TBK, TBM, promo, swz);
     for (int o = 0; o < 3 && ok; ++o) {
         if (VSPLIT != (v[o].vlo != nullptr) || v[o].rpr % TBK != 0) return cudaErrorInvalidValue;
         ok = make_map_v3(&mv[2 * o], v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox, TBK, swz) &&
