@@ -97,3 +97,19 @@ def test_fused_mi_kernel_level_entry(R, orc):
     got = R.mutual_information([kx], ky, p)
     for key in TERMS:
         assert abs(getattr(got, key) - ref[key]) <= 1e-4 * abs(ref[key]), key
+
+
+def test_fused_mi_bitwise_reproducible(R):
+    """Three runs of the fused pass at n = 20000 (157 row blocks, waves plus a stream-K tail) give
+    bitwise identical terms: the partial slots are summed in a fixed order and no ring phase may
+    alias (an A/B ring variant whose consumers could read a stale stage failed exactly this)."""
+    n = 20000
+    x, y = _inputs(n, 1)
+    p = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60, seed=1, s_q=22, s_g=46,
+                          bounds=R.SpectrumBounds(u=0, v=1))
+    ctx = R.Context(0)
+    runs = [R.mutual_information_samples(x, R.GaussianKernel(4.0), y, R.GaussianKernel(math.sqrt(8)), p,
+                                         precision="fp32", ctx=ctx) for _ in range(3)]
+    for r in runs[1:]:
+        for key in TERMS:
+            assert getattr(r, key) == getattr(runs[0], key), key
