@@ -47,7 +47,10 @@ namespace {
 
 constexpr int BM = 256;  // rows per CTA (two UMMA M=128 tiles)
 constexpr int TM = 128;  // UMMA M
-constexpr int BK = 32;   // K per stage: one 64-byte swizzle row of fp16
+#ifndef RB_TC_BK
+#define RB_TC_BK 32
+#endif
+constexpr int BK = RB_TC_BK;  // K per stage: one 64-byte (32) or 128-byte (64) swizzle row of fp16
 constexpr int kThreads = 320;
 #ifndef RB_SMEM_BUDGET_KB
 #define RB_SMEM_BUDGET_KB 220
@@ -70,8 +73,8 @@ struct TcCfg {
                                                          : (kTmemNeed <= 256) ? 256 : 512;
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024;
     static_assert(NPAD % 16 == 0 && NPAD >= 16 && NPAD <= 128, "NPAD must be a multiple of 16 in [16,128]");
-    static_assert(kStages >= 3, "need a deep enough TMA ring");
-    static_assert(kVPlane % 512 == 0, "64-byte swizzle atoms are 512 bytes");
+    static_assert(kStages >= (BK == 32 ? 3 : 2), "need a deep enough TMA ring");
+    static_assert(kVPlane % (BK * 16) == 0, "swizzle atoms are 8 rows");
 };
 
 struct TcArgs {
@@ -92,6 +95,11 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t smem_addr) {
     d |= static_cast<uint64_t>(1) << 46;                      // descriptor version (sm100)
     d |= static_cast<uint64_t>(4) << 61;                      // SWIZZLE_64B
     return d;
+}
+
+// descriptor of the single-matrix kernel's K-major tiles (64- or 128-byte swizzle rows)
+__device__ __forceinline__ uint64_t desc_tc(uint32_t smem_addr) {
+    return BK == 64 ? umma_desc_sw128(smem_addr) : desc_sw64(smem_addr);
 }
 
 template <int NPAD, bool VSPLIT>
@@ -202,14 +210,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint32_t off = kk * 32;  // 16 fp16 along K = 32 bytes
-                            const uint64_t dv = desc_sw64(v + off);
+                            const uint64_t dv = desc_tc(v + off);
 #pragma unroll
                             for (int t = 0; t < BM / TM; ++t) {
                                 const uint32_t acc = (it > cstart || kk > 0) ? 1u : 0u;
                                 const uint32_t d = d0 + t * C::kAccCols;
                                 // A_hi x [V_hi | V_lo]: the two V planes are adjacent in smem (N' = 2N rows)
-                                umma_f16(d, desc_sw64(st + t * C::kATile + off), dv, VSPLIT ? idesc2 : idesc, acc);
-                                umma_f16(d, desc_sw64(st + C::kAPlane + t * C::kATile + off), dv, idesc, 1u);
+                                umma_f16(d, desc_tc(st + t * C::kATile + off), dv, VSPLIT ? idesc2 : idesc, acc);
+                                umma_f16(d, desc_tc(st + C::kAPlane + t * C::kATile + off), dv, idesc, 1u);
                             }
                         }
                         umma_commit_mc(&empty_bar[stage], 0x3);  // release the stage in both CTAs
@@ -322,10 +330,11 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     // measured on B200 (r1): 256-byte L2 promotion + evict_first for the A stream beats no/128-byte
     // promotion and evict_normal by 1-2%
     const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM, promo) &&
-              make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM, promo) &&
-              make_map_v3(&m_v, v.v, v.rpr, v.cols, v.world, vbox) &&
-              make_map_v3(&m_vlo, VSPLIT ? v.vlo : v.v, v.rpr, v.cols, v.world, vbox);
+    constexpr CUtensorMapSwizzle swz_tc = BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM, promo, swz_tc) &&
+              make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM, promo, swz_tc) &&
+              make_map_v3(&m_v, v.v, v.rpr, v.cols, v.world, vbox, BK, swz_tc) &&
+              make_map_v3(&m_vlo, VSPLIT ? v.vlo : v.v, v.rpr, v.cols, v.world, vbox, BK, swz_tc);
     if (v.rpr % BK != 0) return cudaErrorInvalidValue;
     if (!ok) return cudaErrorInvalidValue;
     if (cudaError_t e =
@@ -851,7 +860,7 @@ StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc) {
     if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);
     p.grid = pairs;  // stream-K participants (pairs)
     p.cluster = 2;
-    p.kc = kc;
+    p.kc = std::max(1, kc * 32 / BK);  // kc counts 32-column tiles
     p.slots = static_cast<int>(2 * (pair_blocks + pairs));
     p.rows_per_block = BM;
     return p;
@@ -894,7 +903,7 @@ StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc) {
     // half the split product's TMEM accumulation length: all three split products land in one accumulator,
     // whose truncation bias grows with the chunk (config 4 vars entropy: +5e-6 from 256 to 512 columns,
     // +1.6e-5 more at 1024; the drain cost is invisible in the pass time)
-    p.kc = std::max(1, kc * BK / TBK / 2);
+    p.kc = std::max(1, kc * 32 / TBK / 2);
     p.slots = static_cast<int>(2 * (pair_blocks + pairs));
     p.rows_per_block = TBM;
     p.dp_blocks = static_cast<int>((pair_blocks / pairs) * pairs);  // whole waves; the remainder stream-K
