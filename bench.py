@@ -1,26 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 path on BASELINE.json's headline workload.
+"""Benchmark of the B200 path on BASELINE.json's workloads.
 
-metric  : entropy estimates/sec at n=100k (config 4: mutual information of
-          X (100000x16) and Y = XW + 0.5 noise (100000x8); each step is one MI
-          estimate = three entropy estimates (A, B, normalised A∘B), each a
-          Chebyshev m=60 Hutch++ s=90 estimate, Gram builds included)
-value   : device-timed throughput with X, Y resident in HBM (CUDA events on the
-          engine stream), whole job over all ranks
-e2e     : the same metric through the public C-ABI call with host buffers
-          (renyi_mutual_information_samples): H2D of X, Y and the D2H of every
-          result inside the timed region
-roofline: dominant kernel = the tcgen05 block product. Default (--fused-mi on):
-          the fused MI pass Y_A = A·V_A, Y_B = B·V_B, Y_J = (nA∘B)·V_J reading A
-          and B once, algorithmic bytes per launch 8·n_local·n + 3·(4·n·s +
-          4·n_local·s); --fused-mi off: one product per matrix, 4·n_local·n +
-          4·n·s + 4·n_local·s; over the launches' CUDA-event
-          durations, against MEASURED_PEAKS.json hbm_gbs
---impl reference: the CPU restatement of the reference (oracle/, the reference
-          itself is unbuildable here) on a bounded row-slab sample of the same
-          workload, extrapolated per estimate
+Default (--config c4, BASELINE.json's headline "... at n=100k"): mutual information of
+X (100000x16) and Y = XW + 0.5 noise (100000x8); one step = one MI estimate = three entropy
+estimates (A, B, normalised A∘B), each a Chebyshev m=60 Hutch++ s=90 estimate, Gram builds
+included. --config c1|c2|c3|c5: the other BASELINE configurations, one entropy estimate per step
+(c1: n=2000 fp64 Hutchinson; c2: n=20k fp32 Chebyshev Hutch++; c3: n=50k fp32 Taylor with
+device power iteration for v; c5: n=400k matrix-free bf16).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--samples N]
+value   : device-timed throughput with the samples resident in HBM (CUDA events on the engine
+          stream), whole job over all ranks
+e2e     : the same metric through the public C-ABI call with host buffers (H2D of the samples and
+          the D2H of every result inside the timed region)
+roofline: dominant kernel = the tcgen05 block product (c4: the fused MI pass; c5: the matrix-free
+          product, tensor-bound), algorithmic bytes (or flops) per launch over the launches'
+          CUDA-event durations, against MEASURED_PEAKS.json
+--impl reference: the CPU restatement of the reference (oracle/; the reference itself is
+          unbuildable here) on a bounded row-slab sample of the same workload, extrapolated per
+          estimate and labelled so; c4 also times one FULL (non-extrapolated) config-2 estimate.
+          It maps no product library (inputs from the oracle's RNG).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c5]
 """
 from __future__ import annotations
 
@@ -43,6 +43,38 @@ sys.path.insert(0, str(ROOT))
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 FALLBACK_BF16_TFLOPS = 1590.0
 
+# ---------------------------------------------------------------- the five BASELINE configurations
+# (workloads.py draws the inputs from the reference RNG)
+CONFIGS = {
+    "c1": dict(n=2000, d=10, data="iid", precision="fp64", sigma=math.sqrt(10),
+               params=dict(alpha=2.0, method="int", s=30, probe_kind="rademacher", s_q=0, s_g=30),
+               workload="c1: n=2000 d=10 fp64, alpha=2 tr(A^2) Hutchinson s=30 Rademacher",
+               passes="1 (x.A^2 x = (Ax).(Ax), DESIGN.md §8)", sketch=0, q=0, w=30, cpu_passes=2,
+               metric="entropy estimates/sec at n=2000 (config 1, fp64)"),
+    "c2": dict(n=20000, d=32, data="iid", precision="fp32", sigma=math.sqrt(32),
+               params=dict(alpha=1.5, method="chebyshev", s=60, m=40, probe_kind="rademacher", s_q=20, s_g=40,
+                           bounds=(0.0, 1.0)),
+               workload="c2: n=20000 d=32 fp32, alpha=1.5 Chebyshev[0,1] m=40, Hutch++ 20+40 Rademacher",
+               passes="1 sketch + 20 (degree-40 moments by doubling)", sketch=20, q=20, w=40, cpu_passes=40,
+               metric="entropy estimates/sec at n=20k (config 2)"),
+    "c3": dict(n=50000, d=64, data="mixture10", precision="fp32", sigma=8.0,
+               params=dict(alpha=0.5, method="taylor", s=100, m=30, probe_kind="gaussian", s_q=0, s_g=100),
+               workload="c3: n=50000 d=64 fp32 10-Gaussian mixture, alpha=0.5 Taylor m=30 (v by device power "
+                        "iteration), Hutchinson s=100 Gaussian",
+               passes="power iteration for v and u (<= 2 x 100 GEMV passes) + 15 (degree-30 moments by doubling)",
+               sketch=0, q=0, w=100, cpu_passes=30, cpu_power=200,
+               metric="entropy estimates/sec at n=50k (config 3)"),
+    "c5": dict(n=400000, d=128, data="iid", precision="mf", sigma=math.sqrt(128),
+               params=dict(alpha=3.0, method="int", s=120, probe_kind="gaussian"),
+               workload="c5: n=400000 d=128 sigma=sqrt(d) alpha=3 integer power, Hutch++ s=120 (reference split "
+                        "30+60), Gaussian probes drawn on device, A never stored",
+               passes="1 sketch + 2 (x.A^3 x = (Ax).A(Ax), DESIGN.md §8)", sketch=30, q=30, w=60, cpu_passes=3,
+               metric="entropy estimates/sec at n=400k (config 5, matrix-free)"),
+}
+C4_METRIC = "entropy estimates/sec at n=100k (config 4 MI: 3 estimates per step)"
+C4_WORKLOAD = ("c4: MI n=100000 dx=16 dy=8 sigma=sqrt(d) alpha=1.01 Chebyshev[0,1] m=60 Hutch++ s=90 "
+               "(reference split 22+46), Gaussian probes")
+
 
 def parse():
     p = argparse.ArgumentParser()
@@ -50,7 +82,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--samples", type=int, default=0, help="override n (default: config 4 n = 100000)")
+    p.add_argument("--samples", type=int, default=0, help="override n")
     p.add_argument("--seed", type=int, default=2205)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -61,14 +93,13 @@ def parse():
                    help="iterate operand of the block product: fp16 hi+lo (split), hi only (fast), or auto "
                         "(split where vectors are returned, fast for the trace-only passes)")
     p.add_argument("--kc", type=int, default=16, help="k tiles (x32 columns) per TMEM accumulation chunk")
-    p.add_argument("--config", default="c4", choices=["c4", "c5"],
-                   help="c4 (default, BASELINE headline): MI at n=100k, materialised fp32 A; "
-                        "c5: entropy at n=400k d=128, bf16 matrix-free (tensor-pipe bound)")
+    p.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--mf-kc", type=int, default=8, help="c5: j-blocks (x128) per TMEM accumulation chunk")
     p.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period during the timed region")
     p.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                    help="N > 1: row-shard one estimate over all ranks (NCCL, strong scaling) or run "
                         "independent replicas (weak scaling)")
+    p.add_argument("--slab-rows", type=int, default=32, help="--impl reference: rows per CPU slab sample")
     return p.parse_args()
 
 
@@ -90,39 +121,42 @@ def dist_env():
     return rank, world, local
 
 
-def measured_peaks():
+def _peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
         try:
-            d = json.loads(f.read_text())
-            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+            return json.loads(f.read_text())
         except Exception:
-            pass
+            return {}
+    return {}
+
+
+def measured_peaks():
+    d = _peaks()
+    if "hbm_gbs" in d:
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
 def measured_tensor_peak():
     """bf16 dense TFLOP/s: the sustained (power-capped) figure, since the block product is timed
     inside a seconds-long estimate."""
-    f = ROOT / "MEASURED_PEAKS.json"
-    if f.exists():
-        try:
-            d = json.loads(f.read_text())
-            return float(d["bf16_tflops_sustained"]), "measured (MEASURED_PEAKS.json bf16_tflops_sustained)"
-        except Exception:
-            pass
+    d = _peaks()
+    if "bf16_tflops_sustained" in d:
+        return float(d["bf16_tflops_sustained"]), "measured (MEASURED_PEAKS.json bf16_tflops_sustained)"
     return FALLBACK_BF16_TFLOPS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(operand: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one block-product launch (68-column pass at
-    n=100k) from the committed ncu --set full capture, if present."""
-    f = ROOT / "profiles" / f"r1_ncu_block_av_{operand}.json"
-    if f.exists():
-        try:
-            return json.loads(f.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            return None
+def ncu_traffic(name: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the named kernel capture under
+    profiles/ (newest round first), if present."""
+    for rnd in ("r2", "r1"):
+        f = ROOT / "profiles" / f"{rnd}_ncu_{name}.json"
+        if f.exists():
+            try:
+                return json.loads(f.read_text()).get("dram_bytes_per_launch")
+            except Exception:
+                return None
     return None
 
 
@@ -187,101 +221,263 @@ class ClockSampler:
         return out
 
 
+# ------------------------------------------------------------------ inputs (identical in both arms)
+def entropy_inputs(cfg, n, seed, gen):
+    from workloads import bf16, f32, iid, mixture10
+
+    x = mixture10(n, cfg["d"], seed, gen) if cfg["data"] == "mixture10" else iid(n, cfg["d"], seed, gen)
+    return {"fp64": lambda v: v, "fp32": f32, "mf": bf16}[cfg["precision"]](x)
+
+
+def c4_inputs(n, seed, gen):
+    from workloads import f32, mi_inputs
+
+    x, y = mi_inputs(n, seed, gen=gen)
+    return f32(x), f32(y)
+
+
+def config_dict(args, world, n):
+    """The `config` object, identical for --impl ours and --impl reference on the same arguments."""
+    sharded = world > 1 and args.mode == "sharded"
+    par = (f"rowshard x{world}: A (or K's rows) split by rank, NCCL all-gather of the operand planes per pass"
+           if sharded else (f"replicas x{world}" if world > 1 else "single GPU"))
+    if args.config == "c4":
+        return {"workload": C4_WORKLOAD, "n": n, "estimates_per_step": 3, "seed": args.seed,
+                "passes_per_estimate": "1 sketch + 30 (degree-60 Chebyshev moments by doubling, DESIGN.md §8)",
+                "l2": "inputs larger than L2: each A is 40 GB (n^2 x 4 B) vs 126 MB L2", "parallelism": par}
+    cfg = CONFIGS[args.config]
+    a_bytes = {"fp64": 8, "fp32": 4, "mf": 0}[cfg["precision"]] * n * n
+    l2 = ("A is 32 MB: L2-resident (a latency configuration, SURVEY §8(d))" if a_bytes and a_bytes < 126e6 else
+          (f"inputs larger than L2: A is {a_bytes / 1e9:.1f} GB vs 126 MB L2" if a_bytes else
+           "A never stored; X (102 MB bf16) + operand planes exceed the 126 MB L2"))
+    return {"workload": cfg["workload"], "n": n, "estimates_per_step": 1, "seed": args.seed,
+            "passes_per_estimate": cfg["passes"], "l2": l2, "parallelism": par}
+
+
 # ------------------------------------------------------------------ CPU baseline (oracle restatement)
-def cpu_slab_rate(x, y, sx, sy, h, seed):
-    """Seconds per MI estimate on the host, extrapolated from one h-row slab of each of the three
-    kernels (Gram rows + sketch pass + 60 Chebyshev passes over Q (22 cols) and W (46 cols))."""
+def cpu_slab(args, n, rows, seed_off=0):
+    """Seconds for `rows` rows of one step on the host: kernel rows + the passes of the reference's
+    cost structure (Q and W applied separately as 8-column panels re-streaming the slab). Returns
+    (seconds for the slab, extrapolation factor to one step, threads, description)."""
     from oracle import oracle
 
-    n = x.shape[0]
-    r0 = int(np.random.default_rng(seed).integers(0, max(1, n - h)))
-    xy = np.hstack([x, y])
-    # the joint's slab cost equals a Gram over both feature sets (d = dx + dy) with the same passes
-    secs = [oracle.slab_sample_seconds(x, sx, r0, h, 22, 60, 22, 46),
-            oracle.slab_sample_seconds(y, sy, r0, h, 22, 60, 22, 46),
-            oracle.slab_sample_seconds(xy, math.sqrt(sx * sx + sy * sy), r0, h, 22, 60, 22, 46)]
-    wall = sum(secs)
-    return wall * n / h, wall, oracle.threads()
+    r0 = int(np.random.default_rng(args.seed + seed_off).integers(0, max(1, n - rows)))
+    if args.config == "c4":
+        x, y = c4_inputs(n, args.seed, "oracle")
+        xy = np.hstack([x, y])
+        secs = [oracle.slab_sample_seconds(z, sg, r0, rows, 22, 60, 22, 46)
+                for z, sg in ((x, 4.0), (y, math.sqrt(8.0)), (xy, math.sqrt(16.0 + 8.0)))]
+        desc = (f"rows [r0, r0+{rows}) of each of the 3 kernels (n={n}): kernel rows + sketch pass + 60 Chebyshev "
+                f"passes, Q (22 cols) and W (46 cols) as 8-column panels re-streaming the slab")
+        return sum(secs), n / rows, oracle.threads(), desc
+    cfg = CONFIGS[args.config]
+    x = entropy_inputs(cfg, n, args.seed, "oracle")
+    t = oracle.slab_sample_seconds(x, cfg["sigma"], r0, rows, cfg["sketch"], cfg["cpu_passes"], cfg["q"], cfg["w"])
+    desc = (f"rows [r0, r0+{rows}) of A (n={n}): kernel rows + {'sketch pass + ' if cfg['sketch'] else ''}"
+            f"{cfg['cpu_passes']} passes over Q ({cfg['q']}) and W ({cfg['w']}) as 8-column panels")
+    if cfg.get("cpu_power"):
+        t += oracle.slab_sample_seconds(x, cfg["sigma"], r0, rows, 0, cfg["cpu_power"], 1, 0)
+        desc += f" + {cfg['cpu_power']} power-iteration GEMV passes"
+    return t, n / rows, oracle.threads(), desc
+
+
+def cpu_full_c1(args):
+    """One full config-1 estimate on the host (no extrapolation: A is 32 MB)."""
+    from oracle import oracle
+
+    cfg = CONFIGS["c1"]
+    x = entropy_inputs(cfg, cfg["n"], args.seed, "oracle")
+    t = time.perf_counter()
+    a = oracle.build_kernel(x, cfg["sigma"])
+    oracle.estimate(a, seed=args.seed, **cfg["params"])
+    return time.perf_counter() - t
+
+
+def cpu_full_c2_anchor(args):
+    """One FULL config-2 estimate (n = 20k, dense fp64 A, reference cost structure): the
+    non-extrapolated CPU anchor next to the slab extrapolation."""
+    from oracle import oracle
+
+    cfg = CONFIGS["c2"]
+    x = entropy_inputs(cfg, cfg["n"], args.seed, "oracle")
+    t = time.perf_counter()
+    a = oracle.build_kernel(x, cfg["sigma"])
+    e = oracle.estimate(a, seed=args.seed, **cfg["params"])
+    wall = time.perf_counter() - t
+    return {"config": CONFIGS["c2"]["workload"], "seconds_per_estimate": wall, "estimates_per_s": 1.0 / wall,
+            "entropy": e["entropy"], "cores": oracle.threads(), "extrapolated": False}
 
 
 def run_reference(args):
+    """bench.py --impl reference: the oracle port of the reference on the host cores."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle
-    from workloads import f32, mi_inputs
 
     oracle.build()
-    n = args.samples or 100000
-    x, y = mi_inputs(n, args.seed)
-    x, y = f32(x), f32(y)
-    sx, sy = 4.0, math.sqrt(8.0)
-    h = 64
-    for _ in range(args.warmup):
-        cpu_slab_rate(x, y, sx, sy, h, args.seed)
-    per_mi, walls = [], []
-    for k in range(args.steps):
-        t, wall, threads = cpu_slab_rate(x, y, sx, sy, h, args.seed + k)
-        per_mi.append(t)
-        walls.append(wall)
-    mean_mi = statistics.mean(per_mi)
-    value = 3.0 / mean_mi
-    sample = (f"rows [r0, r0+{h}) of each of the 3 kernels (n={n}): Gram rows + sketch pass + 60 Chebyshev passes, "
-              f"Q (22 cols) and W (46 cols) applied separately as 8-column panels re-streaming the slab "
-              f"(reference cost structure); per-estimate time extrapolated x n/{h}; mean slab wall "
-              f"{statistics.mean(walls):.2f} s")
+    n = args.samples or (100000 if args.config == "c4" else CONFIGS[args.config]["n"])
+    per_step = 3 if args.config == "c4" else 1
+    anchor = cpu_full_c2_anchor(args) if (args.config == "c4" and not args.samples) else None
+    walls, factors = [], []
+    threads, desc = oracle.threads(), ""
+    for k in range(args.warmup + args.steps):
+        if args.config == "c1":
+            wall, factor, desc = cpu_full_c1(args), 1.0, "one full config-1 estimate (fp64 A, 32 MB)"
+        else:
+            wall, factor, threads, desc = cpu_slab(args, n, args.slab_rows, seed_off=k)
+        if k >= args.warmup:
+            walls.append(wall)
+            factors.append(factor)
+    per_est = statistics.mean(w * f for w, f in zip(walls, factors)) / per_step
+    value = 1.0 / per_est
+    extrap = args.config != "c1"
+    sample = desc + (f"; per-estimate time extrapolated x n/{args.slab_rows} (the full fp64 A does not fit host "
+                     "memory at this n)" if extrap else "")
+    metric = C4_METRIC if args.config == "c4" else CONFIGS[args.config]["metric"]
     line = {
-        "impl": "reference",
-        "metric": "entropy estimates/sec at n=100k (config 4 MI: 3 estimates per step)",
-        "value": value, "unit": "estimates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": mean_mi * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference RNG), fp32-rounded samples",
-        "config": {"workload": "c4: MI n=100000 dx=16 dy=8 alpha=1.01 Chebyshev[0,1] m=60 Hutch++ s=90 (22+46)",
-                   "n": n, "parallelism": "host OpenMP (block products parallel over 8-column panels)"},
+        "impl": "reference", "metric": metric, "value": value, "unit": "estimates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(walls) * 1e3,  # the measured (sample) wall per step
+        "ms_per_step_note": ("wall of the bounded sample each step timed; value = extrapolated estimates/s"
+                             if extrap else "wall of one full estimate"),
+        "extrapolated": extrap, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference RNG via the oracle), rounded as the GPU arm's inputs",
+        "config": config_dict(args, 1, n),
+        "impl_note": "host OpenMP restatement of the reference (oracle/), block products as 8-column panels",
         "cpu_baseline": {"value": value, "unit": "estimates/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if anchor:
+        line["full_estimate_anchor"] = anchor
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ------------------------------------------------------------------ our arm
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+# ------------------------------------------------------------------ our arm: shared plumbing
+class Arm:
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
 
-    rank, world, local = dist_env()
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.local = dist_env()
+        if self.world > 1 and not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        torch.cuda.set_device(self.local)
+        import paper_2205_07426_b200 as R
 
-    import paper_2205_07426_b200 as R
-    from workloads import f32, mi_inputs
+        self.R = R
+        self.args = args
+        self.sharded = self.world > 1 and args.mode == "sharded"
+        self.ctx = R.Context(self.local)
+        if self.sharded:
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if self.rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, src=0)
+            self.ctx.init_nccl(self.rank, self.world, bytes(uid.cpu().numpy().tobytes()))
 
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, v):
+        if self.world > 1:
+            t = self.torch.tensor([v], device="cuda", dtype=self.torch.float64)
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+            v = float(t.item())
+        return v
+
+    def timed(self, step, steps):
+        """K steps between barriers: CUDA-event ms on the engine stream (max over ranks), clocks,
+        launches and the block-product profile."""
+        self.barrier()
+        clocks = ClockSampler(self.local, self.args.clock_ms)
+        clocks.start()
+        ctx = self.ctx
+        ctx.profile(True)
+        l0 = ctx.launch_count()
+        ctx.timer_begin()
+        for _ in range(steps):
+            out = step()
+        ms = ctx.timer_end()
+        self.barrier()
+        clk = clocks.stop()
+        launches = ctx.launch_count() - l0
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        return out, self.max_over_ranks(ms), clk, launches, prof
+
+    def e2e(self, call, units_per_step):
+        ctx, steps = self.ctx, self.args.steps
+        h0, d0 = ctx.io_bytes()
+        self.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            call()
+        ctx.sync()
+        self.barrier()
+        wall = self.max_over_ranks(time.perf_counter() - t0)
+        h1, d1 = ctx.io_bytes()
+        return {"value": units_per_step * steps / wall, "unit": "estimates/s",
+                "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
+                "ms_per_step": wall * 1e3 / steps}
+
+
+def roofline_of(prof, ms, bound, kernel, traffic=None):
+    nprof, prof_ms, prof_bytes, prof_flops = prof
+    if bound == "tensor":
+        peak, src = measured_tensor_peak()
+        achieved = prof_flops / (prof_ms / 1e3) / 1e12 if prof_ms > 0 else 0.0
+        unit = "TFLOP/s"
+    else:
+        peak, src = measured_peaks()
+        achieved = prof_bytes / (prof_ms / 1e3) / 1e9 if prof_ms > 0 else 0.0
+        unit = "GB/s"
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": traffic, "peak_source": src, "kernel": kernel, "launches": nprof,
+            "avg_launch_ms": prof_ms / max(nprof, 1), "algorithmic_bytes_per_launch": prof_bytes / max(nprof, 1),
+            "algorithmic_flops_per_launch": prof_flops / max(nprof, 1),
+            "share_of_step": prof_ms / ms if ms > 0 else None,
+            "tflops": prof_flops / (prof_ms / 1e3) / 1e12 if prof_ms > 0 else 0.0}
+
+
+def cpu_baseline_line(args, n, per_step):
+    try:
+        from oracle import oracle
+
+        oracle.build()
+        if args.config == "c1":
+            wall = cpu_full_c1(args)
+            return {"value": 1.0 / wall, "unit": "estimates/s", "cores": oracle.threads(), "kind": "port",
+                    "sample": "one full config-1 estimate (no extrapolation)"}
+        wall, factor, threads, desc = cpu_slab(args, n, 64)
+        return {"value": per_step / (wall * factor), "unit": "estimates/s", "cores": threads, "kind": "port",
+                "sample": f"{desc}; extrapolated x n/64; slab wall {wall:.2f} s", "extrapolated": True}
+    except Exception as exc:  # the baseline is reported, never required
+        return {"value": None, "unit": "estimates/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+
+# ------------------------------------------------------------------ config 4: mutual information
+def run_ours_c4(args):
+    arm = Arm(args)
+    R, ctx, torch = arm.R, arm.ctx, arm.torch
     n = args.samples or 100000
     dx, dy = 16, 8
     sx, sy = R.GaussianKernel(4.0), R.GaussianKernel(math.sqrt(8.0))
-    sharded = world > 1 and args.mode == "sharded"
     # sharded: every rank holds the same X, Y and rows [row0, row0+rows) of each A (one estimate
     # per step over all ranks, strong scaling); replicas: each rank its own seeded X, Y (weak scaling)
-    salt = 0 if sharded else 7919 * rank
-    x, y = mi_inputs(n, args.seed + salt)
-    x, y = f32(x), f32(y)
-    params = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60, seed=args.seed + (0 if sharded else rank),
+    salt = 0 if arm.sharded else 7919 * arm.rank
+    x, y = c4_inputs(n, args.seed + salt, "product")
+    params = R.EstimatorParams(alpha=1.01, method="chebyshev", s=90, m=60,
+                               seed=args.seed + (0 if arm.sharded else arm.rank),
                                bounds=R.SpectrumBounds(u=0.0, v=1.0))
-    ctx = R.Context(local)
     ctx.set_tuning(0, args.kc)
     ctx.set_operand_mode(args.operand)
     fused = args.fused_mi == "on"
     ctx.set_fused_mi(fused)
-    if sharded:
-        import torch
-
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, src=0)
-        ctx.init_nccl(rank, world, bytes(uid.cpu().numpy().tobytes()))
     d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()  # (dx, n) row-major == column-major n x dx
     d_y = torch.from_numpy(np.ascontiguousarray(y.T)).cuda()
     torch.cuda.synchronize()
@@ -293,57 +489,18 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     ctx.sync()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    barrier()
-    clocks = ClockSampler(local, args.clock_ms)
-    clocks.start()
-    ctx.profile(True)
-    l0 = ctx.launch_count()
-    ctx.timer_begin()
-    for _ in range(args.steps):
-        mi = step()
-    ms = ctx.timer_end()
-    barrier()
-    clk = clocks.stop()
-    launches = ctx.launch_count() - l0
-    nprof, prof_ms, prof_bytes, prof_flops = ctx.profile_read()
-    ctx.profile(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    units = 1 if sharded else world  # MI estimates completed per step over the whole job
+    mi, ms, clk, launches, prof = arm.timed(step, args.steps)
+    units = 1 if arm.sharded else arm.world  # MI estimates completed per step over the whole job
     value = 3.0 * args.steps * units / (ms / 1e3)
 
-    # ---- end to end through the public C-ABI call with host buffers ----
     e2e = None
     if not args.no_e2e:
         xf, yf = pinned_colmajor(x), pinned_colmajor(y)  # column-major like the reference's Eigen inputs
-        h0, d0 = ctx.io_bytes()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            R.mutual_information_samples(xf, sx, yf, sy, params, "fp32", ctx)
-        ctx.sync()
-        barrier()
-        wall = time.perf_counter() - t0
-        h1, d1 = ctx.io_bytes()
-        if world > 1:
-            t = torch.tensor([wall], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
-        e2e = {"value": 3.0 * args.steps * units / wall, "unit": "estimates/s",
-               "h2d_bytes_per_step": (h1 - h0) // args.steps, "d2h_bytes_per_step": (d1 - d0) // args.steps,
-               "ms_per_step": wall * 1e3 / args.steps}
+        e2e = arm.e2e(lambda: R.mutual_information_samples(xf, sx, yf, sy, params, "fp32", ctx), 3.0 * units)
 
     # ---- the single-matrix product (block_av_tc) on A, when the fused pass is the dominant kernel ----
     single = None
-    if world == 1 and fused and rank == 0:
+    if arm.world == 1 and fused:
         k = R.build_kernel_dev(d_x.data_ptr(), n, dx, n, sx, "fp32", ctx)
         v = np.random.default_rng(1).standard_normal((n, 68))
         R.ops.matmul_panel(k, v)  # warm-up
@@ -353,77 +510,39 @@ def run_ours(args):
         cnt, pms, pbytes, _ = ctx.profile_read()
         ctx.profile(False)
         del k
+        peak, _ = measured_peaks()
+        ach = pbytes / (pms / 1e3) / 1e9 if pms > 0 else 0.0
         single = {"kernel": "block_av_tc_kernel (one matrix, 68 columns, split operand)", "launches": cnt,
-                  "avg_launch_ms": pms / max(cnt, 1), "achieved": pbytes / (pms / 1e3) / 1e9 if pms > 0 else 0.0,
-                  "unit": "GB/s", "traffic": ncu_traffic("split"),
+                  "avg_launch_ms": pms / max(cnt, 1), "achieved": ach, "unit": "GB/s", "peak": peak,
+                  "frac": ach / peak, "traffic": ncu_traffic("block_av_split"),
                   "note": "measured after the timed region on the same A; the unfused MI path (--fused-mi off) "
                           "runs this kernel 93 times per step"}
-
-    if rank != 0:
+    if arm.rank != 0:
         return 0
 
-    peak, peak_src = measured_peaks()
-    if single:
-        single["peak"] = peak
-        single["frac"] = single["achieved"] / peak
-    achieved = prof_bytes / (prof_ms / 1e3) / 1e9 if prof_ms > 0 else 0.0
-    per_launch_bytes = prof_bytes / max(nprof, 1)
-    traffic = ncu_traffic("tri" if fused else ("fast" if args.operand == "auto" else args.operand))
     kernel = ("block_av_tri_kernel (fused MI pass: A, B read once, joint n·A∘B formed in TMEM; tcgen05 "
               "cta_group::2, A operands from TMEM)" if fused else "block_av_tc_kernel (tcgen05, fp16 hi/lo A)")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "kernel": kernel,
-                "launches": nprof, "avg_launch_ms": prof_ms / max(nprof, 1),
-                "algorithmic_bytes_per_launch": per_launch_bytes,
-                "share_of_step": prof_ms / ms if ms > 0 else None,
-                "tflops": prof_flops / (prof_ms / 1e3) / 1e12 if prof_ms > 0 else 0.0}
-
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            from oracle import oracle
-
-            oracle.build()
-            h = 64
-            t_mi, wall, threads = cpu_slab_rate(x, y, sx.sigma, sy.sigma, h, args.seed)
-            cpu = {"value": 3.0 / t_mi, "unit": "estimates/s", "cores": threads, "kind": "port",
-                   "sample": (f"one {h}-row slab of each of the 3 kernels (Gram rows + sketch + 60 Chebyshev "
-                              f"passes, Q/W separately as 8-column panels), extrapolated x n/{h}; "
-                              f"slab wall {wall:.2f} s")}
-        except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "estimates/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
-
+    traffic = ncu_traffic("block_av_tri" if fused else f"block_av_{'fast' if args.operand == 'auto' else args.operand}")
+    cfg = config_dict(args, arm.world, n)
+    cfg.update({"operand": args.operand, "kc": args.kc,
+                "mi_passes": ("fused: the three estimates' passes run in lockstep, each one launch over A and B "
+                              "(80 GB) with the joint kernel formed on the fly; 31 launches per step" if fused else
+                              "separate: 31 passes over each of A, B and the materialised joint (40 GB each); "
+                              "93 launches per step")})
     line = {
-        "metric": "entropy estimates/sec at n=100k (config 4 MI: 3 estimates per step)",
-        "value": value, "unit": "estimates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None,
-        "dtype": "f32",
+        "metric": C4_METRIC, "value": value, "unit": "estimates/s", "n_gpus": arm.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if arm.sharded else "weak", "vs_baseline": None, "dtype": "f32",
         "dtype_note": ("A stored as an fp16 hi/lo split of A*n*2^14 (4 B/entry, 22-bit significand); iterate "
                        + {"split": "fp16 hi+lo (3 tcgen05 products)", "fast": "fp16 hi (2 products)",
                           "auto": "fp16 hi (2 products) on the trace passes, hi+lo on the Hutch++ sketch"}[args.operand]
-                       + f"; fp32 TMEM accumulate drained every {32 * args.kc} columns; fp32 recurrence state; "
-                         "fp64 trace partials"),
+                       + "; fp32 TMEM accumulate drained in chunks; fp32 recurrence state; fp64 trace partials"),
         "data": "synthetic: X~N(0,1) 100000x16, W~N(0,1) 16x8, Y=XW+0.5N(0,1), reference RNG, fp32-rounded",
-        "config": {"workload": "c4: MI n=100000 dx=16 dy=8 sigma=sqrt(d) alpha=1.01 Chebyshev[0,1] m=60 "
-                               "Hutch++ s=90 (reference split 22+46), Gaussian probes drawn on device",
-                   "n": n, "estimates_per_step": 3, "operand": args.operand, "kc": args.kc,
-                   "passes_per_estimate": "1 sketch + 30 (degree-60 Chebyshev moments by doubling, DESIGN.md §8)",
-                   "mi_passes": ("fused: the three estimates' passes run in lockstep, each one launch over A and "
-                                 "B (80 GB) with the joint kernel formed on the fly; 31 launches per step"
-                                 if fused else "separate: 31 passes over each of A, B and the materialised joint "
-                                 "(40 GB each); 93 launches per step"),
-                   "l2": "inputs larger than L2: each A is 40 GB (n^2 x 4 B) vs 126 MB L2",
-                   "parallelism": (f"rowshard x{world}: A split by rows, NCCL all-gather of the operand planes "
-                                   "per pass, fp64 trace partials all-reduced per estimate") if sharded else
-                                  (f"replicas x{world} (one independent MI estimate per rank, no collective)"
-                                   if world > 1 else "single GPU")},
-        "roofline": roofline,
+        "config": cfg,
+        "roofline": roofline_of(prof, ms, "hbm", kernel, traffic),
         "roofline_single_matrix_product": single,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "gpu_launches_per_step": launches / max(args.steps, 1),
+        "cpu_baseline": None if (arm.world > 1 or args.no_cpu_baseline) else cpu_baseline_line(args, n, 3.0),
+        "e2e": e2e, "gpu_launches": launches, "gpu_launches_per_step": launches / max(args.steps, 1),
         "clocks": clk,
         "result": {"mi": mi.value, "vars": mi.vars_entropy, "target": mi.target_entropy, "joint": mi.joint_entropy},
     }
@@ -431,209 +550,105 @@ def run_ours(args):
     return 0
 
 
-# ------------------------------------------------------------------ config 5 (matrix-free)
-C5_D, C5_S, C5_SQ, C5_SG, C5_ALPHA = 128, 120, 30, 60, 3.0
-
-
-def c5_inputs(n, seed):
-    from workloads import bf16, iid
-
-    return bf16(iid(n, C5_D, seed))  # X ~ N(0,1), bf16 inputs
-
-
-def c5_cpu_rate(x, h, seed):
-    """Seconds per c5 estimate on the host, extrapolated from one h-row slab: kernel rows from X
-    (computed once and reused across passes — the CPU restatement cannot store A at n=400k, so
-    this is a lower bound on a matrix-free CPU pass) + the sketch pass (30 columns) + alpha=3
-    passes over Q (30) and W (60) as 8-column panels."""
-    from oracle import oracle
-
-    n = x.shape[0]
-    r0 = int(np.random.default_rng(seed).integers(0, max(1, n - h)))
-    wall = oracle.slab_sample_seconds(x, math.sqrt(C5_D), r0, h, C5_SQ, int(C5_ALPHA), C5_SQ, C5_SG)
-    return wall * n / h, wall, oracle.threads()
-
-
-def run_reference_c5(args):
-    rank, world, local = dist_env()
-    if rank != 0:
-        return 0
-    from oracle import oracle
-
-    oracle.build()
-    n = args.samples or 400000
-    x = c5_inputs(n, args.seed)
-    h = 64
-    for _ in range(args.warmup):
-        c5_cpu_rate(x, h, args.seed)
-    per, walls = [], []
-    for k in range(args.steps):
-        t, wall, threads = c5_cpu_rate(x, h, args.seed + k)
-        per.append(t)
-        walls.append(wall)
-    mean = statistics.mean(per)
-    value = 1.0 / mean
-    sample = (f"rows [r0, r0+{h}) of A (n={n}, d=128): kernel rows + sketch pass + 3 passes over Q (30) and "
-              f"W (60) as 8-column panels; per-estimate time extrapolated x n/{h}; mean slab wall "
-              f"{statistics.mean(walls):.2f} s")
-    print(json.dumps({
-        "impl": "reference",
-        "metric": "entropy estimates/sec at n=400k (config 5, matrix-free)",
-        "value": value, "unit": "estimates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference RNG), bf16-rounded samples",
-        "config": {"workload": "c5: n=400000 d=128 alpha=3 integer power Hutch++ s=120 (30+60)", "n": n,
-                   "parallelism": "host OpenMP (block products parallel over 8-column panels)"},
-        "cpu_baseline": {"value": value, "unit": "estimates/s", "cores": threads, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
-    return 0
-
-
-def run_ours_c5(args):
-    import torch
-    import torch.distributed as dist
-
-    rank, world, local = dist_env()
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-
-    import paper_2205_07426_b200 as R
-
-    n = args.samples or 400000
-    sigma = math.sqrt(C5_D)
-    sharded = world > 1 and args.mode == "sharded"
-    x = c5_inputs(n, args.seed + (0 if sharded else 7919 * rank))
-    params = R.EstimatorParams(alpha=C5_ALPHA, method="int", s=C5_S, seed=args.seed + (0 if sharded else rank))
-    ctx = R.Context(local)
+# ------------------------------------------------------------------ configs 1, 2, 3, 5: one entropy per step
+def run_ours_entropy(args):
+    arm = Arm(args)
+    R, ctx, torch = arm.R, arm.ctx, arm.torch
+    cfg = CONFIGS[args.config]
+    n = args.samples or cfg["n"]
+    x = entropy_inputs(cfg, n, args.seed + (0 if arm.sharded else 7919 * arm.rank), "product")
+    pr = dict(cfg["params"])
+    bounds = pr.pop("bounds", None)
+    params = R.EstimatorParams(seed=args.seed + (0 if arm.sharded else arm.rank),
+                               bounds=R.SpectrumBounds(u=bounds[0], v=bounds[1]) if bounds else None, **pr)
+    prec = cfg["precision"]
+    ctx.set_tuning(0, args.kc)
+    ctx.set_operand_mode(args.operand)
     ctx.set_matrix_free_chunk(args.mf_kc)
-    if sharded:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, src=0)
-        ctx.init_nccl(rank, world, bytes(uid.cpu().numpy().tobytes()))
-    d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()  # (d, n) row-major == column-major n x d
+    d = cfg["d"]
+    d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()  # column-major n x d
     torch.cuda.synchronize()
 
     def step():
-        return R.entropy_dev(d_x.data_ptr(), n, C5_D, n, sigma, params, "mf", ctx)
+        return R.entropy_dev(d_x.data_ptr(), n, d, n, cfg["sigma"], params, prec, ctx)
 
     for _ in range(args.warmup):
         step()
     ctx.sync()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    barrier()
-    clocks = ClockSampler(local, args.clock_ms)
-    clocks.start()
-    ctx.profile(True)
-    l0 = ctx.launch_count()
-    ctx.timer_begin()
-    for _ in range(args.steps):
-        est = step()
-    ms = ctx.timer_end()
-    barrier()
-    clk = clocks.stop()
-    launches = ctx.launch_count() - l0
-    nprof, prof_ms, prof_bytes, prof_flops = ctx.profile_read()
-    ctx.profile(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    units = 1 if sharded else world
+    est, ms, clk, launches, prof = arm.timed(step, args.steps)
+    units = 1 if arm.sharded else arm.world
     value = args.steps * units / (ms / 1e3)
-
     e2e = None
     if not args.no_e2e:
-        x_host = pinned_colmajor(x)  # the reference's Eigen X is column-major: hand the C ABI that layout
-        h0, d0 = ctx.io_bytes()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            R.entropy(x_host, sigma, params, "mf", ctx)
-        ctx.sync()
-        barrier()
-        wall = time.perf_counter() - t0
-        h1, d1 = ctx.io_bytes()
-        if world > 1:
-            t = torch.tensor([wall], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
-        e2e = {"value": args.steps * units / wall, "unit": "estimates/s",
-               "h2d_bytes_per_step": (h1 - h0) // args.steps, "d2h_bytes_per_step": (d1 - d0) // args.steps,
-               "ms_per_step": wall * 1e3 / args.steps}
-    if rank != 0:
+        xh = pinned_colmajor(x)
+        e2e = arm.e2e(lambda: R.entropy(xh, cfg["sigma"], params, prec, ctx), float(units))
+
+    # phase breakdown after the timed region (same kernels, one estimate): Gram build, spectrum
+    # bounds (c3's power iteration) and the estimator with the bounds supplied
+    phases = None
+    if arm.world == 1:
+        phases = {}
+        ctx.timer_begin()
+        k = R.build_kernel_dev(d_x.data_ptr(), n, d, n, R.GaussianKernel(cfg["sigma"]), prec, ctx)
+        phases["gram_ms"] = ctx.timer_end()
+        if params.bounds is None and params.method in ("taylor", "chebyshev", "auto"):
+            ctx.profile(True)
+            ctx.timer_begin()
+            b = R.estimate_bounds(k, params.power)
+            phases["bounds_ms"] = ctx.timer_end()
+            pn, pms, pbytes, _ = ctx.profile_read()
+            ctx.profile(False)
+            peak, _ = measured_peaks()
+            phases["bounds_iterations"] = b.iterations_used
+            phases["bounds_product_launches"] = pn
+            phases["bounds_product_ms"] = pms
+            phases["bounds_product_frac_hbm"] = (pbytes / (pms / 1e3) / 1e9) / peak if pms > 0 else None
+            pb = R.EstimatorParams(**{**params.__dict__, "bounds": b})
+        else:
+            pb = params
+        ctx.timer_begin()
+        R.estimate(k, pb)
+        phases["estimator_ms"] = ctx.timer_end()
+        del k
+    if arm.rank != 0:
         return 0
-
-    peak, peak_src = measured_tensor_peak()
-    achieved = prof_flops / (prof_ms / 1e3) / 1e12 if prof_ms > 0 else 0.0
-    traffic = ncu_traffic("mf")
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src,
-                "kernel": "block_av_mf_kernel (tcgen05 cta_group::2, kernel entries recomputed from bf16 X)",
-                "launches": nprof, "avg_launch_ms": prof_ms / max(nprof, 1),
-                "algorithmic_flops_per_launch": prof_flops / max(nprof, 1),
-                "flops_formula": "2 * n_local * n * (d + s) per pass (SURVEY §8(d), C5)",
-                "share_of_step": prof_ms / ms if ms > 0 else None,
-                "exp_per_launch": float(n) * n / max(world if sharded else 1, 1)}
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            from oracle import oracle
-
-            oracle.build()
-            h = 64
-            t_est, wall, threads = c5_cpu_rate(x, h, args.seed)
-            cpu = {"value": 1.0 / t_est, "unit": "estimates/s", "cores": threads, "kind": "port",
-                   "sample": (f"one {h}-row slab of A (kernel rows computed once, reused by the sketch pass and "
-                              f"3 passes over Q (30) and W (60) as 8-column panels), extrapolated x n/{h}; "
-                              f"slab wall {wall:.2f} s")}
-        except Exception as exc:
-            cpu = {"value": None, "unit": "estimates/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
-    print(json.dumps({
-        "metric": "entropy estimates/sec at n=400k (config 5, matrix-free)",
-        "value": value, "unit": "estimates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None, "dtype": "bf16",
-        "dtype_note": ("X rounded to bf16; S = X_i X_j^T - |x_i|^2/2 - |x_j|^2/2 on tcgen05 (bf16 in, fp32 TMEM "
-                       "accumulate, norms as 3 bf16 terms in 16 augmented K columns); K = exp2 (MUFU) rounded to "
-                       "fp16 in TMEM; O += K V (fp16 in, fp32 accumulate, drained to fp32 registers every "
-                       f"{128 * args.mf_kc} samples); fp32 recurrence state; fp64 trace partials"),
-        "data": "synthetic: X~N(0,1) 400000x128 from the reference RNG, rounded to bf16",
-        "config": {"workload": "c5: n=400000 d=128 sigma=sqrt(d) alpha=3 integer power, Hutch++ s=120 "
-                               "(reference split 30+60), Gaussian probes drawn on device, A never stored",
-                   "n": n, "estimates_per_step": 1, "mf_kc": args.mf_kc,
-                   "passes_per_estimate": "1 sketch + 2 (x.A^3 x = (Ax).A(Ax), DESIGN.md §8)",
-                   "l2": "X (102 MB bf16) + operand planes (96 MB) exceed the 126 MB L2; the kernel streams them "
-                         "in waves (HBM reads ~8 GB per pass per ncu)",
-                   "parallelism": (f"rowshard x{world}: rows of K split by rank, NCCL all-gather of the operand "
-                                   "planes per pass") if sharded else
-                                  (f"replicas x{world}" if world > 1 else "single GPU, CTA pairs (cluster 2)")},
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "gpu_launches_per_step": launches / max(args.steps, 1),
+    tensor = prec == "mf"
+    kernel = {"mf": "block_av_mf_kernel (tcgen05 cta_group::2, kernel entries recomputed from bf16 X)",
+              "fp32": "block_av_tc_kernel (tcgen05, fp16 hi/lo A)",
+              "fp64": "block_av_f64_kernel (fp64 SIMT, A L2-resident)"}[prec]
+    traffic = ncu_traffic({"mf": "block_av_mf", "fp32": "block_av_split", "fp64": "block_av_f64"}[prec]) \
+        if args.config == "c5" else ncu_traffic(f"block_av_{args.config}")
+    roof = roofline_of(prof, ms, "tensor" if tensor else "hbm", kernel, traffic)
+    if tensor:
+        roof["flops_formula"] = "2 * n_local * n * (d + s) per pass (SURVEY §8(d), C5)"
+        roof["exp_per_launch"] = float(n) * n / max(arm.world if arm.sharded else 1, 1)
+    else:
+        roof["bytes_formula"] = "e_A * n_local * n + e_V * n * s + e_Y * n_local * s per pass (SURVEY §8(d))"
+    if args.config == "c1":
+        roof["note"] = "A (32 MB) is L2-resident: a latency configuration; the HBM fraction is not a bound"
+    line = {
+        "metric": cfg["metric"], "value": value, "unit": "estimates/s", "n_gpus": arm.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if arm.sharded else "weak", "vs_baseline": None,
+        "dtype": {"fp64": "f64", "fp32": "f32", "mf": "bf16"}[prec],
+        "data": f"synthetic ({cfg['data']}, reference RNG), {prec} samples",
+        "config": config_dict(args, arm.world, n),
+        "roofline": roof, "phases": phases,
+        "cpu_baseline": None if (arm.world > 1 or args.no_cpu_baseline) else cpu_baseline_line(args, n, 1.0),
+        "e2e": e2e, "gpu_launches": launches, "gpu_launches_per_step": launches / max(args.steps, 1),
         "clocks": clk,
-        "result": {"entropy": est.entropy, "trace_estimate": est.trace_estimate, "s_used": est.s_used},
-    }), flush=True)
+        "result": {"entropy": est.entropy, "trace_estimate": est.trace_estimate, "s_used": est.s_used,
+                   "v": est.bounds_used.v if est.bounds_used else None},
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 
 def main():
     args = parse()
-    if args.config == "c5":
-        return run_reference_c5(args) if args.impl == "reference" else run_ours_c5(args)
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    return run_ours_c4(args) if args.config == "c4" else run_ours_entropy(args)
 
 
 if __name__ == "__main__":

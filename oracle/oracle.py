@@ -9,6 +9,7 @@ Parity status: pinned by the reference's own analytic known-answer tests
 from __future__ import annotations
 
 import ctypes as C
+import os
 import subprocess
 from dataclasses import dataclass
 from pathlib import Path
@@ -50,6 +51,7 @@ class OracleError(RuntimeError):
 
 
 _lib = None
+MUL_FN = C.CFUNCTYPE(C.c_int, C.c_int64, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double))
 KINDS = {"int": 0, "int_power": 0, "taylor": 1, "chebyshev": 2}
 METHODS = {"exact": 0, "int": 1, "taylor": 2, "chebyshev": 3, "auto": 4}
 PROBES = {"gaussian": 0, "rademacher": 1}
@@ -61,12 +63,21 @@ def build() -> Path:
     return LIB
 
 
+NATIVE = HERE / "_build" / "librenyi_oracle_native.so"
+
+
 def lib():
+    """The portable build; ORACLE_NATIVE=1 selects the -march=native build of the same source
+    (tests/golden/gen_fullsize.py, one-off fixture generation on this container)."""
     global _lib
     if _lib is None:
-        if not LIB.exists():
+        path = LIB
+        if os.environ.get("ORACLE_NATIVE") == "1":
+            subprocess.run(["make", "-s", "-C", str(HERE), "native"], check=True)
+            path = NATIVE
+        elif not LIB.exists():
             build()
-        h = C.CDLL(str(LIB))
+        h = C.CDLL(str(path))
         h.oracle_last_error.restype = C.c_char_p
         for name in ("oracle_mix64", "oracle_derive_key", "oracle_hash_name"):
             getattr(h, name).restype = C.c_uint64
@@ -109,6 +120,15 @@ def lib():
                                      C.c_int, C.c_uint64, C.c_int, _D, _D, C.POINTER(COut)]
         h.oracle_estimate.argtypes = [_D, _I64, C.POINTER(CParams), C.POINTER(COut)]
         h.oracle_eigvals.argtypes = [_D, _I64, _D]
+        h.oracle_cb_estimate.argtypes = [_I64, MUL_FN, C.POINTER(CParams), C.POINTER(COut)]
+        h.oracle_cb_matfun_traces.argtypes = [_I64, MUL_FN, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
+                                              _D, C.c_int, _D]
+        h.oracle_kernel_block.argtypes = [_D, _I64, _I64, _D, _D, C.c_double, C.c_double, C.c_double, C.c_int, _D]
+        _MF = [_D, _I64, _I64, C.c_double, _D, _I64, C.c_double]
+        h.oracle_mf_matmul.argtypes = _MF + [_D, C.c_int, _D]
+        h.oracle_mf_estimate.argtypes = _MF + [C.POINTER(CParams), C.POINTER(COut)]
+        h.oracle_mf_matfun_traces.argtypes = _MF + [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double, _D,
+                                                    C.c_int, _D]
         h.oracle_entropy_from_trace.argtypes = [C.c_double, C.c_double, _D]
         h.oracle_select_params.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                            _I64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -445,3 +465,134 @@ def load_csv(text, label_column=None, source=None):
                     labels=strings(1, n.value) if hl.value else [])
     finally:
         lib().oracle_csv_free(h)
+
+
+# ---- matrix-free (kernel entries recomputed from the samples; full-size fixtures) ----
+def _mf_args(x, sigma, y=None, sigma_y=None):
+    x = _f(x)
+    yy = _f(y) if y is not None else None
+    keep = (x, yy)
+    args = (_p(x), x.shape[0], x.shape[1], float(sigma), _p(yy) if yy is not None else None,
+            yy.shape[1] if yy is not None else 0, float(sigma_y or 0.0))
+    return keep, args
+
+
+def mf_matmul(x, sigma, v, y=None, sigma_y=None):
+    """A·V with A = build_kernel(X, sigma) (or the joint n·A∘B of X, Y), never stored."""
+    keep, args = _mf_args(x, sigma, y, sigma_y)
+    v = _f(v)
+    out = np.empty((x.shape[0], v.shape[1]), order="F")
+    _chk(lib().oracle_mf_matmul(*args, _p(v), v.shape[1], _p(out)))
+    return out
+
+
+def mf_estimate(x, sigma, y=None, sigma_y=None, **params):
+    """estimate(build_kernel(X, sigma) [∘ joint with Y], params) without storing A."""
+    keep, args = _mf_args(x, sigma, y, sigma_y)
+    p = _params(**params)
+    o = COut()
+    _chk(lib().oracle_mf_estimate(*args, C.byref(p), C.byref(o)))
+    return _out(o)
+
+
+def mf_matfun_traces(spec: Spec, x, sigma, probes, y=None, sigma_y=None):
+    keep, args = _mf_args(x, sigma, y, sigma_y)
+    q = _f(probes)
+    out = np.empty(q.shape[1])
+    _chk(lib().oracle_mf_matfun_traces(*args, *spec.args(), _p(q), q.shape[1], _p(out)))
+    return out
+
+
+def mf_mutual_information(x, sigma_x, y, sigma_y, **params):
+    """measures.cpp:36-46 (per-term seeds) over the three kernels, none stored."""
+    seed = params.pop("seed", 0)
+    tv = mf_estimate(x, sigma_x, seed=derive_key(seed, hash_name("term:vars")), **params)
+    tt = mf_estimate(y, sigma_y, seed=derive_key(seed, hash_name("term:target")), **params)
+    tj = mf_estimate(x, sigma_x, y, sigma_y, seed=derive_key(seed, hash_name("term:joint")), **params)
+    return dict(value=tv["entropy"] + tt["entropy"] - tj["entropy"], vars_entropy=tv["entropy"],
+                target_entropy=tt["entropy"], joint_entropy=tj["entropy"], terms=dict(vars=tv, target=tt, joint=tj))
+
+
+class KernelBlocksOp:
+    """y = A x for A = build_kernel(X, sigma) (or the joint n·A∘B with Y) in square blocks,
+    never stored: feature dots by BLAS (X_I X_J^T), entries by oracle_kernel_block (the
+    reference's d2/clamp/exp/normalisation arithmetic), both triangles from one block, products
+    by BLAS. The estimator itself is the restated C++ one (oracle_cb_*), called back through
+    ctypes. Differs from GaussOp (bit-exact entries) only in BLAS summation order (~1e-15, checked
+    in tests/test_oracle_fullsize.py)."""
+
+    def __init__(self, x, sigma, y=None, sigma_y=None, block=4096):
+        self.n = x.shape[0]
+        self.block = block
+        self.inv_n = 1.0 / self.n
+        self.feats = []
+        for z, sg in ((x, sigma), (y, sigma_y)):
+            if z is None:
+                continue
+            z = np.ascontiguousarray(z, dtype=np.float64)
+            sq = np.zeros(self.n)
+            for k in range(z.shape[1]):  # rowwise sum of squares in feature order (ops.cpp:41)
+                sq += z[:, k] * z[:, k]
+            self.feats.append((z, sq, 1.0 / (2.0 * sg * sg)))
+        self.calls = 0
+        self._fn = MUL_FN(self._cb)
+
+    def kernel_block(self, i0, i1, j0, j1):
+        out = np.empty((i1 - i0, j1 - j0))
+        for f, (z, sq, inv2) in enumerate(self.feats):
+            dot = np.ascontiguousarray(z[i0:i1] @ z[j0:j1].T)
+            sqi, sqj = np.ascontiguousarray(sq[i0:i1]), np.ascontiguousarray(sq[j0:j1])
+            lib().oracle_kernel_block(_p(dot), i1 - i0, j1 - j0, _p(sqi), _p(sqj), inv2, self.inv_n,
+                                      float(self.n), 1 if f else 0, _p(out))
+        if i0 == j0:
+            np.fill_diagonal(out, self.inv_n)
+        return out
+
+    def mul(self, v):
+        n, b = self.n, self.block
+        y = np.zeros_like(v)
+        for i0 in range(0, n, b):
+            i1 = min(n, i0 + b)
+            for j0 in range(i0, n, b):
+                j1 = min(n, j0 + b)
+                k = self.kernel_block(i0, i1, j0, j1)
+                y[i0:i1] += k @ v[j0:j1]
+                if j0 != i0:
+                    y[j0:j1] += k.T @ v[i0:i1]
+        return y
+
+    def _cb(self, n, c, x, out):
+        try:
+            v = np.ctypeslib.as_array(x, shape=(c, n)).T  # column-major n x c
+            y = self.mul(np.ascontiguousarray(v))
+            np.ctypeslib.as_array(out, shape=(c, n))[...] = y.T
+            self.calls += 1
+            return 0
+        except Exception:  # reported as a failed callback by the C++ side
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    def estimate(self, **params):
+        p = _params(**params)
+        o = COut()
+        _chk(lib().oracle_cb_estimate(self.n, self._fn, C.byref(p), C.byref(o)))
+        return _out(o)
+
+    def matfun_traces(self, spec: Spec, probes):
+        q = _f(probes)
+        out = np.empty(q.shape[1])
+        _chk(lib().oracle_cb_matfun_traces(self.n, self._fn, *spec.args(), _p(q), q.shape[1], _p(out)))
+        return out
+
+
+def blocks_mutual_information(x, sigma_x, y, sigma_y, block=4096, **params):
+    """measures.cpp:36-46 (per-term seeds) over KernelBlocksOp operators."""
+    seed = params.pop("seed", 0)
+    tv = KernelBlocksOp(x, sigma_x, block=block).estimate(seed=derive_key(seed, hash_name("term:vars")), **params)
+    tt = KernelBlocksOp(y, sigma_y, block=block).estimate(seed=derive_key(seed, hash_name("term:target")), **params)
+    tj = KernelBlocksOp(x, sigma_x, y, sigma_y, block=block).estimate(seed=derive_key(seed, hash_name("term:joint")),
+                                                                      **params)
+    return dict(value=tv["entropy"] + tt["entropy"] - tj["entropy"], vars_entropy=tv["entropy"],
+                target_entropy=tt["entropy"], joint_entropy=tj["entropy"], terms=dict(vars=tv, target=tt, joint=tj))

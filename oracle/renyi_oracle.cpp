@@ -12,12 +12,14 @@
 //
 // Pinned by the reference's own known-answer tests (tests/test_oracle_kats.py).
 #include <algorithm>
+#include <bit>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <limits>
 #include <map>
+#include <memory>
 #include <numbers>
 #include <stdexcept>
 #include <string>
@@ -182,6 +184,41 @@ Mat hadamard_scaled(const Mat& a, const Mat& b, double scale) {
     return c;
 }
 
+// ---------------------------------------------------------------- operator seam
+// The estimator reaches A only through matmul_panel / matvec (poly.cpp:155,163, hutchpp.cpp:90,
+// spectrum.cpp:31) and the dense shifted copy of estimate_bounds (spectrum.cpp:87-91). Op is that
+// seam: DenseOp is the reference's own cost structure over a stored matrix; GaussOp (below)
+// recomputes the kernel entries from the samples for the full-size fixtures, where the fp64 A
+// (20-1280 GB) does not fit host memory. The restated algorithms are written once over Op.
+struct Op {
+    int64_t n = 0;
+    Op() = default;
+    Op(const Op&) = delete;
+    Op& operator=(const Op&) = delete;
+    virtual ~Op() = default;
+    virtual Mat mul(const Mat& x) const = 0;                  // ops::matmul_panel(a, x)
+    virtual Vec mv(const Vec& x) const = 0;                   // ops::matvec(a, x)
+    virtual std::unique_ptr<Op> shifted(double v) const = 0;  // v I - A (estimate_bounds)
+};
+
+struct DenseOp final : Op {
+    const Mat* a;
+    Mat own;
+    explicit DenseOp(const Mat& m) : a(&m) { n = m.r; }
+    explicit DenseOp(Mat&& m) : a(nullptr), own(std::move(m)) {
+        a = &own;
+        n = own.r;
+    }
+    Mat mul(const Mat& x) const override { return matmul_panel(*a, x); }
+    Vec mv(const Vec& x) const override { return matvec(*a, x); }
+    std::unique_ptr<Op> shifted(double v) const override {  // spectrum.cpp:87-91: dense v I - A
+        Mat s(a->r, a->c);
+        for (size_t i = 0; i < a->d.size(); ++i) s.d[i] = -a->d[i];
+        for (int64_t i = 0; i < a->r; ++i) s(i, i) += v;
+        return std::make_unique<DenseOp>(std::move(s));
+    }
+};
+
 // ---------------------------------------------------------------- kernel.cpp
 uint64_t matrix_hash(const Mat& m) {  // kernel.cpp:13-23
     uint64_t h = 0xcbf29ce484222325ULL;
@@ -246,6 +283,192 @@ Mat hadamard_joint(std::vector<const Mat*> ks) {  // kernel.cpp:74-101
     return prod;
 }
 
+// ---------------------------------------------------------------- matrix-free kernel operator
+// A = build_kernel(X, GaussianKernel{sigma}) -- or the joint n·A∘B of hadamard_joint over two
+// sample sets -- applied without storing it. Every product recomputes the entries with
+// gaussian_gram's arithmetic (ops.cpp:39-47: sq rowwise, d2 = sq_i + sq_j - 2 x_i·x_j summed
+// over the features in order, clamp at 0, exp(-d2/(2σ²))) and build_kernel's normalisation
+// (kernel.cpp:51-70: inv_n·K with isd = 1 on the Gaussian diagonal, A_ii = inv_n); the joint is
+// n·(A_ij·B_ij) with diagonal inv_n (kernel.cpp:91-99). Each entry equals the dense oracle's
+// bit for bit (the library is built with -ffp-contract=off); only the summation order of the
+// product differs (square tiles, both triangles from one evaluation, per-thread partial sums
+// reduced in thread order). Used for the full-size fixtures (tests/golden/gen_fullsize.py).
+// exp(x) for x <= 0 without a libm call (so loops over kernel entries vectorise): Cody-Waite
+// reduction x = k ln2 + r, |r| <= ln2/2, a degree-13 Taylor polynomial (truncation < 4e-18
+// relative), and the scale 2^k applied in two halves so results down to the subnormal range are
+// right; x < -745.2 gives 0 like glibc. Max error measured <= 2 ulp against glibc exp
+// (tests/test_oracle_fullsize.py).
+inline double exp_nonpos(double x) {
+    x = x < -745.2 ? -745.2 : x;
+    const double shifter = 0x1.8p52;
+    double kd = x * 1.4426950408889634 + shifter;
+    const int64_t k = static_cast<int32_t>(static_cast<uint32_t>(std::bit_cast<uint64_t>(kd)));
+    kd -= shifter;
+    const double r = (x - kd * 0x1.62e42fefa3800p-1) - kd * 0x1.ef35793c7673p-45;
+    double p = 1.0 / 6227020800.0;
+    p = p * r + 1.0 / 479001600.0;
+    p = p * r + 1.0 / 39916800.0;
+    p = p * r + 1.0 / 3628800.0;
+    p = p * r + 1.0 / 362880.0;
+    p = p * r + 1.0 / 40320.0;
+    p = p * r + 1.0 / 5040.0;
+    p = p * r + 1.0 / 720.0;
+    p = p * r + 1.0 / 120.0;
+    p = p * r + 1.0 / 24.0;
+    p = p * r + 1.0 / 6.0;
+    p = p * r + 0.5;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    const int64_t k1 = k / 2, k2 = k - k1;  // 2^k1 * 2^k2, both normal for k >= -1075
+    const double s1 = std::bit_cast<double>(static_cast<uint64_t>(k1 + 1023) << 52);
+    const double s2 = std::bit_cast<double>(static_cast<uint64_t>(k2 + 1023) << 52);
+    return p * s1 * s2;
+}
+
+struct GaussOp final : Op {
+    struct Samples {
+        const double* x;  // n x d column-major
+        int64_t d;
+        Vec sq;
+        double inv2;
+    };
+    static constexpr int64_t T = 256;
+    std::vector<Samples> feats;
+    double inv_n, scale;
+
+    GaussOp(const double* x, int64_t n_, int64_t d, double sigma, const double* y, int64_t dy, double sigma_y) {
+        n = n_;
+        if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
+        auto add = [&](const double* z, int64_t dz, double sg) {
+            if (sg <= 0.0) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
+            Samples s{z, dz, Vec(n, 0.0), 1.0 / (2.0 * sg * sg)};
+            for (int64_t i = 0; i < n; ++i) {
+                double a = 0.0;
+                for (int64_t k = 0; k < dz; ++k) a += z[i + k * n] * z[i + k * n];
+                s.sq[i] = a;
+            }
+            feats.push_back(std::move(s));
+        };
+        add(x, d, sigma);
+        if (y) add(y, dy, sigma_y);
+        inv_n = 1.0 / static_cast<double>(n);
+        scale = static_cast<double>(n);  // n^(L-1), L = 2
+    }
+
+    // blk[ii * T + jj] = A(i0 + ii, j0 + jj); dot/kv scratch of T doubles each
+    void tile(int64_t i0, int64_t ni, int64_t j0, int64_t nj, double* blk, double* dot) const {
+        for (size_t f = 0; f < feats.size(); ++f) {
+            const Samples& s = feats[f];
+            for (int64_t ii = 0; ii < ni; ++ii) {
+                const int64_t i = i0 + ii;
+                for (int64_t jj = 0; jj < nj; ++jj) dot[jj] = 0.0;
+                for (int64_t t = 0; t < s.d; ++t) {
+                    const double xi = s.x[i + t * n];
+                    const double* xj = s.x + t * n + j0;
+                    for (int64_t jj = 0; jj < nj; ++jj) dot[jj] += xi * xj[jj];
+                }
+                double* row = blk + ii * T;
+                for (int64_t jj = 0; jj < nj; ++jj) {
+                    double d2 = s.sq[i] + s.sq[j0 + jj] - 2.0 * dot[jj];
+                    if (d2 < 0.0) d2 = 0.0;
+                    const double a = inv_n * std::exp(-d2 * s.inv2);
+                    row[jj] = f == 0 ? a : scale * (row[jj] * a);
+                }
+                if (i >= j0 && i < j0 + nj) row[i - j0] = inv_n;
+            }
+        }
+    }
+
+    Mat mul(const Mat& x) const override {
+        const int64_t c = x.c;
+        Mat out(n, c);
+        if (c == 0) return out;
+        Vec xr(static_cast<size_t>(n) * c);  // row-major copy of the operand
+        for (int64_t j = 0; j < c; ++j)
+            for (int64_t i = 0; i < n; ++i) xr[i * c + j] = x(i, j);
+        const int64_t nt = (n + T - 1) / T;
+        std::vector<std::pair<int64_t, int64_t>> pairs;
+        for (int64_t a = 0; a < nt; ++a)
+            for (int64_t b = a; b < nt; ++b) pairs.push_back({a, b});
+        int nth = 1;
+#ifdef _OPENMP
+        nth = omp_get_max_threads();
+#endif
+        std::vector<Vec> part(static_cast<size_t>(nth));
+#pragma omp parallel num_threads(nth)
+        {
+            int tid = 0;
+#ifdef _OPENMP
+            tid = omp_get_thread_num();
+#endif
+            Vec& y = part[static_cast<size_t>(tid)];
+            y.assign(static_cast<size_t>(n) * c, 0.0);
+            Vec blk(static_cast<size_t>(T) * T), dot(T), acc(static_cast<size_t>(c));
+#pragma omp for schedule(static, 1)
+            for (size_t p = 0; p < pairs.size(); ++p) {
+                const int64_t i0 = pairs[p].first * T, j0 = pairs[p].second * T;
+                const int64_t ni = std::min(T, n - i0), nj = std::min(T, n - j0);
+                tile(i0, ni, j0, nj, blk.data(), dot.data());
+                for (int64_t ii = 0; ii < ni; ++ii) {  // y_I += A_IJ x_J
+                    double* yi = y.data() + (i0 + ii) * c;
+                    const double* row = blk.data() + ii * T;
+                    for (int64_t k = 0; k < c; ++k) acc[k] = 0.0;
+                    for (int64_t jj = 0; jj < nj; ++jj) {
+                        const double a = row[jj];
+                        const double* xj = xr.data() + (j0 + jj) * c;
+                        for (int64_t k = 0; k < c; ++k) acc[k] += a * xj[k];
+                    }
+                    for (int64_t k = 0; k < c; ++k) yi[k] += acc[k];
+                }
+                if (i0 == j0) continue;
+                for (int64_t jj = 0; jj < nj; ++jj) {  // y_J += A_IJ^T x_I
+                    double* yj = y.data() + (j0 + jj) * c;
+                    for (int64_t k = 0; k < c; ++k) acc[k] = 0.0;
+                    for (int64_t ii = 0; ii < ni; ++ii) {
+                        const double a = blk[ii * T + jj];
+                        const double* xi = xr.data() + (i0 + ii) * c;
+                        for (int64_t k = 0; k < c; ++k) acc[k] += a * xi[k];
+                    }
+                    for (int64_t k = 0; k < c; ++k) yj[k] += acc[k];
+                }
+            }
+        }
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t k = 0; k < c; ++k) {
+                double v = 0.0;
+                for (int t = 0; t < nth; ++t) v += part[static_cast<size_t>(t)][i * c + k];
+                out(i, k) = v;
+            }
+        return out;
+    }
+    Vec mv(const Vec& x) const override {
+        Mat m(n, 1);
+        std::copy(x.begin(), x.end(), m.d.begin());
+        return mul(m).d;
+    }
+    std::unique_ptr<Op> shifted(double v) const override;
+};
+
+// v I - A applied as v x - A x (the dense shifted copy of spectrum.cpp:87-91 without storing it)
+struct ShiftOp final : Op {
+    const Op* a;
+    double v;
+    ShiftOp(const Op* base, double shift) : a(base), v(shift) { n = base->n; }
+    Mat mul(const Mat& x) const override {
+        Mat y = a->mul(x);
+        for (size_t i = 0; i < y.d.size(); ++i) y.d[i] = v * x.d[i] - y.d[i];
+        return y;
+    }
+    Vec mv(const Vec& x) const override {
+        Vec y = a->mv(x);
+        for (size_t i = 0; i < y.size(); ++i) y[i] = v * x[i] - y[i];
+        return y;
+    }
+    std::unique_ptr<Op> shifted(double) const override { fail(kInvalidArgument, "nested shift"); }
+};
+std::unique_ptr<Op> GaussOp::shifted(double v) const { return std::make_unique<ShiftOp>(this, v); }
+
 // ---------------------------------------------------------------- spectrum.cpp
 struct PowerOptions {
     int max_iters = 100;
@@ -281,12 +504,12 @@ Vec seeded_start(int64_t n, uint64_t seed) {  // spectrum.cpp:13-21
     return x;
 }
 
-PowerResult power_method(const Mat& a, const PowerOptions& o) {  // spectrum.cpp:25-49
-    Vec x = seeded_start(a.r, o.seed);
+PowerResult power_method(const Op& a, const PowerOptions& o) {  // spectrum.cpp:25-49
+    Vec x = seeded_start(a.n, o.seed);
     PowerResult res;
     double prev = 0.0;
     for (int it = 1; it <= o.max_iters; ++it) {
-        Vec y = matvec(a, x);
+        Vec y = a.mv(x);
         const double q = dot(x, y);
         res.rayleigh = q;
         res.iterations = it;
@@ -305,18 +528,18 @@ PowerResult power_method(const Mat& a, const PowerOptions& o) {  // spectrum.cpp
     return res;
 }
 
-Bounds estimate_bounds(const Mat& a, const PowerOptions& o) {  // spectrum.cpp:80-103
+PowerResult power_method(const Mat& a, const PowerOptions& o) { return power_method(DenseOp(a), o); }
+
+Bounds estimate_bounds(const Op& a, const PowerOptions& o) {  // spectrum.cpp:80-103
     Bounds b;
     const PowerResult rv = power_method(a, o);
-    const double inv_n = 1.0 / static_cast<double>(a.r);
+    const double inv_n = 1.0 / static_cast<double>(a.n);
     b.v = std::clamp(rv.rayleigh * (1.0 + o.tol), inv_n, 1.0);
     b.v_converged = rv.converged;
-    Mat shifted(a.r, a.c);
-    for (size_t i = 0; i < a.d.size(); ++i) shifted.d[i] = -a.d[i];
-    for (int64_t i = 0; i < a.r; ++i) shifted(i, i) += b.v;
+    const std::unique_ptr<Op> shifted = a.shifted(b.v);
     PowerOptions so = o;
     so.seed = derive_key(o.seed, hash_name("shifted"));
-    const PowerResult ru = power_method(shifted, so);
+    const PowerResult ru = power_method(*shifted, so);
     b.u_converged = ru.converged;
     double u = (b.v - ru.rayleigh) * (1.0 - o.tol);
     const double floor = std::max(o.rank_floor, b.v * o.tol * 100.0);
@@ -329,6 +552,7 @@ Bounds estimate_bounds(const Mat& a, const PowerOptions& o) {  // spectrum.cpp:8
     b.iterations_used = rv.iterations + ru.iterations;
     return b;
 }
+Bounds estimate_bounds(const Mat& a, const PowerOptions& o) { return estimate_bounds(DenseOp(a), o); }
 
 // ---------------------------------------------------------------- poly.cpp
 Vec binomial_coeffs(double alpha, int m) {  // poly.cpp:10-16
@@ -426,11 +650,11 @@ void add_scaled(Mat& acc, double c, const Mat& t) {
     for (size_t i = 0; i < acc.d.size(); ++i) acc.d[i] += c * t.d[i];
 }
 
-Mat apply_panel(const Spec& s, const Mat& a, const Mat& x) {
-    if (a.r != a.c || a.c != x.r) fail(kSizeMismatch, "apply_panel: size mismatch");
+Mat apply_panel(const Spec& s, const Op& a, const Mat& x) {
+    if (a.n != x.r) fail(kSizeMismatch, "apply_panel: size mismatch");
     if (s.kind == 0) {
         Mat y = x;
-        for (int k = 0; k < s.degree; ++k) y = matmul_panel(a, y);
+        for (int k = 0; k < s.degree; ++k) y = a.mul(y);
         return y;
     }
     if (s.kind == 1) {
@@ -439,7 +663,7 @@ Mat apply_panel(const Spec& s, const Mat& a, const Mat& x) {
         Mat acc(x.r, x.c);
         for (size_t i = 0; i < acc.d.size(); ++i) acc.d[i] = s.coeffs[0] * x.d[i];
         for (int k = 1; k <= s.degree; ++k) {
-            Mat at = matmul_panel(a, term);
+            Mat at = a.mul(term);
             term = axpby(inv_v, at, -1.0, term);  // inv_v * mul(term) - term
             add_scaled(acc, s.coeffs[k], term);
         }
@@ -449,7 +673,7 @@ Mat apply_panel(const Spec& s, const Mat& a, const Mat& x) {
     }
     const double scale = 2.0 / (s.v - s.u);
     const double center = (s.v + s.u) / (s.v - s.u);
-    auto mapped = [&](const Mat& w) { return axpby(scale, matmul_panel(a, w), -center, w); };
+    auto mapped = [&](const Mat& w) { return axpby(scale, a.mul(w), -center, w); };
     Mat t_prev = x;
     Mat acc(x.r, x.c);
     for (size_t i = 0; i < acc.d.size(); ++i) acc.d[i] = (0.5 * s.coeffs[0]) * x.d[i];
@@ -466,6 +690,11 @@ Mat apply_panel(const Spec& s, const Mat& a, const Mat& x) {
         }
     }
     return acc;
+}
+
+Mat apply_panel(const Spec& s, const Mat& a, const Mat& x) {
+    if (a.r != a.c || a.c != x.r) fail(kSizeMismatch, "apply_panel: size mismatch");
+    return apply_panel(s, DenseOp(a), x);
 }
 
 double scalar_value(const Spec& s, double lam) {  // poly.cpp:166-168
@@ -609,12 +838,12 @@ void sub_mul(Mat& w, const Mat& q, const Mat& c) {  // w -= q c
         }
 }
 
-double projected_trace(const Spec& f, const Mat& a, const Mat& q) {  // hutchpp.cpp:33-39
+double projected_trace(const Spec& f, const Op& a, const Mat& q) {  // hutchpp.cpp:33-39
     if (q.c == 0) return 0.0;
     return col_dot_sum(q, apply_panel(f, a, q));
 }
 
-double residual_probe_trace(const Spec& f, const Mat& a, const Mat& q, Mat w) {  // hutchpp.cpp:41-51
+double residual_probe_trace(const Spec& f, const Op& a, const Mat& q, Mat w) {  // hutchpp.cpp:41-51
     const int64_t s_g = w.c;
     if (q.c > 0) sub_mul(w, q, mul_t(q, w));
     Mat fw = apply_panel(f, a, w);
@@ -622,8 +851,8 @@ double residual_probe_trace(const Spec& f, const Mat& a, const Mat& q, Mat w) { 
     return col_dot_sum(w, fw) / static_cast<double>(s_g);
 }
 
-double exact_trace(const Spec& f, const Mat& a) {  // hutchpp.cpp:53-65
-    const int64_t n = a.r;
+double exact_trace(const Spec& f, const Op& a) {  // hutchpp.cpp:53-65
+    const int64_t n = a.n;
     double sum = 0.0;
     for (int64_t j0 = 0; j0 < n; j0 += 256) {
         const int64_t len = std::min<int64_t>(256, n - j0);
@@ -636,9 +865,8 @@ double exact_trace(const Spec& f, const Mat& a) {  // hutchpp.cpp:53-65
 }
 
 // hutchpp (hutchpp.cpp:69-115); S / G may be injected; s_q = 0 gives plain Hutchinson
-Trace hutchpp(const Spec& f, const Mat& a, int s_q, int s_g, uint64_t seed, int kind, const Mat* S, const Mat* G) {
-    if (a.r != a.c) fail(kSizeMismatch, "hutchpp needs a square matrix");
-    const int64_t n = a.r;
+Trace hutchpp(const Spec& f, const Op& a, int s_q, int s_g, uint64_t seed, int kind, const Mat* S, const Mat* G) {
+    const int64_t n = a.n;
     const int cost = f.query_cost();
     Trace est;
     if (s_q >= n) {
@@ -652,7 +880,7 @@ Trace hutchpp(const Spec& f, const Mat& a, int s_q, int s_g, uint64_t seed, int 
     PivQR qr;
     if (s_q > 0) {
         const Mat sketch = S ? *S : probe_panel(n, s_q, seed, "hutchpp-sketch", kind);
-        const Mat y = matmul_panel(a, sketch);
+        const Mat y = a.mul(sketch);
         qr = colpiv_qr(y, 1e-12);
         if (qr.rank == 0) fail(kRankCollapse, "hutchpp sketch A*S is numerically zero");
         est.rank = qr.rank;
@@ -678,6 +906,10 @@ Trace hutchpp(const Spec& f, const Mat& a, int s_q, int s_g, uint64_t seed, int 
     est.queries += s_g * cost;
     est.value = est.low + est.residual;
     return est;
+}
+Trace hutchpp(const Spec& f, const Mat& a, int s_q, int s_g, uint64_t seed, int kind, const Mat* S, const Mat* G) {
+    if (a.r != a.c) fail(kSizeMismatch, "hutchpp needs a square matrix");
+    return hutchpp(f, DenseOp(a), s_q, s_g, seed, kind, S, G);
 }
 
 // ---------------------------------------------------------------- entropy.cpp
@@ -856,7 +1088,7 @@ void select_params(double alpha, double eps, double delta, const Bounds& b, int6
     }
 }
 
-Estimate from_hutchpp(const Mat& a, const Spec& f, double alpha, int s, const Params& p, int method, int m_used) {
+Estimate from_hutchpp(const Op& a, const Spec& f, double alpha, int s, const Params& p, int method, int m_used) {
     int s_q, s_g;
     if (p.s_q >= 0 || p.s_g >= 0) {
         s_q = std::max(p.s_q, 0);
@@ -877,10 +1109,9 @@ Estimate from_hutchpp(const Mat& a, const Spec& f, double alpha, int s, const Pa
     return e;
 }
 
-Estimate estimate(const Mat& a, const Params& p) {  // entropy.cpp:201-275
+Estimate estimate(const Op& a, const Params& p, const Mat* dense) {  // entropy.cpp:201-275
     validate_alpha(p.alpha);
-    if (a.r != a.c) fail(kSizeMismatch, "estimate needs a square matrix");
-    const int64_t n = a.r;
+    const int64_t n = a.n;
     int ai = 0;
     const bool is_int = integer_alpha(p.alpha, &ai);
     bool have = p.has_bounds;
@@ -907,7 +1138,8 @@ Estimate estimate(const Mat& a, const Params& p) {  // entropy.cpp:201-275
     Estimate est;
     if (method == 0) {
         if (n > 20000) fail(kInvalidArgument, "entropy_exact is guarded at n <= 20000");
-        est.trace = exact_trace_power(a, p.alpha);
+        if (!dense) fail(kInvalidArgument, "entropy_exact needs the stored matrix");
+        est.trace = exact_trace_power(*dense, p.alpha);
         est.entropy = entropy_from_trace(est.trace, p.alpha);
         est.method = 0;
         est.deterministic = true;
@@ -936,6 +1168,11 @@ Estimate estimate(const Mat& a, const Params& p) {  // entropy.cpp:201-275
     est.has_bounds = have;
     est.bounds = bounds;
     return est;
+}
+Estimate estimate(const Mat& a, const Params& p) {
+    validate_alpha(p.alpha);
+    if (a.r != a.c) fail(kSizeMismatch, "estimate needs a square matrix");
+    return estimate(DenseOp(a), p, &a);
 }
 
 void mu_bound(double u, double v, double alpha, int64_t n, double* mu, double* lower, double* upper) {
@@ -1452,6 +1689,98 @@ long oracle_expected_queries(int kind, double alpha, int m, double u, double v, 
 }
 int oracle_estimate(const double* a, int64_t n, const CParams* p, COut* out) {
     return guard([&] { to_out(orc::estimate(wrap(a, n, n), to_params(p)), out); });
+}
+// matrix-free variants (GaussOp): the kernel of X (y == NULL) or the joint n·A∘B of (X, Y),
+// never stored; for the full-size fixtures
+int oracle_mf_matmul(const double* x, int64_t n, int64_t d, double sigma, const double* y, int64_t dy,
+                     double sigma_y, const double* v, int s, double* out) {
+    return guard([&] { unwrap(orc::GaussOp(x, n, d, sigma, y, dy, sigma_y).mul(wrap(v, n, s)), out); });
+}
+int oracle_mf_estimate(const double* x, int64_t n, int64_t d, double sigma, const double* y, int64_t dy,
+                       double sigma_y, const CParams* p, COut* out) {
+    return guard([&] {
+        const orc::GaussOp op(x, n, d, sigma, y, dy, sigma_y);
+        to_out(orc::estimate(op, to_params(p), nullptr), out);
+    });
+}
+// x_j^T f(A) x_j per column (projected_trace per probe, hutchpp.cpp:33-39)
+int oracle_mf_matfun_traces(const double* x, int64_t n, int64_t d, double sigma, const double* y, int64_t dy,
+                            double sigma_y, int kind, double alpha, int m, double u, double v, const double* probes,
+                            int s, double* out) {
+    return guard([&] {
+        const orc::GaussOp op(x, n, d, sigma, y, dy, sigma_y);
+        const orc::Mat q = wrap(probes, n, s);
+        const orc::Mat fq = orc::apply_panel(orc::make_spec(kind, alpha, m, u, v), op, q);
+        for (int j = 0; j < s; ++j) {
+            double acc = 0.0;
+            for (int64_t i = 0; i < n; ++i) acc += q(i, j) * fq(i, j);
+            out[j] = acc;
+        }
+    });
+}
+// Operator supplied by the caller (a ctypes callback computing y = A x, column-major n x c):
+// runs the restated estimator over an A the caller applies matrix-free with BLAS blocks
+// (oracle.py KernelBlocksOp, the full-size fixtures). Validated against GaussOp at small n.
+typedef int (*oracle_mul_fn)(int64_t n, int64_t c, const double* x, double* y);
+}  // extern "C"
+namespace orc {
+struct CallbackOp final : Op {
+    oracle_mul_fn f;
+    CallbackOp(int64_t n_, oracle_mul_fn fn) : f(fn) { n = n_; }
+    Mat mul(const Mat& x) const override {
+        Mat y(n, x.c);
+        if (x.c > 0 && f(n, x.c, x.d.data(), y.d.data()) != 0) fail(kInvalidArgument, "operator callback failed");
+        return y;
+    }
+    Vec mv(const Vec& x) const override {
+        Vec y(static_cast<size_t>(n));
+        if (f(n, 1, x.data(), y.data()) != 0) fail(kInvalidArgument, "operator callback failed");
+        return y;
+    }
+    std::unique_ptr<Op> shifted(double v) const override { return std::make_unique<ShiftOp>(this, v); }
+};
+}  // namespace orc
+extern "C" {
+int oracle_cb_estimate(int64_t n, oracle_mul_fn f, const CParams* p, COut* out) {
+    return guard([&] {
+        const orc::CallbackOp op(n, f);
+        to_out(orc::estimate(op, to_params(p), nullptr), out);
+    });
+}
+int oracle_cb_matfun_traces(int64_t n, oracle_mul_fn f, int kind, double alpha, int m, double u, double v,
+                            const double* probes, int s, double* out) {
+    return guard([&] {
+        const orc::CallbackOp op(n, f);
+        const orc::Mat q = wrap(probes, n, s);
+        const orc::Mat fq = orc::apply_panel(orc::make_spec(kind, alpha, m, u, v), op, q);
+        for (int j = 0; j < s; ++j) {
+            double acc = 0.0;
+            for (int64_t i = 0; i < n; ++i) acc += q(i, j) * fq(i, j);
+            out[j] = acc;
+        }
+    });
+}
+// Kernel entries of one row-major bi x bj block from the feature dot products (gaussian_gram's
+// d2 = sq_i + sq_j - 2 dot, clamp, exp; build_kernel's inv_n·K): combine = 0 writes A, 1
+// multiplies into out as the joint n·(A∘B) (hadamard_scaled, ops.cpp:116-122).
+// The exponential is exp_nonpos below (vectorisable, <= 2 ulp from glibc's exp over the
+// kernel's argument range x <= 0), so these blocks agree with GaussOp's std::exp entries to
+// a few ulp; the fixture tolerances are 1e-4 and 1e-9 on values whose entry error is 1e-16.
+int oracle_kernel_block(const double* dot, int64_t bi, int64_t bj, const double* sq_i, const double* sq_j,
+                        double inv2, double inv_n, double scale, int combine, double* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < bi; ++i) {
+        const double* dr = dot + i * bj;
+        double* o = out + i * bj;
+        const double si = sq_i[i];
+        for (int64_t j = 0; j < bj; ++j) {
+            double d2 = si + sq_j[j] - 2.0 * dr[j];
+            d2 = d2 < 0.0 ? 0.0 : d2;
+            const double a = inv_n * orc::exp_nonpos(-d2 * inv2);
+            o[j] = combine ? scale * (o[j] * a) : a;
+        }
+    }
+    return 0;
 }
 int oracle_eigvals(const double* a, int64_t n, double* out) {
     return guard([&] {

@@ -32,34 +32,46 @@ def stream_u64(key: int, count: int) -> np.ndarray:
     return mix64_np(k ^ mix64_np(np.arange(count, dtype=np.uint64)))
 
 
-def _R():
+def _gen(gen: str):
+    """The reference RNG from the product library (gen="product", the GPU arm) or from the CPU
+    oracle (gen="oracle": bench.py --impl reference and the fixture generator, so that those
+    never map librenyi_b200.so). Both are bitwise equal (tests/test_abi_host.py)."""
+    if gen == "oracle":
+        from oracle import oracle as O
+
+        return O.gaussian_panel, O.derive_key, O.hash_name
     import paper_2205_07426_b200 as R
 
-    return R
+    return R.gaussian_panel, R.derive_key, R.hash_name
 
 
-def gaussian(n: int, d: int, seed: int, label: str) -> np.ndarray:
+def gaussian(n: int, d: int, seed: int, label: str, gen: str = "product") -> np.ndarray:
     """n x d, column j from RandomStream(derive_key(derive_key(seed, hash(label)), j)) (gaussian_panel)."""
-    return _R().gaussian_panel(n, d, seed, label)
+    return _gen(gen)[0](n, d, seed, label)
 
 
-def iid(n: int, d: int, seed: int) -> np.ndarray:
-    return gaussian(n, d, seed, "X")
+def iid(n: int, d: int, seed: int, gen: str = "product") -> np.ndarray:
+    return gaussian(n, d, seed, "X", gen)
 
 
-def mixture10(n: int, d: int, seed: int) -> np.ndarray:
+def mixture10(n: int, d: int, seed: int, gen: str = "product") -> np.ndarray:
     """Config 3: 10 isotropic unit-variance Gaussians, means ~ N(0, 4I), component = next_u64() % 10."""
-    R = _R()
-    means = 2.0 * gaussian(d, 10, seed, "means")
-    comp = (stream_u64(R.derive_key(seed, R.hash_name("component")), n) % np.uint64(10)).astype(np.int64)
-    return means[:, comp].T + gaussian(n, d, seed, "noise")
+    panel, derive_key, hash_name = _gen(gen)
+    means = 2.0 * panel(d, 10, seed, "means")
+    comp = (stream_u64(derive_key(seed, hash_name("component")), n) % np.uint64(10)).astype(np.int64)
+    return means[:, comp].T + panel(n, d, seed, "noise")
 
 
-def mi_inputs(n: int, seed: int, dx: int = 16, dy: int = 8):
-    """Config 4: X ~ N(0, I_16); Y = X W + 0.5 noise with W ~ N(0,1)^{16x8}."""
-    x = gaussian(n, dx, seed, "X")
-    w = gaussian(dx, dy, seed, "W")
-    y = x @ w + 0.5 * gaussian(n, dy, seed, "noise")
+def mi_inputs(n: int, seed: int, dx: int = 16, dy: int = 8, gen: str = "product"):
+    """Config 4: X ~ N(0, I_16); Y = X W + 0.5 noise with W ~ N(0,1)^{16x8}. The product X W is
+    summed feature by feature in fixed order (elementwise IEEE arithmetic, no BLAS), so Y is
+    bitwise the same on every host CPU."""
+    x = gaussian(n, dx, seed, "X", gen)
+    w = gaussian(dx, dy, seed, "W", gen)
+    y = np.zeros((n, dy))
+    for k in range(dx):
+        y += x[:, k:k + 1] * w[k:k + 1, :]
+    y = y + 0.5 * gaussian(n, dy, seed, "noise", gen)
     return x, y
 
 
