@@ -3,6 +3,8 @@
 // roofline path). Same partial layout as the tensor-core kernel with one slot
 // per 128-row block, so the shared pass epilogue consumes both.
 // Reference: ops::matmul_panel / panel_block, proj/src/ops.cpp:30-35,98-107.
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace rb {
@@ -13,45 +15,57 @@ constexpr int FM = 128;  // rows per CTA (matches the epilogue's row block)
 constexpr int FN = 32;   // columns per CTA
 constexpr int FK = 32;   // K per smem tile
 
+// Stream-K over (row block, 32-column k tile) iterations: CTA c owns iterations
+// [T·c/G, T·(c+1)/G) and writes one partial per row block it touches to slot rb + c (the pass
+// epilogue sums a row block's slots in CTA order, so results are run-to-run identical). At
+// n = 2000 this spreads the 32 MB of A over every SM instead of 16 row-block CTAs.
 __global__ void __launch_bounds__(256) block_av_f64_kernel(const double* __restrict__ a, int64_t rows, int64_t cols,
                                                            int64_t lda, const double* __restrict__ v, int s,
-                                                           int64_t ldv, int npad, double* __restrict__ partial) {
+                                                           int64_t ldv, int npad, double* __restrict__ partial,
+                                                           int64_t total_iters, int k_tiles) {
     __shared__ double as[FK][FM + 1];
     __shared__ double vs[FK][FN + 1];
     const int tx = threadIdx.x % 32;
     const int ty = threadIdx.x / 32;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * FM;
+    const int G = gridDim.x, c = blockIdx.x;
     const int col0 = blockIdx.y * FN;
-    double acc[FM / 8];
+    int64_t it = total_iters * c / G;
+    const int64_t it_end = total_iters * (c + 1) / G;
+    while (it < it_end) {
+        const int64_t rb = it / k_tiles;
+        const int64_t seg_end = min(it_end, (rb + 1) * k_tiles);
+        const int64_t row0 = rb * FM;
+        double acc[FM / 8];
 #pragma unroll
-    for (int i = 0; i < FM / 8; ++i) acc[i] = 0.0;
-
-    for (int64_t k0 = 0; k0 < cols; k0 += FK) {
-        for (int idx = threadIdx.x; idx < FM * FK; idx += blockDim.x) {
-            const int rr = idx / FK, kk = idx % FK;
-            const int64_t gr = row0 + rr, gk = k0 + kk;
-            as[kk][rr] = (gr < rows && gk < cols) ? a[gr * lda + gk] : 0.0;
-        }
-        for (int idx = threadIdx.x; idx < FN * FK; idx += blockDim.x) {
-            const int cc = idx / FK, kk = idx % FK;
-            const int gc = col0 + cc;
-            const int64_t gk = k0 + kk;
-            vs[kk][cc] = (gc < s && gk < cols) ? v[static_cast<int64_t>(gc) * ldv + gk] : 0.0;
-        }
-        __syncthreads();
+        for (int i = 0; i < FM / 8; ++i) acc[i] = 0.0;
+        for (; it < seg_end; ++it) {
+            const int64_t k0 = (it - rb * k_tiles) * FK;
+            for (int idx = threadIdx.x; idx < FM * FK; idx += blockDim.x) {
+                const int rr = idx / FK, kk = idx % FK;
+                const int64_t gr = row0 + rr, gk = k0 + kk;
+                as[kk][rr] = (gr < rows && gk < cols) ? a[gr * lda + gk] : 0.0;
+            }
+            for (int idx = threadIdx.x; idx < FN * FK; idx += blockDim.x) {
+                const int cc = idx / FK, kk = idx % FK;
+                const int gc = col0 + cc;
+                const int64_t gk = k0 + kk;
+                vs[kk][cc] = (gc < s && gk < cols) ? v[static_cast<int64_t>(gc) * ldv + gk] : 0.0;
+            }
+            __syncthreads();
 #pragma unroll 4
-        for (int kk = 0; kk < FK; ++kk) {
-            const double vv = vs[kk][tx];
+            for (int kk = 0; kk < FK; ++kk) {
+                const double vv = vs[kk][tx];
 #pragma unroll
-            for (int i = 0; i < FM / 8; ++i) acc[i] = fma(as[kk][ty + 8 * i], vv, acc[i]);
+                for (int i = 0; i < FM / 8; ++i) acc[i] = fma(as[kk][ty + 8 * i], vv, acc[i]);
+            }
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    const int col = col0 + tx;
-    if (col < s) {
-        double* dst = partial + (static_cast<int64_t>(blockIdx.x) * npad + col) * FM;
+        const int col = col0 + tx;
+        if (col < s) {
+            double* dst = partial + ((rb + c) * npad + col) * FM;
 #pragma unroll
-        for (int i = 0; i < FM / 8; ++i) dst[ty + 8 * i] = acc[i];
+            for (int i = 0; i < FM / 8; ++i) dst[ty + 8 * i] = acc[i];
+        }
     }
 }
 
@@ -59,25 +73,26 @@ __global__ void __launch_bounds__(256) block_av_f64_kernel(const double* __restr
 
 int f64_npad(int cols) { return ((cols + FN - 1) / FN) * FN; }
 
-StreamKPlan make_f64_plan(int64_t rows, int64_t cols) {
-    // one "CTA" in stream-K terms: slot == row block
+StreamKPlan make_f64_plan(int64_t rows, int64_t cols, int grid) {
     StreamKPlan p;
     p.row_blocks = static_cast<int>((rows + FM - 1) / FM);
-    p.k_tiles = 1;
-    p.total_iters = p.row_blocks;
-    p.grid = 1;
+    p.k_tiles = static_cast<int>((cols + FK - 1) / FK);
+    p.total_iters = static_cast<int64_t>(p.row_blocks) * p.k_tiles;
+    p.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, p.total_iters)));
     p.kc = 1;
-    p.slots = p.row_blocks + 1;
+    p.cluster = 1;
+    p.dp_blocks = 0;
+    p.slots = p.row_blocks + p.grid;
     p.rows_per_block = FM;
-    (void)cols;
     return p;
 }
 
 cudaError_t launch_block_av_f64(const double* a, int64_t rows, int64_t cols, int64_t lda, const double* v, int s,
-                                int64_t ldv, double* partial, cudaStream_t stream) {
+                                int64_t ldv, const StreamKPlan& plan, double* partial, cudaStream_t stream) {
     const int npad = f64_npad(s);
-    dim3 grid(static_cast<unsigned>((rows + FM - 1) / FM), static_cast<unsigned>(npad / FN));
-    block_av_f64_kernel<<<grid, 256, 0, stream>>>(a, rows, cols, lda, v, s, ldv, npad, partial);
+    dim3 grid(static_cast<unsigned>(plan.grid), static_cast<unsigned>(npad / FN));
+    block_av_f64_kernel<<<grid, 256, 0, stream>>>(a, rows, cols, lda, v, s, ldv, npad, partial, plan.total_iters,
+                                                  plan.k_tiles);
     return cudaGetLastError();
 }
 

@@ -380,14 +380,6 @@ constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 #ifndef RB_TRI_AB_STAGES
 #define RB_TRI_AB_STAGES 2
 #endif
-#ifndef RB_TRI_CP
-// 1: A/B planes reach TMEM by tcgen05.cp.cta_group::2 issued with the MMAs, builders store only J. Measured
-// slower (22.7 vs 20.7 ms per config-4 pass): the A/B stage is then held until the MMAs complete
-#define RB_TRI_CP 0
-#endif
-#ifndef RB_TRI_ABLATE
-#define RB_TRI_ABLATE 0  // timing experiments only: 1 no J arithmetic, 2 no TMEM stores, 3 no MMAs
-#endif
 #ifndef RB_TRI_SETMAXNREG
 #define RB_TRI_SETMAXNREG 1
 #endif
@@ -533,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (VSPLIT) prefetch_tmap(&map_valo), prefetch_tmap(&map_vblo), prefetch_tmap(&map_vjlo);
         for (int s = 0; s < C::kABStages; ++s) {
             mbar_init(&ab_full[s], 1);
-            mbar_init(&ab_empty[s], kTriConv + RB_TRI_CP);  // converters read the tiles (+ the pair's copies)
+            mbar_init(&ab_empty[s], kTriConv);  // every builder warp has read the tiles
         }
         for (int s = 0; s < C::kVStages; ++s) {
             mbar_init(&v_full[s], 1);   // leader: both CTAs' V halves landed
@@ -604,8 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (leader) {
             constexpr uint32_t idesc = umma_idesc_f16_f32(2 * TBM, NPAD);
             const uint64_t dv0 = umma_desc_sw128(v_u32);
-            const uint64_t da0 = umma_desc_sw128(base_u32);
-            int vs = 0, as = 0;
+            int vs = 0;
             uint32_t vph = 0, u = 0, chunk = 0;
             TriSegs sg(args, pair, G);
             int64_t rp;
@@ -630,18 +621,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                             tc_fence_after();
                             const uint32_t ta = tmem + C::kOpCol0 + slot * C::kOpCols;
                             if (elect_one()) {
-                                if (RB_TRI_CP) {  // A_hi, A_lo, B_hi, B_lo slices of this K group into the slot
-                                    const uint64_t da = da0 + static_cast<uint64_t>((as * C::kABStage + kk * 32) >> 4);
-#pragma unroll
-                                    for (int pl = 0; pl < 4; ++pl)
-                                        tmem_cp2_128x256b(ta + pl * 8, da + ((pl * C::kAPlane) >> 4));
-                                }
 #pragma unroll
                                 for (int o = 0; o < 3; ++o) {
                                     const uint32_t d = d0 + o * NPAD;
                                     const uint32_t th = ta + o * 16;  // operand o: hi at +0, lo at +8
                                     const uint64_t vh = dv + (((o * C::kVPer) * C::kVHalf + kk * 32) >> 4);
-                                    if (RB_TRI_ABLATE == 3) continue;
                                     umma2_f16_ts(d, th, vh, idesc, cont | (kk > 0));             // hi·hi
                                     umma2_f16_ts(d, th + 8, vh, idesc, 1u);                      // lo·hi
                                     if (VSPLIT) umma2_f16_ts(d, th, vh + (C::kVHalf >> 4), idesc, 1u);  // hi·lo
@@ -650,13 +634,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                             }
                             __syncwarp();
                         }
-                        if (elect_one()) {
-                            umma2_commit_mc(&v_empty[vs], kBoth);
-                            if (RB_TRI_CP) umma2_commit_mc(&ab_empty[as], kBoth);  // copies done with the A/B stage
-                        }
+                        if (elect_one()) umma2_commit_mc(&v_empty[vs], kBoth);
                         __syncwarp();
                         if (++vs == C::kVStages) vs = 0, vph ^= 1u;
-                        if (++as == C::kABStages) as = 0;
                     }
                     if (elect_one()) umma2_commit_mc(&acc_full[buf], kBoth);
                     __syncwarp();
@@ -705,10 +685,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         if (lane == 0) mbar_arrive(&ab_empty[as]);  // this warp is done with the A/B stage
                     }
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        if (RB_TRI_ABLATE == 1 && NPAD == 80) jh[t] = pa_h[t] ^ pb_h[t], jl[t] = pa_l[t] ^ pb_l[t];
-                        else joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
-                    }
+                    for (int t = 0; t < 8; ++t)
+                        joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
                     const int64_t e = grow - static_cast<int64_t>(k) * TBK - 16 * g;  // J_ii = 1/n (kernel.cpp:98-99)
                     if (e >= 0 && e < 16) {
                         const int q = static_cast<int>(e);
@@ -725,18 +703,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
                     tc_fence_after();
                     const uint32_t ta = tmem + lane_off + C::kOpCol0 + slot * C::kOpCols;
-                    if (RB_TRI_ABLATE == 2 && NPAD == 80) {
-                        if (lane == 99) tmem_st8(ta, jh);  // never: no TMEM stores
-                    } else {
-                    if (!RB_TRI_CP) {
-                        tmem_st8(ta, pa_h);
-                        tmem_st8(ta + 8, pa_l);
-                        tmem_st8(ta + 16, pb_h);
-                        tmem_st8(ta + 24, pb_l);
-                    }
+                    tmem_st8(ta, pa_h);
+                    tmem_st8(ta + 8, pa_l);
+                    tmem_st8(ta + 16, pb_h);
+                    tmem_st8(ta + 24, pb_l);
                     tmem_st8(ta + 32, jh);
                     tmem_st8(ta + 40, jl);
-                    }
                     tmem_st_wait();
                     tc_fence_before();
                     __syncwarp();

@@ -434,13 +434,6 @@ __device__ __forceinline__ void umma2_f16_ts(uint32_t d_tmem, uint32_t a_tmem, u
         : "memory");
 }
 
-// smem -> TMEM copy of a 128-row x 256-bit slice (one K=16 slice of a 16-bit K-major operand, lane = row),
-// for both CTAs of the pair (each from its own shared memory at the descriptor's address); ordered with
-// the issuing thread's MMAs
-__device__ __forceinline__ void tmem_cp2_128x256b(uint32_t taddr, uint64_t sdesc) {
-    asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
-}
-
 // arrive (in every CTA of cta_mask, same offset) once the pair's previously issued MMAs complete
 __device__ __forceinline__ void umma2_commit_mc(uint64_t* bar, uint16_t cta_mask) {
     asm volatile(

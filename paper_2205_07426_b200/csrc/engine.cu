@@ -16,6 +16,12 @@
 
 namespace rb {
 
+// Row pitch (elements) of a stored kernel matrix: a multiple of 64 so every row starts on a
+// 128-byte line in the fp16 planes (and on a 512-byte boundary in fp64). With the former
+// round_up(n, 8) pitch, n = 100000 put odd rows 64 bytes into a line, so each 128-byte TMA row
+// touched two L2 lines (twice the requests, partial-line DRAM traffic).
+static inline int64_t matrix_pitch(int64_t n) { return ((n + 63) / 64) * 64; }
+
 void cuda_check(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;
     (void)cudaGetLastError();
@@ -428,7 +434,7 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
     k->prec = prec;
     assign_shard(ctx, *k);
     if (prec == kF64 && k->world > 1) fail(kInvalidArgument, "the fp64 configuration is single-rank");
-    k->ld = round_up(n, 8);
+    k->ld = matrix_pitch(n);
     const double inv_n = 1.0 / static_cast<double>(n);
     k->normalized = true;
     k->a_norm = 1.0;
@@ -512,7 +518,7 @@ KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
     k->prec = prec;
     assign_shard(ctx, *k);
     if (prec == kF64 && k->world > 1) fail(kInvalidArgument, "the fp64 configuration is single-rank");
-    k->ld = round_up(n, 8);
+    k->ld = matrix_pitch(n);
     k->normalized = false;
     std::vector<double> rm(static_cast<size_t>(k->rows) * k->ld, 0.0);
     double mx = 0.0, norm = 0.0;
@@ -652,7 +658,7 @@ public:
             plan_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.mf_kc));
             npad_ = tc_npad(s);
         } else {
-            plan_ = make_f64_plan(rows_, k.n);
+            plan_ = make_f64_plan(rows_, k.n, 2 * ctx.sms());
             npad_ = f64_npad(s);
         }
         const int rpb = plan_.rows_per_block;
@@ -803,7 +809,7 @@ public:
         {
             ctx_.prof_begin();
             launched(ctx_,
-                     launch_block_av_f64(k_.a64.as<double>(), rows_, k_.n, k_.ld, buf<double>(k), s_, ld_,
+                     launch_block_av_f64(k_.a64.as<double>(), rows_, k_.n, k_.ld, buf<double>(k), s_, ld_, plan_,
                                          w_.partial.as<double>(), ctx_.stream()),
                      "block_av_f64");
             ctx_.prof_end();

@@ -90,10 +90,10 @@ cudaError_t launch_block_av_mf(const MfMatrixView& a, const SplitPanelView& v, c
 cudaError_t launch_mf_prepare(const double* x, int64_t n, int d, int64_t rs, int64_t cs, int dp, int64_t npad,
                               __nv_bfloat16* xb, __nv_bfloat16* xa, cudaStream_t stream);
 
-StreamKPlan make_f64_plan(int64_t rows, int64_t cols);
+StreamKPlan make_f64_plan(int64_t rows, int64_t cols, int grid);
 int f64_npad(int cols);
 cudaError_t launch_block_av_f64(const double* a, int64_t rows, int64_t cols, int64_t lda, const double* v, int s,
-                                int64_t ldv, double* partial, cudaStream_t stream);
+                                int64_t ldv, const StreamKPlan& plan, double* partial, cudaStream_t stream);
 
 // ---- pass epilogue (recurrence + fused fp64 trace partials) --------------
 template <typename PT, typename ST>
