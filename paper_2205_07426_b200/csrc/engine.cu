@@ -385,6 +385,7 @@ void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, in
 // ---------------------------------------------------------------- kernel matrices
 KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
                          const double* y, int64_t dy, int64_t ldy, double sigma_y) {
+    NvtxRange nvtx("kernel build (Gram)");
     // upload column-major as given; validate_samples (proj/src/kernel.cpp:25-29) runs on the device copy
     if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
     if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
@@ -406,6 +407,7 @@ KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, in
 
 KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
                              const double* y, int64_t dy, int64_t ldy, double sigma_y) {
+    NvtxRange nvtx("kernel build (Gram)");
     // build_kernel(X, GaussianKernel{sigma}) (proj/src/kernel.cpp:35-72), samples resident on the device
     if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
     if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
@@ -715,6 +717,7 @@ public:
 
     // all ranks' operand slices -> full planes (in place)
     void gather_planes() {
+        NvtxRange nvtx("all-gather operand planes");
         if (!ctx_.exchange || k_.prec == kF64) return;
         const size_t chunk = static_cast<size_t>(s_) * ld_ * sizeof(__half);
         ctx_.exchange->allgather_inplace(w_.vhi.as<__half>(), chunk, ctx_.stream());
@@ -738,6 +741,7 @@ public:
 
     // block product of the current pass into the partials (split / matrix-free paths)
     void product() {
+        NvtxRange nvtx("block product");
         if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
         {
             SplitPanelView v = operand();
@@ -767,6 +771,7 @@ public:
 
     // pass epilogue over the partials the product left: T_new = a1·(A T) + a2·T + a3·T_prev, next planes
     void finish(double a1, double a2, double a3, double acc_coef) {
+        NvtxRange nvtx("pass epilogue");
         if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
         const int k = k_done_;
         const size_t s = static_cast<size_t>(s_);
@@ -839,6 +844,7 @@ public:
 
     // dots for passes [p0, p1] (inclusive), [p][3][s]; synchronizes
     std::vector<double> dots(int p0, int p1) {
+        NvtxRange nvtx("trace partials (reduce, all-reduce, read back)");
         const int np = p1 - p0 + 1;
         const size_t s = static_cast<size_t>(s_);
         if (R_ > 0) {
@@ -1044,6 +1050,7 @@ void matfun_traces(Context& ctx, const KernelMatrix& k, const MatFun& f, const d
 
 // ---------------------------------------------------------------- spectrum
 PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, double shift) {
+    NvtxRange nvtx("power iteration");
     // proj/src/spectrum.cpp:13-49; shift > 0 runs on (shift·I − A) without forming it
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     const int64_t ld = k.rpr;  // local rows of the start vector (row-sharded: counters from row0)
@@ -1272,6 +1279,7 @@ double exact_trace(Context& ctx, const KernelMatrix& k, const MatFun& f) {
 }  // namespace
 
 TraceEst hutchpp(Context& ctx, const KernelMatrix& k, const MatFun& f, const SketchCfg& cfg) {
+    NvtxRange nvtx("hutchpp");
     // proj/src/hutchpp.cpp:69-115, with probe injection / explicit split / Q-empty Hutchinson.
     // Row-sharded: every panel below holds this rank's rows; Grams are summed over ranks.
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
@@ -1481,6 +1489,7 @@ Resolved resolve(Context& ctx, const KernelMatrix& k, const EstParams& p) {
 }  // namespace
 
 EntropyEst estimate(Context& ctx, const KernelMatrix& k, const EstParams& p) {
+    NvtxRange nvtx("estimate");
     // proj/src/entropy.cpp:201-275
     const auto t0 = std::chrono::steady_clock::now();
     const Resolved r = resolve(ctx, k, p);
@@ -1710,6 +1719,7 @@ std::array<PanelResult, 3> run_panel3(Context& ctx, const Tri& t, const double* 
     for (int p = 0; p < P; ++p) {
         const SplitPanelView v[3] = {ps[0]->operand(), ps[1]->operand(), ps[2]->operand()};
         float* const part[3] = {ps[0]->partial(), ps[1]->partial(), ps[2]->partial()};
+        NvtxRange nvtx("fused MI pass");
         ctx.prof_begin();
         if (a.rows > 0)
             launched(ctx,
@@ -1883,6 +1893,7 @@ bool mutual_information_fused(Context& ctx, const KernelMatrix& a, const KernelM
 }  // namespace
 
 MutualInfo mutual_information(Context& ctx, const KernelMatrix& a, const KernelMatrix& b, const EstParams& p) {
+    NvtxRange nvtx("mutual_information");
     // proj/src/measures.cpp:36-46 (single-variable set: vars_joint = a)
     MutualInfo fused;
     if (mutual_information_fused(ctx, a, b, p, &fused)) return fused;

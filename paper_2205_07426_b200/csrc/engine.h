@@ -13,10 +13,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "host_math.h"
 #include "kernels.h"
 
 namespace rb {
+
+// NVTX range around one pass, collective or estimator phase (header-only NVTX v3: a no-op unless a
+// profiler injects its handler, so the ranges stay compiled in)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // kF64: fp64 A; kF32: A as fp16 hi/lo planes (fp32-class); kMF: matrix-free (bf16 samples, A never stored)
 enum Precision : int { kF64 = 0, kF32 = 1, kMF = 2 };

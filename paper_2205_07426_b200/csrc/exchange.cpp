@@ -54,6 +54,7 @@ public:
     int world() const override { return g_->world; }
 
     void allgather_inplace(void* buf, size_t chunk, cudaStream_t s) override {
+        NvtxRange nvtx("local group all-gather");
         cuda_check(cudaStreamSynchronize(s), "local group: stream sync");
         g_->ptrs[rank_] = buf;
         g_->barrier();
@@ -91,6 +92,7 @@ public:
 private:
     template <typename F>
     void reduce(void* buf, size_t bytes, cudaStream_t s, F&& combine) {
+        NvtxRange nvtx("local group all-reduce");
         cuda_check(cudaStreamSynchronize(s), "local group: stream sync");
         g_->ptrs[rank_] = buf;
         g_->barrier();
@@ -156,13 +158,16 @@ public:
     int rank() const override { return rank_; }
     int world() const override { return world_; }
     void allgather_inplace(void* buf, size_t chunk, cudaStream_t s) override {
+        NvtxRange nvtx("ncclAllGather");
         nccl_check(nccl().all_gather(static_cast<char*>(buf) + rank_ * chunk, buf, chunk, ncclUint8, comm_, s),
                    "ncclAllGather");
     }
     void allreduce_sum_f64(double* buf, size_t count, cudaStream_t s) override {
+        NvtxRange nvtx("ncclAllReduce sum");
         nccl_check(nccl().all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm_, s), "ncclAllReduce");
     }
     void allreduce_max_u32(unsigned* buf, size_t count, cudaStream_t s) override {
+        NvtxRange nvtx("ncclAllReduce max");
         nccl_check(nccl().all_reduce(buf, buf, count, ncclUint32, ncclMax, comm_, s), "ncclAllReduce");
     }
 
