@@ -124,6 +124,8 @@ def lib():
         h.oracle_cb_matfun_traces.argtypes = [_I64, MUL_FN, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
                                               _D, C.c_int, _D]
         h.oracle_kernel_block.argtypes = [_D, _I64, _I64, _D, _D, C.c_double, C.c_double, C.c_double, C.c_int, _D]
+        h.oracle_kernel_block_rows.argtypes = [_D, _D, _I64, _I64, _I64, _D, _D, C.c_double, C.c_double, C.c_double,
+                                               C.c_int, _D]
         _MF = [_D, _I64, _I64, C.c_double, _D, _I64, C.c_double]
         h.oracle_mf_matmul.argtypes = _MF + [_D, C.c_int, _D]
         h.oracle_mf_estimate.argtypes = _MF + [C.POINTER(CParams), C.POINTER(COut)]
@@ -540,8 +542,13 @@ class KernelBlocksOp:
     def kernel_block(self, i0, i1, j0, j1):
         out = np.empty((i1 - i0, j1 - j0))
         for f, (z, sq, inv2) in enumerate(self.feats):
-            dot = np.ascontiguousarray(z[i0:i1] @ z[j0:j1].T)
             sqi, sqj = np.ascontiguousarray(sq[i0:i1]), np.ascontiguousarray(sq[j0:j1])
+            if z.shape[1] <= 64:  # few features: dots in feature order in C (BLAS is slow at small K)
+                zi, zjt = np.ascontiguousarray(z[i0:i1]), np.ascontiguousarray(z[j0:j1].T)
+                lib().oracle_kernel_block_rows(_p(zi), _p(zjt), i1 - i0, j1 - j0, z.shape[1], _p(sqi), _p(sqj),
+                                               inv2, self.inv_n, float(self.n), 1 if f else 0, _p(out))
+                continue
+            dot = np.ascontiguousarray(z[i0:i1] @ z[j0:j1].T)
             lib().oracle_kernel_block(_p(dot), i1 - i0, j1 - j0, _p(sqi), _p(sqj), inv2, self.inv_n,
                                       float(self.n), 1 if f else 0, _p(out))
         if i0 == j0:

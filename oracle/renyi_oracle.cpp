@@ -1782,6 +1782,31 @@ int oracle_kernel_block(const double* dot, int64_t bi, int64_t bj, const double*
     }
     return 0;
 }
+// The same block from the samples directly (small d): dots summed over the features in order, as
+// gaussian_gram does (ops.cpp:43-45), vectorised over the block's columns. xi: bi x d row-major;
+// xjt: d x bj row-major (the block's columns transposed).
+int oracle_kernel_block_rows(const double* xi, const double* xjt, int64_t bi, int64_t bj, int64_t d,
+                             const double* sq_i, const double* sq_j, double inv2, double inv_n, double scale,
+                             int combine, double* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < bi; ++i) {
+        double* o = out + i * bj;
+        std::vector<double> dot(static_cast<size_t>(bj), 0.0);
+        for (int64_t t = 0; t < d; ++t) {
+            const double a = xi[i * d + t];
+            const double* xr = xjt + t * bj;
+            for (int64_t j = 0; j < bj; ++j) dot[j] += a * xr[j];
+        }
+        const double si = sq_i[i];
+        for (int64_t j = 0; j < bj; ++j) {
+            double d2 = si + sq_j[j] - 2.0 * dot[j];
+            d2 = d2 < 0.0 ? 0.0 : d2;
+            const double v = inv_n * orc::exp_nonpos(-d2 * inv2);
+            o[j] = combine ? scale * (o[j] * v) : v;
+        }
+    }
+    return 0;
+}
 int oracle_eigvals(const double* a, int64_t n, double* out) {
     return guard([&] {
         const orc::Vec l = orc::sym_eigvals(wrap(a, n, n));

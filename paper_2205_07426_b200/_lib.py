@@ -9,7 +9,10 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "librenyi_b200.so"
+# RB_LIB_VARIANT=<name> loads librenyi_b200_<name>.so (same-box A/B experiments built with
+# RB_LIB_VARIANT and RB_EXTRA_NVCC_FLAGS, see build.py); unset: the product library
+_VARIANT = os.environ.get("RB_LIB_VARIANT", "")
+LIB_PATH = Path(__file__).resolve().parent / (f"librenyi_b200_{_VARIANT}.so" if _VARIANT else "librenyi_b200.so")
 
 # errc kinds (proj/include/renyi/common.hpp:14-25) + 1, then device/runtime kinds
 STATUS_NAMES = {

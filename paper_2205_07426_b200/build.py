@@ -12,8 +12,10 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "_build"
-LIB = PKG / "librenyi_b200.so"
+# RB_LIB_VARIANT=<name>: developer A/B builds into _build_<name>/ and librenyi_b200_<name>.so
+_VARIANT = os.environ.get("RB_LIB_VARIANT", "")
+OBJ = PKG / (f"_build_{_VARIANT}" if _VARIANT else "_build")
+LIB = PKG / (f"librenyi_b200_{_VARIANT}.so" if _VARIANT else "librenyi_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
