@@ -77,7 +77,9 @@ struct MfCfg {
 
 struct MfArgs {
     int64_t total_iters;  // pair_blocks * j_blocks
-    int j_blocks;
+    int j_blocks;         // j-blocks of this launch's window
+    int j_off, j_total;   // window: j-block jb of the launch is global block (j_off + jb) mod j_total
+    __device__ int global_jb(int jb) const { return jb + j_off < j_total ? jb + j_off : jb + j_off - j_total; }
     int kc;               // j-blocks per O accumulation chunk
     int64_t row0;         // first global row of this rank
     int kt_chunk;         // j-blocks per V chunk (rpr / 128)
@@ -284,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                     tma_load_2d_2sm(base + h * C::kXSub, &map_xi, xi_full_l, h * 64, gi0, pol);
                 tma_load_2d_2sm(base + C::kXTile, &map_ar, xi_full_l, 0, gi0, pol);
                 for (int jb = j0; jb < j1; ++jb) {
-                    const int jr = jb * JB + static_cast<int>(rank) * (JB / 2);
+                    const int jr = args.global_jb(jb) * JB + static_cast<int>(rank) * (JB / 2);
                     mbar_wait(&x_empty[stage], phase ^ 1u);
                     if (leader) mbar_arrive_expect_tx(&x_full[stage], 2 * C::kXSlot);
                     const uint32_t bar = mapa_shared(&x_full[stage], 0);
@@ -314,7 +316,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                     if (leader) mbar_arrive_expect_tx(&v_full[stage], 2 * C::kVTile);
                     const uint32_t bar = mapa_shared(&v_full[stage], 0);
                     uint8_t* st = base + (vs_smem - base_u32) + stage * C::kVTile;
-                    const int vz = jb / args.kt_chunk, vx = (jb - vz * args.kt_chunk) * JB;
+                    const int jg = args.global_jb(jb);
+                    const int vz = jg / args.kt_chunk, vx = (jg - vz * args.kt_chunk) * JB;
                     for (int h = 0; h < 2; ++h)
                         tma_load_3d_2sm(st + h * C::kVSub, &map_v, bar, vx + h * 64, static_cast<int>(rank) * C::kNH,
                                         vz, pol);
@@ -473,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMfThreads, 1)
                 if (warp == 4 && lane == 0) { MF_STAMP(9, jc) }
                 tc_fence_after();
                 const uint32_t taddr = tmem + lane_off + sb * JB + h * CW;
-                if (jb == diag_jb)
+                if (args.global_jb(jb) == diag_jb)
                     exp_cols<true>(taddr, c2v, h * CW, row);
                 else
                     exp_cols<false>(taddr, c2v, h * CW, row);
@@ -557,6 +560,8 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     MfArgs args;
     args.total_iters = plan.total_iters;
     args.j_blocks = plan.k_tiles;
+    args.j_off = plan.k_off;
+    args.j_total = plan.k_total > 0 ? plan.k_total : plan.k_tiles;
     args.kc = plan.kc;
     args.row0 = a.row0;
     args.kt_chunk = static_cast<int>(v.rpr / JB);
@@ -617,12 +622,12 @@ __global__ void mf_prepare_kernel(const double* __restrict__ x, int64_t n, int d
 
 }  // namespace
 
-StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc) {
+StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc, KWindow w) {
     // CTA pairs over 256-row blocks; the epilogue reads 128-row blocks with cluster = 2
     StreamKPlan p;
     const int64_t pair_blocks = (rows + 2 * MB - 1) / (2 * MB);
     p.row_blocks = static_cast<int>((rows + MB - 1) / MB);
-    p.k_tiles = static_cast<int>((n + JB - 1) / JB);  // j-blocks
+    apply_window(p, n, JB, w);  // k tiles = j-blocks
     p.total_iters = pair_blocks * p.k_tiles;
     int pairs = std::max(1, grid / 2);
     if (p.total_iters < pairs) pairs = static_cast<int>(p.total_iters > 0 ? p.total_iters : 1);

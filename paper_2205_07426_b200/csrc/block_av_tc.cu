@@ -79,7 +79,8 @@ struct TcCfg {
 
 struct TcArgs {
     int64_t total_iters;  // row_blocks * k_tiles
-    int k_tiles;          // k tiles per row block
+    int k_tiles;          // k tiles per row block (of this launch's K window)
+    int k_off, k_total;   // K window: tile k of the launch is global tile (k_off + k) mod k_total
     int kt_chunk;         // k tiles per V chunk (rpr / BK)
     int kc;               // k tiles per TMEM chunk
     float* partial;       // [slots][NPAD][BM]
@@ -162,13 +163,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int rp = static_cast<int>(it / KT);
                 const int k = static_cast<int>(it - static_cast<int64_t>(rp) * KT);
                 const int r = 2 * rp + rank;
+                const int kg = k + args.k_off < args.k_total ? k + args.k_off : k + args.k_off - args.k_total;
                 mbar_wait(&empty_bar[stage], phase ^ 1u);  // both CTAs released this stage
                 uint8_t* st = smem_base + stage * C::kStageBytes;
                 mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
-                tma_load_2d(st, &map_ahi, &full_bar[stage], k * BK, r * BM, pol_stream);
-                tma_load_2d(st + C::kAPlane, &map_alo, &full_bar[stage], k * BK, r * BM, pol_stream);
-                const int vz = k / args.kt_chunk;               // V chunk (shard) holding these K rows
-                const int vx = (k - vz * args.kt_chunk) * BK;   // offset inside the chunk
+                tma_load_2d(st, &map_ahi, &full_bar[stage], kg * BK, r * BM, pol_stream);
+                tma_load_2d(st + C::kAPlane, &map_alo, &full_bar[stage], kg * BK, r * BM, pol_stream);
+                const int vz = kg / args.kt_chunk;              // V chunk (shard) holding these K rows
+                const int vx = (kg - vz * args.kt_chunk) * BK;  // offset inside the chunk
                 if (VSPLIT) {  // rank 0 multicasts V_hi, rank 1 V_lo
                     tma_load_3d_mc(st + 2 * C::kAPlane + rank * C::kVPlane, rank ? &map_vlo : &map_v,
                                    &full_bar[stage], vx, 0, vz, 0x3, pol_keep);
@@ -344,6 +346,8 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     TcArgs args;
     args.total_iters = plan.total_iters;
     args.k_tiles = plan.k_tiles;
+    args.k_off = plan.k_off;
+    args.k_total = plan.k_total > 0 ? plan.k_total : plan.k_tiles;
     args.kt_chunk = static_cast<int>(v.rpr / BK);
     args.kc = plan.kc;
     args.partial = partial;
@@ -409,7 +413,8 @@ struct TriCfg {
 
 struct TriArgs {
     int64_t total_iters;  // pair_blocks * k_tiles
-    int k_tiles;
+    int k_tiles;          // k tiles of this launch's K window
+    int k_off, k_total;   // K window: tile k of the launch is global tile (k_off + k) mod k_total
     int kt_chunk;         // k tiles per V chunk (rpr / BK)
     int kc;               // k tiles per TMEM chunk
     int64_t dp_blocks;    // pair blocks owned whole (waves of pairs); stream-K over the rest
@@ -566,22 +571,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
             while (sg.next(rp, k0, k1)) {
                 const int r = static_cast<int>(2 * rp + rank);
                 for (int k = k0; k < k1; ++k) {
+                    const int kg = k + args.k_off < args.k_total ? k + args.k_off : k + args.k_off - args.k_total;
                     if (warp == 0) {
                         mbar_wait(&ab_empty[as], aph ^ 1u);
                         uint8_t* st = base + as * C::kABStage;
                         mbar_arrive_expect_tx(&ab_full[as], C::kABStage);
-                        tma_load_2d(st, &map_ahi, &ab_full[as], k * TBK, r * TBM, pol_stream);
-                        tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], k * TBK, r * TBM, pol_stream);
-                        tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], k * TBK, r * TBM, pol_stream);
-                        tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], k * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st, &map_ahi, &ab_full[as], kg * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], kg * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], kg * TBK, r * TBM, pol_stream);
+                        tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], kg * TBK, r * TBM, pol_stream);
                         if (++as == C::kABStages) as = 0, aph ^= 1u;
                     } else {
                         mbar_wait(&v_empty[vs], vph ^ 1u);
                         if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * C::kVStage);
                         const uint32_t bar = mapa_shared(&v_full[vs], 0);
                         uint8_t* vt = base + (v_u32 - base_u32) + vs * C::kVStage;
-                        const int vz = k / args.kt_chunk;
-                        const int vx = (k - vz * args.kt_chunk) * TBK;
+                        const int vz = kg / args.kt_chunk;
+                        const int vx = (kg - vz * args.kt_chunk) * TBK;
 #pragma unroll
                         for (int q = 0; q < 3 * C::kVPer; ++q)  // rows [rank·NPAD/2, +NPAD/2) of every plane
                             tma_load_3d_2sm(vt + q * C::kVHalf, vmap[q / C::kVPer][q % C::kVPer], bar, vx,
@@ -662,6 +668,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         while (sg.next(rp, k0, k1)) {
             const int64_t grow = args.row0 + (2 * rp + rank) * TBM + row;  // global row (J diagonal)
             for (int k = k0; k < k1; ++k, ++u) {
+                const int kg = k + args.k_off < args.k_total ? k + args.k_off : k + args.k_off - args.k_total;
                 mbar_wait(&ab_full[as], aph);
                 const uint8_t* src = base + as * C::kABStage + row * 128;
 #pragma unroll
@@ -687,7 +694,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
 #pragma unroll
                     for (int t = 0; t < 8; ++t)
                         joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
-                    const int64_t e = grow - static_cast<int64_t>(k) * TBK - 16 * g;  // J_ii = 1/n (kernel.cpp:98-99)
+                    const int64_t e = grow - static_cast<int64_t>(kg) * TBK - 16 * g;  // J_ii = 1/n (kernel.cpp:98-99)
                     if (e >= 0 && e < 16) {
                         const int q = static_cast<int>(e);
                         const uint32_t mask = (q & 1) ? 0xFFFF0000u : 0x0000FFFFu;
@@ -801,6 +808,8 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
     TriArgs args;
     args.total_iters = plan.total_iters;
     args.k_tiles = plan.k_tiles;
+    args.k_off = plan.k_off;
+    args.k_total = plan.k_total > 0 ? plan.k_total : plan.k_tiles;
     args.kt_chunk = static_cast<int>(v[0].rpr / TBK);
     args.kc = plan.kc;
     args.dp_blocks = plan.dp_blocks;
@@ -826,11 +835,28 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
 int tc_block_rows() { return BM; }
 int tc_block_k() { return BK; }
 
-StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc) {
+// k tiles of a window: [col0 / tile, ceil(min(col0 + cols, n) / tile)), the end wrapping past n
+void apply_window(StreamKPlan& p, int64_t n, int tile, KWindow w) {
+    const int total = static_cast<int>((n + tile - 1) / tile);
+    if (w.cols < 0 || (w.col0 == 0 && w.cols >= n)) {
+        p.k_tiles = total;
+        p.k_off = 0, p.k_total = 0;
+        return;
+    }
+    const int64_t c0 = w.col0 % n;
+    const int off = static_cast<int>(c0 / tile);
+    const int64_t end = c0 + w.cols;  // may pass n: the window wraps
+    const int cnt = end <= n ? static_cast<int>((end + tile - 1) / tile) - off
+                             : (total - off) + static_cast<int>((end - n + tile - 1) / tile);
+    p.k_tiles = std::max(0, std::min(cnt, total));
+    p.k_off = off, p.k_total = total;
+}
+
+StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc, KWindow w) {
     // grid = CTAs (rounded down to pairs); iterations are (row-block-pair, k-tile)
     StreamKPlan p;
     p.row_blocks = static_cast<int>((rows + BM - 1) / BM);
-    p.k_tiles = static_cast<int>((cols + BK - 1) / BK);
+    apply_window(p, cols, BK, w);
     const int64_t pair_blocks = (p.row_blocks + 1) / 2;
     p.total_iters = pair_blocks * p.k_tiles;
     int pairs = std::max(1, grid / 2);
@@ -866,11 +892,11 @@ cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v
 #undef RB_TC_CASE
 }
 
-StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc) {
+StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc, KWindow w) {
     // 128-row blocks, CTA pairs walking the same k tiles (iterations: (row-block-pair, k-tile))
     StreamKPlan p;
     p.row_blocks = static_cast<int>((rows + TBM - 1) / TBM);
-    p.k_tiles = static_cast<int>((cols + TBK - 1) / TBK);
+    apply_window(p, cols, TBK, w);
     const int64_t pair_blocks = (p.row_blocks + 1) / 2;
     p.total_iters = pair_blocks * p.k_tiles;
     int pairs = std::max(1, grid / 2);

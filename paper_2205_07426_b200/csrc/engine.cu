@@ -282,10 +282,31 @@ Context::Context(int device) : device_(device) {
     probe_err.alloc(sizeof(int));
 }
 
+cudaStream_t Context::comm_stream() {
+    if (!comm_) {
+        cuda_check(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_main_, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    return comm_;
+}
+
+void Context::comm_after_main() {
+    cudaStream_t c = comm_stream();
+    cuda_check(cudaEventRecord(ev_main_, stream_), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(c, ev_main_, 0), "cudaStreamWaitEvent");
+}
+
+void Context::main_after_comm() {
+    cuda_check(cudaEventRecord(ev_comm_, comm_stream()), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(stream_, ev_comm_, 0), "cudaStreamWaitEvent");
+}
+
 Context::~Context() {
     cudaSetDevice(device_);
     // the members' scratch returns to the pool after this body: the stream is drained and no
     // longer tags those frees
+    if (comm_) cudaStreamSynchronize(comm_);
     if (stream_) cudaStreamSynchronize(stream_);
     if (t_stream == stream_) t_stream = nullptr;
     if (t0_) cudaEventDestroy(t0_);
@@ -294,10 +315,16 @@ Context::~Context() {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    if (ev_main_) cudaEventDestroy(ev_main_);
+    if (ev_comm_) cudaEventDestroy(ev_comm_);
+    if (comm_) cudaStreamDestroy(comm_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
-void Context::sync() { cuda_check(cudaStreamSynchronize(stream_), "stream synchronize"); }
+void Context::sync() {
+    cuda_check(cudaStreamSynchronize(stream_), "stream synchronize");
+    if (comm_) cuda_check(cudaStreamSynchronize(comm_), "comm stream synchronize");
+}
 
 void Context::prof_enable(bool on) {
     prof_ = on;
@@ -651,13 +678,24 @@ public:
         rows_ = k.rows;
         ld_ = k.rpr;  // state [s][rpr] (local rows); operand planes [world][s][rpr]
         mf_ = k.prec == kMF;
+        // row-sharded: each pass's product runs as two K windows, the rank's own operand chunk (ready
+        // after its own epilogue, overlapping the all-gather of the others on the comm stream) and the
+        // rest; both windows' partials meet in the epilogue (SURVEY §8(e) "overlap")
+        split_ = ctx.exchange && ctx.world() > 1 && k.prec != kF64;
+        if (split_) ctx.main_after_comm();  // a previous session's last gather may still be in flight
+        const KWindow own{k.row0, rows_}, rest{k.row0 + rows_, k.n - rows_};
         if (k.prec == kF32) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
-            plan_ = tri ? make_tri_plan(rows_, k.n, grid, ctx.kc) : make_streamk_plan(rows_, k.n, grid, ctx.kc);
+            auto mk = [&](KWindow w) {
+                return tri ? make_tri_plan(rows_, k.n, grid, ctx.kc, w) : make_streamk_plan(rows_, k.n, grid, ctx.kc, w);
+            };
+            plan_ = mk(split_ ? own : KWindow{});
+            if (split_) plan2_ = mk(rest);
             npad_ = tc_npad(s);
         } else if (mf_) {
             const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
-            plan_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.mf_kc));
+            plan_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.mf_kc), split_ ? own : KWindow{});
+            if (split_) plan2_ = make_mf_plan(rows_, k.n, grid, std::max(1, ctx.mf_kc), rest);
             npad_ = tc_npad(s);
         } else {
             plan_ = make_f64_plan(rows_, k.n, 2 * ctx.sms());
@@ -690,6 +728,7 @@ public:
         cuda_check(cudaMemsetAsync(w_.cmax.as<unsigned>(), 0, P1 * s * sizeof(unsigned), ctx.stream()), "memset");
         if (f32) {
             w_.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(float));
+            if (split_) w_.partial2.ensure(static_cast<size_t>(plan2_.slots) * npad_ * rpb * sizeof(float));
             PrepArgs<float> p{};
             p.x = x, p.ldx = ldx, p.rows = rows_, p.rows_per_block = rpb, p.s = s, p.ld = ld_;
             p.t0 = buf<float>(0);
@@ -702,7 +741,7 @@ public:
             if (rows_ > 0) launched(ctx, launch_prepare_split_stats(p, ctx.stream()), "prepare");
             if (ctx.exchange) ctx.exchange->allreduce_max_u32(w_.cmax.as<unsigned>(), s, ctx.stream());
             launched(ctx, launch_prepare_split_planes(p, ctx.stream()), "prepare");  // also writes e0
-            gather_planes();
+            gather_planes(-1);
         } else {
             w_.partial.ensure(static_cast<size_t>(plan_.slots) * npad_ * rpb * sizeof(double));
             PrepArgs<double> p{};
@@ -715,13 +754,20 @@ public:
         }
     }
 
-    // all ranks' operand slices -> full planes (in place)
-    void gather_planes() {
+    // all ranks' operand slices -> full planes (in place), on the comm stream after the epilogue that
+    // wrote this rank's slice; with the column maxima of pass `cmax_pass` (>= 0) all-reduced first (the
+    // next epilogue's plane scale). The next product's own-chunk window runs meanwhile; its other
+    // window waits for these collectives (product()).
+    void gather_planes(int cmax_pass) {
         NvtxRange nvtx("all-gather operand planes");
         if (!ctx_.exchange || k_.prec == kF64) return;
+        ctx_.comm_after_main();
+        cudaStream_t cs = ctx_.comm_stream();
+        if (cmax_pass >= 0)
+            ctx_.exchange->allreduce_max_u32(w_.cmax.as<unsigned>() + static_cast<size_t>(cmax_pass) * s_, s_, cs);
         const size_t chunk = static_cast<size_t>(s_) * ld_ * sizeof(__half);
-        ctx_.exchange->allgather_inplace(w_.vhi.as<__half>(), chunk, ctx_.stream());
-        if (vlo_) ctx_.exchange->allgather_inplace(vlo_, chunk, ctx_.stream());
+        ctx_.exchange->allgather_inplace(w_.vhi.as<__half>(), chunk, cs);
+        if (vlo_) ctx_.exchange->allgather_inplace(vlo_, chunk, cs);
     }
 
     void step(double a1, double a2, double a3, double acc_coef) {
@@ -733,38 +779,45 @@ public:
         }
     }
 
-    // the operand planes of the next pass, the partial buffer and the plan (fused MI pass)
+    // the operand planes of the next pass, the partial buffers and the plans (fused MI pass); split():
+    // two K windows (plan: own operand chunk, plan2: the rest after the all-gather)
     SplitPanelView operand() const { return SplitPanelView{w_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world}; }
     float* partial() const { return w_.partial.as<float>(); }
+    float* partial2() const { return w_.partial2.as<float>(); }
     const StreamKPlan& plan() const { return plan_; }
+    const StreamKPlan& plan2() const { return plan2_; }
+    bool split() const { return split_; }
     int64_t rows() const { return rows_; }
 
     // block product of the current pass into the partials (split / matrix-free paths)
     void product() {
         NvtxRange nvtx("block product");
         if (k_done_ >= max_passes_) fail(kInternal, "panel session pass budget exceeded");
-        {
-            SplitPanelView v = operand();
+        const SplitPanelView v = operand();
+        for (int w = 0; w < (split_ ? 2 : 1); ++w) {
+            const StreamKPlan& pl = w == 0 ? plan_ : plan2_;
+            float* part = w == 0 ? w_.partial.as<float>() : w_.partial2.as<float>();
+            if (w == 1) ctx_.main_after_comm();  // the other ranks' operand chunks have landed
+            // fraction of the pass's columns in this window (algorithmic accounting)
+            const double frac = split_ ? static_cast<double>(w == 0 ? rows_ : k_.n - rows_) / k_.n : 1.0;
             ctx_.prof_begin();
             if (mf_) {
                 MfMatrixView a{k_.xb.as<__nv_bfloat16>(), k_.xa.as<__nv_bfloat16>(), k_.n, round_up(k_.n, 128), k_.dp,
                                k_.row0, k_.c2};
-                if (rows_ > 0)
-                    launched(ctx_, launch_block_av_mf(a, v, plan_, w_.partial.as<float>(), ctx_.stream()),
-                             "block_av_mf");
+                if (rows_ > 0 && pl.k_tiles > 0)
+                    launched(ctx_, launch_block_av_mf(a, v, pl, part, ctx_.stream()), "block_av_mf");
                 ctx_.prof_end();
                 // algorithmic flops (SURVEY §8d matrix-free): 2·n_local·n·(d + s); bytes: X, V, Y
-                ctx_.prof_account(2.0 * k_.n * k_.dfeat + 2.0 * k_.n * s_ + 4.0 * rows_ * s_,
-                                  2.0 * rows_ * k_.n * (k_.dfeat + s_));
+                ctx_.prof_account(frac * (2.0 * k_.n * k_.dfeat + 2.0 * k_.n * s_) + 4.0 * rows_ * s_,
+                                  frac * 2.0 * rows_ * k_.n * (k_.dfeat + s_));
             } else {
                 SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
-                if (rows_ > 0)
-                    launched(ctx_, launch_block_av_tc(a, v, plan_, w_.partial.as<float>(), ctx_.stream()),
-                             "block_av_tc");
+                if (rows_ > 0 && pl.k_tiles > 0)
+                    launched(ctx_, launch_block_av_tc(a, v, pl, part, ctx_.stream()), "block_av_tc");
                 ctx_.prof_end();
                 // algorithmic bytes: A (4 B/entry) + V planes (4 B) + Y (4 B)
-                ctx_.prof_account(4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_ + 4.0 * rows_ * s_,
-                                  2.0 * rows_ * k_.n * s_);
+                ctx_.prof_account(frac * (4.0 * rows_ * k_.n + (vlo_ ? 4.0 : 2.0) * k_.n * s_) + 4.0 * rows_ * s_,
+                                  frac * 2.0 * rows_ * k_.n * s_);
             }
         }
     }
@@ -798,11 +851,16 @@ public:
             e.vop_lo = vlo_ ? vlo_ + slice_ : nullptr;
             e.stats = w_.stats.as<double>() + static_cast<size_t>(k + 1) * 3 * R_ * s;
             e.acc = acc_, e.acc_coef = acc_coef;
-            if (rows_ > 0) launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
-            if (ctx_.exchange) {
-                ctx_.exchange->allreduce_max_u32(w_.cmax.as<unsigned>() + (k + 1) * s, s, ctx_.stream());
-                gather_planes();
+            if (split_) {
+                e.partial2 = w_.partial2.as<float>();
+                e.total_iters2 = plan2_.total_iters, e.k_tiles2 = plan2_.k_tiles, e.grid2 = plan2_.grid;
+                e.dp_blocks2 = plan2_.dp_blocks;
             }
+            if (rows_ > 0) launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
+            // the last pass of the budget has no successor: no all-gather (its maxima are not read)
+            if (ctx_.exchange && k + 1 < max_passes_) gather_planes(k + 1);
+            else if (ctx_.exchange)
+                ctx_.exchange->allreduce_max_u32(w_.cmax.as<unsigned>() + (k + 1) * s, s, ctx_.stream());
         }
         ++k_done_;
     }
@@ -896,7 +954,8 @@ private:
     bool mf_ = false;
     __half* vlo_ = nullptr;
     size_t slice_ = 0;  // this rank's chunk offset in the operand planes
-    StreamKPlan plan_;
+    StreamKPlan plan_, plan2_;
+    bool split_ = false;
 };
 
 }  // namespace
@@ -1719,16 +1778,25 @@ std::array<PanelResult, 3> run_panel3(Context& ctx, const Tri& t, const double* 
     for (int p = 0; p < P; ++p) {
         const SplitPanelView v[3] = {ps[0]->operand(), ps[1]->operand(), ps[2]->operand()};
         float* const part[3] = {ps[0]->partial(), ps[1]->partial(), ps[2]->partial()};
+        float* const part2[3] = {ps[0]->partial2(), ps[1]->partial2(), ps[2]->partial2()};
         NvtxRange nvtx("fused MI pass");
-        ctx.prof_begin();
-        if (a.rows > 0)
-            launched(ctx,
-                     launch_block_av_tri(av, bv, v, ps[0]->plan(), part, a.row0, t.j.factor, t.j.diag, ctx.stream()),
-                     "block_av_tri");
-        ctx.prof_end();
-        // algorithmic bytes: A and B (4 B/entry each) + three operand panels + three results
-        ctx.prof_account(8.0 * a.rows * a.n + 3.0 * ((v[0].vlo ? 4.0 : 2.0) * a.n * s + 4.0 * a.rows * s),
-                         3.0 * 2.0 * a.rows * a.n * s);
+        // row-sharded: the rank's own operand chunk first, the other chunks after the sessions' all-gathers
+        for (int w = 0; w < (ps[0]->split() ? 2 : 1); ++w) {
+            const StreamKPlan& pl = w == 0 ? ps[0]->plan() : ps[0]->plan2();
+            if (w == 1) ctx.main_after_comm();
+            const double frac = ps[0]->split() ? static_cast<double>(w == 0 ? a.rows : a.n - a.rows) / a.n : 1.0;
+            ctx.prof_begin();
+            if (a.rows > 0 && pl.k_tiles > 0)
+                launched(ctx,
+                         launch_block_av_tri(av, bv, v, pl, w == 0 ? part : part2, a.row0, t.j.factor, t.j.diag,
+                                             ctx.stream()),
+                         "block_av_tri");
+            ctx.prof_end();
+            // algorithmic bytes: A and B (4 B/entry each) + three operand panels + three results
+            ctx.prof_account(frac * (8.0 * a.rows * a.n + 3.0 * (v[0].vlo ? 4.0 : 2.0) * a.n * s) +
+                                 3.0 * 4.0 * a.rows * s,
+                             frac * 3.0 * 2.0 * a.rows * a.n * s);
+        }
         for (int i = 0; i < 3; ++i) ps[i]->finish(sched[i][p][0], sched[i][p][1], sched[i][p][2], 0.0);
     }
     std::array<PanelResult, 3> r;

@@ -93,7 +93,7 @@ void shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* rows, in
 
 // device buffers of one panel session (recurrence state, operand planes, partials, reductions)
 struct PanelWorkspace {
-    DevBuf partial, stats, red, cmax, eexp;
+    DevBuf partial, partial2, stats, red, cmax, eexp;  // partial2: second K window (row-sharded passes)
     DevBuf state[4], vhi, vlo;
 };
 
@@ -108,6 +108,11 @@ public:
     }
     int sms() const { return sms_; }
     void sync();
+    // row-sharded passes: the operand all-gather (and the column-maxima all-reduce) run on a second
+    // stream, overlapped with the product over the rank's own operand chunk (created on first use)
+    cudaStream_t comm_stream();
+    void comm_after_main();  // comm stream waits for the work queued so far on the engine stream
+    void main_after_comm();  // engine stream waits for the collectives queued so far on the comm stream
 
     // tuning knobs of the block product
     int grid = 0;  // CTAs of the persistent stream-K kernel (0 = SM count)
@@ -154,6 +159,8 @@ private:
     size_t prof_used_ = 0;
     double prof_bytes_ = 0.0, prof_flops_ = 0.0;
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+    cudaStream_t comm_ = nullptr;
+    cudaEvent_t ev_main_ = nullptr, ev_comm_ = nullptr;
 };
 
 struct KernelMatrix {

@@ -53,19 +53,32 @@ struct StreamKPlan {
     // row blocks [0, dp_blocks) are owned whole, block r by CTA r % grid (data-parallel waves, slot r);
     // the remaining row blocks' iterations are split stream-K over the grid (slot r + CTA)
     int dp_blocks = 0;
+    // K window of the launch: its k tile k is global tile (k_off + k) mod k_total (k_total 0: no window,
+    // the launch covers every k tile). A row-sharded pass runs two windows: the rank's own chunk of the
+    // operand (ready right after its epilogue) and the other ranks' chunks (after the all-gather).
+    int k_off = 0;
+    int k_total = 0;
+};
+
+// window [col0, col0 + cols) (columns of A = rows of the operand, wrapping at n) in a plan's k tiles
+struct KWindow {
+    int64_t col0 = 0;
+    int64_t cols = -1;  // -1: all columns
 };
 
 // ---- block product -------------------------------------------------------
 int tc_block_rows();
 int tc_block_k();
 int tc_npad(int cols);
-StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc);
+// sets p.k_tiles / k_off / k_total for window w over n columns in tiles of `tile` columns
+void apply_window(StreamKPlan& p, int64_t n, int tile, KWindow w);
+StreamKPlan make_streamk_plan(int64_t rows, int64_t cols, int grid, int kc, KWindow w = {});
 cudaError_t launch_block_av_tc(const SplitMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream);
 // fused mutual-information pass: Y_A = A·V[0], Y_B = B·V[1], Y_J = J·V[2] with J = n·(A∘B) (J_ii = 1/n)
 // formed from the staged A and B tiles (stored J = factor·stored A·stored B, stored J_ii = diag);
 // 128-row blocks (make_tri_plan), all three panels of the same width <= tri_max_cols()
-StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc);
+StreamKPlan make_tri_plan(int64_t rows, int64_t cols, int grid, int kc, KWindow w = {});
 int tri_max_cols();
 cudaError_t launch_block_av_tri(const SplitMatrixView& a, const SplitMatrixView& b, const SplitPanelView* v,
                                 const StreamKPlan& plan, float* const* partial, int64_t row0, double factor,
@@ -81,7 +94,7 @@ struct MfMatrixView {
     int64_t row0;
     double c2;  // log2(e)/σ²
 };
-StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc);
+StreamKPlan make_mf_plan(int64_t rows, int64_t n, int grid, int kc, KWindow w = {});
 int mf_aug_cols();
 cudaError_t launch_block_av_mf(const MfMatrixView& a, const SplitPanelView& v, const StreamKPlan& plan,
                                float* partial, cudaStream_t stream);
@@ -126,6 +139,13 @@ struct EpiArgs {
     double* stats;  // [3][row_blocks][s]
     double* acc;    // optional vector accumulator (fp64, [s][ld])
     double acc_coef;
+    // second K window of a row-sharded pass (the other ranks' operand chunks, see StreamKPlan::k_off):
+    // its slots are summed after the first window's, in the same fixed order; partial2 == nullptr: none
+    const PT* partial2 = nullptr;
+    int64_t total_iters2 = 0;
+    int k_tiles2 = 0;
+    int grid2 = 1;
+    int dp_blocks2 = 0;
 };
 
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream);

@@ -61,20 +61,27 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     const int warp = tid / 32, lane = tid % 32;
     const int64_t i = static_cast<int64_t>(r) * ER + tid;
     const bool valid = i < p.rows;
-    const int64_t KT = p.k_tiles;
     const int64_t cl = p.cluster, rb = r / cl, rr = r % cl;
-    int64_t c_lo = 0, c_hi = 0;  // whole row block owned by one CTA: slot rb
-    if (rb >= p.dp_blocks) {
-        const int64_t rt = rb - p.dp_blocks, tail = p.total_iters - static_cast<int64_t>(p.dp_blocks) * KT;
-        c_lo = streamk_owner(rt * KT, tail, p.grid);
-        c_hi = streamk_owner((rt + 1) * KT - 1, tail, p.grid);
-    }
+    // slots [c_lo, c_hi] of row block rb under a plan (whole row blocks: slot rb)
+    auto owners = [&](int64_t KT, int64_t total_iters, int grid, int64_t dp, int64_t& lo, int64_t& hi) {
+        lo = hi = 0;
+        if (rb >= dp) {
+            const int64_t rt = rb - dp, tail = total_iters - dp * KT;
+            lo = streamk_owner(rt * KT, tail, grid);
+            hi = streamk_owner((rt + 1) * KT - 1, tail, grid);
+        }
+    };
+    int64_t c_lo, c_hi, c2_lo = 0, c2_hi = -1;
+    owners(p.k_tiles, p.total_iters, p.grid, p.dp_blocks, c_lo, c_hi);
+    if (p.partial2) owners(p.k_tiles2, p.total_iters2, p.grid2, p.dp_blocks2, c2_lo, c2_hi);
     const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
 
     for (int j = jb0; j < jb1; ++j) {
         double y = 0.0;
         for (int64_t c = c_lo; c <= c_hi; ++c)
             y += static_cast<double>(p.partial[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
+        for (int64_t c = c2_lo; c <= c2_hi; ++c)
+            y += static_cast<double>(p.partial2[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
         if (SPLIT) y = ldexp(y * p.unscale, -p.e_cur[j]);
         double tc = 0.0, tp = 0.0, x0 = 0.0;
         const int64_t idx = static_cast<int64_t>(j) * p.ld + i;

@@ -2,7 +2,8 @@
 
 The device path shards A by rows: rank p owns rows
 [p·rpr, (p+1)·rpr) of A (rpr a multiple of 256), each pass computes its rows of
-A·V, all-gathers the next fp16 operand planes laid out [world][s][rpr], max-reduces
+A·V in two K windows -- its own operand chunk while the all-gather of the others is in
+flight, then the rest -- all-gathers the next fp16 operand planes laid out [world][s][rpr], max-reduces
 the per-column maxima (so every rank picks the same plane scale) and sum-reduces the
 row-separable fp64 trace partials once per estimate; CholeskyQR2/projection Grams are
 sum-reduced. These tests run that exact protocol with the fp64 oracle as the compute
@@ -62,14 +63,20 @@ def _worker(rank, world, port, n, out_path):
     G_full = R.gaussian_panel(n, s_g, 3, "hutchpp-probe")
     S, G = S_full[row0:row0 + rows], G_full[row0:row0 + rows]
 
-    def allgather_rows(local, cols):
-        """[rows x cols] local -> full [n x cols] through the [world][cols][rpr] plane layout."""
+    own = np.arange(row0, row0 + rows)
+    rest = np.r_[np.arange(row0 + rows, n), np.arange(0, row0)]  # the other chunks, wrapping at n
+
+    def product(local, cols):
+        """A_p · V with the device schedule: the all-gather of V's chunks in flight while the rank's
+        own K window (its own chunk) is multiplied, then the other window once the gather lands."""
         chunk = torch.zeros((cols, rpr), dtype=torch.float64)
         chunk[:, :rows] = torch.from_numpy(np.ascontiguousarray(local.T))
         planes = [torch.zeros_like(chunk) for _ in range(world)]
-        dist.all_gather(planes, chunk)
-        full = torch.cat([p for p in planes], dim=1)[:, :n]  # chunk w holds global rows w*rpr ..
-        return full.numpy().T.copy()
+        work = dist.all_gather(planes, chunk, async_op=True)
+        y = a_p[:, own] @ local  # own window: no remote data needed
+        work.wait()
+        full = torch.cat([p for p in planes], dim=1)[:, :n].numpy().T
+        return y + a_p[:, rest] @ full[rest]  # second window, summed after the first (epilogue order)
 
     def allreduce(arr, op=dist.ReduceOp.SUM):
         t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
@@ -77,7 +84,7 @@ def _worker(rank, world, port, n, out_path):
         return t.numpy()
 
     # sketch pass and CholeskyQR2 with summed Grams
-    Y = a_p @ allgather_rows(S, s_q)
+    Y = product(S, s_q)
     g = allreduce(Y.T @ Y)
     w, v = np.linalg.eigh(g)
     keep = w > 1e-13 * w.max()
@@ -90,11 +97,11 @@ def _worker(rank, world, port, n, out_path):
     c, safe_v = orc.spec_coeffs(orc.Spec("chebyshev", alpha, m, 0.0, 1.0))
     scale, center = 2.0 / safe_v, 1.0
     dots = [allreduce(np.einsum("ij,ij->j", X0, X0))]
-    tp, tc = X0, scale * (a_p @ allgather_rows(X0, X0.shape[1])) - center * X0
+    tp, tc = X0, scale * product(X0, X0.shape[1]) - center * X0
     cmax = allreduce(np.abs(tc).max(axis=0) if rows else np.zeros(X0.shape[1]), dist.ReduceOp.MAX)
     local_dots = [np.einsum("ij,ij->j", X0, tc)]
     for _ in range(2, m + 1):
-        tn = 2 * (scale * (a_p @ allgather_rows(tc, tc.shape[1])) - center * tc) - tp
+        tn = 2 * (scale * product(tc, tc.shape[1]) - center * tc) - tp
         local_dots.append(np.einsum("ij,ij->j", X0, tn))
         cmax = allreduce(np.abs(tn).max(axis=0), dist.ReduceOp.MAX)
         tp, tc = tc, tn
