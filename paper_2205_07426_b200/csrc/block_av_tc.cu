@@ -553,7 +553,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_base_smem;
 
-    // registers move only between warpgroups of the CTA: 4x(80-40) + 8x(80-72) >= 12x(96-80) per thread
+    // registers move only between warpgroups of the CTA: 4x(80-40) + 8x(80-64) = 12x(104-80) per thread
+    // (drains: 80 fp32 accumulators + a 16-column TMEM load in flight)
     if (RB_TRI_SETMAXNREG && warp < kTriConv0) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 0 || warp == 2) {
         // ---------------- TMA: A/B tiles of this CTA's rows (warp 0, local ring); its half of the V planes
@@ -652,8 +653,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         }
     } else if (warp >= kTriConv0 && warp < kTriConv0 + kTriConv) {
         // ---------------- operand builders: A, B and J = n·(A∘B) into TMEM ----------------
-        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
-        const int half = (warp - kTriConv0) / 4;  // K groups {2·half, 2·half + 1} (16 columns each) of the tile
+        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+        // K groups {half, half + 2} (16 columns each) of the tile: the two halves build groups 0 and 1
+        // side by side, then 2 and 3 -- the order the MMA issuer consumes them in
+        const int half = (warp - kTriConv0) / 4;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int sw = row & 7;  // 128-byte swizzle: 16-byte chunk c of row r sits at c ^ (r & 7)
@@ -673,7 +676,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                 const uint8_t* src = base + as * C::kABStage + row * 128;
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
-                    const int g = 2 * half + sub;  // K group: columns [16g, 16g + 16) of the tile
+                    const int g = half + 2 * sub;  // K group: columns [16g, 16g + 16) of the tile
                     uint32_t pa_h[8], pa_l[8], pb_h[8], pb_l[8], jh[8], jl[8];
 #pragma unroll
                     for (int c2 = 0; c2 < 2; ++c2) {
@@ -726,7 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         }
     } else if (warp >= kTriDrain0) {
         // ---------------- TMEM drains: operand (warp-12)/4, lane quarter warp%4 ----------------
-        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");
+        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
         const int op = (warp - kTriDrain0) / 4;
         const int quarter = warp & 3;
         const int row_local = quarter * 32 + lane;
@@ -745,13 +748,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                 mbar_wait(&acc_full[buf], (chunk / C::kBufs) & 1u);
                 tc_fence_after();
                 const uint32_t t0 = lane_base + buf * (3 * NPAD);
+                // 16 columns per TMEM load round trip (the MMA issuer waits for this drain at every
+                // chunk boundary: the accumulator is single-buffered)
 #pragma unroll
-                for (int j0 = 0; j0 < NPAD; j0 += 8) {
-                    float m[8];
-                    tmem_ld8(t0 + j0, m);
+                for (int j0 = 0; j0 < NPAD; j0 += 16) {
+                    float m[16];
+                    tmem_ld16(t0 + j0, m);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[j0 + i] += m[i];
+                    for (int i = 0; i < 16; ++i) acc[j0 + i] += m[i];
                 }
                 tc_fence_before();
                 __syncwarp();
