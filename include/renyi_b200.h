@@ -155,6 +155,10 @@ int renyi_ctx_set_operand_mode(renyi_ctx* ctx, int mode);
  * A and B per pass with the joint kernel n·A∘B formed on the fly (never stored); 0: three separate
  * estimates over a materialised joint (proj/src/measures.cpp:36-46) */
 int renyi_ctx_set_fused_mi(renyi_ctx* ctx, int on);
+/* rank_features / select_features over fp32 kernels: 1 (default) scores the candidates of a step as
+ * grouped stacks (one block product per pass for up to 64 candidates' kernels); 0: one
+ * candidate at a time, as the reference's loop (proj/src/features.cpp:95-162) */
+int renyi_ctx_set_feature_grouping(renyi_ctx* ctx, int on);
 /* matrix-free product: j-blocks (of 128 samples) accumulated in TMEM before each fp32 drain */
 int renyi_ctx_set_matrix_free_chunk(renyi_ctx* ctx, int jblocks);
 int renyi_ctx_sync(renyi_ctx* ctx);

@@ -71,6 +71,11 @@ class Context:
         joint kernel n·A∘B is formed on the fly, never stored); False: three separate estimates."""
         check(L.lib().renyi_ctx_set_fused_mi(self._h, 1 if on else 0))
 
+    def set_feature_grouping(self, on: bool = True) -> None:
+        """rank_features / select_features over fp32 kernels: score each step's candidates as grouped
+        stacks (default) or one at a time (the reference's loop)."""
+        check(L.lib().renyi_ctx_set_feature_grouping(self._h, 1 if on else 0))
+
     def sync(self) -> None:
         check(L.lib().renyi_ctx_sync(self._h))
 

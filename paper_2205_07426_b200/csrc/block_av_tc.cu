@@ -82,6 +82,7 @@ struct TcArgs {
     int k_tiles;          // k tiles per row block (of this launch's K window)
     int k_off, k_total;   // K window: tile k of the launch is global tile (k_off + k) mod k_total
     int kt_chunk;         // k tiles per V chunk (rpr / BK)
+    int64_t g_rows;       // grouped stacked matrices: operand offset of row block r's group (0: none)
     int kc;               // k tiles per TMEM chunk
     float* partial;       // [slots][NPAD][BM]
     int a_policy;         // 0: evict_first for the A stream, 1: evict_normal
@@ -170,7 +171,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tma_load_2d(st, &map_ahi, &full_bar[stage], kg * BK, r * BM, pol_stream);
                 tma_load_2d(st + C::kAPlane, &map_alo, &full_bar[stage], kg * BK, r * BM, pol_stream);
                 const int vz = kg / args.kt_chunk;              // V chunk (shard) holding these K rows
-                const int vx = (kg - vz * args.kt_chunk) * BK;  // offset inside the chunk
+                int vx = (kg - vz * args.kt_chunk) * BK;        // offset inside the chunk
+                if (args.g_rows > 0)  // the group's own operand rows (a CTA pair never straddles groups)
+                    vx += static_cast<int>((static_cast<int64_t>(r) * BM / args.g_rows) * args.g_rows);
                 if (VSPLIT) {  // rank 0 multicasts V_hi, rank 1 V_lo
                     tma_load_3d_mc(st + 2 * C::kAPlane + rank * C::kVPlane, rank ? &map_vlo : &map_v,
                                    &full_bar[stage], vx, 0, vz, 0x3, pol_keep);
@@ -349,6 +352,7 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     args.k_off = plan.k_off;
     args.k_total = plan.k_total > 0 ? plan.k_total : plan.k_tiles;
     args.kt_chunk = static_cast<int>(v.rpr / BK);
+    args.g_rows = v.group_rows;
     args.kc = plan.kc;
     args.partial = partial;
     args.a_policy = 0;

@@ -247,6 +247,13 @@ int renyi_ctx_set_fused_mi(renyi_ctx* ctx, int on) {
     });
 }
 
+int renyi_ctx_set_feature_grouping(renyi_ctx* ctx, int on) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        ctx->ctx.feature_groups = on != 0;
+    });
+}
+
 int renyi_ctx_sync(renyi_ctx* ctx) {
     return guarded([&] {
         need(ctx, "ctx");

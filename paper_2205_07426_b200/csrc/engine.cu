@@ -685,7 +685,7 @@ public:
         if (split_) ctx.main_after_comm();  // a previous session's last gather may still be in flight
         const KWindow own{k.row0, rows_}, rest{k.row0 + rows_, k.n - rows_};
         if (k.prec == kF32) {
-            const int grid = ctx.grid > 0 ? ctx.grid : ctx.sms();
+            const int grid = k.group_grid > 0 ? k.group_grid : ctx.grid > 0 ? ctx.grid : ctx.sms();
             auto mk = [&](KWindow w) {
                 return tri ? make_tri_plan(rows_, k.n, grid, ctx.kc, w) : make_streamk_plan(rows_, k.n, grid, ctx.kc, w);
             };
@@ -781,7 +781,9 @@ public:
 
     // the operand planes of the next pass, the partial buffers and the plans (fused MI pass); split():
     // two K windows (plan: own operand chunk, plan2: the rest after the all-gather)
-    SplitPanelView operand() const { return SplitPanelView{w_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world}; }
+    SplitPanelView operand() const {
+        return SplitPanelView{w_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world, k_.group_rows};
+    }
     float* partial() const { return w_.partial.as<float>(); }
     float* partial2() const { return w_.partial2.as<float>(); }
     const StreamKPlan& plan() const { return plan_; }
@@ -921,6 +923,21 @@ public:
         ctx_.sync();
         return out;
     }
+
+    // dots of row blocks [r0, r0 + count) only (one group of a grouped stack; single rank), [p][3][s]
+    std::vector<double> dots_range(int p0, int p1, int r0, int count) {
+        const int np = p1 - p0 + 1;
+        const size_t s = static_cast<size_t>(s_);
+        launched(ctx_,
+                 launch_reduce_stats(w_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
+                                     w_.red.as<double>(), ctx_.stream(), r0, count),
+                 "reduce_stats");
+        std::vector<double> out(static_cast<size_t>(np) * 3 * s);
+        d2h(ctx_, out.data(), w_.red.as<double>(), out.size() * sizeof(double));
+        ctx_.sync();
+        return out;
+    }
+    int rows_per_block() const { return plan_.rows_per_block; }
 
     void state_f64(int k, double* out, int64_t ldo) {
         const bool f32 = k_.prec != kF64;
@@ -2027,6 +2044,241 @@ std::string FeatureData::name(int j) const {
     return j < static_cast<int>(names.size()) ? names[j] : "feature_" + std::to_string(j);
 }
 
+// ---------------------------------------------------------------- grouped estimates (feature tools)
+// Scoring feature candidates (proj/src/features.cpp:44-162) is many estimates with identical
+// parameters over different n x n kernels of the same n; at the reference's n <= 14k each estimate
+// alone is latency-bound (a few hundred KB-MB per pass, host round trips for Hutch++'s QR). Here G
+// candidates' kernels sit in ONE stacked allocation (KernelMatrix::groups) and every pass is one
+// block product over all of them (the operand chunk of each group read through the stacked operand
+// planes), one epilogue, one trace reduction per group; only the small per-candidate QR stays
+// per group. Every row block is computed whole by one CTA pair (the stack is padded to whole
+// pair-block waves), so a candidate's numbers do not depend on its position in the stack: identical
+// features score bitwise identically, as in the reference's sequential loop.
+namespace {
+
+constexpr int kGroupMax = 64;                  // candidates per stack
+constexpr double kGroupBytes = 12e9;           // per stacked matrix
+
+int64_t group_rows_of(int64_t n) { return round_up(n, 512); }
+
+int group_capacity(int64_t n) {
+    const double per = static_cast<double>(group_rows_of(n)) * matrix_pitch(n) * 4.0;
+    return static_cast<int>(std::max(1.0, std::min<double>(kGroupMax, std::floor(kGroupBytes / per))));
+}
+
+KernelPtr alloc_group(Context& ctx, int64_t n, int groups) {
+    auto k = std::make_unique<KernelMatrix>();
+    k->n = n, k->prec = kF32, k->world = 1, k->rank = 0, k->row0 = 0;
+    k->ld = matrix_pitch(n);
+    k->groups = groups;
+    k->group_rows = group_rows_of(n);
+    const int64_t pb = static_cast<int64_t>(groups) * k->group_rows / 512;  // CTA-pair row blocks
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(ctx.sms() / 2, pb));
+    const int64_t waves = (pb + pairs - 1) / pairs;
+    k->rows = pairs * waves * 512;  // zero pair blocks pad the last wave
+    k->rpr = k->rows;
+    k->group_grid = static_cast<int>(2 * pairs);
+    k->unscale = (1.0 / static_cast<double>(n)) / kSplitScale;
+    k->a_norm = 1.0;
+    k->normalized = true;
+    const size_t elems = static_cast<size_t>(k->rows) * k->ld;
+    k->hi.alloc(elems * sizeof(__half));
+    k->lo.alloc(elems * sizeof(__half));
+    cuda_check(cudaMemsetAsync(k->hi.as<void>(), 0, elems * sizeof(__half), ctx.stream()), "memset");
+    cuda_check(cudaMemsetAsync(k->lo.as<void>(), 0, elems * sizeof(__half), ctx.stream()), "memset");
+    return k;
+}
+
+__half* group_hi(const KernelMatrix& k, int g) { return k.hi.as<__half>() + static_cast<size_t>(g) * k.group_rows * k.ld; }
+__half* group_lo(const KernelMatrix& k, int g) { return k.lo.as<__half>() + static_cast<size_t>(g) * k.group_rows * k.ld; }
+
+// build_kernel(X[:, col], GaussianKernel{sigma}) into group g: the fp32 build_gaussian_dev's Gram, same
+// arguments, so the planes are bitwise those of a singly built feature kernel
+void group_gram(Context& ctx, const KernelMatrix& k, int g, const double* d_col, double sigma) {
+    GramArgs ga{};
+    ga.x = d_col, ga.dx = 1, ga.x_rs = 1, ga.x_cs = k.n;
+    ga.inv_two_sigma2_x = 1.0 / (2.0 * sigma * sigma);
+    ga.y = nullptr, ga.dy = 0, ga.y_rs = 1, ga.y_cs = 0, ga.inv_two_sigma2_y = 0.0;
+    ga.n = k.n, ga.row0 = 0, ga.rows = k.n, ga.ld = k.ld;
+    ga.inv_n = 1.0 / static_cast<double>(k.n);
+    ga.f32_compute = 1;
+    DevBuf scratch;
+    scratch.alloc(gram_split_scratch_bytes(ga));
+    launched(ctx, launch_gram_split(ga, group_hi(k, g), group_lo(k, g), scratch.as<void>(), ctx.stream()), "gram_split");
+}
+
+// group g <- hadamard_joint(a, b) (proj/src/kernel.cpp:74-101, L = 2), a / b single fp32 kernels or groups
+void group_hadamard(Context& ctx, const KernelMatrix& out, int g, const __half* ahi, const __half* alo,
+                    const __half* bhi, const __half* blo) {
+    const double inv_n = 1.0 / static_cast<double>(out.n);
+    const double factor = static_cast<double>(out.n) * out.unscale * out.unscale / out.unscale;
+    const double diag = inv_n / out.unscale;
+    launched(ctx,
+             launch_hadamard_split(ahi, alo, bhi, blo, out.n, out.n, out.ld, 0, factor, diag, group_hi(out, g),
+                                   group_lo(out, g), ctx.stream()),
+             "hadamard_split");
+}
+
+// Hutch++ (proj/src/hutchpp.cpp:69-115) for groups [0, count) of a stack, seeded probes shared by all
+// (every candidate of a feature-scoring step uses the same term seed). Callers guarantee the
+// non-degenerate branch: 0 < s_q < n and s_g < n - s_q. errors[g] receives a candidate's failure.
+std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int count, const MatFun& f,
+                                    const SketchCfg& cfg, std::vector<std::string>& errors, std::vector<int>& codes) {
+    const int64_t n = k.n, gr = k.group_rows, ld = k.rpr;
+    const int s_q = cfg.s_q, s_g = cfg.s_g, cost = f.query_cost();
+    std::vector<TraceEst> est(count);
+    auto replicate = [&](DevBuf& dst, int cols, const char* label) {
+        DevBuf one;
+        one.alloc(static_cast<size_t>(cols) * n * sizeof(double));
+        cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
+        launched(ctx,
+                 launch_rng_panel(derive_key(cfg.seed, hash_name(label)), true, cfg.probe_kind, 0, n, cols, 0,
+                                  one.as<double>(), n, ctx.probe_err.as<int>(), ctx.stream()),
+                 "rng_panel");
+        dst.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
+        cuda_check(cudaMemsetAsync(dst.as<void>(), 0, static_cast<size_t>(cols) * ld * sizeof(double), ctx.stream()),
+                   "memset");
+        for (int g = 0; g < count; ++g)
+            cuda_check(cudaMemcpy2DAsync(dst.as<double>() + g * gr, ld * sizeof(double), one.as<double>(),
+                                         n * sizeof(double), n * sizeof(double), cols, cudaMemcpyDeviceToDevice,
+                                         ctx.stream()),
+                       "replicate probes");
+        int err = 0;
+        d2h(ctx, &err, ctx.probe_err.as<int>(), sizeof(int));
+        ctx.sync();
+        if (err) fail(kInternal, "probe stream hit the 2^-53 Box-Muller redraw; pass the probes explicitly");
+    };
+    // sketch products of every group in one pass: Y = A·S
+    DevBuf sk, y;
+    replicate(sk, s_q, "hutchpp-sketch");
+    y.alloc(static_cast<size_t>(s_q) * ld * sizeof(double));
+    for (int j0 = 0; j0 < s_q; j0 += kMaxPanelCols) {
+        const int w = std::min(kMaxPanelCols, s_q - j0);
+        run_panel(ctx, k, sk.as<double>() + static_cast<int64_t>(j0) * ld, ld, w, {{1.0, 0.0, 0.0}}, nullptr, nullptr,
+                  y.as<double>() + static_cast<int64_t>(j0) * ld, ld);
+    }
+    std::vector<DevBuf> q(count);
+    std::vector<int> rank(count, 0);
+    int rmax = 0;
+    for (int g = 0; g < count; ++g) {  // the per-candidate QR (s_q columns of n rows)
+        rank[g] = orthonormal_range(ctx, y.as<double>() + g * gr, s_q, ld, n, q[g]);
+        if (rank[g] == 0 && errors[g].empty()) {
+            errors[g] = "hutchpp sketch A*S is numerically zero";
+            codes[g] = kRankCollapse;
+        }
+        rmax = std::max(rmax, rank[g]);
+    }
+    // X0 = [Q_g (zero-padded to rmax columns) | W_g],  W_g = G - Q_g (Q_gᵀ G)
+    const int cols = rmax + s_g;
+    DevBuf gp, x0;
+    replicate(gp, s_g, "hutchpp-probe");
+    x0.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
+    cuda_check(cudaMemsetAsync(x0.as<void>(), 0, static_cast<size_t>(cols) * ld * sizeof(double), ctx.stream()),
+               "memset");
+    for (int g = 0; g < count; ++g) {
+        double* xg = x0.as<double>() + g * gr;
+        double* wg = xg + static_cast<int64_t>(rmax) * ld;
+        const double* gg = gp.as<double>() + g * gr;
+        if (rank[g] > 0) {
+            cuda_check(cudaMemcpy2DAsync(xg, ld * sizeof(double), q[g].as<double>(), ld * sizeof(double),
+                                         n * sizeof(double), rank[g], cudaMemcpyDeviceToDevice, ctx.stream()),
+                       "copy Q");
+            std::vector<double> c = gram_host(ctx, q[g].as<double>(), rank[g], ld, gg, s_g, ld, n);
+            for (double& v : c) v = -v;
+            update(ctx, 1.0, gg, ld, q[g].as<double>(), rank[g], ld, c, s_g, n, wg, ld);
+        } else {
+            cuda_check(cudaMemcpy2DAsync(wg, ld * sizeof(double), gg, ld * sizeof(double), n * sizeof(double), s_g,
+                                         cudaMemcpyDeviceToDevice, ctx.stream()),
+                       "copy probes");
+        }
+    }
+    // quadratic forms of every group by moment doubling (panel_traces), dots reduced per group
+    const auto full = schedule(f);
+    const int passes = (f.degree + 1) / 2;
+    const std::vector<std::array<double, 3>> sched(full.begin(), full.begin() + passes);
+    std::vector<std::vector<double>> tr(count, std::vector<double>(cols, 0.0));
+    for (int j0 = 0; j0 < cols; j0 += kMaxPanelCols) {
+        const int w = std::min(kMaxPanelCols, cols - j0);
+        PanelSession ps(ctx, k, x0.as<double>() + static_cast<int64_t>(j0) * ld, ld, w, std::max(passes, 1), nullptr,
+                        0.0, false);
+        for (int p = 0; p < passes; ++p) ps.step(sched[p][0], sched[p][1], sched[p][2], 0.0);
+        const int rg = static_cast<int>(gr / ps.rows_per_block());
+        std::vector<double> mu(f.degree + 1);
+        for (int g = 0; g < count; ++g) {
+            PanelResult r;
+            r.passes = passes;
+            r.s = w;
+            r.dots = ps.dots_range(0, passes, g * rg, rg);
+            for (int j = 0; j < w; ++j) {
+                doubled_moments(f, r, j, mu.data());
+                tr[g][j0 + j] = f.combine(mu.data(), 1);
+            }
+        }
+    }
+    for (int g = 0; g < count; ++g) {
+        TraceEst& e = est[g];
+        e.sketch_rank = rank[g];
+        e.queries_used = s_q + rank[g] * cost + s_g * cost;
+        double low = 0.0, res = 0.0;
+        for (int j = 0; j < rank[g]; ++j) low += tr[g][j];
+        for (int j = rmax; j < cols; ++j) res += tr[g][j];
+        e.low_rank_part = low;
+        e.residual_part = s_g > 0 ? res / s_g : 0.0;
+        e.value = e.low_rank_part + e.residual_part;
+    }
+    return est;
+}
+
+// whether estimate() with these parameters runs as a grouped Hutch++ (no per-kernel power iteration,
+// no exact branches, seeded probes)
+bool group_eligible(Context& ctx, const KernelMatrix& k, const EstParams& p) {
+    if (!ctx.feature_groups || k.prec != kF32 || ctx.world() != 1 || p.method == kMethodExact) return false;
+    int ai = 0;
+    if (!integer_alpha(p.alpha, &ai) && !p.has_bounds) return false;
+    try {
+        const Resolved r = resolve(ctx, k, p);
+        const SketchCfg c = sketch_cfg(p, r.s);
+        return c.s_q > 0 && c.s_q < k.n && c.s_g < k.n - c.s_q;
+    } catch (const Error&) {
+        return false;  // the sequential path raises the reference's error
+    }
+}
+
+// estimate() (proj/src/entropy.cpp:201-275) for groups [0, count) of a stack
+std::vector<EntropyEst> estimate_group(Context& ctx, const KernelMatrix& k, int count, const EstParams& p,
+                                       std::vector<std::string>& errors, std::vector<int>& codes) {
+    const Resolved r = resolve(ctx, k, p);
+    const std::vector<TraceEst> tr = hutchpp_group(ctx, k, count, r.f, sketch_cfg(p, r.s), errors, codes);
+    std::vector<EntropyEst> out(count);
+    for (int g = 0; g < count; ++g) {
+        if (!errors[g].empty()) continue;
+        try {
+            out[g] = entropy_of(tr[g], r.alpha, r.method, r.s, r.m_used);
+            out[g].has_bounds = r.has_bounds;
+            out[g].bounds_used = r.bounds;
+        } catch (const Error& e) {
+            errors[g] = e.what();
+            codes[g] = e.code();
+        }
+    }
+    return out;
+}
+
+bool features_finite(Context& ctx, const double* d_x, int64_t n, int64_t d) {
+    ctx.small.ensure(4 * sizeof(unsigned));
+    unsigned* flags = ctx.small.as<unsigned>();
+    cuda_check(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned), ctx.stream()), "memset");
+    launched(ctx, launch_check_samples(d_x, n, static_cast<int>(d), 1, n, flags, ctx.stream()), "check_samples");
+    unsigned hf[2];
+    d2h(ctx, hf, flags, sizeof(hf));
+    ctx.sync();
+    float mx;
+    std::memcpy(&mx, &hf[1], sizeof(float));
+    return hf[0] == 0 && !(mx > 1e18f);
+}
+
+}  // namespace
+
 namespace {
 
 void validate_features(const FeatureData& data, int k) {  // features.cpp:18-26
@@ -2099,6 +2351,42 @@ DevBuf upload_features(Context& ctx, const FeatureData& data) {
     return xs;
 }
 
+// Scores S(F) + S(Y) - S(F∘Y) (StepScorer::score) of candidates `cand` in stacks of up to
+// group_capacity(n): build(stack, g, j) fills group g with candidate j's kernel F; the joints F∘Y are
+// stacked beside them and each term is one grouped estimate. Errors surface for the first failing
+// candidate in order, with the reference's "feature '<name>': " prefix.
+template <typename Build>
+void score_grouped(Context& ctx, const FeatureData& data, const KernelMatrix& label, const StepScorer& scorer,
+                   const std::vector<int>& cand, Build&& build, std::vector<double>& sc, std::vector<double>* elapsed) {
+    const int64_t n = data.n;
+    const int cap = group_capacity(n);
+    EstParams pv = scorer.step, pj = scorer.step;
+    pv.seed = derive_key(scorer.step.seed, hash_name("term:vars"));
+    pj.seed = derive_key(scorer.step.seed, hash_name("term:joint"));
+    for (size_t c0 = 0; c0 < cand.size(); c0 += cap) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const int cnt = static_cast<int>(std::min<size_t>(cap, cand.size() - c0));
+        KernelPtr f = alloc_group(ctx, n, cnt), jk = alloc_group(ctx, n, cnt);
+        for (int g = 0; g < cnt; ++g) {
+            build(*f, g, cand[c0 + g]);
+            group_hadamard(ctx, *jk, g, group_hi(*f, g), group_lo(*f, g), label.hi.as<__half>(), label.lo.as<__half>());
+        }
+        std::vector<std::string> ef(cnt), ej(cnt);
+        std::vector<int> cf(cnt, 0), cj(cnt, 0);
+        const std::vector<EntropyEst> sv = estimate_group(ctx, *f, cnt, pv, ef, cf);
+        const std::vector<EntropyEst> sj = estimate_group(ctx, *jk, cnt, pj, ej, cj);
+        for (int g = 0; g < cnt; ++g) {
+            const int j = cand[c0 + g];
+            if (!ef[g].empty()) fail(cf[g], "feature '" + data.name(j) + "': " + ef[g]);
+            if (!ej[g].empty()) fail(cj[g], "feature '" + data.name(j) + "': " + ej[g]);
+            sc[j] = sv[g].entropy + scorer.label_entropy - sj[g].entropy;
+        }
+        const double per = seconds_since(t0) / cnt;
+        if (elapsed)
+            for (int g = 0; g < cnt; ++g) (*elapsed)[cand[c0 + g]] = per;
+    }
+}
+
 }  // namespace
 
 FeatureRanking rank_features(Context& ctx, const FeatureData& data, double sigma, const EstParams& p, int prec, int k) {
@@ -2110,11 +2398,20 @@ FeatureRanking rank_features(Context& ctx, const FeatureData& data, double sigma
     DevBuf xs = upload_features(ctx, data);
     const StepScorer scorer(ctx, *label, p, derive_key(p.seed, 0));
     std::vector<double> scores(d), elapsed(d);
-    for (int j = 0; j < d; ++j) {
-        const auto t0 = std::chrono::steady_clock::now();
-        KernelPtr f = feature_kernel(ctx, data, xs.as<double>(), sigma, prec, j);
-        scores[j] = scorer.score(*f, data.name(j));
-        elapsed[j] = seconds_since(t0);
+    if (group_eligible(ctx, *label, scorer.step) && features_finite(ctx, xs.as<double>(), data.n, d)) {
+        std::vector<int> cand(d);
+        for (int j = 0; j < d; ++j) cand[j] = j;
+        const double* dx = xs.as<double>();
+        score_grouped(ctx, data, *label, scorer, cand,
+                      [&](const KernelMatrix& st, int g, int j) { group_gram(ctx, st, g, dx + j * data.n, sigma); },
+                      scores, &elapsed);
+    } else {
+        for (int j = 0; j < d; ++j) {
+            const auto t0 = std::chrono::steady_clock::now();
+            KernelPtr f = feature_kernel(ctx, data, xs.as<double>(), sigma, prec, j);
+            scores[j] = scorer.score(*f, data.name(j));
+            elapsed[j] = seconds_since(t0);
+        }
     }
     std::vector<int> order(d);
     for (int j = 0; j < d; ++j) order[j] = j;
@@ -2147,21 +2444,50 @@ FeatureSelection select_features(Context& ctx, const FeatureData& data, double s
     FeatureSelection res;
     std::vector<bool> taken(d, false);
     KernelPtr selected;  // running Hadamard product of the picks
+    const bool grouped = group_eligible(ctx, *label, p);  // every step's estimates as grouped stacks
     for (int step = 0; step < k; ++step) {
         const auto t0 = std::chrono::steady_clock::now();
         const StepScorer scorer(ctx, *label, p, derive_key(p.seed, static_cast<uint64_t>(step)));
         int best = -1;
         double best_score = 0.0;
         KernelPtr best_joint;
-        for (int j = 0; j < d; ++j) {
-            if (taken[j]) continue;
-            KernelPtr cand = step == 0 ? nullptr : hadamard_joint(ctx, *selected, *kernels[j]);
-            const KernelMatrix& cm = step == 0 ? *kernels[j] : *cand;
-            const double sc = scorer.score(cm, data.name(j));
-            if (best < 0 || sc > best_score) {
-                best = j;
-                best_score = sc;
-                best_joint = std::move(cand);
+        if (grouped) {  // candidates' kernels (step 0) or joints with the picks so far, stacked
+            std::vector<int> cand;
+            for (int j = 0; j < d; ++j)
+                if (!taken[j]) cand.push_back(j);
+            std::vector<double> sc(d, 0.0);
+            score_grouped(ctx, data, *label, scorer, cand,
+                          [&](const KernelMatrix& st, int g, int j) {
+                              if (step == 0) {
+                                  const size_t bytes = static_cast<size_t>(data.n) * st.ld * sizeof(__half);
+                                  cuda_check(cudaMemcpyAsync(group_hi(st, g), kernels[j]->hi.as<__half>(), bytes,
+                                                             cudaMemcpyDeviceToDevice, ctx.stream()), "copy kernel");
+                                  cuda_check(cudaMemcpyAsync(group_lo(st, g), kernels[j]->lo.as<__half>(), bytes,
+                                                             cudaMemcpyDeviceToDevice, ctx.stream()), "copy kernel");
+                              } else {
+                                  group_hadamard(ctx, st, g, selected->hi.as<__half>(), selected->lo.as<__half>(),
+                                                 kernels[j]->hi.as<__half>(), kernels[j]->lo.as<__half>());
+                              }
+                          },
+                          sc, nullptr);
+            for (int j : cand) {  // first maximum in column order (features.cpp:140-152)
+                if (best < 0 || sc[j] > best_score) {
+                    best = j;
+                    best_score = sc[j];
+                }
+            }
+            if (step > 0) best_joint = hadamard_joint(ctx, *selected, *kernels[best]);
+        } else {
+            for (int j = 0; j < d; ++j) {
+                if (taken[j]) continue;
+                KernelPtr cand = step == 0 ? nullptr : hadamard_joint(ctx, *selected, *kernels[j]);
+                const KernelMatrix& cm = step == 0 ? *kernels[j] : *cand;
+                const double sc = scorer.score(cm, data.name(j));
+                if (best < 0 || sc > best_score) {
+                    best = j;
+                    best_score = sc;
+                    best_joint = std::move(cand);
+                }
             }
         }
         taken[best] = true;

@@ -147,6 +147,7 @@ public:
     PanelWorkspace ws;         // the panel session's buffers
     PanelWorkspace ws_aux[2];  // the second and third operand of a fused mutual-information pass
     bool fused_mi = true;      // mutual information: one pass over A and B for all three terms
+    bool feature_groups = true;  // feature tools: candidates' estimates as grouped stacks (fp32)
     DevBuf gram_partial, small, probe_err;
     DevBuf x0, work, acc;
 
@@ -180,6 +181,12 @@ struct KernelMatrix {
     int dp = 0;
     int dfeat = 0;  // true feature count (algorithmic flops)
     double c2 = 0.0;  // log2(e)/σ²
+    // grouped stack (feature tools): `groups` n x n kernels of the same n in one allocation, group g in
+    // rows [g·group_rows, g·group_rows + n) (rows past n zero), padded to whole CTA-pair blocks per
+    // pair of a `group_grid`-CTA product so every row block is computed whole by one pair
+    int groups = 1;
+    int64_t group_rows = 0;
+    int group_grid = 0;
 };
 
 using KernelPtr = std::unique_ptr<KernelMatrix>;

@@ -35,6 +35,9 @@ struct SplitPanelView {
     int cols;
     int64_t rpr;  // rows per rank chunk (multiple of 256)
     int world;
+    // grouped stacked matrices (feature tools, single rank): row block r of A belongs to group
+    // r·rows_per_block / group_rows, whose operand rows sit at offset group·group_rows (0: one matrix)
+    int64_t group_rows = 0;
 };
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device, once per (fn, device);
@@ -175,8 +178,9 @@ cudaError_t launch_prepare_split_planes(const PrepArgs<float>& a, cudaStream_t s
 cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream);
 
 // out[p][q][j] = sum_r stats[p][q][r][j] (fixed order)
+// (row blocks [r0, r0 + count) only, count < 0: to the end -- one group of a grouped stack)
 cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks, int s, double* out,
-                                cudaStream_t stream);
+                                cudaStream_t stream, int r0 = 0, int count = -1);
 
 // state (fp32/fp64, [s][ld]) -> fp64 [s][ldo]
 cudaError_t launch_state_to_f64(const void* state, bool is_f32, int64_t rows, int s, int64_t ld, double* out,

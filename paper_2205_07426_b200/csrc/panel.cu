@@ -172,16 +172,17 @@ __global__ void prep_planes_kernel(PrepArgs<float> p) {
     split_store(ldexp(static_cast<double>(p.t0[idx]), e), p.vop, p.vop_lo, idx);
 }
 
-__global__ void reduce_stats_kernel(const double* __restrict__ stats, int passes, int R, int s,
+// out[p][q][j] = sum over row blocks [r0, r0 + count) of stats[p][q][r][j] (R row blocks per (p, q))
+__global__ void reduce_stats_kernel(const double* __restrict__ stats, int passes, int R, int r0, int count, int s,
                                     double* __restrict__ out) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t total = static_cast<int64_t>(passes) * 3 * s;
     if (t >= total) return;
     const int64_t j = t % s;
     const int64_t pq = t / s;  // pass*3 + q
-    const double* src = stats + pq * R * s + j;
+    const double* src = stats + (pq * R + r0) * s + j;
     double acc = 0.0;
-    for (int r = 0; r < R; ++r) acc += src[static_cast<int64_t>(r) * s];
+    for (int r = 0; r < count; ++r) acc += src[static_cast<int64_t>(r) * s];
     out[t] = acc;
 }
 
@@ -379,11 +380,12 @@ cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream) {
 }
 
 cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks, int s, double* out,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int r0, int count) {
     const int64_t total = static_cast<int64_t>(passes) * 3 * s;
     if (total == 0) return cudaSuccess;
+    if (count < 0) count = row_blocks - r0;
     reduce_stats_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, stream>>>(stats, passes, row_blocks,
-                                                                                        s, out);
+                                                                                        r0, count, s, out);
     return cudaGetLastError();
 }
 

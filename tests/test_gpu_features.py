@@ -103,3 +103,44 @@ def test_validation(R):  # test_features.cpp:177-183
 def test_one_hot_labels(R):  # test_features.cpp:185-192
     oh = R.one_hot_labels(["b", "a", "b", "c"])
     assert oh.shape == (4, 3) and np.all(oh.sum(axis=1) == 1.0) and oh[1, 0] == 1.0
+
+
+def test_grouped_candidates_match_sequential_and_timed(R):
+    """fp32 feature scoring as grouped stacks (one block product per pass for all candidates of a
+    step) against the one-candidate-at-a-time loop: same picks, scores within the fp32 contract
+    (1e-4 log n absolute; measured ~1e-6), duplicates bitwise equal inside the stack; the wall times
+    of both are printed (-rP) for profiles/r2_features.md."""
+    import time
+
+    n, d = 3000, 24
+    weights = [0.04 * (j % 9) for j in range(d)]
+    x, labels, names = correlated_dataset(n, 97, weights)
+    x = x.astype(np.float32).astype(np.float64)
+    x[:, 5] = x[:, 4]  # a duplicated feature
+    ctx = R.Context(0)
+    res, walls = {}, {}
+    for params in (dict(alpha=1.5, method="chebyshev", s=40, m=30, seed=4), dict(alpha=2.0, method="int", s=32,
+                                                                               seed=9)):
+        rp = dict(params)
+        if rp["method"] == "chebyshev":
+            rp["bounds"] = R.SpectrumBounds(u=0.0, v=1.0)
+        p = R.EstimatorParams(**rp)
+        for grouped in (False, True, False, True):
+            ctx.set_feature_grouping(grouped)
+            t0 = time.perf_counter()
+            rank = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 8, names, precision="fp32", ctx=ctx)
+            sel = R.select_features(x, labels, R.GaussianKernel(1.0), p, 3, names, precision="fp32", ctx=ctx)
+            walls[(params["method"], grouped)] = time.perf_counter() - t0  # the second (warm) run is kept
+            res[(params["method"], grouped)] = (rank, sel)
+        (r0, s0), (r1, s1) = res[(params["method"], False)], res[(params["method"], True)]
+        atol = 1e-4 * np.log(n)
+        assert r1.columns == r0.columns and s1.columns == s0.columns
+        assert np.allclose(r1.scores, r0.scores, rtol=0, atol=atol)
+        assert np.allclose(s1.objective, s0.objective, rtol=0, atol=atol)
+        if 4 in r1.columns and 5 in r1.columns:
+            i4, i5 = r1.columns.index(4), r1.columns.index(5)
+            assert r1.scores[i4] == r1.scores[i5]
+        print(f"FEATURES {params['method']} n={n} d={d}: rank(k=8)+select(k=3) one at a time "
+              f"{walls[(params['method'], False)]:.3f} s, grouped {walls[(params['method'], True)]:.3f} s, "
+              f"speed-up {walls[(params['method'], False)] / walls[(params['method'], True)]:.2f}x, "
+              f"max score diff {np.max(np.abs(np.array(r1.scores) - np.array(r0.scores))):.2e}")
