@@ -99,7 +99,7 @@ def parse():
     p.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                    help="N > 1: row-shard one estimate over all ranks (NCCL, strong scaling) or run "
                         "independent replicas (weak scaling)")
-    p.add_argument("--slab-rows", type=int, default=32, help="--impl reference: rows per CPU slab sample")
+    p.add_argument("--slab-rows", type=int, default=16, help="--impl reference: rows per CPU slab sample")
     return p.parse_args()
 
 

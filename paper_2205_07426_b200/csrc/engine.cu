@@ -2119,6 +2119,209 @@ void group_hadamard(Context& ctx, const KernelMatrix& out, int g, const __half* 
              "hadamard_split");
 }
 
+// ---- batched small panel algebra for the groups: every step below issues the device work of all
+// groups and synchronises once, instead of once per group (orthonormal_range runs ~12 round trips)
+struct GramJob {
+    const double* x;
+    int p;
+    const double* z;
+    int q;
+};
+// X_iᵀ Z_i (n rows, leading dimension ld) for every job, one device round trip
+std::vector<std::vector<double>> grams_batch(Context& ctx, const std::vector<GramJob>& jobs, int64_t ld, int64_t n) {
+    size_t total = 0;
+    for (const auto& j : jobs) total += static_cast<size_t>(j.p) * j.q;
+    std::vector<std::vector<double>> out(jobs.size());
+    if (total == 0) return out;
+    const int grid = std::min<int64_t>(ctx.sms(), std::max<int64_t>(1, (n + 31) / 32));
+    ctx.small.ensure(total * sizeof(double));
+    size_t off = 0;
+    for (const auto& j : jobs) {
+        const int qb_max = std::max(1, 2048 / std::max(j.p, 1));
+        for (int b0 = 0; b0 < j.q; b0 += qb_max) {
+            const int qb = std::min(qb_max, j.q - b0);
+            ctx.gram_partial.ensure(static_cast<size_t>(grid) * j.p * qb * sizeof(double));
+            launched(ctx,
+                     launch_panel_gram(j.x, j.p, ld, j.z + static_cast<int64_t>(b0) * ld, qb, ld, n,
+                                       ctx.gram_partial.as<double>(), grid,
+                                       ctx.small.as<double>() + off + static_cast<size_t>(b0) * j.p, ctx.stream()),
+                     "panel_gram");
+        }
+        off += static_cast<size_t>(j.p) * j.q;
+    }
+    std::vector<double> all(total);
+    d2h(ctx, all.data(), ctx.small.as<double>(), total * sizeof(double));
+    ctx.sync();
+    off = 0;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        const size_t sz = static_cast<size_t>(jobs[i].p) * jobs[i].q;
+        out[i].assign(all.begin() + off, all.begin() + off + sz);
+        off += sz;
+    }
+    return out;
+}
+
+struct UpdateJob {
+    double beta;
+    const double* g;  // may be null (beta = 0)
+    const double* x;
+    int p;
+    std::vector<double> c;  // p x q column-major
+    int q;
+    double* w;
+};
+// W = beta G + X C for every job (leading dimension ld, n rows): one upload of all C, no round trip
+void updates_batch(Context& ctx, const std::vector<UpdateJob>& jobs, int64_t ld, int64_t n) {
+    size_t total = 0;
+    for (const auto& j : jobs) total += j.c.size();
+    if (total == 0) return;
+    std::vector<double> all;
+    all.reserve(total);
+    for (const auto& j : jobs) all.insert(all.end(), j.c.begin(), j.c.end());
+    DevBuf cd;
+    cd.alloc(total * sizeof(double));
+    h2d(ctx, cd.as<double>(), all.data(), total * sizeof(double));
+    size_t off = 0;
+    for (const auto& j : jobs) {
+        const int qb_max = std::max(1, (48 * 1024 / 8) / std::max(j.p, 1));
+        for (int b0 = 0; b0 < j.q; b0 += qb_max) {
+            const int qb = std::min(qb_max, j.q - b0);
+            launched(ctx,
+                     launch_panel_update(j.beta, j.g ? j.g + static_cast<int64_t>(b0) * ld : nullptr, ld, j.x, j.p, ld,
+                                         cd.as<double>() + off + static_cast<size_t>(b0) * j.p, qb, n,
+                                         j.w + static_cast<int64_t>(b0) * ld, ld, ctx.stream()),
+                     "panel_update");
+        }
+        off += j.c.size();
+    }
+    ctx.sync();  // `all` (host) and cd outlive the copies
+}
+
+// orthonormal_range (above) for a batch of sketches Y_i [p][ld] (n rows each): the same steps and
+// rank rules per sketch, each step issued for every sketch before one synchronisation
+std::vector<int> orthonormal_range_batch(Context& ctx, const std::vector<const double*>& ys, int p, int64_t ld,
+                                         int64_t n, std::vector<DevBuf>& q_out) {
+    const size_t G = ys.size();
+    std::vector<int> rank(G, 0), k(G, 0);
+    std::vector<double> w0(G, 0.0);
+    std::vector<DevBuf> q1(G), qa(G), y2(G);
+    auto scaled_vectors = [&](const std::vector<double>& ww, const std::vector<double>& vv, int cols) {
+        std::vector<double> m(static_cast<size_t>(p) * cols);
+        for (int c = 0; c < cols; ++c) {
+            const double sc = 1.0 / std::sqrt(ww[c]);
+            for (int r = 0; r < p; ++r) m[r + static_cast<size_t>(c) * p] = vv[r + static_cast<size_t>(c) * p] * sc;
+        }
+        return m;
+    };
+    // CholeskyQR (eigen fallback) of X_i (cols_i columns) into out_i, batched
+    auto chol_qr = [&](const std::vector<size_t>& ids, const std::vector<const double*>& xs, const std::vector<int>& cols,
+                       const std::vector<double*>& outs) {
+        std::vector<GramJob> gj;
+        for (size_t t = 0; t < ids.size(); ++t) gj.push_back({xs[t], cols[t], xs[t], cols[t]});
+        std::vector<std::vector<double>> gs = grams_batch(ctx, gj, ld, n);
+        std::vector<UpdateJob> uj;
+        for (size_t t = 0; t < ids.size(); ++t) {
+            std::vector<double> r2;
+            const int c = cols[t];
+            if (cholesky_upper(c, gs[t], r2)) {
+                uj.push_back({0.0, nullptr, xs[t], c, upper_inverse(c, r2), c, outs[t]});
+            } else {
+                std::vector<double> w2, v2;
+                sym_eig_desc(c, gs[t], w2, v2);
+                std::vector<double> m2(static_cast<size_t>(c) * c);
+                for (int cc = 0; cc < c; ++cc)
+                    for (int r = 0; r < c; ++r)
+                        m2[r + static_cast<size_t>(cc) * c] = v2[r + static_cast<size_t>(cc) * c] / std::sqrt(w2[cc]);
+                uj.push_back({0.0, nullptr, xs[t], c, std::move(m2), c, outs[t]});
+            }
+        }
+        updates_batch(ctx, uj, ld, n);
+    };
+    std::vector<GramJob> gj;
+    for (size_t g = 0; g < G; ++g) gj.push_back({ys[g], p, ys[g], p});
+    std::vector<std::vector<double>> gs = grams_batch(ctx, gj, ld, n);
+    std::vector<UpdateJob> uj;
+    std::vector<size_t> live;
+    for (size_t g = 0; g < G; ++g) {
+        std::vector<double> w, v;
+        sym_eig_desc(p, gs[g], w, v);
+        if (!(w.size() > 0 && w[0] > 0.0)) continue;
+        w0[g] = w[0];
+        while (k[g] < p && w[k[g]] > 1e-13 * w0[g]) ++k[g];
+        if (k[g] == 0) continue;
+        q1[g].alloc(static_cast<size_t>(p) * ld * sizeof(double));
+        qa[g].alloc(static_cast<size_t>(p) * ld * sizeof(double));
+        uj.push_back({0.0, nullptr, ys[g], p, scaled_vectors(w, v, k[g]), k[g], q1[g].as<double>()});
+        live.push_back(g);
+    }
+    updates_batch(ctx, uj, ld, n);
+    {
+        std::vector<const double*> xs;
+        std::vector<int> cols;
+        std::vector<double*> outs;
+        for (size_t g : live) xs.push_back(q1[g].as<double>()), cols.push_back(k[g]), outs.push_back(qa[g].as<double>());
+        chol_qr(live, xs, cols, outs);  // second pass: orthogonal to working precision
+    }
+    for (size_t g : live) rank[g] = k[g];
+    // residual pass for sketches that dropped columns: Y2 = Y - Q (Q^T Y); keep sigma(Y2) > 1e-12 sigma_0
+    std::vector<size_t> res;
+    for (size_t g : live)
+        if (k[g] < p) res.push_back(g);
+    if (!res.empty()) {
+        gj.clear();
+        for (size_t g : res) gj.push_back({qa[g].as<double>(), k[g], ys[g], p});
+        gs = grams_batch(ctx, gj, ld, n);
+        uj.clear();
+        for (size_t t = 0; t < res.size(); ++t) {
+            const size_t g = res[t];
+            for (double& x : gs[t]) x = -x;
+            y2[g].alloc(static_cast<size_t>(p) * ld * sizeof(double));
+            uj.push_back({1.0, ys[g], qa[g].as<double>(), k[g], gs[t], p, y2[g].as<double>()});
+        }
+        updates_batch(ctx, uj, ld, n);
+        gj.clear();
+        for (size_t g : res) gj.push_back({y2[g].as<double>(), p, y2[g].as<double>(), p});
+        gs = grams_batch(ctx, gj, ld, n);
+        std::vector<size_t> more;
+        std::vector<int> k2(G, 0);
+        uj.clear();
+        for (size_t t = 0; t < res.size(); ++t) {
+            const size_t g = res[t];
+            std::vector<double> w2, v2;
+            sym_eig_desc(p, gs[t], w2, v2);
+            while (k2[g] < p - k[g] && w2[k2[g]] > 1e-24 * w0[g]) ++k2[g];
+            if (k2[g] == 0) continue;
+            uj.push_back({0.0, nullptr, y2[g].as<double>(), p, scaled_vectors(w2, v2, k2[g]), k2[g], q1[g].as<double>()});
+            more.push_back(g);
+        }
+        updates_batch(ctx, uj, ld, n);
+        if (!more.empty()) {  // re-orthogonalise against the first block, then CholeskyQR
+            gj.clear();
+            for (size_t g : more) gj.push_back({qa[g].as<double>(), k[g], q1[g].as<double>(), k2[g]});
+            gs = grams_batch(ctx, gj, ld, n);
+            uj.clear();
+            for (size_t t = 0; t < more.size(); ++t) {
+                const size_t g = more[t];
+                for (double& x : gs[t]) x = -x;
+                uj.push_back({1.0, q1[g].as<double>(), qa[g].as<double>(), k[g], gs[t], k2[g], y2[g].as<double>()});
+            }
+            updates_batch(ctx, uj, ld, n);
+            std::vector<const double*> xs;
+            std::vector<int> cols;
+            std::vector<double*> outs;
+            for (size_t g : more) {
+                xs.push_back(y2[g].as<double>()), cols.push_back(k2[g]);
+                outs.push_back(qa[g].as<double>() + static_cast<int64_t>(k[g]) * ld);
+            }
+            chol_qr(more, xs, cols, outs);
+            for (size_t g : more) rank[g] += k2[g];
+        }
+    }
+    q_out.resize(G);
+    for (size_t g : live) q_out[g] = std::move(qa[g]);  // [rank][ld] (the buffer holds p columns)
+    return rank;
+}
+
 // Hutch++ (proj/src/hutchpp.cpp:69-115) for groups [0, count) of a stack, seeded probes shared by all
 // (every candidate of a feature-scoring step uses the same term seed). Callers guarantee the
 // non-degenerate branch: 0 < s_q < n and s_g < n - s_q. errors[g] receives a candidate's failure.
@@ -2157,11 +2360,12 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
         run_panel(ctx, k, sk.as<double>() + static_cast<int64_t>(j0) * ld, ld, w, {{1.0, 0.0, 0.0}}, nullptr, nullptr,
                   y.as<double>() + static_cast<int64_t>(j0) * ld, ld);
     }
-    std::vector<DevBuf> q(count);
-    std::vector<int> rank(count, 0);
+    std::vector<DevBuf> q;
+    std::vector<const double*> ys(count);
+    for (int g = 0; g < count; ++g) ys[g] = y.as<double>() + g * gr;
+    const std::vector<int> rank = orthonormal_range_batch(ctx, ys, s_q, ld, n, q);  // per-candidate QR, batched
     int rmax = 0;
-    for (int g = 0; g < count; ++g) {  // the per-candidate QR (s_q columns of n rows)
-        rank[g] = orthonormal_range(ctx, y.as<double>() + g * gr, s_q, ld, n, q[g]);
+    for (int g = 0; g < count; ++g) {
         if (rank[g] == 0 && errors[g].empty()) {
             errors[g] = "hutchpp sketch A*S is numerically zero";
             codes[g] = kRankCollapse;
@@ -2175,6 +2379,8 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
     x0.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
     cuda_check(cudaMemsetAsync(x0.as<void>(), 0, static_cast<size_t>(cols) * ld * sizeof(double), ctx.stream()),
                "memset");
+    std::vector<GramJob> gj;
+    std::vector<int> with_q;
     for (int g = 0; g < count; ++g) {
         double* xg = x0.as<double>() + g * gr;
         double* wg = xg + static_cast<int64_t>(rmax) * ld;
@@ -2183,14 +2389,26 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
             cuda_check(cudaMemcpy2DAsync(xg, ld * sizeof(double), q[g].as<double>(), ld * sizeof(double),
                                          n * sizeof(double), rank[g], cudaMemcpyDeviceToDevice, ctx.stream()),
                        "copy Q");
-            std::vector<double> c = gram_host(ctx, q[g].as<double>(), rank[g], ld, gg, s_g, ld, n);
-            for (double& v : c) v = -v;
-            update(ctx, 1.0, gg, ld, q[g].as<double>(), rank[g], ld, c, s_g, n, wg, ld);
-        } else {
+            if (s_g > 0) {
+                gj.push_back({q[g].as<double>(), rank[g], gg, s_g});
+                with_q.push_back(g);
+            }
+        } else if (s_g > 0) {
             cuda_check(cudaMemcpy2DAsync(wg, ld * sizeof(double), gg, ld * sizeof(double), n * sizeof(double), s_g,
                                          cudaMemcpyDeviceToDevice, ctx.stream()),
                        "copy probes");
         }
+    }
+    {  // W_g = G - Q_g (Q_gᵀ G), batched
+        std::vector<std::vector<double>> cs = grams_batch(ctx, gj, ld, n);
+        std::vector<UpdateJob> uj;
+        for (size_t t = 0; t < with_q.size(); ++t) {
+            const int g = with_q[t];
+            for (double& v : cs[t]) v = -v;
+            uj.push_back({1.0, gp.as<double>() + g * gr, q[g].as<double>(), rank[g], std::move(cs[t]), s_g,
+                          x0.as<double>() + g * gr + static_cast<int64_t>(rmax) * ld});
+        }
+        updates_batch(ctx, uj, ld, n);
     }
     // quadratic forms of every group by moment doubling (panel_traces), dots reduced per group
     const auto full = schedule(f);
