@@ -144,3 +144,29 @@ def test_grouped_candidates_match_sequential_and_timed(R):
               f"{walls[(params['method'], False)]:.3f} s, grouped {walls[(params['method'], True)]:.3f} s, "
               f"speed-up {walls[(params['method'], False)] / walls[(params['method'], True)]:.2f}x, "
               f"max score diff {np.max(np.abs(np.array(r1.scores) - np.array(r0.scores))):.2e}")
+
+
+@pytest.mark.parametrize("n", [120, 513, 1030])
+def test_grouped_path_kats_fp32(R, orc, n):
+    """The reference's feature KATs (test_features.cpp:59-114,160-175) on the grouped fp32 path at
+    ragged sizes (n around the 512-row group granularity): label leak first, duplicated features
+    bitwise tied with the lower index first, k = 1 selection = ranking argmax, fixed seeds identical,
+    and the oracle's scores (1e-4 log n absolute) on identical inputs."""
+    ctx = R.Context(0)
+    ctx.set_feature_grouping(True)
+    p = R.EstimatorParams(alpha=2.0, method="int", s=32, seed=9)
+    x, labels, names = label_leak_dataset(n, 91)
+    x = x.astype(np.float32).astype(np.float64)
+    rank = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 5, names, precision="fp32", ctx=ctx)
+    assert rank.names[0] == "leak"
+    cols, scores = orc.rank_features(x, labels, 1.0, 5, names, alpha=2.0, method="int", s=32, seed=9)
+    assert rank.columns == cols
+    assert np.allclose(rank.scores, scores, rtol=0, atol=1e-4 * np.log(n))
+    x, labels, names = duplicate_dataset(n, 93)
+    x = x.astype(np.float32).astype(np.float64)
+    r1 = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 3, names, precision="fp32", ctx=ctx)
+    assert r1.scores[0] == r1.scores[1] and r1.names[:2] == ["a", "b"]
+    r2 = R.rank_features(x, labels, R.GaussianKernel(1.0), p, 3, names, precision="fp32", ctx=ctx)
+    assert r1.scores == r2.scores
+    sel = R.select_features(x, labels, R.GaussianKernel(1.0), p, 1, names, precision="fp32", ctx=ctx)
+    assert sel.names[0] == r1.names[0] and sel.objective[0] == r1.scores[0]
