@@ -792,12 +792,8 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
     const uint32_t vbox = NPAD / 2;  // each CTA of the pair stages half of every V plane's rows
     // measured on B200: 128-byte L2 promotion + evict_first for the A/B stream beats 256 B / none and
     // evict_normal by 2-4 % (profiles/r1_microbench.md)
-#ifndef RB_TRI_PROMO
-#define RB_TRI_PROMO 1  // A/B maps' L2 promotion: 0 none, 1 128 B, 2 256 B (same-box A/B builds only)
-#endif
-    const CUtensorMapL2promotion promo = RB_TRI_PROMO == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                                        : RB_TRI_PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                                            : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    // (round 2, aligned pitch: 128 B 19.5 ms, none 19.7 ms, 256 B 20.2 ms per config-4 pass, same box)
+    const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     constexpr CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
     bool ok = make_map_f16(&ma[0], a.hi, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
               make_map_f16(&ma[1], a.lo, a.cols, a.rows, a.ld * 2ull, TBK, TBM, promo, swz) &&
