@@ -55,6 +55,7 @@ template <typename PT, typename ST, bool SPLIT, int ER>
 __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     constexpr int NW = ER / 32;
     __shared__ double red[3][NW][kEpiCols];
+    __shared__ float mxs[NW][kEpiCols];
     const int jb0 = blockIdx.y * kEpiCols, jb1 = min(p.s, jb0 + kEpiCols);
     const int r = blockIdx.x;
     const int tid = threadIdx.x;
@@ -76,20 +77,39 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     if (p.partial2) owners(p.k_tiles2, p.total_iters2, p.grid2, p.dp_blocks2, c2_lo, c2_hi);
     const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
 
-    for (int j = jb0; j < jb1; ++j) {
+    // all of this block's loads first (kEpiCols independent columns in flight per thread: the loop
+    // below was latency-bound, one column's loads at a time -- 150 us per config-4 epilogue), then
+    // the arithmetic in the same order as before
+    double ys[kEpiCols];
+    ST tcs[kEpiCols], tps[kEpiCols], x0s[kEpiCols];
+#pragma unroll
+    for (int jj = 0; jj < kEpiCols; ++jj) {
+        const int j = jb0 + jj;
+        ys[jj] = 0.0;
+        tcs[jj] = tps[jj] = x0s[jj] = ST(0);
+        if (j >= jb1) continue;
         double y = 0.0;
         for (int64_t c = c_lo; c <= c_hi; ++c)
             y += static_cast<double>(p.partial[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
         for (int64_t c = c2_lo; c <= c2_hi; ++c)
             y += static_cast<double>(p.partial2[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
-        if (SPLIT) y = ldexp(y * p.unscale, -p.e_cur[j]);
-        double tc = 0.0, tp = 0.0, x0 = 0.0;
+        ys[jj] = y;
         const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
         if (valid) {
-            tc = static_cast<double>(p.t_cur[idx]);
-            if (p.t_prev) tp = static_cast<double>(p.t_prev[idx]);
-            x0 = static_cast<double>(p.x0[idx]);
+            tcs[jj] = p.t_cur[idx];
+            if (p.t_prev) tps[jj] = p.t_prev[idx];
+            x0s[jj] = p.x0[idx];
         }
+    }
+#pragma unroll
+    for (int jj = 0; jj < kEpiCols; ++jj) {
+        const int j = jb0 + jj;
+        if (j >= jb1) break;
+        double y = ys[jj];
+        if (SPLIT) y = ldexp(y * p.unscale, -p.e_cur[j]);
+        const double tc = static_cast<double>(tcs[jj]), tp = static_cast<double>(tps[jj]),
+                     x0 = static_cast<double>(x0s[jj]);
+        const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
         double tn = p.a1 * y + p.a2 * tc + p.a3 * tp;
         const ST tns = static_cast<ST>(tn);
         tn = static_cast<double>(tns);
@@ -112,11 +132,17 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
             red[0][warp][j - jb0] = d1;
             red[1][warp][j - jb0] = d2;
             red[2][warp][j - jb0] = d3;
-            atomicMax(p.cmax_new + j, __float_as_uint(mx));
+            mxs[warp][j - jb0] = mx;
         }
     }
     __syncthreads();
     const int R = gridDim.x, w = jb1 - jb0;
+    if (tid < w) {  // one atomic per column and block (the per-warp atomics contended on s addresses)
+        float m = mxs[0][tid];
+#pragma unroll
+        for (int ww = 1; ww < NW; ++ww) m = fmaxf(m, mxs[ww][tid]);
+        atomicMax(p.cmax_new + jb0 + tid, __float_as_uint(m));
+    }
     for (int t = tid; t < 3 * w; t += blockDim.x) {
         const int q = t / w, jj = t % w;
         double v = red[q][0][jj];
