@@ -547,7 +547,8 @@ cudaError_t launch_mf(const MfMatrixView& a, const SplitPanelView& v, const Stre
     {
         cuuint64_t dims[3] = {static_cast<cuuint64_t>(v.rpr), static_cast<cuuint64_t>(v.cols),
                               static_cast<cuuint64_t>(v.world)};
-        cuuint64_t strides[2] = {static_cast<cuuint64_t>(v.rpr) * 2, static_cast<cuuint64_t>(v.rpr) * v.cols * 2};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(v.rpr) * 2,
+                                 static_cast<cuuint64_t>(v.slice ? v.slice : v.rpr * v.cols) * 2};
         cuuint32_t box[3] = {64, static_cast<cuuint32_t>(C::kNH), 1};
         if (enc(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(v.v), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

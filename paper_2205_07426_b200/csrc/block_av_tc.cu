@@ -312,11 +312,11 @@ bool make_map_f16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
 }
 
 bool make_map_v3(CUtensorMap* m, const void* base, uint64_t rpr, uint64_t cols, uint64_t world, uint32_t box_rows,
-                 uint32_t box_k = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B) {
+                 uint32_t box_k = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B, uint64_t slice = 0) {
     TensorMapEncodeFn enc = tensor_map_encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {rpr, cols, world};
-    cuuint64_t strides[2] = {rpr * 2ull, rpr * cols * 2ull};
+    cuuint64_t strides[2] = {rpr * 2ull, (slice ? slice : rpr * cols) * 2ull};
     cuuint32_t box[3] = {box_k, box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
@@ -338,8 +338,8 @@ cudaError_t launch_tc(const SplitMatrixView& a, const SplitPanelView& v, const S
     constexpr CUtensorMapSwizzle swz_tc = BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     bool ok = make_map_f16(&m_ahi, a.hi, a.cols, a.rows, a.ld * 2ull, BK, BM, promo, swz_tc) &&
               make_map_f16(&m_alo, a.lo, a.cols, a.rows, a.ld * 2ull, BK, BM, promo, swz_tc) &&
-              make_map_v3(&m_v, v.v, v.rpr, v.cols, v.world, vbox, BK, swz_tc) &&
-              make_map_v3(&m_vlo, VSPLIT ? v.vlo : v.v, v.rpr, v.cols, v.world, vbox, BK, swz_tc);
+              make_map_v3(&m_v, v.v, v.rpr, v.cols, v.world, vbox, BK, swz_tc, v.slice) &&
+              make_map_v3(&m_vlo, VSPLIT ? v.vlo : v.v, v.rpr, v.cols, v.world, vbox, BK, swz_tc, v.slice);
     if (v.rpr % BK != 0) return cudaErrorInvalidValue;
     if (!ok) return cudaErrorInvalidValue;
     if (cudaError_t e =
@@ -801,9 +801,9 @@ cudaError_t launch_tri(const SplitMatrixView& a, const SplitMatrixView& b, const
               make_map_f16(&ma[3], b.lo, b.cols, b.rows, b.ld * 2ull, TBK, TBM, promo, swz);
     for (int o = 0; o < 3 && ok; ++o) {
         if (VSPLIT != (v[o].vlo != nullptr) || v[o].rpr % TBK != 0) return cudaErrorInvalidValue;
-        ok = make_map_v3(&mv[2 * o], v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox, TBK, swz) &&
+        ok = make_map_v3(&mv[2 * o], v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox, TBK, swz, v[o].slice) &&
              make_map_v3(&mv[2 * o + 1], VSPLIT ? v[o].vlo : v[o].v, v[o].rpr, v[o].cols, v[o].world, vbox, TBK,
-                         swz);
+                         swz, v[o].slice);
     }
     if (!ok) return cudaErrorInvalidValue;
     if (cudaError_t e =

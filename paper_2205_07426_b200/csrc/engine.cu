@@ -707,7 +707,10 @@ public:
         const size_t st = f32 ? sizeof(float) : sizeof(double);
         for (auto& b : w_.state) b.ensure(static_cast<size_t>(s) * ld_ * st);
         if (f32) {
-            const size_t plane = static_cast<size_t>(k.world) * s * ld_ * sizeof(__half);
+            // rank chunks of the operand planes: s columns of rpr rows, plus (row-sharded) a 512-byte tail
+            // carrying the rank's column maxima of the pass through the same all-gather (gather_planes)
+            slice_elems_ = static_cast<int64_t>(s) * ld_ + (ctx.exchange ? kTailElems : 0);
+            const size_t plane = static_cast<size_t>(k.world) * slice_elems_ * sizeof(__half);
             w_.vhi.ensure(plane);
             // rows past n in the last chunk are never written: keep them zero (A's columns there are
             // TMA-zero, but 0 x garbage could be NaN)
@@ -716,7 +719,7 @@ public:
                 w_.vlo.ensure(plane);
                 cuda_check(cudaMemsetAsync(w_.vlo.as<__half>(), 0, plane, ctx.stream()), "memset");
             }
-            slice_ = static_cast<size_t>(k.rank) * s * ld_;
+            slice_ = static_cast<size_t>(k.rank) * slice_elems_;
         }
         // the matrix-free P·V product takes one fp16 operand plane (P itself is fp16)
         vlo_ = (k.prec == kF32 && split_operand(ctx, vectors_out)) ? w_.vlo.as<__half>() : nullptr;
@@ -755,19 +758,29 @@ public:
     }
 
     // all ranks' operand slices -> full planes (in place), on the comm stream after the epilogue that
-    // wrote this rank's slice; with the column maxima of pass `cmax_pass` (>= 0) all-reduced first (the
-    // next epilogue's plane scale). The next product's own-chunk window runs meanwhile; its other
-    // window waits for these collectives (product()).
+    // wrote this rank's slice. The column maxima of pass `cmax_pass` (>= 0; the next epilogue's plane
+    // scale) ride in the tail of every rank's chunk and are merged after the gather -- no separate
+    // all-reduce. The next product's own-chunk window runs meanwhile; its other window waits for these
+    // (product()).
     void gather_planes(int cmax_pass) {
         NvtxRange nvtx("all-gather operand planes");
         if (!ctx_.exchange || k_.prec == kF64) return;
+        unsigned* cm = cmax_pass >= 0 ? w_.cmax.as<unsigned>() + static_cast<size_t>(cmax_pass) * s_ : nullptr;
+        __half* tail = w_.vhi.as<__half>() + slice_ + static_cast<int64_t>(s_) * ld_;
+        if (cm)
+            cuda_check(cudaMemcpyAsync(tail, cm, static_cast<size_t>(s_) * sizeof(unsigned), cudaMemcpyDeviceToDevice,
+                                       ctx_.stream()),
+                       "column maxima -> chunk tail");
         ctx_.comm_after_main();
         cudaStream_t cs = ctx_.comm_stream();
-        if (cmax_pass >= 0)
-            ctx_.exchange->allreduce_max_u32(w_.cmax.as<unsigned>() + static_cast<size_t>(cmax_pass) * s_, s_, cs);
-        const size_t chunk = static_cast<size_t>(s_) * ld_ * sizeof(__half);
+        const size_t chunk = static_cast<size_t>(slice_elems_) * sizeof(__half);
         ctx_.exchange->allgather_inplace(w_.vhi.as<__half>(), chunk, cs);
         if (vlo_) ctx_.exchange->allgather_inplace(vlo_, chunk, cs);
+        if (cm)
+            launched(ctx_,
+                     launch_merge_tails(w_.vhi.as<__half>(), slice_elems_, static_cast<int64_t>(s_) * ld_, k_.world, s_,
+                                        cm, cs),
+                     "merge_tails");
     }
 
     void step(double a1, double a2, double a3, double acc_coef) {
@@ -782,7 +795,7 @@ public:
     // the operand planes of the next pass, the partial buffers and the plans (fused MI pass); split():
     // two K windows (plan: own operand chunk, plan2: the rest after the all-gather)
     SplitPanelView operand() const {
-        return SplitPanelView{w_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world, k_.group_rows};
+        return SplitPanelView{w_.vhi.as<__half>(), vlo_, k_.n, s_, ld_, k_.world, k_.group_rows, slice_elems_};
     }
     float* partial() const { return w_.partial.as<float>(); }
     float* partial2() const { return w_.partial2.as<float>(); }
@@ -861,8 +874,6 @@ public:
             if (rows_ > 0) launched(ctx_, launch_epilogue_split(e, ctx_.stream()), "epilogue");
             // the last pass of the budget has no successor: no all-gather (its maxima are not read)
             if (ctx_.exchange && k + 1 < max_passes_) gather_planes(k + 1);
-            else if (ctx_.exchange)
-                ctx_.exchange->allreduce_max_u32(w_.cmax.as<unsigned>() + (k + 1) * s, s, ctx_.stream());
         }
         ++k_done_;
     }
@@ -971,6 +982,8 @@ private:
     bool mf_ = false;
     __half* vlo_ = nullptr;
     size_t slice_ = 0;  // this rank's chunk offset in the operand planes
+    int64_t slice_elems_ = 0;  // elements per rank chunk (s·rpr + the column-maxima tail when sharded)
+    static constexpr int64_t kTailElems = 256;  // 512 bytes: up to 128 uint32 column maxima
     StreamKPlan plan_, plan2_;
     bool split_ = false;
 };

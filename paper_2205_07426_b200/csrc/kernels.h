@@ -38,6 +38,9 @@ struct SplitPanelView {
     // grouped stacked matrices (feature tools, single rank): row block r of A belongs to group
     // r·rows_per_block / group_rows, whose operand rows sit at offset group·group_rows (0: one matrix)
     int64_t group_rows = 0;
+    // elements between consecutive ranks' chunks (0: cols·rpr). Row-sharded sessions append a tail per
+    // chunk that carries the rank's column maxima through the same all-gather (engine.cu gather_planes)
+    int64_t slice = 0;
 };
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device, once per (fn, device);
@@ -178,6 +181,10 @@ cudaError_t launch_prepare_split_planes(const PrepArgs<float>& a, cudaStream_t s
 cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream);
 
 // out[p][q][j] = sum_r stats[p][q][r][j] (fixed order)
+// out[j] = max over ranks q of the uint32 tail at planes + q·slice_elems + tail_off (j < s): the
+// column maxima every rank appended to its operand chunk, merged after the all-gather
+cudaError_t launch_merge_tails(const __half* planes, int64_t slice_elems, int64_t tail_off, int world, int s,
+                               unsigned* out, cudaStream_t stream);
 // (row blocks [r0, r0 + count) only, count < 0: to the end -- one group of a grouped stack)
 cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks, int s, double* out,
                                 cudaStream_t stream, int r0 = 0, int count = -1);

@@ -415,6 +415,22 @@ cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks,
     return cudaGetLastError();
 }
 
+__global__ void merge_tails_kernel(const __half* planes, int64_t slice_elems, int64_t tail_off, int world, int s,
+                                   unsigned* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= s) return;
+    unsigned m = 0;
+    for (int q = 0; q < world; ++q)
+        m = max(m, reinterpret_cast<const unsigned*>(planes + q * slice_elems + tail_off)[j]);
+    out[j] = m;
+}
+
+cudaError_t launch_merge_tails(const __half* planes, int64_t slice_elems, int64_t tail_off, int world, int s,
+                               unsigned* out, cudaStream_t stream) {
+    merge_tails_kernel<<<(s + 127) / 128, 128, 0, stream>>>(planes, slice_elems, tail_off, world, s, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_state_to_f64(const void* state, bool is_f32, int64_t rows, int s, int64_t ld, double* out,
                                 int64_t ldo, cudaStream_t stream) {
     dim3 grid(static_cast<unsigned>((rows + 255) / 256), s);

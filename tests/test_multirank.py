@@ -3,8 +3,9 @@
 The device path shards A by rows: rank p owns rows
 [p·rpr, (p+1)·rpr) of A (rpr a multiple of 256), each pass computes its rows of
 A·V in two K windows -- its own operand chunk while the all-gather of the others is in
-flight, then the rest -- all-gathers the next fp16 operand planes laid out [world][s][rpr], max-reduces
-the per-column maxima (so every rank picks the same plane scale) and sum-reduces the
+flight, then the rest -- all-gathers the next fp16 operand planes laid out [world][s][rpr] with
+each rank's per-column maxima in a tail of its chunk (merged after the gather, so every rank picks
+the same plane scale without a separate all-reduce) and sum-reduces the
 row-separable fp64 trace partials once per estimate; CholeskyQR2/projection Grams are
 sum-reduced. These tests run that exact protocol with the fp64 oracle as the compute
 and torch.distributed (gloo) as the transport, and check it against the unsharded
@@ -66,17 +67,22 @@ def _worker(rank, world, port, n, out_path):
     own = np.arange(row0, row0 + rows)
     rest = np.r_[np.arange(row0 + rows, n), np.arange(0, row0)]  # the other chunks, wrapping at n
 
-    def product(local, cols):
-        """A_p · V with the device schedule: the all-gather of V's chunks in flight while the rank's
-        own K window (its own chunk) is multiplied, then the other window once the gather lands."""
-        chunk = torch.zeros((cols, rpr), dtype=torch.float64)
+    def product(local, cols, colmax=None):
+        """A_p · V with the device schedule: the all-gather of V's chunks (each with a tail carrying the
+        rank's column maxima of V) in flight while the rank's own K window (its own chunk) is
+        multiplied, then the other window once the gather lands. Returns (A_p V, max over ranks of
+        the column maxima) -- the maxima need no all-reduce of their own."""
+        chunk = torch.zeros((cols, rpr + 1), dtype=torch.float64)
         chunk[:, :rows] = torch.from_numpy(np.ascontiguousarray(local.T))
+        if colmax is not None:
+            chunk[:, rpr] = torch.from_numpy(np.asarray(colmax, dtype=np.float64))
         planes = [torch.zeros_like(chunk) for _ in range(world)]
         work = dist.all_gather(planes, chunk, async_op=True)
         y = a_p[:, own] @ local  # own window: no remote data needed
         work.wait()
-        full = torch.cat([p for p in planes], dim=1)[:, :n].numpy().T
-        return y + a_p[:, rest] @ full[rest]  # second window, summed after the first (epilogue order)
+        full = torch.cat([p[:, :rpr] for p in planes], dim=1)[:, :n].numpy().T
+        merged = np.max(np.stack([p[:, rpr].numpy() for p in planes]), axis=0)
+        return y + a_p[:, rest] @ full[rest], merged  # second window summed after the first (epilogue order)
 
     def allreduce(arr, op=dist.ReduceOp.SUM):
         t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
@@ -84,7 +90,7 @@ def _worker(rank, world, port, n, out_path):
         return t.numpy()
 
     # sketch pass and CholeskyQR2 with summed Grams
-    Y = product(S, s_q)
+    Y, _ = product(S, s_q)
     g = allreduce(Y.T @ Y)
     w, v = np.linalg.eigh(g)
     keep = w > 1e-13 * w.max()
@@ -97,13 +103,16 @@ def _worker(rank, world, port, n, out_path):
     c, safe_v = orc.spec_coeffs(orc.Spec("chebyshev", alpha, m, 0.0, 1.0))
     scale, center = 2.0 / safe_v, 1.0
     dots = [allreduce(np.einsum("ij,ij->j", X0, X0))]
-    tp, tc = X0, scale * product(X0, X0.shape[1]) - center * X0
-    cmax = allreduce(np.abs(tc).max(axis=0) if rows else np.zeros(X0.shape[1]), dist.ReduceOp.MAX)
+    ax0, _ = product(X0, X0.shape[1])
+    tp, tc = X0, scale * ax0 - center * X0
     local_dots = [np.einsum("ij,ij->j", X0, tc)]
+    colmax = np.abs(tc).max(axis=0) if rows else np.zeros(X0.shape[1])
     for _ in range(2, m + 1):
-        tn = 2 * (scale * product(tc, tc.shape[1]) - center * tc) - tp
+        atc, cmax = product(tc, tc.shape[1], colmax)  # cmax: global maxima of tc, gathered with tc
+        assert np.array_equal(cmax, allreduce(colmax, dist.ReduceOp.MAX))
+        tn = 2 * (scale * atc - center * tc) - tp
         local_dots.append(np.einsum("ij,ij->j", X0, tn))
-        cmax = allreduce(np.abs(tn).max(axis=0), dist.ReduceOp.MAX)
+        colmax = np.abs(tn).max(axis=0)
         tp, tc = tc, tn
     dots += [allreduce(d) for d in local_dots]  # one reduction per estimate in the device path
     tr = 0.5 * c[0] * dots[0] + sum(c[k] * dots[k] for k in range(1, m + 1))
