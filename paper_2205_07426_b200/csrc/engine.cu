@@ -935,15 +935,18 @@ public:
         return out;
     }
 
-    // dots of row blocks [r0, r0 + count) only (one group of a grouped stack; single rank), [p][3][s]
-    std::vector<double> dots_range(int p0, int p1, int r0, int count) {
+    // dots of groups g = 0..groups-1 of a grouped stack (rg row blocks each; single rank), one device
+    // round trip: [g][p][3][s]
+    std::vector<double> dots_groups(int p0, int p1, int groups, int rg) {
         const int np = p1 - p0 + 1;
-        const size_t s = static_cast<size_t>(s_);
-        launched(ctx_,
-                 launch_reduce_stats(w_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
-                                     w_.red.as<double>(), ctx_.stream(), r0, count),
-                 "reduce_stats");
-        std::vector<double> out(static_cast<size_t>(np) * 3 * s);
+        const size_t s = static_cast<size_t>(s_), per = static_cast<size_t>(np) * 3 * s;
+        w_.red.ensure(groups * per * sizeof(double));
+        for (int g = 0; g < groups; ++g)
+            launched(ctx_,
+                     launch_reduce_stats(w_.stats.as<double>() + static_cast<size_t>(p0) * 3 * R_ * s, np, R_, s_,
+                                         w_.red.as<double>() + g * per, ctx_.stream(), g * rg, rg),
+                     "reduce_stats");
+        std::vector<double> out(groups * per);
         d2h(ctx_, out.data(), w_.red.as<double>(), out.size() * sizeof(double));
         ctx_.sync();
         return out;
@@ -2435,11 +2438,13 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
         for (int p = 0; p < passes; ++p) ps.step(sched[p][0], sched[p][1], sched[p][2], 0.0);
         const int rg = static_cast<int>(gr / ps.rows_per_block());
         std::vector<double> mu(f.degree + 1);
+        const std::vector<double> all = ps.dots_groups(0, passes, count, rg);
+        const size_t per = static_cast<size_t>(passes + 1) * 3 * w;
         for (int g = 0; g < count; ++g) {
             PanelResult r;
             r.passes = passes;
             r.s = w;
-            r.dots = ps.dots_range(0, passes, g * rg, rg);
+            r.dots.assign(all.begin() + g * per, all.begin() + (g + 1) * per);
             for (int j = 0; j < w; ++j) {
                 doubled_moments(f, r, j, mu.data());
                 tr[g][j0 + j] = f.combine(mu.data(), 1);
