@@ -49,7 +49,10 @@ __device__ __forceinline__ void split_store(double v, __half* hi, __half* lo, in
     if (lo) lo[idx] = __double2half(v - static_cast<double>(__half2float(h)));
 }
 
-constexpr int kEpiCols = 8;  // columns per epilogue CTA (grid = row blocks x column groups)
+// columns per epilogue CTA (grid = row blocks x column groups). Measured on the config-4 fused MI step
+// (93 epilogues, ncu launch list): 16 columns 29.3 ms, 8: 14.8 ms, 4: 9.0 ms, 2: 8.4 ms -- short CTAs
+// keep more loads in flight per SM than long per-thread column loops
+constexpr int kEpiCols = 2;
 
 template <typename PT, typename ST, bool SPLIT, int ER>
 __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
