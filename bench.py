@@ -523,12 +523,12 @@ def run_ours_c4(args):
     kernel = ("block_av_tri_kernel (fused MI pass: A, B read once, joint n·A∘B formed in TMEM; tcgen05 "
               "cta_group::2, A operands from TMEM)" if fused else "block_av_tc_kernel (tcgen05, fp16 hi/lo A)")
     traffic = ncu_traffic("block_av_tri" if fused else f"block_av_{'fast' if args.operand == 'auto' else args.operand}")
-    cfg = config_dict(args, arm.world, n)
-    cfg.update({"operand": args.operand, "kc": args.kc,
-                "mi_passes": ("fused: the three estimates' passes run in lockstep, each one launch over A and B "
+    cfg = config_dict(args, arm.world, n)  # identical to the reference arm's (same_config)
+    impl = {"operand": args.operand, "kc": args.kc,
+            "mi_passes": ("fused: the three estimates' passes run in lockstep, each one launch over A and B "
                               "(80 GB) with the joint kernel formed on the fly; 31 launches per step" if fused else
                               "separate: 31 passes over each of A, B and the materialised joint (40 GB each); "
-                              "93 launches per step")})
+                              "93 launches per step")}
     line = {
         "metric": C4_METRIC, "value": value, "unit": "estimates/s", "n_gpus": arm.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -538,7 +538,7 @@ def run_ours_c4(args):
                           "auto": "fp16 hi (2 products) on the trace passes, hi+lo on the Hutch++ sketch"}[args.operand]
                        + "; fp32 TMEM accumulate drained in chunks; fp32 recurrence state; fp64 trace partials"),
         "data": "synthetic: X~N(0,1) 100000x16, W~N(0,1) 16x8, Y=XW+0.5N(0,1), reference RNG, fp32-rounded",
-        "config": cfg,
+        "config": cfg, "impl_config": impl,
         "roofline": roofline_of(prof, ms, "hbm", kernel, traffic),
         "roofline_single_matrix_product": single,
         "cpu_baseline": None if (arm.world > 1 or args.no_cpu_baseline) else cpu_baseline_line(args, n, 3.0),

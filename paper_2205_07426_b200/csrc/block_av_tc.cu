@@ -388,6 +388,9 @@ constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 #ifndef RB_TRI_AB_STAGES
 #define RB_TRI_AB_STAGES 2
 #endif
+#ifndef RB_TRI_PREFETCH
+#define RB_TRI_PREFETCH 0  // A/B k tiles prefetched into L2 ahead of the TMA ring (0: off)
+#endif
 #ifndef RB_TRI_SETMAXNREG
 #define RB_TRI_SETMAXNREG 1
 #endif
@@ -567,6 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (lane == 0) {
             const uint64_t pol_stream = args.a_policy ? policy_evict_normal() : policy_evict_first();
             const uint64_t pol_keep = policy_evict_last();
+            const uint64_t pol_pref = policy_evict_normal();
             const CUtensorMap* vmap[3][2] = {{&map_va, &map_valo}, {&map_vb, &map_vblo}, {&map_vj, &map_vjlo}};
             int as = 0, vs = 0;
             uint32_t aph = 0, vph = 0;
@@ -585,6 +589,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], kg * TBK, r * TBM, pol_stream);
                         tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], kg * TBK, r * TBM, pol_stream);
                         tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], kg * TBK, r * TBM, pol_stream);
+                        if (RB_TRI_PREFETCH > 0 && k + RB_TRI_PREFETCH < k1) {
+                            int kp = kg + RB_TRI_PREFETCH;
+                            if (kp >= args.k_total) kp -= args.k_total;
+                            tma_prefetch_2d(&map_ahi, kp * TBK, r * TBM, pol_pref);
+                            tma_prefetch_2d(&map_alo, kp * TBK, r * TBM, pol_pref);
+                            tma_prefetch_2d(&map_bhi, kp * TBK, r * TBM, pol_pref);
+                            tma_prefetch_2d(&map_blo, kp * TBK, r * TBM, pol_pref);
+                        }
                         if (++as == C::kABStages) as = 0, aph ^= 1u;
                     } else {
                         mbar_wait(&v_empty[vs], vph ^ 1u);
@@ -701,17 +713,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
 #pragma unroll
                     for (int t = 0; t < 8; ++t)
                         joint_pair(pa_h[t], pa_l[t], pb_h[t], pb_l[t], args.scale_a, args.scale_b, jh[t], jl[t]);
-                    const int64_t e = grow - static_cast<int64_t>(kg) * TBK - 16 * g;  // J_ii = 1/n (kernel.cpp:98-99)
-                    if (e >= 0 && e < 16) {
-                        const int q = static_cast<int>(e);
-                        const uint32_t mask = (q & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+                    // J_ii = 1/n (kernel.cpp:98-99). Branch-free per-register selects: a conditional write to
+                    // jh[e / 2] is compiled into a dynamically indexed local-memory array (spilled to the stack
+                    // every K group: ~40 GB of local stores per config-4 launch, round-2 ncu)
+                    const int64_t e = grow - static_cast<int64_t>(kg) * TBK - 16 * g;
+                    const int qd = (e >= 0 && e < 16) ? static_cast<int>(e) : -2;
+                    const uint32_t dmask = (qd & 1) ? 0xFFFF0000u : 0x0000FFFFu;
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) {
-                            if (t == q / 2) {
-                                jh[t] = (jh[t] & ~mask) | (dh & mask);
-                                jl[t] &= ~mask;
-                            }
-                        }
+                    for (int t = 0; t < 8; ++t) {
+                        const uint32_t sel = (t == (qd >> 1)) ? dmask : 0u;
+                        jh[t] = (jh[t] & ~sel) | (dh & sel);
+                        jl[t] &= ~sel;
                     }
                     const uint32_t q = (TBK / 16) * u + g, slot = q % C::kSlots;
                     mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot

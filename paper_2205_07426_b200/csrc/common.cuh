@@ -95,6 +95,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// L2 prefetch of one tensor tile (no shared-memory destination): warms L2 ahead of the TMA load
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y, uint64_t policy) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile.L2::cache_hint [%0, {%1, %2}], %3;" ::"l"(map),
+                 "r"(x), "r"(y), "l"(policy)
+                 : "memory");
+}
+
 // multicast to every CTA in cta_mask (same smem offset, same mbarrier offset)
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
                                                uint16_t cta_mask, uint64_t policy) {
