@@ -483,6 +483,13 @@ __device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
+// a·b − c with the negation folded into the FMA's operand modifier (no separate sign-flip instruction)
+__device__ __forceinline__ uint32_t hfma2_negc(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("{\n\t.reg .b32 nc;\n\tneg.f16x2 nc, %3;\n\tfma.rn.f16x2 %0, %1, %2, nc;\n\t}" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 // 2 entries of J from packed (hi, lo) fp16 pairs of A and B, as a (hi, lo) fp16 split, in packed
 // half2 arithmetic: with a = a_h + a_l and b = b_h + b_l prescaled by exact powers of two,
 //   j_h = fl16(a_h b_h),  r = a_h b_h - j_h (exact: an 11x11-bit product minus its rounding),
@@ -492,7 +499,7 @@ __device__ __forceinline__ void joint_pair(uint32_t ah, uint32_t al, uint32_t bh
                                            uint32_t sb, uint32_t& jh, uint32_t& jl) {
     ah = hmul2(ah, sa), al = hmul2(al, sa), bh = hmul2(bh, sb), bl = hmul2(bl, sb);
     jh = hmul2(ah, bh);
-    const uint32_t r = hfma2(ah, bh, jh ^ 0x80008000u);
+    const uint32_t r = hfma2_negc(ah, bh, jh);
     jl = hfma2(ah, bl, hfma2(al, bh, r));
 }
 
@@ -686,6 +693,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         int k0, k1;
         while (sg.next(rp, k0, k1)) {
             const int64_t grow = args.row0 + (2 * rp + rank) * TBM + row;  // global row (J diagonal)
+            const int64_t wrow = grow - lane;                                  // the warp's first row
             for (int k = k0; k < k1; ++k, ++u) {
                 const int kg = k + args.k_off < args.k_total ? k + args.k_off : k + args.k_off - args.k_total;
                 mbar_wait(&ab_full[as], aph);
@@ -716,14 +724,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                     // J_ii = 1/n (kernel.cpp:98-99). Branch-free per-register selects: a conditional write to
                     // jh[e / 2] is compiled into a dynamically indexed local-memory array (spilled to the stack
                     // every K group: ~40 GB of local stores per config-4 launch, round-2 ncu)
-                    const int64_t e = grow - static_cast<int64_t>(kg) * TBK - 16 * g;
-                    const int qd = (e >= 0 && e < 16) ? static_cast<int>(e) : -2;
-                    const uint32_t dmask = (qd & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+                    // Only the few K groups whose 16 columns meet this warp's 32 rows take the branch
+                    // (warp-uniform test: rows [wrow, wrow + 32) vs columns [c0, c0 + 16)).
+                    const int64_t c0 = static_cast<int64_t>(kg) * TBK + 16 * g;
+                    if (wrow < c0 + 16 && c0 < wrow + 32) {
+                        const int64_t e = grow - c0;
+                        const int qd = (e >= 0 && e < 16) ? static_cast<int>(e) : -2;
+                        const uint32_t dmask = (qd & 1) ? 0xFFFF0000u : 0x0000FFFFu;
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        const uint32_t sel = (t == (qd >> 1)) ? dmask : 0u;
-                        jh[t] = (jh[t] & ~sel) | (dh & sel);
-                        jl[t] &= ~sel;
+                        for (int t = 0; t < 8; ++t) {
+                            const uint32_t sel = (t == (qd >> 1)) ? dmask : 0u;
+                            jh[t] = (jh[t] & ~sel) | (dh & sel);
+                            jl[t] &= ~sel;
+                        }
                     }
                     const uint32_t q = (TBK / 16) * u + g, slot = q % C::kSlots;
                     mbar_wait(&op_empty[slot], ((q / C::kSlots) & 1u) ^ 1u);  // earlier MMAs are done with the slot
