@@ -143,6 +143,7 @@ def lib():
         h.oracle_csv_free.argtypes = [C.c_void_p]
         h.oracle_threads.restype = C.c_int
         h.oracle_set_threads.argtypes = [C.c_int]
+        h.oracle_set_merge_panels.argtypes = [C.c_int]
         _lib = h
     return _lib
 
@@ -603,3 +604,130 @@ def blocks_mutual_information(x, sigma_x, y, sigma_y, block=4096, **params):
                                                                       **params)
     return dict(value=tv["entropy"] + tt["entropy"] - tj["entropy"], vars_entropy=tv["entropy"],
                 target_entropy=tt["entropy"], joint_entropy=tj["entropy"], terms=dict(vars=tv, target=tt, joint=tj))
+
+
+def set_merge_panels(on: bool):
+    """Hutch++ applies f(A) to [Q, W - Q(Q^T W)] in one apply_panel instead of two (the same
+    per-column recurrences, half the operator passes). Off by default (the reference's
+    structure); on only for the one-off full-size fixtures."""
+    lib().oracle_set_merge_panels(1 if on else 0)
+
+
+class _Lockstep:
+    """Runs several callback estimators in threads whose operator calls are served together:
+    each call posts its panel and waits until every active estimator has posted one, then one
+    sweep over the kernel blocks serves all of them (shared block evaluations)."""
+
+    def __init__(self, serve):
+        import threading
+
+        self.serve = serve  # serve({term: v}) -> {term: y}
+        self.cv = threading.Condition()
+        self.active = set()
+        self.pending = {}
+        self.results = {}
+        self.gen = 0
+        self.error = None
+
+    def _run_if_ready(self):
+        if self.pending and set(self.pending) >= self.active:
+            reqs, self.pending = self.pending, {}
+            try:
+                self.results = self.serve(reqs)
+            except Exception as e:  # surfaced to every waiting estimator
+                self.error = e
+                self.results = {}
+            self.gen += 1
+            self.cv.notify_all()
+
+    def fn(self, term):
+        def cb(n, c, x, out):
+            try:
+                v = np.ascontiguousarray(np.ctypeslib.as_array(x, shape=(c, n)).T)
+                with self.cv:
+                    self.pending[term] = v
+                    g = self.gen
+                    self._run_if_ready()
+                    while self.gen == g:
+                        self.cv.wait()
+                    if self.error is not None:
+                        return 1
+                    y = self.results.pop(term)
+                np.ctypeslib.as_array(out, shape=(c, n))[...] = y.T
+                return 0
+            except Exception:
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        return MUL_FN(cb)
+
+    def run(self, n, jobs):
+        """jobs: {term: params dict} -> {term: estimate dict}"""
+        import threading
+
+        out, errs, fns = {}, {}, {t: self.fn(t) for t in jobs}
+        self.active = set(jobs)
+
+        def work(term):
+            try:
+                p = _params(**jobs[term])
+                o = COut()
+                _chk(lib().oracle_cb_estimate(n, fns[term], C.byref(p), C.byref(o)))
+                out[term] = _out(o)
+            except Exception as e:
+                errs[term] = e
+            finally:
+                with self.cv:
+                    self.active.discard(term)
+                    self._run_if_ready()
+
+        ths = [threading.Thread(target=work, args=(t,)) for t in jobs]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        if errs:
+            raise next(iter(errs.values()))
+        return out
+
+
+def lockstep_mutual_information(x, sigma_x, y, sigma_y, block=4096, **params):
+    """measures.cpp:36-46 (per-term seeds) like blocks_mutual_information, with the three terms'
+    operator passes served together: one evaluation of the A and B blocks per sweep gives the
+    vars, target and joint (n·A∘B, hadamard_scaled's scale·(a·b)) blocks. Same estimator, same
+    blocks as KernelBlocksOp; only the scheduling differs."""
+    seed = params.pop("seed", 0)
+    ox = KernelBlocksOp(x, sigma_x, block=block)
+    oy = KernelBlocksOp(y, sigma_y, block=block)
+    n = ox.n
+    scale = float(n)
+
+    def serve(reqs):
+        ys = {t: np.zeros_like(v) for t, v in reqs.items()}
+        for i0 in range(0, n, block):
+            i1 = min(n, i0 + block)
+            for j0 in range(i0, n, block):
+                j1 = min(n, j0 + block)
+                ka = ox.kernel_block(i0, i1, j0, j1) if ("vars" in reqs or "joint" in reqs) else None
+                kb = oy.kernel_block(i0, i1, j0, j1) if ("target" in reqs or "joint" in reqs) else None
+                blocks = {"vars": ka, "target": kb}
+                if "joint" in reqs:
+                    kj = scale * (ka * kb)
+                    if i0 == j0:
+                        np.fill_diagonal(kj, 1.0 / n)
+                    blocks["joint"] = kj
+                for t, v in reqs.items():
+                    k = blocks[t]
+                    ys[t][i0:i1] += k @ v[j0:j1]
+                    if j0 != i0:
+                        ys[t][j0:j1] += k.T @ v[i0:i1]
+        return ys
+
+    terms = {"vars": "term:vars", "target": "term:target", "joint": "term:joint"}
+    jobs = {t: dict(params, seed=derive_key(seed, hash_name(lbl))) for t, lbl in terms.items()}
+    est = _Lockstep(serve).run(n, jobs)
+    tv, tt, tj = est["vars"], est["target"], est["joint"]
+    return dict(value=tv["entropy"] + tt["entropy"] - tj["entropy"], vars_entropy=tv["entropy"],
+                target_entropy=tt["entropy"], joint_entropy=tj["entropy"], terms=est)

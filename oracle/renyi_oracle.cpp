@@ -838,6 +838,10 @@ void sub_mul(Mat& w, const Mat& q, const Mat& c) {  // w -= q c
         }
 }
 
+// Off by default (the reference's structure: Q and W through separate apply_panel calls,
+// hutchpp.cpp:109-113); oracle_set_merge_panels(1) batches them for the full-size fixtures.
+inline bool g_merge_panels = false;
+
 double projected_trace(const Spec& f, const Op& a, const Mat& q) {  // hutchpp.cpp:33-39
     if (q.c == 0) return 0.0;
     return col_dot_sum(q, apply_panel(f, a, q));
@@ -900,9 +904,26 @@ Trace hutchpp(const Spec& f, const Op& a, int s_q, int s_g, uint64_t seed, int k
         }
         q = householder_q(qr, qr.rank);
     }
-    est.low = projected_trace(f, a, q);
     const Mat w = G ? *G : probe_panel(n, s_g, seed, "hutchpp-probe", kind);
-    est.residual = s_g > 0 ? residual_probe_trace(f, a, q, w) : 0.0;
+    if (g_merge_panels && q.c > 0 && s_g > 0) {
+        // one apply_panel over [Q, W - Q(Q^T W)]: the same per-column recurrences as the two
+        // separate calls below, in half the operator passes (fixture generation only)
+        Mat wp = w;
+        sub_mul(wp, q, mul_t(q, wp));
+        Mat both(n, q.c + wp.c);
+        std::copy(q.d.begin(), q.d.end(), both.d.begin());
+        std::copy(wp.d.begin(), wp.d.end(), both.d.begin() + n * q.c);
+        const Mat fb = apply_panel(f, a, both);
+        Mat fq(n, q.c), fw(n, wp.c);
+        std::copy(fb.d.begin(), fb.d.begin() + n * q.c, fq.d.begin());
+        std::copy(fb.d.begin() + n * q.c, fb.d.end(), fw.d.begin());
+        est.low = col_dot_sum(q, fq);
+        sub_mul(fw, q, mul_t(q, fw));
+        est.residual = col_dot_sum(wp, fw) / static_cast<double>(s_g);
+    } else {
+        est.low = projected_trace(f, a, q);
+        est.residual = s_g > 0 ? residual_probe_trace(f, a, q, w) : 0.0;
+    }
     est.queries += s_g * cost;
     est.value = est.low + est.residual;
     return est;
@@ -1531,6 +1552,7 @@ int oracle_threads() {
     return 1;
 #endif
 }
+void oracle_set_merge_panels(int on) { orc::g_merge_panels = on != 0; }
 void oracle_set_threads(int t) {
 #ifdef _OPENMP
     if (t > 0) omp_set_num_threads(t);
@@ -1788,21 +1810,35 @@ int oracle_kernel_block(const double* dot, int64_t bi, int64_t bj, const double*
 int oracle_kernel_block_rows(const double* xi, const double* xjt, int64_t bi, int64_t bj, int64_t d,
                              const double* sq_i, const double* sq_j, double inv2, double inv_n, double scale,
                              int combine, double* out) {
+    // 32-column chunks keep the partial dots in registers; each entry still sums its d products
+    // in feature order (bitwise the same dots as one full-row pass)
+    constexpr int64_t CH = 32;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < bi; ++i) {
         double* o = out + i * bj;
-        std::vector<double> dot(static_cast<size_t>(bj), 0.0);
-        for (int64_t t = 0; t < d; ++t) {
-            const double a = xi[i * d + t];
-            const double* xr = xjt + t * bj;
-            for (int64_t j = 0; j < bj; ++j) dot[j] += a * xr[j];
-        }
         const double si = sq_i[i];
-        for (int64_t j = 0; j < bj; ++j) {
-            double d2 = si + sq_j[j] - 2.0 * dot[j];
-            d2 = d2 < 0.0 ? 0.0 : d2;
-            const double v = inv_n * orc::exp_nonpos(-d2 * inv2);
-            o[j] = combine ? scale * (o[j] * v) : v;
+        for (int64_t j0 = 0; j0 < bj; j0 += CH) {
+            const int64_t len = std::min<int64_t>(CH, bj - j0);
+            double dot[CH] = {};
+            if (len == CH) {
+                for (int64_t t = 0; t < d; ++t) {
+                    const double a = xi[i * d + t];
+                    const double* xr = xjt + t * bj + j0;
+                    for (int64_t j = 0; j < CH; ++j) dot[j] += a * xr[j];
+                }
+            } else {
+                for (int64_t t = 0; t < d; ++t) {
+                    const double a = xi[i * d + t];
+                    const double* xr = xjt + t * bj + j0;
+                    for (int64_t j = 0; j < len; ++j) dot[j] += a * xr[j];
+                }
+            }
+            for (int64_t j = 0; j < len; ++j) {
+                double d2 = si + sq_j[j0 + j] - 2.0 * dot[j];
+                d2 = d2 < 0.0 ? 0.0 : d2;
+                const double v = inv_n * orc::exp_nonpos(-d2 * inv2);
+                o[j0 + j] = combine ? scale * (o[j0 + j] * v) : v;
+            }
         }
     }
     return 0;

@@ -94,11 +94,18 @@ def c4():
     sx, sy = 4.0, math.sqrt(8.0)
     params = dict(alpha=1.01, method="chebyshev", s=90, m=60, bounds=(0.0, 1.0), probe_kind="gaussian")
     t = time.time()
-    mi = O.blocks_mutual_information(x, sx, y, sy, seed=SEED, **params)
+    # the three terms' passes served together (one A/B block evaluation per sweep) and Hutch++'s
+    # Q and W panels through one apply_panel: the same estimator and blocks as
+    # blocks_mutual_information up to BLAS summation order (1e-14, tests/test_oracle_fullsize.py)
+    O.set_merge_panels(True)
+    try:
+        mi = O.lockstep_mutual_information(x, sx, y, sy, seed=SEED, **params)
+    finally:
+        O.set_merge_panels(False)
     terms = {k: _est(v) for k, v in mi.pop("terms").items()}
     return dict(n=n, dx=16, dy=8, sigma_x=sx, sigma_y=sy, seed=SEED,
                 inputs="X, Y = f32(mi_inputs(n, seed)) (Y = X W + 0.5 noise)", precision="fp32",
-                params=dict(params, seed=SEED), mi=mi, terms=terms, oracle="matrix-free blocks",
+                params=dict(params, seed=SEED), mi=mi, terms=terms, oracle="matrix-free blocks, three terms in lockstep, Q and W merged",
                 seconds=time.time() - t)
 
 

@@ -77,6 +77,22 @@ def test_matrix_free_mutual_information(data):
         assert got[key] == pytest.approx(ref[key], rel=1e-10, abs=1e-12)
 
 
+def test_lockstep_mutual_information(data):
+    """The config-4 fixture's scheduling (three terms served by one block sweep, Hutch++'s Q and W
+    through one apply_panel) changes only BLAS summation order (wider panels)."""
+    x, y, a, b, j = data
+    kw = dict(alpha=1.01, method="chebyshev", s=40, m=30, seed=11, bounds=(0.0, 1.0))
+    ref = O.blocks_mutual_information(x, 2.0, y, 1.5, block=256, **dict(kw))
+    O.set_merge_panels(True)
+    try:
+        got = O.lockstep_mutual_information(x, 2.0, y, 1.5, block=256, **dict(kw))
+    finally:
+        O.set_merge_panels(False)
+    for key in ("value", "vars_entropy", "target_entropy", "joint_entropy"):
+        assert got[key] == pytest.approx(ref[key], rel=1e-12)
+    assert got["terms"]["joint"]["queries_used"] == ref["terms"]["joint"]["queries_used"]
+
+
 def test_matrix_free_probe_traces(data):
     x, y, a, b, j = data
     spec = O.Spec("chebyshev", 1.5, 25, 0.0, 1.0)
