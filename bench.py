@@ -100,6 +100,9 @@ def parse():
                    help="N > 1: row-shard one estimate over all ranks (NCCL, strong scaling) or run "
                         "independent replicas (weak scaling)")
     p.add_argument("--slab-rows", type=int, default=16, help="--impl reference: rows per CPU slab sample")
+    p.add_argument("--probes", default="device", choices=["device", "host"],
+                   help="seeded Gaussian probes: drawn on the device (CUDA log/sin/cos) or on the host with the "
+                        "reference's arithmetic (bitwise the reference's probes)")
     return p.parse_args()
 
 
@@ -371,6 +374,7 @@ class Arm:
         self.args = args
         self.sharded = self.world > 1 and args.mode == "sharded"
         self.ctx = R.Context(self.local)
+        self.ctx.set_probe_source(args.probes)
         if self.sharded:
             uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
             if self.rank == 0:
@@ -525,6 +529,9 @@ def run_ours_c4(args):
     traffic = ncu_traffic("block_av_tri" if fused else f"block_av_{'fast' if args.operand == 'auto' else args.operand}")
     cfg = config_dict(args, arm.world, n)  # identical to the reference arm's (same_config)
     impl = {"operand": args.operand, "kc": args.kc,
+            "probes": ("host: the reference's Gaussian draws bitwise, generated on the host threads while the "
+                       "device builds A and B" if args.probes == "host" else
+                       "device: the reference's substreams drawn with CUDA log/sin/cos (<= 2 ulp per draw)"),
             "mi_passes": ("fused: the three estimates' passes run in lockstep, each one launch over A and B "
                               "(80 GB) with the joint kernel formed on the fly; 31 launches per step" if fused else
                               "separate: 31 passes over each of A, B and the materialised joint (40 GB each); "

@@ -159,6 +159,14 @@ int renyi_ctx_set_fused_mi(renyi_ctx* ctx, int on);
  * grouped stacks (one block product per pass for up to 64 candidates' kernels); 0: one
  * candidate at a time, as the reference's loop (proj/src/features.cpp:95-162) */
 int renyi_ctx_set_feature_grouping(renyi_ctx* ctx, int on);
+/* seeded Gaussian probes (detail::gaussian_panel, proj/src/hutchpp.cpp:13-22): RENYI_PROBES_DEVICE
+ * (default) draws them on the device from the reference's substreams with CUDA's log/sin/cos (<= 2 ulp
+ * per draw from glibc's); RENYI_PROBES_HOST draws them with the reference's own arithmetic on the host
+ * threads (bitwise the reference's probes) and copies them; mutual information requests its panels
+ * before the kernel builds so the host work overlaps them. Rademacher probes are exact either way. */
+#define RENYI_PROBES_DEVICE 0
+#define RENYI_PROBES_HOST 1
+int renyi_ctx_set_probe_source(renyi_ctx* ctx, int source);
 /* matrix-free product: j-blocks (of 128 samples) accumulated in TMEM before each fp32 drain */
 int renyi_ctx_set_matrix_free_chunk(renyi_ctx* ctx, int jblocks);
 int renyi_ctx_sync(renyi_ctx* ctx);

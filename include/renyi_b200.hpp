@@ -77,6 +77,8 @@ public:
         h_.reset(c);
     }
     renyi_ctx* get() const { return h_.get(); }
+    // RENYI_PROBES_DEVICE (default) or RENYI_PROBES_HOST (bitwise the reference's Gaussian probes)
+    void set_probe_source(int source) const { check(renyi_ctx_set_probe_source(get(), source)); }
 
 private:
     struct Del {

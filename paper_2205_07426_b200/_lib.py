@@ -163,6 +163,7 @@ SIGNATURES = {
     "renyi_ctx_set_operand_mode": (C.c_int, [_P, C.c_int]),
     "renyi_ctx_set_fused_mi": (C.c_int, [_P, C.c_int]),
     "renyi_ctx_set_feature_grouping": (C.c_int, [_P, C.c_int]),
+    "renyi_ctx_set_probe_source": (C.c_int, [_P, C.c_int]),
     "renyi_ctx_set_matrix_free_chunk": (C.c_int, [_P, C.c_int]),
     "renyi_ctx_sync": (C.c_int, [_P]),
     "renyi_release_cached_memory": (C.c_int, []),

@@ -76,6 +76,16 @@ class Context:
         stacks (default) or one at a time (the reference's loop)."""
         check(L.lib().renyi_ctx_set_feature_grouping(self._h, 1 if on else 0))
 
+    def set_probe_source(self, source: str = "device") -> None:
+        """Seeded Gaussian probes: "device" (default; CUDA log/sin/cos, <= 2 ulp per draw from the
+        reference's glibc draws) or "host" (the reference's own arithmetic on the host threads: bitwise
+        the reference's probes, copied to the device; overlapped with the kernel builds for mutual
+        information)."""
+        codes = {"device": 0, "host": 1}
+        if source not in codes:
+            raise ValueError(f"probe source must be one of {sorted(codes)}")
+        check(L.lib().renyi_ctx_set_probe_source(self._h, codes[source]))
+
     def sync(self) -> None:
         check(L.lib().renyi_ctx_sync(self._h))
 

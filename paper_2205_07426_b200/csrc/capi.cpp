@@ -247,6 +247,15 @@ int renyi_ctx_set_fused_mi(renyi_ctx* ctx, int on) {
     });
 }
 
+int renyi_ctx_set_probe_source(renyi_ctx* ctx, int source) {
+    return guarded([&] {
+        need(ctx, "ctx");
+        if (source != RENYI_PROBES_DEVICE && source != RENYI_PROBES_HOST)
+            rb::fail(rb::kInvalidArgument, "probe source must be RENYI_PROBES_DEVICE or RENYI_PROBES_HOST");
+        ctx->ctx.probe_source = source;
+    });
+}
+
 int renyi_ctx_set_feature_grouping(renyi_ctx* ctx, int on) {
     return guarded([&] {
         need(ctx, "ctx");

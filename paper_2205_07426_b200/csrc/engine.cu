@@ -321,6 +321,76 @@ Context::~Context() {
     if (stream_) cudaStreamDestroy(stream_);
 }
 
+namespace {
+std::string probe_key(int64_t n, int cols, uint64_t seed, const char* label, int kind) {
+    return std::to_string(n) + "/" + std::to_string(cols) + "/" + std::to_string(seed) + "/" + label + "/" +
+           std::to_string(kind);
+}
+}  // namespace
+
+void Context::prefetch_probes(const std::vector<ProbeReq>& reqs) {
+    if (probe_source != 1) return;
+    if (probe_job_.valid()) probe_job_.wait();  // one batch at a time
+    struct Job {
+        std::vector<ProbeReq> reqs;
+        std::vector<uint64_t> base;
+        std::vector<Panel> panels;
+        std::vector<std::promise<Panel>> done;
+        std::unique_ptr<std::atomic<int>[]> left;
+        std::vector<std::pair<int, int>> tasks;  // (panel, column), in request order
+    };
+    auto job = std::make_shared<Job>();
+    for (const ProbeReq& r : reqs) {
+        const std::string key = probe_key(r.n, r.cols, r.seed, r.label.c_str(), r.kind);
+        if (r.kind != kProbeGaussian || r.cols <= 0 || probe_prefetch_.count(key)) continue;
+        const int p = static_cast<int>(job->reqs.size());
+        job->reqs.push_back(r);
+        job->base.push_back(derive_key(r.seed, hash_name(r.label.c_str())));
+        job->panels.push_back(std::make_shared<std::vector<double>>(static_cast<size_t>(r.n) * r.cols));
+        job->done.emplace_back();
+        probe_prefetch_.emplace(key, job->done.back().get_future().share());
+        for (int j = 0; j < r.cols; ++j) job->tasks.emplace_back(p, j);
+    }
+    if (job->tasks.empty()) return;
+    job->left.reset(new std::atomic<int>[job->reqs.size()]);
+    for (size_t p = 0; p < job->reqs.size(); ++p) job->left[p] = job->reqs[p].cols;
+    probe_job_ = std::async(std::launch::async, [job] {
+        std::atomic<size_t> next{0};
+        auto work = [&] {
+            for (size_t t; (t = next.fetch_add(1)) < job->tasks.size();) {
+                const auto [p, j] = job->tasks[t];
+                const ProbeReq& r = job->reqs[p];
+                probe_column(job->base[p], j, r.n, r.kind, job->panels[p]->data() + static_cast<int64_t>(j) * r.n);
+                if (job->left[p].fetch_sub(1) == 1) job->done[p].set_value(job->panels[p]);
+            }
+        };
+        // leave two hardware threads to the engine's own thread (kernel launches, synchronisations)
+        const unsigned hw = std::thread::hardware_concurrency();
+        const unsigned nt = hw > 3 ? hw - 2 : 1;
+        std::vector<std::thread> pool;
+        for (unsigned i = 1; i < nt; ++i) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+    });
+}
+
+Context::Panel Context::take_probes(int64_t n, int cols, uint64_t seed, const char* label, int kind) {
+    auto it = probe_prefetch_.find(probe_key(n, cols, seed, label, kind));
+    if (it != probe_prefetch_.end()) {
+        Panel v = it->second.get();
+        probe_prefetch_.erase(it);
+        return v;
+    }
+    auto v = std::make_shared<std::vector<double>>(static_cast<size_t>(n) * cols);
+    probe_panel_mt(n, cols, seed, label, kind, v->data());
+    return v;
+}
+
+void Context::drop_prefetched_probes() {
+    if (probe_job_.valid()) probe_job_.wait();
+    probe_prefetch_.clear();
+}
+
 void Context::sync() {
     cuda_check(cudaStreamSynchronize(stream_), "stream synchronize");
     if (comm_) cuda_check(cudaStreamSynchronize(comm_), "comm stream synchronize");
@@ -1221,6 +1291,13 @@ void make_probes(Context& ctx, const KernelMatrix& k, DevBuf& dst, int cols, int
                k.rows * sizeof(double), cols);
         return;
     }
+    if (ctx.probe_source == 1 && kind == kProbeGaussian) {  // the reference's draws, bitwise (host threads)
+        const auto v = ctx.take_probes(k.n, cols, seed, label, kind);
+        h2d_2d(ctx, dst.as<double>(), ld * sizeof(double), v->data() + k.row0, k.n * sizeof(double),
+               k.rows * sizeof(double), cols);
+        ctx.sync();  // v is pageable host memory owned by this frame
+        return;
+    }
     cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
     launched(ctx,
              launch_rng_panel(derive_key(seed, hash_name(label)), true, kind, k.row0, k.rows, cols, 0,
@@ -2032,10 +2109,23 @@ MutualInfo mutual_information_samples_dev(Context& ctx, const double* x, int64_t
                                           const EstParams& p, int prec) {
     MutualInfo mi;
     if (prec == kF32 && ctx.fused_mi && fused_mi_params(p)) {
+        // host-drawn probes: all six panels (sketch and residual probes of the three terms,
+        // hutchpp3's seeds and labels) are generated on the host while the device builds A and B
+        if (ctx.probe_source == 1 && p.s > 0) {  // sketch panels first: they are needed first
+            std::vector<Context::ProbeReq> reqs;
+            for (const char* label : {"hutchpp-sketch", "hutchpp-probe"})
+                for (const char* term : {"term:vars", "term:target", "term:joint"}) {
+                    const SketchCfg c = sketch_cfg(with_seed(p, term), p.s);
+                    reqs.push_back({n, label[8] == 's' ? c.s_q : c.s_g, c.seed, label, c.probe_kind});
+                }
+            ctx.prefetch_probes(reqs);
+        }
         // A and B resident together; the joint term is formed inside the fused passes
         KernelPtr a = build_gaussian_dev(ctx, x, n, dx, ldx, sigma_x, prec);
         KernelPtr b = build_gaussian_dev(ctx, y, n, dy, ldy, sigma_y, prec);
-        if (mutual_information_fused(ctx, *a, *b, p, &mi)) return mi;
+        const bool done = mutual_information_fused(ctx, *a, *b, p, &mi);
+        ctx.drop_prefetched_probes();
+        if (done) return mi;
     }
     {
         KernelPtr a = build_gaussian_dev(ctx, x, n, dx, ldx, sigma_x, prec);

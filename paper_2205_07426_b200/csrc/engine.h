@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <atomic>
+#include <future>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -148,6 +151,23 @@ public:
     PanelWorkspace ws_aux[2];  // the second and third operand of a fused mutual-information pass
     bool fused_mi = true;      // mutual information: one pass over A and B for all three terms
     bool feature_groups = true;  // feature tools: candidates' estimates as grouped stacks (fp32)
+    // source of seeded Gaussian probes (Rademacher probes are exact on the device either way):
+    // 0 device (rng_panel: the reference's substreams with CUDA's log/sin/cos, <= 2 ulp from glibc per
+    // draw), 1 host (the reference's own stream arithmetic, bitwise the probes of
+    // proj/src/hutchpp.cpp:13-22, generated on the host's threads and copied; mutual information
+    // requests its six panels before the kernel builds so the host work overlaps them)
+    int probe_source = 0;
+    struct ProbeReq {
+        int64_t n;
+        int cols;
+        uint64_t seed;
+        std::string label;
+        int kind;
+    };
+    // starts generating the panels on the host threads, columns handed out in request order
+    void prefetch_probes(const std::vector<ProbeReq>& reqs);
+    std::shared_ptr<std::vector<double>> take_probes(int64_t n, int cols, uint64_t seed, const char* label, int kind);
+    void drop_prefetched_probes();  // waits for unused panels, frees them
     DevBuf gram_partial, small, probe_err;
     DevBuf x0, work, acc;
 
@@ -162,6 +182,10 @@ private:
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
     cudaStream_t comm_ = nullptr;
     cudaEvent_t ev_main_ = nullptr, ev_comm_ = nullptr;
+    // requested panels, generated one after another in request order (each on all host threads)
+    using Panel = std::shared_ptr<std::vector<double>>;
+    std::map<std::string, std::shared_future<Panel>> probe_prefetch_;
+    std::future<void> probe_job_;
 };
 
 struct KernelMatrix {

@@ -1,5 +1,7 @@
 #include "host_math.h"
 
+#include <thread>
+
 #include <algorithm>
 #include <cmath>
 #include <numbers>
@@ -52,6 +54,27 @@ void probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind
         else
             for (int64_t i = 0; i < n; ++i) col[i] = s.next_gaussian();
     }
+}
+
+void probe_column(uint64_t base, int j, int64_t n, int kind, double* col) {
+    RandomStream s(derive_key(base, static_cast<uint64_t>(j)));
+    if (kind == kProbeRademacher)
+        for (int64_t i = 0; i < n; ++i) col[i] = s.next_rademacher();
+    else
+        for (int64_t i = 0; i < n; ++i) col[i] = s.next_gaussian();
+}
+
+void probe_panel_mt(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out) {
+    const uint64_t base = derive_key(seed, hash_name(label));
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int nt = std::max(1, std::min(cols, hw));
+    auto work = [&](int t) {
+        for (int j = t; j < cols; j += nt) probe_column(base, j, n, kind, out + static_cast<int64_t>(j) * n);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
 }
 
 // ---- coefficients -------------------------------------------------------------

@@ -70,6 +70,10 @@ enum ProbeKind : int { kProbeGaussian = 0, kProbeRademacher = 1 };
 // detail::gaussian_panel (proj/src/hutchpp.cpp:13-22), column-major n x cols;
 // kind Rademacher uses the same per-column substreams.
 void probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out);
+// the same panel with its columns (independent substreams) spread over the host's hardware threads
+void probe_panel_mt(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out);
+// column j of a panel whose base key is derive_key(seed, hash_name(label))
+void probe_column(uint64_t base, int j, int64_t n, int kind, double* col);
 
 // ---- polynomial coefficients: proj/src/poly.cpp:10-58 ----------------------
 std::vector<double> binomial_coeffs(double alpha, int m);
