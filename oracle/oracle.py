@@ -102,6 +102,8 @@ def lib():
         h.oracle_mixture_samples.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, _D]
         h.oracle_gaussian_gram.argtypes = [_D, _I64, _I64, C.c_double, _D]
         h.oracle_build_kernel.argtypes = [_D, _I64, _I64, C.c_double, _D]
+        h.oracle_polynomial_gram.argtypes = [_D, _I64, _I64, C.c_int, C.c_double, _D]
+        h.oracle_build_kernel_polynomial.argtypes = [_D, _I64, _I64, C.c_int, C.c_double, _D]
         h.oracle_hadamard_joint.argtypes = [_D, _I64, _D, _I64, _D]
         h.oracle_matvec.argtypes = [_D, _I64, _D, _D]
         h.oracle_matmul_panel.argtypes = [_D, _I64, _D, C.c_int, _D]
@@ -209,6 +211,21 @@ def build_kernel(x, sigma):
     x = _f(x)
     out = np.empty((x.shape[0], x.shape[0]), order="F")
     _chk(lib().oracle_build_kernel(_p(x), x.shape[0], x.shape[1], sigma, _p(out)))
+    return out
+
+
+def polynomial_gram(x, degree, offset):
+    x = _f(x)
+    out = np.empty((x.shape[0], x.shape[0]), order="F")
+    _chk(lib().oracle_polynomial_gram(_p(x), x.shape[0], x.shape[1], int(degree), float(offset), _p(out)))
+    return out
+
+
+def build_kernel_polynomial(x, degree, offset):
+    """build_kernel(X, PolynomialKernel{degree, offset}) (kernel.cpp:35-72, ops.cpp:22-28)."""
+    x = _f(x)
+    out = np.empty((x.shape[0], x.shape[0]), order="F")
+    _chk(lib().oracle_build_kernel_polynomial(_p(x), x.shape[0], x.shape[1], int(degree), float(offset), _p(out)))
     return out
 
 

@@ -237,11 +237,43 @@ bool all_finite(const Mat& m) {
     return true;
 }
 
+// polynomial_row / polynomial_gram (ops.cpp:22-28,58-64): K_ij = pow(x_i·x_j + offset, degree),
+// the dot summed over the features in order
+Mat polynomial_gram(const Mat& x, int degree, double offset) {
+    const int64_t n = x.r, d = x.c;
+    Mat k(n, n);
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = i; j < n; ++j) {
+            double dot = 0.0;
+            for (int64_t t = 0; t < d; ++t) dot += x(i, t) * x(j, t);
+            const double v = std::pow(dot + offset, static_cast<double>(degree));
+            k(i, j) = v;
+            k(j, i) = v;
+        }
+    }
+    return k;
+}
+
+Mat normalise_kernel(Mat k);
+
 Mat build_kernel(const Mat& x, double sigma) {  // kernel.cpp:35-72 (Gaussian branch)
     if (x.r < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(x.r));
     if (!all_finite(x)) fail(kNonFinite, "sample matrix contains non-finite values");
     if (sigma <= 0.0) fail(kInvalidArgument, "gaussian kernel needs sigma > 0");
-    Mat k = gaussian_gram(x, sigma);
+    return normalise_kernel(gaussian_gram(x, sigma));
+}
+
+Mat build_kernel_polynomial(const Mat& x, int degree, double offset) {  // kernel.cpp:35-72 (polynomial branch)
+    if (x.r < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(x.r));
+    if (!all_finite(x)) fail(kNonFinite, "sample matrix contains non-finite values");
+    if (degree < 1) fail(kInvalidArgument, "polynomial kernel needs degree >= 1");
+    if (offset < 0.0) fail(kInvalidArgument, "polynomial kernel needs offset >= 0");
+    return normalise_kernel(polynomial_gram(x, degree, offset));
+}
+
+// kernel.cpp:51-70: finiteness, positive diagonal, A_ij = ((inv_n·K_ij)·isd_i)·isd_j, A_ii = inv_n
+Mat normalise_kernel(Mat k) {
     const int64_t n = k.r;
     if (!all_finite(k)) fail(kNonFinite, "kernel evaluation produced non-finite values");
     Vec isd(n);
@@ -1616,6 +1648,12 @@ int oracle_gaussian_gram(const double* x, int64_t n, int64_t d, double sigma, do
 }
 int oracle_build_kernel(const double* x, int64_t n, int64_t d, double sigma, double* out) {
     return guard([&] { unwrap(orc::build_kernel(wrap(x, n, d), sigma), out); });
+}
+int oracle_polynomial_gram(const double* x, int64_t n, int64_t d, int degree, double offset, double* out) {
+    return guard([&] { unwrap(orc::polynomial_gram(wrap(x, n, d), degree, offset), out); });
+}
+int oracle_build_kernel_polynomial(const double* x, int64_t n, int64_t d, int degree, double offset, double* out) {
+    return guard([&] { unwrap(orc::build_kernel_polynomial(wrap(x, n, d), degree, offset), out); });
 }
 int oracle_hadamard_joint(const double* a, int64_t na, const double* b, int64_t nb, double* out) {
     return guard([&] {

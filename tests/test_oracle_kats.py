@@ -87,6 +87,64 @@ def test_kernel_invariants_and_psd(orc):  # test_kernel.cpp:52-63 (Gaussian reps
         assert np.linalg.eigvalsh(a).min() >= -1e-10
 
 
+def test_polynomial_gram_matches_naive_formula(orc):  # test_ops.cpp:51-56
+    x = orc.fill_gaussian(12, 23, 3)
+    p = orc.polynomial_gram(x, 3, 0.5)
+    np.testing.assert_allclose(p, (x @ x.T + 0.5) ** 3, rtol=1e-12, atol=0)
+    assert np.array_equal(p, p.T)
+
+
+def test_polynomial_kernel_invariants_and_psd(orc):  # test_kernel.cpp:52-63 (polynomial reps)
+    for rep in (1, 3):
+        x = orc.fill_gaussian(21 + rep, 40 + 3 * rep, 4)
+        a = orc.build_kernel_polynomial(x, 2, 1.0)
+        _invariants(a)
+        assert np.linalg.eigvalsh(a).min() >= -1e-10
+        k = (x @ x.T + 1.0) ** 2
+        isd = 1.0 / np.sqrt(np.diag(k))
+        ref = (k / x.shape[0]) * isd[:, None] * isd[None, :]
+        np.fill_diagonal(ref, 1.0 / x.shape[0])
+        np.testing.assert_allclose(a, ref, rtol=1e-12, atol=1e-16)
+
+
+def test_polynomial_kernel_errors(orc):  # test_kernel.cpp:65-77
+    x = np.zeros((3, 2))
+    x[1] = [1.0, 0.0]
+    x[2] = [0.0, 1.0]
+    with pytest.raises(orc.OracleError) as e:  # zero diagonal: sample 0 with offset 0
+        orc.build_kernel_polynomial(x, 2, 0.0)
+    assert e.value.code == 2 and "not positive" in str(e.value)
+    with pytest.raises(orc.OracleError) as e:  # non-finite kernel values
+        orc.build_kernel_polynomial(np.array([[1e200], [-1e200]]), 2, 1.0)
+    assert e.value.code == 3
+    for deg, off in ((0, 1.0), (2, -0.5)):
+        with pytest.raises(orc.OracleError) as e:
+            orc.build_kernel_polynomial(orc.fill_gaussian(3, 4, 2), deg, off)
+        assert e.value.code == 1
+
+
+def test_chebyshev_rank_deficient_polynomial_kernel(orc):  # test_entropy.cpp:121-131
+    x = orc.fill_gaussian(65, 120, 4)
+    x[90:] = x[:30]  # duplicates force u = 0
+    a = orc.build_kernel_polynomial(x, 2, 1.0)
+    exact = orc.entropy_exact(a, 2.5)
+    b = orc.estimate_bounds(a)
+    est = orc.estimate(a, alpha=2.5, method="chebyshev", s=64, m=30, seed=3, bounds=(0.0, b["v"]))
+    assert abs(est["entropy"] - exact) <= 1e-2 * abs(exact)
+
+
+def test_acceptance_rank_deficient_polynomial(orc):  # acceptance.cpp:230-254 (criterion 6)
+    x = orc.fill_gaussian(888, 400, 8)
+    x[300:] = x[:100]
+    a = orc.build_kernel_polynomial(x, 2, 1.0)
+    exact = orc.entropy_exact(a, 2.5)
+    b = orc.estimate_bounds(a, seed=5)
+    assert b["rank_deficient"]
+    worst = max(abs(orc.estimate(a, alpha=2.5, method="chebyshev", s=64, m=30, seed=sd,
+                                 bounds=(0.0, b["v"]))["entropy"] - exact) / abs(exact) for sd in range(20))
+    assert worst <= 1e-2
+
+
 def test_kernel_errors(orc):  # test_kernel.cpp:65-83
     with pytest.raises(orc.OracleError) as e:
         orc.build_kernel(np.array([[1.0, 2.0]]), 1.0)
