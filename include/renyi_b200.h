@@ -208,6 +208,14 @@ int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n
 int renyi_kernel_build_gaussian_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx,
                                     double sigma, const double* d_y, int64_t dy, int64_t ldy, double sigma_y,
                                     int precision, renyi_kernel** out);
+/* build_kernel(X, PolynomialKernel{degree, offset}) — proj/src/kernel.cpp:35-72 + ops.cpp:22-28,58-64:
+ * K_ij = pow(x_i·x_j + offset, degree) in fp64, A_ij = K_ij / (n sqrt(K_ii K_jj)); RENYI_F64 or
+ * RENYI_F32 (stored as the split every fp32 product consumes); errors as the reference's: degree < 1
+ * or offset < 0 invalid_argument, non-finite kernel values non_finite, K_ii <= 0 zero_diagonal */
+int renyi_kernel_build_polynomial(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree,
+                                  double offset, int precision, renyi_kernel** out);
+int renyi_kernel_build_polynomial_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx,
+                                      int degree, double offset, int precision, renyi_kernel** out);
 /* NormalizedKernel(Matrix) — kernel.hpp:33 (caller asserts the invariants) */
 int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int precision, renyi_kernel** out);
 /* hadamard_joint({a, b}) — kernel.cpp:74-101 */

@@ -17,6 +17,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "renyi_b200.h"
@@ -91,6 +92,13 @@ struct GaussianKernel {  // proj/include/renyi/kernel.hpp:12-14
     double sigma = 1.0;
 };
 
+struct PolynomialKernel {  // proj/include/renyi/kernel.hpp:16-19
+    int degree = 2;
+    double offset = 1.0;
+};
+
+using KernelSpec = std::variant<GaussianKernel, PolynomialKernel>;  // kernel.hpp:22
+
 // NormalizedKernel (proj/include/renyi/kernel.hpp:27-42), device resident.
 class NormalizedKernel {
 public:
@@ -122,6 +130,19 @@ inline NormalizedKernel build_kernel(const Context& ctx, const Matrix& samples, 
     check(renyi_kernel_build_gaussian(ctx.get(), samples.data.data(), samples.rows, samples.cols, samples.rows,
                                       spec.sigma, static_cast<int>(prec), &k));
     return NormalizedKernel(k);
+}
+
+inline NormalizedKernel build_kernel(const Context& ctx, const Matrix& samples, const PolynomialKernel& spec,
+                                     Precision prec = Precision::fp64) {  // kernel.cpp:35-72, ops.cpp:22-28
+    renyi_kernel* k = nullptr;
+    check(renyi_kernel_build_polynomial(ctx.get(), samples.data.data(), samples.rows, samples.cols, samples.rows,
+                                        spec.degree, spec.offset, static_cast<int>(prec), &k));
+    return NormalizedKernel(k);
+}
+
+inline NormalizedKernel build_kernel(const Context& ctx, const Matrix& samples, const KernelSpec& spec,
+                                     Precision prec = Precision::fp64) {
+    return std::visit([&](const auto& s) { return build_kernel(ctx, samples, s, prec); }, spec);
 }
 
 inline NormalizedKernel from_matrix(const Context& ctx, const Matrix& a, Precision prec = Precision::fp64) {

@@ -182,6 +182,10 @@ SIGNATURES = {
     "renyi_ctx_join_local_group": (C.c_int, [_P, _P, C.c_int]),
     "renyi_ctx_rank": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "renyi_kernel_build_gaussian": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)]),
+    "renyi_kernel_build_polynomial": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_int, C.c_double, C.c_int,
+                                                C.POINTER(_P)]),
+    "renyi_kernel_build_polynomial_dev": (C.c_int, [_P, C.c_void_p, _I64, _I64, _I64, C.c_int, C.c_double, C.c_int,
+                                                    C.POINTER(_P)]),
     "renyi_csv_load": (C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
     "renyi_csv_parse": (C.c_int, [_P, C.c_char_p, _I64, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
     "renyi_dataset_shape": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(C.c_int)]),

@@ -200,6 +200,12 @@ class GaussianKernel:
     sigma: float = 1.0
 
 
+@dataclass
+class PolynomialKernel:  # proj/include/renyi/kernel.hpp:16-19
+    degree: int = 2
+    offset: float = 1.0
+
+
 class NormalizedKernel:
     """Device-resident trace-one kernel matrix (proj/include/renyi/kernel.hpp:27-42)."""
 
@@ -248,10 +254,14 @@ def build_kernel(samples, spec: GaussianKernel, precision="fp64", ctx: Optional[
     x = _colmajor(samples)
     if x.ndim != 2:
         raise RenyiError(1, "samples must be a 2-D array")
-    if not isinstance(spec, GaussianKernel):
-        raise RenyiError(1, "only the Gaussian kernel is on the device path (polynomial is out of scope)")
     h = C.c_void_p()
     n, d = x.shape
+    if isinstance(spec, PolynomialKernel):
+        check(L.lib().renyi_kernel_build_polynomial(ctx.handle, _dptr(x), n, d, max(n, 1), int(spec.degree),
+                                                    float(spec.offset), PRECISIONS[precision], C.byref(h)))
+        return NormalizedKernel(h, ctx, PRECISIONS[precision])
+    if not isinstance(spec, GaussianKernel):
+        raise RenyiError(1, "kernel spec must be GaussianKernel or PolynomialKernel")
     check(L.lib().renyi_kernel_build_gaussian(ctx.handle, _dptr(x), n, d, max(n, 1), spec.sigma,
                                               PRECISIONS[precision], C.byref(h)))
     return NormalizedKernel(h, ctx, PRECISIONS[precision])
@@ -967,6 +977,10 @@ def build_kernel_dev(d_x: int, n: int, d: int, ldx: int, spec: GaussianKernel, p
                      ctx: Optional[Context] = None) -> NormalizedKernel:
     ctx = ctx or default_context()
     h = C.c_void_p()
+    if isinstance(spec, PolynomialKernel):
+        check(L.lib().renyi_kernel_build_polynomial_dev(ctx.handle, C.c_void_p(d_x), n, d, ldx, int(spec.degree),
+                                                        float(spec.offset), PRECISIONS[precision], C.byref(h)))
+        return NormalizedKernel(h, ctx, PRECISIONS[precision])
     check(L.lib().renyi_kernel_build_gaussian_dev(ctx.handle, C.c_void_p(d_x), n, d, ldx, spec.sigma, None, 0, 0,
                                                   1.0, PRECISIONS[precision], C.byref(h)))
     return NormalizedKernel(h, ctx, PRECISIONS[precision])

@@ -338,6 +338,28 @@ int renyi_kernel_build_gaussian(renyi_ctx* ctx, const double* x, int64_t n, int6
     });
 }
 
+int renyi_kernel_build_polynomial(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree,
+                                  double offset, int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(out, "out");
+        check_precision(precision);
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::build_polynomial(ctx->ctx, x, n, d, ldx, degree, offset, precision);
+        });
+    });
+}
+
+int renyi_kernel_build_polynomial_dev(renyi_ctx* ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx,
+                                      int degree, double offset, int precision, renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(d_x, "samples"), need(out, "out");
+        check_precision(precision);
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) {
+            h.k = rb::build_polynomial_dev(ctx->ctx, d_x, n, d, ldx, degree, offset, precision);
+        });
+    });
+}
+
 int renyi_kernel_build_gaussian_joint(renyi_ctx* ctx, const double* x, int64_t n, int64_t dx, int64_t ldx,
                                       double sigma_x, const double* y, int64_t dy, int64_t ldy, double sigma_y,
                                       int precision, renyi_kernel** out) {

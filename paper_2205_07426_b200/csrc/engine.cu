@@ -608,6 +608,87 @@ KernelPtr build_gaussian_dev(Context& ctx, const double* x, int64_t n, int64_t d
     return k;
 }
 
+KernelPtr build_polynomial(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree, double offset,
+                           int prec) {
+    if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
+    if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
+    if (ldx < n) fail(kInvalidArgument, "leading dimension smaller than the sample count");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    DevBuf xs;
+    xs.alloc(static_cast<size_t>(n) * d * sizeof(double));
+    if (ldx == n) h2d_staged(ctx, xs.as<double>(), x, static_cast<size_t>(n) * d * sizeof(double));
+    else h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), d);
+    KernelPtr k = build_polynomial_dev(ctx, xs.as<double>(), n, d, n, degree, offset, prec);
+    ctx.sync();  // xs goes out of scope
+    return k;
+}
+
+KernelPtr build_polynomial_dev(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree,
+                               double offset, int prec) {
+    NvtxRange nvtx("kernel build (polynomial Gram)");
+    // validate_samples (kernel.cpp:25-29), then the spec (kernel.cpp:44-45)
+    if (n < 2) fail(kInvalidArgument, "need at least 2 samples, got " + std::to_string(n));
+    if (d < 1) fail(kInvalidArgument, "samples need at least one feature");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    ctx.small.ensure(4 * sizeof(unsigned));
+    unsigned* flags = ctx.small.as<unsigned>();
+    cuda_check(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned), ctx.stream()), "memset");
+    launched(ctx, launch_check_samples(x, n, static_cast<int>(d), 1, ldx, flags, ctx.stream()), "check_samples");
+    unsigned hf[2];
+    d2h(ctx, hf, flags, sizeof(hf));
+    ctx.sync();
+    if (hf[0]) fail(kNonFinite, "sample matrix contains non-finite values");
+    if (degree < 1) fail(kInvalidArgument, "polynomial kernel needs degree >= 1");
+    if (!(offset >= 0.0)) fail(kInvalidArgument, "polynomial kernel needs offset >= 0");
+    if (prec == kMF) fail(kInvalidArgument, "the matrix-free path recomputes Gaussian kernel entries only");
+
+    auto k = std::make_unique<KernelMatrix>();
+    k->n = n;
+    k->prec = prec;
+    assign_shard(ctx, *k);
+    if (prec == kF64 && k->world > 1) fail(kInvalidArgument, "the fp64 configuration is single-rank");
+    k->ld = matrix_pitch(n);
+    const double inv_n = 1.0 / static_cast<double>(n);
+    k->normalized = true;
+    k->a_norm = 1.0;  // |A_ij| <= 1/n (Cauchy-Schwarz on the PSD kernel): row sums <= 1
+    GramArgs g{};
+    g.x = x;
+    g.dx = static_cast<int>(d);
+    g.x_rs = 1, g.x_cs = ldx;
+    g.n = n;
+    g.row0 = k->row0;
+    g.rows = k->rows;
+    g.ld = k->ld;
+    g.inv_n = inv_n;
+    const size_t elems = static_cast<size_t>(k->rows) * k->ld;
+    DevBuf isd;
+    isd.alloc(static_cast<size_t>(n) * sizeof(double));
+    cuda_check(cudaMemsetAsync(flags, 0, sizeof(unsigned), ctx.stream()), "memset");
+    cuda_check(cudaMemsetAsync(flags + 1, 0xFF, sizeof(unsigned), ctx.stream()), "memset");
+    if (prec == kF32) {
+        k->hi.alloc(elems * sizeof(__half));
+        k->lo.alloc(elems * sizeof(__half));
+        k->unscale = inv_n / kSplitScale;
+        launched(ctx, launch_poly_gram(g, degree, offset, isd.as<double>(), k->hi.as<__half>(), k->lo.as<__half>(),
+                                       nullptr, flags, ctx.stream()),
+                 "poly_gram");
+    } else {
+        k->a64.alloc(elems * sizeof(double));
+        k->unscale = 1.0;
+        launched(ctx, launch_poly_gram(g, degree, offset, isd.as<double>(), nullptr, nullptr, k->a64.as<double>(),
+                                       flags, ctx.stream()),
+                 "poly_gram");
+    }
+    // a non-finite entry in any rank's rows fails every rank (the diagonal is computed on all of them)
+    if (ctx.exchange) ctx.exchange->allreduce_max_u32(flags, 1, ctx.stream());
+    d2h(ctx, hf, flags, sizeof(hf));
+    ctx.sync();  // isd goes out of scope
+    if (hf[0]) fail(kNonFinite, "kernel evaluation produced non-finite values");
+    if (hf[1] != 0xFFFFFFFFu)
+        fail(kZeroDiagonal, "kernel diagonal entry " + std::to_string(hf[1]) + " is not positive");
+    return k;
+}
+
 KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
     if (n < 1) fail(kInvalidArgument, "matrix must be non-empty");
     if (prec == kMF) fail(kInvalidArgument, "the matrix-free precision builds from samples only");

@@ -219,6 +219,11 @@ using KernelPtr = std::unique_ptr<KernelMatrix>;
 // x: host column-major n x d (Eigen layout of the reference), ld >= n.
 KernelPtr build_gaussian(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, int prec,
                          const double* y = nullptr, int64_t dy = 0, int64_t ldy = 0, double sigma_y = 1.0);
+// build_kernel(X, PolynomialKernel{degree, offset}) (kernel.cpp:35-72, ops.cpp:22-28,58-64), host or device samples
+KernelPtr build_polynomial(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree, double offset,
+                           int prec);
+KernelPtr build_polynomial_dev(Context& ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, int degree,
+                               double offset, int prec);
 // device-resident samples (column-major, leading dimension ld)
 KernelPtr build_gaussian_dev(Context& ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, double sigma,
                              int prec, const double* d_y = nullptr, int64_t dy = 0, int64_t ldy = 0,

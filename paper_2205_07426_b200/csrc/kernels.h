@@ -239,6 +239,10 @@ bool gram_tc_supported(const GramArgs& g);
 size_t gram_tc_scratch_bytes(const GramArgs& g);
 cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scratch, cudaStream_t stream);
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream);
+// polynomial kernel build (x, n, dx, strides, rows/row0/ld, inv_n of g): isd [n] scratch; hi/lo (fp32
+// configuration) or a64 (fp64); flags[0] |= 1 on a non-finite entry, flags[1] = min i with K_ii <= 0
+cudaError_t launch_poly_gram(const GramArgs& g, int degree, double offset, double* isd, __half* hi, __half* lo,
+                             double* a64, unsigned* flags, cudaStream_t stream);
 
 // A (fp64 row-major) -> planes holding A*scale.
 cudaError_t launch_matrix_to_split(const double* a, int64_t rows, int64_t cols, int64_t lda, double scale,

@@ -507,6 +507,88 @@ cudaError_t launch_gram_split(const GramArgs& g, __half* hi, __half* lo, void* s
     return cudaGetLastError();
 }
 
+namespace {
+// ---------------------------------------------------------------- polynomial kernel
+// build_kernel(X, PolynomialKernel{degree, offset}) (proj/src/kernel.cpp:35-72, ops.cpp:22-28,58-64):
+// K_ij = pow(x_i·x_j + offset, degree) in fp64 (dots summed over the features in order), normalised
+// A_ij = ((fl(1/n)·K_ij)·isd_i)·isd_j with isd_i = 1/sqrt(K_ii), A_ii = 1/n. Stored as fp64 (fp64
+// configuration) or as the fp16 hi/lo split of A·n·2^14 = K_ij·isd_i·isd_j·2^14 (|.| <= 2^14 by
+// Cauchy-Schwarz: the kernel is PSD), the format every block product consumes.
+// flags[0]: a non-finite K entry; flags[1]: the smallest i with K_ii <= 0 (n when none).
+__global__ void poly_diag_kernel(const double* __restrict__ x, int64_t n, int d, int64_t rs, int64_t cs, double deg,
+                                 double offset, double* __restrict__ isd, unsigned* __restrict__ flags) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double dot = 0.0;
+    for (int k = 0; k < d; ++k) {
+        const double v = x[i * rs + k * cs];
+        dot = fma(v, v, dot);
+    }
+    const double kii = pow(dot + offset, deg);
+    if (!isfinite(kii)) atomicOr(flags, 1u);
+    if (!(kii > 0.0)) atomicMin(flags + 1, static_cast<unsigned>(i));
+    isd[i] = 1.0 / sqrt(kii);
+}
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) poly_gram_kernel(GramArgs g, double deg, double offset,
+                                                        const double* __restrict__ isd, __half* __restrict__ hi,
+                                                        __half* __restrict__ lo, double* __restrict__ a64,
+                                                        unsigned* __restrict__ flags) {
+    __shared__ double xr[TKd][TM + 1];
+    __shared__ double xc[TKd][TN + 4];
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t row0 = g.row0 + static_cast<int64_t>(blockIdx.y) * TM;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * TN;
+    double dot[4][4], sqr[4], sqc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        sqr[u] = sqc[u] = 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dot[u][v] = 0.0;
+    }
+    GramTile<double>::accumulate(g.x, g.dx, g.x_rs, g.x_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t gi = row0 + ty + 16 * u;
+        if (gi >= g.row0 + g.rows || gi >= g.n) continue;
+        const int64_t li = gi - g.row0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t gj = col0 + 4 * tx + v;
+            if (gj >= g.n) continue;
+            const double k = pow(dot[u][v] + offset, deg);
+            bad |= !isfinite(k);
+            // the reference evaluates each pair once, i < j: ((inv_n·K)·isd_i)·isd_j, mirrored (exact symmetry)
+            const double s1 = isd[gi < gj ? gi : gj], s2 = isd[gi < gj ? gj : gi];
+            if (SPLIT) {
+                const double s = gi == gj ? static_cast<double>(kSplitScale) : k * s1 * s2 * kSplitScale;
+                const __half h = __double2half(s);
+                hi[li * g.ld + gj] = h;
+                lo[li * g.ld + gj] = __double2half(s - static_cast<double>(__half2float(h)));
+            } else {
+                a64[li * g.ld + gj] = gi == gj ? g.inv_n : g.inv_n * k * s1 * s2;
+            }
+        }
+    }
+    if (bad) atomicOr(flags, 1u);
+}
+
+}  // namespace
+
+cudaError_t launch_poly_gram(const GramArgs& g, int degree, double offset, double* isd, __half* hi, __half* lo,
+                             double* a64, unsigned* flags, cudaStream_t stream) {
+    const double deg = static_cast<double>(degree);
+    poly_diag_kernel<<<static_cast<unsigned>((g.n + 255) / 256), 256, 0, stream>>>(g.x, g.n, g.dx, g.x_rs, g.x_cs,
+                                                                                  deg, offset, isd, flags);
+    dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
+    if (hi) poly_gram_kernel<true><<<grid, 256, 0, stream>>>(g, deg, offset, isd, hi, lo, nullptr, flags);
+    else poly_gram_kernel<false><<<grid, 256, 0, stream>>>(g, deg, offset, isd, nullptr, nullptr, a64, flags);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream) {
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
     gram_kernel<double, false><<<grid, 256, 0, stream>>>(g, nullptr, nullptr, a);
