@@ -252,6 +252,16 @@ int renyi_dataset_destroy(renyi_dataset* ds);
 /* ---- hot-path seams ------------------------------------------------------- */
 /* ops::matmul_panel(a, x) — proj/src/ops.cpp:98-107: Y = A V, V n x s */
 int renyi_matmul_panel(renyi_ctx* ctx, const renyi_kernel* k, const double* v, int s, double* y);
+/* the raw ops seam (proj/include/renyi/ops.hpp:12-33) on host column-major matrices:
+ * ops::gaussian_gram (ops.cpp:9-20,39-47): K n x n, K_ii = 1, exactly symmetric;
+ * ops::polynomial_gram (ops.cpp:22-28,58-64): K_ij = pow(x_i·x_j + offset, degree);
+ * ops::hadamard_scaled (ops.cpp:116-122): C = scale * (A ∘ B), rows x cols */
+int renyi_ops_gaussian_gram(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                            double* k);
+int renyi_ops_polynomial_gram(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree,
+                              double offset, double* k);
+int renyi_ops_hadamard_scaled(renyi_ctx* ctx, const double* a, const double* b, int64_t rows, int64_t cols,
+                              double scale, double* c);
 /* ops::matvec(a, x) — proj/src/ops.cpp:73-85 */
 int renyi_matvec(renyi_ctx* ctx, const renyi_kernel* k, const double* x, double* y);
 /* apply_panel(spec, a, x) — proj/src/poly.cpp:158-164 */

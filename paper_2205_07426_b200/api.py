@@ -314,6 +314,39 @@ class ops:  # namespace mirror of renyi::ops
         """y = A x (proj/src/ops.cpp:73-85)."""
         return ops.matmul_panel(a, np.asarray(x, dtype=np.float64).reshape(-1, 1))[:, 0]
 
+    @staticmethod
+    def gaussian_gram(samples, sigma: float, ctx: Optional[Context] = None) -> np.ndarray:
+        """K_ij = exp(-||x_i - x_j||^2 / (2 sigma^2)), unnormalised (proj/src/ops.cpp:9-20,39-47)."""
+        ctx = ctx or default_context()
+        x = _colmajor(samples)
+        n, d = x.shape
+        k = np.empty((n, n), order="F")
+        check(L.lib().renyi_ops_gaussian_gram(ctx.handle, _dptr(x), n, d, max(n, 1), float(sigma), _dptr(k)))
+        return k
+
+    @staticmethod
+    def polynomial_gram(samples, degree: int, offset: float, ctx: Optional[Context] = None) -> np.ndarray:
+        """K_ij = (x_i . x_j + offset)^degree, unnormalised (proj/src/ops.cpp:22-28,58-64)."""
+        ctx = ctx or default_context()
+        x = _colmajor(samples)
+        n, d = x.shape
+        k = np.empty((n, n), order="F")
+        check(L.lib().renyi_ops_polynomial_gram(ctx.handle, _dptr(x), n, d, max(n, 1), int(degree), float(offset),
+                                                _dptr(k)))
+        return k
+
+    @staticmethod
+    def hadamard_scaled(a, b, scale: float, ctx: Optional[Context] = None) -> np.ndarray:
+        """C = scale * (A o B) elementwise (proj/src/ops.cpp:116-122)."""
+        ctx = ctx or default_context()
+        am, bm = _colmajor(a), _colmajor(b)
+        if am.shape != bm.shape or am.ndim != 2:
+            raise RenyiError(4, "hadamard_scaled: matrices must have the same 2-D shape")
+        c = np.empty_like(am, order="F")
+        check(L.lib().renyi_ops_hadamard_scaled(ctx.handle, _dptr(am), _dptr(bm), am.shape[0], am.shape[1],
+                                                float(scale), _dptr(c)))
+        return c
+
 
 # ---------------------------------------------------------------- matrix functions (poly.hpp)
 def binomial_coeffs(alpha: float, m: int) -> np.ndarray:

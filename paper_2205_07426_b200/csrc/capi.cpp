@@ -338,6 +338,30 @@ int renyi_kernel_build_gaussian(renyi_ctx* ctx, const double* x, int64_t n, int6
     });
 }
 
+int renyi_ops_gaussian_gram(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma,
+                            double* k) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(k, "out");
+        rb::ops_gaussian_gram(ctx->ctx, x, n, d, ldx, sigma, k);
+    });
+}
+
+int renyi_ops_polynomial_gram(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree,
+                              double offset, double* k) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(x, "samples"), need(k, "out");
+        rb::ops_polynomial_gram(ctx->ctx, x, n, d, ldx, degree, offset, k);
+    });
+}
+
+int renyi_ops_hadamard_scaled(renyi_ctx* ctx, const double* a, const double* b, int64_t rows, int64_t cols,
+                              double scale, double* c) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(a, "a"), need(b, "b"), need(c, "out");
+        rb::ops_hadamard_scaled(ctx->ctx, a, b, rows, cols, scale, c);
+    });
+}
+
 int renyi_kernel_build_polynomial(renyi_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree,
                                   double offset, int precision, renyi_kernel** out) {
     return guarded([&] {

@@ -689,6 +689,67 @@ KernelPtr build_polynomial_dev(Context& ctx, const double* x, int64_t n, int64_t
     return k;
 }
 
+namespace {
+// n x n fp64 Gram of host samples into a host column-major matrix (the Gram is exactly symmetric, so
+// the device's row-major rows are the host's columns)
+template <typename Launch>
+void raw_gram(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double* k, Launch&& launch) {
+    if (n < 1 || d < 1) fail(kInvalidArgument, "samples must be non-empty");
+    if (ldx < n) fail(kInvalidArgument, "leading dimension smaller than the sample count");
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    DevBuf xs, out;
+    xs.alloc(static_cast<size_t>(n) * d * sizeof(double));
+    h2d_2d(ctx, xs.as<double>(), n * sizeof(double), x, ldx * sizeof(double), n * sizeof(double), d);
+    const int64_t ld = matrix_pitch(n);
+    out.alloc(static_cast<size_t>(n) * ld * sizeof(double));
+    GramArgs g{};
+    g.x = xs.as<double>();
+    g.dx = static_cast<int>(d);
+    g.x_rs = 1, g.x_cs = n;
+    g.n = n, g.row0 = 0, g.rows = n, g.ld = ld;
+    g.inv_n = 1.0;  // fl(1·K) = K: the unnormalised Gram
+    launched(ctx, launch(g, out.as<double>()), "gram");
+    d2h_2d(ctx, k, n * sizeof(double), out.as<double>(), ld * sizeof(double), n * sizeof(double), n);
+    ctx.sync();
+}
+}  // namespace
+
+void ops_gaussian_gram(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, double* k) {
+    NvtxRange nvtx("ops::gaussian_gram");
+    raw_gram(ctx, x, n, d, ldx, k, [&](GramArgs& g, double* out) {
+        g.inv_two_sigma2_x = 1.0 / (2.0 * sigma * sigma);  // ops.cpp:42
+        return launch_gram_f64(g, out, ctx.stream());
+    });
+}
+
+void ops_polynomial_gram(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree, double offset,
+                         double* k) {
+    NvtxRange nvtx("ops::polynomial_gram");
+    ctx.small.ensure(4 * sizeof(unsigned));  // the raw op checks nothing (ops.cpp:58-64); flags unused
+    raw_gram(ctx, x, n, d, ldx, k, [&](GramArgs& g, double* out) {
+        return launch_poly_gram(g, degree, offset, nullptr, nullptr, nullptr, out, ctx.small.as<unsigned>(),
+                                ctx.stream());
+    });
+}
+
+void ops_hadamard_scaled(Context& ctx, const double* a, const double* b, int64_t rows, int64_t cols, double scale,
+                         double* c) {
+    NvtxRange nvtx("ops::hadamard_scaled");
+    if (rows < 0 || cols < 0) fail(kInvalidArgument, "matrix sizes must be non-negative");
+    const int64_t count = rows * cols;
+    if (count == 0) return;
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    DevBuf da, db;
+    da.alloc(static_cast<size_t>(count) * sizeof(double));
+    db.alloc(static_cast<size_t>(count) * sizeof(double));
+    h2d(ctx, da.as<double>(), a, static_cast<size_t>(count) * sizeof(double));
+    h2d(ctx, db.as<double>(), b, static_cast<size_t>(count) * sizeof(double));
+    launched(ctx, launch_scaled_product(da.as<double>(), db.as<double>(), count, scale, da.as<double>(), ctx.stream()),
+             "scaled_product");
+    d2h(ctx, c, da.as<double>(), static_cast<size_t>(count) * sizeof(double));
+    ctx.sync();
+}
+
 KernelPtr from_matrix(Context& ctx, const double* a, int64_t n, int prec) {
     if (n < 1) fail(kInvalidArgument, "matrix must be non-empty");
     if (prec == kMF) fail(kInvalidArgument, "the matrix-free precision builds from samples only");

@@ -224,6 +224,14 @@ KernelPtr build_polynomial(Context& ctx, const double* x, int64_t n, int64_t d, 
                            int prec);
 KernelPtr build_polynomial_dev(Context& ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, int degree,
                                double offset, int prec);
+// the raw ops seam (proj/include/renyi/ops.hpp:12-33), host matrices in and out (column-major):
+// K = gaussian_gram(X, sigma) / polynomial_gram(X, degree, offset) (n x n, single rank), and
+// C = hadamard_scaled(A, B, scale) over rows x cols
+void ops_gaussian_gram(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, double sigma, double* k);
+void ops_polynomial_gram(Context& ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int degree, double offset,
+                         double* k);
+void ops_hadamard_scaled(Context& ctx, const double* a, const double* b, int64_t rows, int64_t cols, double scale,
+                         double* c);
 // device-resident samples (column-major, leading dimension ld)
 KernelPtr build_gaussian_dev(Context& ctx, const double* d_x, int64_t n, int64_t d, int64_t ldx, double sigma,
                              int prec, const double* d_y = nullptr, int64_t dy = 0, int64_t ldy = 0,

@@ -241,6 +241,9 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream);
 // polynomial kernel build (x, n, dx, strides, rows/row0/ld, inv_n of g): isd [n] scratch; hi/lo (fp32
 // configuration) or a64 (fp64); flags[0] |= 1 on a non-finite entry, flags[1] = min i with K_ii <= 0
+// c = scale * (a ∘ b) elementwise over count entries (ops::hadamard_scaled, ops.cpp:116-122)
+cudaError_t launch_scaled_product(const double* a, const double* b, int64_t count, double scale, double* c,
+                                  cudaStream_t stream);
 cudaError_t launch_poly_gram(const GramArgs& g, int degree, double offset, double* isd, __half* hi, __half* lo,
                              double* a64, unsigned* flags, cudaStream_t stream);
 

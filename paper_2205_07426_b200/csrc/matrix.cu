@@ -561,6 +561,10 @@ __global__ void __launch_bounds__(256) poly_gram_kernel(GramArgs g, double deg, 
             if (gj >= g.n) continue;
             const double k = pow(dot[u][v] + offset, deg);
             bad |= !isfinite(k);
+            if (!isd) {  // ops::polynomial_gram: the raw K (no normalisation)
+                a64[li * g.ld + gj] = k;
+                continue;
+            }
             // the reference evaluates each pair once, i < j: ((inv_n·K)·isd_i)·isd_j, mirrored (exact symmetry)
             const double s1 = isd[gi < gj ? gi : gj], s2 = isd[gi < gj ? gj : gi];
             if (SPLIT) {
@@ -581,8 +585,9 @@ __global__ void __launch_bounds__(256) poly_gram_kernel(GramArgs g, double deg, 
 cudaError_t launch_poly_gram(const GramArgs& g, int degree, double offset, double* isd, __half* hi, __half* lo,
                              double* a64, unsigned* flags, cudaStream_t stream) {
     const double deg = static_cast<double>(degree);
-    poly_diag_kernel<<<static_cast<unsigned>((g.n + 255) / 256), 256, 0, stream>>>(g.x, g.n, g.dx, g.x_rs, g.x_cs,
-                                                                                  deg, offset, isd, flags);
+    if (isd)  // isd == nullptr: the raw K of ops::polynomial_gram into a64
+        poly_diag_kernel<<<static_cast<unsigned>((g.n + 255) / 256), 256, 0, stream>>>(g.x, g.n, g.dx, g.x_rs, g.x_cs,
+                                                                                      deg, offset, isd, flags);
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
     if (hi) poly_gram_kernel<true><<<grid, 256, 0, stream>>>(g, deg, offset, isd, hi, lo, nullptr, flags);
     else poly_gram_kernel<false><<<grid, 256, 0, stream>>>(g, deg, offset, isd, nullptr, nullptr, a64, flags);
@@ -636,6 +641,23 @@ cudaError_t launch_hadamard_split(const __half* ahi, const __half* alo, const __
                                   double diag_value, __half* chi, __half* clo, cudaStream_t stream) {
     hadamard_split_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(ahi, alo, bhi, blo, rows, cols, ld, row0, factor,
                                                                       diag_value, chi, clo);
+    return cudaGetLastError();
+}
+
+namespace {
+__global__ void scaled_product_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t count,
+                                      double scale, double* __restrict__ c) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        c[k] = scale * (a[k] * b[k]);
+}
+}  // namespace
+
+cudaError_t launch_scaled_product(const double* a, const double* b, int64_t count, double scale, double* c,
+                                  cudaStream_t stream) {
+    if (count <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>(148 * 8, (count + 255) / 256);
+    scaled_product_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(a, b, count, scale, c);
     return cudaGetLastError();
 }
 

@@ -103,3 +103,24 @@ def test_polynomial_mutual_information_fused(R, orc):
         mi = R.mutual_information([ka], kb, p)
         for key in ("vars_entropy", "target_entropy", "joint_entropy"):
             assert getattr(mi, key) == pytest.approx(ref[key], rel=tol), (prec, key)
+
+
+def test_raw_ops_seam(R, orc):
+    """ops::gaussian_gram / polynomial_gram / hadamard_scaled (proj/include/renyi/ops.hpp:12-33) on the
+    device: the reference's KATs (test_ops.cpp:39-56, 69-76) and the oracle, unnormalised."""
+    ctx = R.Context(0)
+    x = orc.fill_gaussian(12, 23, 3)
+    g = R.ops.gaussian_gram(x, 1.3, ctx=ctx)
+    d2 = ((x[:, None, :] - x[None, :, :]) ** 2).sum(-1)
+    np.testing.assert_allclose(g, np.exp(-d2 / (2 * 1.3 * 1.3)), rtol=1e-12, atol=0)
+    p = R.ops.polynomial_gram(x, 3, 0.5, ctx=ctx)
+    np.testing.assert_allclose(p, (x @ x.T + 0.5) ** 3, rtol=1e-12, atol=0)
+    x = orc.fill_gaussian(13, 640, 5)
+    g = R.ops.gaussian_gram(x, 1.0, ctx=ctx)
+    assert np.array_equal(g, g.T) and np.all(np.diag(g) == 1.0)
+    np.testing.assert_allclose(g, orc.gaussian_gram(x, 1.0), rtol=1e-13, atol=1e-300)
+    p = R.ops.polynomial_gram(x, 2, 1.0, ctx=ctx)
+    assert np.array_equal(p, p.T)
+    np.testing.assert_allclose(p, orc.polynomial_gram(x, 2, 1.0), rtol=1e-12, atol=1e-12 * np.abs(p).max())
+    a, b = orc.fill_gaussian(1, 300, 7), orc.fill_gaussian(2, 300, 7)
+    assert np.array_equal(R.ops.hadamard_scaled(a, b, 2.5, ctx=ctx), 2.5 * (a * b))
