@@ -341,6 +341,11 @@ uint64_t renyi_hash_name(const char* name);                  /* rng.cpp:20-28 */
 int renyi_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out);
 int renyi_binomial_coeffs(double alpha, int m, double* out);                   /* poly.cpp:10-16 */
 int renyi_chebyshev_coeffs(double alpha, int m, double u, double v, double* out); /* poly.cpp:42-46 */
+/* chebyshev_node_coeffs(f, m, a, b) (poly.cpp:18-40) for a caller-supplied f: out has m + 1 entries */
+typedef double (*renyi_scalar_fn)(double x, void* user);
+int renyi_chebyshev_node_coeffs(renyi_scalar_fn f, void* user, int m, double a, double b, double* out);
+/* method_name (entropy.cpp:51-60): "exact", "int", "taylor", "chebyshev", "auto" ("?" otherwise) */
+const char* renyi_method_name(int method);
 double renyi_chebyshev_safeguard(double u, double v);                           /* poly.hpp:27-30 */
 double renyi_taylor_tail_constant(double alpha, int k_max);                     /* poly.cpp:48-58 */
 int renyi_matfun_scalar(const renyi_matfun* f, double lambda, double* out);     /* poly.cpp:166-168 */

@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -169,6 +170,24 @@ inline std::vector<double> matvec(const Context& ctx, const NormalizedKernel& a,
     check(renyi_matvec(ctx.get(), a.get(), x.data(), y.data()));
     return y;
 }
+// the unnormalised Grams and the scaled Hadamard product (ops.hpp:12-33); samples rows = samples
+inline Matrix gaussian_gram(const Context& ctx, const Matrix& samples, double sigma) {
+    Matrix k(samples.rows, samples.rows);
+    check(renyi_ops_gaussian_gram(ctx.get(), samples.data.data(), samples.rows, samples.cols, samples.rows, sigma,
+                                  k.data.data()));
+    return k;
+}
+inline Matrix polynomial_gram(const Context& ctx, const Matrix& samples, int degree, double offset) {
+    Matrix k(samples.rows, samples.rows);
+    check(renyi_ops_polynomial_gram(ctx.get(), samples.data.data(), samples.rows, samples.cols, samples.rows, degree,
+                                    offset, k.data.data()));
+    return k;
+}
+inline Matrix hadamard_scaled(const Context& ctx, const Matrix& a, const Matrix& b, double scale) {
+    Matrix c(a.rows, a.cols);
+    check(renyi_ops_hadamard_scaled(ctx.get(), a.data.data(), b.data.data(), a.rows, a.cols, scale, c.data.data()));
+    return c;
+}
 }  // namespace ops
 
 // MatrixFunctionSpec factories (proj/include/renyi/poly.hpp:54-70)
@@ -181,6 +200,15 @@ struct MatrixFunctionSpec {
     }
     int query_cost() const { return f.kind == RENYI_MATFUN_INT_POWER ? static_cast<int>(f.alpha) : f.degree; }
 };
+
+// chebyshev_node_coeffs (proj/src/poly.cpp:18-40) for any f
+inline std::vector<double> chebyshev_node_coeffs(const std::function<double(double)>& f, int m, double a, double b) {
+    std::vector<double> c(m > 0 ? m + 1 : 1);
+    auto tramp = [](double x, void* user) { return (*static_cast<const std::function<double(double)>*>(user))(x); };
+    check(renyi_chebyshev_node_coeffs(tramp, const_cast<void*>(static_cast<const void*>(&f)), m, a, b, c.data()));
+    return c;
+}
+inline std::string method_name(int method) { return renyi_method_name(method); }  // entropy.cpp:51-60
 
 inline Matrix apply_panel(const Context& ctx, const MatrixFunctionSpec& spec, const NormalizedKernel& a,
                           const Matrix& x) {  // poly.cpp:158-164

@@ -267,6 +267,8 @@ SIGNATURES = {
     "renyi_probe_panel": (C.c_int, [_I64, C.c_int, C.c_uint64, C.c_char_p, C.c_int, _D]),
     "renyi_binomial_coeffs": (C.c_int, [C.c_double, C.c_int, _D]),
     "renyi_chebyshev_coeffs": (C.c_int, [C.c_double, C.c_int, C.c_double, C.c_double, _D]),
+    "renyi_chebyshev_node_coeffs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, _D]),
+    "renyi_method_name": (C.c_char_p, [C.c_int]),
     "renyi_chebyshev_safeguard": (C.c_double, [C.c_double, C.c_double]),
     "renyi_taylor_tail_constant": (C.c_double, [C.c_double, C.c_int]),
     "renyi_matfun_scalar": (C.c_int, [C.POINTER(Matfun), C.c_double, _D]),

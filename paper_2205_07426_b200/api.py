@@ -361,6 +361,23 @@ def chebyshev_coeffs(alpha: float, m: int, u: float, v: float) -> np.ndarray:
     return out
 
 
+_SCALAR_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
+
+
+def chebyshev_node_coeffs(f, m: int, a: float, b: float) -> np.ndarray:
+    """Chebyshev coefficients of f on [a, b] from the m + 1 first-kind nodes (proj/src/poly.cpp:18-40)."""
+    out = np.empty(max(m + 1, 1))
+    cb = _SCALAR_FN(lambda x, _user: float(f(x)))
+    check(L.lib().renyi_chebyshev_node_coeffs(C.cast(cb, C.c_void_p), None, m, a, b, _dptr(out)))
+    return out
+
+
+def method_name(method) -> str:
+    """method_name (proj/src/entropy.cpp:51-60)."""
+    code = METHODS[method] if isinstance(method, str) else int(method)
+    return L.lib().renyi_method_name(code).decode()
+
+
 def chebyshev_safeguard(u: float, v: float) -> float:
     return L.lib().renyi_chebyshev_safeguard(u, v)
 

@@ -843,6 +843,25 @@ int renyi_chebyshev_coeffs(double alpha, int m, double u, double v, double* out)
     });
 }
 
+int renyi_chebyshev_node_coeffs(renyi_scalar_fn f, void* user, int m, double a, double b, double* out) {
+    return guarded([&] {
+        need(reinterpret_cast<const void*>(f), "f"), need(out, "out");
+        const auto c = rb::chebyshev_node_coeffs([&](double x) { return f(x, user); }, m, a, b);
+        std::copy(c.begin(), c.end(), out);
+    });
+}
+
+const char* renyi_method_name(int method) {
+    switch (method) {
+        case RENYI_METHOD_EXACT: return "exact";
+        case RENYI_METHOD_INT: return "int";
+        case RENYI_METHOD_TAYLOR: return "taylor";
+        case RENYI_METHOD_CHEBYSHEV: return "chebyshev";
+        case RENYI_METHOD_AUTO: return "auto";
+        default: return "?";
+    }
+}
+
 double renyi_chebyshev_safeguard(double u, double v) { return rb::chebyshev_safeguard(u, v); }
 double renyi_taylor_tail_constant(double alpha, int k_max) { return rb::taylor_tail_constant(alpha, k_max); }
 

@@ -89,13 +89,18 @@ std::vector<double> binomial_coeffs(double alpha, int m) {  // proj/src/poly.cpp
 // chebyshev_node_coeffs + chebyshev_coeffs for f = lambda^alpha (proj/src/poly.cpp:18-46)
 std::vector<double> chebyshev_power_coeffs(double alpha, int m, double a, double b) {
     if (a < 0.0 || b <= a) fail(kDomainError, "chebyshev_coeffs needs 0 <= u < v");
+    return chebyshev_node_coeffs([alpha](double lam) { return std::pow(lam, alpha); }, m, a, b);
+}
+
+// chebyshev_node_coeffs (proj/src/poly.cpp:18-40): c_k = (2/(m+1)) Σ_i f(g(x_i)) T_k(x_i)
+std::vector<double> chebyshev_node_coeffs(const std::function<double(double)>& f, int m, double a, double b) {
     if (m < 1) fail(kInvalidArgument, "chebyshev_node_coeffs needs m >= 1");
     const int n_nodes = m + 1;
     std::vector<double> c(m + 1, 0.0);
     for (int i = 0; i < n_nodes; ++i) {
         const double theta = std::numbers::pi * (i + 0.5) / n_nodes;
         const double x = std::cos(theta);
-        const double fx = std::pow(a + 0.5 * (b - a) * (x + 1.0), alpha);
+        const double fx = f(a + 0.5 * (b - a) * (x + 1.0));
         double t_prev = 1.0, t_cur = x;
         c[0] += fx;
         if (m >= 1) c[1] += fx * x;

@@ -5,6 +5,7 @@
 // reference routine it restates.
 #pragma once
 
+#include <functional>
 #include <cstdint>
 #include <limits>
 #include <stdexcept>
@@ -77,6 +78,7 @@ void probe_column(uint64_t base, int j, int64_t n, int kind, double* col);
 
 // ---- polynomial coefficients: proj/src/poly.cpp:10-58 ----------------------
 std::vector<double> binomial_coeffs(double alpha, int m);
+std::vector<double> chebyshev_node_coeffs(const std::function<double(double)>& f, int m, double a, double b);
 std::vector<double> chebyshev_power_coeffs(double alpha, int m, double a, double b);
 double taylor_tail_constant(double alpha, int k_max = 10000);
 double chebyshev_safeguard(double u, double v);

@@ -68,6 +68,18 @@ def test_coefficients_match_oracle(R, orc):
             assert R.scalar_value(spec, lam) == pytest.approx(orc.scalar_value(ospec, lam), rel=1e-14)
 
 
+def test_chebyshev_node_coeffs_and_method_name(R, orc):  # test_poly.cpp:58-64, entropy.cpp:51-60
+    c = R.chebyshev_node_coeffs(lambda x: x, 1, 0.0, 1.0)  # f = lambda on [0, 1]: c0 = 1, c1 = 1/2
+    assert c[0] == pytest.approx(1.0, abs=1e-15) and c[1] == pytest.approx(0.5, abs=1e-15)
+    for alpha, m, u, v in ((1.5, 40, 0.0, 1.0), (1.01, 60, 0.0, 1.0), (2.5, 30, 0.05, 0.6)):
+        np.testing.assert_array_equal(R.chebyshev_node_coeffs(lambda x: x ** alpha, m, u, v),
+                                      R.chebyshev_coeffs(alpha, m, u, v))
+    with pytest.raises(R.RenyiError):
+        R.chebyshev_node_coeffs(math.exp, 0, 0.0, 1.0)
+    assert [R.method_name(k) for k in range(5)] == ["exact", "int", "taylor", "chebyshev", "auto"]
+    assert R.method_name("chebyshev") == "chebyshev" and R.method_name(9) == "?"
+
+
 def test_expected_queries(R):  # test_hutchpp.cpp:74-78
     assert R.expected_queries(R.MatrixFunctionSpec.int_power(2), R.SketchConfig(8)) == 22
     assert R.expected_queries(R.MatrixFunctionSpec.taylor(0.5, 15, 1.0), R.SketchConfig(8)) == 100
