@@ -339,6 +339,17 @@ uint64_t renyi_derive_key(uint64_t seed, uint64_t tag);      /* rng.cpp:16-18 */
 uint64_t renyi_hash_name(const char* name);                  /* rng.cpp:20-28 */
 /* detail::gaussian_panel (hutchpp.cpp:13-22); kind RENYI_PROBE_RADEMACHER = sign of the top bit */
 int renyi_probe_panel(int64_t n, int cols, uint64_t seed, const char* label, int kind, double* out);
+/* RandomStream (proj/include/renyi/rng.hpp:12-36, rng.cpp:30-64): counter-based splitmix stream,
+ * Box-Muller normals with the spare, column-wise fills (prefix-stable in the column count) */
+typedef struct renyi_rng renyi_rng;
+int renyi_rng_create(uint64_t key, renyi_rng** out);
+int renyi_rng_destroy(renyi_rng* r);
+int renyi_rng_derive(const renyi_rng* r, uint64_t tag, renyi_rng** out);
+uint64_t renyi_rng_key(const renyi_rng* r);
+uint64_t renyi_rng_next_u64(renyi_rng* r);
+double renyi_rng_next_uniform(renyi_rng* r);
+double renyi_rng_next_gaussian(renyi_rng* r);
+int renyi_rng_fill_gaussian(renyi_rng* r, int64_t rows, int64_t cols, double* out); /* column-major */
 int renyi_binomial_coeffs(double alpha, int m, double* out);                   /* poly.cpp:10-16 */
 int renyi_chebyshev_coeffs(double alpha, int m, double u, double v, double* out); /* poly.cpp:42-46 */
 /* chebyshev_node_coeffs(f, m, a, b) (poly.cpp:18-40) for a caller-supplied f: out has m + 1 entries */

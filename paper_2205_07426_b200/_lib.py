@@ -267,6 +267,14 @@ SIGNATURES = {
     "renyi_probe_panel": (C.c_int, [_I64, C.c_int, C.c_uint64, C.c_char_p, C.c_int, _D]),
     "renyi_binomial_coeffs": (C.c_int, [C.c_double, C.c_int, _D]),
     "renyi_chebyshev_coeffs": (C.c_int, [C.c_double, C.c_int, C.c_double, C.c_double, _D]),
+    "renyi_rng_create": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
+    "renyi_rng_destroy": (C.c_int, [_P]),
+    "renyi_rng_derive": (C.c_int, [_P, C.c_uint64, C.POINTER(_P)]),
+    "renyi_rng_key": (C.c_uint64, [_P]),
+    "renyi_rng_next_u64": (C.c_uint64, [_P]),
+    "renyi_rng_next_uniform": (C.c_double, [_P]),
+    "renyi_rng_next_gaussian": (C.c_double, [_P]),
+    "renyi_rng_fill_gaussian": (C.c_int, [_P, _I64, _I64, _D]),
     "renyi_chebyshev_node_coeffs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, _D]),
     "renyi_method_name": (C.c_char_p, [C.c_int]),
     "renyi_chebyshev_safeguard": (C.c_double, [C.c_double, C.c_double]),

@@ -364,6 +364,47 @@ def chebyshev_coeffs(alpha: float, m: int, u: float, v: float) -> np.ndarray:
 _SCALAR_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
 
 
+class RandomStream:
+    """RandomStream (proj/include/renyi/rng.hpp:12-36): the reference's host stream, bit for bit."""
+
+    def __init__(self, key: int = 0, _handle=None):
+        self._h = _handle
+        if self._h is None:
+            self._h = C.c_void_p()
+            check(L.lib().renyi_rng_create(int(key) & (2**64 - 1), C.byref(self._h)))
+
+    def derive(self, tag: int) -> "RandomStream":
+        h = C.c_void_p()
+        check(L.lib().renyi_rng_derive(self._h, int(tag) & (2**64 - 1), C.byref(h)))
+        return RandomStream(_handle=h)
+
+    def key(self) -> int:
+        return int(L.lib().renyi_rng_key(self._h))
+
+    def next_u64(self) -> int:
+        return int(L.lib().renyi_rng_next_u64(self._h))
+
+    def next_uniform(self) -> float:
+        return float(L.lib().renyi_rng_next_uniform(self._h))
+
+    def next_gaussian(self) -> float:
+        return float(L.lib().renyi_rng_next_gaussian(self._h))
+
+    def fill_gaussian(self, rows: int, cols: int = 1) -> np.ndarray:
+        """A rows x cols panel filled column-wise (rng.cpp:60-64)."""
+        out = np.empty((rows, cols), order="F")
+        check(L.lib().renyi_rng_fill_gaussian(self._h, rows, cols, _dptr(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if self._h:
+                L.lib().renyi_rng_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
 def chebyshev_node_coeffs(f, m: int, a: float, b: float) -> np.ndarray:
     """Chebyshev coefficients of f on [a, b] from the m + 1 first-kind nodes (proj/src/poly.cpp:18-40)."""
     out = np.empty(max(m + 1, 1))

@@ -843,6 +843,39 @@ int renyi_chebyshev_coeffs(double alpha, int m, double u, double v, double* out)
     });
 }
 
+struct renyi_rng {
+    rb::RandomStream s;
+};
+
+int renyi_rng_create(uint64_t key, renyi_rng** out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = new renyi_rng{rb::RandomStream(key)};
+    });
+}
+int renyi_rng_destroy(renyi_rng* r) {
+    delete r;
+    return 0;
+}
+int renyi_rng_derive(const renyi_rng* r, uint64_t tag, renyi_rng** out) {
+    return guarded([&] {
+        need(r, "rng"), need(out, "out");
+        *out = new renyi_rng{r->s.derive(tag)};
+    });
+}
+uint64_t renyi_rng_key(const renyi_rng* r) { return r ? r->s.key() : 0; }
+uint64_t renyi_rng_next_u64(renyi_rng* r) { return r ? r->s.next_u64() : 0; }
+double renyi_rng_next_uniform(renyi_rng* r) { return r ? r->s.next_uniform() : 0.0; }
+double renyi_rng_next_gaussian(renyi_rng* r) { return r ? r->s.next_gaussian() : 0.0; }
+int renyi_rng_fill_gaussian(renyi_rng* r, int64_t rows, int64_t cols, double* out) {
+    return guarded([&] {
+        need(r, "rng"), need(out, "out");
+        if (rows < 0 || cols < 0) rb::fail(rb::kInvalidArgument, "fill sizes must be non-negative");
+        for (int64_t j = 0; j < cols; ++j)  // rng.cpp:60-64: column-wise
+            for (int64_t i = 0; i < rows; ++i) out[i + j * rows] = r->s.next_gaussian();
+    });
+}
+
 int renyi_chebyshev_node_coeffs(renyi_scalar_fn f, void* user, int m, double a, double b, double* out) {
     return guarded([&] {
         need(reinterpret_cast<const void*>(f), "f"), need(out, "out");

@@ -58,6 +58,8 @@ public:
     double next_uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
     double next_gaussian();
     double next_rademacher() { return (next_u64() >> 63) ? -1.0 : 1.0; }
+    RandomStream derive(uint64_t tag) const { return RandomStream(derive_key(key_, tag)); }  // rng.cpp:30-32
+    uint64_t key() const { return key_; }
 
 private:
     uint64_t key_;

@@ -80,6 +80,20 @@ def test_chebyshev_node_coeffs_and_method_name(R, orc):  # test_poly.cpp:58-64, 
     assert R.method_name("chebyshev") == "chebyshev" and R.method_name(9) == "?"
 
 
+def test_random_stream_bitwise(R, orc):  # rng.hpp:12-36 against the oracle's restatement
+    key = orc.derive_key(7, orc.hash_name("X"))
+    s = R.RandomStream(key)
+    np.testing.assert_array_equal(s.fill_gaussian(500, 3), orc.fill_gaussian(key, 500, 3))
+    t = R.RandomStream(11)
+    d = t.derive(5)
+    assert d.key() == orc.derive_key(11, 5)
+    u = [t.next_u64() for _ in range(3)]
+    assert u[0] != u[1] and all(0 <= v < 2**64 for v in u)
+    assert 0.0 <= t.next_uniform() < 1.0
+    g1, g2 = R.RandomStream(3).next_gaussian(), R.RandomStream(3).fill_gaussian(2, 1)[:, 0]
+    assert g1 == g2[0]
+
+
 def test_expected_queries(R):  # test_hutchpp.cpp:74-78
     assert R.expected_queries(R.MatrixFunctionSpec.int_power(2), R.SketchConfig(8)) == 22
     assert R.expected_queries(R.MatrixFunctionSpec.taylor(0.5, 15, 1.0), R.SketchConfig(8)) == 100
