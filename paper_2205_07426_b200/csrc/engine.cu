@@ -1361,10 +1361,18 @@ PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, d
     ctx.x0.ensure(static_cast<size_t>(ld) * sizeof(double));
     cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
     const uint64_t key = derive_key(o.seed, hash_name("power-start"));
-    launched(ctx,
-             launch_rng_panel(key, false, kProbeGaussian, k.row0, k.rows, 1, 0, ctx.x0.as<double>(), ld,
-                              ctx.probe_err.as<int>(), ctx.stream()),
-             "rng_panel");
+    if (ctx.probe_source == 1) {  // seeded_start (spectrum.cpp:13-21) with the reference's own draws
+        std::vector<double> v(static_cast<size_t>(k.n));
+        RandomStream rs(key);
+        for (double& e : v) e = rs.next_gaussian();
+        h2d(ctx, ctx.x0.as<double>(), v.data() + k.row0, static_cast<size_t>(k.rows) * sizeof(double));
+        ctx.sync();  // v is pageable host memory owned by this frame
+    } else {
+        launched(ctx,
+                 launch_rng_panel(key, false, kProbeGaussian, k.row0, k.rows, 1, 0, ctx.x0.as<double>(), ld,
+                                  ctx.probe_err.as<int>(), ctx.stream()),
+                 "rng_panel");
+    }
     PowerRes res;
     const int iters = std::max(o.max_iters, 0);
     PanelSession ps(ctx, k, ctx.x0.as<double>(), ld, 1, std::max(iters, 1), nullptr, 0.0, false);
@@ -2582,10 +2590,16 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
         DevBuf one;
         one.alloc(static_cast<size_t>(cols) * n * sizeof(double));
         cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
-        launched(ctx,
-                 launch_rng_panel(derive_key(cfg.seed, hash_name(label)), true, cfg.probe_kind, 0, n, cols, 0,
-                                  one.as<double>(), n, ctx.probe_err.as<int>(), ctx.stream()),
-                 "rng_panel");
+        if (ctx.probe_source == 1 && cfg.probe_kind == kProbeGaussian) {  // the reference's draws (host)
+            const auto v = ctx.take_probes(n, cols, cfg.seed, label, cfg.probe_kind);
+            h2d(ctx, one.as<double>(), v->data(), v->size() * sizeof(double));
+            ctx.sync();
+        } else {
+            launched(ctx,
+                     launch_rng_panel(derive_key(cfg.seed, hash_name(label)), true, cfg.probe_kind, 0, n, cols, 0,
+                                      one.as<double>(), n, ctx.probe_err.as<int>(), ctx.stream()),
+                     "rng_panel");
+        }
         dst.alloc(static_cast<size_t>(cols) * ld * sizeof(double));
         cuda_check(cudaMemsetAsync(dst.as<void>(), 0, static_cast<size_t>(cols) * ld * sizeof(double), ctx.stream()),
                    "memset");

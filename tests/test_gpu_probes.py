@@ -60,3 +60,18 @@ def test_probe_source_rejects_unknown(R):
     ctx = R.Context(0)
     with pytest.raises(ValueError):
         ctx.set_probe_source("gpu")
+
+
+def test_host_power_start_matches_oracle(R, orc):
+    """seeded_start (spectrum.cpp:13-21) drawn on the host: the fp64 power iteration then follows the
+    oracle's to rounding and stops at the same iteration."""
+    n = 1800
+    x = orc.fill_gaussian(77, n, 5)
+    a = orc.build_kernel(x, math.sqrt(5.0))
+    ref = orc.estimate_bounds(a, seed=4)
+    ctx = R.Context(0)
+    ctx.set_probe_source("host")
+    k = R.build_kernel(x, R.GaussianKernel(math.sqrt(5.0)), "fp64", ctx=ctx)
+    b = R.estimate_bounds(k, R.PowerOptions(seed=4))
+    assert b.iterations_used == ref["iterations_used"]
+    assert b.v == pytest.approx(ref["v"], rel=1e-12) and b.u == pytest.approx(ref["u"], rel=1e-9, abs=1e-15)
