@@ -280,6 +280,7 @@ Context::Context(int device) : device_(device) {
     sms_ = prop.multiProcessorCount;
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     probe_err.alloc(sizeof(int));
+    cuda_check(cudaMemsetAsync(probe_err.as<int>(), 0, sizeof(int), stream_), "memset");
 }
 
 cudaStream_t Context::comm_stream() {
@@ -877,6 +878,15 @@ bool split_operand(const Context& ctx, bool vectors_out) {
     return ctx.operand_mode == 0 || (ctx.operand_mode == 2 && vectors_out);
 }
 
+// a seeded Gaussian probe panel drawn on the device hit the reference's redraw branch (u1 <= 0,
+// p = 2^-53 per pair, rng.cpp:47): the device draws cannot follow it, so the estimate is refused
+void check_probe_err(Context& ctx, int err) {
+    if (!err) return;
+    cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream());
+    ctx.sync();
+    fail(kInternal, "probe stream hit the 2^-53 Box-Muller redraw; pass the probes explicitly");
+}
+
 class PanelSession {
 public:
     // ws: the session's buffers (default ctx.ws); tri: the panel is one operand of a fused
@@ -1143,7 +1153,10 @@ public:
         if (ctx_.exchange) ctx_.exchange->allreduce_sum_f64(w_.red.as<double>(), np * 3 * s, ctx_.stream());
         std::vector<double> out(static_cast<size_t>(np) * 3 * s);
         d2h(ctx_, out.data(), w_.red.as<double>(), out.size() * sizeof(double));
+        int err = 0;
+        d2h(ctx_, &err, ctx_.probe_err.as<int>(), sizeof(int));
         ctx_.sync();
+        check_probe_err(ctx_, err);
         return out;
     }
 
@@ -1160,7 +1173,10 @@ public:
                      "reduce_stats");
         std::vector<double> out(groups * per);
         d2h(ctx_, out.data(), w_.red.as<double>(), out.size() * sizeof(double));
+        int err = 0;
+        d2h(ctx_, &err, ctx_.probe_err.as<int>(), sizeof(int));
         ctx_.sync();
+        check_probe_err(ctx_, err);
         return out;
     }
     int rows_per_block() const { return plan_.rows_per_block; }
@@ -1359,7 +1375,6 @@ PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, d
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     const int64_t ld = k.rpr;  // local rows of the start vector (row-sharded: counters from row0)
     ctx.x0.ensure(static_cast<size_t>(ld) * sizeof(double));
-    cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
     const uint64_t key = derive_key(o.seed, hash_name("power-start"));
     if (ctx.probe_source == 1) {  // seeded_start (spectrum.cpp:13-21) with the reference's own draws
         std::vector<double> v(static_cast<size_t>(k.n));
@@ -1448,15 +1463,12 @@ void make_probes(Context& ctx, const KernelMatrix& k, DevBuf& dst, int cols, int
         ctx.sync();  // v is pageable host memory owned by this frame
         return;
     }
-    cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
+    // no round trip here: a (p = 2^-53) Box-Muller redraw raises ctx.probe_err, which every pass
+    // session reads back with its trace partials (check_probe_err) before any result leaves
     launched(ctx,
              launch_rng_panel(derive_key(seed, hash_name(label)), true, kind, k.row0, k.rows, cols, 0,
                               dst.as<double>(), ld, ctx.probe_err.as<int>(), ctx.stream()),
              "rng_panel");
-    int err = 0;
-    d2h(ctx, &err, ctx.probe_err.as<int>(), sizeof(int));
-    ctx.sync();
-    if (err) fail(kInternal, "probe stream hit the 2^-53 Box-Muller redraw; pass the probes explicitly");
 }
 
 std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx, const double* z, int q,
@@ -2589,7 +2601,6 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
     auto replicate = [&](DevBuf& dst, int cols, const char* label) {
         DevBuf one;
         one.alloc(static_cast<size_t>(cols) * n * sizeof(double));
-        cuda_check(cudaMemsetAsync(ctx.probe_err.as<int>(), 0, sizeof(int), ctx.stream()), "memset");
         if (ctx.probe_source == 1 && cfg.probe_kind == kProbeGaussian) {  // the reference's draws (host)
             const auto v = ctx.take_probes(n, cols, cfg.seed, label, cfg.probe_kind);
             h2d(ctx, one.as<double>(), v->data(), v->size() * sizeof(double));
@@ -2608,10 +2619,7 @@ std::vector<TraceEst> hutchpp_group(Context& ctx, const KernelMatrix& k, int cou
                                          n * sizeof(double), n * sizeof(double), cols, cudaMemcpyDeviceToDevice,
                                          ctx.stream()),
                        "replicate probes");
-        int err = 0;
-        d2h(ctx, &err, ctx.probe_err.as<int>(), sizeof(int));
-        ctx.sync();
-        if (err) fail(kInternal, "probe stream hit the 2^-53 Box-Muller redraw; pass the probes explicitly");
+        ctx.sync();  // `one` is released at scope end; probe_err is read with the trace partials
     };
     // sketch products of every group in one pass: Y = A·S
     DevBuf sk, y;
