@@ -152,3 +152,24 @@ def test_nccl_transport_single_rank(R):
     assert ctx.rank_world() == (0, 1)
     got = R.mutual_information_samples(x, sx, y, sy, p, "fp32", ctx)
     assert got.value == ref.value and got.joint_entropy == ref.joint_entropy
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_polynomial_kernel_estimate(R, orc, world):
+    """The polynomial kernel (kernel.cpp:35-72, ops.cpp:22-28) built row-sharded: each rank computes the
+    whole diagonal (normalisation) and its own rows; the Hutch++ estimate over the shards equals the
+    single-rank one to the fp32 sharding tolerance and the oracle to the fp32 contract."""
+    n = 2600
+    x = orc.fill_gaussian(44, n, 5)
+    p = R.EstimatorParams(alpha=2.5, method="chebyshev", s=40, m=30, seed=3, bounds=R.SpectrumBounds(u=0, v=1))
+    ref = orc.estimate(orc.build_kernel_polynomial(x, 2, 1.0), alpha=2.5, method="chebyshev", s=40, m=30, seed=3,
+                       bounds=(0.0, 1.0))
+    one = R.estimate(R.build_kernel(x, R.PolynomialKernel(2, 1.0), "fp32", ctx=R.Context(0)), p).entropy
+
+    def fn(ctx, rank):
+        return R.estimate(R.build_kernel(x, R.PolynomialKernel(2, 1.0), "fp32", ctx=ctx), p).entropy
+
+    got = run_ranks(R, world, fn)
+    assert all(g == got[0] for g in got)
+    assert got[0] == pytest.approx(one, rel=2e-5)
+    assert got[0] == pytest.approx(ref["entropy"], rel=1e-4)
