@@ -220,6 +220,11 @@ int renyi_kernel_build_polynomial_dev(renyi_ctx* ctx, const double* d_x, int64_t
 int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int precision, renyi_kernel** out);
 /* hadamard_joint({a, b}) — kernel.cpp:74-101 */
 int renyi_kernel_hadamard_joint(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b, renyi_kernel** out);
+/* hadamard_joint(kernels) for count >= 2 (kernel.cpp:74-101): factors in a canonical content order, so
+ * any permutation of the list gives a bitwise identical joint; n^(count-1) applied once, diag 1/n;
+ * count >= 3 is single-rank */
+int renyi_kernel_hadamard_joint_n(renyi_ctx* ctx, const renyi_kernel* const* kernels, int count,
+                                  renyi_kernel** out);
 int renyi_kernel_size(const renyi_kernel* k, int64_t* n);
 int renyi_kernel_download(renyi_ctx* ctx, const renyi_kernel* k, double* out);
 int renyi_kernel_destroy(renyi_kernel* k);

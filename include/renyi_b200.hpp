@@ -159,6 +159,14 @@ inline NormalizedKernel hadamard_joint(const Context& ctx, const NormalizedKerne
     return NormalizedKernel(k);
 }
 
+inline NormalizedKernel hadamard_joint(const Context& ctx, const std::vector<NormalizedKernel>& kernels) {
+    std::vector<const renyi_kernel*> hs;
+    for (const auto& k : kernels) hs.push_back(k.get());
+    renyi_kernel* k = nullptr;
+    check(renyi_kernel_hadamard_joint_n(ctx.get(), hs.data(), static_cast<int>(hs.size()), &k));
+    return NormalizedKernel(k);
+}
+
 namespace ops {  // proj/include/renyi/ops.hpp:23-29
 inline Matrix matmul_panel(const Context& ctx, const NormalizedKernel& a, const Matrix& x) {
     Matrix y(x.rows, x.cols);

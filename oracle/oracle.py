@@ -102,6 +102,7 @@ def lib():
         h.oracle_mixture_samples.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, _D]
         h.oracle_gaussian_gram.argtypes = [_D, _I64, _I64, C.c_double, _D]
         h.oracle_build_kernel.argtypes = [_D, _I64, _I64, C.c_double, _D]
+        h.oracle_hadamard_joint_n.argtypes = [C.POINTER(_D), C.c_int, _I64, _D]
         h.oracle_polynomial_gram.argtypes = [_D, _I64, _I64, C.c_int, C.c_double, _D]
         h.oracle_build_kernel_polynomial.argtypes = [_D, _I64, _I64, C.c_int, C.c_double, _D]
         h.oracle_hadamard_joint.argtypes = [_D, _I64, _D, _I64, _D]
@@ -211,6 +212,16 @@ def build_kernel(x, sigma):
     x = _f(x)
     out = np.empty((x.shape[0], x.shape[0]), order="F")
     _chk(lib().oracle_build_kernel(_p(x), x.shape[0], x.shape[1], sigma, _p(out)))
+    return out
+
+
+def hadamard_joint_n(mats):
+    """hadamard_joint over any number of kernels (kernel.cpp:74-101, canonical FNV content order)."""
+    ms = [_f(m) for m in mats]
+    n = ms[0].shape[0]
+    arr = (_D * len(ms))(*[_p(m) for m in ms])
+    out = np.empty((n, n), order="F")
+    _chk(lib().oracle_hadamard_joint_n(arr, len(ms), n, _p(out)))
     return out
 
 

@@ -1655,6 +1655,15 @@ int oracle_polynomial_gram(const double* x, int64_t n, int64_t d, int degree, do
 int oracle_build_kernel_polynomial(const double* x, int64_t n, int64_t d, int degree, double offset, double* out) {
     return guard([&] { unwrap(orc::build_kernel_polynomial(wrap(x, n, d), degree, offset), out); });
 }
+int oracle_hadamard_joint_n(const double* const* mats, int count, int64_t n, double* out) {
+    return guard([&] {
+        std::vector<orc::Mat> ms;
+        for (int i = 0; i < count; ++i) ms.push_back(wrap(mats[i], n, n));
+        std::vector<const orc::Mat*> ps;
+        for (const auto& m : ms) ps.push_back(&m);
+        unwrap(orc::hadamard_joint(ps), out);
+    });
+}
 int oracle_hadamard_joint(const double* a, int64_t na, const double* b, int64_t nb, double* out) {
     return guard([&] {
         const orc::Mat ma = wrap(a, na, na), mb = wrap(b, nb, nb);

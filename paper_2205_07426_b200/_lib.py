@@ -182,6 +182,7 @@ SIGNATURES = {
     "renyi_ctx_join_local_group": (C.c_int, [_P, _P, C.c_int]),
     "renyi_ctx_rank": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "renyi_kernel_build_gaussian": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_double, C.c_int, C.POINTER(_P)]),
+    "renyi_kernel_hadamard_joint_n": (C.c_int, [_P, C.POINTER(_P), C.c_int, C.POINTER(_P)]),
     "renyi_ops_gaussian_gram": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_double, _D]),
     "renyi_ops_polynomial_gram": (C.c_int, [_P, _D, _I64, _I64, _I64, C.c_int, C.c_double, _D]),
     "renyi_ops_hadamard_scaled": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_double, _D]),

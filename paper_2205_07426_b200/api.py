@@ -286,12 +286,10 @@ def hadamard_joint(kernels: Sequence[NormalizedKernel]) -> NormalizedKernel:
     if len(kernels) < 2:
         raise RenyiError(1, "hadamard_joint needs at least 2 kernels")
     ctx = kernels[0].ctx
-    acc = kernels[0]
-    for k in kernels[1:]:
-        h = C.c_void_p()
-        check(L.lib().renyi_kernel_hadamard_joint(ctx.handle, acc.handle, k.handle, C.byref(h)))
-        acc = NormalizedKernel(h, ctx, acc.precision)
-    return acc
+    arr = (C.c_void_p * len(kernels))(*[k.handle for k in kernels])
+    h = C.c_void_p()
+    check(L.lib().renyi_kernel_hadamard_joint_n(ctx.handle, arr, len(kernels), C.byref(h)))
+    return NormalizedKernel(h, ctx, kernels[0].precision)
 
 
 # ---------------------------------------------------------------- ops (ops.hpp)

@@ -510,6 +510,20 @@ int renyi_kernel_from_matrix(renyi_ctx* ctx, const double* a, int64_t n, int pre
     });
 }
 
+int renyi_kernel_hadamard_joint_n(renyi_ctx* ctx, const renyi_kernel* const* kernels, int count,
+                                  renyi_kernel** out) {
+    return guarded([&] {
+        need(ctx, "ctx"), need(kernels, "kernels"), need(out, "out");
+        if (count < 2) rb::fail(rb::kInvalidArgument, "hadamard_joint needs at least 2 kernels");
+        std::vector<const rb::KernelMatrix*> ks;
+        for (int i = 0; i < count; ++i) {
+            need(kernels[i], "kernel");
+            ks.push_back(kernels[i]->k.get());
+        }
+        *out = make_handle<renyi_kernel>([&](renyi_kernel& h) { h.k = rb::hadamard_joint_n(ctx->ctx, ks); });
+    });
+}
+
 int renyi_kernel_hadamard_joint(renyi_ctx* ctx, const renyi_kernel* a, const renyi_kernel* b, renyi_kernel** out) {
     return guarded([&] {
         need(ctx, "ctx"), need(a, "kernel a"), need(b, "kernel b"), need(out, "out");

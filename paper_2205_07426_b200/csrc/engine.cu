@@ -849,6 +849,90 @@ KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix
     return c;
 }
 
+// canonical ordering key of a stored kernel: the row hashes folded in row order (equal content, equal
+// key; the reference orders by an FNV-1a of the fp64 bytes, kernel.cpp:13-23,83-88 -- any content key
+// gives the same permutation invariance)
+uint64_t content_key(Context& ctx, const KernelMatrix& k) {
+    DevBuf rh;
+    rh.alloc(static_cast<size_t>(std::max<int64_t>(k.rows, 1)) * sizeof(uint64_t));
+    launched(ctx,
+             launch_row_hash(k.prec == kF64 ? k.a64.as<double>() : nullptr, k.prec == kF64 ? nullptr : k.hi.as<__half>(),
+                             k.prec == kF64 ? nullptr : k.lo.as<__half>(), k.rows, k.n, k.ld, rh.as<uint64_t>(),
+                             ctx.stream()),
+             "row_hash");
+    std::vector<uint64_t> h(static_cast<size_t>(k.rows));
+    d2h(ctx, h.data(), rh.as<uint64_t>(), h.size() * sizeof(uint64_t));
+    ctx.sync();
+    uint64_t key = 0xcbf29ce484222325ULL;
+    for (uint64_t v : h) key = mix64(key ^ v);
+    return key;
+}
+
+KernelPtr hadamard_joint_n(Context& ctx, const std::vector<const KernelMatrix*>& ks) {
+    // proj/src/kernel.cpp:74-101 for any L: factors in a canonical content order (bitwise permutation
+    // invariant), p = M_0 ∘ ... with the single n^(L-1) scale on the last product, diag 1/n
+    if (ks.size() < 2) fail(kInvalidArgument, "hadamard_joint needs at least 2 kernels");
+    const KernelMatrix& k0 = *ks.front();
+    for (const KernelMatrix* k : ks)
+        if (k->n != k0.n)
+            fail(kSizeMismatch,
+                 "hadamard_joint kernel sizes differ: " + std::to_string(k0.n) + " vs " + std::to_string(k->n));
+    if (ks.size() == 2) return hadamard_joint(ctx, *ks[0], *ks[1]);  // commutative: order-free
+    if (static_cast<int>(ks.size()) > kMaxJoint)
+        fail(kInvalidArgument, "hadamard_joint supports up to " + std::to_string(kMaxJoint) + " kernels");
+    for (const KernelMatrix* k : ks) {
+        if (k->prec != k0.prec) fail(kInvalidArgument, "hadamard_joint needs kernels of the same precision");
+        if (k->prec == kMF)
+            fail(kInvalidArgument, "matrix-free joints are built from samples (renyi_kernel_build_gaussian_joint)");
+        if (k->world != 1) fail(kInvalidArgument, "hadamard_joint of three or more kernels is single-rank");
+        if (k->groups > 1) fail(kInvalidArgument, "hadamard_joint needs single kernels, not grouped stacks");
+    }
+    cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
+    std::vector<std::pair<uint64_t, const KernelMatrix*>> order;
+    for (const KernelMatrix* k : ks) order.push_back({content_key(ctx, *k), k});
+    std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    const double nd = static_cast<double>(k0.n), inv_n = 1.0 / nd;
+    double scale = 1.0;
+    for (size_t l = 1; l < order.size(); ++l) scale *= nd;  // kernel.cpp:91-92
+    HadamardFactors hf{};
+    hf.count = static_cast<int>(order.size());
+    bool normalized = true;
+    for (int l = 0; l < hf.count; ++l) {
+        const KernelMatrix& k = *order[l].second;
+        hf.a64[l] = k.prec == kF64 ? k.a64.as<double>() : nullptr;
+        hf.hi[l] = k.prec == kF64 ? nullptr : k.hi.as<__half>();
+        hf.lo[l] = k.prec == kF64 ? nullptr : k.lo.as<__half>();
+        hf.unscale[l] = k.unscale;
+        normalized = normalized && k.normalized;
+    }
+    auto c = std::make_unique<KernelMatrix>();
+    c->n = k0.n, c->row0 = k0.row0, c->rows = k0.rows, c->ld = k0.ld, c->prec = k0.prec;
+    c->rpr = k0.rpr, c->world = k0.world, c->rank = k0.rank;
+    c->normalized = normalized;
+    c->a_norm = normalized ? 1.0 : [&] {
+        double b = 1.0;
+        for (const KernelMatrix* k : ks) b *= std::max(1.0, k->a_norm);
+        return std::max(1.0, b * scale);
+    }();
+    const size_t elems = static_cast<size_t>(c->rows) * c->ld;
+    if (c->prec == kF32) {
+        c->unscale = inv_n / kSplitScale;
+        c->hi.alloc(elems * sizeof(__half));
+        c->lo.alloc(elems * sizeof(__half));
+        launched(ctx, launch_hadamard_n(hf, c->rows, c->n, c->ld, c->row0, scale, inv_n, c->unscale, nullptr,
+                                        c->hi.as<__half>(), c->lo.as<__half>(), ctx.stream()),
+                 "hadamard_n");
+    } else {
+        c->unscale = 1.0;
+        c->a64.alloc(elems * sizeof(double));
+        launched(ctx, launch_hadamard_n(hf, c->rows, c->n, c->ld, c->row0, scale, inv_n, 1.0, c->a64.as<double>(),
+                                        nullptr, nullptr, ctx.stream()),
+                 "hadamard_n");
+    }
+    ctx.sync();
+    return c;
+}
+
 void download(Context& ctx, const KernelMatrix& k, double* out) {
     cuda_check(cudaSetDevice(ctx.device()), "cudaSetDevice");
     if (k.prec == kMF) fail(kInvalidArgument, "matrix-free kernels are never materialised");

@@ -250,6 +250,8 @@ std::unique_ptr<Dataset> load_csv_text(Context& ctx, const char* text, size_t le
                                        const std::string& source);
 std::unique_ptr<Dataset> load_csv_file(Context& ctx, const std::string& path, const char* label_column);
 KernelPtr hadamard_joint(Context& ctx, const KernelMatrix& a, const KernelMatrix& b);
+// hadamard_joint of any number of kernels (kernel.cpp:74-101): canonical content order, one scale
+KernelPtr hadamard_joint_n(Context& ctx, const std::vector<const KernelMatrix*>& ks);
 void download(Context& ctx, const KernelMatrix& k, double* out_colmajor);
 
 // ---- passes ----

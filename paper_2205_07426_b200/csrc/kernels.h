@@ -241,6 +241,22 @@ cudaError_t launch_gram_tc(const GramArgs& g, __half* hi, __half* lo, void* scra
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream);
 // polynomial kernel build (x, n, dx, strides, rows/row0/ld, inv_n of g): isd [n] scratch; hi/lo (fp32
 // configuration) or a64 (fp64); flags[0] |= 1 on a non-finite entry, flags[1] = min i with K_ii <= 0
+// hadamard_joint of L >= 3 stored factors in a given order (kernel.cpp:74-101): fp64 factors by a64, split
+// factors by hi/lo with their unscale; the output fp64 (c64) or split (chi/clo, stored = value / out_unscale)
+constexpr int kMaxJoint = 16;
+struct HadamardFactors {
+    const double* a64[kMaxJoint];
+    const __half* hi[kMaxJoint];
+    const __half* lo[kMaxJoint];
+    double unscale[kMaxJoint];
+    int count;
+};
+cudaError_t launch_hadamard_n(const HadamardFactors& h, int64_t rows, int64_t cols, int64_t ld, int64_t row0,
+                              double scale, double inv_n, double out_unscale, double* c64, __half* chi, __half* clo,
+                              cudaStream_t stream);
+// one content hash per stored row (the canonical factor order of hadamard_joint)
+cudaError_t launch_row_hash(const double* a64, const __half* hi, const __half* lo, int64_t rows, int64_t cols,
+                            int64_t ld, uint64_t* out, cudaStream_t stream);
 // c = scale * (a ∘ b) elementwise over count entries (ops::hadamard_scaled, ops.cpp:116-122)
 cudaError_t launch_scaled_product(const double* a, const double* b, int64_t count, double scale, double* c,
                                   cudaStream_t stream);

@@ -661,6 +661,82 @@ cudaError_t launch_scaled_product(const double* a, const double* b, int64_t coun
     return cudaGetLastError();
 }
 
+namespace {
+// hadamard_joint of L >= 3 factors (proj/src/kernel.cpp:74-101) in the caller's canonical order:
+// p = M_0; p = 1.0·(p·M_l) for the middle factors (= p·M_l exactly); p = scale·(p·M_{L-1}); diag 1/n
+__global__ void hadamard_n_kernel(HadamardFactors h, int64_t rows, int64_t cols, int64_t ld, int64_t row0,
+                                  double scale, double inv_n, double out_unscale, double* __restrict__ c64,
+                                  __half* __restrict__ chi, __half* __restrict__ clo) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = i * ld + j;
+        auto val = [&](int l) {
+            return h.a64[l] ? h.a64[l][k]
+                            : (static_cast<double>(__half2float(h.hi[l][k])) +
+                               static_cast<double>(__half2float(h.lo[l][k]))) * h.unscale[l];
+        };
+        double v;
+        if (row0 + i == j) {
+            v = inv_n;
+        } else {
+            v = val(0);
+            for (int l = 1; l + 1 < h.count; ++l) v = v * val(l);
+            v = scale * (v * val(h.count - 1));
+        }
+        if (c64) {
+            c64[k] = v;
+        } else {
+            const double s = v / out_unscale;
+            const __half hh = __double2half(s);
+            chi[k] = hh;
+            clo[k] = __double2half(s - static_cast<double>(__half2float(hh)));
+        }
+    }
+}
+
+// order key material: one 64-bit hash per row of the stored entries (fp64 values or the hi/lo
+// fp16 pairs), lanes of a warp hashing interleaved elements, folded in lane order
+__global__ void row_hash_kernel(const double* __restrict__ a64, const __half* __restrict__ hi,
+                                const __half* __restrict__ lo, int64_t rows, int64_t cols, int64_t ld,
+                                uint64_t* __restrict__ out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (r >= rows) return;
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (int64_t j = lane; j < cols; j += 32) {
+        uint64_t w;
+        if (a64) {
+            w = static_cast<uint64_t>(__double_as_longlong(a64[r * ld + j]));
+        } else {
+            w = (static_cast<uint64_t>(__half_as_ushort(hi[r * ld + j])) << 16) | __half_as_ushort(lo[r * ld + j]);
+        }
+        h = (h ^ w) * 0x100000001b3ULL;
+    }
+    uint64_t acc = 0;
+    for (int l = 0; l < 32; ++l) {  // fold the lanes' hashes in lane order
+        const uint64_t hl = __shfl_sync(0xffffffffu, h, l);
+        acc = l == 0 ? hl : ((acc ^ hl) * 0x100000001b3ULL);
+    }
+    if (lane == 0) out[r] = acc;
+}
+}  // namespace
+
+cudaError_t launch_hadamard_n(const HadamardFactors& h, int64_t rows, int64_t cols, int64_t ld, int64_t row0,
+                              double scale, double inv_n, double out_unscale, double* c64, __half* chi, __half* clo,
+                              cudaStream_t stream) {
+    hadamard_n_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(h, rows, cols, ld, row0, scale, inv_n, out_unscale,
+                                                                 c64, chi, clo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_hash(const double* a64, const __half* hi, const __half* lo, int64_t rows, int64_t cols,
+                            int64_t ld, uint64_t* out, cudaStream_t stream) {
+    if (rows <= 0) return cudaSuccess;
+    row_hash_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, stream>>>(a64, hi, lo, rows, cols, ld, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_hadamard_f64(const double* a, const double* b, int64_t rows, int64_t cols, int64_t ld,
                                 int64_t row0, double n, double* c, cudaStream_t stream) {
     hadamard_f64_kernel<<<row_grid(rows, cols), 256, 0, stream>>>(a, b, rows, cols, ld, row0, n, c);

@@ -124,3 +124,23 @@ def test_raw_ops_seam(R, orc):
     np.testing.assert_allclose(p, orc.polynomial_gram(x, 2, 1.0), rtol=1e-12, atol=1e-12 * np.abs(p).max())
     a, b = orc.fill_gaussian(1, 300, 7), orc.fill_gaussian(2, 300, 7)
     assert np.array_equal(R.ops.hadamard_scaled(a, b, 2.5, ctx=ctx), 2.5 * (a * b))
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_hadamard_joint_of_three_is_permutation_invariant(R, orc, prec):
+    """hadamard_joint over three kernels (kernel.cpp:74-101; test_kernel.cpp:113-127): a canonical
+    content order makes every permutation bitwise identical; fp64 matches the oracle to rounding."""
+    ctx = R.Context(0)
+    xs = [orc.fill_gaussian(24 + v, 300, 2) for v in range(3)]
+    ks = [R.build_kernel(x, R.GaussianKernel(1.0), prec, ctx=ctx) for x in xs]
+    j = R.hadamard_joint(ks).matrix()
+    for perm in ((2, 0, 1), (1, 2, 0), (0, 2, 1)):
+        assert np.array_equal(R.hadamard_joint([ks[p] for p in perm]).matrix(), j)
+    ref = orc.hadamard_joint_n([orc.build_kernel(x, 1.0) for x in xs])
+    tol = 1e-14 if prec == "fp64" else 2e-6
+    assert np.max(np.abs(j - ref)) <= tol * np.abs(ref).max()
+    assert abs(np.trace(j) - 1.0) <= 1e-12
+    # joint entropy over three variables (measures.cpp:15-21) on top of it
+    p = R.EstimatorParams(alpha=2.0, method="int", s=40, seed=1)
+    e = R.joint_entropy(ks, p)
+    assert np.isfinite(e.entropy)

@@ -483,3 +483,12 @@ def test_mi_identities(orc):  # test_measures.cpp:77-92,132-146
     mi = orc.mutual_information(a, b, alpha=2.0, method="int", s=16, seed=11)
     assert mi["value"] == pytest.approx(mi["vars_entropy"] + mi["target_entropy"] - mi["joint_entropy"], rel=1e-14)
     assert mi == orc.mutual_information(a, b, alpha=2.0, method="int", s=16, seed=11)
+
+
+def test_hadamard_joint_n_permutation_invariant(orc):  # test_kernel.cpp:113-127
+    ks = [orc.build_kernel(orc.fill_gaussian(24 + v, 10, 2), 1.0) for v in range(3)]
+    ref = orc.hadamard_joint_n(ks)
+    assert np.array_equal(ref, orc.hadamard_joint_n([ks[2], ks[0], ks[1]]))
+    assert abs(np.trace(ref) - 1.0) <= 1e-12
+    # L = 2 equals the pairwise entry bitwise
+    assert np.array_equal(orc.hadamard_joint_n(ks[:2]), orc.hadamard_joint(ks[0], ks[1]))
