@@ -144,3 +144,18 @@ def test_hadamard_joint_of_three_is_permutation_invariant(R, orc, prec):
     p = R.EstimatorParams(alpha=2.0, method="int", s=40, seed=1)
     e = R.joint_entropy(ks, p)
     assert np.isfinite(e.entropy)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_measures_permutation_invariant(R, orc, prec):  # test_measures.cpp:112-130
+    ctx = R.Context(0)
+    ks = [R.build_kernel(orc.fill_gaussian(80 + i, 250, dd), R.GaussianKernel(1.0), prec, ctx=ctx)
+          for i, dd in enumerate((2, 3, 1))]
+    a, b, c = ks
+    p = R.EstimatorParams(alpha=1.5, method="chebyshev", s=16, m=20, seed=4, bounds=R.SpectrumBounds(u=0.0, v=1.0))
+    r1 = R.joint_entropy([a, b, c], p).entropy
+    r2 = R.joint_entropy([b, c, a], p).entropy
+    assert r1 == r2
+    if prec == "fp64":
+        ex = R.EstimatorParams(alpha=1.5, method="exact")
+        assert R.joint_entropy([a, b, c], ex).entropy == R.joint_entropy([c, a, b], ex).entropy
