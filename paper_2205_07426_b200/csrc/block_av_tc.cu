@@ -388,12 +388,6 @@ constexpr int kTriConv0 = 4, kTriDrain0 = 12;
 #ifndef RB_TRI_AB_STAGES
 #define RB_TRI_AB_STAGES 2
 #endif
-#ifndef RB_TRI_PREFETCH
-#define RB_TRI_PREFETCH 0  // A/B k tiles prefetched into L2 ahead of the TMA ring (0: off)
-#endif
-#ifndef RB_TRI_SETMAXNREG
-#define RB_TRI_SETMAXNREG 1
-#endif
 constexpr int kTriThreads = 32 * 24;  // warpgroup 0: TMA (warp 0), MMA (warp 1); setmaxnreg per role
 
 template <int NPAD, bool VSPLIT>
@@ -569,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
 
     // registers move only between warpgroups of the CTA: 4x(80-40) + 8x(80-64) = 12x(104-80) per thread
     // (drains: 80 fp32 accumulators + a 16-column TMEM load in flight)
-    if (RB_TRI_SETMAXNREG && warp < kTriConv0) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp < kTriConv0) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 0 || warp == 2) {
         // ---------------- TMA: A/B tiles of this CTA's rows (warp 0, local ring); its half of the V planes
         // (warp 2, completing on the leader's barriers). Separate issuers: neither ring's back-pressure
@@ -577,7 +571,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         if (lane == 0) {
             const uint64_t pol_stream = args.a_policy ? policy_evict_normal() : policy_evict_first();
             const uint64_t pol_keep = policy_evict_last();
-            const uint64_t pol_pref = policy_evict_normal();
             const CUtensorMap* vmap[3][2] = {{&map_va, &map_valo}, {&map_vb, &map_vblo}, {&map_vj, &map_vjlo}};
             int as = 0, vs = 0;
             uint32_t aph = 0, vph = 0;
@@ -596,14 +589,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
                         tma_load_2d(st + C::kAPlane, &map_alo, &ab_full[as], kg * TBK, r * TBM, pol_stream);
                         tma_load_2d(st + 2 * C::kAPlane, &map_bhi, &ab_full[as], kg * TBK, r * TBM, pol_stream);
                         tma_load_2d(st + 3 * C::kAPlane, &map_blo, &ab_full[as], kg * TBK, r * TBM, pol_stream);
-                        if (RB_TRI_PREFETCH > 0 && k + RB_TRI_PREFETCH < k1) {
-                            int kp = kg + RB_TRI_PREFETCH;
-                            if (kp >= args.k_total) kp -= args.k_total;
-                            tma_prefetch_2d(&map_ahi, kp * TBK, r * TBM, pol_pref);
-                            tma_prefetch_2d(&map_alo, kp * TBK, r * TBM, pol_pref);
-                            tma_prefetch_2d(&map_bhi, kp * TBK, r * TBM, pol_pref);
-                            tma_prefetch_2d(&map_blo, kp * TBK, r * TBM, pol_pref);
-                        }
                         if (++as == C::kABStages) as = 0, aph ^= 1u;
                     } else {
                         mbar_wait(&v_empty[vs], vph ^ 1u);
@@ -676,7 +661,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         }
     } else if (warp >= kTriConv0 && warp < kTriConv0 + kTriConv) {
         // ---------------- operand builders: A, B and J = n·(A∘B) into TMEM ----------------
-        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
         // K groups {half, half + 2} (16 columns each) of the tile: the two halves build groups 0 and 1
         // side by side, then 2 and 3 -- the order the MMA issuer consumes them in
         const int half = (warp - kTriConv0) / 4;
@@ -758,7 +743,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads, 1)
         }
     } else if (warp >= kTriDrain0) {
         // ---------------- TMEM drains: operand (warp-12)/4, lane quarter warp%4 ----------------
-        if (RB_TRI_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
         const int op = (warp - kTriDrain0) / 4;
         const int quarter = warp & 3;
         const int row_local = quarter * 32 + lane;
