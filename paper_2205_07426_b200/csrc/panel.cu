@@ -42,6 +42,9 @@ __device__ __forceinline__ int plane_exponent(double bound) {
     return e;
 }
 
+// 2^e as an exact double for the exponents the planes use (|e| <= 120): scaling by it equals ldexp
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(1023 + e) << 52); }
+
 // fp16 operand (+ optional low plane carrying the rounding residual)
 __device__ __forceinline__ void split_store(double v, __half* hi, __half* lo, int64_t idx) {
     const __half h = __double2half(v);
@@ -59,6 +62,8 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     constexpr int NW = ER / 32;
     __shared__ double red[3][NW][kEpiCols];
     __shared__ float mxs[NW][kEpiCols];
+    __shared__ int64_t sown[4];                        // the row block's partial slot ranges
+    __shared__ double sscale[kEpiCols], snext[kEpiCols];  // 2^-e_cur·unscale and 2^e_next per column
     const int jb0 = blockIdx.y * kEpiCols, jb1 = min(p.s, jb0 + kEpiCols);
     const int r = blockIdx.x;
     const int tid = threadIdx.x;
@@ -66,19 +71,33 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     const int64_t i = static_cast<int64_t>(r) * ER + tid;
     const bool valid = i < p.rows;
     const int64_t cl = p.cluster, rb = r / cl, rr = r % cl;
-    // slots [c_lo, c_hi] of row block rb under a plan (whole row blocks: slot rb)
-    auto owners = [&](int64_t KT, int64_t total_iters, int grid, int64_t dp, int64_t& lo, int64_t& hi) {
-        lo = hi = 0;
-        if (rb >= dp) {
-            const int64_t rt = rb - dp, tail = total_iters - dp * KT;
-            lo = streamk_owner(rt * KT, tail, grid);
-            hi = streamk_owner((rt + 1) * KT - 1, tail, grid);
-        }
-    };
-    int64_t c_lo, c_hi, c2_lo = 0, c2_hi = -1;
-    owners(p.k_tiles, p.total_iters, p.grid, p.dp_blocks, c_lo, c_hi);
-    if (p.partial2) owners(p.k_tiles2, p.total_iters2, p.grid2, p.dp_blocks2, c2_lo, c2_hi);
-    const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
+    // block-uniform work once per block (the 64-bit stream-K owner divisions and the plane exponents
+    // were ~40 % of the kernel's instructions when every thread repeated them)
+    if (tid == 0) {
+        // slots [c_lo, c_hi] of row block rb under a plan (whole row blocks: slot rb)
+        auto owners = [&](int64_t KT, int64_t total_iters, int grid, int64_t dp, int64_t* out) {
+            out[0] = 0, out[1] = 0;
+            if (rb >= dp) {
+                const int64_t rt = rb - dp, tail = total_iters - dp * KT;
+                out[0] = streamk_owner(rt * KT, tail, grid);
+                out[1] = streamk_owner((rt + 1) * KT - 1, tail, grid);
+            }
+        };
+        owners(p.k_tiles, p.total_iters, p.grid, p.dp_blocks, sown);
+        if (p.partial2) owners(p.k_tiles2, p.total_iters2, p.grid2, p.dp_blocks2, sown + 2);
+        else sown[2] = 0, sown[3] = -1;
+    }
+    if (SPLIT && tid < kEpiCols && jb0 + tid < jb1) {
+        const int j = jb0 + tid;
+        const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
+        const double bound = growth * cm_value(p.cmax_cur, j) + fabs(p.a3) * cm_value(p.cmax_prev, j);
+        const int e = plane_exponent(bound);
+        if (r == 0) p.e_next[j] = e;
+        sscale[tid] = pow2(-p.e_cur[j]);
+        snext[tid] = pow2(e);
+    }
+    __syncthreads();
+    const int64_t c_lo = sown[0], c_hi = sown[1], c2_lo = sown[2], c2_hi = sown[3];
 
     // all of this block's loads first (kEpiCols independent columns in flight per thread: the loop
     // below was latency-bound, one column's loads at a time -- 150 us per config-4 epilogue), then
@@ -109,7 +128,7 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
         const int j = jb0 + jj;
         if (j >= jb1) break;
         double y = ys[jj];
-        if (SPLIT) y = ldexp(y * p.unscale, -p.e_cur[j]);
+        if (SPLIT) y = (y * p.unscale) * sscale[jj];  // = ldexp(y·unscale, −e_cur) (exact power of two)
         const double tc = static_cast<double>(tcs[jj]), tp = static_cast<double>(tps[jj]),
                      x0 = static_cast<double>(x0s[jj]);
         const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
@@ -121,12 +140,7 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
             p.t_new[idx] = tns;
             if (p.acc) p.acc[idx] += p.acc_coef * tn;
         }
-        if (SPLIT) {
-            const double bound = growth * cm_value(p.cmax_cur, j) + fabs(p.a3) * cm_value(p.cmax_prev, j);
-            const int e = plane_exponent(bound);
-            if (r == 0 && tid == 0) p.e_next[j] = e;
-            if (valid) split_store(ldexp(tn, e), p.vop, p.vop_lo, idx);
-        }
+        if (SPLIT && valid) split_store(tn * snext[jj], p.vop, p.vop_lo, idx);
         const double d1 = warp_sum(x0 * tn);
         const double d2 = warp_sum(tc * tn);
         const double d3 = warp_sum(tn * tn);
