@@ -38,20 +38,42 @@ __global__ void __launch_bounds__(256) block_av_f64_kernel(const double* __restr
         double acc[FM / 8];
 #pragma unroll
         for (int i = 0; i < FM / 8; ++i) acc[i] = 0.0;
-        for (; it < seg_end; ++it) {
-            const int64_t k0 = (it - rb * k_tiles) * FK;
-            for (int idx = threadIdx.x; idx < FM * FK; idx += blockDim.x) {
+        // software pipeline: the next k tile's loads are in flight in registers while this one computes
+        // (A is L2-resident: each tile is an L2 round trip, which the compute of the previous tile hides)
+        constexpr int NA = FM * FK / 256, NV = FN * FK / 256;
+        double ra[NA], rv[NV];
+        auto load = [&](int64_t t) {
+            const int64_t k0 = (t - rb * k_tiles) * FK;
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                const int idx = threadIdx.x + 256 * q;
                 const int rr = idx / FK, kk = idx % FK;
                 const int64_t gr = row0 + rr, gk = k0 + kk;
-                as[kk][rr] = (gr < rows && gk < cols) ? a[gr * lda + gk] : 0.0;
+                ra[q] = (gr < rows && gk < cols) ? a[gr * lda + gk] : 0.0;
             }
-            for (int idx = threadIdx.x; idx < FN * FK; idx += blockDim.x) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const int idx = threadIdx.x + 256 * q;
                 const int cc = idx / FK, kk = idx % FK;
                 const int gc = col0 + cc;
                 const int64_t gk = k0 + kk;
-                vs[kk][cc] = (gc < s && gk < cols) ? v[static_cast<int64_t>(gc) * ldv + gk] : 0.0;
+                rv[q] = (gc < s && gk < cols) ? v[static_cast<int64_t>(gc) * ldv + gk] : 0.0;
+            }
+        };
+        load(it);
+        for (; it < seg_end; ++it) {
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                const int idx = threadIdx.x + 256 * q;
+                as[idx % FK][idx / FK] = ra[q];
+            }
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const int idx = threadIdx.x + 256 * q;
+                vs[idx % FK][idx / FK] = rv[q];
             }
             __syncthreads();
+            if (it + 1 < seg_end) load(it + 1);
 #pragma unroll 4
             for (int kk = 0; kk < FK; ++kk) {
                 const double vv = vs[kk][tx];
