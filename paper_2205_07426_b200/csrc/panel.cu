@@ -169,18 +169,29 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     }
 }
 
+// grid = row blocks x column groups of kEpiCols (as the pass epilogue: a serial loop over every column
+// in one block left the first pass's statistics latency-bound, 21-108 us per launch); each block's
+// per-column sums are the same warp sums added in the same warp order as before
 template <typename ST, int ER>
 __global__ void __launch_bounds__(ER) prep_stats_kernel(PrepArgs<ST> p) {
     constexpr int NW = ER / 32;
-    __shared__ double red[NW][kMaxPanelCols];
+    __shared__ double red[NW][kEpiCols];
     const int r = blockIdx.x;
+    const int jb0 = blockIdx.y * kEpiCols, jb1 = min(p.s, jb0 + kEpiCols);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int64_t i = static_cast<int64_t>(r) * ER + tid;
     const bool valid = i < p.rows;
-    for (int j = 0; j < p.s; ++j) {
+    ST xs[kEpiCols];
+#pragma unroll
+    for (int jj = 0; jj < kEpiCols; ++jj)  // every column's load in flight first
+        xs[jj] = (valid && jb0 + jj < jb1) ? static_cast<ST>(p.x[static_cast<int64_t>(jb0 + jj) * p.ldx + i]) : ST(0);
+#pragma unroll
+    for (int jj = 0; jj < kEpiCols; ++jj) {
+        const int j = jb0 + jj;
+        if (j >= jb1) break;
         double v = 0.0;
         if (valid) {
-            const ST vs = static_cast<ST>(p.x[static_cast<int64_t>(j) * p.ldx + i]);
+            const ST vs = xs[jj];
             v = static_cast<double>(vs);
             p.t0[static_cast<int64_t>(j) * p.ld + i] = vs;
             if (p.acc) p.acc[static_cast<int64_t>(j) * p.ld + i] = p.acc_coef * v;
@@ -188,16 +199,17 @@ __global__ void __launch_bounds__(ER) prep_stats_kernel(PrepArgs<ST> p) {
         const double d = warp_sum(v * v);
         const float mx = warp_max(static_cast<float>(fabs(v)));
         if (lane == 0) {
-            red[warp][j] = d;
+            red[warp][jj] = d;
             atomicMax(p.cmax0 + j, __float_as_uint(mx));
         }
     }
     __syncthreads();
     const int R = gridDim.x;
-    for (int j = tid; j < p.s; j += blockDim.x) {
-        double v = red[0][j];
+    if (tid < jb1 - jb0) {
+        const int j = jb0 + tid;
+        double v = red[0][tid];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) v += red[w][j];
+        for (int w = 1; w < NW; ++w) v += red[w][tid];
         // q = 0 (x0·T0), 1 (T0·T0 as "Rayleigh" slot), 2 (T0·T0)
         p.stats[(0 * static_cast<int64_t>(R) + r) * p.s + j] = v;
         p.stats[(1 * static_cast<int64_t>(R) + r) * p.s + j] = v;
@@ -397,12 +409,13 @@ cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t s
 
 cudaError_t launch_prepare_split_stats(const PrepArgs<float>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
+    const unsigned groups = static_cast<unsigned>((a.s + kEpiCols - 1) / kEpiCols);
     if (a.rows_per_block == 256) {
         const int R = static_cast<int>((a.rows + 255) / 256);
-        if (R > 0) prep_stats_kernel<float, 256><<<R, 256, 0, stream>>>(a);
+        if (R > 0) prep_stats_kernel<float, 256><<<dim3(R, groups), 256, 0, stream>>>(a);
     } else if (a.rows_per_block == 128) {
         const int R = static_cast<int>((a.rows + 127) / 128);
-        if (R > 0) prep_stats_kernel<float, 128><<<R, 128, 0, stream>>>(a);
+        if (R > 0) prep_stats_kernel<float, 128><<<dim3(R, groups), 128, 0, stream>>>(a);
     } else {
         return cudaErrorInvalidValue;
     }
@@ -418,7 +431,8 @@ cudaError_t launch_prepare_split_planes(const PrepArgs<float>& a, cudaStream_t s
 cudaError_t launch_prepare_f64(const PrepArgs<double>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols || a.rows_per_block != 128) return cudaErrorInvalidValue;
     const int R = static_cast<int>((a.rows + 127) / 128);
-    prep_stats_kernel<double, 128><<<R, 128, 0, stream>>>(a);
+    const unsigned groups = static_cast<unsigned>((a.s + kEpiCols - 1) / kEpiCols);
+    prep_stats_kernel<double, 128><<<dim3(R, groups), 128, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
