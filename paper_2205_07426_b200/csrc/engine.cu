@@ -143,6 +143,27 @@ struct PoolBlock {
 };
 std::mutex g_pool_mu;
 std::multimap<std::pair<int, size_t>, PoolBlock> g_pool;  // (device, capacity) -> block
+// recycled stream-order events per device (cudaEventCreate costs microseconds on every free of a
+// latency-bound estimate; a recorded event is reusable once its block has been handed out again)
+std::map<int, std::vector<cudaEvent_t>> g_free_events;
+
+cudaEvent_t take_event(int device) {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto& v = g_free_events[device];
+        if (!v.empty()) {
+            cudaEvent_t e = v.back();
+            v.pop_back();
+            return e;
+        }
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    return e;
+}
 thread_local cudaStream_t t_stream = nullptr;
 
 size_t pool_round(size_t bytes) {
@@ -180,7 +201,7 @@ void* pool_alloc(size_t bytes, size_t* capacity, int* device) {
                     if (t_stream) cudaStreamWaitEvent(t_stream, b.ready, 0);
                     else cudaEventSynchronize(b.ready);
                 }
-                cudaEventDestroy(b.ready);
+                g_free_events[dev].push_back(b.ready);  // the wait above (if any) is already enqueued
             }
             return b.p;
         }
@@ -205,10 +226,8 @@ void pool_free(void* p, size_t capacity, int device) {
         int cur = 0;
         cudaGetDevice(&cur);
         if (cur != device) cudaSetDevice(device);
-        if (cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming) != cudaSuccess) {
-            (void)cudaGetLastError();
-            b.ready = nullptr;
-        } else if (cudaEventRecord(b.ready, t_stream) != cudaSuccess) {
+        b.ready = take_event(device);
+        if (b.ready && cudaEventRecord(b.ready, t_stream) != cudaSuccess) {
             (void)cudaGetLastError();
             cudaEventDestroy(b.ready);
             b.ready = nullptr;
@@ -236,6 +255,11 @@ void pool_release_all() {
         cudaFree(kv.second.p);
     }
     g_pool.clear();
+    for (auto& kv : g_free_events) {
+        cudaSetDevice(kv.first);
+        for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
+    }
+    g_free_events.clear();
     cudaSetDevice(cur);
 }
 
