@@ -1582,9 +1582,18 @@ void make_probes(Context& ctx, const KernelMatrix& k, DevBuf& dst, int cols, int
 std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx, const double* z, int q,
                               int64_t ldz, int64_t rows) {
     std::vector<double> out(static_cast<size_t>(p) * q);
+    if (p > 128) {  // wide sketches (s/4 > 128 columns): row blocks of X^T Z, assembled on the host
+        for (int p0 = 0; p0 < p; p0 += 128) {
+            const int pb = std::min(128, p - p0);
+            const std::vector<double> sub = gram_host(ctx, x + static_cast<int64_t>(p0) * ldx, pb, ldx, z, q, ldz, rows);
+            for (int c = 0; c < q; ++c)
+                for (int r = 0; r < pb; ++r) out[(p0 + r) + static_cast<size_t>(c) * p] = sub[r + static_cast<size_t>(c) * pb];
+        }
+        return out;
+    }
     const int grid = std::min<int64_t>(ctx.sms(), std::max<int64_t>(1, (rows + 31) / 32));
-    // column blocks of z so p * qb <= 2048
-    const int qb_max = std::max(1, 2048 / std::max(p, 1));
+    // column blocks of z so p * qb <= 2048 and the kernel's 32-row staging of p + qb columns fits 48 KB
+    const int qb_max = std::max(1, std::min(2048 / std::max(p, 1), 192 - p));
     ctx.small.ensure(static_cast<size_t>(p) * q * sizeof(double));
     for (int b0 = 0; b0 < q; b0 += qb_max) {
         const int qb = std::min(qb_max, q - b0);
