@@ -172,3 +172,18 @@ def test_wide_sketch_hutchpp_matches_oracle(R, orc, prec, tol):
     est = R.estimate(k, R.EstimatorParams(alpha=3.0, method="int", s=1080, seed=17))
     assert est.trace.sketch_rank == ref["sketch_rank"]
     assert est.entropy == pytest.approx(ref["entropy"], rel=tol)
+
+
+def test_generous_parameters_track_the_oracle(R, orc):  # test_entropy.cpp:273-293
+    """Auto routing with select_params(1e-3, 1e-2) budgets: 50 seeds x alpha in {0.5, 2, 2.5} x n in
+    {100, 220}, every estimate within 1 % of the eigendecomposition entropy."""
+    ctx = R.Context(0)
+    for n in (100, 220):
+        a = random_unit_trace_spd(n, 68 + n, orc, floor=0.25)
+        lam = np.clip(np.linalg.eigvalsh(a), 0.0, 1.0)
+        k = R.NormalizedKernel.from_matrix(a, "fp64", ctx=ctx)
+        for alpha in (0.5, 2.0, 2.5):
+            exact = exact_entropy(lam, alpha)
+            hits = sum(abs(R.estimate(k, R.EstimatorParams(alpha=alpha, epsilon=1e-3, delta=1e-2, seed=t)).entropy
+                           - exact) <= 1e-2 * abs(exact) for t in range(50))
+            assert hits == 50, (n, alpha, hits)
