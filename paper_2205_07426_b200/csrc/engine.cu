@@ -8,6 +8,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -305,6 +306,7 @@ Context::Context(int device) : device_(device) {
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     probe_err.alloc(sizeof(int));
     cuda_check(cudaMemsetAsync(probe_err.as<int>(), 0, sizeof(int), stream_), "memset");
+    if (const char* e = std::getenv("RB_SYMV")) symv = std::string(e) != "0";
 }
 
 cudaStream_t Context::comm_stream() {
@@ -1014,7 +1016,19 @@ public:
         split_ = ctx.exchange && ctx.world() > 1 && k.prec != kF64;
         if (split_) ctx.main_after_comm();  // a previous session's last gather may still be in flight
         const KWindow own{k.row0, rows_}, rest{k.row0 + rows_, k.n - rows_};
-        if (k.prec == kF32) {
+        // s = 1 on one whole symmetric fp32 matrix: the upper-triangle product (half the bytes of A)
+        symv_ = k.prec == kF32 && s == 1 && !tri && !split_ && k.world == 1 && k.groups <= 1 && k.normalized &&
+                ctx.symv && k.rows == k.n;
+        if (symv_) {
+            nb_ = symv_blocks(k.n);
+            plan_ = StreamKPlan{};
+            plan_.row_blocks = static_cast<int>(nb_);
+            plan_.rows_per_block = 128;
+            plan_.cluster = 1;
+            plan_.slots = static_cast<int>(nb_ * nb_);
+            plan_.grid = 8 * ctx.sms();
+            npad_ = 1;
+        } else if (k.prec == kF32) {
             const int grid = k.group_grid > 0 ? k.group_grid : ctx.grid > 0 ? ctx.grid : ctx.sms();
             auto mk = [&](KWindow w) {
                 return tri ? make_tri_plan(rows_, k.n, grid, ctx.kc, w) : make_streamk_plan(rows_, k.n, grid, ctx.kc, w);
@@ -1155,6 +1169,14 @@ public:
                 // algorithmic flops (SURVEY §8d matrix-free): 2·n_local·n·(d + s); bytes: X, V, Y
                 ctx_.prof_account(frac * (2.0 * k_.n * k_.dfeat + 2.0 * k_.n * s_) + 4.0 * rows_ * s_,
                                   frac * 2.0 * rows_ * k_.n * (k_.dfeat + s_));
+            } else if (symv_) {
+                SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
+                launched(ctx_, launch_symv_split(a, v.v, v.vlo, part, pl.grid, ctx_.stream()), "symv");
+                ctx_.prof_end();
+                // algorithmic bytes of the symmetric product: the upper triangle of A (4 B/entry) + x + y
+                const double nn = static_cast<double>(k_.n);
+                ctx_.prof_account(4.0 * nn * (nn + 1.0) / 2.0 + (vlo_ ? 4.0 : 2.0) * nn + 4.0 * nn, 2.0 * nn * nn);
+                continue;
             } else {
                 SplitMatrixView a{k_.hi.as<__half>(), k_.lo.as<__half>(), rows_, k_.n, k_.ld};
                 if (rows_ > 0 && pl.k_tiles > 0)
@@ -1180,6 +1202,7 @@ public:
             e.total_iters = plan_.total_iters, e.k_tiles = plan_.k_tiles, e.grid = plan_.grid;
             e.cluster = plan_.cluster;
             e.dp_blocks = plan_.dp_blocks;
+            e.symv_nb = symv_ ? nb_ : 0;
             e.rows = rows_, e.rows_per_block = plan_.rows_per_block, e.s = s_, e.ld = ld_;
             e.e_cur = w_.eexp.as<int>() + k * s;
             e.e_next = w_.eexp.as<int>() + (k + 1) * s;
@@ -1325,6 +1348,8 @@ private:
     static constexpr int64_t kTailElems = 256;  // 512 bytes: up to 128 uint32 column maxima
     StreamKPlan plan_, plan2_;
     bool split_ = false;
+    bool symv_ = false;  // s = 1 through the upper-triangle product (symv.cu)
+    int64_t nb_ = 0;     // its 128-row blocks
 };
 
 }  // namespace

@@ -151,6 +151,9 @@ public:
     PanelWorkspace ws_aux[2];  // the second and third operand of a fused mutual-information pass
     bool fused_mi = true;      // mutual information: one pass over A and B for all three terms
     bool feature_groups = true;  // feature tools: candidates' estimates as grouped stacks (fp32)
+    // single-column fp32 passes (power iteration, matvec) through the upper-triangle product (symv.cu);
+    // RB_SYMV=0 in the environment selects the tensor-core block product for A/B comparisons
+    bool symv = true;
     // source of seeded Gaussian probes (Rademacher probes are exact on the device either way):
     // 0 device (rng_panel: the reference's substreams with CUDA's log/sin/cos, <= 2 ulp from glibc per
     // draw), 1 host (the reference's own stream arithmetic, bitwise the probes of

@@ -72,6 +72,14 @@ struct KWindow {
     int64_t cols = -1;  // -1: all columns
 };
 
+// ---- symmetric single-column product (s = 1 passes, symv.cu) ---------------
+// 128-row blocks of an n x n matrix
+int64_t symv_blocks(int64_t n);
+// partials of y = A·x from the upper triangle: slot I·nb + J holds block I's share from tile (I, J) or
+// (J, I); partial [nb·nb][128] floats, one column
+cudaError_t launch_symv_split(const SplitMatrixView& a, const __half* xhi, const __half* xlo, float* partial,
+                              int grid, cudaStream_t stream);
+
 // ---- block product -------------------------------------------------------
 int tc_block_rows();
 int tc_block_k();
@@ -148,6 +156,8 @@ struct EpiArgs {
     // second K window of a row-sharded pass (the other ranks' operand chunks, see StreamKPlan::k_off):
     // its slots are summed after the first window's, in the same fixed order; partial2 == nullptr: none
     const PT* partial2 = nullptr;
+    // symmetric single-column product (launch_symv_split): nb partial slots per row block, [I·nb, I·nb + nb)
+    int64_t symv_nb = 0;
     int64_t total_iters2 = 0;
     int k_tiles2 = 0;
     int grid2 = 1;

@@ -83,7 +83,11 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
                 out[1] = streamk_owner((rt + 1) * KT - 1, tail, grid);
             }
         };
-        owners(p.k_tiles, p.total_iters, p.grid, p.dp_blocks, sown);
+        if (p.symv_nb > 0) {  // slots rb·nb .. rb·nb + nb - 1 (cluster 1: slot = rb + c)
+            sown[0] = rb * (p.symv_nb - 1), sown[1] = sown[0] + p.symv_nb - 1;
+        } else {
+            owners(p.k_tiles, p.total_iters, p.grid, p.dp_blocks, sown);
+        }
         if (p.partial2) owners(p.k_tiles2, p.total_iters2, p.grid2, p.dp_blocks2, sown + 2);
         else sown[2] = 0, sown[3] = -1;
     }
