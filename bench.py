@@ -623,6 +623,9 @@ def run_ours_entropy(args):
     kernel = {"mf": "block_av_mf_kernel (tcgen05 cta_group::2, kernel entries recomputed from bf16 X)",
               "fp32": "block_av_tc_kernel (tcgen05, fp16 hi/lo A)",
               "fp64": "block_av_f64_kernel (fp64 SIMT, A L2-resident)"}[prec]
+    if args.config == "c3":
+        kernel = ("symv_split_kernel (power iteration: upper triangle of A, row and column sums per tile) + "
+                  "block_av_tc_kernel (Taylor passes, tcgen05)")
     traffic = ncu_traffic({"mf": "block_av_mf", "fp32": "block_av_split", "fp64": "block_av_f64"}[prec]) \
         if args.config == "c5" else ncu_traffic(f"block_av_{args.config}")
     roof = roofline_of(prof, ms, "tensor" if tensor else "hbm", kernel, traffic)
@@ -630,7 +633,8 @@ def run_ours_entropy(args):
         roof["flops_formula"] = "2 * n_local * n * (d + s) per pass (SURVEY §8(d), C5)"
         roof["exp_per_launch"] = float(n) * n / max(arm.world if arm.sharded else 1, 1)
     else:
-        roof["bytes_formula"] = "e_A * n_local * n + e_V * n * s + e_Y * n_local * s per pass (SURVEY §8(d))"
+        roof["bytes_formula"] = ("e_A * n_local * n + e_V * n * s + e_Y * n_local * s per pass (SURVEY §8(d)); "
+                                 "the symmetric s = 1 passes read the upper triangle: e_A * n (n + 1) / 2")
     if args.config == "c1":
         roof["note"] = "A (32 MB) is L2-resident: a latency configuration; the HBM fraction is not a bound"
     line = {
