@@ -306,6 +306,8 @@ Context::Context(int device) : device_(device) {
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     probe_err.alloc(sizeof(int));
     cuda_check(cudaMemsetAsync(probe_err.as<int>(), 0, sizeof(int), stream_), "memset");
+    gram_ticket.alloc(sizeof(unsigned));
+    cuda_check(cudaMemsetAsync(gram_ticket.as<unsigned>(), 0, sizeof(unsigned), stream_), "memset");
     if (const char* e = std::getenv("RB_SYMV")) symv = std::string(e) != "0";
 }
 
@@ -1617,8 +1619,9 @@ std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx,
         return out;
     }
     const int grid = std::min<int64_t>(ctx.sms(), std::max<int64_t>(1, (rows + 31) / 32));
-    // column blocks of z so p * qb <= 2048 and the kernel's 32-row staging of p + qb columns fits 48 KB
-    const int qb_max = std::max(1, std::min(2048 / std::max(p, 1), 192 - p));
+    // column blocks of z so p * qb <= 2048 and the kernel's 32-row staging of p + qb columns (plus its
+    // static shared flag) fits the 48 KB default
+    const int qb_max = std::max(1, std::min(2048 / std::max(p, 1), 190 - p));
     ctx.small.ensure(static_cast<size_t>(p) * q * sizeof(double));
     for (int b0 = 0; b0 < q; b0 += qb_max) {
         const int qb = std::min(qb_max, q - b0);
@@ -1626,7 +1629,7 @@ std::vector<double> gram_host(Context& ctx, const double* x, int p, int64_t ldx,
         launched(ctx,
                  launch_panel_gram(x, p, ldx, z + static_cast<int64_t>(b0) * ldz, qb, ldz, rows,
                                    ctx.gram_partial.as<double>(), grid, ctx.small.as<double>() + static_cast<size_t>(b0) * p,
-                                   ctx.stream()),
+                                   ctx.stream(), ctx.gram_ticket.as<unsigned>()),
                  "panel_gram");
     }
     // Grams over row-sharded panels: one sum over ranks (CholeskyQR2 / projection)
@@ -2543,18 +2546,24 @@ std::vector<std::vector<double>> grams_batch(Context& ctx, const std::vector<Gra
     for (const auto& j : jobs) total += static_cast<size_t>(j.p) * j.q;
     std::vector<std::vector<double>> out(jobs.size());
     if (total == 0) return out;
+    for (const auto& j : jobs)
+        if (j.p > 128) {  // wide sketches: one row-blocked Gram per job (gram_host)
+            for (size_t i = 0; i < jobs.size(); ++i) out[i] = gram_host(ctx, jobs[i].x, jobs[i].p, ld, jobs[i].z, jobs[i].q, ld, n);
+            return out;
+        }
     const int grid = std::min<int64_t>(ctx.sms(), std::max<int64_t>(1, (n + 31) / 32));
     ctx.small.ensure(total * sizeof(double));
     size_t off = 0;
     for (const auto& j : jobs) {
-        const int qb_max = std::max(1, 2048 / std::max(j.p, 1));
+        const int qb_max = std::max(1, std::min(2048 / std::max(j.p, 1), 190 - j.p));
         for (int b0 = 0; b0 < j.q; b0 += qb_max) {
             const int qb = std::min(qb_max, j.q - b0);
             ctx.gram_partial.ensure(static_cast<size_t>(grid) * j.p * qb * sizeof(double));
             launched(ctx,
                      launch_panel_gram(j.x, j.p, ld, j.z + static_cast<int64_t>(b0) * ld, qb, ld, n,
                                        ctx.gram_partial.as<double>(), grid,
-                                       ctx.small.as<double>() + off + static_cast<size_t>(b0) * j.p, ctx.stream()),
+                                       ctx.small.as<double>() + off + static_cast<size_t>(b0) * j.p, ctx.stream(),
+                                       ctx.gram_ticket.as<unsigned>()),
                      "panel_gram");
         }
         off += static_cast<size_t>(j.p) * j.q;

@@ -171,7 +171,7 @@ public:
     void prefetch_probes(const std::vector<ProbeReq>& reqs);
     std::shared_ptr<std::vector<double>> take_probes(int64_t n, int cols, uint64_t seed, const char* label, int kind);
     void drop_prefetched_probes();  // waits for unused panels, frees them
-    DevBuf gram_partial, small, probe_err;
+    DevBuf gram_partial, small, probe_err, gram_ticket;
     DevBuf x0, work, acc;
 
 private:

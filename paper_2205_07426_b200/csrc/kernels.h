@@ -205,8 +205,11 @@ cudaError_t launch_state_to_f64(const void* state, bool is_f32, int64_t rows, in
 
 // ---- small dense panel algebra (fp64) ------------------------------------
 // C[p x q] = X^T Z over rows; partial buffer must hold grid*p*q doubles.
+// ticket: a zeroed device counter (reset by the kernel): the last CTA reduces the partials in CTA order
+// instead of a separate reduction launch; nullptr: separate reduction kernel
 cudaError_t launch_panel_gram(const double* x, int p, int64_t ldx, const double* z, int q, int64_t ldz,
-                              int64_t rows, double* partial, int grid, double* out, cudaStream_t stream);
+                              int64_t rows, double* partial, int grid, double* out, cudaStream_t stream,
+                              unsigned* ticket = nullptr);
 // W = beta*G + X*C   (X: rows x p, C: p x q column-major, W/G: rows x q)
 cudaError_t launch_panel_update(double beta, const double* g, int64_t ldg, const double* x, int p, int64_t ldx,
                                 const double* c, int q, int64_t rows, double* w, int64_t ldw, cudaStream_t stream);

@@ -257,7 +257,8 @@ __global__ void state_to_f64_kernel(const ST* __restrict__ st, int64_t rows, int
 constexpr int GR = 32;  // rows per smem chunk
 __global__ void __launch_bounds__(256) panel_gram_kernel(const double* __restrict__ x, int p, int64_t ldx,
                                                          const double* __restrict__ z, int q, int64_t ldz,
-                                                         int64_t rows, double* __restrict__ partial) {
+                                                         int64_t rows, double* __restrict__ partial,
+                                                         unsigned* __restrict__ ticket, double* __restrict__ out) {
     extern __shared__ double sm[];
     double* xs = sm;            // [GR][p]
     double* zs = sm + GR * p;   // [GR][q]
@@ -298,6 +299,22 @@ __global__ void __launch_bounds__(256) panel_gram_kernel(const double* __restric
         const int o = threadIdx.x + u * blockDim.x;
         if (o < outs) partial[static_cast<int64_t>(blockIdx.x) * outs + o] = acc[u];
     }
+    // the last CTA to finish sums every CTA's partial in CTA order (the separate reduce kernel's
+    // order: bitwise the same Gram), saving a launch per Gram of the latency-bound QR steps
+    if (!ticket) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == static_cast<unsigned>(G - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int o = threadIdx.x; o < outs; o += blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < G; ++c) s += __ldcg(partial + static_cast<int64_t>(c) * outs + o);
+        out[o] = s;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;  // ready for the next Gram on this stream
 }
 
 __global__ void panel_gram_reduce_kernel(const double* __restrict__ partial, int G, int outs,
@@ -477,16 +494,21 @@ cudaError_t launch_state_to_f64(const void* state, bool is_f32, int64_t rows, in
 }
 
 cudaError_t launch_panel_gram(const double* x, int p, int64_t ldx, const double* z, int q, int64_t ldz,
-                              int64_t rows, double* partial, int grid, double* out, cudaStream_t stream) {
+                              int64_t rows, double* partial, int grid, double* out, cudaStream_t stream,
+                              unsigned* ticket) {
     if (p <= 0 || q <= 0) return cudaSuccess;
     if (p * q > 8 * 256) return cudaErrorInvalidValue;
     const size_t smem = static_cast<size_t>(GR) * (p + q) * sizeof(double);
     if (smem > 48 * 1024) return cudaErrorInvalidValue;
-    panel_gram_kernel<<<grid, 256, smem, stream>>>(x, p, ldx, z, q, ldz, rows, partial);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    const int outs = p * q;
-    panel_gram_reduce_kernel<<<(outs + 127) / 128, 128, 0, stream>>>(partial, grid, outs, out);
+    if (!ticket) {  // no completion counter: separate reduction
+        panel_gram_kernel<<<grid, 256, smem, stream>>>(x, p, ldx, z, q, ldz, rows, partial, nullptr, nullptr);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const int outs = p * q;
+        panel_gram_reduce_kernel<<<(outs + 127) / 128, 128, 0, stream>>>(partial, grid, outs, out);
+        return cudaGetLastError();
+    }
+    panel_gram_kernel<<<grid, 256, smem, stream>>>(x, p, ldx, z, q, ldz, rows, partial, ticket, out);
     return cudaGetLastError();
 }
 
