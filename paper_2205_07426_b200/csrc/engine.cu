@@ -1020,7 +1020,7 @@ public:
         const KWindow own{k.row0, rows_}, rest{k.row0 + rows_, k.n - rows_};
         // s = 1 on one whole symmetric fp32 matrix: the upper-triangle product (half the bytes of A)
         symv_ = k.prec == kF32 && s == 1 && !tri && !split_ && k.world == 1 && k.groups <= 1 && k.normalized &&
-                ctx.symv && k.rows == k.n;
+                ctx.symv && k.rows == k.n && split_operand(ctx, vectors_out);
         if (symv_) {
             nb_ = symv_blocks(k.n);
             plan_ = StreamKPlan{};
@@ -1028,7 +1028,7 @@ public:
             plan_.rows_per_block = 128;
             plan_.cluster = 1;
             plan_.slots = static_cast<int>(nb_ * nb_);
-            plan_.grid = 8 * ctx.sms();
+            plan_.grid = ctx.sms();  // persistent: one CTA per SM (a 3-stage 65 KB TMA ring each)
             npad_ = 1;
         } else if (k.prec == kF32) {
             const int grid = k.group_grid > 0 ? k.group_grid : ctx.grid > 0 ? ctx.grid : ctx.sms();

@@ -5,8 +5,9 @@
 // (proj/src/ops.cpp:73-85) reads every entry; A is symmetric by construction (ops.cpp:9-20, mirrored
 // Gram), so the result is the same product in a different summation order.
 //
-// Each CTA takes tiles of the upper triangle in row-major order (persistent stride); a half-warp owns
-// a tile row (16 lanes x 8 columns, two 16-byte loads per plane), rows in fp32 FMA chains of 8 reduced
+// Each CTA takes tiles of the upper triangle in row-major order (persistent, one CTA per SM, tiles
+// streamed by TMA through a 3-stage ring); a half-warp owns a tile row (16 lanes x 8 columns, one
+// 16-byte shared-memory read per plane), rows in fp32 FMA chains of 8 reduced
 // by shuffles in a fixed tree, columns accumulated per thread over its 8 rows and summed across the 16
 // row groups in a fixed order through shared memory. Every row block I receives exactly nb partials
 // (row sums of tiles (I, J >= I), column sums of tiles (I' < I, I)) in slot I·nb + (other tile index):
@@ -23,7 +24,6 @@ namespace rb {
 namespace {
 
 constexpr int ST = 128;  // tile rows / columns
-constexpr int kSymvThreads = 256;
 
 __device__ __forceinline__ void upper_tile(int64_t t, int64_t nb, int64_t* bi, int64_t* bj) {
     // tile t of the row-major upper triangle: row I holds nb - I tiles
@@ -48,58 +48,96 @@ __device__ __forceinline__ void unpack8(uint4 h, uint4 l, float* out) {
     }
 }
 
-__global__ void __launch_bounds__(kSymvThreads) symv_split_kernel(const __half* __restrict__ ahi,
-                                                                  const __half* __restrict__ alo, int64_t n,
-                                                                  int64_t lda, const __half* __restrict__ xhi,
-                                                                  const __half* __restrict__ xlo, int64_t nb,
-                                                                  float* __restrict__ partial) {
-    __shared__ float xs_i[ST], xs_j[ST];
+// Streaming structure: one producer thread keeps kStages tiles in flight by TMA (A_hi and A_lo 128 x 128
+// boxes, zero-filled past n, plus the tile's 128-entry slices of the operand planes by 1-D bulk copies);
+// eight consumer warps compute from shared memory and release each stage when their reads are done.
+constexpr int kStages = 3;
+constexpr int kPlaneBytes = ST * ST * 2;                // one fp16 plane of a tile
+constexpr int kXBytes = ST * 2;                         // one fp16 operand slice
+constexpr int kStageBytes = 2 * kPlaneBytes + 4 * kXBytes;  // A_hi, A_lo, x_i hi/lo, x_j hi/lo
+constexpr int kSymvSmem = kStages * kStageBytes + 1024;
+constexpr int kConsumers = 8;
+constexpr int kSymvThreadsTma = 32 * (kConsumers + 1);
+
+__global__ void __launch_bounds__(kSymvThreadsTma, 1)
+    symv_split_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                      const __half* __restrict__ xhi, const __half* __restrict__ xlo, int64_t nb,
+                      float* __restrict__ partial) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     __shared__ float cs[16][ST + 1];  // column partials of the 16 row groups
     const int tid = threadIdx.x;
-    const int lane = tid % 32, warp = tid / 32;
-    const int half = lane / 16, c = lane % 16;  // tile row parity inside the warp, 8-column chunk
-    const int rg = warp * 2 + half;             // row group 0..15: rows rg, rg + 16, ...
+    const int warp = tid / 32, lane = tid % 32;
     const int64_t tiles = nb * (nb + 1) / 2;
+    if (tid == 0) {
+        prefetch_tmap(&map_hi);
+        prefetch_tmap(&map_lo);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == kConsumers) {  // producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int st = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int64_t bi, bj;
+                upper_tile(t, nb, &bi, &bj);
+                mbar_wait(&empty[st], ph ^ 1u);
+                uint8_t* dst = smem + st * kStageBytes;
+                mbar_arrive_expect_tx(&full[st], kStageBytes);
+                tma_load_2d(dst, &map_hi, &full[st], static_cast<int>(bj * ST), static_cast<int>(bi * ST), pol);
+                tma_load_2d(dst + kPlaneBytes, &map_lo, &full[st], static_cast<int>(bj * ST), static_cast<int>(bi * ST),
+                            pol);
+                uint8_t* xd = dst + 2 * kPlaneBytes;
+                bulk_load_1d(xd, xhi + bi * ST, kXBytes, &full[st], pol);
+                bulk_load_1d(xd + kXBytes, xlo + bi * ST, kXBytes, &full[st], pol);
+                bulk_load_1d(xd + 2 * kXBytes, xhi + bj * ST, kXBytes, &full[st], pol);
+                bulk_load_1d(xd + 3 * kXBytes, xlo + bj * ST, kXBytes, &full[st], pol);
+                if (++st == kStages) st = 0, ph ^= 1u;
+            }
+        }
+        return;
+    }
+    // consumers: a half-warp owns a tile row (16 lanes x 8 columns), rows rg, rg + 16, ...
+    const int half = lane / 16, c = lane % 16;
+    const int rg = warp * 2 + half;
+    int st = 0;
+    uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         int64_t bi, bj;
         upper_tile(t, nb, &bi, &bj);
-        const int64_t i0 = bi * ST, j0 = bj * ST;
         const bool diag = bi == bj;
-        __syncthreads();  // the previous tile's shared arrays are consumed
-        if (tid < ST) {
-            const int64_t gi = i0 + tid, gj = j0 + tid;
-            xs_i[tid] = gi < n ? __half2float(xhi[gi]) + (xlo ? __half2float(xlo[gi]) : 0.f) : 0.f;
-            xs_j[tid] = gj < n ? __half2float(xhi[gj]) + (xlo ? __half2float(xlo[gj]) : 0.f) : 0.f;
-        }
-        __syncthreads();
+        mbar_wait(&full[st], ph);
+        const uint8_t* tile = smem + st * kStageBytes;
+        const __half* xs = reinterpret_cast<const __half*>(tile + 2 * kPlaneBytes);  // [x_i hi | lo | x_j hi | lo]
         float xj[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) xj[e] = xs_j[c * 8 + e];
+        for (int e = 0; e < 8; ++e)
+            xj[e] = __half2float(xs[2 * ST + c * 8 + e]) + __half2float(xs[3 * ST + c * 8 + e]);
         float cacc[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) cacc[e] = 0.f;
-        const int64_t gc = j0 + c * 8;  // first column of this thread's chunk
-        const bool cols_full = gc + 8 <= n;
-        // the 8 rows of this row group: loads first (16 independent 16-byte loads in flight)
         uint4 rh[8], rl[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int64_t gi = i0 + rg + 16 * q;
-            if (gi < n && cols_full) {
-                rh[q] = *reinterpret_cast<const uint4*>(ahi + gi * lda + gc);
-                rl[q] = *reinterpret_cast<const uint4*>(alo + gi * lda + gc);
-            } else {
-                __half hv[8], lv[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const bool ok = gi < n && gc + e < n;
-                    hv[e] = ok ? ahi[gi * lda + gc + e] : __float2half(0.f);
-                    lv[e] = ok ? alo[gi * lda + gc + e] : __float2half(0.f);
-                }
-                rh[q] = *reinterpret_cast<const uint4*>(hv);
-                rl[q] = *reinterpret_cast<const uint4*>(lv);
-            }
+            const int row = rg + 16 * q;
+            rh[q] = *reinterpret_cast<const uint4*>(tile + row * (ST * 2) + c * 16);
+            rl[q] = *reinterpret_cast<const uint4*>(tile + kPlaneBytes + row * (ST * 2) + c * 16);
         }
+        float xi[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int row = rg + 16 * q;
+            xi[q] = __half2float(xs[row]) + __half2float(xs[ST + row]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp's reads of the stage are in registers
+        if (++st == kStages) st = 0, ph ^= 1u;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int row = rg + 16 * q;
@@ -113,15 +151,15 @@ __global__ void __launch_bounds__(kSymvThreads) symv_split_kernel(const __half* 
             for (int o = 8; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
             if (c == 0) partial[(bi * nb + bj) * ST + row] = r;  // row sums of tile (I, J): slot I·nb + J
             if (!diag) {
-                const float xi = xs_i[row];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) cacc[e] = fmaf(a[e], xi, cacc[e]);
+                for (int e = 0; e < 8; ++e) cacc[e] = fmaf(a[e], xi[q], cacc[e]);
             }
         }
         if (!diag) {
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // the previous tile's column sums are read
 #pragma unroll
             for (int e = 0; e < 8; ++e) cs[rg][c * 8 + e] = cacc[e];
-            __syncthreads();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             if (tid < ST) {
                 float v = 0.f;
 #pragma unroll
@@ -138,13 +176,26 @@ int64_t symv_blocks(int64_t n) { return (n + ST - 1) / ST; }
 
 cudaError_t launch_symv_split(const SplitMatrixView& a, const __half* xhi, const __half* xlo, float* partial,
                               int grid, cudaStream_t stream) {
-    if (a.rows != a.cols) return cudaErrorInvalidValue;
-    if (a.ld % 8 != 0) return cudaErrorInvalidValue;  // 16-byte row chunks
+    if (a.rows != a.cols || !xlo) return cudaErrorInvalidValue;
     const int64_t nb = symv_blocks(a.cols);
     const int64_t tiles = nb * (nb + 1) / 2;
+    TensorMapEncodeFn enc = tensor_map_encoder();
+    if (!enc) return cudaErrorInvalidValue;
+    CUtensorMap mh, ml;
+    for (int p = 0; p < 2; ++p) {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.cols), static_cast<cuuint64_t>(a.rows)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld) * 2};
+        cuuint32_t box[2] = {ST, ST};
+        cuuint32_t estr[2] = {1, 1};
+        if (enc(p ? &ml : &mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(p ? a.lo : a.hi), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(symv_split_kernel), kSymvSmem); e != cudaSuccess)
+        return e;
     const int64_t g = std::min<int64_t>(std::max(grid, 1), tiles);
-    symv_split_kernel<<<static_cast<unsigned>(g), kSymvThreads, 0, stream>>>(a.hi, a.lo, a.cols, a.ld, xhi, xlo, nb,
-                                                                             partial);
+    symv_split_kernel<<<static_cast<unsigned>(g), kSymvThreadsTma, kSymvSmem, stream>>>(mh, ml, xhi, xlo, nb, partial);
     return cudaGetLastError();
 }
 
