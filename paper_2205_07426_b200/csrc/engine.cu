@@ -309,6 +309,27 @@ Context::Context(int device) : device_(device) {
     gram_ticket.alloc(sizeof(unsigned));
     cuda_check(cudaMemsetAsync(gram_ticket.as<unsigned>(), 0, sizeof(unsigned), stream_), "memset");
     if (const char* e = std::getenv("RB_SYMV")) symv = std::string(e) != "0";
+    if (const char* e = std::getenv("RB_SPECULATE")) speculate = std::string(e) != "0";
+}
+
+double* Context::pinned_dots(size_t count) {
+    if (count > pin_cap_) {
+        if (pin_dots_) {
+            cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");  // no copy still lands in it
+            cudaFreeHost(pin_dots_);
+            pin_dots_ = nullptr;
+        }
+        const size_t cap = std::max<size_t>(count, 4096);
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&pin_dots_), cap * sizeof(double), cudaHostAllocDefault),
+                   "cudaHostAlloc");
+        pin_cap_ = cap;
+    }
+    return pin_dots_;
+}
+
+cudaEvent_t Context::dots_event(int i) {
+    if (!dots_ev_[i]) cuda_check(cudaEventCreateWithFlags(&dots_ev_[i], cudaEventDisableTiming), "cudaEventCreate");
+    return dots_ev_[i];
 }
 
 cudaStream_t Context::comm_stream() {
@@ -344,6 +365,9 @@ Context::~Context() {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    if (pin_dots_) cudaFreeHost(pin_dots_);
+    for (cudaEvent_t e : dots_ev_)
+        if (e) cudaEventDestroy(e);
     if (ev_main_) cudaEventDestroy(ev_main_);
     if (ev_comm_) cudaEventDestroy(ev_comm_);
     if (comm_) cudaStreamDestroy(comm_);
@@ -1212,7 +1236,7 @@ public:
             e.cmax_cur = w_.cmax.as<unsigned>() + k * s;
             e.cmax_prev = k > 0 ? w_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
             e.cmax_new = w_.cmax.as<unsigned>() + (k + 1) * s;
-            e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm;
+            e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm, e.gscale = gscale_;
             e.t_cur = buf<float>(k);
             e.t_prev = k > 0 ? buf<float>(k - 1) : nullptr;
             e.t_new = buf<float>(k + 1);
@@ -1256,7 +1280,7 @@ public:
             e.cmax_cur = w_.cmax.as<unsigned>() + k * s;
             e.cmax_prev = k > 0 ? w_.cmax.as<unsigned>() + (k - 1) * s : nullptr;
             e.cmax_new = w_.cmax.as<unsigned>() + (k + 1) * s;
-            e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm;
+            e.a1 = a1, e.a2 = a2, e.a3 = a3, e.a_norm = k_.a_norm, e.gscale = gscale_;
             e.t_cur = buf<double>(k);
             e.t_prev = k > 0 ? buf<double>(k - 1) : nullptr;
             e.t_new = buf<double>(k + 1);
@@ -1314,6 +1338,20 @@ public:
     }
     int rows_per_block() const { return plan_.rows_per_block; }
 
+    // the epilogue's a1, a2, a3 are multiplied by *g (device) from here on
+    void set_gscale(const double* g) { gscale_ = g; }
+
+    // the dots of pass p (single rank) into dst (device, [3][s]); no synchronize
+    void reduce_pass(int p, double* dst) {
+        if (R_ > 0)
+            launched(ctx_,
+                     launch_reduce_stats(w_.stats.as<double>() + static_cast<size_t>(p) * 3 * R_ * s_, 1, R_, s_, dst,
+                                         ctx_.stream()),
+                     "reduce_stats");
+        else
+            cuda_check(cudaMemsetAsync(dst, 0, 3 * static_cast<size_t>(s_) * sizeof(double), ctx_.stream()), "memset");
+    }
+
     void state_f64(int k, double* out, int64_t ldo) {
         const bool f32 = k_.prec != kF64;
         launched(ctx_,
@@ -1351,6 +1389,7 @@ private:
     StreamKPlan plan_, plan2_;
     bool split_ = false;
     bool symv_ = false;  // s = 1 through the upper-triangle product (symv.cu)
+    const double* gscale_ = nullptr;
     int64_t nb_ = 0;     // its 128-row blocks
 };
 
@@ -1531,6 +1570,56 @@ PowerRes power_method(Context& ctx, const KernelMatrix& k, const PowerOpts& o, d
     if (norm == 0.0) fail(kInternal, "power-start vector is zero");
     double g = 1.0 / norm;  // x = T/||T||
     double prev = 0.0;
+    if (ctx.speculate && ctx.world() == 1 && iters > 0) {
+        // Pass it+1 is queued before the host reads pass it's dots: its normalisation g = 1/||T_it|| is
+        // computed on the device (launch_power_norm, the same IEEE sqrt and division as the host's) and
+        // scales the epilogue's coefficients, so every pass is bitwise the one the synchronous loop
+        // below runs; the host's readback and convergence test overlap the next product, and the pass
+        // queued past convergence is discarded.
+        DevBuf dd;
+        dd.alloc(sizeof(double) * (3 * static_cast<size_t>(iters + 1) + 1));
+        double* red = dd.as<double>();
+        double* gdev = red + 3 * static_cast<size_t>(iters + 1);
+        double* pin = ctx.pinned_dots(3 * static_cast<size_t>(iters + 1));
+        ps.reduce_pass(0, red);
+        launched(ctx, launch_power_norm(red, gdev, ctx.stream()), "power_norm");
+        ps.set_gscale(gdev);
+        auto enqueue = [&](int p) {
+            if (shift != 0.0)
+                ps.step(-1.0, shift, 0.0, 0.0);  // (-1)·g = -g, shift·g: the coefficients below
+            else
+                ps.step(1.0, 0.0, 0.0, 0.0);
+            double* rp = red + 3 * static_cast<size_t>(p);
+            ps.reduce_pass(p, rp);
+            launched(ctx, launch_power_norm(rp, gdev, ctx.stream()), "power_norm");
+            cuda_check(cudaMemcpyAsync(pin + 3 * static_cast<size_t>(p), rp, 3 * sizeof(double),
+                                       cudaMemcpyDeviceToHost, ctx.stream()),
+                       "device->host copy");
+            ctx.d2h_bytes += 3 * sizeof(double);
+            cuda_check(cudaEventRecord(ctx.dots_event(p & 1), ctx.stream()), "cudaEventRecord");
+        };
+        enqueue(1);
+        for (int it = 1; it <= iters; ++it) {
+            if (it < iters) enqueue(it + 1);
+            cuda_check(cudaEventSynchronize(ctx.dots_event(it & 1)), "power iteration dots");
+            const double* d = pin + 3 * static_cast<size_t>(it);
+            const double quotient = g * d[1];
+            res.rayleigh = quotient;
+            res.iterations = it;
+            if (it > 1 && std::abs(quotient - prev) <= o.tol * std::abs(quotient)) {
+                res.converged = true;
+                break;
+            }
+            prev = quotient;
+            const double ny = std::sqrt(d[2]);
+            if (ny == 0.0) {
+                res.converged = true;
+                break;
+            }
+            g = 1.0 / ny;
+        }
+        return res;
+    }
     for (int it = 1; it <= iters; ++it) {
         if (shift != 0.0)
             ps.step(-g, shift * g, 0.0, 0.0);

@@ -154,6 +154,12 @@ public:
     // single-column fp32 passes (power iteration, matvec) through the upper-triangle product (symv.cu);
     // RB_SYMV=0 in the environment selects the tensor-core block product for A/B comparisons
     bool symv = true;
+    // power iteration: queue pass it+1 behind pass it's dots (its 1/||T|| computed on the device) so the
+    // host's readback and convergence test overlap the next product; RB_SPECULATE=0 turns it off
+    bool speculate = true;
+    // page-locked landing slots for per-pass dots read back without a stream synchronize (grow-only)
+    double* pinned_dots(size_t count);
+    cudaEvent_t dots_event(int i);  // i in {0, 1}
     // source of seeded Gaussian probes (Rademacher probes are exact on the device either way):
     // 0 device (rng_panel: the reference's substreams with CUDA's log/sin/cos, <= 2 ulp from glibc per
     // draw), 1 host (the reference's own stream arithmetic, bitwise the probes of
@@ -185,6 +191,9 @@ private:
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
     cudaStream_t comm_ = nullptr;
     cudaEvent_t ev_main_ = nullptr, ev_comm_ = nullptr;
+    double* pin_dots_ = nullptr;
+    size_t pin_cap_ = 0;
+    cudaEvent_t dots_ev_[2] = {nullptr, nullptr};
     // requested panels, generated one after another in request order (each on all host threads)
     using Panel = std::shared_ptr<std::vector<double>>;
     std::map<std::string, std::shared_future<Panel>> probe_prefetch_;

@@ -158,6 +158,9 @@ struct EpiArgs {
     const PT* partial2 = nullptr;
     // symmetric single-column product (launch_symv_split): nb partial slots per row block, [I·nb, I·nb + nb)
     int64_t symv_nb = 0;
+    // optional device scale of a1, a2, a3 (the power iteration's 1/||T||, computed on the device from the
+    // previous pass's dots so the next pass can be queued before the host reads them)
+    const double* gscale = nullptr;
     int64_t total_iters2 = 0;
     int k_tiles2 = 0;
     int grid2 = 1;
@@ -165,6 +168,8 @@ struct EpiArgs {
 };
 
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream);
+// g = 1 / sqrt(red[2]) (red: one pass's [3][1] dots): the power iteration's next normalisation
+cudaError_t launch_power_norm(const double* red, double* g, cudaStream_t stream);
 cudaError_t launch_epilogue_f64(const EpiArgs<double, double>& a, cudaStream_t stream);
 
 // T0 <- X0 (fp64 input); stats[0] and cmax[0]; then planes with exponent e0.

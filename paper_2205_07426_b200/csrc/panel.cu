@@ -57,6 +57,22 @@ __device__ __forceinline__ void split_store(double v, __half* hi, __half* lo, in
 // keep more loads in flight per SM than long per-thread column loops
 constexpr int kEpiCols = 2;
 
+// y += base[c·stride] for c = 0 .. n-1, in slot order (fp64), 16 loads in flight: the symmetric product
+// leaves nb ≈ 400 slots per row block, which a load-add chain walked one L2 round trip at a time
+// (96 us per s = 1 epilogue at n = 50k)
+template <typename PT>
+__device__ __forceinline__ void sum_slots(double& y, const PT* base, int64_t stride, int64_t n) {
+    int64_t c = 0;
+    for (; c + 16 <= n; c += 16) {
+        PT v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = base[(c + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) y += static_cast<double>(v[u]);
+    }
+    for (; c < n; ++c) y += static_cast<double>(base[c * stride]);
+}
+
 template <typename PT, typename ST, bool SPLIT, int ER>
 __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     constexpr int NW = ER / 32;
@@ -71,6 +87,8 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     const int64_t i = static_cast<int64_t>(r) * ER + tid;
     const bool valid = i < p.rows;
     const int64_t cl = p.cluster, rb = r / cl, rr = r % cl;
+    const double gs = p.gscale ? *p.gscale : 1.0;  // fl(1.0·a) = a: no device scale, same coefficients
+    const double a1 = p.a1 * gs, a2 = p.a2 * gs, a3 = p.a3 * gs;
     // block-uniform work once per block (the 64-bit stream-K owner divisions and the plane exponents
     // were ~40 % of the kernel's instructions when every thread repeated them)
     if (tid == 0) {
@@ -93,8 +111,8 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
     }
     if (SPLIT && tid < kEpiCols && jb0 + tid < jb1) {
         const int j = jb0 + tid;
-        const double growth = fabs(p.a1) * p.a_norm + fabs(p.a2);
-        const double bound = growth * cm_value(p.cmax_cur, j) + fabs(p.a3) * cm_value(p.cmax_prev, j);
+        const double growth = fabs(a1) * p.a_norm + fabs(a2);
+        const double bound = growth * cm_value(p.cmax_cur, j) + fabs(a3) * cm_value(p.cmax_prev, j);
         const int e = plane_exponent(bound);
         if (r == 0) p.e_next[j] = e;
         sscale[tid] = pow2(-p.e_cur[j]);
@@ -115,10 +133,10 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
         tcs[jj] = tps[jj] = x0s[jj] = ST(0);
         if (j >= jb1) continue;
         double y = 0.0;
-        for (int64_t c = c_lo; c <= c_hi; ++c)
-            y += static_cast<double>(p.partial[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
-        for (int64_t c = c2_lo; c <= c2_hi; ++c)
-            y += static_cast<double>(p.partial2[((cl * (rb + c) + rr) * p.npad + j) * ER + tid]);
+        const int64_t stride = cl * p.npad * ER;
+        sum_slots(y, p.partial + ((cl * (rb + c_lo) + rr) * p.npad + j) * ER + tid, stride, c_hi - c_lo + 1);
+        if (c2_hi >= c2_lo)
+            sum_slots(y, p.partial2 + ((cl * (rb + c2_lo) + rr) * p.npad + j) * ER + tid, stride, c2_hi - c2_lo + 1);
         ys[jj] = y;
         const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
         if (valid) {
@@ -136,7 +154,7 @@ __global__ void __launch_bounds__(ER) epilogue_kernel(EpiArgs<PT, ST> p) {
         const double tc = static_cast<double>(tcs[jj]), tp = static_cast<double>(tps[jj]),
                      x0 = static_cast<double>(x0s[jj]);
         const int64_t idx = static_cast<int64_t>(j) * p.ld + i;
-        double tn = p.a1 * y + p.a2 * tc + p.a3 * tp;
+        double tn = a1 * y + a2 * tc + a3 * tp;
         const ST tns = static_cast<ST>(tn);
         tn = static_cast<double>(tns);
         if (!valid) tn = 0.0;
@@ -232,17 +250,24 @@ __global__ void prep_planes_kernel(PrepArgs<float> p) {
 }
 
 // out[p][q][j] = sum over row blocks [r0, r0 + count) of stats[p][q][r][j] (R row blocks per (p, q))
+// one warp per output: lane l sums row blocks l, l + 32, ... of the range in order, then a fixed xor
+// tree (the order depends only on the count and the blocks' positions in the range, so a group of a
+// grouped stack reduces exactly as the same rows in their own session); a thread per output walked
+// the ~400 row blocks of an s = 1 pass one L2 round trip at a time (35 us per launch)
 __global__ void reduce_stats_kernel(const double* __restrict__ stats, int passes, int R, int r0, int count, int s,
                                     double* __restrict__ out) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
     const int64_t total = static_cast<int64_t>(passes) * 3 * s;
-    if (t >= total) return;
+    if (t >= total) return;  // warp-uniform
     const int64_t j = t % s;
     const int64_t pq = t / s;  // pass*3 + q
     const double* src = stats + (pq * R + r0) * s + j;
     double acc = 0.0;
-    for (int r = 0; r < count; ++r) acc += src[static_cast<int64_t>(r) * s];
-    out[t] = acc;
+    for (int r = lane; r < count; r += 32) acc += src[static_cast<int64_t>(r) * s];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[t] = acc;
 }
 
 template <typename ST>
@@ -405,6 +430,17 @@ cudaError_t ensure_smem_attr(const void* fn, int bytes) {
     return e;
 }
 
+namespace {
+__global__ void power_norm_kernel(const double* __restrict__ red, double* __restrict__ g) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) g[0] = 1.0 / sqrt(red[2]);  // spectrum.cpp:45-47 (x = y/||y||)
+}
+}  // namespace
+
+cudaError_t launch_power_norm(const double* red, double* g, cudaStream_t stream) {
+    power_norm_kernel<<<1, 32, 0, stream>>>(red, g);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_epilogue_split(const EpiArgs<float, float>& a, cudaStream_t stream) {
     if (a.s > kMaxPanelCols) return cudaErrorInvalidValue;
     const unsigned groups = static_cast<unsigned>((a.s + kEpiCols - 1) / kEpiCols);
@@ -462,8 +498,8 @@ cudaError_t launch_reduce_stats(const double* stats, int passes, int row_blocks,
     const int64_t total = static_cast<int64_t>(passes) * 3 * s;
     if (total == 0) return cudaSuccess;
     if (count < 0) count = row_blocks - r0;
-    reduce_stats_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, stream>>>(stats, passes, row_blocks,
-                                                                                        r0, count, s, out);
+    reduce_stats_kernel<<<static_cast<unsigned>((total + 3) / 4), 128, 0, stream>>>(stats, passes, row_blocks, r0,
+                                                                                    count, s, out);
     return cudaGetLastError();
 }
 
