@@ -19,14 +19,14 @@ constexpr int FK = 32;   // K per smem tile
 // [T·c/G, T·(c+1)/G) and writes one partial per row block it touches to slot rb + c (the pass
 // epilogue sums a row block's slots in CTA order, so results are run-to-run identical). At
 // n = 2000 this spreads the 32 MB of A over every SM instead of 16 row-block CTAs.
-__global__ void __launch_bounds__(256) block_av_f64_kernel(const double* __restrict__ a, int64_t rows, int64_t cols,
+__global__ void __launch_bounds__(256, 2) block_av_f64_kernel(const double* __restrict__ a, int64_t rows, int64_t cols,
                                                            int64_t lda, const double* __restrict__ v, int s,
                                                            int64_t ldv, int npad, double* __restrict__ partial,
                                                            int64_t total_iters, int k_tiles) {
     __shared__ double as[FK][FM + 1];
     __shared__ double vs[FK][FN + 1];
-    const int tx = threadIdx.x % 32;
-    const int ty = threadIdx.x / 32;
+    const int tx = threadIdx.x % 8;  // columns tx + 8j
+    const int ty = threadIdx.x / 8;  // rows ty + 32i
     const int G = gridDim.x, c = blockIdx.x;
     const int col0 = blockIdx.y * FN;
     int64_t it = total_iters * c / G;
@@ -35,9 +35,13 @@ __global__ void __launch_bounds__(256) block_av_f64_kernel(const double* __restr
         const int64_t rb = it / k_tiles;
         const int64_t seg_end = min(it_end, (rb + 1) * k_tiles);
         const int64_t row0 = rb * FM;
-        double acc[FM / 8];
+        // 4x4 register tile per thread: rows ty + 32i, columns tx + 8j (8 shared loads per 16 DFMA; each
+        // output's k sum runs in the same order as before, so results are bitwise unchanged)
+        double acc[4][4];
 #pragma unroll
-        for (int i = 0; i < FM / 8; ++i) acc[i] = 0.0;
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
         // software pipeline: the next k tile's loads are in flight in registers while this one computes
         // (A is L2-resident: each tile is an L2 round trip, which the compute of the previous tile hides)
         constexpr int NA = FM * FK / 256, NV = FN * FK / 256;
@@ -76,17 +80,26 @@ __global__ void __launch_bounds__(256) block_av_f64_kernel(const double* __restr
             if (it + 1 < seg_end) load(it + 1);
 #pragma unroll 4
             for (int kk = 0; kk < FK; ++kk) {
-                const double vv = vs[kk][tx];
+                double ar[4], vr[4];
 #pragma unroll
-                for (int i = 0; i < FM / 8; ++i) acc[i] = fma(as[kk][ty + 8 * i], vv, acc[i]);
+                for (int i = 0; i < 4; ++i) ar[i] = as[kk][ty + 32 * i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) vr[j] = vs[kk][tx + 8 * j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(ar[i], vr[j], acc[i][j]);
             }
             __syncthreads();
         }
-        const int col = col0 + tx;
-        if (col < s) {
-            double* dst = partial + ((rb + c) * npad + col) * FM;
 #pragma unroll
-            for (int i = 0; i < FM / 8; ++i) dst[ty + 8 * i] = acc[i];
+        for (int j = 0; j < 4; ++j) {
+            const int col = col0 + tx + 8 * j;
+            if (col < s) {
+                double* dst = partial + ((rb + c) * npad + col) * FM;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[ty + 32 * i] = acc[i][j];
+            }
         }
     }
 }

@@ -175,6 +175,88 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g, __half* __restric
     }
 }
 
+// fp64 storage, whole matrix on one rank: only tiles with column tile >= row tile are evaluated
+// (the per-entry arithmetic of gram_kernel<double, false>, which is symmetric bit for bit: the dot is a
+// chain of fma(x_ik, x_jk, .) and the norm sum is commutative), and each off-diagonal tile is also
+// written mirrored through shared memory with coalesced row stores. Halves the exp work of config 1.
+constexpr int kSymF64Smem = (TKd * (TM + 1) + TKd * (TN + 4)) > TM * (TN + 1) ? (TKd * (TM + 1) + TKd * (TN + 4))
+                                                                               : TM * (TN + 1);
+
+__global__ void __launch_bounds__(256) gram_sym_f64_kernel(GramArgs g, double* __restrict__ a64, int tiles) {
+    __shared__ double buf[kSymF64Smem];
+    auto xr = reinterpret_cast<double(*)[TM + 1]>(buf);
+    auto xc = reinterpret_cast<double(*)[TN + 4]>(buf + TKd * (TM + 1));
+    auto stg = reinterpret_cast<double(*)[TN + 1]>(buf);  // reused after the accumulation
+    // upper-triangle tile b -> (bi, bj), bi <= bj, row-major over the triangle
+    int bi = 0, rem = blockIdx.x;
+    while (rem >= tiles - bi) rem -= tiles - bi, ++bi;
+    const int bj = bi + rem;
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t row0 = static_cast<int64_t>(bi) * TM, col0 = static_cast<int64_t>(bj) * TN;
+
+    double dot[4][4], sqr[4], sqc[4], kval[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        sqr[u] = sqc[u] = 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dot[u][v] = 0.0;
+    }
+    GramTile<double>::accumulate(g.x, g.dx, g.x_rs, g.x_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            double d2 = (sqr[u] + sqc[v]) - 2.0 * dot[u][v];
+            if (d2 < 0.0) d2 = 0.0;
+            kval[u][v] = exp(-d2 * g.inv_two_sigma2_x);
+        }
+    if (g.y) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sqr[u] = sqc[u] = 0.0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dot[u][v] = 0.0;
+        }
+        GramTile<double>::accumulate(g.y, g.dy, g.y_rs, g.y_cs, g.n, row0, col0, dot, sqr, sqc, xr, xc);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                double d2 = (sqr[u] + sqc[v]) - 2.0 * dot[u][v];
+                if (d2 < 0.0) d2 = 0.0;
+                dot[u][v] = exp(-d2 * g.inv_two_sigma2_y);  // Ky
+            }
+    }
+    // accumulate() ends with a barrier: the feature tiles are dead, buf is the mirror staging now
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int r = ty + 16 * u;
+        const int64_t gi = row0 + r;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t gj = col0 + 4 * tx + v;
+            double val;
+            if (gi == gj) {
+                val = g.inv_n;
+            } else if (g.y) {  // reference op order: n * ((inv_n*Kx) * (inv_n*Ky))
+                val = static_cast<double>(g.n) * ((g.inv_n * kval[u][v]) * (g.inv_n * dot[u][v]));
+            } else {
+                val = g.inv_n * kval[u][v];
+            }
+            if (gi < g.n && gj < g.n) a64[gi * g.ld + gj] = val;
+            stg[r][4 * tx + v] = val;
+        }
+    }
+    if (bi == bj) return;
+    __syncthreads();
+    for (int idx = tid; idx < TM * TN; idx += blockDim.x) {
+        const int c = idx / TM, r = idx % TM;  // mirror row col0 + c, consecutive threads: consecutive columns
+        const int64_t gi = col0 + c, gj = row0 + r;
+        if (gi < g.n && gj < g.n) a64[gi * g.ld + gj] = stg[r][c];
+    }
+}
+
 // fp32 configurations: symmetric tiles. Only tiles with column tile >= row tile are
 // evaluated; the mirrored tile is written through shared memory (coalesced), so the
 // distance/exp work halves while every entry of A is still written once.
@@ -595,6 +677,14 @@ cudaError_t launch_poly_gram(const GramArgs& g, int degree, double offset, doubl
 }
 
 cudaError_t launch_gram_f64(const GramArgs& g, double* a, cudaStream_t stream) {
+    if (g.row0 == 0 && g.rows == g.n) {  // whole matrix: symmetric tiles
+        const int64_t tiles = (g.n + TM - 1) / TM;
+        if (tiles * (tiles + 1) / 2 <= 0x7FFFFFFF) {
+            gram_sym_f64_kernel<<<static_cast<unsigned>(tiles * (tiles + 1) / 2), 256, 0, stream>>>(
+                g, a, static_cast<int>(tiles));
+            return cudaGetLastError();
+        }
+    }
     dim3 grid(static_cast<unsigned>((g.n + TN - 1) / TN), static_cast<unsigned>((g.rows + TM - 1) / TM));
     gram_kernel<double, false><<<grid, 256, 0, stream>>>(g, nullptr, nullptr, a);
     return cudaGetLastError();
