@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256) gram_sym_f64_kernel(GramArgs g, double* _
         const int64_t gi = row0 + r;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            const int64_t gj = col0 + 4 * tx + v;
+            const int64_t gj = col0 + 4 * tx + v;  // (entries past n are staged but never stored)
             double val;
             if (gi == gj) {
                 val = g.inv_n;
@@ -244,12 +244,17 @@ __global__ void __launch_bounds__(256) gram_sym_f64_kernel(GramArgs g, double* _
             } else {
                 val = g.inv_n * kval[u][v];
             }
-            if (gi < g.n && gj < g.n) a64[gi * g.ld + gj] = val;
             stg[r][4 * tx + v] = val;
         }
     }
-    if (bi == bj) return;
     __syncthreads();
+    // both the tile and its mirror leave shared memory as whole 512-byte row segments
+    for (int idx = tid; idx < TM * TN; idx += blockDim.x) {
+        const int r = idx / TN, c = idx % TN;  // tile row row0 + r, consecutive threads: consecutive columns
+        const int64_t gi = row0 + r, gj = col0 + c;
+        if (gi < g.n && gj < g.n) a64[gi * g.ld + gj] = stg[r][c];
+    }
+    if (bi == bj) return;
     for (int idx = tid; idx < TM * TN; idx += blockDim.x) {
         const int c = idx / TM, r = idx % TM;  // mirror row col0 + c, consecutive threads: consecutive columns
         const int64_t gi = col0 + c, gj = row0 + r;
