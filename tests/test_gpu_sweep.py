@@ -1,0 +1,95 @@
+"""Seeded random sweep of the estimator through the C ABI against the fp64 oracle: ragged sizes
+(n off every tile grid), every matrix function the reference routes to (entropy.cpp:201-275:
+integer powers, Taylor, Chebyshev), both probe kinds, Hutch++ splits with and without a sketch,
+fp64 and fp32 storage. Each case draws its configuration from numpy's generator with a fixed
+seed, builds the same kernel on both sides and compares the trace estimate and the entropy at
+the north_star tolerances (fp64 1e-9, fp32 1e-4 relative)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp64": 1e-9, "fp32": 1e-4}
+
+
+def draw_case(k):
+    g = np.random.default_rng(20220507 + k)
+    n = int(g.choice([g.integers(50, 130), g.integers(130, 600), g.integers(600, 1400)]))
+    n += int(n % 128 == 0)  # stay off the tile grid
+    d = int(g.integers(1, 40))
+    sigma = float(math.sqrt(d) * g.uniform(0.6, 1.6))
+    kind = ["int", "taylor", "chebyshev"][k % 3]
+    if kind == "int":
+        alpha, m, bounds = float(g.integers(2, 6)), 0, None
+    elif kind == "taylor":
+        # v is set from the oracle's power iteration in the test (a Taylor centre below lambda_max diverges)
+        alpha, m, bounds = float(g.choice([0.5, 0.8, 1.3, 1.7])), int(g.integers(4, 31)), (0.0, float(g.uniform(1.0, 1.3)))
+    else:
+        alpha, m = float(g.choice([0.6, 1.01, 1.5, 2.5])), int(g.integers(5, 41))
+        bounds = (0.0, 1.0) if g.random() < 0.5 else (float(g.uniform(1e-4, 1e-2)), float(g.uniform(0.5, 1.0)))
+    s_q = int(g.choice([0, g.integers(1, max(2, n // 8))]))
+    s_g = int(g.integers(1, 70))
+    probe = "rademacher" if g.random() < 0.5 else "gaussian"
+    return dict(n=n, d=d, sigma=sigma, method=kind, alpha=alpha, m=m, bounds=bounds, s_q=s_q, s_g=s_g,
+                probe_kind=probe, seed=int(g.integers(1, 2**31)))
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("k", range(48))
+def test_estimator_sweep(R, orc, k, prec):
+    c = draw_case(k)
+    x = np.asarray(orc.fill_gaussian(orc.derive_key(c["seed"], orc.hash_name("X")), c["n"], c["d"]),
+                   dtype=np.float32).astype(np.float64)
+    if k % 5 == 0:  # duplicated rows: a rank-deficient kernel
+        x[c["n"] // 2:] = x[: c["n"] - c["n"] // 2]
+    a = orc.build_kernel(x, c["sigma"])
+    if c["method"] == "taylor":
+        lam = orc.estimate_bounds(a, seed=c["seed"])["v"]
+        c["bounds"] = (0.0, min(1.0, lam * c["bounds"][1]))
+    kw = dict(alpha=c["alpha"], method=c["method"], s=c["s_q"] + c["s_g"], m=c["m"], seed=c["seed"],
+              probe_kind=c["probe_kind"], s_q=c["s_q"], s_g=c["s_g"])
+    b = None if c["bounds"] is None else R.SpectrumBounds(u=c["bounds"][0], v=c["bounds"][1])
+    try:
+        ref = orc.estimate(a, bounds=c["bounds"], **kw)
+    except orc.OracleError as err:
+        # a low-degree Taylor polynomial can go negative: the reference refuses the estimate
+        # (entropy.cpp:62-69), and so must the device path, with the same text
+        with pytest.raises(R.RenyiError) as e:
+            R.entropy(x, c["sigma"], R.EstimatorParams(bounds=b, **kw), precision=prec)
+        assert str(err).split(": ")[-1] in str(e.value), c
+        return
+    got = R.entropy(x, c["sigma"], R.EstimatorParams(bounds=b, **kw), precision=prec)
+    assert got.s_used == ref["s"], c
+    assert abs(got.trace_estimate - ref["trace"]) <= TOL[prec] * abs(ref["trace"]), c
+    assert abs(got.entropy - ref["entropy"]) <= TOL[prec] * max(abs(ref["entropy"]), 1.0), c
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("k", range(10))
+def test_mutual_information_sweep(R, orc, k, prec):
+    """measures.cpp:9-46 at random ragged sizes: the three entropies of the (fused, for fp32) MI
+    estimate against the oracle's three separate estimates on the same seeds."""
+    g = np.random.default_rng(7426 + k)
+    n = int(g.integers(60, 1300))
+    n += int(n % 128 == 0)
+    dx, dy = int(g.integers(1, 20)), int(g.integers(1, 10))
+    seed = int(g.integers(1, 2**31))
+    x = np.asarray(orc.fill_gaussian(orc.derive_key(seed, orc.hash_name("X")), n, dx), dtype=np.float32).astype(np.float64)
+    w = orc.fill_gaussian(orc.derive_key(seed, orc.hash_name("W")), dx, dy)
+    y = x @ w + float(g.uniform(0.1, 1.0)) * orc.fill_gaussian(orc.derive_key(seed, orc.hash_name("E")), n, dy)
+    y = np.asarray(y, dtype=np.float32).astype(np.float64)
+    sx, sy = float(math.sqrt(dx) * g.uniform(0.7, 1.5)), float(math.sqrt(dy) * g.uniform(0.7, 1.5))
+    if k % 2:
+        kw = dict(alpha=float(g.choice([1.01, 1.5, 2.5])), method="chebyshev", m=int(g.integers(8, 61)), bounds=(0.0, 1.0))
+    else:
+        kw = dict(alpha=float(g.integers(2, 5)), method="int", m=0, bounds=None)
+    s = int(g.integers(6, 100))
+    probe = "rademacher" if g.random() < 0.5 else "gaussian"
+    ref = orc.mutual_information(orc.build_kernel(x, sx), orc.build_kernel(y, sy), seed=seed, s=s, probe_kind=probe, **kw)
+    b = None if kw["bounds"] is None else R.SpectrumBounds(u=0.0, v=1.0)
+    p = R.EstimatorParams(alpha=kw["alpha"], method=kw["method"], s=s, m=kw["m"], seed=seed, bounds=b, probe_kind=probe)
+    got = R.mutual_information_samples(x, R.GaussianKernel(sx), y, R.GaussianKernel(sy), p, precision=prec)
+    for key in ("vars_entropy", "target_entropy", "joint_entropy"):
+        assert abs(getattr(got, key) - ref[key]) <= TOL[prec] * max(abs(ref[key]), 1.0), (key, n, dx, dy, s, kw, probe)
