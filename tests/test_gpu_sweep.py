@@ -93,3 +93,32 @@ def test_mutual_information_sweep(R, orc, k, prec):
     got = R.mutual_information_samples(x, R.GaussianKernel(sx), y, R.GaussianKernel(sy), p, precision=prec)
     for key in ("vars_entropy", "target_entropy", "joint_entropy"):
         assert abs(getattr(got, key) - ref[key]) <= TOL[prec] * max(abs(ref[key]), 1.0), (key, n, dx, dy, s, kw, probe)
+
+
+@pytest.mark.parametrize("k", range(12))
+def test_matrix_free_sweep(R, orc, k):
+    """Config 5's path (kernel entries recomputed from bf16 samples, A never stored) at random
+    ragged n, d and panel widths: Hutch++ on integer powers with injected probes against the
+    oracle on the same bf16-rounded samples. Tolerance on the trace: 1e-4 with >= 30 residual probes
+    (config 5 has 60; tests/test_gpu_matrix_free.py), 3e-4 below that: the fp16 rounding of the
+    recomputed entries (2^-11 per entry, unbiased) averages over the probes, and a 7-probe case
+    measured 1.4e-4 on B200 (n = 940, d = 123, alpha = 3)."""
+    from test_gpu_matrix_free import bf16
+
+    g = np.random.default_rng(400000 + k)
+    n = int(g.integers(70, 2600))
+    n += int(n % 128 == 0)
+    d = int(g.integers(1, 129))
+    sigma = float(math.sqrt(d) * g.uniform(0.8, 1.4))
+    alpha = int(g.integers(2, 5))
+    s_q, s_g = int(g.choice([0, g.integers(1, 40)])), int(g.integers(1, 97))
+    x = orc.fill_gaussian(500 + k, n, d)
+    a = orc.build_kernel(bf16(x), sigma)
+    S = orc.fill_gaussian(600 + k, n, s_q) if s_q else None
+    G = orc.fill_gaussian(700 + k, n, s_g)
+    ref = orc.hutchpp(orc.Spec("int", alpha), a, s_q, s_g, sketch=S, probes=G)
+    kern = R.build_kernel(x, R.GaussianKernel(sigma), "mf")
+    got = R.hutchpp(R.MatrixFunctionSpec.int_power(alpha), kern, R.SketchConfig(s_q=s_q, s_g=s_g, sketch=S, probes=G))
+    assert got.sketch_rank == ref["sketch_rank"], (n, d, alpha, s_q, s_g)
+    tol = 1e-4 if s_g >= 30 else 3e-4
+    assert abs(got.value - ref["value"]) <= tol * abs(ref["value"]), (n, d, alpha, s_q, s_g)
